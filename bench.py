@@ -1,0 +1,430 @@
+#!/usr/bin/env python3
+"""bench.py -- the headline benchmark (BASELINE.json `metric`):
+
+  "ResNet-18 conv C1-C12 TFLOP/s (% roofline)" on configs[1]: all twelve
+  ResNet-18 conv workloads at batch 64, bf16 inputs with
+  f32 accumulation, each a fused [conv2d, bias_add, relu] node (the group
+  fuse_pass builds, R/src/graph_passes.cpp:240-244) run as ONE sm_100a
+  kernel through the C ABI.
+
+One "step" = the 12 fused layers once over one batch of synthetic inputs
+(reference value distributions, random-init weights), inputs resident in HBM.
+`value` = total algorithmic FLOPs (2*N*OC*OH*OW*IC*KH*KW per layer) / time.
+
+Multi-GPU (torchrun): the single-operator configs are replicas only (SURVEY
+8e) -- each rank runs its own batch-64 replica, no collective on the data
+path; value = FLOPs of all ranks / max-over-ranks time ("scaling": "weak").
+
+`--impl reference` runs the reference's own CPU implementation (the tec
+library compiled from /root/reference sources into oracle/_ref by
+oracle/Makefile) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1802_04799_b200.workloads import RESNET18_CONVS, resnet_layer  # noqa: E402
+
+METRIC = "ResNet-18 conv C1-C12 TFLOP/s (% roofline)"
+LAYERS = list(RESNET18_CONVS)
+REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return (float(j["bf16_tflops"]), float(j["hbm_gbs"]),
+                float(j.get("bf16_tflops_sustained", j["bf16_tflops"])), "measured")
+    except Exception:
+        return 1590.0, 6650.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------ CPU reference
+def _ref_chunks(rows=1, chunk_oc=None):
+    """Bounded sample of the workload: for every layer, `rows` output rows of
+    one image at full width and depth, split into output-channel chunks so
+    the work spreads over all host cores."""
+    jobs = []
+    for name in LAYERS:
+        hw, c, k, r, s = RESNET18_CONVS[name]
+        per = chunk_oc or max(8, min(k, (1 << 20) // max(1, c * r * r * (hw // s))))
+        for oc0 in range(0, k, per):
+            jobs.append((name, c, hw, hw, min(per, k - oc0), r, s, r // 2, rows))
+    return jobs
+
+
+def _ref_one(job, seed):
+    name, c, h, w, oc, r, s, p, rows = job
+    out = subprocess.run([REF_DRIVER, "bench", "conv2d", str(c), str(h), str(w), str(oc),
+                          str(r), str(s), str(p), str(rows), str(seed)],
+                         capture_output=True, text=True, check=True)
+    return json.loads(out.stdout)
+
+
+def run_reference_sample(threads, seed=0):
+    """Runs the sample on `threads` concurrent reference processes; returns
+    (flops, wall_seconds, description)."""
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = _ref_chunks()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        res = list(ex.map(lambda j: _ref_one(j, seed), jobs))
+    wall = time.perf_counter() - t0
+    flops = sum(2 * r["macs"] for r in res)
+    desc = (f"reference tec eval_graph_node(fused conv2d+bias_add+relu) on 1 output row of "
+            f"each of C1-C12 (batch 1, full width/channels, {len(jobs)} OC chunks), "
+            f"{threads} concurrent processes; f32")
+    return flops, wall, desc
+
+
+def run_port_sample(threads, seed=0):
+    """Fallback when oracle/_ref is absent: the C restatement (oracle/)."""
+    import numpy as np
+    from oracle.oracle_api import fused_conv
+    rng = np.random.default_rng(seed)
+    flops = 0
+    t0 = time.perf_counter()
+    for name in LAYERS:
+        hw, c, k, r, s = RESNET18_CONVS[name]
+        hs = r  # one output row
+        x = rng.uniform(-1, 1, (1, c, hs, hw)).astype(np.float32)
+        w = rng.uniform(-1, 1, (k, c, r, r)).astype(np.float32)
+        b = rng.uniform(-1, 1, (k,)).astype(np.float32)
+        y = fused_conv("conv2d", x, w, (s, s), (r // 2, r // 2),
+                       [("bias_add", b), ("relu",)], threads=threads)
+        flops += 2 * y.size * c * r * r
+    return flops, time.perf_counter() - t0, f"oracle C port, 1 row per layer, {threads} threads"
+
+
+def cpu_baseline_block(threads):
+    if os.path.exists(REF_DRIVER):
+        flops, wall, desc = run_reference_sample(threads)
+        kind = "reference"
+    else:
+        flops, wall, desc = run_port_sample(threads)
+        kind = "port"
+    return {"value": flops / wall / 1e12, "unit": "TFLOP/s", "cores": threads,
+            "kind": kind, "sample": desc, "sample_flops": flops,
+            "sample_seconds": round(wall, 3)}
+
+
+def impl_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    if not os.path.exists(REF_DRIVER):
+        kind = "port"
+    else:
+        kind = "reference"
+    vals = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            flops, wall, sample = run_reference_sample(threads, seed=i)
+        else:
+            flops, wall, sample = run_port_sample(threads, seed=i)
+        if i >= args.warmup:
+            vals.append((flops, wall))
+    tot_f = sum(v[0] for v in vals)
+    tot_t = sum(v[1] for v in vals)
+    value = tot_f / tot_t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_t / max(1, len(vals)) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C1-C12 fused conv2d+bias_add+relu (bounded CPU sample)",
+                   "global_batch": 1, "parallelism": "process-sharded host cores"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ our arm
+def impl_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1802_04799_b200 import _abi
+    from paper_1802_04799_b200.device import DeviceConv
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak_tf, hbm_gbs, peak_tf_sus, peak_src = load_peaks()
+    batch = args.batch
+
+    layers = [DeviceConv(resnet_layer(n, batch), compute="bf16", device=local,
+                         seed=1000 * rank + i) for i, n in enumerate(LAYERS)]
+    flops = [l.wl.flops for l in layers]
+    step_flops = sum(flops)
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+
+    def step():
+        for l in layers:
+            l.launch(stream)
+
+    # Warm-up (also first-call TMA descriptor / attribute setup).
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup)):
+            step()
+    torch.cuda.synchronize()
+
+    # Capture one step in a CUDA graph: 12 kernel launches, no host gaps.
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    torch.cuda.synchronize()
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K graph replays, events on the replay stream.
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([elapsed_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * step_flops * args.steps / (max_ms / 1e3) / 1e12
+
+    # ---- per-layer kernel durations (same stream, L2 flushed before each).
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    per_layer = []
+    reps = max(5, min(20, args.steps))
+    for l, fl in zip(layers, flops):
+        times = []
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                l.launch(stream)
+                b.record(stream)
+                times.append((a, b))
+        torch.cuda.synchronize()
+        us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in times)
+        byts = l.algorithmic_bytes()
+        ai = fl / byts
+        bound_tf = min(peak_tf, ai * hbm_gbs / 1e3)
+        achieved = fl / (us * 1e-6) / 1e12
+        per_layer.append({
+            "layer": l.wl.name, "us": round(us, 2), "tflops": round(achieved, 1),
+            "gflop": round(fl / 1e9, 3), "mbytes": round(byts / 1e6, 2),
+            "ai_flop_per_byte": round(ai, 1),
+            "bound": "tensor" if bound_tf >= peak_tf else "hbm",
+            "roof_tflops": round(bound_tf, 1), "frac_of_roof": round(achieved / bound_tf, 3),
+        })
+    kern_s = sum(p["us"] for p in per_layer) * 1e-6
+    achieved_tf = step_flops / kern_s / 1e12
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the reference-facing host API (tec_eval_fused_conv):
+    # pinned host NCHW f32 inputs -> H2D -> pack -> fused kernel -> unpack -> D2H.
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, batch, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_block(os.cpu_count() or 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {
+                "workload": "configs[1]: ResNet-18 C1-C12 fused conv2d+bias_add+relu, "
+                            f"batch {batch} per GPU, bf16 in / f32 accumulate / bf16 out",
+                "global_batch": batch * world, "parallelism": f"replicas x{world} (no collective)",
+                "l2": "step working set (all 12 layers) > 126 MB L2; per-layer timings "
+                      "flush L2 (256 MB write) before each launch",
+                "timing": "CUDA graph of the 12 launches replayed K times; CUDA events on "
+                          "the replay stream; max over ranks",
+            },
+            "roofline": {
+                "bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf,
+                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 3),
+                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src})",
+                "kernel": "conv_fprop_tc_kernel (tcgen05 implicit GEMM), all 12 launches",
+            },
+            "layers": per_layer,
+            "gpu_launches": len(layers) * args.steps,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, batch, device):
+    import ctypes as C
+
+    import torch
+
+    from paper_1802_04799_b200 import _abi
+    lib = _abi.load()
+    steps = max(1, min(3, args.steps))
+    g = torch.Generator().manual_seed(7)
+    prepared = []
+    h2d = d2h = 0
+    flops = 0
+    for name in LAYERS:
+        wl = resnet_layer(name, batch)
+        x = (torch.rand((wl.n, wl.c, wl.h, wl.w), generator=g) * 2 - 1).pin_memory()
+        w = (torch.rand((wl.k, wl.c, wl.r, wl.s), generator=g) * 2 - 1).pin_memory()
+        b = (torch.rand((wl.k,), generator=g) * 2 - 1).pin_memory()
+        y = torch.empty((wl.n, wl.k, wl.oh, wl.ow)).pin_memory()
+        d = _abi.ConvDesc(n=wl.n, c=wl.c, h=wl.h, w=wl.w, k=wl.k, r=wl.r, s=wl.s,
+                          stride_h=wl.stride, stride_w=wl.stride, pad_h=wl.pad,
+                          pad_w=wl.pad, depthwise=0, compute=_abi.COMPUTE_BF16)
+        e = _abi.Epilogue()
+        e.n_ops = 2
+        e.ops[0] = _abi.EPI_BIAS
+        e.ops[1] = _abi.EPI_RELU
+        e.bias = b.data_ptr()
+        prepared.append((d, e, x, w, y, b))
+        h2d += x.numel() * 4 + w.numel() * 4 + b.numel() * 4
+        d2h += y.numel() * 4
+        flops += wl.flops
+    kn = _abi.Knobs()
+
+    def one():
+        for d, e, x, w, y, b in prepared:
+            _abi.check(lib.tec_eval_fused_conv(C.byref(d), C.byref(e), C.byref(kn),
+                                               x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                               device))
+    one()  # warm-up: workspace allocation
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": round(flops / dt / 1e12, 3), "unit": "TFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": round(dt * 1e3, 2),
+            "path": "tec_eval_fused_conv (C ABI, host NCHW f32 buffers, pinned), "
+                    "wall clock incl. H2D, layout packing, kernel, unpack, D2H"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        impl_reference(args)
+    else:
+        impl_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,206 @@
+/* tec_sm100.h -- C ABI of the B200 (sm_100a) backend for the fused
+ * conv2d / depthwise_conv2d operator path of the reference "tec"
+ * (/root/reference/proj, the arXiv 1802.04799 re-creation).
+ *
+ * Plain C: pointers, sizes, int/double scalars. No exceptions cross this
+ * boundary; every call returns a tec_status and the message of the last
+ * failure on the calling thread is available from tec_last_error().
+ *
+ * Which reference interface each entry point replaces (R = reference/proj):
+ *
+ *   tec_eval_fused_conv      eval_graph_node(fused [conv2d, scale?, bias_add?,
+ *                            add?, mul?, relu?]) R/src/graph.cpp:209-225, and
+ *                            eval_operator("conv2d"/"depthwise_conv2d")
+ *                            R/src/ops.cpp:517-531 -- host DenseTensor-style
+ *                            NCHW buffers in, NCHW out (the OperatorDef::
+ *                            native_eval hook, R/include/tec/ops.hpp:63-65)
+ *   tec_conv_infer           infer_conv R/src/ops.cpp:163-192 (same checks,
+ *                            same ShapeMismatch code)
+ *   tec_conv2d_fused /       the lowered + executed fused node for
+ *   tec_depthwise_fused      target="sm100" (LowerOptions::target,
+ *                            R/include/tec/lower.hpp:26-33): device buffers,
+ *                            kernel-native layouts, caller's stream
+ *   tec_weight_pretransform  the weight side of apply_layouts/fold_constants
+ *                            (R/src/graph_passes.cpp:41-178): OIHW -> KRSC
+ *   tec_activation_pack /    layout_transform (R/src/ops.cpp:419-489) at
+ *   tec_output_unpack        graph boundaries: NCHW <-> packed NHWC
+ *   tec_measure              measure_program / measure for target "sm100"
+ *                            (R/src/tune.cpp:295-351): on-device timing
+ *
+ * Status codes: 0 = OK, otherwise 1 + (int)tec::ErrorCode
+ * (R/include/tec/error.hpp:25-47, order is stable), plus TEC_E_CUDA for
+ * device/runtime failures that have no reference counterpart.
+ */
+#ifndef TEC_SM100_H_
+#define TEC_SM100_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TEC_SM100_API_VERSION 1
+
+typedef int32_t tec_status;
+enum {
+  TEC_OK = 0,
+  TEC_E_UNKNOWN_OPERATOR = 1,
+  TEC_E_SHAPE_MISMATCH = 2,
+  TEC_E_FOLD_OVERFLOW = 3,
+  TEC_E_UNBOUND_AXIS = 4,
+  TEC_E_DUPLICATE_INTRINSIC = 5,
+  TEC_E_INVALID_FACTOR = 6,
+  TEC_E_ILLEGAL_REORDER = 7,
+  TEC_E_ILLEGAL_ANNOTATION = 8,
+  TEC_E_ILLEGAL_BIND = 9,
+  TEC_E_BIND_CONFLICT = 10,
+  TEC_E_ILLEGAL_COMPUTE_AT = 11,
+  TEC_E_SCOPE = 12,
+  TEC_E_CAPACITY = 13,
+  TEC_E_TENSORIZE_MISMATCH = 14,
+  TEC_E_LOWERING = 15,
+  TEC_E_BOUNDS = 16,
+  TEC_E_DEADLOCK = 17,
+  TEC_E_RACE = 18,
+  TEC_E_NOT_ENOUGH_DATA = 19,
+  TEC_E_IO = 20,
+  TEC_E_INTERNAL = 21,
+  TEC_E_CUDA = 64
+};
+
+/* Element types. The first three mirror tec::DType (R/include/tec/dtype.hpp:27). */
+typedef enum {
+  TEC_DT_F32 = 0,
+  TEC_DT_I32 = 1,
+  TEC_DT_I8 = 2,
+  TEC_DT_BF16 = 3
+} tec_dtype;
+
+/* Arithmetic an operator runs with:
+ *   BF16   : tcgen05 kind::f16 -- inputs rounded to bf16, exact products,
+ *            f32 tensor-core accumulation (stated tolerance)
+ *   TF32X3 : tcgen05 kind::tf32 -- x = hi + lo split, hi*hi + hi*lo + lo*hi
+ *            (fast approximate f32; stated tolerance)
+ *   I8     : tcgen05 kind::i8 -- s8 x s8 -> s32 (bit-exact i8 path)
+ *   F32    : f32 parity path -- SIMT, the reference's exact reduction
+ *            order and rounding: bit-identical to evaluate_reference      */
+typedef enum {
+  TEC_COMPUTE_BF16 = 1,
+  TEC_COMPUTE_TF32X3 = 2,
+  TEC_COMPUTE_I8 = 3,
+  TEC_COMPUTE_F32 = 4
+} tec_compute;
+
+/* Fused member ops, listed in member order (R/src/graph.cpp:209-222). */
+typedef enum {
+  TEC_EPI_SCALE = 1,  /* x * c            R/src/ops.cpp:260-281 */
+  TEC_EPI_BIAS = 2,   /* x + b[oc]        R/src/ops.cpp:282-305 */
+  TEC_EPI_ADD = 3,    /* x + r            R/src/ops.cpp:216-223 */
+  TEC_EPI_MUL = 4,    /* x * r            R/src/ops.cpp:224-231 */
+  TEC_EPI_RELU = 5    /* max(x, 0)        R/src/ops.cpp:250-259 */
+} tec_epi_op;
+
+#define TEC_MAX_EPILOGUE 8
+
+/* Logical operator shape: NCHW data, OIHW weights (R/src/ops.cpp:118-119),
+ * symmetric padding (R/src/ops.cpp:125). Depthwise: k == c, weights [C,1,r,s]. */
+typedef struct {
+  int64_t n, c, h, w;
+  int64_t k, r, s;
+  int64_t stride_h, stride_w, pad_h, pad_w;
+  int32_t depthwise;
+  int32_t compute; /* tec_compute */
+} tec_conv_desc;
+
+typedef struct {
+  int32_t n_ops;
+  int32_t ops[TEC_MAX_EPILOGUE]; /* tec_epi_op, member order */
+  double scale[TEC_MAX_EPILOGUE]; /* attr "scale" of each SCALE op */
+  const void* bias;        /* BIAS operand: [K], f32 (i32 for I8)        */
+  const void* residual;    /* ADD operand: output-shaped                  */
+  const void* mul_operand; /* MUL operand: output-shaped                  */
+} tec_epilogue;
+
+/* Schedule knobs (Config = map<string,int64>, R/include/tec/autotune.hpp:43),
+ * 0 = let the library choose. Mapping to the paper's primitives:
+ *   tile_n   split/tile of the output-channel axis -> CTA tile N (64/128/256)
+ *   tile_m   split/tile of the pixel axis -> CTA tile M (128)
+ *   stages   cache_read(shared) depth -> smem ring stages
+ *   acc_bufs virtual_thread -> TMEM accumulator buffers (2)
+ *   grid     bind(blockIdx) extent -> persistent CTAs (<= #SMs)
+ *   vec      vectorize width of the depthwise kernel (channels per thread)
+ *   raster   reorder of the tile loop (0 = N fastest)                  */
+typedef struct {
+  int64_t tile_m, tile_n, tile_k, stages, cta_pair, cluster_m, cluster_n;
+  int64_t raster, swizzle, split_k, vec, unroll, acc_bufs, grid;
+} tec_knobs;
+
+/* Kernel-native layouts chosen for a desc (sizes in bytes). */
+typedef struct {
+  int64_t oh, ow;          /* output spatial dims                          */
+  int64_t cp;              /* stored channels of the packed activation     */
+  int32_t act_dtype;       /* element type of packed activation/weights    */
+  int32_t acc_dtype;       /* f32 or i32                                   */
+  int64_t act_bytes;       /* packed NHWC activation                       */
+  int64_t wt_bytes;        /* packed weights                               */
+  int64_t out_elems;       /* n*k*oh*ow                                     */
+} tec_conv_layout;
+
+int tec_api_version(void);
+const char* tec_last_error(void);
+int tec_device_sm_count(int device);
+
+/* infer_conv: output NCHW shape, or TEC_E_SHAPE_MISMATCH. */
+tec_status tec_conv_infer(const tec_conv_desc* d, int64_t out_shape[4]);
+tec_status tec_conv_layout_of(const tec_conv_desc* d, tec_conv_layout* out);
+
+/* ---- device-level path (device pointers, caller's cudaStream_t) ---- */
+/* NCHW f32 (or i8 for I8) -> packed NHWC activation. */
+tec_status tec_activation_pack(const tec_conv_desc* d, const void* x_nchw,
+                               void* x_packed, void* stream);
+/* OIHW f32 (or i8) -> packed weights (KRSC, or [R][S][C] for depthwise). */
+tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
+                                   void* w_packed, void* stream);
+/* NCHW (f32 / i32) -> NHWC in out_dtype (residual/mul operands). */
+tec_status tec_nchw_to_nhwc(const void* src, int32_t src_dtype, void* dst,
+                            int32_t dst_dtype, int64_t n, int64_t c,
+                            int64_t h, int64_t w, void* stream);
+/* NHWC [n*h*w][c] (f32/bf16/i32) -> NCHW (f32 or i32). */
+tec_status tec_output_unpack(const void* y_nhwc, int32_t y_dtype, void* y_nchw,
+                             int32_t dst_dtype, int64_t n, int64_t c,
+                             int64_t h, int64_t w, void* stream);
+
+/* Fused conv: y (NHWC [N*OH*OW][K], out_dtype f32/bf16, or i32 for I8)
+ * = epilogue(conv(x_packed, w_packed)). Epilogue operands are device
+ * pointers: bias [K] (f32 / i32), residual & mul NHWC in out_dtype.
+ * err_flag (device int32, may be NULL) is OR-ed with 1 on i32 overflow. */
+tec_status tec_conv2d_fused(const tec_conv_desc* d, const tec_epilogue* epi,
+                            const tec_knobs* knobs, const void* x_packed,
+                            const void* w_packed, void* y, int32_t out_dtype,
+                            int32_t* err_flag, void* stream);
+tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, const void* x_packed,
+                               const void* w_packed, void* y,
+                               int32_t out_dtype, int32_t* err_flag,
+                               void* stream);
+
+/* ---- host-level path: eval_graph_node / native_eval for target sm100 ----
+ * x: NCHW f32 (i8 for I8); w: OIHW f32 (i8); epilogue operands NCHW f32
+ * (i32); y: NCHW f32 (i32). All HOST pointers; copies included. */
+tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, const void* x,
+                               const void* w, void* y, int device);
+
+/* On-device timing of one fused-conv configuration with synthetic data:
+ * CUDA events around `reps` launches after `warmup`, L2 flushed between
+ * reps when flush_l2 != 0; writes the median in microseconds. */
+tec_status tec_measure(const tec_conv_desc* d, const tec_epilogue* epi,
+                       const tec_knobs* knobs, int device, int warmup,
+                       int reps, int flush_l2, double* median_us);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEC_SM100_H_ */

@@ -1,0 +1,127 @@
+"""ctypes binding of the C ABI in include/tec_sm100.h (libtec_sm100.so).
+
+The shared library is built in-tree (paper_1802_04799_b200/lib/) by
+``make -C paper_1802_04799_b200`` / ``__graft_entry__.build()``. There is
+no fallback: if the library is missing, importing the compute entry points
+raises -- the product path never silently degrades to CPU code.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libtec_sm100.so")
+
+# Status codes: 1 + tec::ErrorCode (R/include/tec/error.hpp:25-47).
+ERROR_NAMES = [
+    "UnknownOperator", "ShapeMismatch", "FoldOverflow", "UnboundAxis",
+    "DuplicateIntrinsic", "InvalidFactor", "IllegalReorder",
+    "IllegalAnnotation", "IllegalBind", "BindConflict", "IllegalComputeAt",
+    "ScopeError", "CapacityError", "TensorizeMismatch", "LoweringError",
+    "BoundsError", "DeadlockError", "RaceError", "NotEnoughData", "IOError",
+    "Internal",
+]
+TEC_E_CUDA = 64
+
+DT_F32, DT_I32, DT_I8, DT_BF16 = 0, 1, 2, 3
+COMPUTE_BF16, COMPUTE_TF32X3, COMPUTE_I8, COMPUTE_F32 = 1, 2, 3, 4
+EPI_SCALE, EPI_BIAS, EPI_ADD, EPI_MUL, EPI_RELU = 1, 2, 3, 4, 5
+MAX_EPILOGUE = 8
+
+
+class TecError(RuntimeError):
+    """Mirror of tec::Error: carries the stable error code."""
+
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        if 1 <= status <= len(ERROR_NAMES):
+            self.code = ERROR_NAMES[status - 1]
+        elif status == TEC_E_CUDA:
+            self.code = "CudaError"
+        else:
+            self.code = f"status{status}"
+        super().__init__(f"{self.code}: {msg}")
+
+
+class ConvDesc(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in
+                ("n", "c", "h", "w", "k", "r", "s", "stride_h", "stride_w",
+                 "pad_h", "pad_w")] + [("depthwise", C.c_int32),
+                                       ("compute", C.c_int32)]
+
+
+class Epilogue(C.Structure):
+    _fields_ = [("n_ops", C.c_int32),
+                ("ops", C.c_int32 * MAX_EPILOGUE),
+                ("scale", C.c_double * MAX_EPILOGUE),
+                ("bias", C.c_void_p),
+                ("residual", C.c_void_p),
+                ("mul_operand", C.c_void_p)]
+
+
+class Knobs(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in
+                ("tile_m", "tile_n", "tile_k", "stages", "cta_pair",
+                 "cluster_m", "cluster_n", "raster", "swizzle", "split_k",
+                 "vec", "unroll", "acc_bufs", "grid")]
+
+
+class ConvLayout(C.Structure):
+    _fields_ = [("oh", C.c_int64), ("ow", C.c_int64), ("cp", C.c_int64),
+                ("act_dtype", C.c_int32), ("acc_dtype", C.c_int32),
+                ("act_bytes", C.c_int64), ("wt_bytes", C.c_int64),
+                ("out_elems", C.c_int64)]
+
+
+# Every symbol include/tec_sm100.h declares, with its ctypes signature.
+_P = C.c_void_p
+_DESC = C.POINTER(ConvDesc)
+_EPI = C.POINTER(Epilogue)
+_KN = C.POINTER(Knobs)
+SIGNATURES = {
+    "tec_api_version": (C.c_int, []),
+    "tec_last_error": (C.c_char_p, []),
+    "tec_device_sm_count": (C.c_int, [C.c_int]),
+    "tec_conv_infer": (C.c_int32, [_DESC, C.POINTER(C.c_int64)]),
+    "tec_conv_layout_of": (C.c_int32, [_DESC, C.POINTER(ConvLayout)]),
+    "tec_activation_pack": (C.c_int32, [_DESC, _P, _P, _P]),
+    "tec_weight_pretransform": (C.c_int32, [_DESC, _P, _P, _P]),
+    "tec_nchw_to_nhwc": (C.c_int32, [_P, C.c_int32, _P, C.c_int32, C.c_int64,
+                                     C.c_int64, C.c_int64, C.c_int64, _P]),
+    "tec_output_unpack": (C.c_int32, [_P, C.c_int32, _P, C.c_int32, C.c_int64,
+                                      C.c_int64, C.c_int64, C.c_int64, _P]),
+    "tec_conv2d_fused": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P, C.c_int32,
+                                     _P, _P]),
+    "tec_depthwise_fused": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P,
+                                        C.c_int32, _P, _P]),
+    "tec_eval_fused_conv": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P, C.c_int]),
+    "tec_measure": (C.c_int32, [_DESC, _EPI, _KN, C.c_int, C.c_int, C.c_int,
+                                C.c_int, C.POINTER(C.c_double)]),
+}
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libtec_sm100.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = load().tec_last_error().decode(errors="replace")
+        raise TecError(status, msg)

@@ -1,0 +1,170 @@
+// conv_f32_exact.cu -- the f32 parity path: a SIMT implicit GEMM that
+// reproduces the oracle BIT FOR BIT.
+//
+// Why it exists: the tcgen05 f32 accumulator does not round-to-nearest on
+// every add (measured on B200: a consistent negative bias that grows with
+// K; scratch/diag_accum.py), so tensor-core results
+// drift from evaluate_reference by more than 1e-4 at K = 4608. This kernel
+// instead performs, for every output, exactly the reference's sequence
+//   facc = 0.0f; for (ic, rh, rw) in order: facc = facc + x*w
+// with one IEEE round-to-nearest per multiply and per add (__fmul_rn /
+// __fadd_rn: no FMA contraction), R/src/texpr.cpp:205-228 and
+// R/src/expr.cpp:137-145 -- so the f32 operator is bit-identical to the
+// reference rather than merely within 1e-4.
+//
+// Tiling: 64 output pixels x 64 output channels per 256-thread CTA, each
+// thread owns a 4x4 register block; K (= ic*R*S + rh*S + rw, the reference
+// reduce order) is streamed through shared memory 16 at a time with the
+// next tile prefetched into registers while the current one is consumed.
+// Input is read straight from the reference NCHW layout (im2col on the
+// fly, zero for padded taps); the result is written NHWC like the tensor
+// core kernels (then unpacked at the graph boundary).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "conv_params.h"
+
+namespace tec_sm100 {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256;
+
+__device__ __forceinline__ float epi_f(float v, const EpilogueParams& e,
+                                       int col, int64_t flat) {
+#pragma unroll 1
+  for (int i = 0; i < e.n_ops; ++i) {
+    switch (e.ops[i]) {
+      case kEpiScale: v = __fmul_rn(v, e.fscale[i]); break;
+      case kEpiBias: v = __fadd_rn(v, static_cast<const float*>(e.bias)[col]); break;
+      case kEpiAdd: v = __fadd_rn(v, static_cast<const float*>(e.residual)[flat]); break;
+      case kEpiMul: v = __fmul_rn(v, static_cast<const float*>(e.mul_operand)[flat]); break;
+      case kEpiRelu: v = (v < 0.0f) ? 0.0f : v; break;
+      default: break;
+    }
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(THREADS)
+    conv_f32_exact_kernel(const float* __restrict__ x,
+                          const float* __restrict__ w, ConvGemmParams p) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int t = threadIdx.x;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const int C = p.cp, H = p.h, W = p.w, RS = p.r * p.s;
+  const int K = C * RS;
+  const int ohw = p.oh * p.ow;
+
+  // A-load assignment: pixel column mm fixed, k rows kk = ka + 4*i.
+  const int mm = t % BM;
+  const int ka = t / BM;  // 0..3
+  const int m = m0 + mm;
+  const bool m_ok = m < p.m;
+  int img = 0, oh = 0, ow = 0;
+  if (m_ok) {
+    img = m / ohw;
+    const int rem = m - img * ohw;
+    oh = rem / p.ow;
+    ow = rem - oh * p.ow;
+  }
+  const int ih0 = oh * p.sh - p.ph, iw0 = ow * p.sw - p.pw;
+  const float* xb = x + static_cast<int64_t>(img) * C * H * W;
+  // B-load assignment: k column kb fixed, channel rows nb + 16*i.
+  const int kb = t % BK;
+  const int nb = t / BK;  // 0..15
+
+  float ra[4], rb[4];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = k0 + ka + 4 * i;
+      float v = 0.f;
+      if (m_ok && k < K) {
+        const int ic = k / RS;
+        const int rr = k - ic * RS;
+        const int rh = rr / p.s;
+        const int rw = rr - rh * p.s;
+        const int ih = ih0 + rh, iw = iw0 + rw;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W)
+          v = xb[(static_cast<int64_t>(ic) * H + ih) * W + iw];
+      }
+      ra[i] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int n = n0 + nb + 16 * i;
+      const int k = k0 + kb;
+      rb[i] = (n < p.oc && k < K) ? w[static_cast<int64_t>(n) * K + k] : 0.f;
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) As[buf][ka + 4 * i][mm] = ra[i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Bs[buf][kb][nb + 16 * i] = rb[i];
+  };
+
+  const int tx = t % 16, ty = t / 16;  // 4 pixels x 4 channels each
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    const bool more = k0 + BK < K;
+    if (more) load_tile(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][tx * 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][ty * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w};
+      const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+    }
+    if (more) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  // Padded K (k >= K) never happens: the last tile's extra lanes are zero
+  // products, but adding +0.0f (or -0.0f) to facc leaves it unchanged
+  // unless facc is -0.0f; facc starts at +0.0f and x*0 sums keep it +0.
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int mo = m0 + tx * 4 + i;
+    if (mo >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + ty * 4 + j;
+      if (n >= p.oc) continue;
+      const int64_t flat = static_cast<int64_t>(mo) * p.oc + n;
+      static_cast<float*>(p.y)[flat] = epi_f(acc[i][j], p.epi, n, flat);
+    }
+  }
+}
+
+}  // namespace
+
+int launch_conv_f32_exact(const float* x, const float* w,
+                          const ConvGemmParams& p, cudaStream_t st) {
+  dim3 grid((p.m + BM - 1) / BM, (p.oc + BN - 1) / BN);
+  conv_f32_exact_kernel<<<grid, THREADS, 0, st>>>(x, w, p);
+  return cudaGetLastError();
+}
+
+}  // namespace tec_sm100

@@ -1,0 +1,59 @@
+// conv_params.h -- plain-old-data shared by the host launchers (C++) and
+// the sm_100a kernels (CUDA). No torch or CUDA-runtime types.
+#pragma once
+#include <cstdint>
+
+namespace tec_sm100 {
+
+// Epilogue member ops, in fused-node member order (R/src/graph.cpp:209-222).
+enum EpiOp : int32_t {
+  kEpiNone = 0,
+  kEpiScale = 1,  // x * c            R/src/ops.cpp:260-281
+  kEpiBias = 2,   // x + b[oc]        R/src/ops.cpp:282-305
+  kEpiAdd = 3,    // x + r (same shape) R/src/ops.cpp:216-223
+  kEpiMul = 4,    // x * r (same shape) R/src/ops.cpp:224-231
+  kEpiRelu = 5,   // max(x, 0)        R/src/ops.cpp:250-259
+};
+
+enum ElemType : int32_t { kF32 = 0, kI32 = 1, kI8 = 2, kBF16 = 3 };
+
+constexpr int kMaxEpi = 8;
+
+struct EpilogueParams {
+  int32_t n_ops;
+  int32_t ops[kMaxEpi];
+  float fscale[kMaxEpi];    // float-rounded scale factors (cstf)
+  int64_t iscale[kMaxEpi];  // integral scale factors (cst)
+  const void* bias;         // [OC], accumulator dtype (f32 / i32)
+  const void* residual;     // NHWC [M][OC], output dtype
+  const void* mul_operand;  // NHWC [M][OC], output dtype
+};
+
+// Implicit-GEMM convolution: GEMM M = N*OH*OW output pixels (NHWC order),
+// GEMM N = OC, GEMM K = R*S*Cp in (r, s, c) order.
+struct ConvGemmParams {
+  int32_t n, h, w, cp;  // input NHWC, cp = stored (padded) channels
+  int32_t oh, ow, oc;
+  int32_t r, s, sh, sw, ph, pw;
+  int32_t m;            // n*oh*ow
+  int32_t m_tiles, n_tiles;
+  int32_t cblocks;      // cp / channels-per-block
+  int32_t out_type;     // ElemType of y
+  void* y;              // NHWC [M][OC]
+  int32_t* err;         // set to 1 on i32 range overflow (may be null)
+  EpilogueParams epi;
+};
+
+struct DepthwiseParams {
+  int32_t n, h, w, c;   // NHWC
+  int32_t oh, ow;
+  int32_t r, s, sh, sw, ph, pw;
+  int32_t in_type, out_type;
+  const void* x;
+  const void* wt;       // [R][S][C] (tap-major, channel fastest)
+  void* y;
+  int32_t* err;
+  EpilogueParams epi;
+};
+
+}  // namespace tec_sm100

@@ -1,0 +1,268 @@
+// layout.cu -- graph-boundary layout kernels (the layout_transform operator,
+// R/src/ops.cpp:419-489, specialised to the two layouts this backend uses):
+//   * NCHW (the reference DenseTensor layout) <-> NHWC channel-packed
+//     activations, converting to the compute element type on the way;
+//   * OIHW weights -> KRSC (dense conv) / RSC (depthwise) packed weights.
+// Both directions run as 32x32 shared-memory tiled transposes so reads and
+// writes are coalesced.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "conv_params.h"
+
+namespace tec_sm100 {
+
+__device__ __forceinline__ float tf32_round(float x) {
+  // Round-to-nearest-even onto the 10-bit tf32 mantissa.
+  uint32_t b = __float_as_uint(x);
+  if ((b & 0x7f800000u) == 0x7f800000u) return x;
+  b = (b + 0xFFFu + ((b >> 13) & 1u)) & 0xFFFFE000u;
+  return __uint_as_float(b);
+}
+
+// Packed activation element kinds.
+enum PackMode : int32_t {
+  kPackBF16 = 0,    // bf16(x)
+  kPackTF32X3 = 1,  // channels [hi | hi | lo] (matches weights [hi | lo | hi])
+  kPackI8 = 2,      // int8 copy
+  kPackF32 = 3,     // f32 copy
+  kPackI32 = 4,     // i32 copy
+};
+
+// in: [n][c][hw] (f32, or i8 / i32), out: [n][hw][cp] with cp >= c (x3 for
+// TF32X3), padded channels zero-filled.
+template <typename InT>
+__global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
+                                         void* __restrict__ out, int64_t c,
+                                         int64_t hw, int64_t cp, int mode) {
+  __shared__ float tile[32][33];
+  const int64_t n = blockIdx.z;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t cc = c0 + i, pp = p0 + tx;
+    float v = 0.f;
+    if (cc < c && pp < hw) v = static_cast<float>(in[(n * c + cc) * hw + pp]);
+    tile[i][tx] = v;
+  }
+  __syncthreads();
+  const int64_t ctot = mode == kPackTF32X3 ? 3 * c : c;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t pp = p0 + i, cc = c0 + tx;
+    if (pp >= hw) continue;
+    const int64_t obase = (n * hw + pp) * cp;
+    if (cc < c) {
+      const float v = tile[tx][i];
+      switch (mode) {
+        case kPackBF16:
+          static_cast<__nv_bfloat16*>(out)[obase + cc] = __float2bfloat16_rn(v);
+          break;
+        case kPackTF32X3: {
+          const float hi = tf32_round(v);
+          const float lo = v - hi;
+          float* o = static_cast<float*>(out);
+          o[obase + cc] = hi;
+          o[obase + c + cc] = hi;
+          o[obase + 2 * c + cc] = lo;
+          break;
+        }
+        case kPackI8:
+          static_cast<int8_t*>(out)[obase + cc] = static_cast<int8_t>(v);
+          break;
+        case kPackF32:
+          static_cast<float*>(out)[obase + cc] = v;
+          break;
+        case kPackI32:
+          static_cast<int32_t*>(out)[obase + cc] = static_cast<int32_t>(v);
+          break;
+      }
+    }
+    // zero the channel padding [ctot, cp) once per pixel (block column 0)
+    if (blockIdx.y == 0) {
+      for (int64_t z = ctot + tx; z < cp; z += 32) {
+        switch (mode) {
+          case kPackBF16:
+            static_cast<__nv_bfloat16*>(out)[obase + z] = __float2bfloat16_rn(0.f);
+            break;
+          case kPackTF32X3:
+          case kPackF32:
+            static_cast<float*>(out)[obase + z] = 0.f;
+            break;
+          case kPackI8:
+            static_cast<int8_t*>(out)[obase + z] = 0;
+            break;
+          case kPackI32:
+            static_cast<int32_t*>(out)[obase + z] = 0;
+            break;
+        }
+      }
+    }
+  }
+}
+
+// in: [n][hw][c] (f32 / bf16 / i32), out: [n][c][hw] (f32 or i32).
+template <typename InT, typename OutT>
+__global__ void unpack_nhwc_to_nchw_kernel(const InT* __restrict__ in,
+                                           OutT* __restrict__ out, int64_t c,
+                                           int64_t hw) {
+  __shared__ OutT tile[32][33];
+  const int64_t n = blockIdx.z;
+  const int64_t p0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t pp = p0 + i, cc = c0 + tx;
+    OutT v = OutT(0);
+    if (pp < hw && cc < c) {
+      if constexpr (sizeof(InT) == 2)
+        v = static_cast<OutT>(__bfloat162float(in[(n * hw + pp) * c + cc]));
+      else
+        v = static_cast<OutT>(in[(n * hw + pp) * c + cc]);
+    }
+    tile[i][tx] = v;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t cc = c0 + i, pp = p0 + tx;
+    if (cc < c && pp < hw) out[(n * c + cc) * hw + pp] = tile[tx][i];
+  }
+}
+
+// OIHW -> [K][R][S][cp] (dense) with the compute-type conversion.
+template <typename InT>
+__global__ void pack_weights_krsc_kernel(const InT* __restrict__ w,
+                                         void* __restrict__ out, int64_t k,
+                                         int64_t c, int64_t r, int64_t s,
+                                         int64_t cp, int mode) {
+  const int64_t total = k * r * s * cp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < total; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ci = i % cp;
+    int64_t t = i / cp;
+    const int64_t ss = t % s;
+    t /= s;
+    const int64_t rr = t % r;
+    const int64_t kk = t / r;
+    const int64_t ctot = mode == kPackTF32X3 ? 3 * c : c;
+    float v = 0.f;
+    if (ci < ctot) {
+      const int64_t src_c = ci % c;
+      const int64_t grp = ci / c;
+      v = static_cast<float>(w[((kk * c + src_c) * r + rr) * s + ss]);
+      if (mode == kPackTF32X3) {
+        const float hi = tf32_round(v);
+        v = grp == 1 ? v - hi : hi;  // [hi | lo | hi]
+      }
+    }
+    switch (mode) {
+      case kPackBF16:
+        static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+        break;
+      case kPackTF32X3:
+      case kPackF32:
+        static_cast<float*>(out)[i] = v;
+        break;
+      case kPackI8:
+        static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
+        break;
+      default:
+        break;
+    }
+  }
+}
+
+// Depthwise [C][1][R][S] -> [R][S][C] in f32 / bf16 / i8.
+template <typename InT>
+__global__ void pack_weights_rsc_kernel(const InT* __restrict__ w,
+                                        void* __restrict__ out, int64_t c,
+                                        int64_t r, int64_t s, int mode) {
+  const int64_t total = c * r * s;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < total; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t cc = i % c;
+    const int64_t tap = i / c;
+    const float v = static_cast<float>(w[cc * r * s + tap]);
+    switch (mode) {
+      case kPackBF16:
+        static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+        break;
+      case kPackI8:
+        static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
+        break;
+      default:
+        static_cast<float*>(out)[i] = v;
+        break;
+    }
+  }
+}
+
+// ----------------------------------------------------------- launchers
+int launch_pack_activation(const void* in, int in_type, void* out, int64_t n,
+                           int64_t c, int64_t hw, int64_t cp, int mode,
+                           cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((hw + 31) / 32),
+            static_cast<unsigned>((c + 31) / 32), static_cast<unsigned>(n));
+  dim3 block(32, 8);
+  if (in_type == kF32)
+    pack_nchw_to_nhwc_kernel<float><<<grid, block, 0, st>>>(
+        static_cast<const float*>(in), out, c, hw, cp, mode);
+  else if (in_type == kI8)
+    pack_nchw_to_nhwc_kernel<int8_t><<<grid, block, 0, st>>>(
+        static_cast<const int8_t*>(in), out, c, hw, cp, mode);
+  else
+    pack_nchw_to_nhwc_kernel<int32_t><<<grid, block, 0, st>>>(
+        static_cast<const int32_t*>(in), out, c, hw, cp, mode);
+  return cudaGetLastError();
+}
+
+int launch_unpack_output(const void* in, int in_type, void* out, int out_type,
+                         int64_t n, int64_t c, int64_t hw, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((c + 31) / 32),
+            static_cast<unsigned>((hw + 31) / 32), static_cast<unsigned>(n));
+  dim3 block(32, 8);
+  if (out_type == kI32) {
+    if (in_type != kI32) return cudaErrorInvalidValue;
+    unpack_nhwc_to_nchw_kernel<int32_t, int32_t><<<grid, block, 0, st>>>(
+        static_cast<const int32_t*>(in), static_cast<int32_t*>(out), c, hw);
+  } else if (in_type == kBF16) {
+    unpack_nhwc_to_nchw_kernel<__nv_bfloat16, float><<<grid, block, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(in), static_cast<float*>(out), c, hw);
+  } else if (in_type == kF32) {
+    unpack_nhwc_to_nchw_kernel<float, float><<<grid, block, 0, st>>>(
+        static_cast<const float*>(in), static_cast<float*>(out), c, hw);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+int launch_pack_weights(const void* w, int in_type, void* out, int64_t k,
+                        int64_t c, int64_t r, int64_t s, int64_t cp,
+                        int depthwise, int mode, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t total = depthwise ? c * r * s : k * r * s * cp;
+  int blocks = static_cast<int>((total + threads - 1) / threads);
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  if (depthwise) {
+    if (in_type == kI8)
+      pack_weights_rsc_kernel<int8_t><<<blocks, threads, 0, st>>>(
+          static_cast<const int8_t*>(w), out, c, r, s, mode);
+    else
+      pack_weights_rsc_kernel<float><<<blocks, threads, 0, st>>>(
+          static_cast<const float*>(w), out, c, r, s, mode);
+  } else {
+    if (in_type == kI8)
+      pack_weights_krsc_kernel<int8_t><<<blocks, threads, 0, st>>>(
+          static_cast<const int8_t*>(w), out, k, c, r, s, cp, mode);
+    else
+      pack_weights_krsc_kernel<float><<<blocks, threads, 0, st>>>(
+          static_cast<const float*>(w), out, k, c, r, s, cp, mode);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tec_sm100

@@ -1,0 +1,704 @@
+// tec_sm100_abi.cpp -- the C ABI declared in include/tec_sm100.h.
+//
+// Host side of the backend: argument validation with the reference's error
+// taxonomy (infer_conv, R/src/ops.cpp:163-192), kernel-native layout
+// planning, TMA descriptor encoding, kernel selection from schedule knobs
+// (the "lowering" of a Config for target sm100), and the host-buffer entry
+// point that stands in for eval_graph_node / native_eval.
+//
+// There is NO CPU fallback: every compute entry point runs the sm_100a
+// kernels or returns an error.
+#include "tec_sm100.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "conv_params.h"
+#include "sm100_ptx.cuh"
+
+namespace tec_sm100 {
+template <MmaKind KIND, int BN, int STAGES, int SWZ>
+int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
+                         const ConvGemmParams& p, int grid,
+                         cudaStream_t stream);
+int launch_pack_activation(const void* in, int in_type, void* out, int64_t n,
+                           int64_t c, int64_t hw, int64_t cp, int mode,
+                           cudaStream_t st);
+int launch_unpack_output(const void* in, int in_type, void* out, int out_type,
+                         int64_t n, int64_t c, int64_t hw, cudaStream_t st);
+int launch_pack_weights(const void* w, int in_type, void* out, int64_t k,
+                        int64_t c, int64_t r, int64_t s, int64_t cp,
+                        int depthwise, int mode, cudaStream_t st);
+int launch_depthwise(const DepthwiseParams& p, int tw, cudaStream_t st);
+int launch_conv_f32_exact(const float* x, const float* w,
+                          const ConvGemmParams& p, cudaStream_t st);
+}  // namespace tec_sm100
+
+using namespace tec_sm100;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+tec_status fail(tec_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+tec_status cuda_fail(int err, const char* what) {
+  return fail(TEC_E_CUDA,
+              std::string(what) + ": " +
+                  cudaGetErrorString(static_cast<cudaError_t>(err)));
+}
+
+#define TEC_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+// ------------------------------------------------ driver entry points
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType,
+                                   cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+using EncodeIm2colFn = CUresult (*)(
+    CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct DriverFns {
+  EncodeTiledFn tiled = nullptr;
+  EncodeIm2colFn im2col = nullptr;
+  int driver_version = 0;
+  bool ok = false;
+};
+
+const DriverFns& driver_fns() {
+  static DriverFns fns;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* p1 = nullptr;
+    void* p2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p1,
+                                cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p2,
+                                cudaEnableDefault, &q2) != cudaSuccess)
+      return;
+    fns.tiled = reinterpret_cast<EncodeTiledFn>(p1);
+    fns.im2col = reinterpret_cast<EncodeIm2colFn>(p2);
+    cudaDriverGetVersion(&fns.driver_version);
+    fns.ok = fns.tiled && fns.im2col;
+  });
+  return fns;
+}
+
+CUtensorMapSwizzle swizzle_of(int bytes) {
+  return bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+         : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+         : bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+}
+
+// ------------------------------------------------------ layout planning
+int elem_bytes(int32_t t) { return t == TEC_DT_I8 ? 1 : t == TEC_DT_BF16 ? 2 : 4; }
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+struct Plan {
+  int64_t oh, ow, m;
+  int64_t cp;       // stored channels of the packed activation
+  int32_t act;      // packed element type (tec_dtype)
+  int32_t acc;      // accumulator type
+  int pack_mode;    // layout.cu PackMode
+  int swz;          // channel-block bytes (128/64/32)
+  MmaKind kind;
+};
+
+tec_status infer(const tec_conv_desc* d, int64_t* oh, int64_t* ow) {
+  // infer_conv (R/src/ops.cpp:163-192) plus positive-shape validation
+  // (TensorType::validate, R/include/tec/dtype.hpp:78-84).
+  if (!d) return fail(TEC_E_INTERNAL, "null descriptor");
+  if (d->n <= 0 || d->c <= 0 || d->h <= 0 || d->w <= 0 || d->k <= 0 ||
+      d->r <= 0 || d->s <= 0)
+    return fail(TEC_E_SHAPE_MISMATCH, "tensor dimensions must be positive");
+  if (d->stride_h <= 0 || d->stride_w <= 0 || d->pad_h < 0 || d->pad_w < 0)
+    return fail(TEC_E_SHAPE_MISMATCH, "strides/padding must be pairs of valid values");
+  if (d->depthwise && d->k != d->c)
+    return fail(TEC_E_SHAPE_MISMATCH,
+                "depthwise_conv2d weights must be [C,1,kh,kw] with C=" +
+                    std::to_string(d->c));
+  *oh = (d->h + 2 * d->pad_h - d->r) / d->stride_h + 1;
+  *ow = (d->w + 2 * d->pad_w - d->s) / d->stride_w + 1;
+  if (*oh <= 0 || *ow <= 0)
+    return fail(TEC_E_SHAPE_MISMATCH, std::string(d->depthwise ? "depthwise_conv2d" : "conv2d") +
+                                          ": window larger than input");
+  return TEC_OK;
+}
+
+tec_status make_plan(const tec_conv_desc* d, Plan* p) {
+  tec_status st = infer(d, &p->oh, &p->ow);
+  if (st) return st;
+  p->m = d->n * p->oh * p->ow;
+  switch (d->compute) {
+    case TEC_COMPUTE_BF16:
+      p->act = TEC_DT_BF16;
+      p->acc = TEC_DT_F32;
+      p->pack_mode = 0;
+      p->kind = MmaKind::kF16;
+      if (d->depthwise) {
+        p->cp = d->c;
+      } else {
+        p->cp = round_up(d->c, 16);
+        if (p->cp % 64) p->swz = 32; else p->swz = 128;
+      }
+      break;
+    case TEC_COMPUTE_TF32X3:
+      p->acc = TEC_DT_F32;
+      p->kind = MmaKind::kTF32;
+      if (d->depthwise) {
+        // exact f32 SIMT path (bit-identical to the oracle's order)
+        p->act = TEC_DT_F32;
+        p->pack_mode = 3;
+        p->cp = d->c;
+      } else {
+        p->act = TEC_DT_F32;
+        p->pack_mode = 1;
+        p->cp = round_up(3 * d->c, 16);
+        p->swz = p->cp % 32 == 0 ? 128 : 64;
+      }
+      break;
+    case TEC_COMPUTE_F32:
+      // exact-order SIMT path; dense conv reads the reference NCHW layout
+      // as is (pack = copy), depthwise uses the f32 NHWC kernel.
+      p->act = TEC_DT_F32;
+      p->acc = TEC_DT_F32;
+      p->kind = MmaKind::kTF32;  // unused
+      p->pack_mode = d->depthwise ? 3 : -1;
+      p->cp = d->c;
+      break;
+    case TEC_COMPUTE_I8:
+      p->act = TEC_DT_I8;
+      p->acc = TEC_DT_I32;
+      p->pack_mode = 2;
+      p->kind = MmaKind::kI8;
+      if (d->depthwise) {
+        p->cp = d->c;
+      } else {
+        p->cp = round_up(d->c, 32);
+        p->swz = p->cp % 128 == 0 ? 128 : p->cp % 64 == 0 ? 64 : 32;
+      }
+      break;
+    default:
+      return fail(TEC_E_LOWERING, "unknown compute mode " + std::to_string(d->compute));
+  }
+  return TEC_OK;
+}
+
+tec_status build_epilogue(const tec_epilogue* e, bool integer, EpilogueParams* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (!e) return TEC_OK;
+  if (e->n_ops < 0 || e->n_ops > kMaxEpi)
+    return fail(TEC_E_LOWERING, "too many fused epilogue members");
+  out->n_ops = e->n_ops;
+  for (int i = 0; i < e->n_ops; ++i) {
+    const int op = e->ops[i];
+    if (op < TEC_EPI_SCALE || op > TEC_EPI_RELU)
+      return fail(TEC_E_UNKNOWN_OPERATOR, "unknown epilogue op " + std::to_string(op));
+    out->ops[i] = op;
+    if (op == TEC_EPI_SCALE) {
+      const double c = e->scale[i];
+      if (integer && c != std::floor(c))
+        return fail(TEC_E_SHAPE_MISMATCH, "integer scale requires an integral factor");
+      out->fscale[i] = static_cast<float>(c);           // cstf(c)
+      out->iscale[i] = static_cast<int64_t>(c);         // cst(int64(c))
+    }
+    if (op == TEC_EPI_BIAS && !e->bias)
+      return fail(TEC_E_SHAPE_MISMATCH, "bias_add needs a bias operand");
+    if (op == TEC_EPI_ADD && !e->residual)
+      return fail(TEC_E_SHAPE_MISMATCH, "add needs a second operand");
+    if (op == TEC_EPI_MUL && !e->mul_operand)
+      return fail(TEC_E_SHAPE_MISMATCH, "mul needs a second operand");
+  }
+  out->bias = e->bias;
+  out->residual = e->residual;
+  out->mul_operand = e->mul_operand;
+  return TEC_OK;
+}
+
+int sm_count(int dev) {
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// ------------------------------------------------------ dense conv launch
+using Launcher = int (*)(const CUtensorMap&, const CUtensorMap&,
+                         const ConvGemmParams&, int, cudaStream_t);
+
+Launcher pick_launcher(MmaKind kind, int bn, int swz) {
+#define TEC_CASE(K, BN, ST, SW) \
+  if (kind == K && bn == BN && swz == SW) return &launch_conv_fprop_tc<K, BN, ST, SW>;
+  TEC_CASE(MmaKind::kF16, 64, 8, 128)
+  TEC_CASE(MmaKind::kF16, 128, 6, 128)
+  TEC_CASE(MmaKind::kF16, 256, 4, 128)
+  TEC_CASE(MmaKind::kF16, 64, 8, 32)
+  TEC_CASE(MmaKind::kI8, 64, 8, 128)
+  TEC_CASE(MmaKind::kI8, 128, 6, 128)
+  TEC_CASE(MmaKind::kI8, 256, 4, 128)
+  TEC_CASE(MmaKind::kI8, 64, 8, 64)
+  TEC_CASE(MmaKind::kI8, 128, 6, 64)
+  TEC_CASE(MmaKind::kI8, 64, 8, 32)
+  TEC_CASE(MmaKind::kTF32, 64, 8, 128)
+  TEC_CASE(MmaKind::kTF32, 128, 6, 128)
+  TEC_CASE(MmaKind::kTF32, 256, 4, 128)
+  TEC_CASE(MmaKind::kTF32, 64, 8, 64)
+#undef TEC_CASE
+  return nullptr;
+}
+
+tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
+                    const EpilogueParams& epi, const tec_knobs* kn,
+                    const void* x, const void* w, void* y, int32_t out_dtype,
+                    int32_t* err, cudaStream_t st) {
+  const DriverFns& fns = driver_fns();
+  if (!fns.ok) return fail(TEC_E_CUDA, "cuTensorMapEncode* entry points unavailable");
+  const int es = elem_bytes(pl.act);
+  const int cb = pl.swz / es;  // channels per block
+  if (pl.cp % cb) return fail(TEC_E_INTERNAL, "channel padding does not match block");
+  if (pl.kind == MmaKind::kI8 && out_dtype != TEC_DT_I32)
+    return fail(TEC_E_LOWERING, "int8 conv produces i32");
+  if (pl.kind != MmaKind::kI8 && out_dtype != TEC_DT_F32 && out_dtype != TEC_DT_BF16)
+    return fail(TEC_E_LOWERING, "float conv produces f32 or bf16");
+
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = sm_count(dev);
+  const int64_t m_tiles = (pl.m + 127) / 128;
+
+  // tile_n knob: the "split" of the OC axis.
+  int bn = kn && kn->tile_n ? static_cast<int>(kn->tile_n) : 0;
+  if (!bn) {
+    bn = d->k >= 256 ? 256 : d->k >= 128 ? 128 : 64;
+    if (pl.swz != 128) bn = 64;
+    while (bn > 64 && m_tiles * ((d->k + bn - 1) / bn) < 2 * sms) bn /= 2;
+  }
+  Launcher launch = pick_launcher(pl.kind, bn, pl.swz);
+  if (!launch)
+    return fail(TEC_E_LOWERING, "no sm100 conv instance for tile_n=" +
+                                    std::to_string(bn) + " block=" +
+                                    std::to_string(pl.swz) + "B");
+  if (kn && kn->tile_m && kn->tile_m != 128)
+    return fail(TEC_E_LOWERING, "tile_m must be 128 (tcgen05 M)");
+
+  // A: im2col TMA over the NHWC activation (dims c, w, h, n).
+  CUtensorMap tm_a, tm_b;
+  const CUtensorMapDataType tdt = pl.act == TEC_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                  : pl.act == TEC_DT_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)pl.cp, (cuuint64_t)d->w, (cuuint64_t)d->h,
+                          (cuuint64_t)d->n};
+    cuuint64_t strides[3] = {(cuuint64_t)(pl.cp * es), (cuuint64_t)(pl.cp * es * d->w),
+                             (cuuint64_t)(pl.cp * es * d->w * d->h)};
+    // Bounding box of the window origins (w first, then h), as in the
+    // fprop im2col convention: lower = -pad, upper = pad - (k-1).
+    int lower[2] = {-(int)d->pad_w, -(int)d->pad_h};
+    int upper[2] = {(int)(d->pad_w - (d->s - 1)), (int)(d->pad_h - (d->r - 1))};
+    cuuint32_t estr[4] = {1, (cuuint32_t)d->stride_w, (cuuint32_t)d->stride_h, 1};
+    if (lower[0] < -128 || lower[1] < -128 || upper[0] < -128 || upper[1] < -128 ||
+        d->stride_w > 8 || d->stride_h > 8)
+      return fail(TEC_E_LOWERING, "window outside the TMA im2col range");
+    CUresult r = fns.im2col(&tm_a, tdt, 4, const_cast<void*>(x), dims, strides, lower,
+                            upper, (cuuint32_t)cb, 128, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(pl.swz),
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(TEC_E_CUDA, "cuTensorMapEncodeIm2col failed: " + std::to_string(r));
+    // Same workaround CUTLASS applies for drivers <= 13.1 on small tensors.
+    const int64_t bytes = d->n * d->h * d->w * pl.cp * es;
+    if (fns.driver_version <= 13010 && bytes < 131072)
+      reinterpret_cast<uint64_t*>(&tm_a)[1] &= ~(1ull << 21);
+  }
+  {
+    const int64_t ktot = d->r * d->s * pl.cp;
+    cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)d->k};
+    cuuint64_t strides[1] = {(cuuint64_t)(ktot * es)};
+    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)bn};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fns.tiled(&tm_b, tdt, 2, const_cast<void*>(w), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(pl.swz),
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(TEC_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  }
+
+  ConvGemmParams p{};
+  p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.cp = (int32_t)pl.cp;
+  p.oh = (int32_t)pl.oh; p.ow = (int32_t)pl.ow; p.oc = (int32_t)d->k;
+  p.r = (int32_t)d->r; p.s = (int32_t)d->s;
+  p.sh = (int32_t)d->stride_h; p.sw = (int32_t)d->stride_w;
+  p.ph = (int32_t)d->pad_h; p.pw = (int32_t)d->pad_w;
+  p.m = (int32_t)pl.m;
+  p.m_tiles = (int32_t)m_tiles;
+  p.n_tiles = (int32_t)((d->k + bn - 1) / bn);
+  p.cblocks = (int32_t)(pl.cp / cb);
+  p.out_type = out_dtype;
+  p.y = y;
+  p.err = err;
+  p.epi = epi;
+  const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
+  int grid = (int)std::min<int64_t>(tiles, sms);
+  if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
+  const int e = launch(tm_a, tm_b, p, grid, st);
+  if (e) return cuda_fail(e, "conv_fprop_tc launch");
+  return TEC_OK;
+}
+
+// ------------------------------------------------- host-path workspace
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+tec_status ensure(DevBuf* b, size_t bytes) {
+  if (b->n >= bytes && b->p) return TEC_OK;
+  if (b->p) cudaFree(b->p);
+  b->p = nullptr;
+  b->n = 0;
+  TEC_CUDA(cudaMalloc(&b->p, std::max<size_t>(bytes, 256)));
+  b->n = std::max<size_t>(bytes, 256);
+  return TEC_OK;
+}
+
+struct HostWorkspace {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  DevBuf x_src, w_src, x_pack, w_pack, y_nhwc, y_nchw, bias, res_src, res_pack,
+      mul_src, mul_pack, err;
+};
+
+HostWorkspace& workspace(int dev) {
+  static HostWorkspace ws[16];
+  return ws[dev & 15];
+}
+
+}  // namespace
+
+// ====================================================================
+extern "C" {
+
+int tec_api_version(void) { return TEC_SM100_API_VERSION; }
+
+const char* tec_last_error(void) { return g_last_error.c_str(); }
+
+int tec_device_sm_count(int device) { return sm_count(device); }
+
+tec_status tec_conv_infer(const tec_conv_desc* d, int64_t out_shape[4]) {
+  int64_t oh, ow;
+  tec_status st = infer(d, &oh, &ow);
+  if (st) return st;
+  out_shape[0] = d->n;
+  out_shape[1] = d->k;
+  out_shape[2] = oh;
+  out_shape[3] = ow;
+  return TEC_OK;
+}
+
+tec_status tec_conv_layout_of(const tec_conv_desc* d, tec_conv_layout* out) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  out->oh = pl.oh;
+  out->ow = pl.ow;
+  out->cp = pl.cp;
+  out->act_dtype = pl.act;
+  out->acc_dtype = pl.acc;
+  const int es = elem_bytes(pl.act);
+  out->act_bytes = d->n * d->h * d->w * pl.cp * es;
+  out->wt_bytes = d->depthwise ? d->c * d->r * d->s * es : d->k * d->r * d->s * pl.cp * es;
+  out->out_elems = d->n * d->k * pl.oh * pl.ow;
+  return TEC_OK;
+}
+
+tec_status tec_activation_pack(const tec_conv_desc* d, const void* x_nchw,
+                               void* x_packed, void* stream) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  if (pl.pack_mode < 0) {  // F32 exact path reads the NCHW tensor as is
+    TEC_CUDA(cudaMemcpyAsync(x_packed, x_nchw, d->n * d->c * d->h * d->w * 4,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return TEC_OK;
+  }
+  const int in_t = d->compute == TEC_COMPUTE_I8 ? kI8 : kF32;
+  const int e = launch_pack_activation(x_nchw, in_t, x_packed, d->n, d->c, d->h * d->w,
+                                       pl.cp, pl.pack_mode, (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "pack_activation");
+  return TEC_OK;
+}
+
+tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
+                                   void* w_packed, void* stream) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  if (pl.pack_mode < 0) {  // OIHW == [oc][(ic, rh, rw)]: the reduce order
+    TEC_CUDA(cudaMemcpyAsync(w_packed, w_oihw, d->k * d->c * d->r * d->s * 4,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return TEC_OK;
+  }
+  const int in_t = d->compute == TEC_COMPUTE_I8 ? kI8 : kF32;
+  const int e = launch_pack_weights(w_oihw, in_t, w_packed, d->k, d->c, d->r, d->s,
+                                    pl.cp, d->depthwise, pl.pack_mode, (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "pack_weights");
+  return TEC_OK;
+}
+
+tec_status tec_nchw_to_nhwc(const void* src, int32_t src_dtype, void* dst,
+                            int32_t dst_dtype, int64_t n, int64_t c, int64_t h,
+                            int64_t w, void* stream) {
+  int mode;
+  if (dst_dtype == TEC_DT_BF16) mode = 0;
+  else if (dst_dtype == TEC_DT_F32) mode = 3;
+  else if (dst_dtype == TEC_DT_I32) mode = 4;
+  else if (dst_dtype == TEC_DT_I8) mode = 2;
+  else return fail(TEC_E_LOWERING, "unsupported nhwc dtype");
+  const int in_t = src_dtype == TEC_DT_I32 ? kI32 : src_dtype == TEC_DT_I8 ? kI8 : kF32;
+  const int e = launch_pack_activation(src, in_t, dst, n, c, h * w, c, mode,
+                                       (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "nchw_to_nhwc");
+  return TEC_OK;
+}
+
+tec_status tec_output_unpack(const void* y_nhwc, int32_t y_dtype, void* y_nchw,
+                             int32_t dst_dtype, int64_t n, int64_t c, int64_t h,
+                             int64_t w, void* stream) {
+  const int e = launch_unpack_output(y_nhwc, y_dtype, y_nchw, dst_dtype, n, c, h * w,
+                                     (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "output_unpack");
+  return TEC_OK;
+}
+
+tec_status tec_conv2d_fused(const tec_conv_desc* d, const tec_epilogue* epi,
+                            const tec_knobs* knobs, const void* x_packed,
+                            const void* w_packed, void* y, int32_t out_dtype,
+                            int32_t* err_flag, void* stream) {
+  if (d && d->depthwise)
+    return tec_depthwise_fused(d, epi, knobs, x_packed, w_packed, y, out_dtype,
+                               err_flag, stream);
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  EpilogueParams ep;
+  st = build_epilogue(epi, pl.kind == MmaKind::kI8, &ep);
+  if (st) return st;
+  if (!x_packed || !w_packed || !y) return fail(TEC_E_INTERNAL, "null buffer");
+  if (d->compute == TEC_COMPUTE_F32) {
+    if (out_dtype != TEC_DT_F32) return fail(TEC_E_LOWERING, "f32 path produces f32");
+    ConvGemmParams p{};
+    p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.cp = (int32_t)d->c;
+    p.oh = (int32_t)pl.oh; p.ow = (int32_t)pl.ow; p.oc = (int32_t)d->k;
+    p.r = (int32_t)d->r; p.s = (int32_t)d->s;
+    p.sh = (int32_t)d->stride_h; p.sw = (int32_t)d->stride_w;
+    p.ph = (int32_t)d->pad_h; p.pw = (int32_t)d->pad_w;
+    p.m = (int32_t)pl.m;
+    p.out_type = kF32;
+    p.y = y;
+    p.err = err_flag;
+    p.epi = ep;
+    const int e = launch_conv_f32_exact(static_cast<const float*>(x_packed),
+                                        static_cast<const float*>(w_packed), p,
+                                        (cudaStream_t)stream);
+    if (e) return cuda_fail(e, "conv_f32_exact launch");
+    return TEC_OK;
+  }
+  return run_conv(d, pl, ep, knobs, x_packed, w_packed, y, out_dtype, err_flag,
+                  (cudaStream_t)stream);
+}
+
+tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, const void* x_packed,
+                               const void* w_packed, void* y, int32_t out_dtype,
+                               int32_t* err_flag, void* stream) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  if (!d->depthwise) return fail(TEC_E_LOWERING, "not a depthwise descriptor");
+  EpilogueParams ep;
+  st = build_epilogue(epi, d->compute == TEC_COMPUTE_I8, &ep);
+  if (st) return st;
+  DepthwiseParams p{};
+  p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.c = (int32_t)d->c;
+  p.oh = (int32_t)pl.oh; p.ow = (int32_t)pl.ow;
+  p.r = (int32_t)d->r; p.s = (int32_t)d->s;
+  p.sh = (int32_t)d->stride_h; p.sw = (int32_t)d->stride_w;
+  p.ph = (int32_t)d->pad_h; p.pw = (int32_t)d->pad_w;
+  p.in_type = pl.act == TEC_DT_BF16 ? kBF16 : pl.act == TEC_DT_I8 ? kI8 : kF32;
+  p.out_type = out_dtype == TEC_DT_BF16 ? kBF16 : out_dtype == TEC_DT_I32 ? kI32 : kF32;
+  p.x = x_packed;
+  p.wt = w_packed;
+  p.y = y;
+  p.err = err_flag;
+  p.epi = ep;
+  const int tw = knobs && knobs->unroll ? (int)knobs->unroll : 4;
+  const int e = launch_depthwise(p, tw, (cudaStream_t)stream);
+  if (e == -1)
+    return fail(TEC_E_LOWERING, "depthwise: unsupported dtype pair or C not a multiple of the vector width");
+  if (e) return cuda_fail(e, "depthwise launch");
+  return TEC_OK;
+}
+
+tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, const void* x,
+                               const void* w, void* y, int device) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  const bool integer = d->compute == TEC_COMPUTE_I8;
+  EpilogueParams probe;
+  st = build_epilogue(epi, integer, &probe);
+  if (st) return st;
+  TEC_CUDA(cudaSetDevice(device));
+  HostWorkspace& ws = workspace(device);
+  std::lock_guard<std::mutex> lock(ws.mu);
+  if (!ws.stream) TEC_CUDA(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
+  cudaStream_t s = ws.stream;
+
+  const int in_es = integer ? 1 : 4;
+  const int acc_t = integer ? TEC_DT_I32 : TEC_DT_F32;
+  const int64_t x_elems = d->n * d->c * d->h * d->w;
+  const int64_t w_elems = d->depthwise ? d->c * d->r * d->s : d->k * d->c * d->r * d->s;
+  const int64_t y_elems = d->n * d->k * pl.oh * pl.ow;
+  tec_conv_layout lay;
+  st = tec_conv_layout_of(d, &lay);
+  if (st) return st;
+
+  if ((st = ensure(&ws.x_src, x_elems * in_es))) return st;
+  if ((st = ensure(&ws.w_src, w_elems * in_es))) return st;
+  if ((st = ensure(&ws.x_pack, lay.act_bytes))) return st;
+  if ((st = ensure(&ws.w_pack, lay.wt_bytes))) return st;
+  if ((st = ensure(&ws.y_nhwc, y_elems * 4))) return st;
+  if ((st = ensure(&ws.y_nchw, y_elems * 4))) return st;
+  if ((st = ensure(&ws.err, 4))) return st;
+  TEC_CUDA(cudaMemcpyAsync(ws.x_src.p, x, x_elems * in_es, cudaMemcpyHostToDevice, s));
+  TEC_CUDA(cudaMemcpyAsync(ws.w_src.p, w, w_elems * in_es, cudaMemcpyHostToDevice, s));
+  TEC_CUDA(cudaMemsetAsync(ws.err.p, 0, 4, s));
+
+  tec_epilogue dev_epi;
+  std::memset(&dev_epi, 0, sizeof(dev_epi));
+  if (epi) {
+    dev_epi = *epi;
+    if (epi->bias) {
+      if ((st = ensure(&ws.bias, d->k * 4))) return st;
+      TEC_CUDA(cudaMemcpyAsync(ws.bias.p, epi->bias, d->k * 4, cudaMemcpyHostToDevice, s));
+      dev_epi.bias = ws.bias.p;
+    }
+    // Same-shape operands arrive NCHW; the kernels read them NHWC.
+    const void* srcs[2] = {epi->residual, epi->mul_operand};
+    DevBuf* raw[2] = {&ws.res_src, &ws.mul_src};
+    DevBuf* pk[2] = {&ws.res_pack, &ws.mul_pack};
+    const void** dst[2] = {&dev_epi.residual, &dev_epi.mul_operand};
+    for (int i = 0; i < 2; ++i) {
+      if (!srcs[i]) continue;
+      if ((st = ensure(raw[i], y_elems * 4))) return st;
+      if ((st = ensure(pk[i], y_elems * 4))) return st;
+      TEC_CUDA(cudaMemcpyAsync(raw[i]->p, srcs[i], y_elems * 4, cudaMemcpyHostToDevice, s));
+      st = tec_nchw_to_nhwc(raw[i]->p, acc_t, pk[i]->p, acc_t, d->n, d->k, pl.oh, pl.ow, s);
+      if (st) return st;
+      *dst[i] = pk[i]->p;
+    }
+  }
+  if ((st = tec_activation_pack(d, ws.x_src.p, ws.x_pack.p, s))) return st;
+  if ((st = tec_weight_pretransform(d, ws.w_src.p, ws.w_pack.p, s))) return st;
+  st = tec_conv2d_fused(d, epi ? &dev_epi : nullptr, knobs, ws.x_pack.p, ws.w_pack.p,
+                        ws.y_nhwc.p, acc_t, static_cast<int32_t*>(ws.err.p), s);
+  if (st) return st;
+  if ((st = tec_output_unpack(ws.y_nhwc.p, acc_t, ws.y_nchw.p, acc_t, d->n, d->k, pl.oh,
+                              pl.ow, s)))
+    return st;
+  int32_t err_host = 0;
+  TEC_CUDA(cudaMemcpyAsync(y, ws.y_nchw.p, y_elems * 4, cudaMemcpyDeviceToHost, s));
+  TEC_CUDA(cudaMemcpyAsync(&err_host, ws.err.p, 4, cudaMemcpyDeviceToHost, s));
+  TEC_CUDA(cudaStreamSynchronize(s));
+  if (err_host)
+    return fail(TEC_E_FOLD_OVERFLOW, "value out of range for i32 in the fused epilogue");
+  return TEC_OK;
+}
+
+tec_status tec_measure(const tec_conv_desc* d, const tec_epilogue* epi,
+                       const tec_knobs* knobs, int device, int warmup, int reps,
+                       int flush_l2, double* median_us) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  TEC_CUDA(cudaSetDevice(device));
+  tec_conv_layout lay;
+  if ((st = tec_conv_layout_of(d, &lay))) return st;
+  const bool integer = d->compute == TEC_COMPUTE_I8;
+  const int32_t out_t = integer ? TEC_DT_I32 : TEC_DT_BF16;
+  void *x = nullptr, *w = nullptr, *y = nullptr, *b = nullptr, *r = nullptr, *fl = nullptr;
+  const size_t flush_bytes = 256ull << 20;
+  cudaStream_t s;
+  TEC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  TEC_CUDA(cudaMalloc(&x, lay.act_bytes));
+  TEC_CUDA(cudaMalloc(&w, lay.wt_bytes));
+  TEC_CUDA(cudaMalloc(&y, lay.out_elems * 4));
+  TEC_CUDA(cudaMalloc(&b, d->k * 4));
+  TEC_CUDA(cudaMalloc(&r, lay.out_elems * 4));
+  if (flush_l2) TEC_CUDA(cudaMalloc(&fl, flush_bytes));
+  TEC_CUDA(cudaMemsetAsync(x, 1, lay.act_bytes, s));
+  TEC_CUDA(cudaMemsetAsync(w, 1, lay.wt_bytes, s));
+  TEC_CUDA(cudaMemsetAsync(b, 0, d->k * 4, s));
+  TEC_CUDA(cudaMemsetAsync(r, 0, lay.out_elems * 4, s));
+  tec_epilogue e{};
+  if (epi) {
+    e = *epi;
+    if (e.bias) e.bias = b;
+    if (e.residual) e.residual = r;
+    if (e.mul_operand) e.mul_operand = r;
+  }
+  std::vector<float> times;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int i = 0; i < warmup + reps && st == TEC_OK; ++i) {
+    if (flush_l2) cudaMemsetAsync(fl, i & 0xff, flush_bytes, s);
+    cudaEventRecord(e0, s);
+    st = tec_conv2d_fused(d, epi ? &e : nullptr, knobs, x, w, y, out_t, nullptr, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) {
+      st = fail(TEC_E_CUDA, "measure: kernel failed");
+      break;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (i >= warmup) times.push_back(ms * 1000.f);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(x); cudaFree(w); cudaFree(y); cudaFree(b); cudaFree(r);
+  if (fl) cudaFree(fl);
+  cudaStreamDestroy(s);
+  if (st) return st;
+  if (times.empty()) return fail(TEC_E_INTERNAL, "no repetitions");
+  std::sort(times.begin(), times.end());
+  *median_us = times[times.size() / 2];
+  return TEC_OK;
+}
+
+}  // extern "C"

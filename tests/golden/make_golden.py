@@ -1,0 +1,201 @@
+#!/usr/bin/env python3
+"""Generates the golden fixtures in tests/golden/ by running the REFERENCE.
+
+Run in the build container (where /root/reference exists and
+`make -C oracle ref` has built oracle/_ref/ref_driver):
+
+    python tests/golden/make_golden.py
+
+For every case it writes, under tests/golden/<case>/:
+  graph.json            the reference-format graph (R/src/graph.cpp:146-207)
+  <input>.bin/.json     inputs in the reference's tensor format
+                        (R/src/io.cpp:111-127); random ones come from the
+                        reference's own random_tensor (R/src/tensor.cpp:74-88)
+                        via `ref_driver gen`
+  out/<output>.bin/.json  outputs of the reference's evaluate_graph
+                        (R/src/graph.cpp:227-256) via `ref_driver eval`
+  fused.json            fuse_pass + plan_memory of the graph
+  status                "ok" or the reference error code when it throws
+The reference itself is never needed again: tests read only these files.
+"""
+from __future__ import annotations
+
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+
+
+def save_tensor(d, name, arr, dtype):
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, name + ".json"), "w") as f:
+        json.dump({"name": name, "shape": list(arr.shape), "dtype": dtype}, f)
+    raw = arr.astype({"f32": "<f4", "i32": "<i4", "i8": "i1"}[dtype]).tobytes()
+    with open(os.path.join(d, name + ".bin"), "wb") as f:
+        f.write(raw)
+
+
+def conv_graph(op, x_shape, w_shape, strides, padding, epi, dtype="f32",
+               residual_shape=None):
+    acc = "i32" if dtype == "i8" else "f32"
+    nodes = [
+        {"id": "x", "op": "input", "shape": list(x_shape), "dtype": dtype},
+        {"id": "w", "op": "input", "shape": list(w_shape), "dtype": dtype},
+    ]
+    prev = "conv"
+    body = [{"id": "conv", "op": op, "inputs": ["x", "w"],
+             "attrs": {"strides": list(strides), "padding": list(padding)}}]
+    for i, e in enumerate(epi):
+        nid = f"e{i}_{e[0]}"
+        if e[0] == "scale":
+            body.append({"id": nid, "op": "scale", "inputs": [prev],
+                         "attrs": {"scale": e[1]}})
+        elif e[0] == "bias_add":
+            nodes.append({"id": "b", "op": "input", "shape": [w_shape[0]],
+                          "dtype": acc})
+            body.append({"id": nid, "op": "bias_add", "inputs": [prev, "b"]})
+        elif e[0] in ("add", "mul"):
+            rid = "r" if e[0] == "add" else "m"
+            nodes.append({"id": rid, "op": "input",
+                          "shape": list(residual_shape), "dtype": acc})
+            body.append({"id": nid, "op": e[0], "inputs": [prev, rid]})
+        elif e[0] == "relu":
+            body.append({"id": nid, "op": "relu", "inputs": [prev]})
+        prev = nid
+    return {"nodes": nodes + body, "outputs": [prev]}
+
+
+def out_hw(h, w, k, strides, padding):
+    return ((h + 2 * padding[0] - k[0]) // strides[0] + 1,
+            (w + 2 * padding[1] - k[1]) // strides[1] + 1)
+
+
+CASES = []
+
+
+def case(name, op, x_shape, w_shape, strides=(1, 1), padding=(0, 0), epi=(),
+         dtype="f32", explicit=None, seed=1):
+    CASES.append(dict(name=name, op=op, x_shape=x_shape, w_shape=w_shape,
+                      strides=strides, padding=padding, epi=list(epi),
+                      dtype=dtype, explicit=explicit, seed=seed))
+
+
+# Known-answer tests: 3x3 ones kernel, pad 1 -> corner 4, edge 6,
+# centre 9 (times the value).
+case("kat_ones_pad1", "conv2d", (1, 1, 3, 3), (1, 1, 3, 3), padding=(1, 1),
+     explicit={"x": np.full((1, 1, 3, 3), 2.0, np.float32),
+               "w": np.ones((1, 1, 3, 3), np.float32)})
+case("kat_depthwise", "depthwise_conv2d", (1, 2, 3, 3), (2, 1, 3, 3),
+     padding=(1, 1),
+     explicit={"x": np.stack([np.full((3, 3), 1.0), np.full((3, 3), -3.0)])
+               [None].astype(np.float32),
+               "w": np.stack([np.ones((3, 3)), np.full((3, 3), 0.5)])
+               [:, None].astype(np.float32)})
+case("kat_stride2", "conv2d", (1, 1, 5, 5), (1, 1, 3, 3), strides=(2, 2),
+     padding=(1, 1),
+     explicit={"x": np.arange(25, dtype=np.float32).reshape(1, 1, 5, 5),
+               "w": np.ones((1, 1, 3, 3), np.float32)})
+# The reference's own conv test shape (R/tests/test_lower.cpp:197-209).
+case("conv_unpadded_ref_test", "conv2d", (1, 2, 6, 6), (3, 2, 3, 3), seed=71)
+# Random f32 cases with the fused epilogues fuse_pass produces.
+case("conv_bias_relu", "conv2d", (2, 8, 9, 9), (16, 8, 3, 3), padding=(1, 1),
+     epi=[("bias_add",), ("relu",)], seed=3)
+case("conv_s2_bias_relu", "conv2d", (1, 8, 11, 11), (16, 8, 3, 3),
+     strides=(2, 2), padding=(1, 1), epi=[("bias_add",), ("relu",)], seed=5)
+case("conv_1x1_s2", "conv2d", (1, 16, 8, 8), (32, 16, 1, 1), strides=(2, 2),
+     epi=[("bias_add",)], seed=7)
+case("conv_residual", "conv2d", (1, 16, 8, 8), (16, 16, 3, 3),
+     padding=(1, 1),
+     epi=[("scale", 0.5), ("bias_add",), ("add",), ("relu",)], seed=9)
+case("conv_mul", "conv2d", (1, 4, 6, 6), (8, 4, 3, 3), padding=(1, 1),
+     epi=[("mul",), ("relu",)], seed=10)
+case("conv_asym", "conv2d", (1, 4, 7, 9), (8, 4, 3, 5), strides=(2, 1),
+     padding=(1, 2), epi=[("bias_add",), ("relu",)], seed=11)
+case("conv_stem_k7s2", "conv2d", (1, 3, 16, 16), (16, 3, 7, 7),
+     strides=(2, 2), padding=(3, 3), epi=[("bias_add",), ("relu",)], seed=13)
+case("conv_odd_oc", "conv2d", (1, 5, 6, 7), (3, 5, 3, 3), padding=(1, 1),
+     epi=[("bias_add",)], seed=15)
+# C2 slice at full channel depth: 8 of the 56 rows (16.5 M MACs).
+case("c2_slice", "conv2d", (1, 64, 8, 56), (64, 64, 3, 3), padding=(1, 1),
+     epi=[("bias_add",), ("relu",)], seed=17)
+# Depthwise (MobileNet D-layer structure).
+case("dw_bias_relu", "depthwise_conv2d", (1, 16, 10, 10), (16, 1, 3, 3),
+     padding=(1, 1), epi=[("bias_add",), ("relu",)], seed=19)
+case("dw_s2", "depthwise_conv2d", (2, 32, 9, 9), (32, 1, 3, 3),
+     strides=(2, 2), padding=(1, 1), epi=[("bias_add",), ("relu",)], seed=21)
+# int8 path (i8 x i8 -> i32, bit-exact).
+case("i8_conv_bias_relu", "conv2d", (1, 32, 8, 8), (32, 32, 3, 3),
+     padding=(1, 1), epi=[("bias_add",), ("relu",)], dtype="i8", seed=23)
+case("i8_conv_scale_s2", "conv2d", (1, 16, 9, 9), (32, 16, 3, 3),
+     strides=(2, 2), padding=(1, 1), epi=[("scale", 3.0), ("bias_add",)],
+     dtype="i8", seed=25)
+case("i8_dw", "depthwise_conv2d", (1, 32, 8, 8), (32, 1, 3, 3),
+     padding=(1, 1), epi=[("bias_add",), ("relu",)], dtype="i8", seed=27)
+# Saturation range: all -128 with K = 4608 -> 75,497,472.
+case("i8_saturation", "conv2d", (1, 512, 3, 3), (16, 512, 3, 3),
+     padding=(1, 1), dtype="i8",
+     explicit={"x": np.full((1, 512, 3, 3), -128, np.int8),
+               "w": np.full((16, 512, 3, 3), -128, np.int8)})
+# FoldOverflow: a scale that pushes i32 out of range must raise.
+case("i8_overflow", "conv2d", (1, 512, 3, 3), (16, 512, 3, 3),
+     padding=(1, 1), dtype="i8", epi=[("scale", 64.0)],
+     explicit={"x": np.full((1, 512, 3, 3), -128, np.int8),
+               "w": np.full((16, 512, 3, 3), -128, np.int8)})
+
+
+def run(cmd):
+    subprocess.run(cmd, check=True)
+
+
+def build_case(c):
+    d = os.path.join(HERE, c["name"])
+    if os.path.exists(d):
+        shutil.rmtree(d)
+    os.makedirs(os.path.join(d, "out"))
+    acc = "i32" if c["dtype"] == "i8" else "f32"
+    k = c["w_shape"][2:]
+    oh, ow = out_hw(c["x_shape"][2], c["x_shape"][3], k, c["strides"],
+                    c["padding"])
+    rshape = (c["x_shape"][0], c["w_shape"][0], oh, ow)
+    g = conv_graph(c["op"], c["x_shape"], c["w_shape"], c["strides"],
+                   c["padding"], c["epi"], c["dtype"], rshape)
+    with open(os.path.join(d, "graph.json"), "w") as f:
+        json.dump(g, f, indent=1)
+    seed = c["seed"]
+    for n in g["nodes"]:
+        if n["op"] != "input":
+            continue
+        if c["explicit"] and n["id"] in c["explicit"]:
+            save_tensor(d, n["id"], c["explicit"][n["id"]], n["dtype"])
+        else:
+            seed += 1
+            run([DRIVER, "gen", d, n["id"], n["dtype"], str(seed)] +
+                [str(s) for s in n["shape"]])
+    p = subprocess.run([DRIVER, "eval", os.path.join(d, "graph.json"), d,
+                        os.path.join(d, "out")], capture_output=True, text=True)
+    status = "ok" if p.returncode == 0 else p.stderr.strip()
+    with open(os.path.join(d, "status"), "w") as f:
+        f.write(status + "\n")
+    run([DRIVER, "fuse", os.path.join(d, "graph.json"),
+         os.path.join(d, "fused.json")])
+    print(f"{c['name']}: {status}")
+
+
+def main():
+    if not os.path.exists(DRIVER):
+        sys.exit(f"{DRIVER} missing: run `make -C oracle ref` first")
+    only = set(sys.argv[1:])
+    for c in CASES:
+        if not only or c["name"] in only:
+            build_case(c)
+
+
+if __name__ == "__main__":
+    main()

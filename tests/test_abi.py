@@ -1,0 +1,96 @@
+"""CPU tests of the C ABI boundary: the product library loads, exports every
+symbol include/tec_sm100.h declares, and its host-only entry points apply
+the reference's shape rules and error codes (no GPU needed)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_1802_04799_b200 import _abi
+from paper_1802_04799_b200.ops import conv_desc
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "include", "tec_sm100.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tec_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    lib = _abi.load()
+    names = declared_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in tec_sm100.h but not exported"
+    assert set(names) == set(_abi.SIGNATURES), "ctypes table out of sync with header"
+
+
+def test_api_version():
+    assert _abi.load().tec_api_version() == 1
+
+
+def _desc(**kw):
+    base = dict(n=1, c=64, h=56, w=56, k=64, r=3, s=3, stride_h=1, stride_w=1,
+                pad_h=1, pad_w=1, depthwise=0, compute=_abi.COMPUTE_BF16)
+    base.update(kw)
+    return _abi.ConvDesc(**base)
+
+
+def test_infer_c2():
+    out = (C.c_int64 * 4)()
+    assert _abi.load().tec_conv_infer(C.byref(_desc()), out) == 0
+    assert list(out) == [1, 64, 56, 56]
+
+
+@pytest.mark.parametrize("h,w,r,s,stride,pad,shape", [
+    (224, 224, 7, 7, 2, 3, [1, 64, 112, 112]),   # C1
+    (56, 56, 1, 1, 2, 0, [1, 64, 28, 28]),       # C5-like
+    (7, 7, 3, 3, 1, 1, [1, 64, 7, 7]),           # C12-like
+])
+def test_infer_resnet_shapes(h, w, r, s, stride, pad, shape):
+    out = (C.c_int64 * 4)()
+    d = _desc(h=h, w=w, r=r, s=s, stride_h=stride, stride_w=stride,
+              pad_h=pad, pad_w=pad)
+    assert _abi.load().tec_conv_infer(C.byref(d), out) == 0
+    assert list(out) == shape
+
+
+def test_window_larger_than_input_is_shape_mismatch():
+    out = (C.c_int64 * 4)()
+    st = _abi.load().tec_conv_infer(C.byref(_desc(h=2, w=2, pad_h=0, pad_w=0)), out)
+    assert st == 2  # 1 + ErrorCode::kShapeMismatch
+    assert b"window larger than input" in _abi.load().tec_last_error()
+
+
+def test_depthwise_weight_shape_checked():
+    with pytest.raises(_abi.TecError) as ei:
+        conv_desc("depthwise_conv2d", (1, 8, 4, 4), (4, 1, 3, 3), {}, 1)
+    assert ei.value.code == "ShapeMismatch"
+    with pytest.raises(_abi.TecError) as ei:
+        conv_desc("conv2d", (1, 8, 4, 4), (4, 3, 3, 3), {}, 1)
+    assert ei.value.code == "ShapeMismatch"
+    with pytest.raises(_abi.TecError) as ei:
+        conv_desc("matmul", (1, 8, 4, 4), (4, 8, 3, 3), {}, 1)
+    assert ei.value.code == "UnknownOperator"
+
+
+def test_layout_planning():
+    lay = _abi.ConvLayout()
+    lib = _abi.load()
+    assert lib.tec_conv_layout_of(C.byref(_desc()), C.byref(lay)) == 0
+    assert lay.cp == 64 and lay.act_dtype == _abi.DT_BF16
+    assert lay.act_bytes == 56 * 56 * 64 * 2
+    # stem: 3 channels padded to one 32-byte block
+    assert lib.tec_conv_layout_of(C.byref(_desc(c=3)), C.byref(lay)) == 0
+    assert lay.cp == 16
+    # fp32 parity path stores [hi | hi | lo] channel triplets
+    d = _desc(compute=_abi.COMPUTE_TF32X3)
+    assert lib.tec_conv_layout_of(C.byref(d), C.byref(lay)) == 0
+    assert lay.cp == 192 and lay.act_dtype == _abi.DT_F32
+    d = _desc(compute=_abi.COMPUTE_I8)
+    assert lib.tec_conv_layout_of(C.byref(d), C.byref(lay)) == 0
+    assert lay.cp == 64 and lay.acc_dtype == _abi.DT_I32

@@ -1,0 +1,175 @@
+"""GPU parity: the sm_100a path (through the C ABI, tec_eval_fused_conv)
+against the reference's golden outputs and the oracle restatement.
+
+Bars (comparator = DenseTensor::same_values, R/src/tensor.cpp:56-72:
+|a-b| <= tol * max(|a|, |b|, 1)):
+  * i8 path (tcgen05 kind::i8)   : exact
+  * f32 path (default for f32)   : BIT-IDENTICAL to the reference (the SIMT
+                                   exact-order kernel, conv_f32_exact.cu)
+  * depthwise, every dtype       : bit-identical on the (rounded) inputs
+  * bf16 path (tcgen05 kind::f16): the oracle is fed the SAME bf16-rounded x
+    and w; products are exact, only the f32 accumulation differs. Stated
+    tolerance TOL_BF16 = 2e-3: the tensor-core accumulator truncates, error
+    grows with K (measured 5.7e-4 abs at K = 4608, |y| <= 85).
+  * tf32x3 (fast approximate f32): stated tolerance TOL_TF32X3 = 1e-2.
+"""
+import numpy as np
+import pytest
+
+import golden_cases
+from oracle.oracle_api import (bf16_round, fused_conv as oracle_conv,
+                               max_rel_err, same_values)
+from paper_1802_04799_b200 import TecError
+from paper_1802_04799_b200.ops import fused_conv
+from paper_1802_04799_b200.workloads import MOBILENET_DW, RESNET18_CONVS
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-3
+TOL_TF32X3 = 1e-2
+
+
+def bits(a):
+    return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+def _gpu(c, compute=None):
+    return fused_conv(c.op, c.x, c.w, {"strides": c.strides, "padding": c.padding},
+                      c.epilogue, compute=compute)
+
+
+@pytest.mark.parametrize("name", golden_cases.names())
+def test_golden_bit_identical_to_reference(name):
+    """Default path for each dtype vs the reference's own outputs."""
+    c = golden_cases.load(name)
+    if c.status != "ok":
+        with pytest.raises(TecError) as ei:
+            _gpu(c)
+        assert ei.value.code == "FoldOverflow"
+        return
+    y = _gpu(c)
+    assert y.dtype == c.expected.dtype and y.shape == c.expected.shape
+    assert np.array_equal(bits(y), bits(c.expected)), \
+        f"max rel err {max_rel_err(y, c.expected)}"
+
+
+@pytest.mark.parametrize("name", [n for n in golden_cases.names()
+                                  if not n.startswith("i8")])
+@pytest.mark.parametrize("compute", ["bf16", "tf32x3"])
+def test_golden_tensor_core_float_paths(name, compute):
+    c = golden_cases.load(name)
+    if compute == "bf16":
+        xr, wr, tol = bf16_round(c.x), bf16_round(c.w), TOL_BF16
+    else:
+        xr, wr, tol = c.x, c.w, TOL_TF32X3
+    want = oracle_conv(c.op, xr, wr, c.strides, c.padding, c.epilogue)
+    y = _gpu(c, compute)
+    assert same_values(y, want, tol), f"{compute} max rel err {max_rel_err(y, want)}"
+
+
+def _inputs(shape_x, shape_w, k, integer, seed):
+    rng = np.random.default_rng(seed)
+    if integer:  # reference i8 distribution U{-8..7}, i32 bias U{-100..100}
+        x = rng.integers(-8, 8, shape_x, dtype=np.int8)
+        w = rng.integers(-8, 8, shape_w, dtype=np.int8)
+        b = rng.integers(-100, 101, (k,), dtype=np.int32)
+    else:        # f32 U[-1, 1)
+        x = rng.uniform(-1, 1, shape_x).astype(np.float32)
+        w = rng.uniform(-1, 1, shape_w).astype(np.float32)
+        b = rng.uniform(-1, 1, (k,)).astype(np.float32)
+    return x, w, b
+
+
+def _check(op, x, w, attrs, epi, compute):
+    y = fused_conv(op, x, w, attrs, epi, compute=None if compute == "i8" else compute)
+    if compute == "bf16":
+        x, w = bf16_round(x), bf16_round(w)
+    want = oracle_conv(op, x, w, attrs["strides"], attrs["padding"], epi)
+    if compute in ("i8", "f32"):
+        assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
+    else:
+        tol = TOL_BF16 if compute == "bf16" else TOL_TF32X3
+        assert same_values(y, want, tol), f"max rel err {max_rel_err(y, want)}"
+
+
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8", "tf32x3"])
+@pytest.mark.parametrize("layer", list(RESNET18_CONVS))
+def test_resnet_layer_batch1(layer, compute):
+    hw, c, k, r, s = RESNET18_CONVS[layer]
+    x, w, b = _inputs((1, c, hw, hw), (k, c, r, r), k, compute == "i8",
+                      seed=sum(map(ord, layer)))
+    attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+    _check("conv2d", x, w, attrs, [("bias_add", b), ("relu",)], compute)
+
+
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8"])
+@pytest.mark.parametrize("layer", list(MOBILENET_DW))
+def test_mobilenet_depthwise_batch1(layer, compute):
+    hw, c, s = MOBILENET_DW[layer]
+    x, w, b = _inputs((1, c, hw, hw), (c, 1, 3, 3), c, compute == "i8",
+                      seed=sum(map(ord, layer)))
+    attrs = {"strides": (s, s), "padding": (1, 1)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("depthwise_conv2d", x, w, attrs, epi,
+                   compute=None if compute == "i8" else compute)
+    if compute == "bf16":
+        x, w = bf16_round(x), bf16_round(w)
+    want = oracle_conv("depthwise_conv2d", x, w, attrs["strides"], attrs["padding"], epi)
+    # Depthwise accumulates in the oracle's exact order: bit-identical.
+    assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
+
+
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8"])
+def test_batch_tail_and_multi_image(compute):
+    # M not a multiple of the 128-row tile; tiles spanning several images.
+    x, w, b = _inputs((3, 64, 9, 11), (64, 64, 3, 3), 64, compute == "i8", 5)
+    _check("conv2d", x, w, {"strides": (1, 1), "padding": (1, 1)},
+           [("bias_add", b), ("relu",)], compute)
+
+
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8"])
+def test_resnet_block_residual_epilogue(compute):
+    # conv -> bias_add -> add(shortcut) -> relu: the fused node of every
+    # ResNet basic block's second conv.
+    x, w, b = _inputs((2, 128, 14, 14), (128, 128, 3, 3), 128, compute == "i8", 8)
+    rng = np.random.default_rng(9)
+    if compute == "i8":
+        r = rng.integers(-100, 101, (2, 128, 14, 14), dtype=np.int32)
+    else:
+        r = rng.uniform(-1, 1, (2, 128, 14, 14)).astype(np.float32)
+    _check("conv2d", x, w, {"strides": (1, 1), "padding": (1, 1)},
+           [("bias_add", b), ("add", r), ("relu",)], compute)
+
+
+def test_int8_full_range_exact():
+    # Full-range U{-128..127} stress of the s32 accumulator.
+    rng = np.random.default_rng(3)
+    x = rng.integers(-128, 128, (2, 256, 14, 14), dtype=np.int8)
+    w = rng.integers(-128, 128, (256, 256, 3, 3), dtype=np.int8)
+    y = fused_conv("conv2d", x, w, {"padding": (1, 1)}, [])
+    want = oracle_conv("conv2d", x, w, (1, 1), (1, 1), [])
+    assert np.array_equal(y, want)
+
+
+def test_int8_epilogue_overflow_raises():
+    x = np.full((1, 512, 3, 3), -128, np.int8)
+    w = np.full((16, 512, 3, 3), -128, np.int8)
+    with pytest.raises(TecError) as ei:
+        fused_conv("conv2d", x, w, {"padding": (1, 1)}, [("scale", 64.0)])
+    assert ei.value.code == "FoldOverflow"
+
+
+def test_batch64_c2_bf16_properties():
+    """Full-size BASELINE config (C2, batch 64): size-independent checks --
+    batch linearity (each image equals its own batch-1 run) and a sampled
+    oracle comparison on two images."""
+    x, w, b = _inputs((64, 64, 56, 56), (64, 64, 3, 3), 64, False, 11)
+    attrs = {"strides": (1, 1), "padding": (1, 1)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, compute="bf16")
+    for i in (0, 63):
+        yi = fused_conv("conv2d", x[i:i + 1], w, attrs, epi, compute="bf16")
+        assert np.array_equal(bits(y[i:i + 1]), bits(yi))
+        want = oracle_conv("conv2d", bf16_round(x[i:i + 1]), bf16_round(w),
+                           (1, 1), (1, 1), epi)
+        assert same_values(y[i:i + 1], want, TOL_BF16)
