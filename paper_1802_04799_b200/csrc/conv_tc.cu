@@ -21,8 +21,9 @@
 //  * "tensorize": tcgen05.mma (M=128, N=BN, K=32 bytes) accumulating in
 //    TMEM; two TMEM accumulators let the epilogue of tile i overlap the
 //    MMAs of tile i+1.
-//  * epilogue "compute_at": TMEM -> registers -> scale/bias/residual/relu
-//    -> one global store; intermediates never touch HBM.
+//  * epilogue "compute_at": TMEM -> registers (32 columns per tcgen05.ld)
+//    -> scale/bias/residual/relu on 32-wide register vectors with 128-bit
+//    operand loads -> 128-bit global stores; intermediates never touch HBM.
 //  * persistent grid (one CTA per SM), tiles strided by gridDim.x.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -39,80 +40,184 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kThreads = 256;  // 4 control warps + 4 epilogue warps
+constexpr int kChunk = 32;     // epilogue columns per tcgen05.ld
 
-template <typename OutT>
-__device__ __forceinline__ float load_as_float(const void* p, int64_t i);
-template <>
-__device__ __forceinline__ float load_as_float<float>(const void* p,
-                                                      int64_t i) {
-  return static_cast<const float*>(p)[i];
-}
-template <>
-__device__ __forceinline__ float load_as_float<__nv_bfloat16>(const void* p,
-                                                              int64_t i) {
-  return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
-}
-
-// Float epilogue chain, one op at a time with float rounding per op (the
-// reference materialises every member: R/src/graph.cpp:215-219). __f*_rn
-// forbids FMA contraction so results round exactly like the oracle.
-template <typename OutT>
-__device__ __forceinline__ float epi_float(float v, const EpilogueParams& e,
-                                           int col, int64_t flat) {
-#pragma unroll 1
-  for (int i = 0; i < e.n_ops; ++i) {
-    switch (e.ops[i]) {
-      case kEpiScale:
-        v = __fmul_rn(v, e.fscale[i]);
-        break;
-      case kEpiBias:
-        v = __fadd_rn(v, static_cast<const float*>(e.bias)[col]);
-        break;
-      case kEpiAdd:
-        v = __fadd_rn(v, load_as_float<OutT>(e.residual, flat));
-        break;
-      case kEpiMul:
-        v = __fmul_rn(v, load_as_float<OutT>(e.mul_operand, flat));
-        break;
-      case kEpiRelu:
-        v = (v < 0.0f) ? 0.0f : v;  // std::max(x, 0.0f)
-        break;
-      default:
-        break;
+// 32 consecutive elements of an output-shaped operand, as floats.
+__device__ __forceinline__ void load32_f(const void* base, int64_t off,
+                                         int type, bool vec, int ncols,
+                                         float (&r)[kChunk]) {
+  if (type == kBF16) {
+    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + off;
+    if (vec) {
+      uint4 u[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(u);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        r[2 * i] = f.x;
+        r[2 * i + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) r[j] = j < ncols ? __bfloat162float(p[j]) : 0.f;
+    }
+  } else {
+    const float* p = static_cast<const float*>(base) + off;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(p) + i);
+        r[4 * i] = f.x; r[4 * i + 1] = f.y; r[4 * i + 2] = f.z; r[4 * i + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) r[j] = j < ncols ? p[j] : 0.f;
     }
   }
-  return v;
+}
+
+__device__ __forceinline__ void load32_i(const int32_t* p, bool vec, int ncols,
+                                         int32_t (&r)[kChunk]) {
+  if (vec) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int4 f = __ldg(reinterpret_cast<const int4*>(p) + i);
+      r[4 * i] = f.x; r[4 * i + 1] = f.y; r[4 * i + 2] = f.z; r[4 * i + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) r[j] = j < ncols ? p[j] : 0;
+  }
+}
+
+// Float epilogue chain over one 32-column chunk of one output row. Each
+// member rounds to float separately (the reference materialises every
+// member, R/src/graph.cpp:215-219); __f*_rn forbids FMA contraction.
+__device__ __forceinline__ void epi_chunk_float(const ConvGemmParams& p, int row,
+                                                int col0, int ncols,
+                                                const uint32_t (&acc)[kChunk]) {
+  const EpilogueParams& e = p.epi;
+  const int64_t base = static_cast<int64_t>(row) * p.oc + col0;
+  const bool vec = ncols == kChunk && (p.oc % 8) == 0;
+  float v[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
+#pragma unroll 1
+  for (int i = 0; i < e.n_ops; ++i) {
+    const int op = e.ops[i];
+    if (op == kEpiScale) {
+      const float s = e.fscale[i];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
+    } else if (op == kEpiBias) {
+      float b[kChunk];
+      load32_f(e.bias, col0, kF32, ncols == kChunk, ncols, b);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], b[j]);
+    } else if (op == kEpiAdd) {
+      float r[kChunk];
+      load32_f(e.residual, base, p.out_type, vec, ncols, r);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], r[j]);
+    } else if (op == kEpiMul) {
+      float r[kChunk];
+      load32_f(e.mul_operand, base, p.out_type, vec, ncols, r);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], r[j]);
+    } else if (op == kEpiRelu) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
+    }
+  }
+  if (p.out_type == kBF16) {
+    __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + base;
+    if (vec) {
+      __nv_bfloat162 h[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      uint4* dst = reinterpret_cast<uint4*>(yp);
+      const uint4* src = reinterpret_cast<const uint4*>(h);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[j] = src[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j)
+        if (j < ncols) yp[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* yp = static_cast<float*>(p.y) + base;
+    if (vec) {
+      float4* dst = reinterpret_cast<float4*>(yp);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j)
+        if (j < ncols) yp[j] = v[j];
+    }
+  }
 }
 
 // Integer epilogue: int64 arithmetic, i32 range check after every member
 // (DenseTensor::set_i, R/include/tec/tensor.hpp:63-69).
-__device__ __forceinline__ int32_t epi_int(int64_t v, const EpilogueParams& e,
-                                           int col, int64_t flat,
-                                           bool* overflow) {
+__device__ __forceinline__ void epi_chunk_int(const ConvGemmParams& p, int row,
+                                              int col0, int ncols,
+                                              const uint32_t (&acc)[kChunk],
+                                              bool* overflow) {
+  const EpilogueParams& e = p.epi;
+  const int64_t base = static_cast<int64_t>(row) * p.oc + col0;
+  const bool vec = ncols == kChunk && (p.oc % 4) == 0;
+  int64_t v[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) v[j] = static_cast<int32_t>(acc[j]);
+  bool ovf = false;
 #pragma unroll 1
   for (int i = 0; i < e.n_ops; ++i) {
-    switch (e.ops[i]) {
-      case kEpiScale:
-        v = v * e.iscale[i];
-        break;
-      case kEpiBias:
-        v = v + static_cast<const int32_t*>(e.bias)[col];
-        break;
-      case kEpiAdd:
-        v = v + static_cast<const int32_t*>(e.residual)[flat];
-        break;
-      case kEpiMul:
-        v = v * static_cast<const int32_t*>(e.mul_operand)[flat];
-        break;
-      case kEpiRelu:
-        v = v < 0 ? 0 : v;
-        break;
-      default:
-        break;
+    const int op = e.ops[i];
+    if (op == kEpiScale) {
+      const int64_t s = e.iscale[i];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] *= s;
+    } else if (op == kEpiBias) {
+      int32_t b[kChunk];
+      load32_i(static_cast<const int32_t*>(e.bias) + col0, ncols == kChunk, ncols, b);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] += b[j];
+    } else if (op == kEpiAdd || op == kEpiMul) {
+      int32_t r[kChunk];
+      load32_i(static_cast<const int32_t*>(op == kEpiAdd ? e.residual : e.mul_operand) + base,
+               vec, ncols, r);
+      if (op == kEpiAdd) {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] += r[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] *= r[j];
+      }
+    } else if (op == kEpiRelu) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = v[j] < 0 ? 0 : v[j];
     }
-    if (v < INT32_MIN || v > INT32_MAX) *overflow = true;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      ovf |= (j < ncols) && (v[j] < INT32_MIN || v[j] > INT32_MAX);
   }
-  return static_cast<int32_t>(v);
+  if (ovf) *overflow = true;
+  int32_t* yp = static_cast<int32_t*>(p.y) + base;
+  if (vec) {
+    int4* dst = reinterpret_cast<int4*>(yp);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      dst[j] = make_int4(static_cast<int32_t>(v[4 * j]), static_cast<int32_t>(v[4 * j + 1]),
+                         static_cast<int32_t>(v[4 * j + 2]), static_cast<int32_t>(v[4 * j + 3]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (j < ncols) yp[j] = static_cast<int32_t>(v[j]);
+  }
 }
 
 template <MmaKind KIND, int BN, int STAGES, int SWZ>
@@ -151,7 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = threadIdx.x & 31;
   const int num_tiles = p.m_tiles * p.n_tiles;
   const int k_iters = p.r * p.s * p.cblocks;
-  constexpr int kCB = SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
+  constexpr int kCB =
+      SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_a);
@@ -259,70 +365,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem_base + ((q * 32) << 16) + acc * BN + c0, v);
+      for (int c0 = 0; c0 < BN; c0 += kChunk) {
+        uint32_t v[kChunk];
+        tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + c0, v);
         tmem_ld_wait();
+        if (c0 + kChunk >= BN) {
+          // Every TMEM read of this accumulator is done: hand it back to
+          // the MMA warp before the global stores of the last chunk.
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
         const int col0 = n_tile * BN + c0;
         if (!row_ok || col0 >= p.oc) continue;
-        const int64_t base = static_cast<int64_t>(row) * p.oc + col0;
-        const int ncols = min(16, p.oc - col0);
-        const bool vec_ok = ncols == 16 && (p.oc % 8) == 0;
-        if constexpr (KIND == MmaKind::kI8) {
-          int32_t o[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            o[j] = j < ncols ? epi_int(static_cast<int32_t>(v[j]), p.epi,
-                                       col0 + j, base + j, &overflow)
-                             : 0;
-          int32_t* yp = static_cast<int32_t*>(p.y) + base;
-          if (vec_ok) {
-            int4* dst = reinterpret_cast<int4*>(yp);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_int4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-          } else {
-            for (int j = 0; j < ncols; ++j) yp[j] = o[j];
-          }
-        } else if (p.out_type == kBF16) {
-          float o[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            o[j] = j < ncols ? epi_float<__nv_bfloat16>(__uint_as_float(v[j]),
-                                                        p.epi, col0 + j, base + j)
-                             : 0.f;
-          __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + base;
-          if (vec_ok) {
-            __nv_bfloat162 h[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) h[j] = __floats2bfloat162_rn(o[2 * j], o[2 * j + 1]);
-            uint4* dst = reinterpret_cast<uint4*>(yp);
-            const uint4* src = reinterpret_cast<const uint4*>(h);
-            dst[0] = src[0];
-            dst[1] = src[1];
-          } else {
-            for (int j = 0; j < ncols; ++j) yp[j] = __float2bfloat16_rn(o[j]);
-          }
-        } else {
-          float o[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            o[j] = j < ncols ? epi_float<float>(__uint_as_float(v[j]), p.epi,
-                                                col0 + j, base + j)
-                             : 0.f;
-          float* yp = static_cast<float*>(p.y) + base;
-          if (vec_ok) {
-            float4* dst = reinterpret_cast<float4*>(yp);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-          } else {
-            for (int j = 0; j < ncols; ++j) yp[j] = o[j];
-          }
-        }
+        const int ncols = min(kChunk, p.oc - col0);
+        if constexpr (KIND == MmaKind::kI8)
+          epi_chunk_int(p, row, col0, ncols, v, &overflow);
+        else
+          epi_chunk_float(p, row, col0, ncols, v);
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
     }
     if (overflow && p.err) atomicOr(p.err, 1);
   }
@@ -368,7 +428,7 @@ TEC_INST(MmaKind::kI8, 256, 4, 128)
 TEC_INST(MmaKind::kI8, 64, 8, 64)
 TEC_INST(MmaKind::kI8, 128, 6, 64)
 TEC_INST(MmaKind::kI8, 64, 8, 32)
-// tf32 (fp32-parity 3xTF32 path, K = [hi|hi|lo] x [hi|lo|hi]): 128 B
+// tf32 (approximate-f32 3xTF32 path, K = [hi|hi|lo] x [hi|lo|hi]): 128 B
 // blocks (32 ch), 64 B (16 ch, the stem: 3*3 -> 16 padded channels).
 TEC_INST(MmaKind::kTF32, 64, 8, 128)
 TEC_INST(MmaKind::kTF32, 128, 6, 128)
