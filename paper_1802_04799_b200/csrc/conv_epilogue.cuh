@@ -1,0 +1,326 @@
+// conv_epilogue.cuh -- fused-epilogue helpers shared by the tensor-core conv
+// kernels: accumulator columns straight from TMEM, through the fused members
+// (scale / bias_add / add / mul / relu, R/src/ops.cpp:216-305) in member
+// order, to global memory.
+//
+// Two forms:
+//  * epi_warp_block (default): a warp owns 32 TMEM lanes (= 32 output rows)
+//    and one 32-column block; rows are transposed through a 4 KB swizzled
+//    shared-memory stage so global loads/stores move whole 32-byte sectors.
+//  * epi_chunk_* (fallback for channel counts that are not a multiple of
+//    one 16-byte vector): one thread, one row, 32 columns.
+// Both round every member to float separately (the reference materialises
+// every member, R/src/graph.cpp:215-219; __f*_rn forbids FMA contraction)
+// and range-check every integer member (DenseTensor::set_i,
+// R/include/tec/tensor.hpp:63-69).
+#pragma once
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "conv_params.h"
+#include "sm100_ptx.cuh"
+
+namespace tec_sm100 {
+namespace epi {
+
+constexpr int kChunk = 32;  // epilogue columns per tcgen05.ld
+
+// 32 elements as raw 32-bit words: bf16 pairs packed (16 words) or f32/i32.
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ float word_elem_f(const uint32_t (&w)[kChunk], bool bf, int j) {
+  if (bf) return (j & 1) ? bf16_hi(w[j >> 1]) : bf16_lo(w[j >> 1]);
+  return __uint_as_float(w[j]);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// ------------------------------------------------- per-thread fallback
+__device__ __forceinline__ void fetch_row32(const void* base, int64_t off, int es, int ncols,
+                                            uint32_t (&w)[kChunk]) {
+  if (es == 2) {
+    const uint16_t* h = static_cast<const uint16_t*>(base) + off;
+#pragma unroll
+    for (int j = 0; j < kChunk / 2; ++j) {
+      const uint32_t lo = 2 * j < ncols ? h[2 * j] : 0u;
+      const uint32_t hi = 2 * j + 1 < ncols ? h[2 * j + 1] : 0u;
+      w[j] = lo | (hi << 16);
+    }
+  } else {
+    const uint32_t* s = static_cast<const uint32_t*>(base) + off;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) w[j] = j < ncols ? s[j] : 0u;
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void epi_chunk_float(const P& p, int64_t row, int col0, int ncols,
+                                                bool active, const float* bias_s,
+                                                uint32_t (&acc)[kChunk]) {
+  const EpilogueParams& e = p.epi;
+  const int64_t base = row * p.oc + col0;
+  const bool bf = p.out_type == kBF16;
+  const int es = bf ? 2 : 4;
+  uint32_t opnd[kChunk];
+  tmem_ld_wait();
+  if (!active) return;
+  float v[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
+#pragma unroll 1
+  for (int i = 0; i < e.n_ops; ++i) {
+    const int op = e.ops[i];
+    if (op == kEpiScale) {
+      const float s = e.fscale[i];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
+    } else if (op == kEpiBias) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], bias_s[j]);
+    } else if (op == kEpiAdd) {
+      fetch_row32(e.residual, base, es, ncols, opnd);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], word_elem_f(opnd, bf, j));
+    } else if (op == kEpiMul) {
+      fetch_row32(e.mul_operand, base, es, ncols, opnd);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], word_elem_f(opnd, bf, j));
+    } else if (op == kEpiRelu) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
+    }
+  }
+  if (bf) {
+    __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + base;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (j < ncols) yp[j] = __float2bfloat16_rn(v[j]);
+  } else {
+    float* yp = static_cast<float*>(p.y) + base;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      if (j < ncols) yp[j] = v[j];
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void epi_chunk_int(const P& p, int64_t row, int col0, int ncols,
+                                              bool active, const int32_t* bias_s,
+                                              uint32_t (&acc)[kChunk], bool* overflow) {
+  const EpilogueParams& e = p.epi;
+  const int64_t base = row * p.oc + col0;
+  uint32_t opnd[kChunk];
+  tmem_ld_wait();
+  if (!active) return;
+  bool ovf = false;
+#pragma unroll 1
+  for (int i = 0; i < e.n_ops; ++i) {
+    const int op = e.ops[i];
+    if (op == kEpiAdd) fetch_row32(e.residual, base, 4, ncols, opnd);
+    if (op == kEpiMul) fetch_row32(e.mul_operand, base, 4, ncols, opnd);
+    const int64_t s = e.iscale[i];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      int64_t t = static_cast<int32_t>(acc[j]);
+      if (op == kEpiScale) t *= s;
+      else if (op == kEpiBias) t += bias_s[j];
+      else if (op == kEpiAdd) t += static_cast<int32_t>(opnd[j]);
+      else if (op == kEpiMul) t *= static_cast<int32_t>(opnd[j]);
+      else if (op == kEpiRelu) t = t < 0 ? 0 : t;
+      ovf |= (j < ncols) && (t < INT32_MIN || t > INT32_MAX);
+      acc[j] = static_cast<uint32_t>(static_cast<int32_t>(t));
+    }
+  }
+  int32_t* yp = static_cast<int32_t*>(p.y) + base;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+    if (j < ncols) yp[j] = static_cast<int32_t>(acc[j]);
+  if (ovf) *overflow = true;
+}
+
+// ------------------------------------------- warp-cooperative, coalesced
+// Stage layout: row r of the 32 x (32 * es) block at r * rowbytes, 16-byte
+// chunks XOR-swizzled by their 128-byte line index (conflict-free for both
+// the row-per-thread writes and the line-per-8-lanes reads).
+__device__ __forceinline__ uint32_t stage_off(int row, int chunk, int rowbytes) {
+  const uint32_t lin = static_cast<uint32_t>(row * rowbytes + chunk * 16);
+  return lin ^ (((lin >> 7) & 7u) << 4);
+}
+
+// Coalesced read of a same-shape operand block into each thread's row words.
+template <typename RowFn>
+__device__ __forceinline__ void coalesced_load_block(const void* src, int es, int64_t oc,
+                                                     int col0, int ncols, int lane,
+                                                     RowFn row_of, uint8_t* stage,
+                                                     uint32_t (&w)[kChunk]) {
+  const int rowbytes = 32 * es, cpr = rowbytes / 16, rpi = 32 / cpr;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i >= cpr) break;
+    const int r = i * rpi + lane / cpr;
+    const int c = lane % cpr;
+    const int64_t g = row_of(r);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    const int cc = c * (16 / es);
+    if (g >= 0 && cc < ncols)
+      v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(src) +
+                                               (g * oc + col0 + cc) * es));
+    *reinterpret_cast<uint4*>(stage + stage_off(r, c, rowbytes)) = v;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < cpr) {
+      const uint4 v = *reinterpret_cast<const uint4*>(stage + stage_off(lane, c, rowbytes));
+      w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
+    }
+  }
+  __syncwarp();
+}
+
+template <typename RowFn>
+__device__ __forceinline__ void coalesced_store_block(void* dst, int es, int64_t oc, int col0,
+                                                      int ncols, int lane, RowFn row_of,
+                                                      uint8_t* stage, const uint32_t (&w)[kChunk]) {
+  const int rowbytes = 32 * es, cpr = rowbytes / 16, rpi = 32 / cpr;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < cpr)
+      *reinterpret_cast<uint4*>(stage + stage_off(lane, c, rowbytes)) =
+          make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i >= cpr) break;
+    const int r = i * rpi + lane / cpr;
+    const int c = lane % cpr;
+    const int64_t g = row_of(r);
+    const int cc = c * (16 / es);
+    if (g >= 0 && cc < ncols)
+      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(dst) + (g * oc + col0 + cc) * es) =
+          *reinterpret_cast<const uint4*>(stage + stage_off(r, c, rowbytes));
+  }
+  __syncwarp();
+}
+
+// One 32-column block of one warp. taddr: TMEM address of this warp's lane
+// quadrant at the block's first accumulator column; col0: global column;
+// bias_s: the block's 32 bias values in shared memory. Requires
+// oc % (16 / out_bytes) == 0 (whole 16-byte chunks per row).
+template <bool kInt, typename P, typename RowFn>
+__device__ __forceinline__ void epi_warp_block(const P& p, uint32_t taddr, int col0, int lane,
+                                               RowFn row_of, const uint32_t* bias_s,
+                                               uint8_t* stage, bool* overflow) {
+  const EpilogueParams& e = p.epi;
+  const bool bf = !kInt && p.out_type == kBF16;
+  const int es = bf ? 2 : 4;
+  const int ncols = min(kChunk, p.oc - col0);
+  // One operand buffer: the first same-shape operand in member order is
+  // fetched before waiting on TMEM; any later one is fetched on demand.
+  uint32_t opnd[kChunk];
+  int have = 0;  // EpiOp currently held in opnd
+  const int first_op = e.residual || e.mul_operand
+                           ? (e.residual && (!e.mul_operand) ? kEpiAdd
+                              : (!e.residual)                ? kEpiMul
+                                                             : -1)
+                           : 0;
+  if (first_op > 0) {
+    coalesced_load_block(first_op == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0,
+                         ncols, lane, row_of, stage, opnd);
+    have = first_op;
+  }
+  auto need = [&](int op) {
+    if (have != op) {
+      coalesced_load_block(op == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0, ncols,
+                           lane, row_of, stage, opnd);
+      have = op;
+    }
+  };
+  uint32_t acc[kChunk];
+  tmem_ld32(taddr, acc);
+  tmem_ld_wait();
+  uint32_t out[kChunk];
+  if constexpr (kInt) {
+    // Each member is evaluated in int64 and range-checked before it is
+    // stored back as i32; after an overflow the kernel reports FoldOverflow
+    // (the reference throws), so the wrapped value is never consumed.
+    const bool live = row_of(lane) >= 0;
+    bool ovf = false;
+#pragma unroll 1
+    for (int i = 0; i < e.n_ops; ++i) {
+      const int op = e.ops[i];
+      if (op == kEpiAdd || op == kEpiMul) need(op);
+      const int64_t s = e.iscale[i];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        int64_t t = static_cast<int32_t>(acc[j]);
+        if (op == kEpiScale) t *= s;
+        else if (op == kEpiBias) t += static_cast<int32_t>(bias_s[j]);
+        else if (op == kEpiAdd) t += static_cast<int32_t>(opnd[j]);
+        else if (op == kEpiMul) t *= static_cast<int32_t>(opnd[j]);
+        else if (op == kEpiRelu) t = t < 0 ? 0 : t;
+        ovf |= live && (j < ncols) && (t < INT32_MIN || t > INT32_MAX);
+        acc[j] = static_cast<uint32_t>(static_cast<int32_t>(t));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) out[j] = acc[j];
+    if (ovf) *overflow = true;
+  } else {
+    float v[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
+#pragma unroll 1
+    for (int i = 0; i < e.n_ops; ++i) {
+      const int op = e.ops[i];
+      if (op == kEpiScale) {
+        const float s = e.fscale[i];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
+      } else if (op == kEpiBias) {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], __uint_as_float(bias_s[j]));
+      } else if (op == kEpiAdd) {
+        need(kEpiAdd);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], word_elem_f(opnd, bf, j));
+      } else if (op == kEpiMul) {
+        need(kEpiMul);
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], word_elem_f(opnd, bf, j));
+      } else if (op == kEpiRelu) {
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
+      }
+    }
+    if (bf) {
+#pragma unroll
+      for (int j = 0; j < kChunk / 2; ++j) out[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+#pragma unroll
+      for (int j = kChunk / 2; j < kChunk; ++j) out[j] = 0u;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) out[j] = __float_as_uint(v[j]);
+    }
+  }
+  coalesced_store_block(p.y, es, p.oc, col0, ncols, lane, row_of, stage, out);
+}
+
+// Cooperative per-tile bias staging: `nthreads` epilogue threads copy the
+// tile's BN bias values into shared memory (zero past OC).
+template <typename T>
+__device__ __forceinline__ void stage_bias(T* dst, const void* bias, int col0, int bn,
+                                           int oc, int tid, int nthreads) {
+  for (int i = tid; i < bn; i += nthreads)
+    dst[i] = (bias && col0 + i < oc) ? static_cast<const T*>(bias)[col0 + i] : T(0);
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+}  // namespace epi
+}  // namespace tec_sm100

@@ -1,0 +1,332 @@
+// conv_halo.cu -- stride-1 fused conv2d as a shifted-window implicit GEMM.
+//
+// Why: the im2col kernel (conv_tc.cu) re-reads every input pixel R*S times
+// from L2 (once per filter tap). For ResNet's 3x3 layers that is 9x the
+// activation bytes per CTA tile and the kernel becomes L2->SM bandwidth
+// bound (ncu: 347 MB of L2->SM traffic for the 25.7 MB C2 input). Here a
+// CTA loads the input rows of its tile ONCE per channel block -- one tiled
+// TMA box with the zero padding supplied by TMA out-of-bounds fill -- and
+// every filter tap is a different start address into that halo:
+//
+//   halo pixel q = row * wp + col      (wp = W + 2*pw; 128 B per pixel)
+//   output virtual row v = oh_local * wp + ow
+//   tap (rh, rw) reads halo pixel v + rh * wp + rw
+//
+// The SWIZZLE_128B K-major UMMA descriptor accepts any 128-B-row start
+// (the swizzle is a function of the absolute smem address; verified on
+// B200 by scratch/umma_shift_test.cu), so the shift is free. Virtual rows
+// with ow >= OW are junk and never stored (wp/OW extra work: 3.6% on C2).
+//
+// Pipelines (the paper's virtual-thread latency hiding, as mbarriers):
+//   halo ring (2 stages)   : TMA producer -> MMA, one stage per channel block
+//   weight ring (WSTAGES)  : one (tap, channel block) B tile per stage
+//   TMEM accumulators      : 2 x MS x BN columns, MMA <-> epilogue
+// Weights per tap are reused by all MS*128 virtual rows of the tile.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "conv_epilogue.cuh"
+#include "conv_params.h"
+#include "sm100_ptx.cuh"
+
+namespace tec_sm100 {
+
+namespace {
+
+constexpr int kThreads = 384;     // 4 control warps + 8 epilogue warps
+constexpr int kEpiThreads = 256;
+
+template <int BN, int MS, int SWZ, int WSTAGES>
+struct HaloCfg {
+  static constexpr int kWBytes = BN * SWZ;
+  static constexpr uint32_t kAccCols = MS * BN;
+  static constexpr uint32_t kTmemCols = 2 * kAccCols <= 32    ? 32
+                                        : 2 * kAccCols <= 64  ? 64
+                                        : 2 * kAccCols <= 128 ? 128
+                                        : 2 * kAccCols <= 256 ? 256
+                                                              : 512;
+  static_assert(2 * kAccCols <= 512, "TMEM holds at most 512 columns");
+  static constexpr int kMmaPerTap = SWZ / 32;
+};
+
+__host__ __device__ inline int halo_bytes_aligned(int halo_px, int swz) {
+  return (halo_px * swz + 1023) & ~1023;
+}
+
+template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap tm_x,
+                     const __grid_constant__ CUtensorMap tm_w,
+                     const ConvHaloParams p) {
+  using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int hbytes = halo_bytes_aligned(p.halo_px, SWZ);
+  uint8_t* sH = smem;                       // 2 halo buffers
+  uint8_t* sW = smem + 2 * hbytes;          // WSTAGES weight tiles
+  uint8_t* sStage = sW + WSTAGES * Cfg::kWBytes;  // 8 warps x 4 KB epilogue stage
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
+  uint64_t* hempty = hfull + 2;
+  uint64_t* wfull = hempty + 2;
+  uint64_t* wempty = wfull + WSTAGES;
+  uint64_t* tfull = wempty + WSTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* sBias = reinterpret_cast<uint32_t*>(
+      reinterpret_cast<uint8_t*>(hfull) + 256);  // [2][BN] f32 / i32
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int taps = p.r * p.s;
+  const int num_tiles = p.n * p.bands * p.n_tiles;
+  long long dbg_wait[5] = {0, 0, 0, 0, 0};
+  const long long t_start = p.dbg ? clock64() : 0;
+  constexpr int kCB =
+      SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
+  const uint32_t halo_tx = static_cast<uint32_t>((p.th + p.r - 1) * p.wp * SWZ);
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_w);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hfull[i], 1);
+      mbar_init(&hempty[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);  // one epilogue group per accumulator
+    }
+    for (int i = 0; i < WSTAGES; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&wempty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int hs = 0, ws = 0;
+      uint32_t hph = 0, wph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int n_tile = tile % p.n_tiles;
+        const int rest = tile / p.n_tiles;
+        const int band = rest % p.bands;
+        const int img = rest / p.bands;
+        const int ih0 = band * p.th - p.ph;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          { const long long t0 = p.dbg ? clock64() : 0;
+            mbar_wait(&hempty[hs], hph ^ 1);
+            if (p.dbg) dbg_wait[0] += clock64() - t0; }
+          mbar_arrive_expect_tx(&hfull[hs], halo_tx);
+          // box {CB, wp, th + r - 1, 1} at (c, -pw, ih0, img); TMA fills
+          // the out-of-image pixels with zeros (the select(..., 0) pad).
+          tma_load_4d(sH + hs * hbytes, &tm_x, &hfull[hs], cb * kCB, -p.pw, ih0, img);
+          if (++hs == 2) { hs = 0; hph ^= 1; }
+          for (int t = 0; t < taps; ++t) {
+            { const long long t0 = p.dbg ? clock64() : 0;
+              mbar_wait(&wempty[ws], wph ^ 1);
+              if (p.dbg) dbg_wait[0] += clock64() - t0; }
+            mbar_arrive_expect_tx(&wfull[ws], Cfg::kWBytes);
+            tma_load_2d(sW + ws * Cfg::kWBytes, &tm_w, &wfull[ws],
+                        t * p.cp + cb * kCB, n_tile * BN);
+            if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------ single-thread MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc<KIND>(128, BN);
+      int hs = 0, ws = 0;
+      uint32_t hph = 0, wph = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        { const long long t0 = p.dbg ? clock64() : 0;
+          mbar_wait(&tempty[acc], (use & 1) ^ 1);
+          if (p.dbg) dbg_wait[2] += clock64() - t0; }
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * Cfg::kAccCols;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          { const long long t0 = p.dbg ? clock64() : 0;
+            mbar_wait(&hfull[hs], hph);
+            if (p.dbg) dbg_wait[1] += clock64() - t0; }
+          tc_fence_after();
+          const uint32_t h_base = smem_u32(sH + hs * hbytes);
+          for (int t = 0; t < taps; ++t) {
+            const int rh = t / p.s, rw = t - rh * p.s;
+            const uint32_t shift = static_cast<uint32_t>((rh * p.wp + rw) * SWZ);
+            { const long long t0 = p.dbg ? clock64() : 0;
+              mbar_wait(&wfull[ws], wph);
+              if (p.dbg) dbg_wait[1] += clock64() - t0; }
+            tc_fence_after();
+            const uint32_t w_base = smem_u32(sW + ws * Cfg::kWBytes);
+            const bool first = cb == 0 && t == 0;
+#pragma unroll
+            for (int ms = 0; ms < MS; ++ms) {
+#pragma unroll
+              for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
+                const uint64_t ad = make_smem_desc<SWZ>(
+                    h_base + ms * 128 * SWZ + shift + kk * 32, 8 * SWZ);
+                const uint64_t bd = make_smem_desc<SWZ>(w_base + kk * 32, 8 * SWZ);
+                tc_mma<KIND>(d0 + ms * BN, ad, bd, idesc,
+                             (first && kk == 0) ? 0u : 1u);
+              }
+            }
+            tc_commit(&wempty[ws]);
+            if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
+          }
+          tc_commit(&hempty[hs]);
+          if (++hs == 2) { hs = 0; hph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------- epilogue warps
+    // Two groups of 4 warps; group g drains accumulator g (every other
+    // tile). Warp w reads TMEM lane quadrant (w % 4): 32 virtual rows of
+    // each sub-tile, all BN columns.
+    const uint32_t q = warp & 3;
+    const int grp = static_cast<int>(warp - 4) >> 2;
+    const int gtid = static_cast<int>(threadIdx.x) - (kThreads - kEpiThreads) - grp * 128;
+    uint8_t* stage = sStage + (warp - 4) * 4096;
+    const bool coalesced =
+        p.epi_mode == 0 &&
+        ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
+    int local = 0;
+    bool overflow = false;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      if (acc != grp) continue;
+      const uint32_t use = static_cast<uint32_t>(local >> 1);
+      const int n_tile = tile % p.n_tiles;
+      const int rest = tile / p.n_tiles;
+      const int band = rest % p.bands;
+      const int img = rest / p.bands;
+      uint32_t* bias_s = sBias + acc * BN;
+      epi::named_bar_sync(1 + grp, 128);
+      epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
+      epi::named_bar_sync(1 + grp, 128);
+      const long long tw0 = p.dbg ? clock64() : 0;
+      mbar_wait(&tfull[acc], use & 1);
+      const long long tw1 = p.dbg ? clock64() : 0;
+      if (p.dbg) dbg_wait[3] += tw1 - tw0;
+      tc_fence_after();
+#pragma unroll 1
+      for (int ms = 0; ms < MS; ++ms) {
+        const int vbase = ms * 128 + static_cast<int>(q * 32);
+        // Virtual row -> output row (or -1 for the junk columns ow >= OW
+        // and rows past the band).
+        auto row_of = [&](int r) -> int64_t {
+          const int v = vbase + r;
+          const int ohl = v / p.wp;
+          const int ow = v - ohl * p.wp;
+          const int oh = band * p.th + ohl;
+          if (ohl >= p.th || oh >= p.oh || ow >= p.ow) return -1;
+          return (static_cast<int64_t>(img) * p.oh + oh) * p.ow + ow;
+        };
+        const int64_t row = row_of(static_cast<int>(lane));
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN && p.epi_mode != 2; c0 += epi::kChunk) {  // 2: diagnostic
+          const uint32_t taddr =
+              tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0;
+          const int col0 = n_tile * BN + c0;
+          if (coalesced) {
+            if (col0 < p.oc)
+              epi::epi_warp_block<KIND == MmaKind::kI8>(p, taddr, col0, lane, row_of,
+                                                        bias_s + c0, stage, &overflow);
+          } else {
+            uint32_t vv[epi::kChunk];
+            tmem_ld32(taddr, vv);
+            const bool active = row >= 0 && col0 < p.oc;
+            const int ncols = min(epi::kChunk, p.oc - col0);
+            if constexpr (KIND == MmaKind::kI8)
+              epi::epi_chunk_int(p, row, col0, ncols, active,
+                                 reinterpret_cast<const int32_t*>(bias_s + c0), vv, &overflow);
+            else
+              epi::epi_chunk_float(p, row, col0, ncols, active,
+                                   reinterpret_cast<const float*>(bias_s + c0), vv);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (p.dbg) dbg_wait[4] += clock64() - tw1;
+    }
+    if (overflow && p.err) atomicOr(p.err, 1);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  if (p.dbg) {
+    const bool rep = (warp <= 1 && lane == 0) || threadIdx.x == kThreads - kEpiThreads;
+    if (rep)
+      for (int i = 0; i < 5; ++i)
+        if (dbg_wait[i]) atomicAdd(&p.dbg[i], static_cast<unsigned long long>(dbg_wait[i]));
+    if (threadIdx.x == 0) {
+      atomicAdd(&p.dbg[5], static_cast<unsigned long long>(clock64() - t_start));
+      atomicAdd(&p.dbg[6], static_cast<unsigned long long>((num_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x));
+    }
+  }
+}
+
+}  // namespace
+
+template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
+int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
+                     const ConvHaloParams& p, int grid, cudaStream_t stream) {
+  using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
+  const int smem = 1024 + 2 * halo_bytes_aligned(p.halo_px, SWZ) +
+                   WSTAGES * Cfg::kWBytes + 8 * 4096 + 256 + 2 * BN * 4;
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kfn<<<grid, kThreads, smem, stream>>>(tm_x, tm_w, p);
+  return cudaGetLastError();
+}
+
+// Returns the dynamic smem a configuration needs (host-side planning).
+int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px) {
+  return 1024 + 2 * halo_bytes_aligned(halo_px, swz) + wstages * bn * swz + 8 * 4096 + 256 +
+         2 * bn * 4;
+}
+
+#define TEC_HALO(KIND, BN, MS, SWZ, WS)                                        \
+  template int launch_conv_halo<KIND, BN, MS, SWZ, WS>(                       \
+      const CUtensorMap&, const CUtensorMap&, const ConvHaloParams&, int,    \
+      cudaStream_t);
+
+TEC_HALO(MmaKind::kF16, 64, 1, 128, 6)
+TEC_HALO(MmaKind::kF16, 64, 2, 128, 6)
+TEC_HALO(MmaKind::kF16, 64, 4, 128, 4)
+TEC_HALO(MmaKind::kF16, 128, 1, 128, 6)
+TEC_HALO(MmaKind::kF16, 128, 2, 128, 4)
+TEC_HALO(MmaKind::kF16, 256, 1, 128, 4)
+TEC_HALO(MmaKind::kF16, 64, 2, 32, 8)
+TEC_HALO(MmaKind::kF16, 64, 4, 32, 8)
+TEC_HALO(MmaKind::kI8, 64, 2, 128, 6)
+TEC_HALO(MmaKind::kI8, 64, 4, 128, 4)
+TEC_HALO(MmaKind::kI8, 128, 2, 128, 4)
+TEC_HALO(MmaKind::kI8, 256, 1, 128, 4)
+TEC_HALO(MmaKind::kI8, 64, 2, 32, 8)
+TEC_HALO(MmaKind::kI8, 64, 4, 32, 8)
+TEC_HALO(MmaKind::kI8, 64, 2, 64, 6)
+TEC_HALO(MmaKind::kI8, 64, 4, 64, 6)
+
+#undef TEC_HALO
+
+}  // namespace tec_sm100

@@ -42,6 +42,36 @@ struct ConvGemmParams {
   void* y;              // NHWC [M][OC]
   int32_t* err;         // set to 1 on i32 range overflow (may be null)
   EpilogueParams epi;
+  // Optional pipeline profile (null in production): cycles summed over
+  // CTAs -- [0] producer waiting for free slots, [1] MMA waiting for data,
+  // [2] MMA waiting for a free accumulator, [3] epilogue waiting for an
+  // accumulator, [4] epilogue busy, [5] CTA lifetime, [6] tiles.
+  unsigned long long* dbg;
+  int32_t epi_mode;     // 0: warp-coalesced epilogue, 1: per-thread rows
+};
+
+// Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA
+// tile is `th` output rows of one image (x BN output channels). The input
+// rows it needs, padded left/right, are loaded ONCE per channel block as a
+// (th + r - 1) x wp pixel halo (wp = w + 2*pw); output pixel (oh, ow) of the
+// tile is "virtual row" v = oh_local * wp + ow, and filter tap (rh, rw)
+// reads halo pixel v + rh * wp + rw -- a plain shift of the MMA operand's
+// start address. Virtual rows with ow >= OW are computed and discarded.
+struct ConvHaloParams {
+  int32_t n, h, w, cp;  // input NHWC, cp = stored channels
+  int32_t oh, ow, oc;
+  int32_t r, s, ph, pw;
+  int32_t th, wp;       // rows per tile, padded halo width
+  int32_t bands;        // ceil(oh / th)
+  int32_t n_tiles;      // ceil(oc / BN)
+  int32_t cblocks;      // cp / channels-per-block
+  int32_t halo_px;      // pixels per halo buffer (>= MS*128 + (r-1)*wp + s)
+  int32_t out_type;
+  void* y;              // NHWC [N*OH*OW][OC]
+  int32_t* err;
+  EpilogueParams epi;
+  unsigned long long* dbg;  // optional pipeline profile, as ConvGemmParams
+  int32_t epi_mode;         // 0: warp-coalesced epilogue, 1: per-thread rows
 };
 
 struct DepthwiseParams {

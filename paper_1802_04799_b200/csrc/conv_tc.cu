@@ -33,192 +33,18 @@
 
 #include "conv_params.h"
 #include "sm100_ptx.cuh"
+#include "conv_epilogue.cuh"
 
 namespace tec_sm100 {
 
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 256;  // 4 control warps + 4 epilogue warps
-constexpr int kChunk = 32;     // epilogue columns per tcgen05.ld
-
-// 32 consecutive elements of an output-shaped operand, as floats.
-__device__ __forceinline__ void load32_f(const void* base, int64_t off,
-                                         int type, bool vec, int ncols,
-                                         float (&r)[kChunk]) {
-  if (type == kBF16) {
-    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(base) + off;
-    if (vec) {
-      uint4 u[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(u);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        r[2 * i] = f.x;
-        r[2 * i + 1] = f.y;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) r[j] = j < ncols ? __bfloat162float(p[j]) : 0.f;
-    }
-  } else {
-    const float* p = static_cast<const float*>(base) + off;
-    if (vec) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(p) + i);
-        r[4 * i] = f.x; r[4 * i + 1] = f.y; r[4 * i + 2] = f.z; r[4 * i + 3] = f.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) r[j] = j < ncols ? p[j] : 0.f;
-    }
-  }
-}
-
-__device__ __forceinline__ void load32_i(const int32_t* p, bool vec, int ncols,
-                                         int32_t (&r)[kChunk]) {
-  if (vec) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int4 f = __ldg(reinterpret_cast<const int4*>(p) + i);
-      r[4 * i] = f.x; r[4 * i + 1] = f.y; r[4 * i + 2] = f.z; r[4 * i + 3] = f.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) r[j] = j < ncols ? p[j] : 0;
-  }
-}
-
-// Float epilogue chain over one 32-column chunk of one output row. Each
-// member rounds to float separately (the reference materialises every
-// member, R/src/graph.cpp:215-219); __f*_rn forbids FMA contraction.
-__device__ __forceinline__ void epi_chunk_float(const ConvGemmParams& p, int row,
-                                                int col0, int ncols,
-                                                const uint32_t (&acc)[kChunk]) {
-  const EpilogueParams& e = p.epi;
-  const int64_t base = static_cast<int64_t>(row) * p.oc + col0;
-  const bool vec = ncols == kChunk && (p.oc % 8) == 0;
-  float v[kChunk];
-#pragma unroll
-  for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
-#pragma unroll 1
-  for (int i = 0; i < e.n_ops; ++i) {
-    const int op = e.ops[i];
-    if (op == kEpiScale) {
-      const float s = e.fscale[i];
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
-    } else if (op == kEpiBias) {
-      float b[kChunk];
-      load32_f(e.bias, col0, kF32, ncols == kChunk, ncols, b);
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], b[j]);
-    } else if (op == kEpiAdd) {
-      float r[kChunk];
-      load32_f(e.residual, base, p.out_type, vec, ncols, r);
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], r[j]);
-    } else if (op == kEpiMul) {
-      float r[kChunk];
-      load32_f(e.mul_operand, base, p.out_type, vec, ncols, r);
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], r[j]);
-    } else if (op == kEpiRelu) {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
-    }
-  }
-  if (p.out_type == kBF16) {
-    __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + base;
-    if (vec) {
-      __nv_bfloat162 h[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) h[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-      uint4* dst = reinterpret_cast<uint4*>(yp);
-      const uint4* src = reinterpret_cast<const uint4*>(h);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dst[j] = src[j];
-    } else {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j)
-        if (j < ncols) yp[j] = __float2bfloat16_rn(v[j]);
-    }
-  } else {
-    float* yp = static_cast<float*>(p.y) + base;
-    if (vec) {
-      float4* dst = reinterpret_cast<float4*>(yp);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j)
-        if (j < ncols) yp[j] = v[j];
-    }
-  }
-}
-
-// Integer epilogue: int64 arithmetic, i32 range check after every member
-// (DenseTensor::set_i, R/include/tec/tensor.hpp:63-69).
-__device__ __forceinline__ void epi_chunk_int(const ConvGemmParams& p, int row,
-                                              int col0, int ncols,
-                                              const uint32_t (&acc)[kChunk],
-                                              bool* overflow) {
-  const EpilogueParams& e = p.epi;
-  const int64_t base = static_cast<int64_t>(row) * p.oc + col0;
-  const bool vec = ncols == kChunk && (p.oc % 4) == 0;
-  int64_t v[kChunk];
-#pragma unroll
-  for (int j = 0; j < kChunk; ++j) v[j] = static_cast<int32_t>(acc[j]);
-  bool ovf = false;
-#pragma unroll 1
-  for (int i = 0; i < e.n_ops; ++i) {
-    const int op = e.ops[i];
-    if (op == kEpiScale) {
-      const int64_t s = e.iscale[i];
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] *= s;
-    } else if (op == kEpiBias) {
-      int32_t b[kChunk];
-      load32_i(static_cast<const int32_t*>(e.bias) + col0, ncols == kChunk, ncols, b);
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] += b[j];
-    } else if (op == kEpiAdd || op == kEpiMul) {
-      int32_t r[kChunk];
-      load32_i(static_cast<const int32_t*>(op == kEpiAdd ? e.residual : e.mul_operand) + base,
-               vec, ncols, r);
-      if (op == kEpiAdd) {
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] += r[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] *= r[j];
-      }
-    } else if (op == kEpiRelu) {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = v[j] < 0 ? 0 : v[j];
-    }
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j)
-      ovf |= (j < ncols) && (v[j] < INT32_MIN || v[j] > INT32_MAX);
-  }
-  if (ovf) *overflow = true;
-  int32_t* yp = static_cast<int32_t*>(p.y) + base;
-  if (vec) {
-    int4* dst = reinterpret_cast<int4*>(yp);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      dst[j] = make_int4(static_cast<int32_t>(v[4 * j]), static_cast<int32_t>(v[4 * j + 1]),
-                         static_cast<int32_t>(v[4 * j + 2]), static_cast<int32_t>(v[4 * j + 3]));
-  } else {
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j)
-      if (j < ncols) yp[j] = static_cast<int32_t>(v[j]);
-  }
-}
+constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
+constexpr int kEpiThreads = 256;
+using epi::kChunk;
+using epi::epi_chunk_float;
+using epi::epi_chunk_int;
 
 template <MmaKind KIND, int BN, int STAGES, int SWZ>
 struct ConvCfg {
@@ -231,8 +57,10 @@ struct ConvCfg {
                                         : 2 * BN <= 128 ? 128
                                         : 2 * BN <= 256 ? 256
                                                         : 512;
-  static constexpr int kSmemBytes =
-      1024 /*align slack*/ + STAGES * kStageBytes + 256 /*barriers*/;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + STAGES * kStageBytes +
+                                    8 * 4096 /*epilogue stage*/ + 256 /*barriers*/ +
+                                    2 * BN * 4 /*bias*/;
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 };
 
 template <MmaKind KIND, int BN, int STAGES, int SWZ>
@@ -246,16 +74,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::kBBytes);
+  uint8_t* sStage = sB + STAGES * Cfg::kBBytes;  // 8 warps x 4 KB epilogue stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* sBias = reinterpret_cast<uint32_t*>(
+      reinterpret_cast<uint8_t*>(full) + 256);  // [2][BN] f32 / i32
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
   const int num_tiles = p.m_tiles * p.n_tiles;
   const int k_iters = p.r * p.s * p.cblocks;
+  long long dbg_wait[5] = {0, 0, 0, 0, 0};
+  const long long t_start = p.dbg ? clock64() : 0;
   constexpr int kCB =
       SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
 
@@ -268,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 128);  // one epilogue group (4 warps) per accumulator
     }
     fence_barrier_init();
   }
@@ -298,7 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int s = 0; s < p.s; ++s) {
             const int kbase = (r * p.s + s) * p.cp;
             for (int cb = 0; cb < p.cblocks; ++cb) {
-              mbar_wait(&empty[stage], phase ^ 1);
+              { const long long t0 = p.dbg ? clock64() : 0;
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (p.dbg) dbg_wait[0] += clock64() - t0; }
               mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
               tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a,
                                  &full[stage], cb * kCB, w0, h0, img,
@@ -326,11 +161,15 @@ __global__ void __launch_bounds__(kThreads, 1)
            tile += gridDim.x, ++local) {
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
-        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        { const long long t0 = p.dbg ? clock64() : 0;
+          mbar_wait(&tempty[acc], (use & 1) ^ 1);
+          if (p.dbg) dbg_wait[2] += clock64() - t0; }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int k = 0; k < k_iters; ++k) {
-          mbar_wait(&full[stage], phase);
+          { const long long t0 = p.dbg ? clock64() : 0;
+            mbar_wait(&full[stage], phase);
+            if (p.dbg) dbg_wait[1] += clock64() - t0; }
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * Cfg::kABytes);
           const uint32_t b_base = smem_u32(sB + stage * Cfg::kBBytes);
@@ -351,38 +190,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------- epilogue warps
-    const uint32_t q = warp - 4;  // TMEM lane quadrant owned by this warp
+    // Two groups of 4 warps; group g drains accumulator g, i.e. every
+    // other tile, so two tiles' epilogues proceed concurrently. Warp w reads
+    // TMEM lane quadrant (w % 4) = 32 output rows, all BN columns.
+    const uint32_t q = warp & 3;
+    const int grp = static_cast<int>(warp - 4) >> 2;
+    const int gtid = static_cast<int>(threadIdx.x) - (kThreads - kEpiThreads) - grp * 128;
+    uint8_t* stage = sStage + (warp - 4) * 4096;
+    const bool coalesced =
+        p.epi_mode == 0 &&
+        ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
     int local = 0;
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles;
          tile += gridDim.x, ++local) {
       const int acc = local & 1;
+      if (acc != grp) continue;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
       const int m_tile = tile / p.n_tiles;
       const int n_tile = tile - m_tile * p.n_tiles;
-      const int row = m_tile * kBM + static_cast<int>(q * 32 + lane);
+      const int row0 = m_tile * kBM + static_cast<int>(q * 32);
+      const int row = row0 + static_cast<int>(lane);
       const bool row_ok = row < p.m;
+      // Per-tile bias copy in smem (one buffer per group).
+      uint32_t* bias_s = sBias + acc * BN;
+      epi::named_bar_sync(1 + grp, 128);  // previous tile's readers are done
+      epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
+      epi::named_bar_sync(1 + grp, 128);
+      const long long tw0 = p.dbg ? clock64() : 0;
       mbar_wait(&tfull[acc], use & 1);
+      const long long tw1 = p.dbg ? clock64() : 0;
+      if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
+      auto row_of = [&](int r) -> int64_t {
+        const int g = row0 + r;
+        return g < p.m ? static_cast<int64_t>(g) : int64_t(-1);
+      };
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += kChunk) {
-        uint32_t v[kChunk];
-        tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + c0, v);
-        tmem_ld_wait();
-        if (c0 + kChunk >= BN) {
-          // Every TMEM read of this accumulator is done: hand it back to
-          // the MMA warp before the global stores of the last chunk.
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
-        }
+      for (int c0 = 0; c0 < BN && p.epi_mode != 2; c0 += kChunk) {  // 2: no epilogue (diagnostic)
+        const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN + c0;
         const int col0 = n_tile * BN + c0;
-        if (!row_ok || col0 >= p.oc) continue;
-        const int ncols = min(kChunk, p.oc - col0);
-        if constexpr (KIND == MmaKind::kI8)
-          epi_chunk_int(p, row, col0, ncols, v, &overflow);
-        else
-          epi_chunk_float(p, row, col0, ncols, v);
+        if (coalesced) {
+          if (col0 < p.oc)
+            epi::epi_warp_block<KIND == MmaKind::kI8>(p, taddr, col0, lane, row_of,
+                                                      bias_s + c0, stage, &overflow);
+        } else {
+          uint32_t v[kChunk];
+          tmem_ld32(taddr, v);
+          const bool active = row_ok && col0 < p.oc;
+          const int ncols = min(kChunk, p.oc - col0);
+          if constexpr (KIND == MmaKind::kI8)
+            epi_chunk_int(p, row, col0, ncols, active,
+                          reinterpret_cast<const int32_t*>(bias_s + c0), v, &overflow);
+          else
+            epi_chunk_float(p, row, col0, ncols, active,
+                            reinterpret_cast<const float*>(bias_s + c0), v);
+        }
       }
+      // All of this thread's TMEM reads of the accumulator are complete
+      // (each block waited on tcgen05.ld): hand it back to the MMA warp.
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (p.dbg) dbg_wait[4] += clock64() - tw1;
     }
     if (overflow && p.err) atomicOr(p.err, 1);
   }
@@ -391,6 +260,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<ConvCfg<KIND, BN, STAGES, SWZ>::kTmemCols>(tmem_base);
+  if (p.dbg) {
+    // one representative thread per role: producer / MMA lane 0 of warps
+    // 0 / 1, and epilogue thread 0 (its waits are typical of the group).
+    const bool rep = (warp <= 1 && lane == 0) || threadIdx.x == kThreads - kEpiThreads;
+    if (rep)
+      for (int i = 0; i < 5; ++i)
+        if (dbg_wait[i]) atomicAdd(&p.dbg[i], static_cast<unsigned long long>(dbg_wait[i]));
+    if (threadIdx.x == 0) {
+      atomicAdd(&p.dbg[5], static_cast<unsigned long long>(clock64() - t_start));
+      atomicAdd(&p.dbg[6], static_cast<unsigned long long>((num_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x));
+    }
+  }
 }
 
 }  // namespace
@@ -417,22 +298,22 @@ int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
 
 // bf16: 128 B channel blocks (64 ch) for Cp % 64 == 0, 32 B (16 ch) for
 // the stem (C1, 3 -> 16 padded channels).
-TEC_INST(MmaKind::kF16, 64, 8, 128)
-TEC_INST(MmaKind::kF16, 128, 6, 128)
-TEC_INST(MmaKind::kF16, 256, 4, 128)
+TEC_INST(MmaKind::kF16, 64, 7, 128)
+TEC_INST(MmaKind::kF16, 128, 5, 128)
+TEC_INST(MmaKind::kF16, 256, 3, 128)
 TEC_INST(MmaKind::kF16, 64, 8, 32)
 // int8: 128 B blocks (128 ch), 64 B (64 ch), 32 B (32 ch, the stem).
-TEC_INST(MmaKind::kI8, 64, 8, 128)
-TEC_INST(MmaKind::kI8, 128, 6, 128)
-TEC_INST(MmaKind::kI8, 256, 4, 128)
+TEC_INST(MmaKind::kI8, 64, 7, 128)
+TEC_INST(MmaKind::kI8, 128, 5, 128)
+TEC_INST(MmaKind::kI8, 256, 3, 128)
 TEC_INST(MmaKind::kI8, 64, 8, 64)
 TEC_INST(MmaKind::kI8, 128, 6, 64)
 TEC_INST(MmaKind::kI8, 64, 8, 32)
 // tf32 (approximate-f32 3xTF32 path, K = [hi|hi|lo] x [hi|lo|hi]): 128 B
 // blocks (32 ch), 64 B (16 ch, the stem: 3*3 -> 16 padded channels).
-TEC_INST(MmaKind::kTF32, 64, 8, 128)
-TEC_INST(MmaKind::kTF32, 128, 6, 128)
-TEC_INST(MmaKind::kTF32, 256, 4, 128)
+TEC_INST(MmaKind::kTF32, 64, 7, 128)
+TEC_INST(MmaKind::kTF32, 128, 5, 128)
+TEC_INST(MmaKind::kTF32, 256, 3, 128)
 TEC_INST(MmaKind::kTF32, 64, 8, 64)
 
 #undef TEC_INST

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "conv_params.h"
@@ -199,7 +200,96 @@ __global__ void pack_weights_rsc_kernel(const InT* __restrict__ w,
   }
 }
 
+// Space-to-depth (factor 2) packing for strided stems (C1: 7x7 stride 2 on
+// 3 channels). The padded input is folded 2x2 into channels so the strided
+// conv becomes a stride-1 conv with ceil(R/2) x ceil(S/2) taps over 4*C
+// channels -- every tensor-core K step then carries real data (12 of 16
+// channels instead of 3 of 16) and the conv runs on the stride-1 kernels.
+//   out[n][i][j][(dy*2+dx)*C + c] = x[n][c][2i+dy-ph][2j+dx-pw]  (0 outside)
+template <typename InT>
+__global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ out,
+                                int64_t n, int64_t c, int64_t h, int64_t w, int64_t ph,
+                                int64_t pw, int64_t h2, int64_t w2, int64_t cp, int mode) {
+  const int64_t total = n * h2 * w2 * cp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ch = i % cp;
+    int64_t t = i / cp;
+    const int64_t jj = t % w2;
+    t /= w2;
+    const int64_t ii = t % h2;
+    const int64_t nn = t / h2;
+    float v = 0.f;
+    if (ch < 4 * c) {
+      const int64_t q = ch / c, cc = ch % c;
+      const int64_t y = 2 * ii + q / 2 - ph, x = 2 * jj + q % 2 - pw;
+      if (y >= 0 && y < h && x >= 0 && x < w)
+        v = static_cast<float>(in[((nn * c + cc) * h + y) * w + x]);
+    }
+    if (mode == kPackBF16)
+      static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    else
+      static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
+  }
+}
+
+// Matching weights: [K][R2][S2][cp], w2[k][ri][sj][(dy*2+dx)*C + c] =
+// w[k][c][2ri+dy][2sj+dx] (0 past the original R x S window).
+template <typename InT>
+__global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restrict__ out,
+                                        int64_t k, int64_t c, int64_t r, int64_t s, int64_t r2,
+                                        int64_t s2, int64_t cp, int mode) {
+  const int64_t total = k * r2 * s2 * cp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ch = i % cp;
+    int64_t t = i / cp;
+    const int64_t sj = t % s2;
+    t /= s2;
+    const int64_t ri = t % r2;
+    const int64_t kk = t / r2;
+    float v = 0.f;
+    if (ch < 4 * c) {
+      const int64_t q = ch / c, cc = ch % c;
+      const int64_t rr = 2 * ri + q / 2, ss = 2 * sj + q % 2;
+      if (rr < r && ss < s) v = static_cast<float>(w[((kk * c + cc) * r + rr) * s + ss]);
+    }
+    if (mode == kPackBF16)
+      static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    else
+      static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
+  }
+}
+
 // ----------------------------------------------------------- launchers
+int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c, int64_t h,
+                    int64_t w, int64_t ph, int64_t pw, int64_t h2, int64_t w2, int64_t cp,
+                    int mode, cudaStream_t st) {
+  const int64_t total = n * h2 * w2 * cp;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+  if (in_type == kI8)
+    pack_s2d_kernel<int8_t><<<blocks, 256, 0, st>>>(static_cast<const int8_t*>(in), out, n, c,
+                                                    h, w, ph, pw, h2, w2, cp, mode);
+  else
+    pack_s2d_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(in), out, n, c, h,
+                                                   w, ph, pw, h2, w2, cp, mode);
+  return cudaGetLastError();
+}
+
+int launch_pack_weights_s2d(const void* w, int in_type, void* out, int64_t k, int64_t c,
+                            int64_t r, int64_t s, int64_t r2, int64_t s2, int64_t cp, int mode,
+                            cudaStream_t st) {
+  const int64_t total = k * r2 * s2 * cp;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4096));
+  if (in_type == kI8)
+    pack_weights_s2d_kernel<int8_t><<<blocks, 256, 0, st>>>(static_cast<const int8_t*>(w), out,
+                                                            k, c, r, s, r2, s2, cp, mode);
+  else
+    pack_weights_s2d_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(w), out, k,
+                                                           c, r, s, r2, s2, cp, mode);
+  return cudaGetLastError();
+}
+
 int launch_pack_activation(const void* in, int in_type, void* out, int64_t n,
                            int64_t c, int64_t hw, int64_t cp, int mode,
                            cudaStream_t st) {

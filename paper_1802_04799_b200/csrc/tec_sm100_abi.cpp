@@ -38,8 +38,18 @@ int launch_pack_weights(const void* w, int in_type, void* out, int64_t k,
                         int64_t c, int64_t r, int64_t s, int64_t cp,
                         int depthwise, int mode, cudaStream_t st);
 int launch_depthwise(const DepthwiseParams& p, int tw, cudaStream_t st);
+int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c, int64_t h,
+                    int64_t w, int64_t ph, int64_t pw, int64_t h2, int64_t w2, int64_t cp,
+                    int mode, cudaStream_t st);
+int launch_pack_weights_s2d(const void* w, int in_type, void* out, int64_t k, int64_t c,
+                            int64_t r, int64_t s, int64_t r2, int64_t s2, int64_t cp, int mode,
+                            cudaStream_t st);
 int launch_conv_f32_exact(const float* x, const float* w,
                           const ConvGemmParams& p, cudaStream_t st);
+template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
+int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
+                     const ConvHaloParams& p, int grid, cudaStream_t stream);
+int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px);
 }  // namespace tec_sm100
 
 using namespace tec_sm100;
@@ -125,6 +135,10 @@ struct Plan {
   int pack_mode;    // layout.cu PackMode
   int swz;          // channel-block bytes (128/64/32)
   MmaKind kind;
+  // Space-to-depth stem layout (stride-2 conv on <= 4 / 8 channels): the
+  // op runs as a stride-1 (r2 x s2) conv over an (h2 x w2 x cp) input.
+  bool s2d = false;
+  int64_t h2 = 0, w2 = 0, r2 = 0, s2 = 0;
 };
 
 tec_status infer(const tec_conv_desc* d, int64_t* oh, int64_t* ow) {
@@ -204,6 +218,19 @@ tec_status make_plan(const tec_conv_desc* d, Plan* p) {
     default:
       return fail(TEC_E_LOWERING, "unknown compute mode " + std::to_string(d->compute));
   }
+  // Strided stem on few channels -> space-to-depth, when the folded
+  // stride-1 conv has exactly the same output grid.
+  const int64_t s2d_c = d->compute == TEC_COMPUTE_BF16 ? 16 : d->compute == TEC_COMPUTE_I8 ? 32 : 0;
+  if (!d->depthwise && s2d_c && d->stride_h == 2 && d->stride_w == 2 && 4 * d->c <= s2d_c) {
+    const int64_t h2 = (d->h + 2 * d->pad_h + 1) / 2, w2 = (d->w + 2 * d->pad_w + 1) / 2;
+    const int64_t r2 = (d->r + 1) / 2, s2 = (d->s + 1) / 2;
+    if (h2 - r2 + 1 == p->oh && w2 - s2 + 1 == p->ow && h2 <= 65535 && w2 <= 256) {
+      p->s2d = true;
+      p->h2 = h2; p->w2 = w2; p->r2 = r2; p->s2 = s2;
+      p->cp = s2d_c;
+      p->swz = 32;
+    }
+  }
   return TEC_OK;
 }
 
@@ -251,22 +278,171 @@ using Launcher = int (*)(const CUtensorMap&, const CUtensorMap&,
 Launcher pick_launcher(MmaKind kind, int bn, int swz) {
 #define TEC_CASE(K, BN, ST, SW) \
   if (kind == K && bn == BN && swz == SW) return &launch_conv_fprop_tc<K, BN, ST, SW>;
-  TEC_CASE(MmaKind::kF16, 64, 8, 128)
-  TEC_CASE(MmaKind::kF16, 128, 6, 128)
-  TEC_CASE(MmaKind::kF16, 256, 4, 128)
+  TEC_CASE(MmaKind::kF16, 64, 7, 128)
+  TEC_CASE(MmaKind::kF16, 128, 5, 128)
+  TEC_CASE(MmaKind::kF16, 256, 3, 128)
   TEC_CASE(MmaKind::kF16, 64, 8, 32)
-  TEC_CASE(MmaKind::kI8, 64, 8, 128)
-  TEC_CASE(MmaKind::kI8, 128, 6, 128)
-  TEC_CASE(MmaKind::kI8, 256, 4, 128)
+  TEC_CASE(MmaKind::kI8, 64, 7, 128)
+  TEC_CASE(MmaKind::kI8, 128, 5, 128)
+  TEC_CASE(MmaKind::kI8, 256, 3, 128)
   TEC_CASE(MmaKind::kI8, 64, 8, 64)
   TEC_CASE(MmaKind::kI8, 128, 6, 64)
   TEC_CASE(MmaKind::kI8, 64, 8, 32)
-  TEC_CASE(MmaKind::kTF32, 64, 8, 128)
-  TEC_CASE(MmaKind::kTF32, 128, 6, 128)
-  TEC_CASE(MmaKind::kTF32, 256, 4, 128)
+  TEC_CASE(MmaKind::kTF32, 64, 7, 128)
+  TEC_CASE(MmaKind::kTF32, 128, 5, 128)
+  TEC_CASE(MmaKind::kTF32, 256, 3, 128)
   TEC_CASE(MmaKind::kTF32, 64, 8, 64)
 #undef TEC_CASE
   return nullptr;
+}
+
+// ------------------------------------------- shifted-window (halo) path
+using HaloLauncher = int (*)(const CUtensorMap&, const CUtensorMap&,
+                             const ConvHaloParams&, int, cudaStream_t);
+struct HaloInst {
+  MmaKind kind;
+  int bn, ms, swz, wstages;
+  HaloLauncher fn;
+};
+#define TEC_H(K, BN, MS, SW, WS) {K, BN, MS, SW, WS, &launch_conv_halo<K, BN, MS, SW, WS>}
+const HaloInst kHaloInsts[] = {
+    TEC_H(MmaKind::kF16, 64, 1, 128, 6),  TEC_H(MmaKind::kF16, 64, 2, 128, 6),
+    TEC_H(MmaKind::kF16, 64, 4, 128, 4),  TEC_H(MmaKind::kF16, 128, 1, 128, 6),
+    TEC_H(MmaKind::kF16, 128, 2, 128, 4), TEC_H(MmaKind::kF16, 256, 1, 128, 4),
+    TEC_H(MmaKind::kF16, 64, 2, 32, 8),   TEC_H(MmaKind::kF16, 64, 4, 32, 8),
+    TEC_H(MmaKind::kI8, 64, 2, 128, 6),   TEC_H(MmaKind::kI8, 64, 4, 128, 4),
+    TEC_H(MmaKind::kI8, 128, 2, 128, 4),  TEC_H(MmaKind::kI8, 256, 1, 128, 4),
+    TEC_H(MmaKind::kI8, 64, 2, 64, 6),    TEC_H(MmaKind::kI8, 64, 4, 64, 6),
+    TEC_H(MmaKind::kI8, 64, 2, 32, 8),    TEC_H(MmaKind::kI8, 64, 4, 32, 8),
+};
+#undef TEC_H
+
+struct HaloChoice {
+  const HaloInst* inst = nullptr;
+  int th = 0, halo_px = 0, bands = 0, n_tiles = 0, tiles = 0;
+};
+
+// Picks (BN, MS, rows per tile) by a two-term model per tile --
+// max(MMA cycles, L2->SM bytes / 40 B/cycle) -- times the number of waves
+// over the SMs. Returns false when no halo instance fits.
+bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int sms,
+               HaloChoice* out) {
+  if (d->stride_h != 1 || d->stride_w != 1) return false;
+  const int wp = (int)(d->w + 2 * d->pad_w);
+  const int es = elem_bytes(pl.act);
+  if (wp > 256 || (pl.oh + d->r - 1) < 1) return false;
+  double best = 1e30;
+  for (const HaloInst& hi : kHaloInsts) {
+    if (hi.kind != pl.kind || hi.swz != pl.swz) continue;
+    if (kn && kn->tile_n && kn->tile_n != hi.bn) continue;
+    if (kn && kn->tile_m && kn->tile_m != 128 * hi.ms) continue;
+    if (hi.bn > 64 && hi.bn > d->k) continue;
+    const int th = (int)std::min<int64_t>(pl.oh, (128 * hi.ms) / wp);
+    if (th < 1 || th + d->r - 1 > 256) continue;
+    const int halo_px = 128 * hi.ms + (int)((d->r - 1) * wp + d->s) + 8;
+    if (conv_halo_smem_bytes(hi.bn, hi.swz, hi.wstages, halo_px) > 227 * 1024) continue;
+    const int bands = (int)((pl.oh + th - 1) / th);
+    const int n_tiles = (int)((d->k + hi.bn - 1) / hi.bn);
+    const int64_t tiles = d->n * bands * n_tiles;
+    const double ktot = (double)d->r * d->s * pl.cp;
+    const double mma = 128.0 * hi.ms * hi.bn * ktot * 2 / 8192.0 *
+                       (pl.kind == MmaKind::kTF32 ? 2 : pl.kind == MmaKind::kI8 ? 0.5 : 1);
+    const double bytes = (double)hi.bn * ktot * es +
+                         (double)(th + d->r - 1) * wp * pl.cp * es;
+    const double per_tile = std::max(mma, bytes / 40.0);
+    const double cost = (double)((tiles + sms - 1) / sms) * per_tile;
+    if (cost < best) {
+      best = cost;
+      out->inst = &hi;
+      out->th = th;
+      out->halo_px = halo_px;
+      out->bands = bands;
+      out->n_tiles = n_tiles;
+      out->tiles = (int)tiles;
+    }
+  }
+  return out->inst != nullptr;
+}
+
+tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoice& hc,
+                         const EpilogueParams& epi, const tec_knobs* kn, const void* x,
+                         const void* w, void* y, int32_t out_dtype, int32_t* err,
+                         cudaStream_t st, int sms) {
+  const DriverFns& fns = driver_fns();
+  const int es = elem_bytes(pl.act);
+  const int cb = pl.swz / es;
+  const int wp = (int)(d->w + 2 * d->pad_w);
+  const CUtensorMapDataType tdt = pl.act == TEC_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                  : pl.act == TEC_DT_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                                        : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap tm_x, tm_w;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)pl.cp, (cuuint64_t)d->w, (cuuint64_t)d->h,
+                          (cuuint64_t)d->n};
+    cuuint64_t strides[3] = {(cuuint64_t)(pl.cp * es), (cuuint64_t)(pl.cp * es * d->w),
+                             (cuuint64_t)(pl.cp * es * d->w * d->h)};
+    cuuint32_t box[4] = {(cuuint32_t)cb, (cuuint32_t)wp, (cuuint32_t)(hc.th + d->r - 1), 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fns.tiled(&tm_x, tdt, 4, const_cast<void*>(x), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(pl.swz),
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(TEC_E_CUDA, "cuTensorMapEncodeTiled (halo) failed: " + std::to_string(r));
+  }
+  {
+    const int64_t ktot = d->r * d->s * pl.cp;
+    cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)d->k};
+    cuuint64_t strides[1] = {(cuuint64_t)(ktot * es)};
+    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)hc.inst->bn};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fns.tiled(&tm_w, tdt, 2, const_cast<void*>(w), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(pl.swz),
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(TEC_E_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string(r));
+  }
+  ConvHaloParams p{};
+  p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.cp = (int32_t)pl.cp;
+  p.oh = (int32_t)pl.oh; p.ow = (int32_t)pl.ow; p.oc = (int32_t)d->k;
+  p.r = (int32_t)d->r; p.s = (int32_t)d->s;
+  p.ph = (int32_t)d->pad_h; p.pw = (int32_t)d->pad_w;
+  p.th = hc.th; p.wp = wp; p.bands = hc.bands; p.n_tiles = hc.n_tiles;
+  p.cblocks = (int32_t)(pl.cp / cb);
+  p.halo_px = hc.halo_px;
+  p.out_type = out_dtype;
+  p.y = y;
+  p.err = err;
+  p.epi = epi;
+  // knob vec: 1 = per-thread epilogue rows, 2 = no epilogue (diagnostic only)
+  p.epi_mode = kn && (kn->vec == 1 || kn->vec == 2) ? (int32_t)kn->vec : 0;
+  int grid = std::min(hc.tiles, sms);
+  if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
+  static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
+  unsigned long long* dbg = nullptr;
+  if (prof) {
+    TEC_CUDA(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
+    TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
+    p.dbg = dbg;
+  }
+  const int e = hc.inst->fn(tm_x, tm_w, p, grid, st);
+  if (e) return cuda_fail(e, "conv_halo launch");
+  if (prof) {
+    unsigned long long h[8];
+    TEC_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TEC_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dbg);
+    const double ctas = (double)grid;
+    std::fprintf(stderr,
+                 "[tec-prof] halo bn=%d ms=%d th=%d wp=%d taps=%d cblocks=%d tiles/cta=%.2f "
+                 "cta_cycles=%.0f | prod_wait_empty=%.0f mma_wait_data=%.0f mma_wait_acc=%.0f "
+                 "epi_wait_acc=%.0f epi_busy=%.0f (per CTA)\n",
+                 hc.inst->bn, hc.inst->ms, hc.th, wp, (int)(d->r * d->s), p.cblocks,
+                 h[6] / ctas, h[5] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
+                 h[4] / ctas);
+  }
+  return TEC_OK;
 }
 
 tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
@@ -286,6 +462,15 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = sm_count(dev);
+  // Path: knob tile_k selects the A-operand strategy -- 0 auto, 1 im2col
+  // TMA (conv_tc.cu), 2 shifted-window halo (conv_halo.cu, stride 1 only).
+  const int64_t path = kn ? kn->tile_k : 0;
+  if (path != 1) {
+    HaloChoice hc;
+    if (plan_halo(d, pl, kn, sms, &hc))
+      return run_conv_halo(d, pl, hc, epi, kn, x, w, y, out_dtype, err, st, sms);
+    if (path == 2) return fail(TEC_E_LOWERING, "no halo configuration for this conv");
+  }
   const int64_t m_tiles = (pl.m + 127) / 128;
 
   // tile_n knob: the "split" of the OC axis.
@@ -361,11 +546,35 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   p.y = y;
   p.err = err;
   p.epi = epi;
+  // knob vec: 1 = per-thread epilogue rows, 2 = no epilogue (diagnostic only)
+  p.epi_mode = kn && (kn->vec == 1 || kn->vec == 2) ? (int32_t)kn->vec : 0;
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
   int grid = (int)std::min<int64_t>(tiles, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
+  // TEC_SM100_PROFILE=1: per-role pipeline wait breakdown on stderr
+  // (synchronises the stream; diagnostics only).
+  static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
+  unsigned long long* dbg = nullptr;
+  if (prof) {
+    TEC_CUDA(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
+    TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
+    p.dbg = dbg;
+  }
   const int e = launch(tm_a, tm_b, p, grid, st);
   if (e) return cuda_fail(e, "conv_fprop_tc launch");
+  if (prof) {
+    unsigned long long h[8];
+    TEC_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TEC_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dbg);
+    const double ctas = (double)grid;
+    std::fprintf(stderr,
+                 "[tec-prof] im2col bn=%d k_iters=%d tiles/cta=%.2f cta_cycles=%.0f | "
+                 "prod_wait_empty=%.0f mma_wait_full=%.0f mma_wait_acc=%.0f "
+                 "epi_wait_acc=%.0f epi_busy=%.0f (per CTA)\n",
+                 bn, (int)(d->r * d->s * p.cblocks), h[6] / ctas, h[5] / ctas, h[0] / ctas,
+                 h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas);
+  }
   return TEC_OK;
 }
 
@@ -431,6 +640,10 @@ tec_status tec_conv_layout_of(const tec_conv_desc* d, tec_conv_layout* out) {
   const int es = elem_bytes(pl.act);
   out->act_bytes = d->n * d->h * d->w * pl.cp * es;
   out->wt_bytes = d->depthwise ? d->c * d->r * d->s * es : d->k * d->r * d->s * pl.cp * es;
+  if (pl.s2d) {
+    out->act_bytes = d->n * pl.h2 * pl.w2 * pl.cp * es;
+    out->wt_bytes = d->k * pl.r2 * pl.s2 * pl.cp * es;
+  }
   out->out_elems = d->n * d->k * pl.oh * pl.ow;
   return TEC_OK;
 }
@@ -440,6 +653,13 @@ tec_status tec_activation_pack(const tec_conv_desc* d, const void* x_nchw,
   Plan pl{};
   tec_status st = make_plan(d, &pl);
   if (st) return st;
+  if (pl.s2d) {
+    const int e = launch_pack_s2d(x_nchw, d->compute == TEC_COMPUTE_I8 ? kI8 : kF32, x_packed,
+                                  d->n, d->c, d->h, d->w, d->pad_h, d->pad_w, pl.h2, pl.w2,
+                                  pl.cp, pl.pack_mode, (cudaStream_t)stream);
+    if (e) return cuda_fail(e, "pack_s2d");
+    return TEC_OK;
+  }
   if (pl.pack_mode < 0) {  // F32 exact path reads the NCHW tensor as is
     TEC_CUDA(cudaMemcpyAsync(x_packed, x_nchw, d->n * d->c * d->h * d->w * 4,
                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -457,6 +677,13 @@ tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
   Plan pl{};
   tec_status st = make_plan(d, &pl);
   if (st) return st;
+  if (pl.s2d) {
+    const int e = launch_pack_weights_s2d(w_oihw, d->compute == TEC_COMPUTE_I8 ? kI8 : kF32,
+                                          w_packed, d->k, d->c, d->r, d->s, pl.r2, pl.s2, pl.cp,
+                                          pl.pack_mode, (cudaStream_t)stream);
+    if (e) return cuda_fail(e, "pack_weights_s2d");
+    return TEC_OK;
+  }
   if (pl.pack_mode < 0) {  // OIHW == [oc][(ic, rh, rw)]: the reduce order
     TEC_CUDA(cudaMemcpyAsync(w_packed, w_oihw, d->k * d->c * d->r * d->s * 4,
                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -526,6 +753,18 @@ tec_status tec_conv2d_fused(const tec_conv_desc* d, const tec_epilogue* epi,
                                         (cudaStream_t)stream);
     if (e) return cuda_fail(e, "conv_f32_exact launch");
     return TEC_OK;
+  }
+  if (pl.s2d) {
+    // The folded stem: a stride-1, unpadded (r2 x s2) conv over the
+    // space-to-depth input; same output grid (checked in make_plan).
+    tec_conv_desc d2 = *d;
+    d2.c = pl.cp; d2.h = pl.h2; d2.w = pl.w2; d2.r = pl.r2; d2.s = pl.s2;
+    d2.stride_h = d2.stride_w = 1;
+    d2.pad_h = d2.pad_w = 0;
+    Plan pl2 = pl;
+    pl2.s2d = false;
+    return run_conv(&d2, pl2, ep, knobs, x_packed, w_packed, y, out_dtype, err_flag,
+                    (cudaStream_t)stream);
   }
   return run_conv(d, pl, ep, knobs, x_packed, w_packed, y, out_dtype, err_flag,
                   (cudaStream_t)stream);
