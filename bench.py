@@ -158,58 +158,48 @@ def impl_reference(args):
 
 # ------------------------------------------------------------ clocks sampler
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and throttle reasons through NVML every ~5 ms while
+    the timed region runs (nvidia-smi's 100 ms loop is longer than a step)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+                time.sleep(0.001)
+        except Exception as e:  # pragma: no cover
+            self.error = repr(e)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        time.sleep(0.05)
         return self
 
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "error": getattr(self, "error", None)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 # ------------------------------------------------------------ our arm
@@ -229,8 +219,21 @@ def impl_ours(args):
     peak_tf, hbm_gbs, peak_tf_sus, peak_src = load_peaks()
     batch = args.batch
 
+    # "with tuned schedule knobs" (configs[1]): the on-device tuner measures
+    # the knob grid of every layer (untimed) and the step uses the best.
+    from paper_1802_04799_b200.device import make_desc
+    from paper_1802_04799_b200.tuner import conv_space, tune
+    tuned = {}
+    for n in LAYERS:
+        if args.no_tune:
+            tuned[n] = {}
+            continue
+        space = conv_space(f"{n}_b{batch}_bf16", make_desc(resnet_layer(n, batch), "bf16"))
+        best = tune(space, budget=space.size(), batch_size=space.size(), method="random",
+                    devices=[local], repeats=5)
+        tuned[n] = best.config if best else {}
     layers = [DeviceConv(resnet_layer(n, batch), compute="bf16", device=local,
-                         seed=1000 * rank + i) for i, n in enumerate(LAYERS)]
+                         seed=1000 * rank + i, knobs=tuned[n]) for i, n in enumerate(LAYERS)]
     flops = [l.wl.flops for l in layers]
     step_flops = sum(flops)
     stream = torch.cuda.Stream()
@@ -299,7 +302,8 @@ def impl_ours(args):
         bound_tf = min(peak_tf, ai * hbm_gbs / 1e3)
         achieved = fl / (us * 1e-6) / 1e12
         per_layer.append({
-            "layer": l.wl.name, "us": round(us, 2), "tflops": round(achieved, 1),
+            "layer": l.wl.name, "knobs": tuned[l.wl.name],
+            "us": round(us, 2), "tflops": round(achieved, 1),
             "gflop": round(fl / 1e9, 3), "mbytes": round(byts / 1e6, 2),
             "ai_flop_per_byte": round(ai, 1),
             "bound": "tensor" if bound_tf >= peak_tf else "hbm",
@@ -417,6 +421,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tune", action="store_true", help="library default knobs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

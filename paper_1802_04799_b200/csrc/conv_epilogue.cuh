@@ -26,6 +26,26 @@ namespace epi {
 
 constexpr int kChunk = 32;  // epilogue columns per tcgen05.ld
 
+// The fused-member program, decoded ONCE per thread into registers (op
+// codes packed 4 bits each; scale factors as f32 and i64), so the per-block
+// loops never index kernel-parameter space dynamically.
+// (Scale factors stay in parameter space: the member loops are fully
+// unrolled, so e.fscale[i] / e.iscale[i] are static-offset constant loads.)
+struct EpiProg {
+  uint32_t ops = 0;
+  int n = 0;
+  __device__ __forceinline__ int op(int i) const { return (ops >> (4 * i)) & 15; }
+};
+
+__device__ __forceinline__ EpiProg make_prog(const EpilogueParams& e) {
+  EpiProg g;
+#pragma unroll
+  for (int i = 0; i < kMaxEpi; ++i)
+    g.ops |= static_cast<uint32_t>(i < e.n_ops ? e.ops[i] : 0) << (4 * i);
+  g.n = e.n_ops;
+  return g;
+}
+
 // 32 elements as raw 32-bit words: bf16 pairs packed (16 words) or f32/i32.
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
@@ -36,6 +56,96 @@ __device__ __forceinline__ float word_elem_f(const uint32_t (&w)[kChunk], bool b
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Explicit shared-space accesses (the stage pointers are carved out of the
+// dynamic smem block; generic addressing would cost an extra conversion).
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+// 32 bias words from shared memory (broadcast reads).
+__device__ __forceinline__ void load_bias32(const uint32_t* bias_s, uint32_t (&b)[kChunk]) {
+  const uint32_t a = smem_u32(bias_s);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 v = lds128(a + 16 * i);
+    b[4 * i] = v.x; b[4 * i + 1] = v.y; b[4 * i + 2] = v.z; b[4 * i + 3] = v.w;
+  }
+}
+
+// Float member chain on 32 values (v) of one row. opnd_fn(op) must leave
+// the same-shape operand of `op` (add / mul) in `opnd`.
+template <typename OpndFn>
+__device__ __forceinline__ void apply_float(const EpiProg& g, const EpilogueParams& e,
+                                            float (&v)[kChunk],
+                                            const uint32_t* bias_s, bool bf,
+                                            uint32_t (&opnd)[kChunk], OpndFn opnd_fn) {
+#pragma unroll 1
+  for (int i = 0; i < g.n; ++i) {
+    const int op = g.op(i);
+    if (op == kEpiScale) {
+      const float s = e.fscale[i];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
+    } else if (op == kEpiBias) {
+      uint32_t b[kChunk];
+      load_bias32(bias_s, b);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], __uint_as_float(b[j]));
+    } else if (op == kEpiAdd) {
+      opnd_fn(kEpiAdd);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], word_elem_f(opnd, bf, j));
+    } else if (op == kEpiMul) {
+      opnd_fn(kEpiMul);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], word_elem_f(opnd, bf, j));
+    } else if (op == kEpiRelu) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
+    }
+  }
+}
+
+// Integer member chain: every member in int64, range-checked, stored back as
+// i32 (after an overflow the kernel reports FoldOverflow -- the reference
+// throws -- so the wrapped value is never consumed).
+template <typename OpndFn>
+__device__ __forceinline__ bool apply_int(const EpiProg& g, const EpilogueParams& e,
+                                          uint32_t (&acc)[kChunk],
+                                          const uint32_t* bias_s, int ncols, bool live,
+                                          uint32_t (&opnd)[kChunk], OpndFn opnd_fn) {
+  bool ovf = false;
+#pragma unroll 1
+  for (int i = 0; i < g.n; ++i) {
+    const int op = g.op(i);
+    if (op == kEpiAdd || op == kEpiMul) opnd_fn(op);
+    uint32_t b[kChunk];
+    if (op == kEpiBias) load_bias32(bias_s, b);
+    const int64_t s = op == kEpiScale ? e.iscale[i] : 1;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      int64_t t = static_cast<int32_t>(acc[j]);
+      if (op == kEpiScale) t *= s;
+      else if (op == kEpiBias) t += static_cast<int32_t>(b[j]);
+      else if (op == kEpiAdd) t += static_cast<int32_t>(opnd[j]);
+      else if (op == kEpiMul) t *= static_cast<int32_t>(opnd[j]);
+      else if (op == kEpiRelu) t = t < 0 ? 0 : t;
+      ovf |= live && (j < ncols) && (t < INT32_MIN || t > INT32_MAX);
+      acc[j] = static_cast<uint32_t>(static_cast<int32_t>(t));
+    }
+  }
+  return ovf;
 }
 
 // ------------------------------------------------- per-thread fallback
@@ -56,164 +166,123 @@ __device__ __forceinline__ void fetch_row32(const void* base, int64_t off, int e
   }
 }
 
-template <typename P>
-__device__ __forceinline__ void epi_chunk_float(const P& p, int64_t row, int col0, int ncols,
-                                                bool active, const float* bias_s,
-                                                uint32_t (&acc)[kChunk]) {
+// One row, 32 columns (any channel count). Waits on the pending TMEM load.
+template <bool kInt, typename P>
+__device__ __forceinline__ void epi_row_chunk(const P& p, const EpiProg& g, int64_t row,
+                                              int col0, int ncols, bool active,
+                                              const uint32_t* bias_s, uint32_t (&acc)[kChunk],
+                                              bool* overflow) {
+  tmem_ld_wait();
+  if (!active) return;
   const EpilogueParams& e = p.epi;
   const int64_t base = row * p.oc + col0;
-  const bool bf = p.out_type == kBF16;
+  const bool bf = !kInt && p.out_type == kBF16;
   const int es = bf ? 2 : 4;
   uint32_t opnd[kChunk];
-  tmem_ld_wait();
-  if (!active) return;
-  float v[kChunk];
-#pragma unroll
-  for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
-#pragma unroll 1
-  for (int i = 0; i < e.n_ops; ++i) {
-    const int op = e.ops[i];
-    if (op == kEpiScale) {
-      const float s = e.fscale[i];
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
-    } else if (op == kEpiBias) {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], bias_s[j]);
-    } else if (op == kEpiAdd) {
-      fetch_row32(e.residual, base, es, ncols, opnd);
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], word_elem_f(opnd, bf, j));
-    } else if (op == kEpiMul) {
-      fetch_row32(e.mul_operand, base, es, ncols, opnd);
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], word_elem_f(opnd, bf, j));
-    } else if (op == kEpiRelu) {
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
-    }
-  }
-  if (bf) {
-    __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + base;
+  auto opnd_fn = [&](int op) {
+    fetch_row32(op == kEpiAdd ? e.residual : e.mul_operand, base, es, ncols, opnd);
+  };
+  if constexpr (kInt) {
+    if (apply_int(g, e, acc, bias_s, ncols, true, opnd, opnd_fn)) *overflow = true;
+    int32_t* yp = static_cast<int32_t*>(p.y) + base;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j)
-      if (j < ncols) yp[j] = __float2bfloat16_rn(v[j]);
+      if (j < ncols) yp[j] = static_cast<int32_t>(acc[j]);
   } else {
-    float* yp = static_cast<float*>(p.y) + base;
+    float v[kChunk];
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j)
-      if (j < ncols) yp[j] = v[j];
-  }
-}
-
-template <typename P>
-__device__ __forceinline__ void epi_chunk_int(const P& p, int64_t row, int col0, int ncols,
-                                              bool active, const int32_t* bias_s,
-                                              uint32_t (&acc)[kChunk], bool* overflow) {
-  const EpilogueParams& e = p.epi;
-  const int64_t base = row * p.oc + col0;
-  uint32_t opnd[kChunk];
-  tmem_ld_wait();
-  if (!active) return;
-  bool ovf = false;
-#pragma unroll 1
-  for (int i = 0; i < e.n_ops; ++i) {
-    const int op = e.ops[i];
-    if (op == kEpiAdd) fetch_row32(e.residual, base, 4, ncols, opnd);
-    if (op == kEpiMul) fetch_row32(e.mul_operand, base, 4, ncols, opnd);
-    const int64_t s = e.iscale[i];
+    for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
+    apply_float(g, e, v, bias_s, bf, opnd, opnd_fn);
+    if (bf) {
+      __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(p.y) + base;
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) {
-      int64_t t = static_cast<int32_t>(acc[j]);
-      if (op == kEpiScale) t *= s;
-      else if (op == kEpiBias) t += bias_s[j];
-      else if (op == kEpiAdd) t += static_cast<int32_t>(opnd[j]);
-      else if (op == kEpiMul) t *= static_cast<int32_t>(opnd[j]);
-      else if (op == kEpiRelu) t = t < 0 ? 0 : t;
-      ovf |= (j < ncols) && (t < INT32_MIN || t > INT32_MAX);
-      acc[j] = static_cast<uint32_t>(static_cast<int32_t>(t));
+      for (int j = 0; j < kChunk; ++j)
+        if (j < ncols) yp[j] = __float2bfloat16_rn(v[j]);
+    } else {
+      float* yp = static_cast<float*>(p.y) + base;
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j)
+        if (j < ncols) yp[j] = v[j];
     }
   }
-  int32_t* yp = static_cast<int32_t*>(p.y) + base;
-#pragma unroll
-  for (int j = 0; j < kChunk; ++j)
-    if (j < ncols) yp[j] = static_cast<int32_t>(acc[j]);
-  if (ovf) *overflow = true;
 }
 
 // ------------------------------------------- warp-cooperative, coalesced
 // Stage layout: row r of the 32 x (32 * es) block at r * rowbytes, 16-byte
 // chunks XOR-swizzled by their 128-byte line index (conflict-free for both
-// the row-per-thread writes and the line-per-8-lanes reads).
+// the row-per-thread writes and the line-per-lanes reads). Rows are given
+// per lane (my_row = global output row of this lane, -1 = junk/padding)
+// and exchanged with shuffles.
 __device__ __forceinline__ uint32_t stage_off(int row, int chunk, int rowbytes) {
   const uint32_t lin = static_cast<uint32_t>(row * rowbytes + chunk * 16);
   return lin ^ (((lin >> 7) & 7u) << 4);
 }
 
-// Coalesced read of a same-shape operand block into each thread's row words.
-template <typename RowFn>
 __device__ __forceinline__ void coalesced_load_block(const void* src, int es, int64_t oc,
-                                                     int col0, int ncols, int lane,
-                                                     RowFn row_of, uint8_t* stage,
-                                                     uint32_t (&w)[kChunk]) {
+                                                     int col0, int ncols, int lane, int my_row,
+                                                     uint8_t* stage, uint32_t (&w)[kChunk]) {
   const int rowbytes = 32 * es, cpr = rowbytes / 16, rpi = 32 / cpr;
+  const uint32_t sbase = smem_u32(stage);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     if (i >= cpr) break;
     const int r = i * rpi + lane / cpr;
     const int c = lane % cpr;
-    const int64_t g = row_of(r);
+    const int g = __shfl_sync(0xffffffffu, my_row, r);
     uint4 v = make_uint4(0, 0, 0, 0);
     const int cc = c * (16 / es);
     if (g >= 0 && cc < ncols)
       v = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(src) +
-                                               (g * oc + col0 + cc) * es));
-    *reinterpret_cast<uint4*>(stage + stage_off(r, c, rowbytes)) = v;
+                                               (static_cast<int64_t>(g) * oc + col0 + cc) * es));
+    sts128(sbase + stage_off(r, c, rowbytes), v);
   }
   __syncwarp();
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     if (c < cpr) {
-      const uint4 v = *reinterpret_cast<const uint4*>(stage + stage_off(lane, c, rowbytes));
+      const uint4 v = lds128(sbase + stage_off(lane, c, rowbytes));
       w[4 * c] = v.x; w[4 * c + 1] = v.y; w[4 * c + 2] = v.z; w[4 * c + 3] = v.w;
     }
   }
   __syncwarp();
 }
 
-template <typename RowFn>
 __device__ __forceinline__ void coalesced_store_block(void* dst, int es, int64_t oc, int col0,
-                                                      int ncols, int lane, RowFn row_of,
+                                                      int ncols, int lane, int my_row,
                                                       uint8_t* stage, const uint32_t (&w)[kChunk]) {
   const int rowbytes = 32 * es, cpr = rowbytes / 16, rpi = 32 / cpr;
+  const uint32_t sbase = smem_u32(stage);
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     if (c < cpr)
-      *reinterpret_cast<uint4*>(stage + stage_off(lane, c, rowbytes)) =
-          make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+      sts128(sbase + stage_off(lane, c, rowbytes),
+             make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]));
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     if (i >= cpr) break;
     const int r = i * rpi + lane / cpr;
     const int c = lane % cpr;
-    const int64_t g = row_of(r);
+    const int g = __shfl_sync(0xffffffffu, my_row, r);
     const int cc = c * (16 / es);
+    const uint4 v = lds128(sbase + stage_off(r, c, rowbytes));
     if (g >= 0 && cc < ncols)
-      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(dst) + (g * oc + col0 + cc) * es) =
-          *reinterpret_cast<const uint4*>(stage + stage_off(r, c, rowbytes));
+      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(dst) +
+                                (static_cast<int64_t>(g) * oc + col0 + cc) * es) = v;
   }
   __syncwarp();
 }
 
 // One 32-column block of one warp. taddr: TMEM address of this warp's lane
 // quadrant at the block's first accumulator column; col0: global column;
-// bias_s: the block's 32 bias values in shared memory. Requires
-// oc % (16 / out_bytes) == 0 (whole 16-byte chunks per row).
-template <bool kInt, typename P, typename RowFn>
-__device__ __forceinline__ void epi_warp_block(const P& p, uint32_t taddr, int col0, int lane,
-                                               RowFn row_of, const uint32_t* bias_s,
-                                               uint8_t* stage, bool* overflow) {
+// bias_s: the block's 32 bias values (raw f32/i32 bits) in shared memory.
+// Requires oc % (16 / out_bytes) == 0 (whole 16-byte chunks per row).
+template <bool kInt, typename P>
+__device__ __forceinline__ void epi_warp_block(const P& p, const EpiProg& g, uint32_t taddr,
+                                               int col0, int lane, int my_row,
+                                               const uint32_t* bias_s, uint8_t* stage,
+                                               bool* overflow, long long* prof = nullptr) {
+  const long long t0 = prof ? clock64() : 0;
   const EpilogueParams& e = p.epi;
   const bool bf = !kInt && p.out_type == kBF16;
   const int es = bf ? 2 : 4;
@@ -221,81 +290,35 @@ __device__ __forceinline__ void epi_warp_block(const P& p, uint32_t taddr, int c
   // One operand buffer: the first same-shape operand in member order is
   // fetched before waiting on TMEM; any later one is fetched on demand.
   uint32_t opnd[kChunk];
-  int have = 0;  // EpiOp currently held in opnd
-  const int first_op = e.residual || e.mul_operand
-                           ? (e.residual && (!e.mul_operand) ? kEpiAdd
-                              : (!e.residual)                ? kEpiMul
-                                                             : -1)
-                           : 0;
-  if (first_op > 0) {
-    coalesced_load_block(first_op == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0,
-                         ncols, lane, row_of, stage, opnd);
-    have = first_op;
+  int have = 0;
+  const int first =
+      e.residual && !e.mul_operand ? kEpiAdd : (!e.residual && e.mul_operand ? kEpiMul : 0);
+  uint32_t acc[kChunk];
+  tmem_ld32(taddr, acc);
+  if (first) {
+    coalesced_load_block(first == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0, ncols,
+                         lane, my_row, stage, opnd);
+    have = first;
   }
-  auto need = [&](int op) {
+  auto opnd_fn = [&](int op) {
     if (have != op) {
       coalesced_load_block(op == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0, ncols,
-                           lane, row_of, stage, opnd);
+                           lane, my_row, stage, opnd);
       have = op;
     }
   };
-  uint32_t acc[kChunk];
-  tmem_ld32(taddr, acc);
   tmem_ld_wait();
+  const long long t1 = prof ? clock64() : 0;
   uint32_t out[kChunk];
   if constexpr (kInt) {
-    // Each member is evaluated in int64 and range-checked before it is
-    // stored back as i32; after an overflow the kernel reports FoldOverflow
-    // (the reference throws), so the wrapped value is never consumed.
-    const bool live = row_of(lane) >= 0;
-    bool ovf = false;
-#pragma unroll 1
-    for (int i = 0; i < e.n_ops; ++i) {
-      const int op = e.ops[i];
-      if (op == kEpiAdd || op == kEpiMul) need(op);
-      const int64_t s = e.iscale[i];
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        int64_t t = static_cast<int32_t>(acc[j]);
-        if (op == kEpiScale) t *= s;
-        else if (op == kEpiBias) t += static_cast<int32_t>(bias_s[j]);
-        else if (op == kEpiAdd) t += static_cast<int32_t>(opnd[j]);
-        else if (op == kEpiMul) t *= static_cast<int32_t>(opnd[j]);
-        else if (op == kEpiRelu) t = t < 0 ? 0 : t;
-        ovf |= live && (j < ncols) && (t < INT32_MIN || t > INT32_MAX);
-        acc[j] = static_cast<uint32_t>(static_cast<int32_t>(t));
-      }
-    }
+    if (apply_int(g, e, acc, bias_s, ncols, my_row >= 0, opnd, opnd_fn)) *overflow = true;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) out[j] = acc[j];
-    if (ovf) *overflow = true;
   } else {
     float v[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) v[j] = __uint_as_float(acc[j]);
-#pragma unroll 1
-    for (int i = 0; i < e.n_ops; ++i) {
-      const int op = e.ops[i];
-      if (op == kEpiScale) {
-        const float s = e.fscale[i];
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], s);
-      } else if (op == kEpiBias) {
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], __uint_as_float(bias_s[j]));
-      } else if (op == kEpiAdd) {
-        need(kEpiAdd);
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] = __fadd_rn(v[j], word_elem_f(opnd, bf, j));
-      } else if (op == kEpiMul) {
-        need(kEpiMul);
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] = __fmul_rn(v[j], word_elem_f(opnd, bf, j));
-      } else if (op == kEpiRelu) {
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) v[j] = (v[j] < 0.0f) ? 0.0f : v[j];  // std::max(x, 0)
-      }
-    }
+    apply_float(g, e, v, bias_s, bf, opnd, opnd_fn);
     if (bf) {
 #pragma unroll
       for (int j = 0; j < kChunk / 2; ++j) out[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
@@ -306,7 +329,13 @@ __device__ __forceinline__ void epi_warp_block(const P& p, uint32_t taddr, int c
       for (int j = 0; j < kChunk; ++j) out[j] = __float_as_uint(v[j]);
     }
   }
-  coalesced_store_block(p.y, es, p.oc, col0, ncols, lane, row_of, stage, out);
+  const long long t2 = prof ? clock64() : 0;
+  coalesced_store_block(p.y, es, p.oc, col0, ncols, lane, my_row, stage, out);
+  if (prof) {
+    prof[0] += t1 - t0;          // operand prefetch + TMEM load
+    prof[1] += t2 - t1;          // member ops
+    prof[2] += clock64() - t2;   // transpose + global stores
+  }
 }
 
 // Cooperative per-tile bias staging: `nthreads` epilogue threads copy the

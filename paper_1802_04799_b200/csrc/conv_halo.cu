@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = threadIdx.x & 31;
   const int taps = p.r * p.s;
   const int num_tiles = p.n * p.bands * p.n_tiles;
-  long long dbg_wait[5] = {0, 0, 0, 0, 0};
+  long long dbg_wait[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_start = p.dbg ? clock64() : 0;
   constexpr int kCB =
       SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool coalesced =
         p.epi_mode == 0 &&
         ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
+    const epi::EpiProg prog = epi::make_prog(p.epi);
     int local = 0;
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -228,15 +229,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int vbase = ms * 128 + static_cast<int>(q * 32);
         // Virtual row -> output row (or -1 for the junk columns ow >= OW
         // and rows past the band).
-        auto row_of = [&](int r) -> int64_t {
-          const int v = vbase + r;
+        int my_row = -1;  // this lane's output row, -1 for junk virtual rows
+        {
+          const int v = vbase + static_cast<int>(lane);
           const int ohl = v / p.wp;
           const int ow = v - ohl * p.wp;
           const int oh = band * p.th + ohl;
-          if (ohl >= p.th || oh >= p.oh || ow >= p.ow) return -1;
-          return (static_cast<int64_t>(img) * p.oh + oh) * p.ow + ow;
-        };
-        const int64_t row = row_of(static_cast<int>(lane));
+          if (ohl < p.th && oh < p.oh && ow < p.ow) my_row = (img * p.oh + oh) * p.ow + ow;
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < BN && p.epi_mode != 2; c0 += epi::kChunk) {  // 2: diagnostic
           const uint32_t taddr =
@@ -244,19 +244,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int col0 = n_tile * BN + c0;
           if (coalesced) {
             if (col0 < p.oc)
-              epi::epi_warp_block<KIND == MmaKind::kI8>(p, taddr, col0, lane, row_of,
-                                                        bias_s + c0, stage, &overflow);
+              epi::epi_warp_block<KIND == MmaKind::kI8>(p, prog, taddr, col0, lane, my_row,
+                                                        bias_s + c0, stage, &overflow,
+                                                        p.dbg ? &dbg_wait[5] : nullptr);
           } else {
             uint32_t vv[epi::kChunk];
             tmem_ld32(taddr, vv);
-            const bool active = row >= 0 && col0 < p.oc;
+            const bool active = my_row >= 0 && col0 < p.oc;
             const int ncols = min(epi::kChunk, p.oc - col0);
-            if constexpr (KIND == MmaKind::kI8)
-              epi::epi_chunk_int(p, row, col0, ncols, active,
-                                 reinterpret_cast<const int32_t*>(bias_s + c0), vv, &overflow);
-            else
-              epi::epi_chunk_float(p, row, col0, ncols, active,
-                                   reinterpret_cast<const float*>(bias_s + c0), vv);
+            epi::epi_row_chunk<KIND == MmaKind::kI8>(p, prog, my_row, col0, ncols, active,
+                                                     bias_s + c0, vv, &overflow);
           }
         }
       }
@@ -274,8 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.dbg) {
     const bool rep = (warp <= 1 && lane == 0) || threadIdx.x == kThreads - kEpiThreads;
     if (rep)
-      for (int i = 0; i < 5; ++i)
-        if (dbg_wait[i]) atomicAdd(&p.dbg[i], static_cast<unsigned long long>(dbg_wait[i]));
+      for (int i = 0; i < 8; ++i)
+        if (dbg_wait[i])
+          atomicAdd(&p.dbg[i < 5 ? i : i + 3], static_cast<unsigned long long>(dbg_wait[i]));
     if (threadIdx.x == 0) {
       atomicAdd(&p.dbg[5], static_cast<unsigned long long>(clock64() - t_start));
       atomicAdd(&p.dbg[6], static_cast<unsigned long long>((num_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x));

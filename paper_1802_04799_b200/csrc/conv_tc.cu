@@ -43,8 +43,6 @@ constexpr int kBM = 128;
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiThreads = 256;
 using epi::kChunk;
-using epi::epi_chunk_float;
-using epi::epi_chunk_int;
 
 template <MmaKind KIND, int BN, int STAGES, int SWZ>
 struct ConvCfg {
@@ -200,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool coalesced =
         p.epi_mode == 0 &&
         ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
+    const epi::EpiProg prog = epi::make_prog(p.epi);
     int local = 0;
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles;
@@ -222,29 +221,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
-      auto row_of = [&](int r) -> int64_t {
-        const int g = row0 + r;
-        return g < p.m ? static_cast<int64_t>(g) : int64_t(-1);
-      };
+      const int my_row = row_ok ? row : -1;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN && p.epi_mode != 2; c0 += kChunk) {  // 2: no epilogue (diagnostic)
         const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN + c0;
         const int col0 = n_tile * BN + c0;
         if (coalesced) {
           if (col0 < p.oc)
-            epi::epi_warp_block<KIND == MmaKind::kI8>(p, taddr, col0, lane, row_of,
+            epi::epi_warp_block<KIND == MmaKind::kI8>(p, prog, taddr, col0, lane, my_row,
                                                       bias_s + c0, stage, &overflow);
         } else {
           uint32_t v[kChunk];
           tmem_ld32(taddr, v);
           const bool active = row_ok && col0 < p.oc;
           const int ncols = min(kChunk, p.oc - col0);
-          if constexpr (KIND == MmaKind::kI8)
-            epi_chunk_int(p, row, col0, ncols, active,
-                          reinterpret_cast<const int32_t*>(bias_s + c0), v, &overflow);
-          else
-            epi_chunk_float(p, row, col0, ncols, active,
-                            reinterpret_cast<const float*>(bias_s + c0), v);
+          epi::epi_row_chunk<KIND == MmaKind::kI8>(p, prog, row, col0, ncols, active,
+                                                   bias_s + c0, v, &overflow);
         }
       }
       // All of this thread's TMEM reads of the accumulator are complete

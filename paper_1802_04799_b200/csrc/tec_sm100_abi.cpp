@@ -422,14 +422,14 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
   unsigned long long* dbg = nullptr;
   if (prof) {
-    TEC_CUDA(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
-    TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
+    TEC_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    TEC_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
   const int e = hc.inst->fn(tm_x, tm_w, p, grid, st);
   if (e) return cuda_fail(e, "conv_halo launch");
   if (prof) {
-    unsigned long long h[8];
+    unsigned long long h[16];
     TEC_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
     TEC_CUDA(cudaStreamSynchronize(st));
     cudaFree(dbg);
@@ -437,10 +437,11 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     std::fprintf(stderr,
                  "[tec-prof] halo bn=%d ms=%d th=%d wp=%d taps=%d cblocks=%d tiles/cta=%.2f "
                  "cta_cycles=%.0f | prod_wait_empty=%.0f mma_wait_data=%.0f mma_wait_acc=%.0f "
-                 "epi_wait_acc=%.0f epi_busy=%.0f (per CTA)\n",
+                 "epi_wait_acc=%.0f epi_busy=%.0f | blk_tmem=%.0f blk_ops=%.0f blk_store=%.0f "
+                 "(per CTA)\n",
                  hc.inst->bn, hc.inst->ms, hc.th, wp, (int)(d->r * d->s), p.cblocks,
                  h[6] / ctas, h[5] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
-                 h[4] / ctas);
+                 h[4] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas);
   }
   return TEC_OK;
 }

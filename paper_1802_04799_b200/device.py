@@ -24,6 +24,12 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
     return s.cuda_stream
 
 
+def make_desc(wl: ConvWorkload, compute: str = "bf16") -> _abi.ConvDesc:
+    return _abi.ConvDesc(n=wl.n, c=wl.c, h=wl.h, w=wl.w, k=wl.k, r=wl.r, s=wl.s,
+                         stride_h=wl.stride, stride_w=wl.stride, pad_h=wl.pad, pad_w=wl.pad,
+                         depthwise=1 if wl.depthwise else 0, compute=_COMPUTE[compute])
+
+
 class DeviceConv:
     """One fused [conv, bias_add, (add), relu] node, resident on a device."""
 
