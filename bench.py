@@ -224,7 +224,12 @@ def impl_ours(args):
     from paper_1802_04799_b200.device import make_desc
     from paper_1802_04799_b200.tuner import conv_space, tune
     tuned = {}
+    if args.knobs_in:
+        with open(args.knobs_in) as f:
+            tuned = json.load(f)
     for n in LAYERS:
+        if n in tuned:
+            continue
         if args.no_tune:
             tuned[n] = {}
             continue
@@ -232,6 +237,9 @@ def impl_ours(args):
         best = tune(space, budget=space.size(), batch_size=space.size(), method="random",
                     devices=[local], repeats=5)
         tuned[n] = best.config if best else {}
+    if args.knobs_out and rank == 0:
+        with open(args.knobs_out, "w") as f:
+            json.dump(tuned, f)
     layers = [DeviceConv(resnet_layer(n, batch), compute="bf16", device=local,
                          seed=1000 * rank + i, knobs=tuned[n]) for i, n in enumerate(LAYERS)]
     flops = [l.wl.flops for l in layers]
@@ -422,6 +430,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tune", action="store_true", help="library default knobs")
+    ap.add_argument("--knobs-in", default="", help="JSON {layer: knobs} to use instead of tuning")
+    ap.add_argument("--knobs-out", default="", help="write the tuned knobs here")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
