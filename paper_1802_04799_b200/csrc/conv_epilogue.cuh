@@ -338,6 +338,120 @@ __device__ __forceinline__ void epi_warp_block(const P& p, const EpiProg& g, uin
   }
 }
 
+// ------------------------------------------- specialised fast path
+// The member programs fuse_pass produces for the benchmark networks, fixed
+// at compile time so a block is ~100 instructions: no op decoding, no
+// partial-block predicates (full 32-column block, oc % 8 == 0).
+enum FastProg : int { kProgGeneric = 0, kProgNone = 1, kProgBias = 2, kProgBiasRelu = 3,
+                      kProgBiasAddRelu = 4 };
+
+__device__ __forceinline__ int classify_prog(const EpilogueParams& e) {
+  if (e.n_ops == 0) return kProgNone;
+  if (e.n_ops == 1 && e.ops[0] == kEpiBias) return kProgBias;
+  if (e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu) return kProgBiasRelu;
+  if (e.n_ops == 3 && e.ops[0] == kEpiBias && e.ops[1] == kEpiAdd && e.ops[2] == kEpiRelu)
+    return kProgBiasAddRelu;
+  return kProgGeneric;
+}
+
+// Fast float block. es = 2 (bf16) or 4 (f32) output bytes; `oc_es` = row
+// pitch in bytes; `ybase` = output base + col0 * es.
+template <int PROG, int ES>
+__device__ __forceinline__ void epi_block_fast(uint8_t* ybase, const uint8_t* rbase,
+                                               int64_t oc_es, uint32_t taddr, int lane,
+                                               int my_row, const uint32_t* bias_s,
+                                               uint32_t sbase) {
+  constexpr int kRowBytes = 32 * ES, kCpr = kRowBytes / 16, kRpi = 32 / kCpr;
+  uint32_t acc[kChunk];
+  tmem_ld32(taddr, acc);
+  uint32_t res[kChunk];
+  if constexpr (PROG == kProgBiasAddRelu) {
+    // coalesced residual read through the stage (same transposition)
+#pragma unroll
+    for (int i = 0; i < kCpr; ++i) {
+      const int r = i * kRpi + lane / kCpr, c = lane % kCpr;
+      const int g = __shfl_sync(0xffffffffu, my_row, r);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (g >= 0) v = __ldg(reinterpret_cast<const uint4*>(rbase + g * oc_es + c * 16));
+      sts128(sbase + stage_off(r, c, kRowBytes), v);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < kCpr; ++c) {
+      const uint4 v = lds128(sbase + stage_off(lane, c, kRowBytes));
+      res[4 * c] = v.x; res[4 * c + 1] = v.y; res[4 * c + 2] = v.z; res[4 * c + 3] = v.w;
+    }
+    __syncwarp();
+  }
+  uint32_t b[kChunk];
+  if constexpr (PROG != kProgNone) load_bias32(bias_s, b);
+  tmem_ld_wait();
+  float v[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    float x = __uint_as_float(acc[j]);
+    if constexpr (PROG != kProgNone) x = __fadd_rn(x, __uint_as_float(b[j]));
+    if constexpr (PROG == kProgBiasAddRelu)
+      x = __fadd_rn(x, ES == 2 ? ((j & 1) ? bf16_hi(res[j >> 1]) : bf16_lo(res[j >> 1]))
+                               : __uint_as_float(res[j]));
+    if constexpr (PROG == kProgBiasRelu || PROG == kProgBiasAddRelu) x = (x < 0.0f) ? 0.0f : x;
+    v[j] = x;
+  }
+  uint32_t out[kChunk];
+  if constexpr (ES == 2) {
+#pragma unroll
+    for (int j = 0; j < kChunk / 2; ++j) out[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) out[j] = __float_as_uint(v[j]);
+  }
+#pragma unroll
+  for (int c = 0; c < kCpr; ++c)
+    sts128(sbase + stage_off(lane, c, kRowBytes),
+           make_uint4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]));
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kCpr; ++i) {
+    const int r = i * kRpi + lane / kCpr, c = lane % kCpr;
+    const int g = __shfl_sync(0xffffffffu, my_row, r);
+    const uint4 val = lds128(sbase + stage_off(r, c, kRowBytes));
+    if (g >= 0) *reinterpret_cast<uint4*>(ybase + g * oc_es + c * 16) = val;
+  }
+  __syncwarp();
+}
+
+// Dispatch one 32-column block: fast path when possible, generic otherwise.
+template <bool kInt, typename P>
+__device__ __forceinline__ void epi_block(const P& p, const EpiProg& g, int prog, uint32_t taddr,
+                                          int col0, int lane, int my_row,
+                                          const uint32_t* bias_s, uint8_t* stage,
+                                          bool* overflow) {
+  const bool full = col0 + kChunk <= p.oc;
+  if (!kInt && full && prog != kProgGeneric) {
+    const uint32_t sbase = smem_u32(stage);
+    const int es = p.out_type == kBF16 ? 2 : 4;
+    uint8_t* yb = static_cast<uint8_t*>(p.y) + static_cast<int64_t>(col0) * es;
+    const uint8_t* rb = static_cast<const uint8_t*>(p.epi.residual) + static_cast<int64_t>(col0) * es;
+    const int64_t oc_es = static_cast<int64_t>(p.oc) * es;
+    if (es == 2) {
+      switch (prog) {
+        case kProgNone: epi_block_fast<kProgNone, 2>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+        case kProgBias: epi_block_fast<kProgBias, 2>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+        case kProgBiasRelu: epi_block_fast<kProgBiasRelu, 2>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+        default: epi_block_fast<kProgBiasAddRelu, 2>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+      }
+    } else {
+      switch (prog) {
+        case kProgNone: epi_block_fast<kProgNone, 4>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+        case kProgBias: epi_block_fast<kProgBias, 4>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+        case kProgBiasRelu: epi_block_fast<kProgBiasRelu, 4>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+        default: epi_block_fast<kProgBiasAddRelu, 4>(yb, rb, oc_es, taddr, lane, my_row, bias_s, sbase); return;
+      }
+    }
+  }
+  epi_warp_block<kInt>(p, g, taddr, col0, lane, my_row, bias_s, stage, overflow);
+}
+
 // Cooperative per-tile bias staging: `nthreads` epilogue threads copy the
 // tile's BN bias values into shared memory (zero past OC).
 template <typename T>

@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.epi_mode == 0 &&
         ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
     const epi::EpiProg prog = epi::make_prog(p.epi);
+    const int fast = epi::classify_prog(p.epi);
     int local = 0;
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
@@ -244,9 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int col0 = n_tile * BN + c0;
           if (coalesced) {
             if (col0 < p.oc)
-              epi::epi_warp_block<KIND == MmaKind::kI8>(p, prog, taddr, col0, lane, my_row,
-                                                        bias_s + c0, stage, &overflow,
-                                                        p.dbg ? &dbg_wait[5] : nullptr);
+              epi::epi_block<KIND == MmaKind::kI8>(p, prog, fast, taddr, col0, lane, my_row,
+                                                   bias_s + c0, stage, &overflow);
           } else {
             uint32_t vv[epi::kChunk];
             tmem_ld32(taddr, vv);
