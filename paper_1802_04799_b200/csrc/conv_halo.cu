@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();  // see conv_tc.cu
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -293,7 +295,8 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
   auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kfn<<<grid, kThreads, smem, stream>>>(tm_x, tm_w, p);
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_x, tm_w, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

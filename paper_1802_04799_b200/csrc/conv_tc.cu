@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Prologue done: let the next layer launch, then wait for the previous
+  // layer's outputs (our inputs) to be complete and visible.
+  pdl_launch_dependents();
+  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer warp
@@ -280,7 +284,8 @@ int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
   cudaError_t e = cudaFuncSetAttribute(
       kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
-  kfn<<<grid, kThreads, Cfg::kSmemBytes, stream>>>(tm_a, tm_b, p);
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, tm_a, tm_b, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

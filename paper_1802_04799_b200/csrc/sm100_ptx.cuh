@@ -5,7 +5,9 @@
 // top of these; no CUTLASS/CuTe types are used.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda.h>
+#include <cuda_runtime.h>
 
 namespace tec_sm100 {
 
@@ -110,6 +112,17 @@ __device__ __forceinline__ void tma_load_im2col_4d(void* dst,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c), "r"(w),
       "r"(h), "r"(n), "h"(off_w), "h"(off_h)
       : "memory");
+}
+
+// ------------------------------------------- programmatic dependent launch
+// The next layer's kernel may be launched while this one drains; it runs
+// its prologue (barrier init, TMEM alloc, descriptor prefetch) and then
+// blocks in pdl_wait() until this grid has completed and flushed memory.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
 // ------------------------------------------------------------ tcgen05/TMEM
@@ -232,6 +245,24 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
   return (d_fmt << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
          (static_cast<uint32_t>(N >> 3) << 17) |
          (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Host: launch with programmatic stream serialization (PDL) allowed, so a
+// kernel that calls pdl_launch_dependents() lets this one start early.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace tec_sm100
