@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "conv_epilogue.cuh"
 #include "conv_params.h"
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int hbytes = halo_bytes_aligned(p.halo_px, SWZ);
   uint8_t* sH = smem;                       // 2 halo buffers
   uint8_t* sW = smem + 2 * hbytes;          // WSTAGES weight tiles
-  uint8_t* sStage = sW + WSTAGES * Cfg::kWBytes;  // 8 warps x 4 KB epilogue stage
+  uint8_t* sStage = sW + p.w_slots * Cfg::kWBytes;  // 8 warps x 4 KB epilogue stage
   uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
   uint64_t* hempty = hfull + 2;
   uint64_t* wfull = hempty + 2;
@@ -112,16 +113,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_launch_dependents();  // see conv_tc.cu
   pdl_wait();
 
+  // Tile order. Streamed weights: tiles strided over the grid, N fastest.
+  // Resident weights (p.resident): each CTA keeps ONE output-channel tile
+  // (n_tile = blockIdx.x % n_tiles) and loads all of its weights once.
+  const int spatial = p.n * p.bands;
+  const int ctas_per_n = static_cast<int>(gridDim.x) / p.n_tiles;
+  auto tile_at = [&](int i, int* n_tile, int* band, int* img) -> bool {
+    int s;
+    if (p.resident) {
+      s = static_cast<int>(blockIdx.x) / p.n_tiles + i * ctas_per_n;
+      if (s >= spatial || static_cast<int>(blockIdx.x) >= ctas_per_n * p.n_tiles) return false;
+      *n_tile = static_cast<int>(blockIdx.x) % p.n_tiles;
+    } else {
+      const int tile = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+      if (tile >= num_tiles) return false;
+      *n_tile = tile % p.n_tiles;
+      s = tile / p.n_tiles;
+    }
+    *band = s % p.bands;
+    *img = s / p.bands;
+    return true;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
       int hs = 0, ws = 0;
       uint32_t hph = 0, wph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int n_tile = tile % p.n_tiles;
-        const int rest = tile / p.n_tiles;
-        const int band = rest % p.bands;
-        const int img = rest / p.bands;
+      int n_tile, band, img;
+      if (p.resident && tile_at(0, &n_tile, &band, &img)) {
+        // every (tap, channel block) weight tile of this CTA's N tile, once
+        mbar_arrive_expect_tx(&wfull[0], static_cast<uint32_t>(taps * p.cblocks * Cfg::kWBytes));
+        for (int cb = 0; cb < p.cblocks; ++cb)
+          for (int t = 0; t < taps; ++t)
+            tma_load_2d(sW + (cb * taps + t) * Cfg::kWBytes, &tm_w, &wfull[0],
+                        t * p.cp + cb * kCB, n_tile * BN);
+      }
+      for (int i = 0; tile_at(i, &n_tile, &band, &img); ++i) {
         const int ih0 = band * p.th - p.ph;
         for (int cb = 0; cb < p.cblocks; ++cb) {
           { const long long t0 = p.dbg ? clock64() : 0;
@@ -132,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // the out-of-image pixels with zeros (the select(..., 0) pad).
           tma_load_4d(sH + hs * hbytes, &tm_x, &hfull[hs], cb * kCB, -p.pw, ih0, img);
           if (++hs == 2) { hs = 0; hph ^= 1; }
+          if (p.resident) continue;
           for (int t = 0; t < taps; ++t) {
             { const long long t0 = p.dbg ? clock64() : 0;
               mbar_wait(&wempty[ws], wph ^ 1);
@@ -150,49 +179,82 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = make_idesc<KIND>(128, BN);
       int hs = 0, ws = 0;
       uint32_t hph = 0, wph = 0;
-      int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t use = static_cast<uint32_t>(local >> 1);
-        { const long long t0 = p.dbg ? clock64() : 0;
-          mbar_wait(&tempty[acc], (use & 1) ^ 1);
-          if (p.dbg) dbg_wait[2] += clock64() - t0; }
-        tc_fence_after();
-        const uint32_t d0 = tmem_base + acc * Cfg::kAccCols;
-        for (int cb = 0; cb < p.cblocks; ++cb) {
-          { const long long t0 = p.dbg ? clock64() : 0;
-            mbar_wait(&hfull[hs], hph);
-            if (p.dbg) dbg_wait[1] += clock64() - t0; }
-          tc_fence_after();
-          const uint32_t h_base = smem_u32(sH + hs * hbytes);
-          for (int t = 0; t < taps; ++t) {
-            const int rh = t / p.s, rw = t - rh * p.s;
-            const uint32_t shift = static_cast<uint32_t>((rh * p.wp + rw) * SWZ);
-            { const long long t0 = p.dbg ? clock64() : 0;
-              mbar_wait(&wfull[ws], wph);
-              if (p.dbg) dbg_wait[1] += clock64() - t0; }
-            tc_fence_after();
-            const uint32_t w_base = smem_u32(sW + ws * Cfg::kWBytes);
-            const bool first = cb == 0 && t == 0;
-#pragma unroll
-            for (int ms = 0; ms < MS; ++ms) {
-#pragma unroll
-              for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
-                const uint64_t ad = make_smem_desc<SWZ>(
-                    h_base + ms * 128 * SWZ + shift + kk * 32, 8 * SWZ);
-                const uint64_t bd = make_smem_desc<SWZ>(w_base + kk * 32, 8 * SWZ);
-                tc_mma<KIND>(d0 + ms * BN, ad, bd, idesc,
-                             (first && kk == 0) ? 0u : 1u);
-              }
-            }
-            tc_commit(&wempty[ws]);
-            if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
-          }
-          tc_commit(&hempty[hs]);
-          if (++hs == 2) { hs = 0; hph ^= 1; }
-        }
-        tc_commit(&tfull[acc]);
+      int n_tile, band, img;
+      if (p.resident) {
+        const long long t0 = p.dbg ? clock64() : 0;
+        mbar_wait(&wfull[0], 0);
+        if (p.dbg) dbg_wait[1] += clock64() - t0;
       }
+      // Descriptors are built once and advanced by adding (byte offset >> 4)
+      // to the start-address field (smem addresses < 2^18, no carry-out).
+      //
+      // The issue loop is the MMA rate limiter when it is not lean: one
+      // thread issues every MMA, and ncu showed the earlier version (tap
+      // index division, per-tap parameter reloads) spending ~1000 cycles
+      // per tap for 8 MMAs that execute in ~430. Taps are therefore walked
+      // as (rh, rw) with incremental descriptor offsets, the resident /
+      // streamed choice is a compile-time branch, and all per-MMA offsets
+      // are immediates.
+      const uint64_t wdesc0 = make_smem_desc<SWZ>(smem_u32(sW), 8 * SWZ);
+      const bool dbg = p.dbg != nullptr;
+      const int pr = p.r, ps = p.s, cblocks = p.cblocks;
+      const uint32_t row_skip = static_cast<uint32_t>((p.wp - ps) * SWZ) >> 4;
+      auto issue = [&](auto resident_c) {
+        constexpr bool kRes = decltype(resident_c)::value;
+        for (int local = 0; tile_at(local, &n_tile, &band, &img); ++local) {
+          const int acc = local & 1;
+          const uint32_t use = static_cast<uint32_t>(local >> 1);
+          { const long long t0 = dbg ? clock64() : 0;
+            mbar_wait(&tempty[acc], (use & 1) ^ 1);
+            if (dbg) dbg_wait[2] += clock64() - t0; }
+          tc_fence_after();
+          const uint32_t d0 = tmem_base + acc * Cfg::kAccCols;
+          uint64_t bd = wdesc0;  // resident: walks all (cb, tap) tiles in order
+          for (int cb = 0; cb < cblocks; ++cb) {
+            { const long long t0 = dbg ? clock64() : 0;
+              mbar_wait(&hfull[hs], hph);
+              if (dbg) dbg_wait[1] += clock64() - t0; }
+            tc_fence_after();
+            uint64_t ad = make_smem_desc<SWZ>(smem_u32(sH + hs * hbytes), 8 * SWZ);
+            uint32_t accum = cb == 0 ? 0u : 1u;
+            for (int rh = 0; rh < pr; ++rh) {
+              for (int rw = 0; rw < ps; ++rw) {
+                if constexpr (!kRes) {
+                  const long long t0 = dbg ? clock64() : 0;
+                  mbar_wait(&wfull[ws], wph);
+                  if (dbg) dbg_wait[1] += clock64() - t0;
+                  tc_fence_after();
+                  bd = wdesc0 + static_cast<uint32_t>((ws * Cfg::kWBytes) >> 4);
+                }
+#pragma unroll
+                for (int ms = 0; ms < MS; ++ms) {
+#pragma unroll
+                  for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk) {
+                    tc_mma<KIND>(d0 + ms * BN, ad + ((ms * 128 * SWZ + kk * 32) >> 4),
+                                 bd + ((kk * 32) >> 4), idesc, kk == 0 ? accum : 1u);
+                  }
+                }
+                accum = 1u;
+                ad += SWZ >> 4;
+                if constexpr (kRes) {
+                  bd += Cfg::kWBytes >> 4;
+                } else {
+                  tc_commit(&wempty[ws]);
+                  if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
+                }
+              }
+              ad += row_skip;
+            }
+            tc_commit(&hempty[hs]);
+            if (++hs == 2) { hs = 0; hph ^= 1; }
+          }
+          tc_commit(&tfull[acc]);
+        }
+      };
+      if (p.resident)
+        issue(std::true_type{});
+      else
+        issue(std::false_type{});
     }
   } else if (warp >= 4) {
     // ------------------------------------------------- epilogue warps
@@ -210,14 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int fast = epi::classify_prog(p.epi);
     int local = 0;
     bool overflow = false;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    int n_tile, band, img;
+    for (; tile_at(local, &n_tile, &band, &img); ++local) {
       const int acc = local & 1;
       if (acc != grp) continue;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
-      const int n_tile = tile % p.n_tiles;
-      const int rest = tile / p.n_tiles;
-      const int band = rest % p.bands;
-      const int img = rest / p.bands;
       uint32_t* bias_s = sBias + acc * BN;
       epi::named_bar_sync(1 + grp, 128);
       epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
@@ -290,7 +349,8 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
                      const ConvHaloParams& p, int grid, cudaStream_t stream) {
   using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
   const int smem = 1024 + 2 * halo_bytes_aligned(p.halo_px, SWZ) +
-                   WSTAGES * Cfg::kWBytes + 8 * 4096 + 256 + 2 * BN * 4;
+                   p.w_slots * Cfg::kWBytes + 8 * 4096 + 256 + 2 * BN * 4;
+  if (!p.resident && p.w_slots != WSTAGES) return cudaErrorInvalidValue;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -301,8 +361,8 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
 }
 
 // Returns the dynamic smem a configuration needs (host-side planning).
-int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px) {
-  return 1024 + 2 * halo_bytes_aligned(halo_px, swz) + wstages * bn * swz + 8 * 4096 + 256 +
+int conv_halo_smem_bytes(int bn, int swz, int w_slots, int halo_px) {
+  return 1024 + 2 * halo_bytes_aligned(halo_px, swz) + w_slots * bn * swz + 8 * 4096 + 256 +
          2 * bn * 4;
 }
 

@@ -66,6 +66,8 @@ struct ConvHaloParams {
   int32_t n_tiles;      // ceil(oc / BN)
   int32_t cblocks;      // cp / channels-per-block
   int32_t halo_px;      // pixels per halo buffer (>= MS*128 + (r-1)*wp + s)
+  int32_t resident;     // 1: all weights of the CTA's N tile stay in smem
+  int32_t w_slots;      // weight tiles in smem (ring stages, or taps*cblocks)
   int32_t out_type;
   void* y;              // NHWC [N*OH*OW][OC]
   int32_t* err;

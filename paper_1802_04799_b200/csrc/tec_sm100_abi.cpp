@@ -320,6 +320,7 @@ const HaloInst kHaloInsts[] = {
 struct HaloChoice {
   const HaloInst* inst = nullptr;
   int th = 0, halo_px = 0, bands = 0, n_tiles = 0, tiles = 0;
+  int resident = 0, w_slots = 0, grid = 0;
 };
 
 // Picks (BN, MS, rows per tile) by a two-term model per tile --
@@ -340,25 +341,52 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
     const int th = (int)std::min<int64_t>(pl.oh, (128 * hi.ms) / wp);
     if (th < 1 || th + d->r - 1 > 256) continue;
     const int halo_px = 128 * hi.ms + (int)((d->r - 1) * wp + d->s) + 8;
-    if (conv_halo_smem_bytes(hi.bn, hi.swz, hi.wstages, halo_px) > 227 * 1024) continue;
     const int bands = (int)((pl.oh + th - 1) / th);
     const int n_tiles = (int)((d->k + hi.bn - 1) / hi.bn);
-    const int64_t tiles = d->n * bands * n_tiles;
+    const int64_t spatial = d->n * bands;
+    const int64_t tiles = spatial * n_tiles;
+    const int taps_cb = (int)(d->r * d->s * (pl.cp * es / hi.swz));
     const double ktot = (double)d->r * d->s * pl.cp;
     const double mma = 128.0 * hi.ms * hi.bn * ktot * 2 / 8192.0 *
                        (pl.kind == MmaKind::kTF32 ? 2 : pl.kind == MmaKind::kI8 ? 0.5 : 1);
-    const double bytes = (double)hi.bn * ktot * es +
-                         (double)(th + d->r - 1) * wp * pl.cp * es;
-    const double per_tile = std::max(mma, bytes / 40.0);
-    const double cost = (double)((tiles + sms - 1) / sms) * per_tile;
-    if (cost < best) {
-      best = cost;
-      out->inst = &hi;
-      out->th = th;
-      out->halo_px = halo_px;
-      out->bands = bands;
-      out->n_tiles = n_tiles;
-      out->tiles = (int)tiles;
+    const double halo_bytes = (double)(th + d->r - 1) * wp * pl.cp * es;
+    // knob `stages`: 0 auto, 1 streamed weight ring, 2 resident weights
+    for (int res = 0; res < 2; ++res) {
+      if (kn && kn->stages == 1 && res) continue;
+      if (kn && kn->stages == 2 && !res) continue;
+      const int w_slots = res ? taps_cb : hi.wstages;
+      static const bool dbg = std::getenv("TEC_SM100_PLAN_DEBUG") != nullptr;
+      if (dbg)
+        std::fprintf(stderr, "[tec-plan] halo bn=%d ms=%d swz=%d res=%d th=%d smem=%d\n", hi.bn,
+                     hi.ms, hi.swz, res, th,
+                     conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px));
+      if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px) > 227 * 1024) continue;
+      int grid;
+      double per_tile, waves;
+      if (res) {
+        const int per_n = (int)std::min<int64_t>(sms / n_tiles, spatial);
+        if (per_n < 1) continue;
+        grid = per_n * n_tiles;
+        waves = (double)((spatial + per_n - 1) / per_n);
+        per_tile = std::max(mma, halo_bytes / 40.0);
+      } else {
+        grid = (int)std::min<int64_t>(tiles, sms);
+        waves = (double)((tiles + sms - 1) / sms);
+        per_tile = std::max(mma, ((double)hi.bn * ktot * es + halo_bytes) / 40.0);
+      }
+      const double cost = waves * per_tile;
+      if (cost < best) {
+        best = cost;
+        out->inst = &hi;
+        out->th = th;
+        out->halo_px = halo_px;
+        out->bands = bands;
+        out->n_tiles = n_tiles;
+        out->tiles = (int)tiles;
+        out->resident = res;
+        out->w_slots = w_slots;
+        out->grid = grid;
+      }
     }
   }
   return out->inst != nullptr;
@@ -411,14 +439,16 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   p.th = hc.th; p.wp = wp; p.bands = hc.bands; p.n_tiles = hc.n_tiles;
   p.cblocks = (int32_t)(pl.cp / cb);
   p.halo_px = hc.halo_px;
+  p.resident = hc.resident;
+  p.w_slots = hc.w_slots;
   p.out_type = out_dtype;
   p.y = y;
   p.err = err;
   p.epi = epi;
   // knob vec: 1 = per-thread epilogue rows, 2 = no epilogue (diagnostic only)
   p.epi_mode = kn && (kn->vec == 1 || kn->vec == 2) ? (int32_t)kn->vec : 0;
-  int grid = std::min(hc.tiles, sms);
-  if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
+  int grid = hc.grid;
+  if (kn && kn->grid > 0 && !hc.resident) grid = (int)std::min<int64_t>(grid, kn->grid);
   static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
   unsigned long long* dbg = nullptr;
   if (prof) {

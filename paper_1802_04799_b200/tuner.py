@@ -131,7 +131,7 @@ def conv_space(name: str, desc: _abi.ConvDesc,
     tile_n = CTA N tile (split of the OC axis), tile_m = M rows per tile
     (halo: MMA sub-tiles x 128)."""
     knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
-             KnobDef("tile_m", [128, 256, 512])]
+             KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2])]
     return KnobSpace(name, knobs, desc, tuple(epilogue))
 
 

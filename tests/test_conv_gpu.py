@@ -175,17 +175,23 @@ def test_batch64_c2_bf16_properties():
         assert same_values(y[i:i + 1], want, TOL_BF16)
 
 
-@pytest.mark.parametrize("path", [1, 2])   # knob tile_k: 1 = im2col TMA, 2 = halo
+@pytest.mark.parametrize("path", [(1, 0), (2, 1), (2, 2)])  # (tile_k, stages)
 @pytest.mark.parametrize("compute", ["bf16", "i8"])
-@pytest.mark.parametrize("layer", ["C2", "C6", "C9", "C12"])
+@pytest.mark.parametrize("layer", ["C1", "C2", "C6", "C9", "C12"])
 def test_a_operand_paths_agree_with_oracle(layer, compute, path):
+    # tile_k: 1 = im2col TMA, 2 = halo; stages: 1 streamed / 2 resident weights
     hw, c, k, r, s = RESNET18_CONVS[layer]
     x, w, b = _inputs((2, c, hw, hw), (k, c, r, r), k, compute == "i8",
                       seed=7 + sum(map(ord, layer)))
     attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
     epi = [("bias_add", b), ("relu",)]
-    y = fused_conv("conv2d", x, w, attrs, epi, knobs={"tile_k": path},
-                   compute=None if compute == "i8" else compute)
+    try:
+        y = fused_conv("conv2d", x, w, attrs, epi,
+                       knobs={"tile_k": path[0], "stages": path[1]},
+                       compute=None if compute == "i8" else compute)
+    except TecError as e:  # a knob combination that does not instantiate
+        assert e.code == "LoweringError"
+        pytest.skip(str(e))
     xr, wr = (bf16_round(x), bf16_round(w)) if compute == "bf16" else (x, w)
     want = oracle_conv("conv2d", xr, wr, attrs["strides"], attrs["padding"], epi)
     if compute == "i8":
@@ -194,13 +200,18 @@ def test_a_operand_paths_agree_with_oracle(layer, compute, path):
         assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
 
 
+@pytest.mark.parametrize("stages", [1, 2])  # 1 streamed weights, 2 resident weights
 @pytest.mark.parametrize("tile_m", [128, 256, 512])
-def test_halo_tile_shapes(tile_m):
+def test_halo_tile_shapes(tile_m, stages):
     # Several virtual-row tile heights, odd sizes, padding != 1.
     x, w, b = _inputs((3, 64, 19, 23), (64, 64, 5, 5), 64, False, 12)
     attrs = {"strides": (1, 1), "padding": (2, 2)}
     epi = [("bias_add", b), ("relu",)]
-    y = fused_conv("conv2d", x, w, attrs, epi, compute="bf16",
-                   knobs={"tile_k": 2, "tile_m": tile_m})
+    try:
+        y = fused_conv("conv2d", x, w, attrs, epi, compute="bf16",
+                       knobs={"tile_k": 2, "tile_m": tile_m, "stages": stages})
+    except TecError as e:  # 5x5x64 resident weights + halo may exceed smem
+        assert e.code == "LoweringError" and stages == 2
+        pytest.skip(str(e))
     want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), (1, 1), (2, 2), epi)
     assert same_values(y, want, TOL_BF16)
