@@ -452,6 +452,85 @@ __device__ __forceinline__ void epi_block(const P& p, const EpiProg& g, int prog
   epi_warp_block<kInt>(p, g, taddr, col0, lane, my_row, bias_s, stage, overflow);
 }
 
+// ---------------------------------------------------- TMA-store epilogue
+// For the fast programs (none / bias / bias+relu) the block goes TMEM ->
+// registers -> output dtype -> a swizzled 32-row x 32-column shared-memory
+// box, and ONE lane stores the box with cp.async.bulk.tensor: no address
+// math, shuffles or predicated global stores per element, and the tensor
+// map clips rows/columns outside the output (M tail, OC tail, the halo
+// kernel's junk virtual rows) for free.
+//
+// Box rows are 32 * ES bytes; 16-byte chunks are placed exactly as the
+// tensor map's swizzle expects: bf16 SWIZZLE_64B (chunk c of row r at
+// c ^ ((r >> 1) & 3)), f32 SWIZZLE_128B (c ^ (r & 7)). Both are
+// bank-conflict free for the one-row-per-lane writes.
+template <int ES>
+__device__ __forceinline__ uint32_t box_off(int row, int chunk) {
+  if constexpr (ES == 2)
+    return static_cast<uint32_t>(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
+  else
+    return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int PROG, int ES>
+__device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const uint32_t* bias_s,
+                                              uint32_t box) {
+  uint32_t acc[kChunk];
+  tmem_ld32(taddr, acc);
+  uint32_t b[kChunk];
+  if constexpr (PROG != kProgNone) load_bias32(bias_s, b);
+  tmem_ld_wait();
+  float v[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    float x = __uint_as_float(acc[j]);
+    if constexpr (PROG != kProgNone) x = __fadd_rn(x, __uint_as_float(b[j]));
+    if constexpr (PROG == kProgBiasRelu) x = (x < 0.0f) ? 0.0f : x;
+    v[j] = x;
+  }
+  constexpr int kCpr = 32 * ES / 16;
+  if constexpr (ES == 2) {
+#pragma unroll
+    for (int c = 0; c < kCpr; ++c)
+      sts128(box + box_off<2>(lane, c),
+             make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                        pack_bf16x2(v[8 * c + 4], v[8 * c + 5]),
+                        pack_bf16x2(v[8 * c + 6], v[8 * c + 7])));
+  } else {
+#pragma unroll
+    for (int c = 0; c < kCpr; ++c)
+      sts128(box + box_off<4>(lane, c),
+             make_uint4(__float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
+                        __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3])));
+  }
+}
+
+// One warp's 32 accumulator rows x BN columns through the TMA-store path.
+// `stage` = this warp's 4 KB (2 bf16 boxes / 1 f32 box, used as a ring;
+// `cnt` counts boxes across calls). `store(box, c0)` runs on lane 0 and
+// issues the TMA store(s) of the box holding columns [c0, c0 + 32).
+template <int PROG, int ES, int BN, typename StoreFn>
+__device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const uint32_t* bias_s,
+                                             uint32_t stage, int valid_cols, uint32_t& cnt,
+                                             StoreFn&& store) {
+  constexpr uint32_t kBox = 32 * 32 * ES;
+  constexpr uint32_t kSlots = 4096 / kBox;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN && c0 < valid_cols; c0 += kChunk) {
+    const uint32_t box = stage + (cnt % kSlots) * kBox;
+    if (lane == 0) bulk_wait_read<kSlots - 1>();  // the box's previous store has read it
+    __syncwarp();
+    epi_block_box<PROG, ES>(taddr0 + c0, lane, bias_s + c0, box);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      store(box, c0);
+      bulk_commit();
+    }
+    ++cnt;
+  }
+}
+
 // Cooperative per-tile bias staging: `nthreads` epilogue threads copy the
 // tile's BN bias values into shared memory (zero past OC).
 template <typename T>

@@ -61,6 +61,7 @@ template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tm_x,
                      const __grid_constant__ CUtensorMap tm_w,
+                     const __grid_constant__ CUtensorMap tm_y,
                      const ConvHaloParams p) {
   using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -69,8 +70,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int hbytes = halo_bytes_aligned(p.halo_px, SWZ);
   uint8_t* sH = smem;                       // 2 halo buffers
   uint8_t* sW = smem + 2 * hbytes;          // WSTAGES weight tiles
-  uint8_t* sStage = sW + p.w_slots * Cfg::kWBytes;  // 8 warps x 4 KB epilogue stage
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
+  uint8_t* sStage = sW + p.w_slots * Cfg::kWBytes;  // epilogue stage (>= 8 warps x 4 KB)
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + p.stage_bytes);
   uint64_t* hempty = hfull + 2;
   uint64_t* wfull = hempty + 2;
   uint64_t* wempty = wfull + WSTAGES;
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_x);
     tma_prefetch_desc(&tm_w);
+    if (p.tma_store) tma_prefetch_desc(&tm_y);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&hfull[i], 1);
       mbar_init(&hempty[i], 1);
@@ -270,6 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
     const epi::EpiProg prog = epi::make_prog(p.epi);
     const int fast = epi::classify_prog(p.epi);
+    const bool tma_epi = p.tma_store && p.epi_mode == 0 && fast != epi::kProgGeneric &&
+                         fast != epi::kProgBiasAddRelu;
+    uint32_t chunk_cnt = 0;
     int local = 0;
     bool overflow = false;
     int n_tile, band, img;
@@ -286,6 +291,66 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
+      if constexpr (KIND != MmaKind::kI8) {
+        if (tma_epi) {
+          // The GROUP stages the whole tile's virtual rows for one 32-column
+          // chunk (MS*128 rows, the row-per-lane writes of its 4 warps), then
+          // one thread stores every output row of the band as a 4-D box
+          // {32 ch, OW px} read from smem row ohl*wp: junk virtual rows are
+          // simply never read, rows past OH are clipped by the map. (A store
+          // per warp would need negative box coordinates for rows that
+          // straddle an output-row boundary; TMA stores reject those.)
+          // Host guarantees: MS*128 rows x 32*ES bytes <= 16 KB and
+          // wp*32*ES a multiple of 128 B (TMA source alignment); the
+          // swizzle is absolute-address based, so any such row start works.
+          auto run = [&](auto prog_c, auto es_c) {
+            constexpr int kProg = decltype(prog_c)::value, kES = decltype(es_c)::value;
+            constexpr uint32_t kRowB = 32 * kES;
+            const uint32_t gbytes = static_cast<uint32_t>(p.stage_bytes) / 2;
+            const uint32_t cbytes = MS * 128 * kRowB;
+            const uint32_t gbase = smem_u32(sStage) + static_cast<uint32_t>(grp) * gbytes;
+            const bool two = gbytes >= 2 * cbytes;  // chunk ring of 2: write one while one drains
+            const bool issuer = q == 0 && lane == 0;
+            const int valid = p.oc - n_tile * BN;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN && c0 < valid; c0 += epi::kChunk) {
+              const uint32_t gbuf = gbase + (two ? (chunk_cnt & 1) * cbytes : 0);
+              ++chunk_cnt;
+              if (issuer) {  // the slot's previous stores have finished reading it
+                if (two) bulk_wait_read<1>(); else bulk_wait_read<0>();
+              }
+              epi::named_bar_sync(1 + grp, 128);
+#pragma unroll 1
+              for (int ms = 0; ms < MS; ++ms)
+                epi::epi_block_box<kProg, kES>(
+                    tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0,
+                    static_cast<int>(lane), bias_s + c0,
+                    gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB);
+              fence_proxy_async_smem();
+              epi::named_bar_sync(1 + grp, 128);
+              if (issuer) {
+                for (int ohl = 0; ohl < p.th && band * p.th + ohl < p.oh; ++ohl)
+                  tma_store_4d(&tm_y, gbuf + static_cast<uint32_t>(ohl * p.wp) * kRowB,
+                               n_tile * BN + c0, 0, band * p.th + ohl, img);
+                bulk_commit();
+              }
+            }
+          };
+          if (p.out_type == kBF16) {
+            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 2>{});
+            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 2>{});
+            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 2>{});
+          } else {
+            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 4>{});
+            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 4>{});
+            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 4>{});
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          if (p.dbg) dbg_wait[4] += clock64() - tw1;
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int ms = 0; ms < MS; ++ms) {
         const int vbase = ms * 128 + static_cast<int>(q * 32);
@@ -322,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[acc]);
       if (p.dbg) dbg_wait[4] += clock64() - tw1;
     }
+    if (lane == 0) bulk_wait_all();  // TMA stores done before smem goes away
     if (overflow && p.err) atomicOr(p.err, 1);
   }
 
@@ -346,30 +412,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
 int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
-                     const ConvHaloParams& p, int grid, cudaStream_t stream) {
+                     const CUtensorMap& tm_y, const ConvHaloParams& p, int grid,
+                     cudaStream_t stream) {
   using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
   const int smem = 1024 + 2 * halo_bytes_aligned(p.halo_px, SWZ) +
-                   p.w_slots * Cfg::kWBytes + 8 * 4096 + 256 + 2 * BN * 4;
+                   p.w_slots * Cfg::kWBytes + p.stage_bytes + 256 + 2 * BN * 4;
+  if (p.stage_bytes < 8 * 4096 || p.stage_bytes % 2048) return cudaErrorInvalidValue;
   if (!p.resident && p.w_slots != WSTAGES) return cudaErrorInvalidValue;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_x, tm_w, p);
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_x, tm_w, tm_y, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 // Returns the dynamic smem a configuration needs (host-side planning).
-int conv_halo_smem_bytes(int bn, int swz, int w_slots, int halo_px) {
-  return 1024 + 2 * halo_bytes_aligned(halo_px, swz) + w_slots * bn * swz + 8 * 4096 + 256 +
+int conv_halo_smem_bytes(int bn, int swz, int w_slots, int halo_px, int stage_bytes) {
+  return 1024 + 2 * halo_bytes_aligned(halo_px, swz) + w_slots * bn * swz + stage_bytes + 256 +
          2 * bn * 4;
 }
 
 #define TEC_HALO(KIND, BN, MS, SWZ, WS)                                        \
   template int launch_conv_halo<KIND, BN, MS, SWZ, WS>(                       \
-      const CUtensorMap&, const CUtensorMap&, const ConvHaloParams&, int,    \
-      cudaStream_t);
+      const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,           \
+      const ConvHaloParams&, int, cudaStream_t);
 
 TEC_HALO(MmaKind::kF16, 64, 1, 128, 6)
 TEC_HALO(MmaKind::kF16, 64, 2, 128, 6)

@@ -48,6 +48,7 @@ struct ConvGemmParams {
   // accumulator, [4] epilogue busy, [5] CTA lifetime, [6] tiles.
   unsigned long long* dbg;
   int32_t epi_mode;     // 0: warp-coalesced epilogue, 1: per-thread rows
+  int32_t tma_store;    // 1: y has a TMA store map (fast programs use it)
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA
@@ -74,6 +75,8 @@ struct ConvHaloParams {
   EpilogueParams epi;
   unsigned long long* dbg;  // optional pipeline profile, as ConvGemmParams
   int32_t epi_mode;         // 0: warp-coalesced epilogue, 1: per-thread rows
+  int32_t tma_store;        // 1: y has a TMA store map (fast programs use it)
+  int32_t stage_bytes;      // epilogue stage (>= 32 KB); two halves, one per group
 };
 
 struct DepthwiseParams {

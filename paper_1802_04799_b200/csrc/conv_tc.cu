@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "conv_params.h"
 #include "sm100_ptx.cuh"
@@ -65,6 +66,7 @@ template <MmaKind KIND, int BN, int STAGES, int SWZ>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fprop_tc_kernel(const __grid_constant__ CUtensorMap tm_a,
                          const __grid_constant__ CUtensorMap tm_b,
+                         const __grid_constant__ CUtensorMap tm_y,
                          const ConvGemmParams p) {
   using Cfg = ConvCfg<KIND, BN, STAGES, SWZ>;
   extern __shared__ uint8_t smem_raw[];
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
+    if (p.tma_store) tma_prefetch_desc(&tm_y);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -204,6 +207,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
     const epi::EpiProg prog = epi::make_prog(p.epi);
     const int fast = epi::classify_prog(p.epi);
+    const bool tma_epi = p.tma_store && p.epi_mode == 0 && fast != epi::kProgGeneric &&
+                         fast != epi::kProgBiasAddRelu;
+    const uint32_t stage_u32 = smem_u32(stage);
+    uint32_t box_cnt = 0;
     int local = 0;
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles;
@@ -226,6 +233,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
+      if constexpr (KIND != MmaKind::kI8) {
+        if (tma_epi) {
+          // One 2-D box store per 32 columns; rows >= M are clipped.
+          auto run = [&](auto prog_c, auto es_c) {
+            constexpr int kProg = decltype(prog_c)::value, kES = decltype(es_c)::value;
+            epi::epi_rows_tma<kProg, kES, BN>(
+                tmem_base + ((q * 32) << 16) + acc * BN, static_cast<int>(lane), bias_s,
+                stage_u32, p.oc - n_tile * BN, box_cnt, [&](uint32_t box, int c0) {
+                  tma_store_2d(&tm_y, box, n_tile * BN + c0, row0);
+                });
+          };
+          if (p.out_type == kBF16) {
+            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 2>{});
+            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 2>{});
+            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 2>{});
+          } else {
+            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 4>{});
+            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 4>{});
+            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 4>{});
+          }
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+          if (p.dbg) dbg_wait[4] += clock64() - tw1;
+          continue;
+        }
+      }
       const int my_row = row_ok ? row : -1;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN && p.epi_mode != 2; c0 += kChunk) {  // 2: no epilogue (diagnostic)
@@ -250,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&tempty[acc]);
       if (p.dbg) dbg_wait[4] += clock64() - tw1;
     }
+    if (lane == 0) bulk_wait_all();  // TMA stores done before smem goes away
     if (overflow && p.err) atomicOr(p.err, 1);
   }
 
@@ -277,22 +311,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Returns a cudaError_t.
 template <MmaKind KIND, int BN, int STAGES, int SWZ>
 int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
-                         const ConvGemmParams& p, int grid,
+                         const CUtensorMap& tm_y, const ConvGemmParams& p, int grid,
                          cudaStream_t stream) {
   using Cfg = ConvCfg<KIND, BN, STAGES, SWZ>;
   auto kfn = conv_fprop_tc_kernel<KIND, BN, STAGES, SWZ>;
   cudaError_t e = cudaFuncSetAttribute(
       kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, tm_a, tm_b, p);
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, tm_a, tm_b, tm_y, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 #define TEC_INST(KIND, BN, ST, SWZ)                                         \
   template int launch_conv_fprop_tc<KIND, BN, ST, SWZ>(                    \
-      const CUtensorMap&, const CUtensorMap&, const ConvGemmParams&, int, \
-      cudaStream_t);
+      const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,          \
+      const ConvGemmParams&, int, cudaStream_t);
 
 // bf16: 128 B channel blocks (64 ch) for Cp % 64 == 0, 32 B (16 ch) for
 // the stem (C1, 3 -> 16 padded channels).

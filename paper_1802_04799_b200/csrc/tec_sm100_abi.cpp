@@ -27,7 +27,7 @@
 namespace tec_sm100 {
 template <MmaKind KIND, int BN, int STAGES, int SWZ>
 int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
-                         const ConvGemmParams& p, int grid,
+                         const CUtensorMap& tm_y, const ConvGemmParams& p, int grid,
                          cudaStream_t stream);
 int launch_pack_activation(const void* in, int in_type, void* out, int64_t n,
                            int64_t c, int64_t hw, int64_t cp, int mode,
@@ -48,8 +48,9 @@ int launch_conv_f32_exact(const float* x, const float* w,
                           const ConvGemmParams& p, cudaStream_t st);
 template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
 int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
-                     const ConvHaloParams& p, int grid, cudaStream_t stream);
-int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px);
+                     const CUtensorMap& tm_y, const ConvHaloParams& p, int grid,
+                     cudaStream_t stream);
+int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px, int stage_bytes);
 }  // namespace tec_sm100
 
 using namespace tec_sm100;
@@ -120,6 +121,30 @@ CUtensorMapSwizzle swizzle_of(int bytes) {
          : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
          : bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                        : CU_TENSOR_MAP_SWIZZLE_NONE;
+}
+
+// TMA store map for a float output y (bf16 / f32): `rank` dims innermost
+// first (dims[0] = OC), box 32 channels x `box_px` pixels (x 1 x 1),
+// swizzled to match epi::box_off. Leaves *ok false when the layout does not
+// allow it (integer output, or an OC row pitch that is not a multiple of 16 B).
+void make_store_map(CUtensorMap* tm, void* y, int32_t out_dtype, int rank,
+                    const cuuint64_t* dims, int box_px, bool* ok) {
+  *ok = false;
+  std::memset(tm, 0, sizeof(*tm));
+  if (out_dtype != TEC_DT_BF16 && out_dtype != TEC_DT_F32) return;
+  const int es = out_dtype == TEC_DT_BF16 ? 2 : 4;
+  if ((dims[0] * es) % 16 || box_px < 1 || box_px > 256) return;
+  cuuint64_t strides[3];
+  cuuint64_t pitch = es;
+  for (int i = 0; i + 1 < rank; ++i) strides[i] = (pitch *= dims[i]);
+  cuuint32_t box[4] = {32, (cuuint32_t)box_px, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = driver_fns().tiled(
+      tm, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+      (cuuint32_t)rank, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      es == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  *ok = r == CUDA_SUCCESS;
 }
 
 // ------------------------------------------------------ layout planning
@@ -272,7 +297,7 @@ int sm_count(int dev) {
 }
 
 // ------------------------------------------------------ dense conv launch
-using Launcher = int (*)(const CUtensorMap&, const CUtensorMap&,
+using Launcher = int (*)(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                          const ConvGemmParams&, int, cudaStream_t);
 
 Launcher pick_launcher(MmaKind kind, int bn, int swz) {
@@ -297,7 +322,7 @@ Launcher pick_launcher(MmaKind kind, int bn, int swz) {
 }
 
 // ------------------------------------------- shifted-window (halo) path
-using HaloLauncher = int (*)(const CUtensorMap&, const CUtensorMap&,
+using HaloLauncher = int (*)(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                              const ConvHaloParams&, int, cudaStream_t);
 struct HaloInst {
   MmaKind kind;
@@ -317,6 +342,9 @@ const HaloInst kHaloInsts[] = {
 };
 #undef TEC_H
 
+constexpr int kStageMin = 8 * 4096;  // epilogue stage: 8 warps x 4 KB
+constexpr int kSmemMax = 227 * 1024;
+
 struct HaloChoice {
   const HaloInst* inst = nullptr;
   int th = 0, halo_px = 0, bands = 0, n_tiles = 0, tiles = 0;
@@ -329,7 +357,7 @@ struct HaloChoice {
 bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int sms,
                HaloChoice* out) {
   if (d->stride_h != 1 || d->stride_w != 1) return false;
-  const int wp = (int)(d->w + 2 * d->pad_w);
+  const int wp = (int)((d->w + 2 * d->pad_w + 1) & ~int64_t(1));  // even: 128-B aligned output rows in the TMA epilogue
   const int es = elem_bytes(pl.act);
   if (wp > 256 || (pl.oh + d->r - 1) < 1) return false;
   double best = 1e30;
@@ -359,8 +387,8 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
       if (dbg)
         std::fprintf(stderr, "[tec-plan] halo bn=%d ms=%d swz=%d res=%d th=%d smem=%d\n", hi.bn,
                      hi.ms, hi.swz, res, th,
-                     conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px));
-      if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px) > 227 * 1024) continue;
+                     conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin));
+      if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin) > kSmemMax) continue;
       int grid;
       double per_tile, waves;
       if (res) {
@@ -399,7 +427,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   const DriverFns& fns = driver_fns();
   const int es = elem_bytes(pl.act);
   const int cb = pl.swz / es;
-  const int wp = (int)(d->w + 2 * d->pad_w);
+  const int wp = (int)((d->w + 2 * d->pad_w + 1) & ~int64_t(1));  // even: 128-B aligned output rows in the TMA epilogue
   const CUtensorMapDataType tdt = pl.act == TEC_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                   : pl.act == TEC_DT_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -447,6 +475,28 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   p.epi = epi;
   // knob vec: 1 = per-thread epilogue rows, 2 = no epilogue (diagnostic only)
   p.epi_mode = kn && (kn->vec == 1 || kn->vec == 2) ? (int32_t)kn->vec : 0;
+  CUtensorMap tm_y;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)d->k, (cuuint64_t)pl.ow, (cuuint64_t)pl.oh,
+                          (cuuint64_t)d->n};
+    // Group-staged TMA epilogue (conv_halo.cu): the tile's MS*128 virtual
+    // rows x 32 columns must fit a group's 16 KB stage, and every output
+    // row's first virtual row must sit on a 128-byte boundary.
+    const int rowb = 32 * elem_bytes(out_dtype);
+    bool ok = false;
+    const int cbytes = hc.inst->ms * 128 * rowb;
+    if (pl.kind != MmaKind::kI8 && 2 * cbytes <= kStageMin && (wp * rowb) % 128 == 0)
+      make_store_map(&tm_y, y, out_dtype, 4, dims, (int)pl.ow, &ok);
+    else std::memset(&tm_y, 0, sizeof(tm_y));
+    // Room left in shared memory -> a 2-chunk ring per group, so one chunk
+    // is written while the previous one's TMA stores drain.
+    p.stage_bytes = kStageMin;
+    if (ok && 4 * cbytes > kStageMin &&
+        conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, 4 * cbytes) <=
+            kSmemMax)
+      p.stage_bytes = 4 * cbytes;
+    p.tma_store = ok && !(kn && kn->vec == 3) ? 1 : 0;  // vec 3: SIMT stores
+  }
   int grid = hc.grid;
   if (kn && kn->grid > 0 && !hc.resident) grid = (int)std::min<int64_t>(grid, kn->grid);
   static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
@@ -456,7 +506,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
-  const int e = hc.inst->fn(tm_x, tm_w, p, grid, st);
+  const int e = hc.inst->fn(tm_x, tm_w, tm_y, p, grid, st);
   if (e) return cuda_fail(e, "conv_halo launch");
   if (prof) {
     unsigned long long h[16];
@@ -579,6 +629,14 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   p.epi = epi;
   // knob vec: 1 = per-thread epilogue rows, 2 = no epilogue (diagnostic only)
   p.epi_mode = kn && (kn->vec == 1 || kn->vec == 2) ? (int32_t)kn->vec : 0;
+  CUtensorMap tm_y;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)d->k, (cuuint64_t)pl.m};
+    bool ok = false;
+    if (pl.kind != MmaKind::kI8) make_store_map(&tm_y, y, out_dtype, 2, dims, 32, &ok);
+    else std::memset(&tm_y, 0, sizeof(tm_y));
+    p.tma_store = ok && !(kn && kn->vec == 3) ? 1 : 0;  // vec 3: SIMT stores
+  }
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
   int grid = (int)std::min<int64_t>(tiles, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
@@ -591,7 +649,7 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
-  const int e = launch(tm_a, tm_b, p, grid, st);
+  const int e = launch(tm_a, tm_b, tm_y, p, grid, st);
   if (e) return cuda_fail(e, "conv_fprop_tc launch");
   if (prof) {
     unsigned long long h[8];
