@@ -186,6 +186,25 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
                                int32_t out_dtype, int32_t* err_flag,
                                void* stream);
 
+/* ---- graph operators around the conv path (ResNet-18 graph).
+ * The reference has no pooling operator; these are new registered ops
+ * whose semantics oracle/tec_oracle.c restates (see pool.cu). NHWC device
+ * tensors; dtype/out_dtype are tec_dtype. */
+typedef struct {
+  int64_t n, c, h, w;                      /* input, logical NCHW dims   */
+  int64_t r, s;                            /* window (max_pool2d)        */
+  int64_t stride_h, stride_w, pad_h, pad_w;
+  int32_t dtype, out_dtype;
+} tec_pool_desc;
+
+/* max_pool2d: y NHWC [n][oh][ow][c], oh = (h + 2ph - r)/sh + 1; padded taps
+ * are skipped. dtype == out_dtype (f32, bf16, i32, i8); c*elem % 16 == 0. */
+tec_status tec_max_pool2d(const tec_pool_desc* d, const void* x, void* y, void* stream);
+/* global_avg_pool == scale(sum(sum(x, W), H), 1/(h*w)) in float:
+ * y [n][c] (f32 or bf16) from x NHWC (f32 or bf16). */
+tec_status tec_global_avg_pool(const tec_pool_desc* d, const void* x, void* y, void* stream);
+tec_status tec_pool_infer(const tec_pool_desc* d, int64_t out_shape[4]);
+
 /* ---- host-level path: eval_graph_node / native_eval for target sm100 ----
  * x: NCHW f32 (i8 for I8); w: OIHW f32 (i8); epilogue operands NCHW f32
  * (i32); y: NCHW f32 (i32). All HOST pointers; copies included. */

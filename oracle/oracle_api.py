@@ -56,8 +56,36 @@ def _load():
             fn.restype = C.c_int
             fn.argtypes = [C.POINTER(_Conv), C.c_void_p, C.c_void_p,
                            C.POINTER(_Epi), C.c_int, C.c_void_p, C.c_int]
+        i64 = C.c_int64
+        lib.tec_oracle_max_pool2d_f32.restype = C.c_int
+        lib.tec_oracle_max_pool2d_f32.argtypes = [C.c_void_p] + [i64] * 10 + [C.c_void_p]
+        lib.tec_oracle_global_avg_pool_f32.restype = C.c_int
+        lib.tec_oracle_global_avg_pool_f32.argtypes = [C.c_void_p] + [i64] * 4 + [C.c_void_p]
         _lib = lib
     return _lib
+
+
+def max_pool2d(x: np.ndarray, kernel=(3, 3), strides=(2, 2), padding=(1, 1)) -> np.ndarray:
+    """max_pool2d on NCHW f32 (tec_oracle.c); padded taps never win."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    n, c, h, w = x.shape
+    (r, s), (sh, sw), (ph, pw) = kernel, strides, padding
+    oh, ow = (h + 2 * ph - r) // sh + 1, (w + 2 * pw - s) // sw + 1
+    y = np.empty((n, c, oh, ow), np.float32)
+    st = _load().tec_oracle_max_pool2d_f32(x.ctypes.data, n, c, h, w, r, s, sh, sw, ph, pw,
+                                           y.ctypes.data)
+    if st:
+        raise OracleError(st)
+    return y
+
+
+def global_avg_pool(x: np.ndarray) -> np.ndarray:
+    """scale(sum(sum(x, axis=3), axis=2), 1/(H*W)) in float: [N, C]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    n, c, h, w = x.shape
+    y = np.empty((n, c), np.float32)
+    _load().tec_oracle_global_avg_pool_f32(x.ctypes.data, n, c, h, w, y.ctypes.data)
+    return y
 
 
 class OracleError(RuntimeError):

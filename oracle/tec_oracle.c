@@ -231,3 +231,54 @@ int tec_oracle_fused_conv_i8(const tec_oracle_conv* d, const int8_t* x,
                              int n_epi, int32_t* y, int threads) {
   return run(d, x, w, epi, n_epi, y, threads, 1);
 }
+
+/* ---------------------------------------------------------------- pooling
+ * New graph operators of the ResNet-18 graph (not in the reference op set;
+ * the build defines them, include/tec_sm100.h tec_pool_desc):
+ *   max_pool2d: max over the in-image taps of each window (padding taps are
+ *     skipped), NCHW, exact.
+ *   global_avg_pool: the reference composition
+ *     scale(sum(sum(x, axis=3), axis=2), 1/(H*W)):
+ *     sum reduces in order from 0 with float rounding (R/src/ops.cpp:111-149,
+ *     R/src/texpr.cpp:205-228), scale multiplies by the attr rounded to
+ *     float (R/src/ops.cpp:260-281). */
+int tec_oracle_max_pool2d_f32(const float* x, int64_t n, int64_t c, int64_t h, int64_t w,
+                              int64_t r, int64_t s, int64_t sh, int64_t sw, int64_t ph,
+                              int64_t pw, float* y) {
+  if (h + 2 * ph < r || w + 2 * pw < s || sh <= 0 || sw <= 0) return ERR_SHAPE;
+  const int64_t oh = (h + 2 * ph - r) / sh + 1, ow = (w + 2 * pw - s) / sw + 1;
+  for (int64_t p = 0; p < n * c; ++p)
+    for (int64_t i = 0; i < oh; ++i)
+      for (int64_t j = 0; j < ow; ++j) {
+        float best = 0.0f;
+        int any = 0;
+        for (int64_t a = 0; a < r; ++a) {
+          const int64_t ih = i * sh + a - ph;
+          if (ih < 0 || ih >= h) continue;
+          for (int64_t b = 0; b < s; ++b) {
+            const int64_t iw = j * sw + b - pw;
+            if (iw < 0 || iw >= w) continue;
+            const float v = x[(p * h + ih) * w + iw];
+            if (!any || v > best) best = v;
+            any = 1;
+          }
+        }
+        y[(p * oh + i) * ow + j] = best;
+      }
+  return ERR_OK;
+}
+
+int tec_oracle_global_avg_pool_f32(const float* x, int64_t n, int64_t c, int64_t h,
+                                   int64_t w, float* y) {
+  const float f = (float)(1.0 / (double)(h * w));
+  for (int64_t p = 0; p < n * c; ++p) {
+    float tot = 0.0f;
+    for (int64_t i = 0; i < h; ++i) {
+      float row = 0.0f;
+      for (int64_t j = 0; j < w; ++j) row = row + x[(p * h + i) * w + j];
+      tot = tot + row;
+    }
+    y[p] = tot * f;
+  }
+  return ERR_OK;
+}

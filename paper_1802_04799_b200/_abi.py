@@ -67,6 +67,13 @@ class Knobs(C.Structure):
                  "vec", "unroll", "acc_bufs", "grid")]
 
 
+class PoolDesc(C.Structure):
+    """tec_pool_desc (include/tec_sm100.h)."""
+    _fields_ = [(f, C.c_int64) for f in ("n", "c", "h", "w", "r", "s", "stride_h", "stride_w",
+                                         "pad_h", "pad_w")] + \
+               [("dtype", C.c_int32), ("out_dtype", C.c_int32)]
+
+
 class ConvLayout(C.Structure):
     _fields_ = [("oh", C.c_int64), ("ow", C.c_int64), ("cp", C.c_int64),
                 ("act_dtype", C.c_int32), ("acc_dtype", C.c_int32),
@@ -98,6 +105,9 @@ SIGNATURES = {
     "tec_eval_fused_conv": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P, C.c_int]),
     "tec_measure": (C.c_int32, [_DESC, _EPI, _KN, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.POINTER(C.c_double)]),
+    "tec_pool_infer": (C.c_int32, [C.POINTER(PoolDesc), C.POINTER(C.c_int64)]),
+    "tec_max_pool2d": (C.c_int32, [C.POINTER(PoolDesc), _P, _P, _P]),
+    "tec_global_avg_pool": (C.c_int32, [C.POINTER(PoolDesc), _P, _P, _P]),
 }
 
 _lib = None

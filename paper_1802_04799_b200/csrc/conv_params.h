@@ -91,4 +91,13 @@ struct DepthwiseParams {
   EpilogueParams epi;
 };
 
+// max_pool2d / global_avg_pool on NHWC activations (pool.cu).
+struct PoolParams {
+  int32_t n, h, w, c, oh, ow, r, s, sh, sw, ph, pw;
+  float scale;  // global_avg_pool factor, float-rounded 1/(H*W)
+  int32_t type, out_type;  // ElemType
+  const void* x;
+  void* y;
+};
+
 }  // namespace tec_sm100

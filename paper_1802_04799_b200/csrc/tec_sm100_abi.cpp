@@ -51,6 +51,8 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
                      const CUtensorMap& tm_y, const ConvHaloParams& p, int grid,
                      cudaStream_t stream);
 int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px, int stage_bytes);
+int launch_max_pool(const PoolParams& p, cudaStream_t st);
+int launch_global_avg_pool(const PoolParams& p, cudaStream_t st);
 }  // namespace tec_sm100
 
 using namespace tec_sm100;
@@ -888,6 +890,77 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
   if (e == -1)
     return fail(TEC_E_LOWERING, "depthwise: unsupported dtype pair or C not a multiple of the vector width");
   if (e) return cuda_fail(e, "depthwise launch");
+  return TEC_OK;
+}
+
+// ------------------------------------------------------------ pooling
+namespace {
+int32_t elem_type_of(int32_t dt) {
+  return dt == TEC_DT_BF16 ? kBF16 : dt == TEC_DT_I8 ? kI8 : dt == TEC_DT_I32 ? kI32 : kF32;
+}
+tec_status pool_check(const tec_pool_desc* d, bool window) {
+  if (!d) return fail(TEC_E_INTERNAL, "null descriptor");
+  if (d->n <= 0 || d->c <= 0 || d->h <= 0 || d->w <= 0)
+    return fail(TEC_E_SHAPE_MISMATCH, "pool: non-positive input shape");
+  if (window) {
+    if (d->r <= 0 || d->s <= 0 || d->stride_h <= 0 || d->stride_w <= 0 || d->pad_h < 0 ||
+        d->pad_w < 0)
+      return fail(TEC_E_SHAPE_MISMATCH, "max_pool2d: bad window/stride/padding");
+    if (d->h + 2 * d->pad_h < d->r || d->w + 2 * d->pad_w < d->s)
+      return fail(TEC_E_SHAPE_MISMATCH, "max_pool2d: window larger than padded input");
+    if (d->pad_h >= d->r || d->pad_w >= d->s)
+      return fail(TEC_E_SHAPE_MISMATCH, "max_pool2d: padding must be smaller than the window");
+  }
+  if (d->n * d->c * d->h * d->w > (int64_t)1 << 40)
+    return fail(TEC_E_SHAPE_MISMATCH, "pool: tensor too large");
+  return TEC_OK;
+}
+}  // namespace
+
+tec_status tec_pool_infer(const tec_pool_desc* d, int64_t out_shape[4]) {
+  tec_status st = pool_check(d, true);
+  if (st) return st;
+  out_shape[0] = d->n;
+  out_shape[1] = d->c;
+  out_shape[2] = (d->h + 2 * d->pad_h - d->r) / d->stride_h + 1;
+  out_shape[3] = (d->w + 2 * d->pad_w - d->s) / d->stride_w + 1;
+  return TEC_OK;
+}
+
+tec_status tec_max_pool2d(const tec_pool_desc* d, const void* x, void* y, void* stream) {
+  int64_t os[4];
+  tec_status st = tec_pool_infer(d, os);
+  if (st) return st;
+  if (d->dtype != d->out_dtype) return fail(TEC_E_LOWERING, "max_pool2d keeps the dtype");
+  if (!x || !y) return fail(TEC_E_INTERNAL, "null buffer");
+  PoolParams p{};
+  p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.c = (int32_t)d->c;
+  p.oh = (int32_t)os[2]; p.ow = (int32_t)os[3];
+  p.r = (int32_t)d->r; p.s = (int32_t)d->s;
+  p.sh = (int32_t)d->stride_h; p.sw = (int32_t)d->stride_w;
+  p.ph = (int32_t)d->pad_h; p.pw = (int32_t)d->pad_w;
+  p.type = p.out_type = elem_type_of(d->dtype);
+  p.x = x; p.y = y;
+  const int e = launch_max_pool(p, (cudaStream_t)stream);
+  if (e == -1) return fail(TEC_E_LOWERING, "max_pool2d: channels x element size must be a multiple of 16 B");
+  if (e) return cuda_fail(e, "max_pool2d launch");
+  return TEC_OK;
+}
+
+tec_status tec_global_avg_pool(const tec_pool_desc* d, const void* x, void* y, void* stream) {
+  tec_status st = pool_check(d, false);
+  if (st) return st;
+  if (!x || !y) return fail(TEC_E_INTERNAL, "null buffer");
+  PoolParams p{};
+  p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.c = (int32_t)d->c;
+  p.oh = p.ow = 1;
+  p.scale = (float)(1.0 / (double)(d->h * d->w));  // scale attr rounded to float (R/src/ops.cpp:260-281)
+  p.type = elem_type_of(d->dtype);
+  p.out_type = elem_type_of(d->out_dtype);
+  p.x = x; p.y = y;
+  const int e = launch_global_avg_pool(p, (cudaStream_t)stream);
+  if (e == -1) return fail(TEC_E_LOWERING, "global_avg_pool: f32/bf16 only, channels x element size a multiple of 16 B");
+  if (e) return cuda_fail(e, "global_avg_pool launch");
   return TEC_OK;
 }
 

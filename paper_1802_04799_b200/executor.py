@@ -1,0 +1,481 @@
+"""Device graph executor: evaluate_graph (R/src/graph.cpp:227-256) for
+target sm100 -- SURVEY 8f.1.
+
+The reference runs a fused node member by member with every intermediate in
+a std::map (R/src/graph.cpp:209-225). Here a graph is compiled ONCE into a
+list of kernel launches on device buffers:
+
+  * fuse_pass (graph.py, R/src/graph_passes.cpp:196-283) groups
+    [conv2d|depthwise_conv2d|matmul, scale?, bias_add?, add?, mul?, relu?]
+    into one node -> ONE fused kernel (tec_conv2d_fused / tec_depthwise_fused;
+    matmul runs as a 1x1 conv over a 1x1 image);
+  * max_pool2d / global_avg_pool -> tec_max_pool2d / tec_global_avg_pool;
+    the reference composition scale(sum(sum(x, 3), 2)) is recognised as a
+    global average pool; flatten of an [N,C,1,1] tensor is an alias;
+  * intermediates live in ONE arena laid out by plan_memory
+    (R/src/graph_passes.cpp:285-329, same greedy best-fit, device byte
+    sizes, 256-B aligned slots); graph inputs and outputs own their buffers;
+  * weights are pre-transformed once (bind_params); activations stay in the
+    kernels' NHWC layout between nodes -- a layout change (NHWC <-> the
+    packed input of the next conv) is inserted only where a consumer needs
+    one (the stem's space-to-depth pack; the f32 parity path's NCHW input);
+  * the launch list is replayed directly or captured into a CUDA graph.
+
+Compute modes: "bf16" (activations bf16 NHWC, f32 accumulate; graph outputs
+f32) and "f32" (the bit-exact SIMT path: every conv equals the reference's
+evaluate_graph bit for bit). Unsupported nodes raise LoweringError -- there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Callable, Dict, List, Optional
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import TecError
+from .graph import ComputeGraph, GraphNode, check_memory_plan, fuse_pass, plan_memory
+
+E_LOWERING, E_IO, E_SHAPE = 15, 5, 2
+_EPI = {"scale": _abi.EPI_SCALE, "bias_add": _abi.EPI_BIAS, "add": _abi.EPI_ADD,
+        "mul": _abi.EPI_MUL, "relu": _abi.EPI_RELU}
+_TORCH = {_abi.DT_F32: torch.float32, _abi.DT_BF16: torch.bfloat16,
+          _abi.DT_I32: torch.int32, _abi.DT_I8: torch.int8}
+_BYTES = {_abi.DT_F32: 4, _abi.DT_BF16: 2, _abi.DT_I32: 4, _abi.DT_I8: 1}
+ALIGN = 256
+
+
+@dataclass
+class DevTensor:
+    """A device tensor of the executor. shape is the LOGICAL (reference)
+    shape; layout "nhwc" stores [N][H][W][C] (rank-2 [N][C] counts as nhwc
+    with H = W = 1), "nchw" the reference row-major order."""
+    buf: torch.Tensor
+    shape: List[int]
+    dtype: int
+    layout: str = "nhwc"
+
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    @property
+    def nchw4(self):
+        s = self.shape
+        return (s[0], s[1], s[2], s[3]) if len(s) == 4 else (s[0], s[1], 1, 1)
+
+
+def _resolve_aliases(g: ComputeGraph) -> ComputeGraph:
+    """The executor's view of a fused graph: nodes that only re-view a
+    buffer are removed and their consumers read the underlying tensor, so
+    plan_memory sees the true lifetimes.
+      * flatten of an [N, C, 1, 1] tensor: same bytes in NHWC;
+      * sum(axis=3) -> sum(axis=2) -> scale(1/(H*W)), each with a single
+        consumer: one global_avg_pool node (the reference composition).
+    The result is internal (node types are kept, not re-validated)."""
+    import copy
+    cons = g.consumers()
+    outs = set(g.outputs)
+    alias: Dict[str, str] = {}
+    gap_of: Dict[str, str] = {}   # scale node id -> pooled input id
+    dropped = set()
+    for a in g.nodes:
+        if a.op != "sum" or int(a.attrs.get("axis", -1)) != 3 or a.id in outs:
+            continue
+        x = g.node(a.inputs[0]).out_type
+        ca = cons.get(a.id, [])
+        if x.rank() != 4 or len(ca) != 1:
+            continue
+        b = g.node(ca[0])
+        cb = cons.get(b.id, [])
+        if b.op != "sum" or int(b.attrs.get("axis", -1)) != 2 or b.id in outs or len(cb) != 1:
+            continue
+        c = g.node(cb[0])
+        if c.op != "scale" or float(c.attrs.get("scale", 1.0)) != 1.0 / (x.shape[2] * x.shape[3]):
+            continue
+        gap_of[c.id] = a.inputs[0]
+        dropped |= {a.id, b.id}
+    shapes = {n.id: n.out_type.shape for n in g.nodes}
+    for n in g.nodes:
+        if n.op == "flatten" and n.id not in outs:
+            src = n.inputs[0]
+            sh = shapes[src]
+            if len(sh) == 4 and sh[2] * sh[3] == 1:
+                alias[n.id] = alias.get(src, src)
+                dropped.add(n.id)
+    out = ComputeGraph([], list(g.outputs))
+    for n in g.nodes:
+        if n.id in dropped:
+            continue
+        m = copy.deepcopy(n)
+        if m.id in gap_of:
+            m.op, m.inputs, m.attrs = "global_avg_pool", [gap_of[m.id]], {}
+        m.inputs = [alias.get(i, i) for i in m.inputs]
+        for mm in m.members:
+            mm.inputs = [alias.get(i, i) for i in mm.inputs]
+        out.nodes.append(m)
+    return out
+
+
+def f32_output(n: GraphNode) -> bool:
+    """Graph outputs kept in f32 in bf16 mode (see DeviceGraph._node_dtype)."""
+    root = n.members[0] if n.op == "fused" else n
+    return root.op in ("matmul", "global_avg_pool", "scale")
+
+
+class DeviceGraph:
+    def __init__(self, g: ComputeGraph, compute: str = "bf16", device: int = 0,
+                 knobs: Optional[Dict[str, dict]] = None):
+        if compute not in ("bf16", "f32"):
+            raise TecError(E_LOWERING, f"executor compute mode '{compute}' (bf16 | f32)")
+        self.lib = _abi.load()
+        self.dev = torch.device("cuda", device)
+        self.compute = compute
+        self.cmode = _abi.COMPUTE_BF16 if compute == "bf16" else _abi.COMPUTE_F32
+        self.act_dt = _abi.DT_BF16 if compute == "bf16" else _abi.DT_F32
+        self.knobs = knobs or {}
+        self.fused = fuse_pass(g)
+        self.g = _resolve_aliases(self.fused)
+        self.outputs = list(self.g.outputs)
+        self._classify_inputs()
+        self.steps: List[Callable[[int], None]] = []
+        self.tensors: Dict[str, DevTensor] = {}
+        self.params: Dict[str, torch.Tensor] = {}
+        self.param_prep: List[Callable[[int], None]] = []
+        self.feeds: Dict[str, DevTensor] = {}
+        self.keep: list = []
+        self._plan()
+        self._compile()
+        self.cuda_graph = None
+
+    # ------------------------------------------------------------ analysis
+    def _classify_inputs(self):
+        """Graph inputs used only as a weight / bias operand are parameters
+        (uploaded and transformed once); the rest are per-run feeds."""
+        uses: Dict[str, set] = {}
+        for n in self.g.nodes:
+            members = n.members if n.op == "fused" else [n]
+            for m in members:
+                for pos, i in enumerate(m.inputs):
+                    role = "data"
+                    if m.op in ("conv2d", "depthwise_conv2d", "matmul") and pos == 1:
+                        role = "weight"
+                    elif m.op == "bias_add" and pos == 1:
+                        role = "bias"
+                    uses.setdefault(i, set()).add(role)
+        self.param_names, self.feed_names = [], []
+        for n in self.g.nodes:
+            if n.op == "const":
+                raise TecError(E_LOWERING, "const nodes: bind them as parameters (inputs)")
+            if n.op != "input":
+                continue
+            u = uses.get(n.id, set())
+            if u and u <= {"weight"} or u == {"bias"}:
+                self.param_names.append(n.id)
+            else:
+                self.feed_names.append(n.id)
+
+    def _node_dtype(self, n: GraphNode) -> int:
+        """bf16 mode: every activation is bf16 (a conv's add/mul operand
+        must share its output dtype); graph outputs of the head (matmul-
+        rooted nodes, pools) are produced in f32."""
+        if n.out_type.dtype == "i32":
+            return _abi.DT_I32
+        return _abi.DT_F32 if n.id in self.outputs and f32_output(n) else self.act_dt
+
+    def _dev_bytes(self, n: GraphNode) -> int:
+        return n.out_type.num_elements() * _BYTES[self._node_dtype(n)]
+
+    def _plan(self):
+        self.plan = plan_memory(self.g, nbytes=self._dev_bytes, align=ALIGN)
+        check_memory_plan(self.g, self.plan, nbytes=self._dev_bytes)
+        self.arena = torch.empty(max(self.plan.total_bytes, ALIGN), dtype=torch.uint8,
+                                 device=self.dev)
+
+    def _out_buffer(self, n: GraphNode, dtype: int, nelem: int) -> torch.Tensor:
+        nbytes = nelem * _BYTES[dtype]
+        if n.id in self.plan.slot_of:
+            off = self.plan.slot_offset[self.plan.slot_of[n.id]]
+            raw = self.arena[off:off + nbytes]
+        else:
+            raw = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        return raw.view(_TORCH[dtype])
+
+    def _scratch(self, nbytes: int) -> torch.Tensor:
+        t = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.dev)
+        self.keep.append(t)
+        return t
+
+    # ------------------------------------------------------------- compile
+    def _compile(self):
+        for n in self.g.nodes:
+            if n.op == "input":
+                if n.id in self.feed_names:
+                    shape = list(n.out_type.shape)
+                    dt = {"f32": _abi.DT_F32, "i32": _abi.DT_I32, "i8": _abi.DT_I8}[n.out_type.dtype]
+                    buf = torch.empty(int(np.prod(shape)), dtype=_TORCH[dt], device=self.dev)
+                    t = DevTensor(buf, shape, dt, "nchw")
+                    self.feeds[n.id] = t
+                    self.tensors[n.id] = t
+                continue
+            if n.op == "fused" or n.op in ("conv2d", "depthwise_conv2d", "matmul"):
+                self._compile_conv(n)
+            elif n.op == "max_pool2d":
+                self._compile_maxpool(n)
+            elif n.op == "global_avg_pool":
+                self._compile_avgpool(n, self.tensors[n.inputs[0]])
+            else:
+                raise TecError(E_LOWERING, f"no sm100 lowering for node '{n.id}' ({n.op})")
+        for o in self.outputs:
+            if o not in self.tensors:
+                raise TecError(E_LOWERING, f"output '{o}' was not produced")
+
+    # ---------------------------------------------------------------- conv
+    def _conv_members(self, n: GraphNode):
+        ms = n.members if n.op == "fused" else [n]
+        root = ms[0]
+        if root.op not in ("conv2d", "depthwise_conv2d", "matmul"):
+            raise TecError(E_LOWERING, f"fused node '{n.id}' is not conv/matmul-rooted")
+        items, prev = [], root.id
+        for m in ms[1:]:
+            if m.op not in _EPI:
+                raise TecError(E_LOWERING, f"member '{m.op}' has no sm100 epilogue")
+            others = [i for i in m.inputs if i != prev]
+            if prev not in m.inputs or len(others) != len(m.inputs) - 1:
+                raise TecError(E_LOWERING, "fused members are not a single chain")
+            if m.op == "bias_add" and int(m.attrs.get("axis", 1)) != 1:
+                raise TecError(E_LOWERING, "bias_add must broadcast over channels")
+            items.append((m.op, others[0] if others else None, m))
+            prev = m.id
+        return root, items
+
+    def _conv_input(self, d: _abi.ConvDesc, src: DevTensor) -> int:
+        """Device pointer of x in the packed layout conv `d` reads,
+        inserting a layout step when the producer's layout differs."""
+        lay = _abi.ConvLayout()
+        _abi.check(self.lib.tec_conv_layout_of(C.byref(d), C.byref(lay)))
+        direct = (src.layout == "nhwc" and src.dtype == lay.act_dtype and lay.cp == d.c
+                  and not (self.cmode == _abi.COMPUTE_F32 and not d.depthwise))
+        if direct:
+            return src.ptr()
+        # src -> NCHW f32 (the reference layout) -> tec_activation_pack
+        if src.layout == "nchw" and src.dtype == _abi.DT_F32:
+            nchw = src.buf
+        else:
+            n_, c_, h_, w_ = src.nchw4
+            nchw = self._scratch(n_ * c_ * h_ * w_ * 4)
+            sdt, sp = src.dtype, src.ptr
+
+            def unpack(st, sp=sp, sdt=sdt, nchw=nchw, shp=(n_, c_, h_, w_)):
+                _abi.check(self.lib.tec_output_unpack(sp(), sdt, nchw.data_ptr(), _abi.DT_F32,
+                                                      *shp, st))
+            self.steps.append(unpack)
+        if self.cmode == _abi.COMPUTE_F32 and not d.depthwise:
+            return nchw.data_ptr()  # the exact path reads NCHW f32 as is
+        packed = self._scratch(lay.act_bytes)
+        dd = d
+
+        def pack(st, nchw=nchw, packed=packed, dd=dd):
+            _abi.check(self.lib.tec_activation_pack(C.byref(dd), nchw.data_ptr(),
+                                                    packed.data_ptr(), st))
+        self.steps.append(pack)
+        return packed.data_ptr()
+
+    def _compile_conv(self, n: GraphNode):
+        root, items = self._conv_members(n)
+        x = self.tensors[root.inputs[0]]
+        wname = root.inputs[1]
+        if wname not in self.param_names:
+            raise TecError(E_LOWERING, f"conv weight '{wname}' must be a graph input parameter")
+        wt = self.g.node(wname).out_type
+        if root.op == "matmul":
+            m_, k_ = x.shape[0], int(np.prod(x.shape[1:]))
+            d = _abi.ConvDesc(n=m_, c=k_, h=1, w=1, k=wt.shape[1], r=1, s=1, stride_h=1,
+                              stride_w=1, pad_h=0, pad_w=0, depthwise=0, compute=self.cmode)
+        else:
+            from .ops import conv_desc
+            d = conv_desc(root.op, self.g.node(root.inputs[0]).out_type.shape, wt.shape,
+                          root.attrs, self.cmode)
+        if self.g.node(root.inputs[0]).out_type.dtype != "f32":
+            raise TecError(E_LOWERING, "executor graphs are f32 (run int8 ops one by one)")
+        xptr = self._conv_input(d, x)
+        lay = _abi.ConvLayout()
+        _abi.check(self.lib.tec_conv_layout_of(C.byref(d), C.byref(lay)))
+        wpk = self._scratch(lay.wt_bytes)
+        self._bind_weight(wname, d, wpk, transpose=root.op == "matmul")
+        out_dt = self._node_dtype(n)
+        oh, ow = (lay.oh, lay.ow)
+        y = self._out_buffer(n, out_dt, d.n * d.k * oh * ow)
+        epi = _abi.Epilogue()
+        for i, (op, other, m) in enumerate(items):
+            epi.ops[i] = _EPI[op]
+            if op == "relu":
+                continue
+            if op == "scale":
+                epi.scale[i] = float(m.attrs.get("scale", 1.0))
+            elif op == "bias_add":
+                if other not in self.param_names:
+                    raise TecError(E_LOWERING, "bias must be a graph input parameter")
+                epi.bias = self._bias_ptr(other)
+            else:
+                r = self.tensors[other]
+                if r.layout != "nhwc" or r.dtype != out_dt:
+                    raise TecError(E_LOWERING, f"'{op}' operand must be an NHWC {out_dt} tensor")
+                if op == "add":
+                    epi.residual = r.ptr()
+                else:
+                    epi.mul_operand = r.ptr()
+        epi.n_ops = len(items)
+        kn = _abi.Knobs(**self.knobs.get(n.id, {}))
+        fn = self.lib.tec_depthwise_fused if d.depthwise else self.lib.tec_conv2d_fused
+        self.keep += [d, epi, kn]
+        yptr = y.data_ptr()
+
+        def launch(st, d=d, epi=epi, kn=kn, xptr=xptr, wpk=wpk, yptr=yptr, out_dt=out_dt):
+            _abi.check(fn(C.byref(d), C.byref(epi), C.byref(kn), xptr, wpk.data_ptr(), yptr,
+                          out_dt, None, st))
+        self.steps.append(launch)
+        shape = list(n.out_type.shape)
+        self.tensors[n.id] = DevTensor(y, shape, out_dt, "nhwc")
+
+    def _bind_weight(self, name: str, d: _abi.ConvDesc, wpk: torch.Tensor, transpose: bool):
+        src_shape = self.g.node(name).out_type.shape
+
+        def prep(params: Dict[str, np.ndarray], st: int, d=d, wpk=wpk):
+            w = np.asarray(params[name], dtype=np.float32)
+            if list(w.shape) != list(src_shape):
+                raise TecError(E_SHAPE, f"parameter '{name}' is {list(w.shape)}, expected {src_shape}")
+            if transpose:  # matmul [K, N] -> OIHW [N, K, 1, 1]
+                w = np.ascontiguousarray(w.T).reshape(w.shape[1], w.shape[0], 1, 1)
+            wd = torch.from_numpy(np.ascontiguousarray(w)).to(self.dev)
+            _abi.check(self.lib.tec_weight_pretransform(C.byref(d), wd.data_ptr(),
+                                                        wpk.data_ptr(), st))
+            torch.cuda.current_stream(self.dev).synchronize()
+        self.param_prep.append(prep)
+
+    def _bias_ptr(self, name: str) -> int:
+        if name not in self.params:
+            k = self.g.node(name).out_type.shape[0]
+            self.params[name] = torch.empty(k, dtype=torch.float32, device=self.dev)
+
+            def prep(params, st, name=name):
+                b = np.asarray(params[name], dtype=np.float32)
+                if b.shape != tuple(self.params[name].shape):
+                    raise TecError(E_SHAPE, f"parameter '{name}' has shape {b.shape}")
+                self.params[name].copy_(torch.from_numpy(b))
+            self.param_prep.append(prep)
+        return self.params[name].data_ptr()
+
+    # ---------------------------------------------------------------- pools
+    def _to_nhwc(self, src: DevTensor) -> DevTensor:
+        if src.layout == "nhwc":
+            return src
+        n_, c_, h_, w_ = src.nchw4
+        out = self._scratch(n_ * c_ * h_ * w_ * _BYTES[self.act_dt]).view(_TORCH[self.act_dt])
+
+        def conv_(st, sp=src.ptr, out=out, shp=(n_, c_, h_, w_), sdt=src.dtype):
+            _abi.check(self.lib.tec_nchw_to_nhwc(sp(), sdt, out.data_ptr(), self.act_dt, *shp, st))
+        self.steps.append(conv_)
+        return DevTensor(out, src.shape, self.act_dt, "nhwc")
+
+    def _compile_maxpool(self, n: GraphNode):
+        x = self._to_nhwc(self.tensors[n.inputs[0]])
+        k = [int(v) for v in n.attrs.get("kernel", [3, 3])]
+        st_ = [int(v) for v in n.attrs.get("strides", [2, 2])]
+        pd = [int(v) for v in n.attrs.get("padding", [1, 1])]
+        nn, c, h, w = x.nchw4
+        pdsc = _abi.PoolDesc(n=nn, c=c, h=h, w=w, r=k[0], s=k[1], stride_h=st_[0],
+                             stride_w=st_[1], pad_h=pd[0], pad_w=pd[1], dtype=x.dtype,
+                             out_dtype=x.dtype)
+        y = self._out_buffer(n, x.dtype, n.out_type.num_elements())
+        if n.id in self.outputs:
+            raise TecError(E_LOWERING, "max_pool2d as a graph output")
+        self.keep.append(pdsc)
+
+        def launch(st, pdsc=pdsc, xp=x.ptr, y=y):
+            _abi.check(self.lib.tec_max_pool2d(C.byref(pdsc), xp(), y.data_ptr(), st))
+        self.steps.append(launch)
+        self.tensors[n.id] = DevTensor(y, list(n.out_type.shape), x.dtype, "nhwc")
+
+    def _compile_avgpool(self, n: GraphNode, src: DevTensor):
+        x = self._to_nhwc(src)
+        nn, c, h, w = x.nchw4
+        out_dt = _abi.DT_F32 if (n.id in self.outputs or self.act_dt == _abi.DT_F32) else self.act_dt
+        pdsc = _abi.PoolDesc(n=nn, c=c, h=h, w=w, r=1, s=1, stride_h=1, stride_w=1,
+                             pad_h=0, pad_w=0, dtype=x.dtype, out_dtype=out_dt)
+        y = self._out_buffer(n, out_dt, nn * c)
+        self.keep.append(pdsc)
+
+        def launch(st, pdsc=pdsc, xp=x.ptr, y=y):
+            _abi.check(self.lib.tec_global_avg_pool(C.byref(pdsc), xp(), y.data_ptr(), st))
+        self.steps.append(launch)
+        self.tensors[n.id] = DevTensor(y, list(n.out_type.shape), out_dt, "nhwc")
+
+    # ------------------------------------------------------------ execution
+    def bind_params(self, params: Dict[str, np.ndarray]) -> None:
+        missing = [p for p in self.param_names if p not in params]
+        if missing:
+            raise TecError(E_IO, f"no value for graph parameter(s) {missing[:4]}")
+        st = torch.cuda.current_stream(self.dev).cuda_stream
+        with torch.cuda.device(self.dev):
+            for prep in self.param_prep:
+                prep(params, st)
+        self.cuda_graph = None
+
+    def set_feed(self, name: str, value, stream: Optional[torch.cuda.Stream] = None) -> None:
+        t = self.feeds[name]
+        v = value if isinstance(value, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(value))
+        if list(v.shape) != t.shape:
+            raise TecError(E_SHAPE, f"input {name} is {list(v.shape)}, expected {t.shape}")
+        t.buf.copy_(v.reshape(-1).to(t.buf.dtype), non_blocking=True)
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Enqueue every step on `stream` (device-resident feeds)."""
+        s = stream or torch.cuda.current_stream(self.dev)
+        if self.cuda_graph is not None:
+            with torch.cuda.stream(s):
+                self.cuda_graph.replay()
+            return
+        for step in self.steps:
+            step(s.cuda_stream)
+
+    def capture(self) -> None:
+        """Capture the launch list into a CUDA graph (replayed by launch)."""
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            for step in self.steps:  # warm-up outside capture (lazy init)
+                step(s.cuda_stream)
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for step in self.steps:
+                step(s.cuda_stream)
+        self.cuda_graph = g
+
+    def output(self, name: str) -> torch.Tensor:
+        """The device output in the reference layout (NCHW / [N, K]), f32."""
+        t = self.tensors[name]
+        shape = t.shape
+        if t.layout == "nhwc" and len(shape) == 4 and shape[2] * shape[3] > 1:
+            n_, c_, h_, w_ = shape
+            out = torch.empty(shape, dtype=torch.float32, device=self.dev)
+            _abi.check(self.lib.tec_output_unpack(t.ptr(), t.dtype, out.data_ptr(), _abi.DT_F32,
+                                                  n_, c_, h_, w_,
+                                                  torch.cuda.current_stream(self.dev).cuda_stream))
+            return out
+        return t.buf[:int(np.prod(shape))].reshape(shape).float()
+
+    def run(self, feeds: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
+        """evaluate_graph(g, feeds) on the device; host arrays in and out."""
+        with torch.cuda.device(self.dev):
+            for name in self.feed_names:
+                if name not in feeds:
+                    raise TecError(E_IO, f"no value for graph input '{name}'")
+                self.set_feed(name, feeds[name])
+            self.launch()
+            outs = {o: self.output(o).cpu().numpy() for o in self.outputs}
+            torch.cuda.current_stream(self.dev).synchronize()
+        return outs

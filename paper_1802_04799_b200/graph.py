@@ -1,0 +1,525 @@
+"""Compute-graph API of the reference (R/include/tec/graph.hpp,
+R/include/tec/graph_passes.hpp), restated for the sm100 executor.
+
+Reference -> here:
+  GraphNode / ComputeGraph          graph.hpp:38-59     -> GraphNode / ComputeGraph
+  ComputeGraph::validate            graph.cpp:83-119    -> ComputeGraph.validate
+  graph_from_json / graph_to_json   graph.cpp:121-207   -> same names, same JSON
+                                                           (base64 const payloads)
+  fuse_pass                         graph_passes.cpp:196-283 -> fuse_pass
+  plan_memory / check_memory_plan   graph_passes.cpp:285-358 -> plan_memory /
+      check_memory_plan (same greedy best-fit; an optional byte-size function
+      and alignment let the device executor plan its bf16 arena)
+  evaluate_graph                    graph.cpp:227-256   -> executor.DeviceGraph
+      (the device executor; there is no host evaluator in the product)
+
+Operator registry (R/src/ops.cpp:196-488): the reference ops keep their
+fusion pattern and type rule. The ResNet-18 graph adds three
+ops the reference lacks: max_pool2d and global_avg_pool (opaque: they never
+join a fused group, so conv -> bias_add -> relu stays one node) and flatten
+(injective; [N,C,1,1] -> [N,C], an alias on the device).
+"""
+from __future__ import annotations
+
+import base64
+import copy
+import json
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._abi import TecError
+
+# ErrorCode numbering of R/include/tec/error.hpp (status = 1 + code).
+E_SHAPE, E_IO, E_NOT_ENOUGH_DATA, E_INTERNAL = 2, 5, 10, 20
+
+INJECTIVE, REDUCTION, COMPLEX, OPAQUE = "injective", "reduction", "complex_out_fusable", "opaque"
+
+DTYPE_BYTES = {"f32": 4, "i32": 4, "i8": 1, "bf16": 2}
+NP_DTYPE = {"f32": "<f4", "i32": "<i4", "i8": "i1"}
+
+
+def _fail(code: int, msg: str):
+    raise TecError(code, msg)
+
+
+@dataclass
+class TensorType:
+    shape: List[int] = field(default_factory=list)
+    dtype: str = "f32"
+
+    def validate(self):
+        if self.dtype not in DTYPE_BYTES:
+            _fail(E_SHAPE, f"unknown dtype {self.dtype}")
+        if any(d <= 0 for d in self.shape):
+            _fail(E_SHAPE, f"non-positive dim in {self.shape}")
+
+    def rank(self) -> int:
+        return len(self.shape)
+
+    def num_elements(self) -> int:
+        n = 1
+        for d in self.shape:
+            n *= d
+        return n
+
+    def num_bytes(self, dtype_bytes: Optional[Dict[str, int]] = None) -> int:
+        return self.num_elements() * (dtype_bytes or DTYPE_BYTES)[self.dtype]
+
+    def __str__(self):
+        return f"{self.dtype}[{','.join(map(str, self.shape))}]"
+
+
+@dataclass
+class GraphNode:
+    """graph.hpp:38-47. op is "input", "const", an operator, or "fused"."""
+    id: str
+    op: str
+    inputs: List[str] = field(default_factory=list)
+    attrs: Dict[str, object] = field(default_factory=dict)
+    out_type: TensorType = field(default_factory=TensorType)
+    data: Optional[np.ndarray] = None
+    members: List["GraphNode"] = field(default_factory=list)
+
+
+# ------------------------------------------------------------ type rules
+def _ints(attrs, key, dflt):
+    v = attrs.get(key, dflt)
+    return [int(x) for x in (v if isinstance(v, (list, tuple)) else [v, v])]
+
+
+def _same_binary(name):
+    def f(ins, attrs):
+        if len(ins) != 2:
+            _fail(E_SHAPE, f"{name} expects 2 inputs")
+        if ins[0].shape != ins[1].shape or ins[0].dtype != ins[1].dtype:
+            _fail(E_SHAPE, f"{name} operands differ: {ins[0]} vs {ins[1]}")
+        return copy.deepcopy(ins[0])
+    return f
+
+
+def _unary(name, float_only):
+    def f(ins, attrs):
+        if len(ins) != 1:
+            _fail(E_SHAPE, f"{name} expects 1 input")
+        if float_only and ins[0].dtype != "f32":
+            _fail(E_SHAPE, f"{name} requires f32 input")
+        return copy.deepcopy(ins[0])
+    return f
+
+
+def _scale(ins, attrs):
+    c = float(attrs.get("scale", 1.0))
+    if ins[0].dtype != "f32" and c != np.floor(c):
+        _fail(E_SHAPE, "integer scale requires an integral factor")
+    return copy.deepcopy(ins[0])
+
+
+def _bias_add(ins, attrs):
+    ax = int(attrs.get("axis", 1 if ins[0].rank() >= 2 else 0))
+    if ax < 0 or ax >= ins[0].rank():
+        _fail(E_SHAPE, "bias_add axis out of range")
+    if ins[1].rank() != 1 or ins[1].shape[0] != ins[0].shape[ax]:
+        _fail(E_SHAPE, f"bias must be rank-1 matching dim {ax}")
+    if ins[0].dtype != ins[1].dtype:
+        _fail(E_SHAPE, "bias dtype differs from data")
+    return copy.deepcopy(ins[0])
+
+
+def _sum(ins, attrs):
+    ax = int(attrs.get("axis", ins[0].rank() - 1))
+    if ax < 0 or ax >= ins[0].rank():
+        _fail(E_SHAPE, "sum axis out of range")
+    shape = [d for i, d in enumerate(ins[0].shape) if i != ax] or [1]
+    return TensorType(shape, ins[0].dtype)
+
+
+def _matmul(ins, attrs):
+    a, b = ins
+    if a.rank() != 2 or b.rank() != 2 or a.shape[1] != b.shape[0]:
+        _fail(E_SHAPE, f"matmul wants [M,K]x[K,N], got {a} x {b}")
+    if a.dtype != b.dtype:
+        _fail(E_SHAPE, "matmul operand dtypes differ")
+    return TensorType([a.shape[0], b.shape[1]], "i32" if a.dtype == "i8" else a.dtype)
+
+
+def _conv(depthwise):
+    name = "depthwise_conv2d" if depthwise else "conv2d"
+
+    def f(ins, attrs):  # infer_conv, R/src/ops.cpp:163-192
+        if len(ins) != 2:
+            _fail(E_SHAPE, f"{name} expects 2 inputs")
+        dt, wt = ins
+        if dt.rank() != 4 or wt.rank() != 4:
+            _fail(E_SHAPE, f"{name} wants NCHW data, OIHW weights")
+        if dt.dtype != wt.dtype:
+            _fail(E_SHAPE, f"{name} operand dtypes differ")
+        st, pd = _ints(attrs, "strides", [1, 1]), _ints(attrs, "padding", [0, 0])
+        if len(st) != 2 or len(pd) != 2:
+            _fail(E_SHAPE, f"{name} strides/padding must be pairs")
+        c = dt.shape[1]
+        if depthwise:
+            if wt.shape[0] != c or wt.shape[1] != 1:
+                _fail(E_SHAPE, f"{name} weights must be [C,1,kh,kw] with C={c}")
+        elif wt.shape[1] != c:
+            _fail(E_SHAPE, f"{name}: weight input-channel dim {wt.shape[1]} != data channels {c}")
+        oh = (dt.shape[2] + 2 * pd[0] - wt.shape[2]) // st[0] + 1
+        ow = (dt.shape[3] + 2 * pd[1] - wt.shape[3]) // st[1] + 1
+        if oh <= 0 or ow <= 0:
+            _fail(E_SHAPE, f"{name}: window larger than input")
+        return TensorType([dt.shape[0], wt.shape[0], oh, ow], "i32" if dt.dtype == "i8" else dt.dtype)
+    return f
+
+
+def _max_pool2d(ins, attrs):
+    x = ins[0]
+    if x.rank() != 4:
+        _fail(E_SHAPE, "max_pool2d wants NCHW data")
+    k = _ints(attrs, "kernel", [3, 3])
+    st, pd = _ints(attrs, "strides", [2, 2]), _ints(attrs, "padding", [1, 1])
+    if pd[0] >= k[0] or pd[1] >= k[1]:
+        _fail(E_SHAPE, "max_pool2d: padding must be smaller than the window")
+    oh = (x.shape[2] + 2 * pd[0] - k[0]) // st[0] + 1
+    ow = (x.shape[3] + 2 * pd[1] - k[1]) // st[1] + 1
+    if oh <= 0 or ow <= 0:
+        _fail(E_SHAPE, "max_pool2d: window larger than input")
+    return TensorType([x.shape[0], x.shape[1], oh, ow], x.dtype)
+
+
+def _global_avg_pool(ins, attrs):
+    x = ins[0]
+    if x.rank() != 4 or x.dtype != "f32":
+        _fail(E_SHAPE, "global_avg_pool wants f32 NCHW data")
+    return TensorType([x.shape[0], x.shape[1], 1, 1], x.dtype)
+
+
+def _flatten(ins, attrs):
+    x = ins[0]
+    if x.rank() < 2:
+        _fail(E_SHAPE, "flatten wants rank >= 2")
+    return TensorType([x.shape[0], int(np.prod(x.shape[1:]))], x.dtype)
+
+
+def _layout_transform(ins, attrs):
+    src, dst = attrs.get("src_layout", "row_major"), attrs.get("dst_layout", "row_major")
+    x = ins[0]
+    if src == "row_major" and dst == "tiled4x4":
+        if x.rank() != 2:
+            _fail(E_SHAPE, "tiled4x4 layout applies to rank-2 tensors")
+        return TensorType([(x.shape[0] + 3) // 4, (x.shape[1] + 3) // 4, 4, 4], x.dtype)
+    if src == "tiled4x4" and dst == "row_major":
+        h, w = int(attrs.get("height", 0)), int(attrs.get("width", 0))
+        if x.rank() != 4 or h <= 0 or w <= 0:
+            _fail(E_SHAPE, "tiled4x4 -> row_major needs a rank-4 source and height/width")
+        return TensorType([h, w], x.dtype)
+    if src == dst:
+        return copy.deepcopy(x)
+    _fail(E_SHAPE, f"unsupported layout pair {src} -> {dst}")
+
+
+# name -> (pattern, arity, infer)
+OPS: Dict[str, Tuple[str, int, Callable]] = {
+    "add": (INJECTIVE, 2, _same_binary("add")),
+    "mul": (INJECTIVE, 2, _same_binary("mul")),
+    "exp": (INJECTIVE, 1, _unary("exp", True)),
+    "sqrt": (INJECTIVE, 1, _unary("sqrt", True)),
+    "relu": (INJECTIVE, 1, _unary("relu", False)),
+    "scale": (INJECTIVE, 1, _scale),
+    "bias_add": (INJECTIVE, 2, _bias_add),
+    "sum": (REDUCTION, 1, _sum),
+    "matmul": (COMPLEX, 2, _matmul),
+    "conv2d": (COMPLEX, 2, _conv(False)),
+    "depthwise_conv2d": (COMPLEX, 2, _conv(True)),
+    "sort": (OPAQUE, 1, _unary("sort", False)),
+    "layout_transform": (INJECTIVE, 1, _layout_transform),
+    # ResNet-18 graph ops (not in the reference registry)
+    "max_pool2d": (OPAQUE, 1, _max_pool2d),
+    "global_avg_pool": (OPAQUE, 1, _global_avg_pool),
+    "flatten": (INJECTIVE, 1, _flatten),
+}
+
+
+def op_def(name: str):
+    if name not in OPS:
+        _fail(E_SHAPE, f"unknown operator '{name}'")
+    return OPS[name]
+
+
+def _infer_node(n: GraphNode, in_types: List[TensorType]) -> TensorType:
+    """graph.cpp:48-81."""
+    if n.op in ("input", "const"):
+        n.out_type.validate()
+        return n.out_type
+    if n.op == "fused":
+        if not n.members:
+            _fail(E_SHAPE, f"fused node {n.id} has no members")
+        env = dict(zip(n.inputs, in_types))
+        last = None
+        for m in n.members:
+            mt = []
+            for i in m.inputs:
+                if i not in env:
+                    _fail(E_SHAPE, f"fused member {m.id} reads unknown tensor {i}")
+                mt.append(env[i])
+            last = op_def(m.op)[2](mt, m.attrs)
+            env[m.id] = last
+        return last
+    pat, arity, infer = op_def(n.op)
+    if len(n.inputs) != arity:
+        _fail(E_SHAPE, f"{n.op} node {n.id} has {len(n.inputs)} inputs, expected {arity}")
+    return infer(in_types, n.attrs)
+
+
+@dataclass
+class ComputeGraph:
+    nodes: List[GraphNode] = field(default_factory=list)  # topologically ordered
+    outputs: List[str] = field(default_factory=list)
+
+    def find(self, nid: str) -> Optional[GraphNode]:
+        for n in self.nodes:
+            if n.id == nid:
+                return n
+        return None
+
+    def node(self, nid: str) -> GraphNode:
+        n = self.find(nid)
+        if n is None:
+            _fail(E_SHAPE, f"graph has no node '{nid}'")
+        return n
+
+    def consumers(self) -> Dict[str, List[str]]:
+        out: Dict[str, List[str]] = {}
+        for n in self.nodes:
+            for i in n.inputs:
+                out.setdefault(i, []).append(n.id)
+        return out
+
+    def validate(self) -> None:
+        """graph.cpp:83-119: unique ids, topological references, outputs,
+        re-inferred types checked against declared ones."""
+        types: Dict[str, TensorType] = {}
+        for n in self.nodes:
+            if n.id in types:
+                _fail(E_SHAPE, f"duplicate node id '{n.id}'")
+            ins = []
+            for i in n.inputs:
+                if i not in types:
+                    _fail(E_SHAPE, f"node {n.id} references '{i}' before its definition")
+                ins.append(types[i])
+            t = _infer_node(n, ins)
+            if n.out_type.shape and (n.out_type.shape != t.shape or n.out_type.dtype != t.dtype):
+                _fail(E_SHAPE, f"node {n.id} declares {n.out_type} but computes {t}")
+            n.out_type = copy.deepcopy(t)
+            if n.op == "const" and n.data is not None and \
+                    list(n.data.shape) != t.shape:
+                _fail(E_SHAPE, f"const {n.id} payload shape {list(n.data.shape)}, declared {t}")
+            types[n.id] = t
+        if not self.outputs:
+            _fail(E_SHAPE, "graph declares no outputs")
+        for o in self.outputs:
+            if o not in types:
+                _fail(E_SHAPE, f"output '{o}' is not a node")
+
+
+# ------------------------------------------------------------- JSON I/O
+def _node_from_json(j: dict) -> GraphNode:
+    n = GraphNode(id=j["id"], op=j["op"], inputs=list(j.get("inputs", [])),
+                  attrs=dict(j.get("attrs", {})))
+    if "shape" in j:
+        n.out_type = TensorType([int(d) for d in j["shape"]], j.get("dtype", "f32"))
+    elif n.op in ("input", "const"):
+        _fail(E_IO, f"node {n.id} needs an explicit shape")
+    if j.get("data"):
+        raw = base64.b64decode(j["data"])
+        n.data = np.frombuffer(raw, dtype=NP_DTYPE[n.out_type.dtype]).reshape(n.out_type.shape).copy()
+    for m in j.get("members", []):
+        n.members.append(_node_from_json(m))
+    return n
+
+
+def _node_to_json(n: GraphNode) -> dict:
+    j = {"id": n.id, "op": n.op, "inputs": list(n.inputs)}
+    if n.attrs:
+        j["attrs"] = {k: (list(v) if isinstance(v, tuple) else v) for k, v in n.attrs.items()}
+    if n.out_type.shape:
+        j["shape"] = list(n.out_type.shape)
+        j["dtype"] = n.out_type.dtype
+    if n.data is not None:
+        j["data"] = base64.b64encode(
+            np.ascontiguousarray(n.data, dtype=NP_DTYPE[n.out_type.dtype]).tobytes()).decode()
+    if n.members:
+        j["members"] = [_node_to_json(m) for m in n.members]
+    return j
+
+
+def graph_from_json(j) -> ComputeGraph:
+    """graph.cpp:189-198 (accepts a dict or JSON text)."""
+    if isinstance(j, (str, bytes)):
+        try:
+            j = json.loads(j)
+        except ValueError:
+            _fail(E_IO, "malformed graph JSON")
+    if not isinstance(j.get("nodes"), list):
+        _fail(E_IO, "graph JSON needs a 'nodes' array")
+    g = ComputeGraph([_node_from_json(n) for n in j["nodes"]], list(j.get("outputs", [])))
+    g.validate()
+    return g
+
+
+def graph_to_json(g: ComputeGraph) -> dict:
+    return {"nodes": [_node_to_json(n) for n in g.nodes], "outputs": list(g.outputs)}
+
+
+# ------------------------------------------------------------- fuse_pass
+def fuse_pass(g: ComputeGraph) -> ComputeGraph:
+    """graph_passes.cpp:196-283: reverse-topological greedy grouping with
+    union-find; a producer joins the single group consuming all its uses
+    when injective -> {injective, reduction} or complex -> injective (the
+    group's anchor becomes complex). Outputs and opaque ops never move."""
+    n = len(g.nodes)
+    index_of = {nd.id: i for i, nd in enumerate(g.nodes)}
+    outputs = set(g.outputs)
+
+    def pattern_of(nd):
+        if nd.op in ("input", "const", "fused"):
+            return None
+        return op_def(nd.op)[0]
+
+    parent = list(range(n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    anchor = [pattern_of(nd) or OPAQUE for nd in g.nodes]
+    cons = g.consumers()
+    for i in range(n - 1, -1, -1):
+        u = g.nodes[i]
+        pu = pattern_of(u)
+        if pu is None or pu == OPAQUE or u.id in outputs:
+            continue
+        cids = cons.get(u.id, [])
+        if not cids:
+            continue
+        groups = {find(index_of[c]) for c in cids}
+        if len(groups) != 1:
+            continue
+        group = groups.pop()
+        if group == find(i):
+            continue
+        ga = anchor[group]
+        nxt = ga
+        if pu == INJECTIVE and ga in (INJECTIVE, REDUCTION):
+            merge = True
+        elif pu == COMPLEX and ga == INJECTIVE:
+            merge, nxt = True, COMPLEX
+        else:
+            merge = False
+        if not merge:
+            continue
+        parent[find(i)] = find(group)
+        anchor[find(i)] = nxt
+
+    groups: Dict[int, List[int]] = {}
+    for i in range(n):
+        groups.setdefault(find(i), []).append(i)
+    out = ComputeGraph([], list(g.outputs))
+    for i in range(n):
+        members = groups[find(i)]
+        if members[-1] != i:
+            continue
+        if len(members) == 1:
+            out.nodes.append(copy.deepcopy(g.nodes[i]))
+            continue
+        internal = {g.nodes[m].id for m in members}
+        fused = GraphNode(id=g.nodes[i].id, op="fused", out_type=copy.deepcopy(g.nodes[i].out_type))
+        for m in members:
+            fused.members.append(copy.deepcopy(g.nodes[m]))
+            for inp in g.nodes[m].inputs:
+                if inp not in internal and inp not in fused.inputs:
+                    fused.inputs.append(inp)
+        out.nodes.append(fused)
+    out.validate()
+    return out
+
+
+# ----------------------------------------------------------- plan_memory
+@dataclass
+class MemoryPlan:
+    slot_of: Dict[str, int] = field(default_factory=dict)
+    slot_bytes: List[int] = field(default_factory=list)
+    total_bytes: int = 0
+    naive_bytes: int = 0
+    slot_offset: List[int] = field(default_factory=list)  # arena offsets (device plan)
+
+
+def plan_memory(g: ComputeGraph, nbytes: Optional[Callable[[GraphNode], int]] = None,
+                align: int = 1) -> MemoryPlan:
+    """graph_passes.cpp:285-329: greedy best-fit slot reuse in execution
+    order; a producer stays live through its last consumer (no in-place
+    update); inputs, consts and graph outputs own their storage.
+    `nbytes` (default: the reference's num_bytes) and `align` let the device
+    executor plan its own arena with the same algorithm."""
+    outputs = set(g.outputs)
+    size = nbytes or (lambda nd: nd.out_type.num_bytes())
+    remaining: Dict[str, int] = {}
+    for nd in g.nodes:
+        for i in nd.inputs:
+            remaining[i] = remaining.get(i, 0) + 1
+    plan = MemoryPlan()
+    free: List[Tuple[int, int]] = []  # sorted (bytes, slot)
+    for nd in g.nodes:
+        if nd.op in ("input", "const"):
+            continue
+        if nd.id not in outputs:
+            need = size(nd)
+            need = (need + align - 1) // align * align
+            plan.naive_bytes += need
+            pick = next((k for k, (b, s) in enumerate(free) if b >= need), None)
+            if pick is not None:
+                slot = free.pop(pick)[1]
+            else:
+                slot = len(plan.slot_bytes)
+                plan.slot_bytes.append(need)
+            plan.slot_of[nd.id] = slot
+        seen = set()
+        for i in nd.inputs:
+            remaining[i] -= 1
+            if remaining[i] == 0 and i in plan.slot_of and i not in seen:
+                s = plan.slot_of[i]
+                free.append((plan.slot_bytes[s], s))
+                free.sort()
+                seen.add(i)
+    off = 0
+    for b in plan.slot_bytes:
+        plan.slot_offset.append(off)
+        off += b
+    plan.total_bytes = off
+    return plan
+
+
+def check_memory_plan(g: ComputeGraph, plan: MemoryPlan,
+                      nbytes: Optional[Callable[[GraphNode], int]] = None) -> None:
+    """graph_passes.cpp:331-358: replay; no operand clobbered before it is
+    read, no slot too small, no node writing its own operand's slot."""
+    size = nbytes or (lambda nd: nd.out_type.num_bytes())
+    content: Dict[int, str] = {}
+    for nd in g.nodes:
+        if nd.op in ("input", "const"):
+            continue
+        for i in nd.inputs:
+            if i not in plan.slot_of:
+                continue
+            if content.get(plan.slot_of[i]) != i:
+                _fail(E_INTERNAL, f"memory plan clobbers '{i}' before node '{nd.id}' reads it")
+        if nd.id in plan.slot_of:
+            s = plan.slot_of[nd.id]
+            if plan.slot_bytes[s] < size(nd):
+                _fail(E_INTERNAL, f"slot too small for '{nd.id}'")
+            for i in nd.inputs:
+                if plan.slot_of.get(i) == s:
+                    _fail(E_INTERNAL, f"node '{nd.id}' would overwrite its own operand")
+            content[s] = nd.id

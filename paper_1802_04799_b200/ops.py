@@ -33,14 +33,8 @@ _EPI_OPS = {"scale": EPI_SCALE, "bias_add": EPI_BIAS, "add": EPI_ADD,
             "mul": EPI_MUL, "relu": EPI_RELU}
 
 
-@dataclass
-class GraphNode:
-    """Mirror of tec::GraphNode (R/include/tec/graph.hpp:38-46)."""
-    id: str
-    op: str
-    inputs: List[str] = field(default_factory=list)
-    attrs: AttrMap = field(default_factory=dict)
-    members: List["GraphNode"] = field(default_factory=list)
+# The graph node type is the reference mirror in graph.py (graph.hpp:38-47).
+from .graph import GraphNode  # noqa: E402
 
 
 def _pair(attrs: AttrMap, key: str, dflt: Sequence[int]) -> List[int]:

@@ -66,3 +66,87 @@ def resnet_layer(name: str, batch: int) -> ConvWorkload:
 def mobilenet_layer(name: str, batch: int) -> ConvWorkload:
     hw, c, s = MOBILENET_DW[name]
     return ConvWorkload(name, batch, c, hw, hw, c, 3, 3, s, 1, depthwise=True)
+
+
+# ------------------------------------------------ ResNet-18 graph (config 4)
+def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
+                   maxpool: bool = True, width: int = 64, head: bool = True):
+    """ResNet-18 inference as a reference-format ComputeGraph (SURVEY 8d
+    config 4): BN folded into each conv's bias, so every conv is
+    conv2d -> bias_add (-> add shortcut) -> relu, which fuse_pass groups
+    into one fused node per conv. Weights and biases are graph inputs
+    (w_<layer>, b_<layer>); the head is global_avg_pool -> flatten ->
+    matmul -> bias_add. `maxpool=False` drops the stem pool (the reference
+    registry has no pooling op; that variant is what the reference's own
+    fuse_pass / plan_memory can be run on) and replaces global_avg_pool by
+    the reference composition scale(sum(sum(x, 3), 2)); `head=False` ends
+    the graph at the last block's relu.
+    Downsample branches are emitted before their block's first conv, so
+    the block's second conv fuses [conv2d, bias_add, add, relu]."""
+    from .graph import ComputeGraph, GraphNode, TensorType
+
+    nodes = []
+
+    def inp(nid, shape):
+        nodes.append(GraphNode(nid, "input", out_type=TensorType(list(shape), "f32")))
+        return nid
+
+    def conv(name, x, cin, cout, k, stride, relu=True, shortcut=None):
+        w = inp(f"w_{name}", (cout, cin, k, k))
+        b = inp(f"b_{name}", (cout,))
+        nodes.append(GraphNode(f"{name}", "conv2d", [x, w],
+                               {"strides": [stride, stride], "padding": [k // 2, k // 2]}))
+        nodes.append(GraphNode(f"{name}_bias", "bias_add", [name, b]))
+        y = f"{name}_bias"
+        if shortcut is not None:
+            nodes.append(GraphNode(f"{name}_add", "add", [y, shortcut]))
+            y = f"{name}_add"
+        if relu:
+            nodes.append(GraphNode(f"{name}_relu", "relu", [y]))
+            y = f"{name}_relu"
+        return y
+
+    x = inp("x", (batch, 3, image, image))
+    y = conv("conv1", x, 3, width, 7, 2)
+    if maxpool:
+        nodes.append(GraphNode("pool1", "max_pool2d", [y],
+                               {"kernel": [3, 3], "strides": [2, 2], "padding": [1, 1]}))
+        y = "pool1"
+    cin = width
+    for stage, (cout, stride) in enumerate([(width, 1), (2 * width, 2), (4 * width, 2),
+                                            (8 * width, 2)], start=1):
+        for blk in range(2):
+            s = stride if blk == 0 else 1
+            pre = f"l{stage}_{blk}"
+            sc = y
+            if s != 1 or cin != cout:
+                sc = conv(f"{pre}_ds", y, cin, cout, 1, s, relu=False)
+            h = conv(f"{pre}_a", y, cin, cout, 3, s)
+            y = conv(f"{pre}_b", h, cout, cout, 3, 1, shortcut=sc)
+            cin = cout
+    if not head:
+        g = ComputeGraph(nodes, [y])
+        g.validate()
+        return g
+    if maxpool:
+        nodes.append(GraphNode("gap", "global_avg_pool", [y]))
+        nodes.append(GraphNode("flat", "flatten", ["gap"]))
+        feat = "flat"
+    else:
+        nodes.append(GraphNode("gap_w", "sum", [y], {"axis": 3}))
+        nodes.append(GraphNode("gap_h", "sum", ["gap_w"], {"axis": 2}))
+        hw = image // 32
+        nodes.append(GraphNode("gap", "scale", ["gap_h"], {"scale": 1.0 / (hw * hw)}))
+        feat = "gap"
+    wfc = inp("w_fc", (cin, num_classes))
+    bfc = inp("b_fc", (num_classes,))
+    nodes.append(GraphNode("fc", "matmul", [feat, wfc]))
+    nodes.append(GraphNode("logits", "bias_add", ["fc", bfc]))
+    g = ComputeGraph(nodes, ["logits"])
+    g.validate()
+    return g
+
+
+# Conv GFLOP per image of resnet18_graph (SURVEY 8d config 4: 1.8136 GMAC
+# conv + 0.512 MMAC FC = 3.628 GFLOP/img).
+RESNET18_GFLOP_PER_IMAGE = 3.628

@@ -188,6 +188,57 @@ def build_case(c):
     print(f"{c['name']}: {status}")
 
 
+# --------------------------------------------------------- whole graphs
+# tests/golden/graphs/<name>/: multi-node reference graphs for the graph
+# passes (fuse_pass + plan_memory -> fused.json) and, when `evaluate`, for
+# the device executor (inputs + out/ from the reference's evaluate_graph).
+def graph_cases():
+    sys.path.insert(0, REPO)
+    from paper_1802_04799_b200.graph import graph_to_json
+    from paper_1802_04799_b200.workloads import resnet18_graph
+    gap = {"nodes": [{"id": "x", "op": "input", "shape": [2, 16, 7, 7], "dtype": "f32"},
+                     {"id": "sw", "op": "sum", "inputs": ["x"], "attrs": {"axis": 3}},
+                     {"id": "sh", "op": "sum", "inputs": ["sw"], "attrs": {"axis": 2}},
+                     {"id": "avg", "op": "scale", "inputs": ["sh"],
+                      "attrs": {"scale": 1.0 / 49}}],
+           "outputs": ["avg"]}
+    fc = {"nodes": [{"id": "x", "op": "input", "shape": [4, 64], "dtype": "f32"},
+                    {"id": "w", "op": "input", "shape": [64, 24], "dtype": "f32"},
+                    {"id": "b", "op": "input", "shape": [24], "dtype": "f32"},
+                    {"id": "mm", "op": "matmul", "inputs": ["x", "w"]},
+                    {"id": "logits", "op": "bias_add", "inputs": ["mm", "b"]}],
+          "outputs": ["logits"]}
+    return [
+        ("gap_chain", gap, True),
+        ("fc_head", fc, True),
+        # ResNet-18 body at width 8 on a 32x32 image (17 convs, residual
+        # adds, downsample branches): evaluated by the reference (~3 s).
+        ("tiny_resnet_body", graph_to_json(resnet18_graph(1, image=32, width=8,
+                                                          maxpool=False, head=False)), True),
+        # Full-size ResNet-18 (reference-compatible variant, batch 8):
+        # graph passes only.
+        ("resnet18_b8", graph_to_json(resnet18_graph(8, maxpool=False)), False),
+    ]
+
+
+def build_graph_case(name, g, evaluate, seed=100):
+    d = os.path.join(HERE, "graphs", name)
+    if os.path.exists(d):
+        shutil.rmtree(d)
+    os.makedirs(os.path.join(d, "out"))
+    with open(os.path.join(d, "graph.json"), "w") as f:
+        json.dump(g, f, indent=1)
+    run([DRIVER, "fuse", os.path.join(d, "graph.json"), os.path.join(d, "fused.json")])
+    if evaluate:
+        for n in g["nodes"]:
+            if n["op"] == "input":
+                seed += 1
+                run([DRIVER, "gen", d, n["id"], n.get("dtype", "f32"), str(seed)] +
+                    [str(v) for v in n["shape"]])
+        run([DRIVER, "eval", os.path.join(d, "graph.json"), d, os.path.join(d, "out")])
+    print(f"graphs/{name}: {'evaluated' if evaluate else 'passes only'}")
+
+
 def main():
     if not os.path.exists(DRIVER):
         sys.exit(f"{DRIVER} missing: run `make -C oracle ref` first")
@@ -195,6 +246,9 @@ def main():
     for c in CASES:
         if not only or c["name"] in only:
             build_case(c)
+    for name, g, ev in graph_cases():
+        if not only or name in only:
+            build_graph_case(name, g, ev)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,100 @@
+"""TEST INFRASTRUCTURE ONLY: evaluate_graph (R/src/graph.cpp:227-256) over a
+fused graph with the oracle restatement (oracle/tec_oracle.c) as the
+arithmetic, to check the device executor.
+
+mode "f32": the reference's own numerics (bit-identical to the reference's
+evaluate_graph -- pinned by tests/test_graph.py against tests/golden/graphs).
+mode "bf16": emulates the executor's bf16 pipeline exactly where it is
+deterministic -- conv/matmul operands rounded to bf16, f32 accumulation in
+the reference order, every activation rounded to bf16 (graph outputs of
+the head -- matmul, pools -- kept in f32, executor.f32_output) -- so the only remaining difference to the device is the
+tensor core's accumulation order.
+"""
+from __future__ import annotations
+
+from typing import Dict
+
+import numpy as np
+
+from oracle.oracle_api import bf16_round, fused_conv, global_avg_pool, max_pool2d
+from paper_1802_04799_b200.executor import f32_output
+
+
+def _epilogue(members, env, prev):
+    items = []
+    for m in members:
+        others = [i for i in m.inputs if i != prev]
+        if m.op == "relu":
+            items.append(("relu",))
+        elif m.op == "scale":
+            items.append(("scale", float(m.attrs.get("scale", 1.0))))
+        else:
+            items.append((m.op, env[others[0]]))
+        prev = m.id
+    return items
+
+
+def evaluate(g, feeds: Dict[str, np.ndarray], params: Dict[str, np.ndarray],
+             mode: str = "f32") -> Dict[str, np.ndarray]:
+    """g: a fuse_pass'ed ComputeGraph (paper_1802_04799_b200.graph)."""
+    rnd = bf16_round if mode == "bf16" else (lambda a: a)
+    outs = set(g.outputs)
+    env = {}
+    env.update({k: np.asarray(v, np.float32) for k, v in feeds.items()})
+    env.update({k: np.asarray(v, np.float32) for k, v in params.items()})
+    cons = g.consumers()
+    gap_src = {}
+    for n in g.nodes:
+        if n.op == "input":
+            continue
+        if n.op == "fused" or n.op in ("conv2d", "depthwise_conv2d", "matmul"):
+            ms = n.members if n.op == "fused" else [n]
+            root = ms[0]
+            x, w = env[root.inputs[0]], env[root.inputs[1]]
+            local = dict(env)
+            items = _epilogue(ms[1:], local, root.id)
+            if root.op == "matmul":
+                xx = x.reshape(x.shape[0], -1, 1, 1)
+                ww = np.ascontiguousarray(w.T)[:, :, None, None]
+                y = fused_conv("conv2d", rnd(xx), rnd(ww), (1, 1), (0, 0),
+                               _reshape_items(items)).reshape(x.shape[0], -1)
+            else:
+                st = tuple(root.attrs.get("strides", (1, 1)))
+                pd = tuple(root.attrs.get("padding", (0, 0)))
+                y = fused_conv(root.op, rnd(x), rnd(w), st, pd, items)
+        elif n.op == "max_pool2d":
+            y = max_pool2d(env[n.inputs[0]], tuple(n.attrs.get("kernel", (3, 3))),
+                           tuple(n.attrs.get("strides", (2, 2))),
+                           tuple(n.attrs.get("padding", (1, 1))))
+        elif n.op == "global_avg_pool":
+            x = env[n.inputs[0]]
+            y = global_avg_pool(x).reshape(x.shape[0], x.shape[1], 1, 1)
+        elif n.op == "flatten":
+            y = env[n.inputs[0]].reshape(n.out_type.shape)
+        elif n.op == "sum":
+            # only as the reference composition scale(sum(sum(x, 3), 2))
+            if int(n.attrs.get("axis", -1)) == 3:
+                gap_src[n.id] = n.inputs[0]
+                y = None
+            else:
+                gap_src[n.id] = gap_src[n.inputs[0]]
+                y = None
+        elif n.op == "scale" and n.inputs[0] in gap_src:
+            y = global_avg_pool(env[gap_src[n.inputs[0]]])
+        else:
+            raise NotImplementedError(n.op)
+        if y is not None and (n.id not in outs or not f32_output(n)):
+            y = rnd(y)
+        env[n.id] = y
+    del cons
+    return {o: env[o] for o in g.outputs}
+
+
+def _reshape_items(items):
+    out = []
+    for it in items:
+        if it[0] in ("add", "mul"):
+            out.append((it[0], it[1].reshape(it[1].shape[0], -1, 1, 1)))
+        else:
+            out.append(it)
+    return out
