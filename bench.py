@@ -432,11 +432,19 @@ def main():
     ap.add_argument("--no-tune", action="store_true", help="library default knobs")
     ap.add_argument("--knobs-in", default="", help="JSON {layer: knobs} to use instead of tuning")
     ap.add_argument("--knobs-out", default="", help="write the tuned knobs here")
+    ap.add_argument("--workload", default="conv",
+                    choices=["conv", "resnet18", "depthwise", "c2b1", "int8"],
+                    help="conv = the headline configs[1]; others: bench_workloads.py")
+    ap.add_argument("--global-batch", type=int, default=0, help="resnet18: total images")
+    ap.add_argument("--dw-compute", default="bf16", choices=["bf16", "f32"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
     if args.impl == "reference":
         impl_reference(args)
+    elif args.workload != "conv":
+        import bench_workloads
+        bench_workloads.WORKLOADS[args.workload](args, sys.modules[__name__])
     else:
         impl_ours(args)
 

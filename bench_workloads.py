@@ -1,0 +1,344 @@
+"""The other SURVEY 8d measurement configs, reached through
+`bench.py --workload <name>` (the default headline stays configs[1], the
+C1-C12 conv step). Each prints ONE JSON line in bench.py's format.
+
+  resnet18   config 4: ResNet-18 inference, global batch 256 sharded over the
+             ranks (strong scaling), img/s; device graph executor, CUDA
+             graph; e2e = H2D of the rank's images + replay + D2H of logits
+             + all_gather of the logits to every rank (the one exchange).
+  depthwise  config 3: MobileNet D1-D9 fused depthwise+bias+relu, batch 64,
+             bf16 (default) or f32; GB/s vs the HBM roofline (replicas).
+  c2b1       config 1: C2 at batch 1, fp32 -- the bit-exact SIMT path and
+             the 3xTF32 tensor-core path; latency (us) per fused layer.
+  int8       config 5: C1-C12 int8 -> i32 at batch 64 (TOPS) plus the
+             sharded tuner's trial throughput.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+import numpy as np
+
+
+def _dist():
+    import torch
+    import torch.distributed as dist
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, ws, local
+
+
+def _max_over_ranks(ms: float) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], device="cuda")
+    if dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier():
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.barrier()
+
+
+def _time_replays(fn, steps, stream):
+    import torch
+    _barrier()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    _barrier()
+    return _max_over_ranks(a.elapsed_time(b))
+
+
+# ------------------------------------------------------------------ resnet18
+def resnet18(args, bench):
+    import torch
+
+    from paper_1802_04799_b200.executor import DeviceGraph
+    from paper_1802_04799_b200.parallel import gather_rows, shard_batch
+    from paper_1802_04799_b200.workloads import RESNET18_GFLOP_PER_IMAGE, resnet18_graph
+
+    rank, ws, local = _dist()
+    gb = args.global_batch or 256
+    start, cnt = shard_batch(gb, ws, rank)
+    g = resnet18_graph(cnt)
+    knobs = _tune_graph_convs(g, local, args) if not args.no_tune else {}
+    dg = DeviceGraph(g, compute="bf16", device=local, knobs=knobs)
+    rng = np.random.default_rng(1234)  # same weights on every rank (replicated)
+    params = {}
+    for n in g.nodes:
+        if n.op == "input" and n.id != "x":
+            shp = n.out_type.shape
+            if n.id.startswith("w_"):
+                fan = int(np.prod(shp[1:])) if len(shp) == 4 else shp[0]
+                params[n.id] = (rng.standard_normal(shp) * np.sqrt(2.0 / fan)).astype(np.float32)
+            else:
+                params[n.id] = rng.uniform(-0.1, 0.1, shp).astype(np.float32)
+    dg.bind_params(params)
+    x_host = torch.from_numpy(
+        np.random.default_rng(rank).uniform(-1, 1, (cnt, 3, 224, 224)).astype(np.float32)
+    ).pin_memory()
+    dg.set_feed("x", x_host)
+    torch.cuda.synchronize()
+    dg.capture()
+    stream = torch.cuda.Stream()
+    for _ in range(args.warmup):
+        dg.launch(stream)
+    torch.cuda.synchronize()
+    with bench.ClockSampler(local) as clk:
+        max_ms = _time_replays(lambda: dg.launch(stream), args.steps, stream)
+    img_s = gb * args.steps / (max_ms / 1e3)
+    gflop_step = RESNET18_GFLOP_PER_IMAGE * cnt
+
+    # e2e: pinned host images -> device, replay, logits -> host, gather.
+    logits = dg.tensors["logits"]
+    out_host = torch.empty((cnt, 1000), dtype=torch.float32).pin_memory()
+    feed = dg.feeds["x"].buf
+
+    def e2e_step():
+        feed.copy_(x_host.reshape(-1), non_blocking=True)
+        dg.launch(torch.cuda.current_stream())
+        full = gather_rows(logits.buf[:cnt * 1000].view(cnt, 1000), gb)
+        out_host.copy_(full[start:start + cnt] if ws > 1 else full, non_blocking=True)
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    _barrier()
+    t0 = time.perf_counter()
+    e_steps = max(3, min(args.steps, 10))
+    for _ in range(e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = _max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps)
+    peak_tf = bench.load_peaks()[0]
+    line = {
+        "metric": "ResNet-18 inference img/s (config 4)", "value": round(img_s, 1),
+        "unit": "img/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"configs[4]: ResNet-18 224x224 inference, global batch {gb} "
+                               f"sharded {cnt}/rank, random-init weights, BN folded",
+                   "global_batch": gb, "parallelism": f"batch-sharded x{ws}, logits gathered",
+                   "timing": "CUDA graph of the whole network per rank, events, max over ranks"},
+        "roofline": {"bound": "tensor", "achieved": round(gflop_step / (max_ms / args.steps), 1),
+                     "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": round(gflop_step / (max_ms / args.steps) / peak_tf, 3),
+                     "traffic": None, "kernel": "all launches of one network step"},
+        "gpu_launches": len(dg.steps) * args.steps,
+        "clocks": clk.summary(),
+        "e2e": {"value": round(gb / (e2e_ms / 1e3), 1), "unit": "img/s",
+                "h2d_bytes_per_step": cnt * 3 * 224 * 224 * 4,
+                "d2h_bytes_per_step": cnt * 1000 * 4, "ms_per_step": round(e2e_ms, 3),
+                "path": "pinned host f32 NCHW -> device, CUDA-graph replay, logits gathered "
+                        "(all_gather) and copied to host"},
+        "cpu_baseline": _resnet_cpu_baseline(bench) if rank == 0 and ws == 1 and
+        not args.no_cpu_baseline else None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def _tune_graph_convs(g, device, args):
+    """Tune each distinct conv shape of the graph once (bf16, bias+relu
+    epilogue as the stand-in cost); returns knobs keyed by fused node id."""
+    from paper_1802_04799_b200 import _abi
+    from paper_1802_04799_b200.graph import fuse_pass
+    from paper_1802_04799_b200.ops import conv_desc
+    from paper_1802_04799_b200.tuner import conv_space, tune
+    f = fuse_pass(g)
+    best, out = {}, {}
+    for n in f.nodes:
+        if n.op != "fused" or n.members[0].op != "conv2d":
+            continue
+        root = n.members[0]
+        xs = f.node(root.inputs[0]).out_type.shape if f.find(root.inputs[0]) else None
+        ws_ = f.node(root.inputs[1]).out_type.shape
+        d = conv_desc("conv2d", xs, ws_, root.attrs, _abi.COMPUTE_BF16)
+        key = (tuple(xs), tuple(ws_), tuple(root.attrs.get("strides", (1, 1))))
+        if key not in best:
+            rec = tune(conv_space(str(key), d), budget=36, batch_size=36, method="random",
+                       devices=[device], repeats=3)
+            best[key] = rec.config if rec else {}
+        out[n.id] = best[key]
+    return out
+
+
+def _resnet_cpu_baseline(bench):
+    """Reference CPU throughput, extrapolated: the reference's fused-conv
+    evaluation rate (MAC/s, measured on bench.py's bounded per-layer
+    sample) applied to ResNet-18's 1.8136 GMAC of conv per image."""
+    if not os.path.exists(bench.REF_DRIVER):
+        return None
+    threads = os.cpu_count() or 1
+    flops, wall, desc = bench.run_reference_sample(threads)
+    img_s = (flops / wall) / (2 * 1.8136e9)
+    return {"value": img_s, "unit": "img/s", "cores": threads, "kind": "reference",
+            "sample": desc + "; extrapolated to ResNet-18 conv MACs per image"}
+
+
+# ----------------------------------------------------------------- depthwise
+def depthwise(args, bench):
+    import torch
+
+    from paper_1802_04799_b200.device import DeviceConv
+    from paper_1802_04799_b200.workloads import MOBILENET_DW, mobilenet_layer
+    rank, ws, local = _dist()
+    batch = args.batch
+    compute = args.dw_compute
+    layers = [DeviceConv(mobilenet_layer(n, batch), compute=compute, device=local, seed=i,
+                         out_dtype=0 if compute == "f32" else None)
+              for i, n in enumerate(MOBILENET_DW)]
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            for l in layers:
+                l.launch(stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for l in layers:
+            l.launch(stream)
+    with bench.ClockSampler(local) as clk:
+        max_ms = _time_replays(graph.replay, args.steps, stream)
+    step_bytes = sum(l.algorithmic_bytes() for l in layers)
+    gbs = ws * step_bytes * args.steps / (max_ms / 1e3) / 1e9
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    per = []
+    for l in layers:
+        ts = []
+        with torch.cuda.stream(stream):
+            for _ in range(10):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                l.launch(stream)
+                b.record(stream)
+                ts.append((a, b))
+        torch.cuda.synchronize()
+        us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ts)
+        byts = l.algorithmic_bytes()
+        per.append({"layer": l.wl.name, "us": round(us, 2), "mbytes": round(byts / 1e6, 2),
+                    "gbs": round(byts / us / 1e3, 1)})
+    hbm = bench.load_peaks()[1]
+    kern_gbs = step_bytes / (sum(p["us"] for p in per) * 1e-6) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "MobileNet D1-D9 fused depthwise GB/s (config 3)", "value": round(gbs, 1),
+            "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": compute, "data": "synthetic",
+            "config": {"workload": f"configs[3]: D1-D9 depthwise 3x3 + bias_add + relu, batch "
+                                   f"{batch}, {compute}", "global_batch": batch * ws,
+                       "parallelism": f"replicas x{ws}"},
+            "roofline": {"bound": "hbm", "achieved": round(kern_gbs, 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(kern_gbs / hbm, 3), "traffic": None},
+            "layers": per, "gpu_launches": len(layers) * args.steps, "clocks": clk.summary(),
+        }), flush=True)
+
+
+# ---------------------------------------------------------------------- c2b1
+def c2b1(args, bench):
+    import torch
+
+    from paper_1802_04799_b200.device import DeviceConv
+    from paper_1802_04799_b200.workloads import resnet_layer
+    rank, ws, local = _dist()
+    wl = resnet_layer("C2", 1)
+    res = {}
+    stream = torch.cuda.Stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for compute in ("f32", "tf32x3", "bf16"):
+        l = DeviceConv(wl, compute=compute, device=local,
+                       out_dtype=None if compute == "bf16" else 0)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                l.launch(stream)
+        ts = []
+        with torch.cuda.stream(stream):
+            for _ in range(max(10, args.steps)):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                l.launch(stream)
+                b.record(stream)
+                ts.append((a, b))
+        torch.cuda.synchronize()
+        us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ts)
+        res[compute] = {"us": round(us, 2), "tflops": round(wl.flops / us / 1e6, 2)}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "C2 batch-1 fused conv latency (config 1)", "value": res["f32"]["us"],
+            "unit": "us", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "configs[0]: C2 x[1,64,56,56] w[64,64,3,3] pad 1 + bias + "
+                                   "relu; L2 flushed before each launch",
+                       "paths": res},
+        }), flush=True)
+
+
+# ---------------------------------------------------------------------- int8
+def int8(args, bench):
+    import torch
+
+    from paper_1802_04799_b200.device import DeviceConv, make_desc
+    from paper_1802_04799_b200.tuner import conv_space, measure
+    from paper_1802_04799_b200.workloads import RESNET18_CONVS, resnet_layer
+    rank, ws, local = _dist()
+    batch = args.batch
+    layers = [DeviceConv(resnet_layer(n, batch), compute="i8", device=local, seed=i)
+              for i, n in enumerate(RESNET18_CONVS)]
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            for l in layers:
+                l.launch(stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        for l in layers:
+            l.launch(stream)
+    with bench.ClockSampler(local) as clk:
+        max_ms = _time_replays(graph.replay, args.steps, stream)
+    ops = sum(l.wl.flops for l in layers)
+    tops = ws * ops * args.steps / (max_ms / 1e3) / 1e12
+    # tuner throughput: the C2 knob grid measured on this GPU
+    space = conv_space("C2_i8", make_desc(resnet_layer("C2", batch), "i8"))
+    cfgs = [space.config_at(i) for i in range(space.size())]
+    t0 = time.perf_counter()
+    recs = measure(space, cfgs, devices=[local], repeats=3)
+    dt = time.perf_counter() - t0
+    ok = [r for r in recs if r.ok()]
+    if rank == 0:
+        print(json.dumps({
+            "metric": "ResNet-18 conv C1-C12 int8 TOPS (config 5)", "value": round(tops, 1),
+            "unit": "TOPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "i8", "data": "synthetic",
+            "config": {"workload": f"configs[5]: C1-C12 int8 x int8 -> i32 + bias + relu, batch "
+                                   f"{batch} (bit-exact path)", "global_batch": batch * ws,
+                       "parallelism": f"replicas x{ws}"},
+            "tuning": {"trials": len(recs), "ok": len(ok), "seconds": round(dt, 2),
+                       "trials_per_s": round(len(recs) / dt, 1),
+                       "best_us": round(min(r.cost for r in ok), 2) if ok else None},
+            "gpu_launches": len(layers) * args.steps, "clocks": clk.summary(),
+        }), flush=True)
+
+
+WORKLOADS = {"resnet18": resnet18, "depthwise": depthwise, "c2b1": c2b1, "int8": int8}

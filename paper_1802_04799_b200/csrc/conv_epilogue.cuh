@@ -472,14 +472,37 @@ __device__ __forceinline__ uint32_t box_off(int row, int chunk) {
     return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-template <int PROG, int ES>
+// kInt: the int8 path -- s32 accumulator + i32 bias in int64 with the
+// reference's i32 range check per member (DenseTensor::set_i,
+// R/include/tec/tensor.hpp:63-69); sets *ovf, stores i32 (ES == 4).
+template <int PROG, int ES, bool kInt = false>
 __device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const uint32_t* bias_s,
-                                              uint32_t box) {
+                                              uint32_t box, bool* ovf = nullptr) {
   uint32_t acc[kChunk];
   tmem_ld32(taddr, acc);
   uint32_t b[kChunk];
   if constexpr (PROG != kProgNone) load_bias32(bias_s, b);
   tmem_ld_wait();
+  if constexpr (kInt) {
+    static_assert(ES == 4, "int8 conv stores i32");
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      int64_t x = static_cast<int32_t>(acc[j]);
+      if constexpr (PROG != kProgNone) {
+        x += static_cast<int32_t>(b[j]);
+        bad |= x < INT32_MIN || x > INT32_MAX;
+      }
+      if constexpr (PROG == kProgBiasRelu) x = x < 0 ? 0 : x;
+      acc[j] = static_cast<uint32_t>(static_cast<int32_t>(x));
+    }
+    if (bad && ovf) *ovf = true;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      sts128(box + box_off<4>(lane, c),
+             make_uint4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]));
+    return;
+  }
   float v[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
@@ -509,10 +532,10 @@ __device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const ui
 // `stage` = this warp's 4 KB (2 bf16 boxes / 1 f32 box, used as a ring;
 // `cnt` counts boxes across calls). `store(box, c0)` runs on lane 0 and
 // issues the TMA store(s) of the box holding columns [c0, c0 + 32).
-template <int PROG, int ES, int BN, typename StoreFn>
+template <int PROG, int ES, int BN, bool kInt, typename StoreFn>
 __device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const uint32_t* bias_s,
                                              uint32_t stage, int valid_cols, uint32_t& cnt,
-                                             StoreFn&& store) {
+                                             bool* ovf, StoreFn&& store) {
   constexpr uint32_t kBox = 32 * 32 * ES;
   constexpr uint32_t kSlots = 4096 / kBox;
 #pragma unroll 1
@@ -520,7 +543,7 @@ __device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const ui
     const uint32_t box = stage + (cnt % kSlots) * kBox;
     if (lane == 0) bulk_wait_read<kSlots - 1>();  // the box's previous store has read it
     __syncwarp();
-    epi_block_box<PROG, ES>(taddr0 + c0, lane, bias_s + c0, box);
+    epi_block_box<PROG, ES, kInt>(taddr0 + c0, lane, bias_s + c0, box, ovf);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {

@@ -291,8 +291,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
-      if constexpr (KIND != MmaKind::kI8) {
+      {
         if (tma_epi) {
+          constexpr bool kInt = KIND == MmaKind::kI8;
           // The GROUP stages the whole tile's virtual rows for one 32-column
           // chunk (MS*128 rows, the row-per-lane writes of its 4 warps), then
           // one thread stores every output row of the band as a 4-D box
@@ -322,10 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               epi::named_bar_sync(1 + grp, 128);
 #pragma unroll 1
               for (int ms = 0; ms < MS; ++ms)
-                epi::epi_block_box<kProg, kES>(
+                epi::epi_block_box<kProg, kES, kInt>(
                     tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0,
                     static_cast<int>(lane), bias_s + c0,
-                    gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB);
+                    gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB,
+                    &overflow);
               fence_proxy_async_smem();
               epi::named_bar_sync(1 + grp, 128);
               if (issuer) {
@@ -336,14 +338,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           };
-          if (p.out_type == kBF16) {
-            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 2>{});
-            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 2>{});
-            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 2>{});
+          using P0 = std::integral_constant<int, epi::kProgNone>;
+          using P1 = std::integral_constant<int, epi::kProgBias>;
+          using P2 = std::integral_constant<int, epi::kProgBiasRelu>;
+          using E2 = std::integral_constant<int, 2>;
+          using E4 = std::integral_constant<int, 4>;
+          if constexpr (kInt) {
+            if (fast == epi::kProgNone) run(P0{}, E4{});
+            else if (fast == epi::kProgBias) run(P1{}, E4{});
+            else run(P2{}, E4{});
+          } else if (p.out_type == kBF16) {
+            if (fast == epi::kProgNone) run(P0{}, E2{});
+            else if (fast == epi::kProgBias) run(P1{}, E2{});
+            else run(P2{}, E2{});
           } else {
-            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 4>{});
-            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 4>{});
-            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 4>{});
+            if (fast == epi::kProgNone) run(P0{}, E4{});
+            else if (fast == epi::kProgBias) run(P1{}, E4{});
+            else run(P2{}, E4{});
           }
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
@@ -447,6 +458,10 @@ TEC_HALO(MmaKind::kF16, 128, 2, 128, 4)
 TEC_HALO(MmaKind::kF16, 256, 1, 128, 4)
 TEC_HALO(MmaKind::kF16, 64, 2, 32, 8)
 TEC_HALO(MmaKind::kF16, 64, 4, 32, 8)
+TEC_HALO(MmaKind::kI8, 64, 1, 128, 6)
+TEC_HALO(MmaKind::kI8, 128, 1, 128, 6)
+TEC_HALO(MmaKind::kI8, 64, 1, 32, 8)
+TEC_HALO(MmaKind::kI8, 64, 1, 64, 6)
 TEC_HALO(MmaKind::kI8, 64, 2, 128, 6)
 TEC_HALO(MmaKind::kI8, 64, 4, 128, 4)
 TEC_HALO(MmaKind::kI8, 128, 2, 128, 4)

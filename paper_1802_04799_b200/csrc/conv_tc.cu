@@ -233,25 +233,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
-      if constexpr (KIND != MmaKind::kI8) {
+      {
         if (tma_epi) {
           // One 2-D box store per 32 columns; rows >= M are clipped.
+          constexpr bool kInt = KIND == MmaKind::kI8;
           auto run = [&](auto prog_c, auto es_c) {
             constexpr int kProg = decltype(prog_c)::value, kES = decltype(es_c)::value;
-            epi::epi_rows_tma<kProg, kES, BN>(
+            epi::epi_rows_tma<kProg, kES, BN, kInt>(
                 tmem_base + ((q * 32) << 16) + acc * BN, static_cast<int>(lane), bias_s,
-                stage_u32, p.oc - n_tile * BN, box_cnt, [&](uint32_t box, int c0) {
+                stage_u32, p.oc - n_tile * BN, box_cnt, &overflow, [&](uint32_t box, int c0) {
                   tma_store_2d(&tm_y, box, n_tile * BN + c0, row0);
                 });
           };
-          if (p.out_type == kBF16) {
-            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 2>{});
-            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 2>{});
-            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 2>{});
+          using P0 = std::integral_constant<int, epi::kProgNone>;
+          using P1 = std::integral_constant<int, epi::kProgBias>;
+          using P2 = std::integral_constant<int, epi::kProgBiasRelu>;
+          using E2 = std::integral_constant<int, 2>;
+          using E4 = std::integral_constant<int, 4>;
+          if constexpr (kInt) {
+            if (fast == epi::kProgNone) run(P0{}, E4{});
+            else if (fast == epi::kProgBias) run(P1{}, E4{});
+            else run(P2{}, E4{});
+          } else if (p.out_type == kBF16) {
+            if (fast == epi::kProgNone) run(P0{}, E2{});
+            else if (fast == epi::kProgBias) run(P1{}, E2{});
+            else run(P2{}, E2{});
           } else {
-            if (fast == epi::kProgNone) run(std::integral_constant<int, epi::kProgNone>{}, std::integral_constant<int, 4>{});
-            else if (fast == epi::kProgBias) run(std::integral_constant<int, epi::kProgBias>{}, std::integral_constant<int, 4>{});
-            else run(std::integral_constant<int, epi::kProgBiasRelu>{}, std::integral_constant<int, 4>{});
+            if (fast == epi::kProgNone) run(P0{}, E4{});
+            else if (fast == epi::kProgBias) run(P1{}, E4{});
+            else run(P2{}, E4{});
           }
           tc_fence_before();
           mbar_arrive(&tempty[acc]);

@@ -264,6 +264,203 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------ 3x3 fast path
+// The MobileNet shape (3x3, stride 1 or 2, float data) with the member
+// programs fuse_pass builds for it (none / bias / bias+relu), all fixed at
+// compile time. A thread owns VEC channels x TW output pixels of one row:
+// per filter row it loads the (TW-1)*SW + 3 input pixels ONCE into
+// registers and reuses them for the three taps of all TW outputs (the
+// generic kernel reloads per tap). Same per-output arithmetic order as the
+// oracle (taps (rh, rw) in order, facc = facc + x*w, float rounding per op;
+// out-of-image taps contribute x = 0 exactly like the reference's select).
+enum DwProg { kDwNone = 0, kDwBias = 1, kDwBiasRelu = 2 };
+
+// Division by a grid-invariant divisor as multiply-high + shift (dividend
+// < 2^31): q = umulhi(n, m) >> s with m = ceil(2^(31+l) / d), l = ceil(log2 d).
+struct FastDiv {
+  uint32_t d, m, s;
+  explicit FastDiv(uint32_t dd) : d(dd), m(0), s(0) {
+    uint32_t l = 0;
+    while ((1u << l) < dd) ++l;
+    const uint64_t p = 31 + l;
+    m = static_cast<uint32_t>(((uint64_t(1) << p) + dd - 1) / dd);
+    s = static_cast<uint32_t>(p - 32);
+  }
+  __device__ __forceinline__ uint32_t divmod(uint32_t n, uint32_t* r) const {
+    const uint32_t q = d == 1 ? n : (__umulhi(n, m) >> s);
+    *r = n - q * d;
+    return q;
+  }
+};
+
+template <typename InT, typename OutT, int TW, int SW, int PROG>
+__global__ void __launch_bounds__(256, 2)
+    dw3x3_kernel(const DepthwiseParams p, const FastDiv div_cg, const FastDiv div_ws,
+                 const FastDiv div_oh) {
+  constexpr int VEC = Vec<InT>::N;
+  constexpr int SPAN = (TW - 1) * SW + 3;
+  // All 9 x C filter taps, converted to f32 once per CTA.
+  extern __shared__ float s_w[];
+  for (int i = threadIdx.x; i < 9 * p.c; i += blockDim.x)
+    s_w[i] = ld_scalar<InT>(p.wt, i);
+  __syncthreads();
+  const uint32_t total = static_cast<uint32_t>(p.n) * p.oh * div_ws.d * div_cg.d;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= total) return;
+  uint32_t t, cg, ws, oh;
+  t = div_cg.divmod(tid, &cg);
+  t = div_ws.divmod(t, &ws);
+  const uint32_t n = div_oh.divmod(t, &oh);
+  const int c0 = static_cast<int>(cg) * VEC;
+  const int ow0 = static_cast<int>(ws) * TW;
+  const int iw0 = ow0 * SW - p.pw;
+  const InT* x = static_cast<const InT*>(p.x);
+
+  float acc[TW][VEC];
+#pragma unroll
+  for (int i = 0; i < TW; ++i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[i][v] = 0.0f;
+
+#pragma unroll
+  for (int rh = 0; rh < 3; ++rh) {
+    const int ih = static_cast<int>(oh) * p.sh + rh - p.ph;
+    const bool row_ok = ih >= 0 && ih < p.h;
+    float wv[3][VEC];
+#pragma unroll
+    for (int rw = 0; rw < 3; ++rw)
+#pragma unroll
+      for (int v = 0; v < VEC; v += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(s_w + (rh * 3 + rw) * p.c + c0 + v);
+        wv[rw][v] = q.x; wv[rw][v + 1] = q.y; wv[rw][v + 2] = q.z; wv[rw][v + 3] = q.w;
+      }
+    const InT* xrow = x + (static_cast<int64_t>(n) * p.h + (row_ok ? ih : 0)) * p.w * p.c + c0;
+    // Stream the row's input columns: column j feeds output i through tap
+    // rw = j - i*SW; for a fixed output the taps arrive in rw order 0,1,2,
+    // so the per-output accumulation order is the reference's.
+#pragma unroll
+    for (int j = 0; j < SPAN; ++j) {
+      const int iw = iw0 + j;
+      float xv[VEC];
+      if (row_ok && iw >= 0 && iw < p.w) {
+        Vec<InT>::load(xrow + static_cast<int64_t>(iw) * p.c, xv);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) xv[v] = 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < TW; ++i) {
+#pragma unroll
+        for (int rw = 0; rw < 3; ++rw) {
+          if (j == i * SW + rw) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              // bf16 x bf16 products are exact in f32 (8-bit mantissas), so
+              // one fused multiply-add rounds exactly like the reference's
+              // facc + (x*w); f32 operands keep the two roundings.
+              if constexpr (std::is_same<InT, __nv_bfloat16>::value)
+                acc[i][v] = __fmaf_rn(xv[v], wv[rw][v], acc[i][v]);
+              else
+                acc[i][v] = __fadd_rn(acc[i][v], __fmul_rn(xv[v], wv[rw][v]));
+            }
+          }
+        }
+      }
+    }
+  }
+  const int oh_i = static_cast<int>(oh);
+
+  float b[VEC];
+  if constexpr (PROG != kDwNone) {
+#pragma unroll
+    for (int v = 0; v < VEC; v += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(static_cast<const float*>(p.epi.bias) + c0 + v);
+      b[v] = q.x; b[v + 1] = q.y; b[v + 2] = q.z; b[v + 3] = q.w;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TW; ++i) {
+    const int ow = ow0 + i;
+    if (ow >= p.ow) break;
+    float o[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float r = acc[i][v];
+      if constexpr (PROG != kDwNone) r = __fadd_rn(r, b[v]);
+      if constexpr (PROG == kDwBiasRelu) r = r < 0.0f ? 0.0f : r;
+      o[v] = r;
+    }
+    const int64_t base = ((static_cast<int64_t>(n) * p.oh + oh_i) * p.ow + ow) * p.c + c0;
+    if constexpr (std::is_same<OutT, __nv_bfloat16>::value) {
+      uint32_t h[VEC / 2];
+#pragma unroll
+      for (int j = 0; j < VEC / 2; ++j) {
+        const __nv_bfloat162 q = __floats2bfloat162_rn(o[2 * j], o[2 * j + 1]);
+        h[j] = *reinterpret_cast<const uint32_t*>(&q);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + base);
+#pragma unroll
+      for (int j = 0; j < VEC / 8; ++j) dst[j] = make_uint4(h[4 * j], h[4 * j + 1], h[4 * j + 2], h[4 * j + 3]);
+    } else {
+      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.y) + base);
+#pragma unroll
+      for (int j = 0; j < VEC / 4; ++j)
+        dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+    }
+  }
+}
+
+// Which compile-time program matches the epilogue (-1: none does).
+int dw_prog_of(const EpilogueParams& e) {
+  if (e.n_ops == 0) return kDwNone;
+  if (e.n_ops == 1 && e.ops[0] == kEpiBias) return kDwBias;
+  if (e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu) return kDwBiasRelu;
+  return -1;
+}
+
+template <typename InT, typename OutT, int TW, int SW>
+int launch_dw3x3(const DepthwiseParams& p, int prog, cudaStream_t st) {
+  constexpr int VEC = Vec<InT>::N;
+  const int64_t total = static_cast<int64_t>(p.n) * p.oh * ((p.ow + TW - 1) / TW) * (p.c / VEC);
+  if (total >= (int64_t(1) << 31)) return 1;  // 32-bit thread index
+  const FastDiv dc(p.c / VEC), dw((p.ow + TW - 1) / TW), dh(p.oh);
+  const unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+  const size_t smem = 9 * static_cast<size_t>(p.c) * sizeof(float);
+  if (smem > 48 * 1024) return 1;
+  switch (prog) {
+    case kDwNone: dw3x3_kernel<InT, OutT, TW, SW, kDwNone><<<blocks, 256, smem, st>>>(p, dc, dw, dh); break;
+    case kDwBias: dw3x3_kernel<InT, OutT, TW, SW, kDwBias><<<blocks, 256, smem, st>>>(p, dc, dw, dh); break;
+    default: dw3x3_kernel<InT, OutT, TW, SW, kDwBiasRelu><<<blocks, 256, smem, st>>>(p, dc, dw, dh); break;
+  }
+  return cudaGetLastError();
+}
+
+// Fast path when applicable; returns 1 if it did not apply.
+int try_dw3x3(const DepthwiseParams& p, int tw, cudaStream_t st) {
+  const int prog = dw_prog_of(p.epi);
+  if (prog < 0 || p.r != 3 || p.s != 3 || (p.sw != 1 && p.sw != 2)) return 1;
+  if (p.in_type == kBF16 && p.c % 8 == 0) {
+    if (p.out_type == kBF16) {
+      if (p.sw == 1) return tw == 2 ? launch_dw3x3<__nv_bfloat16, __nv_bfloat16, 2, 1>(p, prog, st)
+                                    : launch_dw3x3<__nv_bfloat16, __nv_bfloat16, 4, 1>(p, prog, st);
+      return tw == 2 ? launch_dw3x3<__nv_bfloat16, __nv_bfloat16, 2, 2>(p, prog, st)
+                     : launch_dw3x3<__nv_bfloat16, __nv_bfloat16, 4, 2>(p, prog, st);
+    }
+    if (p.out_type == kF32) {
+      if (p.sw == 1) return launch_dw3x3<__nv_bfloat16, float, 4, 1>(p, prog, st);
+      return launch_dw3x3<__nv_bfloat16, float, 4, 2>(p, prog, st);
+    }
+    return 1;
+  }
+  if (p.in_type == kF32 && p.out_type == kF32 && p.c % 4 == 0) {
+    if (p.sw == 1) return tw == 2 ? launch_dw3x3<float, float, 2, 1>(p, prog, st)
+                                  : launch_dw3x3<float, float, 4, 1>(p, prog, st);
+    return tw == 2 ? launch_dw3x3<float, float, 2, 2>(p, prog, st)
+                   : launch_dw3x3<float, float, 4, 2>(p, prog, st);
+  }
+  return 1;
+}
+
 }  // namespace
 
 template <typename InT, typename OutT>
@@ -288,6 +485,10 @@ static int launch_dw(const DepthwiseParams& p, cudaStream_t st) {
 // Returns cudaError_t; -1 when the (in, out) type pair is unsupported or
 // C is not a multiple of the 16-byte vector.
 int launch_depthwise(const DepthwiseParams& p, int tw, cudaStream_t st) {
+  if (tw != 1) {  // knob unroll == 1 selects the generic kernel (diagnostics)
+    const int e = try_dw3x3(p, tw, st);
+    if (e != 1) return e;
+  }
   const int vec = p.in_type == kBF16 ? 8 : p.in_type == kI8 ? 16 : 4;
   if (p.c % vec) {
     if (p.in_type == kBF16 && p.out_type == kBF16)

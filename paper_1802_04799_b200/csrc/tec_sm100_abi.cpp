@@ -133,7 +133,7 @@ void make_store_map(CUtensorMap* tm, void* y, int32_t out_dtype, int rank,
                     const cuuint64_t* dims, int box_px, bool* ok) {
   *ok = false;
   std::memset(tm, 0, sizeof(*tm));
-  if (out_dtype != TEC_DT_BF16 && out_dtype != TEC_DT_F32) return;
+  if (out_dtype != TEC_DT_BF16 && out_dtype != TEC_DT_F32 && out_dtype != TEC_DT_I32) return;
   const int es = out_dtype == TEC_DT_BF16 ? 2 : 4;
   if ((dims[0] * es) % 16 || box_px < 1 || box_px > 256) return;
   cuuint64_t strides[3];
@@ -142,7 +142,9 @@ void make_store_map(CUtensorMap* tm, void* y, int32_t out_dtype, int rank,
   cuuint32_t box[4] = {32, (cuuint32_t)box_px, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = driver_fns().tiled(
-      tm, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+      tm,
+      es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+      : out_dtype == TEC_DT_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
       (cuuint32_t)rank, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
       es == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -337,9 +339,11 @@ const HaloInst kHaloInsts[] = {
     TEC_H(MmaKind::kF16, 64, 4, 128, 4),  TEC_H(MmaKind::kF16, 128, 1, 128, 6),
     TEC_H(MmaKind::kF16, 128, 2, 128, 4), TEC_H(MmaKind::kF16, 256, 1, 128, 4),
     TEC_H(MmaKind::kF16, 64, 2, 32, 8),   TEC_H(MmaKind::kF16, 64, 4, 32, 8),
+    TEC_H(MmaKind::kI8, 64, 1, 128, 6),   TEC_H(MmaKind::kI8, 128, 1, 128, 6),
     TEC_H(MmaKind::kI8, 64, 2, 128, 6),   TEC_H(MmaKind::kI8, 64, 4, 128, 4),
     TEC_H(MmaKind::kI8, 128, 2, 128, 4),  TEC_H(MmaKind::kI8, 256, 1, 128, 4),
     TEC_H(MmaKind::kI8, 64, 2, 64, 6),    TEC_H(MmaKind::kI8, 64, 4, 64, 6),
+    TEC_H(MmaKind::kI8, 64, 1, 32, 8),    TEC_H(MmaKind::kI8, 64, 1, 64, 6),
     TEC_H(MmaKind::kI8, 64, 2, 32, 8),    TEC_H(MmaKind::kI8, 64, 4, 32, 8),
 };
 #undef TEC_H
@@ -357,7 +361,7 @@ struct HaloChoice {
 // max(MMA cycles, L2->SM bytes / 40 B/cycle) -- times the number of waves
 // over the SMs. Returns false when no halo instance fits.
 bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int sms,
-               HaloChoice* out) {
+               int32_t out_dtype, HaloChoice* out) {
   if (d->stride_h != 1 || d->stride_w != 1) return false;
   const int wp = (int)((d->w + 2 * d->pad_w + 1) & ~int64_t(1));  // even: 128-B aligned output rows in the TMA epilogue
   const int es = elem_bytes(pl.act);
@@ -380,6 +384,12 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
     const double mma = 128.0 * hi.ms * hi.bn * ktot * 2 / 8192.0 *
                        (pl.kind == MmaKind::kTF32 ? 2 : pl.kind == MmaKind::kI8 ? 0.5 : 1);
     const double halo_bytes = (double)(th + d->r - 1) * wp * pl.cp * es;
+    // Epilogue term: the group-staged TMA-store path (run_conv_halo) moves
+    // ~48 B/cycle of output, the SIMT fallback ~12 (measured, round 1).
+    const int rowb = 32 * elem_bytes(out_dtype);
+    const bool tma_epi = 2 * hi.ms * 128 * rowb <= kStageMin && (wp * rowb) % 128 == 0;
+    const double epi = (double)th * pl.ow * std::min<int64_t>(hi.bn, d->k) *
+                       elem_bytes(out_dtype) / (tma_epi ? 48.0 : 12.0);
     // knob `stages`: 0 auto, 1 streamed weight ring, 2 resident weights
     for (int res = 0; res < 2; ++res) {
       if (kn && kn->stages == 1 && res) continue;
@@ -398,11 +408,11 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
         if (per_n < 1) continue;
         grid = per_n * n_tiles;
         waves = (double)((spatial + per_n - 1) / per_n);
-        per_tile = std::max(mma, halo_bytes / 40.0);
+        per_tile = std::max(std::max(mma, halo_bytes / 40.0), epi);
       } else {
         grid = (int)std::min<int64_t>(tiles, sms);
         waves = (double)((tiles + sms - 1) / sms);
-        per_tile = std::max(mma, ((double)hi.bn * ktot * es + halo_bytes) / 40.0);
+        per_tile = std::max(std::max(mma, ((double)hi.bn * ktot * es + halo_bytes) / 40.0), epi);
       }
       const double cost = waves * per_tile;
       if (cost < best) {
@@ -487,7 +497,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     const int rowb = 32 * elem_bytes(out_dtype);
     bool ok = false;
     const int cbytes = hc.inst->ms * 128 * rowb;
-    if (pl.kind != MmaKind::kI8 && 2 * cbytes <= kStageMin && (wp * rowb) % 128 == 0)
+    if (2 * cbytes <= kStageMin && (wp * rowb) % 128 == 0)
       make_store_map(&tm_y, y, out_dtype, 4, dims, (int)pl.ow, &ok);
     else std::memset(&tm_y, 0, sizeof(tm_y));
     // Room left in shared memory -> a 2-chunk ring per group, so one chunk
@@ -517,11 +527,11 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     cudaFree(dbg);
     const double ctas = (double)grid;
     std::fprintf(stderr,
-                 "[tec-prof] halo bn=%d ms=%d th=%d wp=%d taps=%d cblocks=%d tiles/cta=%.2f "
+                 "[tec-prof] halo tma_store=%d stage=%d bn=%d ms=%d th=%d wp=%d taps=%d cblocks=%d tiles/cta=%.2f "
                  "cta_cycles=%.0f | prod_wait_empty=%.0f mma_wait_data=%.0f mma_wait_acc=%.0f "
                  "epi_wait_acc=%.0f epi_busy=%.0f | blk_tmem=%.0f blk_ops=%.0f blk_store=%.0f "
                  "(per CTA)\n",
-                 hc.inst->bn, hc.inst->ms, hc.th, wp, (int)(d->r * d->s), p.cblocks,
+                 p.tma_store, p.stage_bytes, hc.inst->bn, hc.inst->ms, hc.th, wp, (int)(d->r * d->s), p.cblocks,
                  h[6] / ctas, h[5] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
                  h[4] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas);
   }
@@ -550,7 +560,7 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   const int64_t path = kn ? kn->tile_k : 0;
   if (path != 1) {
     HaloChoice hc;
-    if (plan_halo(d, pl, kn, sms, &hc))
+    if (plan_halo(d, pl, kn, sms, out_dtype, &hc))
       return run_conv_halo(d, pl, hc, epi, kn, x, w, y, out_dtype, err, st, sms);
     if (path == 2) return fail(TEC_E_LOWERING, "no halo configuration for this conv");
   }
@@ -635,8 +645,7 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   {
     cuuint64_t dims[2] = {(cuuint64_t)d->k, (cuuint64_t)pl.m};
     bool ok = false;
-    if (pl.kind != MmaKind::kI8) make_store_map(&tm_y, y, out_dtype, 2, dims, 32, &ok);
-    else std::memset(&tm_y, 0, sizeof(tm_y));
+    make_store_map(&tm_y, y, out_dtype, 2, dims, 32, &ok);
     p.tma_store = ok && !(kn && kn->vec == 3) ? 1 : 0;  // vec 3: SIMT stores
   }
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
@@ -660,10 +669,10 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     cudaFree(dbg);
     const double ctas = (double)grid;
     std::fprintf(stderr,
-                 "[tec-prof] im2col bn=%d k_iters=%d tiles/cta=%.2f cta_cycles=%.0f | "
+                 "[tec-prof] im2col tma_store=%d bn=%d k_iters=%d tiles/cta=%.2f cta_cycles=%.0f | "
                  "prod_wait_empty=%.0f mma_wait_full=%.0f mma_wait_acc=%.0f "
                  "epi_wait_acc=%.0f epi_busy=%.0f (per CTA)\n",
-                 bn, (int)(d->r * d->s * p.cblocks), h[6] / ctas, h[5] / ctas, h[0] / ctas,
+                 p.tma_store, bn, (int)(d->r * d->s * p.cblocks), h[6] / ctas, h[5] / ctas, h[0] / ctas,
                  h[1] / ctas, h[2] / ctas, h[3] / ctas, h[4] / ctas);
   }
   return TEC_OK;
