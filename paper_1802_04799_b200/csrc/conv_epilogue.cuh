@@ -475,14 +475,13 @@ __device__ __forceinline__ uint32_t box_off(int row, int chunk) {
 // kInt: the int8 path -- s32 accumulator + i32 bias in int64 with the
 // reference's i32 range check per member (DenseTensor::set_i,
 // R/include/tec/tensor.hpp:63-69); sets *ovf, stores i32 (ES == 4).
+// acc: this lane's row, 32 accumulator columns (raw f32 / s32 bits).
 template <int PROG, int ES, bool kInt = false>
-__device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const uint32_t* bias_s,
-                                              uint32_t box, bool* ovf = nullptr) {
-  uint32_t acc[kChunk];
-  tmem_ld32(taddr, acc);
+__device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane,
+                                               const uint32_t* bias_s, uint32_t box,
+                                               bool* ovf = nullptr) {
   uint32_t b[kChunk];
   if constexpr (PROG != kProgNone) load_bias32(bias_s, b);
-  tmem_ld_wait();
   if constexpr (kInt) {
     static_assert(ES == 4, "int8 conv stores i32");
     bool bad = false;
@@ -528,22 +527,35 @@ __device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const ui
   }
 }
 
+template <int PROG, int ES, bool kInt = false>
+__device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const uint32_t* bias_s,
+                                              uint32_t box, bool* ovf = nullptr) {
+  uint32_t acc[kChunk];
+  tmem_ld32(taddr, acc);
+  tmem_ld_wait();
+  epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s, box, ovf);
+}
+
 // One warp's 32 accumulator rows x BN columns through the TMA-store path.
 // `stage` = this warp's 4 KB (2 bf16 boxes / 1 f32 box, used as a ring;
 // `cnt` counts boxes across calls). `store(box, c0)` runs on lane 0 and
 // issues the TMA store(s) of the box holding columns [c0, c0 + 32).
-template <int PROG, int ES, int BN, bool kInt, typename StoreFn>
-__device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const uint32_t* bias_s,
-                                             uint32_t stage, int valid_cols, uint32_t& cnt,
-                                             bool* ovf, StoreFn&& store) {
+// `src(c0, acc)` fills this lane's 32 accumulator columns starting at c0
+// (TMEM, or the split-K partial sums).
+template <int PROG, int ES, int BN, bool kInt, typename SrcFn, typename StoreFn>
+__device__ __forceinline__ void epi_rows_tma_src(SrcFn&& src, int lane, const uint32_t* bias_s,
+                                                 uint32_t stage, int valid_cols, uint32_t& cnt,
+                                                 bool* ovf, StoreFn&& store) {
   constexpr uint32_t kBox = 32 * 32 * ES;
   constexpr uint32_t kSlots = 4096 / kBox;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN && c0 < valid_cols; c0 += kChunk) {
     const uint32_t box = stage + (cnt % kSlots) * kBox;
+    uint32_t acc[kChunk];
+    src(c0, acc);
     if (lane == 0) bulk_wait_read<kSlots - 1>();  // the box's previous store has read it
     __syncwarp();
-    epi_block_box<PROG, ES, kInt>(taddr0 + c0, lane, bias_s + c0, box, ovf);
+    epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s + c0, box, ovf);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -552,6 +564,18 @@ __device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const ui
     }
     ++cnt;
   }
+}
+
+template <int PROG, int ES, int BN, bool kInt, typename StoreFn>
+__device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const uint32_t* bias_s,
+                                             uint32_t stage, int valid_cols, uint32_t& cnt,
+                                             bool* ovf, StoreFn&& store) {
+  epi_rows_tma_src<PROG, ES, BN, kInt>(
+      [&](int c0, uint32_t (&acc)[kChunk]) {
+        tmem_ld32(taddr0 + c0, acc);
+        tmem_ld_wait();
+      },
+      lane, bias_s, stage, valid_cols, cnt, ovf, store);
 }
 
 // Cooperative per-tile bias staging: `nthreads` epilogue threads copy the

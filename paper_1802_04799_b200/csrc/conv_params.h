@@ -49,6 +49,13 @@ struct ConvGemmParams {
   unsigned long long* dbg;
   int32_t epi_mode;     // 0: warp-coalesced epilogue, 1: per-thread rows
   int32_t tma_store;    // 1: y has a TMA store map (fast programs use it)
+  // Split-K (splits > 1): work item = (output tile, split); split s runs
+  // k-iterations [s*kps, min((s+1)*kps, k_iters)), writes its f32 partial
+  // tile to ws, and the last split to arrive (tile_cnt) sums the partials in
+  // split order and runs the epilogue. Requires the TMA-store fast path.
+  int32_t splits, kps;
+  float* ws;            // [m_tiles*n_tiles][splits][128][BN]
+  int32_t* tile_cnt;    // [m_tiles*n_tiles], zero between launches
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA

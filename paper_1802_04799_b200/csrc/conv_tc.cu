@@ -85,8 +85,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  const int splits = p.splits > 1 ? p.splits : 1;
+  const int num_tiles = p.m_tiles * p.n_tiles * splits;  // work items
   const int k_iters = p.r * p.s * p.cblocks;
+  const int kps = splits > 1 ? p.kps : k_iters;  // k-iterations per split
+  const int sc = p.s * p.cblocks;
+  int* s_last = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(full) + 240);  // [2]
   long long dbg_wait[5] = {0, 0, 0, 0, 0};
   const long long t_start = p.dbg ? clock64() : 0;
   constexpr int kCB =
@@ -123,8 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       const int ohw = p.oh * p.ow;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_tile = tile / p.n_tiles;
-        const int n_tile = tile - m_tile * p.n_tiles;
+        const int mn = tile / splits;
+        const int split = tile - mn * splits;
+        const int m_tile = mn / p.n_tiles;
+        const int n_tile = mn - m_tile * p.n_tiles;
         const int m0 = m_tile * kBM;
         const int img = m0 / ohw;
         const int rem = m0 - img * ohw;
@@ -132,25 +138,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ow = rem - oh * p.ow;
         const int w0 = ow * p.sw - p.pw;
         const int h0 = oh * p.sh - p.ph;
-        for (int r = 0; r < p.r; ++r) {
-          for (int s = 0; s < p.s; ++s) {
-            const int kbase = (r * p.s + s) * p.cp;
-            for (int cb = 0; cb < p.cblocks; ++cb) {
-              { const long long t0 = p.dbg ? clock64() : 0;
-                mbar_wait(&empty[stage], phase ^ 1);
-                if (p.dbg) dbg_wait[0] += clock64() - t0; }
-              mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-              tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a,
-                                 &full[stage], cb * kCB, w0, h0, img,
-                                 static_cast<uint16_t>(s),
-                                 static_cast<uint16_t>(r));
-              tma_load_2d(sB + stage * Cfg::kBBytes, &tm_b, &full[stage],
-                          kbase + cb * kCB, n_tile * BN);
-              if (++stage == STAGES) {
-                stage = 0;
-                phase ^= 1;
-              }
-            }
+        const int kb = split * kps, ke = min(k_iters, kb + kps);
+        // k index = (r * S + s) * cblocks + cb, walked incrementally
+        int r = kb / sc, rem_k = kb - r * sc;
+        int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
+        for (int k = kb; k < ke; ++k) {
+          { const long long t0 = p.dbg ? clock64() : 0;
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (p.dbg) dbg_wait[0] += clock64() - t0; }
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a,
+                             &full[stage], cb * kCB, w0, h0, img,
+                             static_cast<uint16_t>(s),
+                             static_cast<uint16_t>(r));
+          tma_load_2d(sB + stage * Cfg::kBBytes, &tm_b, &full[stage],
+                      (r * p.s + s) * p.cp + cb * kCB, n_tile * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++cb == p.cblocks) {
+            cb = 0;
+            if (++s == p.s) { s = 0; ++r; }
           }
         }
       }
@@ -171,7 +180,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.dbg) dbg_wait[2] += clock64() - t0; }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int k = 0; k < k_iters; ++k) {
+        const int kb = (tile % splits) * kps, ke = min(k_iters, kb + kps);
+        for (int k = kb; k < ke; ++k) {
           { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&full[stage], phase);
             if (p.dbg) dbg_wait[1] += clock64() - t0; }
@@ -182,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
             const uint64_t ad = make_smem_desc<SWZ>(a_base + kk * 32, 8 * SWZ);
             const uint64_t bd = make_smem_desc<SWZ>(b_base + kk * 32, 8 * SWZ);
-            tc_mma<KIND>(d_tmem, ad, bd, idesc, (k | kk) != 0 ? 1u : 0u);
+            tc_mma<KIND>(d_tmem, ad, bd, idesc, (k != kb || kk != 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);  // frees the smem slot when MMAs land
           if (++stage == STAGES) {
@@ -218,8 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = local & 1;
       if (acc != grp) continue;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
-      const int m_tile = tile / p.n_tiles;
-      const int n_tile = tile - m_tile * p.n_tiles;
+      const int mn = tile / splits;
+      const int split = tile - mn * splits;
+      const int m_tile = mn / p.n_tiles;
+      const int n_tile = mn - m_tile * p.n_tiles;
       const int row0 = m_tile * kBM + static_cast<int>(q * 32);
       const int row = row0 + static_cast<int>(lane);
       const bool row_ok = row < p.m;
@@ -233,6 +245,74 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
+      if (splits > 1 && tma_epi) {
+        // ---- split-K: publish this split's f32 partial tile, then the last
+        // split of the tile (arrival counter) sums all partials IN SPLIT
+        // ORDER (deterministic) and runs the fused epilogue.
+        // Partial layout [item][warp q][chunk][column j][lane]: for a fixed
+        // register j the 32 lanes write one contiguous 128-byte line.
+        const uint32_t taddr = tmem_base + ((q * 32) << 16) + acc * BN;
+        float* mine = p.ws + ((static_cast<size_t>(mn) * splits + split) * 4 + q) * 32 * BN + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += kChunk) {
+          uint32_t v[kChunk];
+          tmem_ld32(taddr + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) __stcg(mine + (c0 + j) * 32, __uint_as_float(v[j]));
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);  // TMEM free: the partial lives in ws now
+        __threadfence();
+        epi::named_bar_sync(1 + grp, 128);
+        if (gtid == 0) s_last[grp] = atomicAdd(&p.tile_cnt[mn], 1) == splits - 1;
+        epi::named_bar_sync(1 + grp, 128);
+        if (s_last[grp]) {
+          __threadfence();
+          const float* part = p.ws + (static_cast<size_t>(mn) * splits * 4 + q) * 32 * BN + lane;
+          const size_t pstride = static_cast<size_t>(4) * 32 * BN;  // one split's tile
+          auto src = [&](int c0, uint32_t (&a)[epi::kChunk]) {
+            float f[epi::kChunk];
+#pragma unroll
+            for (int j = 0; j < epi::kChunk; ++j) f[j] = __ldcg(part + (c0 + j) * 32);
+#pragma unroll 1
+            for (int sp = 1; sp < splits; ++sp) {
+#pragma unroll
+              for (int j = 0; j < epi::kChunk; ++j)
+                f[j] = __fadd_rn(f[j], __ldcg(part + sp * pstride + (c0 + j) * 32));
+            }
+#pragma unroll
+            for (int j = 0; j < epi::kChunk; ++j) a[j] = __float_as_uint(f[j]);
+          };
+          if constexpr (KIND != MmaKind::kI8) {
+            auto run = [&](auto prog_c, auto es_c) {
+              constexpr int kProg = decltype(prog_c)::value, kES = decltype(es_c)::value;
+              epi::epi_rows_tma_src<kProg, kES, BN, false>(
+                  src, static_cast<int>(lane), bias_s, stage_u32, p.oc - n_tile * BN, box_cnt,
+                  &overflow, [&](uint32_t box, int c0) {
+                    tma_store_2d(&tm_y, box, n_tile * BN + c0, row0);
+                  });
+            };
+            using P0 = std::integral_constant<int, epi::kProgNone>;
+            using P1 = std::integral_constant<int, epi::kProgBias>;
+            using P2 = std::integral_constant<int, epi::kProgBiasRelu>;
+            using E2 = std::integral_constant<int, 2>;
+            using E4 = std::integral_constant<int, 4>;
+            if (p.out_type == kBF16) {
+              if (fast == epi::kProgNone) run(P0{}, E2{});
+              else if (fast == epi::kProgBias) run(P1{}, E2{});
+              else run(P2{}, E2{});
+            } else {
+              if (fast == epi::kProgNone) run(P0{}, E4{});
+              else if (fast == epi::kProgBias) run(P1{}, E4{});
+              else run(P2{}, E4{});
+            }
+          }
+          if (gtid == 0) p.tile_cnt[mn] = 0;  // ready for the next launch
+        }
+        if (p.dbg) dbg_wait[4] += clock64() - tw1;
+        continue;
+      }
       {
         if (tma_epi) {
           // One 2-D box store per 32 columns; rows >= M are clipped.

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -538,6 +539,47 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   return TEC_OK;
 }
 
+// The epilogue programs with a compile-time fast path (epi::classify_prog).
+bool fast_program(const EpilogueParams& e) {
+  if (e.n_ops == 0) return true;
+  if (e.n_ops == 1) return e.ops[0] == kEpiBias;
+  return e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu;
+}
+
+// Per-device split-K scratch: f32 partial tiles + per-tile arrival counters
+// (zeroed once; the kernel resets each counter after use). Grows on demand;
+// growing is a synchronous allocation, so it must happen outside a CUDA-graph
+// capture (the first eager launch of a shape takes care of that).
+tec_status splitk_workspace(int dev, size_t bytes, size_t tiles, cudaStream_t st, float** ws,
+                            int32_t** cnt) {
+  struct Scratch { float* ws = nullptr; size_t bytes = 0; int32_t* cnt = nullptr; size_t n = 0; };
+  static std::mutex mu;
+  static std::map<int, Scratch> per_dev;
+  std::lock_guard<std::mutex> lock(mu);
+  Scratch& sc = per_dev[dev];
+  if (sc.bytes < bytes || sc.n < tiles) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(TEC_E_LOWERING, "split-K workspace must be sized by an eager launch before capture");
+    TEC_CUDA(cudaStreamSynchronize(st));
+    if (sc.bytes < bytes) {
+      if (sc.ws) cudaFree(sc.ws);
+      TEC_CUDA(cudaMalloc(&sc.ws, bytes));
+      sc.bytes = bytes;
+    }
+    if (sc.n < tiles) {
+      if (sc.cnt) cudaFree(sc.cnt);
+      TEC_CUDA(cudaMalloc(&sc.cnt, tiles * sizeof(int32_t)));
+      TEC_CUDA(cudaMemset(sc.cnt, 0, tiles * sizeof(int32_t)));
+      sc.n = tiles;
+    }
+  }
+  *ws = sc.ws;
+  *cnt = sc.cnt;
+  return TEC_OK;
+}
+
 tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
                     const EpilogueParams& epi, const tec_knobs* kn,
                     const void* x, const void* w, void* y, int32_t out_dtype,
@@ -558,7 +600,9 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   // Path: knob tile_k selects the A-operand strategy -- 0 auto, 1 im2col
   // TMA (conv_tc.cu), 2 shifted-window halo (conv_halo.cu, stride 1 only).
   const int64_t path = kn ? kn->tile_k : 0;
-  if (path != 1) {
+  if (path == 2 && kn && kn->split_k > 1)
+    return fail(TEC_E_LOWERING, "split_k applies to the im2col path (tile_k=1)");
+  if (path != 1 && !(kn && kn->split_k > 1)) {
     HaloChoice hc;
     if (plan_halo(d, pl, kn, sms, out_dtype, &hc))
       return run_conv_halo(d, pl, hc, epi, kn, x, w, y, out_dtype, err, st, sms);
@@ -568,10 +612,10 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
 
   // tile_n knob: the "split" of the OC axis.
   int bn = kn && kn->tile_n ? static_cast<int>(kn->tile_n) : 0;
-  if (!bn) {
+  if (!bn) {  // widest tile that still gives ~0.6 x #SMs output tiles
     bn = d->k >= 256 ? 256 : d->k >= 128 ? 128 : 64;
     if (pl.swz != 128) bn = 64;
-    while (bn > 64 && m_tiles * ((d->k + bn - 1) / bn) < 2 * sms) bn /= 2;
+    while (bn > 64 && m_tiles * ((d->k + bn - 1) / bn) * 5 < 3 * sms) bn /= 2;
   }
   Launcher launch = pick_launcher(pl.kind, bn, pl.swz);
   if (!launch)
@@ -649,7 +693,29 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     p.tma_store = ok && !(kn && kn->vec == 3) ? 1 : 0;  // vec 3: SIMT stores
   }
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
-  int grid = (int)std::min<int64_t>(tiles, sms);
+  // Split-K (knob split_k; 0 = auto): more work items when the output has
+  // fewer tiles than SMs (small-image, deep-K layers). Only on the TMA-store
+  // fast programs of the float kinds.
+  p.splits = 1;
+  {
+    const int k_iters = (int)(d->r * d->s * p.cblocks);
+    const bool able = pl.kind != MmaKind::kI8 && p.tma_store && fast_program(epi);
+    int want = kn && kn->split_k > 0 ? (int)kn->split_k : 0;
+    if (want > 1 && !able)
+      return fail(TEC_E_LOWERING, "split_k needs a float conv with a none/bias/bias+relu epilogue");
+    // No automatic split: measured slower than more, narrower tiles on
+    // every ResNet layer (the partials round-trip through L2), and it would
+    // make results depend on the batch size. The tuner explores split_k.
+    if (want > 1) {
+      if (want > k_iters) want = k_iters;
+      p.splits = want;
+      p.kps = (k_iters + want - 1) / want;
+      tec_status wst = splitk_workspace(dev, (size_t)tiles * want * 128 * bn * sizeof(float),
+                                        (size_t)tiles, st, &p.ws, &p.tile_cnt);
+      if (wst) return wst;
+    }
+  }
+  int grid = (int)std::min<int64_t>(tiles * p.splits, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
   // TEC_SM100_PROFILE=1: per-role pipeline wait breakdown on stderr
   // (synchronises the stream; diagnostics only).
@@ -1060,7 +1126,9 @@ tec_status tec_measure(const tec_conv_desc* d, const tec_epilogue* epi,
   tec_conv_layout lay;
   if ((st = tec_conv_layout_of(d, &lay))) return st;
   const bool integer = d->compute == TEC_COMPUTE_I8;
-  const int32_t out_t = integer ? TEC_DT_I32 : TEC_DT_BF16;
+  const int32_t out_t = integer ? TEC_DT_I32
+                        : d->compute == TEC_COMPUTE_F32 || d->compute == TEC_COMPUTE_TF32X3
+                            ? TEC_DT_F32 : TEC_DT_BF16;
   void *x = nullptr, *w = nullptr, *y = nullptr, *b = nullptr, *r = nullptr, *fl = nullptr;
   const size_t flush_bytes = 256ull << 20;
   cudaStream_t s;

@@ -39,7 +39,7 @@ from . import _abi
 from ._abi import TecError
 from .graph import ComputeGraph, GraphNode, check_memory_plan, fuse_pass, plan_memory
 
-E_LOWERING, E_IO, E_SHAPE = 15, 5, 2
+E_LOWERING, E_IO, E_SHAPE = 15, 20, 2
 _EPI = {"scale": _abi.EPI_SCALE, "bias_add": _abi.EPI_BIAS, "add": _abi.EPI_ADD,
         "mul": _abi.EPI_MUL, "relu": _abi.EPI_RELU}
 _TORCH = {_abi.DT_F32: torch.float32, _abi.DT_BF16: torch.bfloat16,

@@ -32,7 +32,7 @@ import numpy as np
 from ._abi import TecError
 
 # ErrorCode numbering of R/include/tec/error.hpp (status = 1 + code).
-E_SHAPE, E_IO, E_NOT_ENOUGH_DATA, E_INTERNAL = 2, 5, 10, 20
+E_SHAPE, E_IO, E_NOT_ENOUGH_DATA, E_INTERNAL = 2, 20, 19, 21
 
 INJECTIVE, REDUCTION, COMPLEX, OPAQUE = "injective", "reduction", "complex_out_fusable", "opaque"
 
@@ -523,3 +523,41 @@ def check_memory_plan(g: ComputeGraph, plan: MemoryPlan,
                 if plan.slot_of.get(i) == s:
                     _fail(E_INTERNAL, f"node '{nd.id}' would overwrite its own operand")
             content[s] = nd.id
+
+
+# ------------------------------------------------------- tensor artifacts
+def save_tensor(directory: str, name: str, arr: np.ndarray, dtype: Optional[str] = None) -> None:
+    """save_tensor (R/src/io.cpp:111-119): <name>.json manifest {name, shape,
+    dtype} + <name>.bin raw little-endian payload (i8 one byte/element)."""
+    import os
+    dtype = dtype or {np.dtype(np.float32): "f32", np.dtype(np.int32): "i32",
+                      np.dtype(np.int8): "i8"}.get(arr.dtype)
+    if dtype not in NP_DTYPE:
+        _fail(E_IO, f"cannot save dtype {arr.dtype}")
+    os.makedirs(directory, exist_ok=True)
+    with open(os.path.join(directory, name + ".json"), "w") as f:
+        json.dump({"name": name, "shape": [int(d) for d in arr.shape], "dtype": dtype}, f, indent=2)
+        f.write("\n")
+    with open(os.path.join(directory, name + ".bin"), "wb") as f:
+        f.write(np.ascontiguousarray(arr, dtype=NP_DTYPE[dtype]).tobytes())
+
+
+def load_tensor(directory: str, name: str) -> np.ndarray:
+    """load_tensor (R/src/io.cpp:121-127); IOError on a missing or
+    malformed manifest / a payload of the wrong size."""
+    import os
+    try:
+        with open(os.path.join(directory, name + ".json")) as f:
+            man = json.load(f)
+        with open(os.path.join(directory, name + ".bin"), "rb") as f:
+            raw = f.read()
+    except (OSError, ValueError) as e:
+        _fail(E_IO, f"cannot load tensor '{name}' from {directory}: {e}")
+    dt = man.get("dtype", "f32")
+    if dt not in NP_DTYPE:
+        _fail(E_IO, f"unknown dtype '{dt}' in {name}.json")
+    shape = [int(d) for d in man["shape"]]
+    a = np.frombuffer(raw, dtype=NP_DTYPE[dt])
+    if a.size != int(np.prod(shape)):
+        _fail(E_IO, f"{name}.bin holds {a.size} elements, manifest says {shape}")
+    return a.reshape(shape).astype({"f32": np.float32, "i32": np.int32, "i8": np.int8}[dt])

@@ -129,10 +129,83 @@ def conv_space(name: str, desc: _abi.ConvDesc,
     """The B200 conv template's knob grid (SURVEY 8a knob mapping):
     tile_k = A-operand strategy (1 im2col TMA, 2 shifted-window halo),
     tile_n = CTA N tile (split of the OC axis), tile_m = M rows per tile
-    (halo: MMA sub-tiles x 128)."""
+    (halo: MMA sub-tiles x 128), stages (halo: 1 streamed / 2 resident
+    weights), split_k (im2col: K split over CTAs, partials summed in order)."""
     knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
-             KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2])]
+             KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2]),
+             KnobDef("split_k", [1, 2, 3, 4])]
     return KnobSpace(name, knobs, desc, tuple(epilogue))
+
+
+def dw_space(name: str, desc: _abi.ConvDesc,
+             epilogue: Sequence[int] = (_abi.EPI_BIAS, _abi.EPI_RELU)) -> KnobSpace:
+    """The depthwise template's knobs: unroll = output columns per thread
+    (1 selects the generic kernel; 2 / 4 the 3x3 column-streaming kernel)."""
+    if not desc.depthwise:
+        raise _abi.TecError(15, "dw_space needs a depthwise descriptor")
+    return KnobSpace(name, [KnobDef("unroll", [1, 2, 4])], desc, tuple(epilogue))
+
+
+# ------------------------------------------------ Config <-> schedule log
+# The reference records a schedule as a JSON list of primitive applications
+# (R/src/schedule.cpp:456-491, Schedule::apply_log_entry). A B200 Config is
+# the same decision in template form (SURVEY 8a knob mapping); these two
+# functions translate between them so trial DBs and schedule logs interoperate.
+_INTRIN = {_abi.COMPUTE_BF16: "sm100.umma.bf16", _abi.COMPUTE_TF32X3: "sm100.umma.tf32",
+           _abi.COMPUTE_I8: "sm100.umma.i8", _abi.COMPUTE_F32: "sm100.simt.f32"}
+
+
+def schedule_log(cfg: Config, desc: _abi.ConvDesc, stage: str = "conv") -> List[dict]:
+    log = []
+    if cfg.get("tile_n"):
+        log.append({"prim": "split", "stage": stage, "axis": "ff", "factor": int(cfg["tile_n"])})
+    if cfg.get("tile_m"):
+        log.append({"prim": "split", "stage": stage, "axis": "nyx", "factor": int(cfg["tile_m"])})
+    if cfg.get("split_k", 1) > 1:
+        log.append({"prim": "split", "stage": stage, "axis": "rc", "factor": int(cfg["split_k"])})
+    src = {1: "im2col", 2: "halo"}.get(int(cfg.get("tile_k", 0)), "auto")
+    log.append({"prim": "cache_read", "src": f"data.{src}", "scope": "shared", "readers": [stage]})
+    if cfg.get("stages"):
+        log.append({"prim": "cache_read", "src": "weight." + ("resident" if cfg["stages"] == 2
+                                                           else "streamed"),
+                    "scope": "shared", "readers": [stage]})
+    log.append({"prim": "set_scope", "stage": stage, "scope": "accel.accum"})
+    log.append({"prim": "tensorize", "stage": stage, "axis": "nyx.inner",
+                "intrin": _INTRIN.get(desc.compute, "sm100.umma.bf16")})
+    if cfg.get("unroll"):
+        log.append({"prim": "unroll", "stage": stage, "axis": f"xx.{int(cfg['unroll'])}"})
+    if cfg.get("grid"):
+        log.append({"prim": "bind", "stage": stage, "axis": f"nyx.outer.{int(cfg['grid'])}",
+                    "tag": "blockIdx.x"})
+    return log
+
+
+def config_from_schedule_log(log: Sequence[dict]) -> Config:
+    """Inverse of schedule_log; unknown primitives are an IOError, as in
+    apply_log_entry."""
+    cfg: Config = {}
+    for e in log:
+        prim = e.get("prim")
+        if prim == "split":
+            key = {"ff": "tile_n", "nyx": "tile_m", "rc": "split_k"}.get(e.get("axis"))
+            if key is None:
+                raise _abi.TecError(20, f"split of unknown axis {e.get('axis')}")
+            cfg[key] = int(e["factor"])
+        elif prim == "cache_read":
+            s = e.get("src", "")
+            if s.startswith("data."):
+                cfg["tile_k"] = {"im2col": 1, "halo": 2}.get(s[5:], 0)
+            elif s.startswith("weight."):
+                cfg["stages"] = 2 if s.endswith("resident") else 1
+        elif prim == "unroll":
+            cfg["unroll"] = int(e["axis"].split(".")[-1])
+        elif prim == "bind":
+            cfg["grid"] = int(e["axis"].split(".")[-1])
+        elif prim in ("set_scope", "tensorize"):
+            continue
+        else:
+            raise _abi.TecError(20, f"unknown schedule primitive '{prim}'")
+    return cfg
 
 
 def _measure_one(space: KnobSpace, cfg: Config, device: int, warmup: int,

@@ -215,3 +215,27 @@ def test_halo_tile_shapes(tile_m, stages):
         pytest.skip(str(e))
     want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), (1, 1), (2, 2), epi)
     assert same_values(y, want, TOL_BF16)
+
+
+@pytest.mark.parametrize("split_k", [2, 3, 4])
+@pytest.mark.parametrize("layer", ["C7", "C10", "C12"])
+def test_split_k_matches_oracle_and_is_deterministic(layer, split_k):
+    hw, c, k, r, s = RESNET18_CONVS[layer]
+    x, w, b = _inputs((2, c, hw, hw), (k, c, r, r), k, False, seed=31 + split_k)
+    attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+    epi = [("bias_add", b), ("relu",)]
+    kn = {"tile_k": 1, "tile_n": 128, "split_k": split_k}
+    y = fused_conv("conv2d", x, w, attrs, epi, knobs=kn, compute="bf16")
+    want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), attrs["strides"],
+                       attrs["padding"], epi)
+    assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
+    assert np.array_equal(bits(y), bits(fused_conv("conv2d", x, w, attrs, epi, knobs=kn,
+                                                  compute="bf16")))
+
+
+def test_split_k_on_halo_path_is_a_lowering_error():
+    x, w, b = _inputs((1, 64, 8, 8), (64, 64, 3, 3), 64, False, 1)
+    with pytest.raises(TecError) as e:
+        fused_conv("conv2d", x, w, {"padding": (1, 1)}, [], knobs={"tile_k": 2, "split_k": 2},
+                   compute="bf16")
+    assert e.value.code == "LoweringError"

@@ -125,3 +125,33 @@ def test_graph_oracle_matches_reference_eval(name):
     for o in g.outputs:
         want = load_tensor(os.path.join(d, "out"), o)
         assert np.array_equal(got[o].reshape(want.shape).view(np.uint32), want.view(np.uint32)), o
+
+
+def test_tensor_io_reads_reference_files_and_round_trips(tmp_path):
+    from paper_1802_04799_b200.graph import load_tensor as gl, save_tensor as gs
+    d = os.path.join(GRAPHS, "tiny_resnet_body")
+    x = gl(d, "x")
+    assert x.dtype == np.float32 and np.array_equal(x, load_tensor(d, "x"))
+    for arr in (x, np.arange(-5, 5, dtype=np.int8).reshape(2, 5), np.arange(6, dtype=np.int32)):
+        gs(str(tmp_path), "t", arr)
+        back = gl(str(tmp_path), "t")
+        assert back.dtype == arr.dtype and np.array_equal(back, arr)
+    with pytest.raises(TecError) as e:
+        gl(str(tmp_path), "missing")
+    assert e.value.code == "IOError"
+
+
+def test_schedule_log_round_trip():
+    from paper_1802_04799_b200.device import make_desc
+    from paper_1802_04799_b200.tuner import config_from_schedule_log, conv_space, schedule_log
+    from paper_1802_04799_b200.workloads import resnet_layer
+    s = conv_space("C6", make_desc(resnet_layer("C6", 1)))
+    for i in range(0, s.size(), 7):
+        cfg = s.config_at(i)
+        log = schedule_log(cfg, s.desc)
+        json.dumps(log)
+        back = config_from_schedule_log(log)
+        want = {k: v for k, v in cfg.items() if not (k == "split_k" and v == 1)}
+        assert back == want
+    with pytest.raises(TecError):
+        config_from_schedule_log([{"prim": "fuse_axes"}])

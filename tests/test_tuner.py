@@ -67,6 +67,23 @@ def test_measure_and_tune_on_device(tmp_path):
     # im2col with tile_m != 128 does not instantiate -> lowering_failed
     assert any(r.status == "lowering_failed" for r in recs)
     db = str(tmp_path / "t.jsonl")
-    best = tune(s, budget=8, batch_size=4, db_path=db, method="ml")
+    best = tune(s, budget=24, batch_size=8, db_path=db, method="ml")
     assert best is not None and best.ok()
-    assert len(load_trials(db)) == 8
+    assert len(load_trials(db)) == 24
+
+
+@pytest.mark.gpu
+def test_depthwise_space_on_device():
+    from paper_1802_04799_b200.tuner import dw_space
+    from paper_1802_04799_b200.workloads import mobilenet_layer
+    s = dw_space("D3_b8", make_desc(mobilenet_layer("D3", 8)))
+    recs = measure(s, [s.config_at(i) for i in range(s.size())])
+    assert [r.status for r in recs] == ["ok"] * 3 and all(r.cost > 0 for r in recs)
+    best = tune(s, budget=3, batch_size=3, method="random")
+    assert best.ok() and best.config["unroll"] in (1, 2, 4)
+
+
+def test_dw_space_rejects_dense_desc():
+    with pytest.raises(_abi.TecError):
+        from paper_1802_04799_b200.tuner import dw_space
+        dw_space("C2", make_desc(resnet_layer("C2", 1)))
