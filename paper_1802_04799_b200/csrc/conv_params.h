@@ -98,6 +98,18 @@ struct DepthwiseParams {
   EpilogueParams epi;
 };
 
+// Tile shape of the TMA depthwise kernel (depthwise_tma.cu).
+struct DwTmaShape {
+  int32_t th;         // output rows per tile
+  int32_t cb;         // channels per tile (block)
+  int32_t rows_in;    // (th-1)*sw + 3
+  int32_t cols_in;    // (ow-1)*sw + 3
+  int32_t bands;      // ceil(oh / th)
+  int32_t cblocks;    // c / cb
+  int32_t buf_bytes;  // ni * rows_in * cols_in * cb * elem, rounded to 128
+  int32_t ni;         // images per tile (TMA box N extent)
+};
+
 // max_pool2d / global_avg_pool on NHWC activations (pool.cu).
 struct PoolParams {
   int32_t n, h, w, c, oh, ow, r, s, sh, sw, ph, pw;

@@ -1,0 +1,299 @@
+// depthwise_tma.cu -- the HBM-roofline depthwise 3x3 kernel (MobileNet D1-D9).
+//
+// Persistent CTAs walk (image, row band, channel block) tiles. For each tile
+// ONE tiled TMA box brings the input halo -- (TH-1)*SW+3 rows x (OW-1)*SW+3
+// columns x CB channels, the zero padding supplied by TMA out-of-bounds fill
+// -- into shared memory, double-buffered so the next tile's load overlaps this
+// tile's arithmetic. Every input byte therefore leaves HBM once; the 9-fold
+// tap reuse is served from shared memory. A thread owns one 16-byte channel
+// vector (fixed for the CTA's lifetime, its 9 taps in registers) and walks
+// output pixels; consecutive threads read consecutive 16-byte chunks of the
+// same / next pixel, so each tap read is a conflict-free contiguous run.
+//
+// Arithmetic is the oracle's per-output sequence (taps (rh, rw) in order,
+// facc = facc + x*w rounded to float; out-of-image taps contribute x = 0
+// exactly like the reference's select): bf16 x bf16 products are exact in
+// f32, so one FMA rounds like the reference's add; f32 operands keep the
+// separate multiply and add.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "conv_params.h"
+#include "sm100_ptx.cuh"
+
+namespace tec_sm100 {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&v)[16 / sizeof(T)]);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 t = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&v)[4]) {
+  const float4 t = *reinterpret_cast<const float4*>(p);
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void lds_vec(uint32_t addr, float (&v)[8]) {  // 8 bf16
+  uint32_t w0, w1, w2, w3;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(addr));
+  const uint32_t w[4] = {w0, w1, w2, w3};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ void lds_vec(uint32_t addr, float (&v)[4]) {  // 4 f32
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(addr));
+}
+
+enum { kDwtNone = 0, kDwtBias = 1, kDwtBiasRelu = 2 };
+
+constexpr int kDwtThreads = 384;  // 12 warps, up to 168 registers per thread
+constexpr int kTW = 4;            // output columns per work item
+
+template <typename InT, typename OutT, int SW, int PROG>
+__global__ void __launch_bounds__(kDwtThreads, 1)
+    dw_tma_kernel(const __grid_constant__ CUtensorMap tm_x, const DepthwiseParams p,
+                  const DwTmaShape t) {
+  constexpr int VEC = 16 / static_cast<int>(sizeof(InT));
+  constexpr int ES = static_cast<int>(sizeof(InT));
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  __shared__ uint64_t full[2];
+  const int tid = threadIdx.x;
+  const int nvec = t.cb / VEC;          // channel vectors per tile
+  const int v = tid % nvec;             // this thread's vector (fixed)
+  const int lane_pix = tid / nvec;      // first pixel slot
+  const int pix_step = blockDim.x / nvec;
+  const int ngroups = (p.n + t.ni - 1) / t.ni;  // images per tile: t.ni (small layers)
+  const int tiles = ngroups * t.bands * t.cblocks;
+  const uint32_t img_bytes = static_cast<uint32_t>(t.rows_in * t.cols_in * t.cb * ES);
+  const uint32_t tx_bytes = img_bytes * t.ni;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tm_x);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+
+  // tile -> (cblk slowest, so a CTA's consecutive tiles mostly share taps)
+  auto decode = [&](int tile, int* n, int* band, int* cblk) {
+    const int per_c = ngroups * t.bands;
+    *cblk = tile / per_c;
+    const int r = tile - *cblk * per_c;
+    *n = (r / t.bands) * t.ni;  // first image of the group
+    *band = r - (r / t.bands) * t.bands;
+  };
+  auto issue = [&](int tile, int buf) {
+    int n, band, cblk;
+    decode(tile, &n, &band, &cblk);
+    mbar_arrive_expect_tx(&full[buf], tx_bytes);
+    tma_load_4d(smem + buf * t.buf_bytes, &tm_x, &full[buf], cblk * t.cb, -p.pw,
+                band * t.th * SW - p.ph, n);
+  };
+
+  int first = blockIdx.x;
+  if (tid == 0 && first < tiles) issue(first, 0);
+  constexpr int V2 = VEC / 2;  // float2 lanes: packed f32x2 FMA (FFMA2)
+  float2 w2[9][V2];
+  float bias[VEC];
+  int cur_cblk = -1;
+  int it = 0;
+  for (int tile = first; tile < tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int next = tile + gridDim.x;
+    if (tid == 0 && next < tiles) issue(next, buf ^ 1);  // its buffer was released last iteration
+    int n, band, cblk;
+    decode(tile, &n, &band, &cblk);
+    const int c0 = cblk * t.cb + v * VEC;
+    if (cblk != cur_cblk) {  // the 9 taps (and bias) of this thread's channels
+      cur_cblk = cblk;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        float wk[VEC];
+        load8<InT>(static_cast<const InT*>(p.wt) + k * p.c + c0, wk);
+#pragma unroll
+        for (int j = 0; j < V2; ++j) w2[k][j] = make_float2(wk[2 * j], wk[2 * j + 1]);
+      }
+      if constexpr (PROG != kDwtNone) {
+#pragma unroll
+        for (int j = 0; j < VEC; j += 4) {
+          const float4 q = *reinterpret_cast<const float4*>(static_cast<const float*>(p.epi.bias) + c0 + j);
+          bias[j] = q.x; bias[j + 1] = q.y; bias[j + 2] = q.z; bias[j + 3] = q.w;
+        }
+      }
+    }
+    mbar_wait(&full[buf], static_cast<uint32_t>((it >> 1) & 1));
+    const uint32_t sbase = smem_u32(smem + buf * t.buf_bytes) + v * 16;
+    const int oh0 = band * t.th;
+    const int rows = min(t.th, p.oh - oh0);
+    const int strips = (p.ow + kTW - 1) / kTW;
+    const int nimg = min(t.ni, p.n - n);
+    const int per_img = rows * strips;
+    const int items = nimg * per_img;
+    // kTW consecutive output columns per item: each loaded (and unpacked)
+    // input column serves up to 3 taps of neighbouring outputs.
+    for (int it2 = lane_pix; it2 < items; it2 += pix_step) {
+      const int im = it2 / per_img;
+      const int rem_i = it2 - im * per_img;
+      const int r = rem_i / strips, ow0 = (rem_i - r * strips) * kTW;
+      float2 acc2[kTW][V2];
+#pragma unroll
+      for (int i = 0; i < kTW; ++i)
+#pragma unroll
+        for (int j = 0; j < V2; ++j) acc2[i][j] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int rh = 0; rh < 3; ++rh) {
+        const uint32_t rowa = sbase + im * img_bytes +
+            static_cast<uint32_t>(((r * SW + rh) * t.cols_in + ow0 * SW) * t.cb * ES);
+#pragma unroll
+        for (int jc = 0; jc < (kTW - 1) * SW + 3; ++jc) {
+          float x[VEC];
+          lds_vec(rowa + static_cast<uint32_t>(jc * t.cb * ES), x);
+#pragma unroll
+          for (int i = 0; i < kTW; ++i) {
+#pragma unroll
+            for (int rw = 0; rw < 3; ++rw) {
+              if (jc == i * SW + rw) {  // taps arrive in rw order per output
+#pragma unroll
+                for (int j = 0; j < V2; ++j) {
+                  if constexpr (std::is_same<InT, __nv_bfloat16>::value) {
+                    acc2[i][j] = __ffma2_rn(make_float2(x[2 * j], x[2 * j + 1]),
+                                            w2[rh * 3 + rw][j], acc2[i][j]);
+                  } else {
+                    acc2[i][j].x = __fadd_rn(acc2[i][j].x, __fmul_rn(x[2 * j], w2[rh * 3 + rw][j].x));
+                    acc2[i][j].y = __fadd_rn(acc2[i][j].y, __fmul_rn(x[2 * j + 1], w2[rh * 3 + rw][j].y));
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kTW; ++i) {
+        const int ow = ow0 + i;
+        if (ow >= p.ow) break;
+        float acc[VEC];
+#pragma unroll
+        for (int j = 0; j < V2; ++j) { acc[2 * j] = acc2[i][j].x; acc[2 * j + 1] = acc2[i][j].y; }
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          if constexpr (PROG != kDwtNone) acc[j] = __fadd_rn(acc[j], bias[j]);
+          if constexpr (PROG == kDwtBiasRelu) acc[j] = acc[j] < 0.0f ? 0.0f : acc[j];
+        }
+        const int64_t o = ((static_cast<int64_t>(n + im) * p.oh + oh0 + r) * p.ow + ow) * p.c + c0;
+        if constexpr (std::is_same<OutT, __nv_bfloat16>::value) {
+          uint32_t h[VEC / 2];
+#pragma unroll
+          for (int j = 0; j < VEC / 2; ++j) {
+            const __nv_bfloat162 q = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+            h[j] = *reinterpret_cast<const uint32_t*>(&q);
+          }
+          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + o) =
+              make_uint4(h[0], h[1], h[2], h[3]);
+        } else if constexpr (VEC == 8) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.y) + o);
+          dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+          *reinterpret_cast<float4*>(static_cast<float*>(p.y) + o) =
+              make_float4(acc[0], acc[1], acc[2], acc[3]);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with `buf` before it is refilled
+  }
+}
+
+}  // namespace
+
+// Plans the tile (rows per band, channel block) for the shared-memory
+// budget; returns false when the layer does not fit this kernel.
+bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
+  if (p.r != 3 || p.s != 3 || (p.sw != 1 && p.sw != 2) || p.sh != p.sw) return false;
+  const int es = p.in_type == kBF16 ? 2 : 4;
+  const int cb = p.c >= 128 / es ? 128 / es : p.c;  // 128-byte channel rows
+  if (p.c % cb || (cb * es) % 16) return false;
+  t->cb = cb;
+  t->cblocks = p.c / cb;
+  // whole kTW-column strips: the last strip reads TMA zero-fill columns
+  t->cols_in = (((p.ow + kTW - 1) / kTW) * kTW - 1) * p.sw + 3;
+  if (t->cols_in > 256) return false;
+  const int budget = 100 * 1024;  // per buffer (two buffers + slack < 227 KB)
+  int th = p.oh;
+  while (th > 1 && ((th - 1) * p.sw + 3) * t->cols_in * cb * es > budget) --th;
+  t->th = th;
+  t->rows_in = (th - 1) * p.sw + 3;
+  if (t->rows_in > 256) return false;
+  t->bands = (p.oh + th - 1) / th;
+  // Small images: several per tile (the TMA box's N extent) so a tile has
+  // enough work to hide the next tile's load, keeping >= 2 tiles per SM.
+  const int img = t->rows_in * t->cols_in * cb * es;
+  t->ni = 1;
+  if (t->bands == 1) {
+    const int sms = 148;
+    while (t->ni < 8 && (t->ni + 1) * img <= budget &&
+           ((p.n + t->ni) / (t->ni + 1)) * t->cblocks >= 2 * sms)
+      ++t->ni;
+  }
+  t->buf_bytes = ((img * t->ni) + 127) & ~127;
+  return t->buf_bytes <= budget;
+}
+
+int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
+                  int prog, int sms, cudaStream_t st) {
+  const int tiles = ((p.n + t.ni - 1) / t.ni) * t.bands * t.cblocks;
+  const int grid = tiles < sms ? tiles : sms;
+  const int smem = 2 * t.buf_bytes + 128;
+  auto go = [&](auto kfn) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(kfn, dim3(grid), dim3(kDwtThreads), smem, st, tm_x, p, t);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  };
+#define TEC_DWT(IN, OUT, SW_)                                                    \
+  switch (prog) {                                                               \
+    case kDwtNone: return go(dw_tma_kernel<IN, OUT, SW_, kDwtNone>);            \
+    case kDwtBias: return go(dw_tma_kernel<IN, OUT, SW_, kDwtBias>);            \
+    default: return go(dw_tma_kernel<IN, OUT, SW_, kDwtBiasRelu>);              \
+  }
+  if (p.in_type == kBF16 && p.out_type == kBF16) {
+    if (p.sw == 1) { TEC_DWT(__nv_bfloat16, __nv_bfloat16, 1) }
+    TEC_DWT(__nv_bfloat16, __nv_bfloat16, 2)
+  }
+  if (p.in_type == kBF16 && p.out_type == kF32) {
+    if (p.sw == 1) { TEC_DWT(__nv_bfloat16, float, 1) }
+    TEC_DWT(__nv_bfloat16, float, 2)
+  }
+  if (p.in_type == kF32 && p.out_type == kF32) {
+    if (p.sw == 1) { TEC_DWT(float, float, 1) }
+    TEC_DWT(float, float, 2)
+  }
+#undef TEC_DWT
+  return -1;
+}
+
+}  // namespace tec_sm100

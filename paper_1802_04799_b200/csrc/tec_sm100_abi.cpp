@@ -53,6 +53,9 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
                      cudaStream_t stream);
 int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px, int stage_bytes);
 int launch_max_pool(const PoolParams& p, cudaStream_t st);
+bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t);
+int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
+                  int prog, int sms, cudaStream_t st);
 int launch_global_avg_pool(const PoolParams& p, cudaStream_t st);
 }  // namespace tec_sm100
 
@@ -960,8 +963,40 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
   p.y = y;
   p.err = err_flag;
   p.epi = ep;
-  const int tw = knobs && knobs->unroll ? (int)knobs->unroll : 4;
-  const int e = launch_depthwise(p, tw, (cudaStream_t)stream);
+  // knob unroll: 0 auto (TMA-tiled kernel when it applies), 8 TMA-tiled,
+  // 2/4 column-streaming kernel with that many outputs per thread, 1 generic.
+  const int tw = knobs && knobs->unroll ? (int)knobs->unroll : 0;
+  if (tw == 0 || tw == 8) {
+    const int prog = epi && fast_program(ep) ? (ep.n_ops == 0 ? 0 : ep.n_ops == 1 ? 1 : 2) : -1;
+    DwTmaShape t{};
+    if (prog >= 0 && (p.in_type == kBF16 || p.in_type == kF32) && dw_tma_plan(p, &t)) {
+      const DriverFns& fns = driver_fns();
+      const int es = p.in_type == kBF16 ? 2 : 4;
+      CUtensorMap tm{};
+      cuuint64_t dims[4] = {(cuuint64_t)d->c, (cuuint64_t)d->w, (cuuint64_t)d->h, (cuuint64_t)d->n};
+      cuuint64_t strides[3] = {(cuuint64_t)(d->c * es), (cuuint64_t)(d->c * es * d->w),
+                               (cuuint64_t)(d->c * es * d->w * d->h)};
+      cuuint32_t box[4] = {(cuuint32_t)t.cb, (cuuint32_t)t.cols_in, (cuuint32_t)t.rows_in,
+                           (cuuint32_t)t.ni};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      CUresult r = fns.ok ? fns.tiled(&tm, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                   : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                      4, const_cast<void*>(x_packed), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                          : CUDA_ERROR_NOT_INITIALIZED;
+      if (r == CUDA_SUCCESS) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int e = launch_dw_tma(p, tm, t, prog, sm_count(dev), (cudaStream_t)stream);
+        if (e == 0) return TEC_OK;
+        if (e != -1) return cuda_fail(e, "depthwise (TMA) launch");
+      }
+    }
+    if (tw == 8) return fail(TEC_E_LOWERING, "TMA depthwise kernel does not apply to this layer");
+  }
+  const int e = launch_depthwise(p, tw == 0 ? 4 : tw, (cudaStream_t)stream);
   if (e == -1)
     return fail(TEC_E_LOWERING, "depthwise: unsupported dtype pair or C not a multiple of the vector width");
   if (e) return cuda_fail(e, "depthwise launch");

@@ -139,11 +139,12 @@ def conv_space(name: str, desc: _abi.ConvDesc,
 
 def dw_space(name: str, desc: _abi.ConvDesc,
              epilogue: Sequence[int] = (_abi.EPI_BIAS, _abi.EPI_RELU)) -> KnobSpace:
-    """The depthwise template's knobs: unroll = output columns per thread
-    (1 selects the generic kernel; 2 / 4 the 3x3 column-streaming kernel)."""
+    """The depthwise template's knobs: unroll selects the kernel -- 1 the
+    generic one, 2 / 4 the 3x3 column-streaming kernel with that many outputs
+    per thread, 8 the TMA-tiled shared-memory kernel."""
     if not desc.depthwise:
         raise _abi.TecError(15, "dw_space needs a depthwise descriptor")
-    return KnobSpace(name, [KnobDef("unroll", [1, 2, 4])], desc, tuple(epilogue))
+    return KnobSpace(name, [KnobDef("unroll", [1, 2, 4, 8])], desc, tuple(epilogue))
 
 
 # ------------------------------------------------ Config <-> schedule log

@@ -239,3 +239,18 @@ def test_split_k_on_halo_path_is_a_lowering_error():
         fused_conv("conv2d", x, w, {"padding": (1, 1)}, [], knobs={"tile_k": 2, "split_k": 2},
                    compute="bf16")
     assert e.value.code == "LoweringError"
+
+
+@pytest.mark.parametrize("compute", ["bf16", "f32"])
+@pytest.mark.parametrize("layer", ["D2", "D8", "D9"])
+def test_depthwise_multi_image_tiles(layer, compute):
+    # batch > 1 exercises the TMA kernel's multi-image tiles and bands
+    hw, c, s = MOBILENET_DW[layer]
+    x, w, b = _inputs((5, c, hw, hw), (c, 1, 3, 3), c, False, seed=77)
+    attrs = {"strides": (s, s), "padding": (1, 1)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("depthwise_conv2d", x, w, attrs, epi, compute=compute)
+    if compute == "bf16":
+        x, w = bf16_round(x), bf16_round(w)
+    want = oracle_conv("depthwise_conv2d", x, w, attrs["strides"], attrs["padding"], epi)
+    assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
