@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          fast != epi::kProgBiasAddRelu;
     uint32_t chunk_cnt = 0;
     int local = 0;
+    int staged_n_tile = -1;
     bool overflow = false;
     int n_tile, band, img;
     for (; tile_at(local, &n_tile, &band, &img); ++local) {
@@ -283,9 +284,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (acc != grp) continue;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
       uint32_t* bias_s = sBias + acc * BN;
-      epi::named_bar_sync(1 + grp, 128);
-      epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
-      epi::named_bar_sync(1 + grp, 128);
+      // The group's bias buffer only changes with the output-channel tile
+      // (a global load + two barriers on the per-tile critical path).
+      if (n_tile != staged_n_tile) {
+        epi::named_bar_sync(1 + grp, 128);  // previous tile's readers are done
+        epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
+        epi::named_bar_sync(1 + grp, 128);
+        staged_n_tile = n_tile;
+      }
       const long long tw0 = p.dbg ? clock64() : 0;
       mbar_wait(&tfull[acc], use & 1);
       const long long tw1 = p.dbg ? clock64() : 0;

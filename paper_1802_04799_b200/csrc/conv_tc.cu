@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t stage_u32 = smem_u32(stage);
     uint32_t box_cnt = 0;
     int local = 0;
+    int staged_n_tile = -1;
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles;
          tile += gridDim.x, ++local) {
@@ -237,9 +238,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < p.m;
       // Per-tile bias copy in smem (one buffer per group).
       uint32_t* bias_s = sBias + acc * BN;
-      epi::named_bar_sync(1 + grp, 128);  // previous tile's readers are done
-      epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
-      epi::named_bar_sync(1 + grp, 128);
+      // The group's bias buffer only changes with the output-channel tile
+      // (a global load + two barriers on the per-tile critical path).
+      if (n_tile != staged_n_tile) {
+        epi::named_bar_sync(1 + grp, 128);  // previous tile's readers are done
+        epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
+        epi::named_bar_sync(1 + grp, 128);
+        staged_n_tile = n_tile;
+      }
       const long long tw0 = p.dbg ? clock64() : 0;
       mbar_wait(&tfull[acc], use & 1);
       const long long tw1 = p.dbg ? clock64() : 0;
