@@ -90,6 +90,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kCB =
       SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
   const uint32_t halo_tx = static_cast<uint32_t>((p.th + p.r - 1) * p.wp * SWZ);
+  // Weight multicast (p.cl > 1, streamed weights): the cl CTAs of a cluster
+  // work on the same output-channel tile at the same time; each loads 1/cl
+  // of every weight tile and multicasts it to all, so weights cross L2->SM
+  // once per cluster instead of once per CTA.
+  const int cl = p.cl > 1 && !p.resident ? p.cl : 1;
+  const int crank = cl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const uint16_t cmask = static_cast<uint16_t>((1u << cl) - 1u);
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_x);
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < WSTAGES; ++i) {
       mbar_init(&wfull[i], 1);
-      mbar_init(&wempty[i], 1);
+      mbar_init(&wempty[i], cl);  // every CTA of the cluster releases the slot
     }
     fence_barrier_init();
   }
@@ -120,9 +127,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (n_tile = blockIdx.x % n_tiles) and loads all of its weights once.
   const int spatial = p.n * p.bands;
   const int ctas_per_n = static_cast<int>(gridDim.x) / p.n_tiles;
-  auto tile_at = [&](int i, int* n_tile, int* band, int* img) -> bool {
+  const int nclusters = static_cast<int>(gridDim.x) / cl;
+  const int cunits = ((spatial + cl - 1) / cl) * p.n_tiles;
+  // *dummy: a cluster's last spatial group may leave a CTA without a tile;
+  // it still runs the shared weight pipeline, but loads and stores nothing.
+  auto tile_at = [&](int i, int* n_tile, int* band, int* img, bool* dummy = nullptr) -> bool {
     int s;
-    if (p.resident) {
+    if (dummy) *dummy = false;
+    if (cl > 1) {
+      const int unit = static_cast<int>(blockIdx.x) / cl + i * nclusters;
+      if (unit >= cunits) return false;
+      *n_tile = unit % p.n_tiles;
+      s = (unit / p.n_tiles) * cl + crank;
+      if (s >= spatial) {
+        if (dummy) *dummy = true;
+        s = spatial - 1;
+      }
+    } else if (p.resident) {
       s = static_cast<int>(blockIdx.x) / p.n_tiles + i * ctas_per_n;
       if (s >= spatial || static_cast<int>(blockIdx.x) >= ctas_per_n * p.n_tiles) return false;
       *n_tile = static_cast<int>(blockIdx.x) % p.n_tiles;
@@ -151,16 +172,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sW + (cb * taps + t) * Cfg::kWBytes, &tm_w, &wfull[0],
                         t * p.cp + cb * kCB, n_tile * BN);
       }
-      for (int i = 0; tile_at(i, &n_tile, &band, &img); ++i) {
+      bool dummy = false;
+      for (int i = 0; tile_at(i, &n_tile, &band, &img, &dummy); ++i) {
         const int ih0 = band * p.th - p.ph;
         for (int cb = 0; cb < p.cblocks; ++cb) {
           { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&hempty[hs], hph ^ 1);
             if (p.dbg) dbg_wait[0] += clock64() - t0; }
-          mbar_arrive_expect_tx(&hfull[hs], halo_tx);
-          // box {CB, wp, th + r - 1, 1} at (c, -pw, ih0, img); TMA fills
-          // the out-of-image pixels with zeros (the select(..., 0) pad).
-          tma_load_4d(sH + hs * hbytes, &tm_x, &hfull[hs], cb * kCB, -p.pw, ih0, img);
+          if (dummy) {
+            mbar_arrive(&hfull[hs]);  // nothing to load; the MMAs run on stale data
+          } else {
+            mbar_arrive_expect_tx(&hfull[hs], halo_tx);
+            // box {CB, wp, th + r - 1, 1} at (c, -pw, ih0, img); TMA fills
+            // the out-of-image pixels with zeros (the select(..., 0) pad).
+            tma_load_4d(sH + hs * hbytes, &tm_x, &hfull[hs], cb * kCB, -p.pw, ih0, img);
+          }
           if (++hs == 2) { hs = 0; hph ^= 1; }
           if (p.resident) continue;
           for (int t = 0; t < taps; ++t) {
@@ -168,8 +194,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_wait(&wempty[ws], wph ^ 1);
               if (p.dbg) dbg_wait[0] += clock64() - t0; }
             mbar_arrive_expect_tx(&wfull[ws], Cfg::kWBytes);
-            tma_load_2d(sW + ws * Cfg::kWBytes, &tm_w, &wfull[ws],
-                        t * p.cp + cb * kCB, n_tile * BN);
+            if (cl > 1) {  // this CTA's 1/cl row slice of the tile, to every CTA
+              const int rows = BN / cl;
+              tma_load_2d_mc(sW + ws * Cfg::kWBytes + crank * rows * SWZ, &tm_w, &wfull[ws],
+                             t * p.cp + cb * kCB, n_tile * BN + crank * rows, cmask);
+            } else {
+              tma_load_2d(sW + ws * Cfg::kWBytes, &tm_w, &wfull[ws],
+                          t * p.cp + cb * kCB, n_tile * BN);
+            }
             if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
           }
         }
@@ -241,7 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (kRes) {
                   bd += Cfg::kWBytes >> 4;
                 } else {
-                  tc_commit(&wempty[ws]);
+                  if (cl > 1) tc_commit_mc(&wempty[ws], cmask);  // release in every CTA
+                  else tc_commit(&wempty[ws]);
                   if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
                 }
               }
@@ -279,7 +312,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int staged_n_tile = -1;
     bool overflow = false;
     int n_tile, band, img;
-    for (; tile_at(local, &n_tile, &band, &img); ++local) {
+    bool dummy = false;
+    for (; tile_at(local, &n_tile, &band, &img, &dummy); ++local) {
       const int acc = local & 1;
       if (acc != grp) continue;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -297,6 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
+      if (dummy) {  // no tile for this CTA in its cluster's last group
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       {
         if (tma_epi) {
           constexpr bool kInt = KIND == MmaKind::kI8;
@@ -411,6 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Peers multicast into this CTA's smem and arrive on its barriers until
+  // they finish: nobody leaves before the whole cluster is done.
+  if (cl > 1) cluster_sync();
   if (warp == 2) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   if (p.dbg) {
     const bool rep = (warp <= 1 && lane == 0) || threadIdx.x == kThreads - kEpiThreads;
@@ -440,7 +482,8 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
   auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_x, tm_w, tm_y, p);
+  e = launch_pdl_cluster(kfn, dim3(grid), dim3(kThreads), smem, stream,
+                         p.cl > 1 && !p.resident ? p.cl : 1, tm_x, tm_w, tm_y, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

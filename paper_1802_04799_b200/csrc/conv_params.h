@@ -84,6 +84,7 @@ struct ConvHaloParams {
   int32_t epi_mode;         // 0: warp-coalesced epilogue, 1: per-thread rows
   int32_t tma_store;        // 1: y has a TMA store map (fast programs use it)
   int32_t stage_bytes;      // epilogue stage (>= 32 KB); two halves, one per group
+  int32_t cl;               // streamed weights: CTAs per cluster sharing them by multicast
 };
 
 struct DepthwiseParams {

@@ -359,6 +359,7 @@ struct HaloChoice {
   const HaloInst* inst = nullptr;
   int th = 0, halo_px = 0, bands = 0, n_tiles = 0, tiles = 0;
   int resident = 0, w_slots = 0, grid = 0;
+  int cl = 1;  // cluster size of the weight multicast (streamed weights)
 };
 
 // Picks (BN, MS, rows per tile) by a two-term model per tile --
@@ -405,31 +406,43 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
                      hi.ms, hi.swz, res, th,
                      conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin));
       if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin) > kSmemMax) continue;
-      int grid;
-      double per_tile, waves;
-      if (res) {
-        const int per_n = (int)std::min<int64_t>(sms / n_tiles, spatial);
-        if (per_n < 1) continue;
-        grid = per_n * n_tiles;
-        waves = (double)((spatial + per_n - 1) / per_n);
-        per_tile = std::max(std::max(mma, halo_bytes / 40.0), epi);
-      } else {
-        grid = (int)std::min<int64_t>(tiles, sms);
-        waves = (double)((tiles + sms - 1) / sms);
-        per_tile = std::max(std::max(mma, ((double)hi.bn * ktot * es + halo_bytes) / 40.0), epi);
-      }
-      const double cost = waves * per_tile;
-      if (cost < best) {
-        best = cost;
-        out->inst = &hi;
-        out->th = th;
-        out->halo_px = halo_px;
-        out->bands = bands;
-        out->n_tiles = n_tiles;
-        out->tiles = (int)tiles;
-        out->resident = res;
-        out->w_slots = w_slots;
-        out->grid = grid;
+      // knob cluster_n: 0 / 1 no multicast, 2 weight multicast over CTA
+      // pairs. Not chosen automatically: measured slower on ResNet layers
+      // (the pair runs in lockstep on the weight ring), so only the tuner
+      // or an explicit knob enables it.
+      for (int cl = 1; cl <= 2; ++cl) {
+        if (cl != (kn && kn->cluster_n ? kn->cluster_n : 1)) continue;
+        if (cl > 1 && (res || hi.bn / cl < 8 || sms < 2)) continue;
+        int grid;
+        double per_tile, waves;
+        if (res) {
+          const int per_n = (int)std::min<int64_t>(sms / n_tiles, spatial);
+          if (per_n < 1) continue;
+          grid = per_n * n_tiles;
+          waves = (double)((spatial + per_n - 1) / per_n);
+          per_tile = std::max(std::max(mma, halo_bytes / 40.0), epi);
+        } else {
+          const int64_t units = ((spatial + cl - 1) / cl) * n_tiles;
+          const int64_t clusters = std::min<int64_t>(units, sms / cl);
+          grid = (int)(clusters * cl);
+          waves = (double)((units + clusters - 1) / clusters);
+          per_tile = std::max(std::max(mma, ((double)hi.bn * ktot * es / cl + halo_bytes) / 40.0),
+                              epi);
+        }
+        const double cost = waves * per_tile;
+        if (cost < best) {
+          best = cost;
+          out->inst = &hi;
+          out->th = th;
+          out->halo_px = halo_px;
+          out->bands = bands;
+          out->n_tiles = n_tiles;
+          out->tiles = (int)tiles;
+          out->resident = res;
+          out->w_slots = w_slots;
+          out->grid = grid;
+          out->cl = cl;
+        }
       }
     }
   }
@@ -466,7 +479,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     const int64_t ktot = d->r * d->s * pl.cp;
     cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)d->k};
     cuuint64_t strides[1] = {(cuuint64_t)(ktot * es)};
-    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)hc.inst->bn};
+    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)(hc.inst->bn / hc.cl)};  // multicast slice
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fns.tiled(&tm_w, tdt, 2, const_cast<void*>(w), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(pl.swz),
@@ -485,6 +498,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   p.halo_px = hc.halo_px;
   p.resident = hc.resident;
   p.w_slots = hc.w_slots;
+  p.cl = hc.cl;
   p.out_type = out_dtype;
   p.y = y;
   p.err = err;
@@ -514,7 +528,9 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     p.tma_store = ok && !(kn && kn->vec == 3) ? 1 : 0;  // vec 3: SIMT stores
   }
   int grid = hc.grid;
-  if (kn && kn->grid > 0 && !hc.resident) grid = (int)std::min<int64_t>(grid, kn->grid);
+  if (kn && kn->grid > 0 && !hc.resident)
+    grid = (int)std::min<int64_t>(grid, kn->grid / hc.cl * hc.cl);
+  if (grid < hc.cl) return fail(TEC_E_LOWERING, "grid smaller than the cluster");
   static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
   unsigned long long* dbg = nullptr;
   if (prof) {
@@ -531,11 +547,11 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     cudaFree(dbg);
     const double ctas = (double)grid;
     std::fprintf(stderr,
-                 "[tec-prof] halo tma_store=%d stage=%d bn=%d ms=%d th=%d wp=%d taps=%d cblocks=%d tiles/cta=%.2f "
+                 "[tec-prof] halo cl=%d tma_store=%d stage=%d bn=%d ms=%d th=%d wp=%d taps=%d cblocks=%d tiles/cta=%.2f "
                  "cta_cycles=%.0f | prod_wait_empty=%.0f mma_wait_data=%.0f mma_wait_acc=%.0f "
                  "epi_wait_acc=%.0f epi_busy=%.0f | blk_tmem=%.0f blk_ops=%.0f blk_store=%.0f "
                  "(per CTA)\n",
-                 p.tma_store, p.stage_bytes, hc.inst->bn, hc.inst->ms, hc.th, wp, (int)(d->r * d->s), p.cblocks,
+                 p.cl, p.tma_store, p.stage_bytes, hc.inst->bn, hc.inst->ms, hc.th, wp, (int)(d->r * d->s), p.cblocks,
                  h[6] / ctas, h[5] / ctas, h[0] / ctas, h[1] / ctas, h[2] / ctas, h[3] / ctas,
                  h[4] / ctas, h[8] / ctas, h[9] / ctas, h[10] / ctas);
   }
@@ -603,6 +619,8 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   // Path: knob tile_k selects the A-operand strategy -- 0 auto, 1 im2col
   // TMA (conv_tc.cu), 2 shifted-window halo (conv_halo.cu, stride 1 only).
   const int64_t path = kn ? kn->tile_k : 0;
+  if (path == 1 && kn && kn->cluster_n > 1)
+    return fail(TEC_E_LOWERING, "cluster_n (weight multicast) applies to the halo path");
   if (path == 2 && kn && kn->split_k > 1)
     return fail(TEC_E_LOWERING, "split_k applies to the im2col path (tile_k=1)");
   if (path != 1 && !(kn && kn->split_k > 1)) {

@@ -130,10 +130,12 @@ def conv_space(name: str, desc: _abi.ConvDesc,
     tile_k = A-operand strategy (1 im2col TMA, 2 shifted-window halo),
     tile_n = CTA N tile (split of the OC axis), tile_m = M rows per tile
     (halo: MMA sub-tiles x 128), stages (halo: 1 streamed / 2 resident
-    weights), split_k (im2col: K split over CTAs, partials summed in order)."""
+    weights), split_k (im2col: K split over CTAs, partials summed in order),
+    cluster_n (halo, streamed weights: CTA pairs share weight tiles by TMA
+    multicast)."""
     knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
              KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2]),
-             KnobDef("split_k", [1, 2, 3, 4])]
+             KnobDef("split_k", [1, 2, 3, 4]), KnobDef("cluster_n", [1, 2])]
     return KnobSpace(name, knobs, desc, tuple(epilogue))
 
 
@@ -178,6 +180,9 @@ def schedule_log(cfg: Config, desc: _abi.ConvDesc, stage: str = "conv") -> List[
     if cfg.get("grid"):
         log.append({"prim": "bind", "stage": stage, "axis": f"nyx.outer.{int(cfg['grid'])}",
                     "tag": "blockIdx.x"})
+    if cfg.get("cluster_n", 1) > 1:
+        log.append({"prim": "bind", "stage": stage, "axis": f"nyx.cluster.{int(cfg['cluster_n'])}",
+                    "tag": "cluster"})
     return log
 
 
@@ -201,7 +206,8 @@ def config_from_schedule_log(log: Sequence[dict]) -> Config:
         elif prim == "unroll":
             cfg["unroll"] = int(e["axis"].split(".")[-1])
         elif prim == "bind":
-            cfg["grid"] = int(e["axis"].split(".")[-1])
+            key = "cluster_n" if e.get("tag") == "cluster" else "grid"
+            cfg[key] = int(e["axis"].split(".")[-1])
         elif prim in ("set_scope", "tensorize"):
             continue
         else:

@@ -254,3 +254,19 @@ def test_depthwise_multi_image_tiles(layer, compute):
         x, w = bf16_round(x), bf16_round(w)
     want = oracle_conv("depthwise_conv2d", x, w, attrs["strides"], attrs["padding"], epi)
     assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
+
+
+@pytest.mark.parametrize("batch", [3, 4])
+@pytest.mark.parametrize("layer", ["C2", "C6", "C9"])
+def test_halo_weight_multicast_cluster(layer, batch):
+    # CTA pairs share streamed weight tiles by TMA multicast; batch 3 leaves
+    # a pair with one real spatial tile and one dummy CTA on some layers.
+    hw, c, k, r, s = RESNET18_CONVS[layer]
+    x, w, b = _inputs((batch, c, hw, hw), (k, c, r, r), k, False, seed=41 + batch)
+    attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, compute="bf16",
+                   knobs={"tile_k": 2, "stages": 1, "cluster_n": 2})
+    want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), attrs["strides"],
+                       attrs["padding"], epi)
+    assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
