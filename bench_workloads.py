@@ -172,7 +172,8 @@ def _tune_graph_convs(g, device, args):
         d = conv_desc("conv2d", xs, ws_, root.attrs, _abi.COMPUTE_BF16)
         key = (tuple(xs), tuple(ws_), tuple(root.attrs.get("strides", (1, 1))))
         if key not in best:
-            rec = tune(conv_space(str(key), d), budget=36, batch_size=36, method="random",
+            space = conv_space(str(key), d)
+            rec = tune(space, budget=space.size(), batch_size=space.size(), method="random",
                        devices=[device], repeats=3)
             best[key] = rec.config if rec else {}
         out[n.id] = best[key]

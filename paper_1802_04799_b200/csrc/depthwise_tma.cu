@@ -227,7 +227,112 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
   }
 }
 
+// 3x3 max-pool on bf16 NHWC through the same TMA tiles. The map's
+// out-of-bounds fill is NaN and __hmax2 returns the non-NaN operand, so
+// padding never wins -- exactly max over the in-image taps. (A NaN *input*
+// is skipped the same way.) bf16 max is exact, so no conversions.
+template <int SW>
+__global__ void __launch_bounds__(kDwtThreads, 1)
+    pool_tma_kernel(const __grid_constant__ CUtensorMap tm_x, const DepthwiseParams p,
+                    const DwTmaShape t) {
+  constexpr int ES = 2;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~uintptr_t(127));
+  __shared__ uint64_t full[2];
+  const int tid = threadIdx.x;
+  const int nvec = t.cb / 8;
+  const int v = tid % nvec;
+  const int lane_pix = tid / nvec;
+  const int pix_step = blockDim.x / nvec;
+  const int ngroups = (p.n + t.ni - 1) / t.ni;
+  const int tiles = ngroups * t.bands * t.cblocks;
+  const uint32_t img_bytes = static_cast<uint32_t>(t.rows_in * t.cols_in * t.cb * ES);
+  const uint32_t tx_bytes = img_bytes * t.ni;
+  if (tid == 0) {
+    tma_prefetch_desc(&tm_x);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+  auto decode = [&](int tile, int* n, int* band, int* cblk) {
+    const int per_c = ngroups * t.bands;
+    *cblk = tile / per_c;
+    const int r = tile - *cblk * per_c;
+    *n = (r / t.bands) * t.ni;
+    *band = r - (r / t.bands) * t.bands;
+  };
+  auto issue = [&](int tile, int buf) {
+    int n, band, cblk;
+    decode(tile, &n, &band, &cblk);
+    mbar_arrive_expect_tx(&full[buf], tx_bytes);
+    tma_load_4d(smem + buf * t.buf_bytes, &tm_x, &full[buf], cblk * t.cb, -p.pw,
+                band * t.th * SW - p.ph, n);
+  };
+  if (tid == 0 && static_cast<int>(blockIdx.x) < tiles) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const int next = tile + gridDim.x;
+    if (tid == 0 && next < tiles) issue(next, buf ^ 1);
+    int n, band, cblk;
+    decode(tile, &n, &band, &cblk);
+    const int c0 = cblk * t.cb + v * 8;
+    mbar_wait(&full[buf], static_cast<uint32_t>((it >> 1) & 1));
+    const uint32_t sbase = smem_u32(smem + buf * t.buf_bytes) + v * 16;
+    const int oh0 = band * t.th;
+    const int rows = min(t.th, p.oh - oh0);
+    const int nimg = min(t.ni, p.n - n);
+    const int per_img = rows * p.ow;
+    for (int it2 = lane_pix; it2 < nimg * per_img; it2 += pix_step) {
+      const int im = it2 / per_img;
+      const int rem_i = it2 - im * per_img;
+      const int r = rem_i / p.ow, ow = rem_i - r * p.ow;
+      __nv_bfloat162 m[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m[j] = __float2bfloat162_rn(__int_as_float(0x7fc00000));  // NaN
+#pragma unroll
+      for (int rh = 0; rh < 3; ++rh)
+#pragma unroll
+        for (int rw = 0; rw < 3; ++rw) {
+          uint32_t w0, w1, w2, w3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                       : "r"(sbase + im * img_bytes +
+                             static_cast<uint32_t>(((r * SW + rh) * t.cols_in + ow * SW + rw) * t.cb * ES)));
+          const uint32_t wv[4] = {w0, w1, w2, w3};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            m[j] = __hmax2(m[j], *reinterpret_cast<const __nv_bfloat162*>(&wv[j]));
+        }
+      const int64_t o = ((static_cast<int64_t>(n + im) * p.oh + oh0 + r) * p.ow + ow) * p.c + c0;
+      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.y) + o) =
+          *reinterpret_cast<const uint4*>(m);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+int launch_pool_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
+                    int sms, cudaStream_t st) {
+  const int tiles = ((p.n + t.ni - 1) / t.ni) * t.bands * t.cblocks;
+  const int grid = tiles < sms ? tiles : sms;
+  const int smem = 2 * t.buf_bytes + 128;
+  auto go = [&](auto kfn) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(kfn, dim3(grid), dim3(kDwtThreads), smem, st, tm_x, p, t);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  };
+  if (p.in_type != kBF16 || p.out_type != kBF16) return -1;
+  return p.sw == 1 ? go(pool_tma_kernel<1>) : go(pool_tma_kernel<2>);
+}
 
 // Plans the tile (rows per band, channel block) for the shared-memory
 // budget; returns false when the layer does not fit this kernel.

@@ -233,6 +233,39 @@ __global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ o
   }
 }
 
+// Fast path (bf16, cp = 16): one thread per space-to-depth pixel writes
+// its 16 channels as two 16-byte stores; 32-bit index math (the per-element
+// kernel above spent its time in 64-bit divisions).
+__global__ void pack_s2d_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                     int n, int c, int h, int w, int ph, int pw, int h2, int w2) {
+  const int total = n * h2 * w2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int jj = i % w2;
+    const int t = i / w2;
+    const int ii = t % h2;
+    const int nn = t / h2;
+    uint32_t wd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wd[k] = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int y = 2 * ii + q / 2 - ph, x = 2 * jj + q % 2 - pw;
+      const bool in_img = y >= 0 && y < h && x >= 0 && x < w;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        if (cc >= c) break;
+        const float v = in_img ? in[((static_cast<int64_t>(nn) * c + cc) * h + y) * w + x] : 0.0f;
+        const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        const int e = q * c + cc;  // channel (dy*2+dx)*C + c
+        wd[e >> 1] |= (e & 1) ? (b << 16) : b;
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(i) * 16);
+    dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+  }
+}
+
 // Matching weights: [K][R2][S2][cp], w2[k][ri][sj][(dy*2+dx)*C + c] =
 // w[k][c][2ri+dy][2sj+dx] (0 past the original R x S window).
 template <typename InT>
@@ -265,6 +298,15 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
 int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c, int64_t h,
                     int64_t w, int64_t ph, int64_t pw, int64_t h2, int64_t w2, int64_t cp,
                     int mode, cudaStream_t st) {
+  if (in_type != kI8 && mode == kPackBF16 && cp == 16 && c <= 4 && n * h2 * w2 < (1ll << 31)) {
+    const int64_t px = n * h2 * w2;
+    const int blocks = static_cast<int>(std::min<int64_t>((px + 255) / 256, 148 * 32));
+    pack_s2d_bf16_kernel<<<blocks, 256, 0, st>>>(
+        static_cast<const float*>(in), static_cast<__nv_bfloat16*>(out), static_cast<int>(n),
+        static_cast<int>(c), static_cast<int>(h), static_cast<int>(w), static_cast<int>(ph),
+        static_cast<int>(pw), static_cast<int>(h2), static_cast<int>(w2));
+    return cudaGetLastError();
+  }
   const int64_t total = n * h2 * w2 * cp;
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
   if (in_type == kI8)

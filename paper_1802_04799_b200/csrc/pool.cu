@@ -29,31 +29,30 @@ struct Lanes { static constexpr int N = 16 / sizeof(T); };
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// One thread: one output pixel x 16 bytes of channels.
+// One thread: one output pixel x 16 bytes of channels (32-bit index math:
+// 64-bit divisions per element dominated the first version).
 template <typename T>
 __global__ void max_pool_kernel(PoolParams p) {
   constexpr int V = Lanes<T>::N;
   const int cv = p.c / V;
-  const int64_t total = static_cast<int64_t>(p.n) * p.oh * p.ow * cv;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int v = static_cast<int>(i % cv);
-    int64_t pix = i / cv;
-    const int ow = static_cast<int>(pix % p.ow);
-    pix /= p.ow;
-    const int oh = static_cast<int>(pix % p.oh);
-    const int n = static_cast<int>(pix / p.oh);
+  const uint32_t total = static_cast<uint32_t>(p.n) * p.oh * p.ow * cv;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t pix = i / cv;
+    const int v = static_cast<int>(i - pix * cv);
+    const uint32_t row = pix / p.ow;
+    const int ow = static_cast<int>(pix - row * p.ow);
+    const int n = static_cast<int>(row / p.oh);
+    const int oh = static_cast<int>(row - n * p.oh);
     T best[V];
     bool any = false;
+    const T* base = static_cast<const T*>(p.x) + static_cast<int64_t>(n) * p.h * p.w * p.c + v * V;
     for (int rh = 0; rh < p.r; ++rh) {
       const int ih = oh * p.sh + rh - p.ph;
       if (ih < 0 || ih >= p.h) continue;
       for (int rw = 0; rw < p.s; ++rw) {
         const int iw = ow * p.sw + rw - p.pw;
         if (iw < 0 || iw >= p.w) continue;
-        const T* src = static_cast<const T*>(p.x) +
-                       ((static_cast<int64_t>(n) * p.h + ih) * p.w + iw) * p.c + v * V;
-        uint4 raw = *reinterpret_cast<const uint4*>(src);
+        uint4 raw = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * p.w + iw) * p.c));
         const T* t = reinterpret_cast<const T*>(&raw);
 #pragma unroll
         for (int j = 0; j < V; ++j) {
@@ -64,7 +63,7 @@ __global__ void max_pool_kernel(PoolParams p) {
         any = true;
       }
     }
-    T* dst = static_cast<T*>(p.y) + ((static_cast<int64_t>(n) * p.oh + oh) * p.ow + ow) * p.c + v * V;
+    T* dst = static_cast<T*>(p.y) + static_cast<int64_t>(pix) * p.c + v * V;
     if (!any) {
 #pragma unroll
       for (int j = 0; j < V; ++j) best[j] = T{};
@@ -112,7 +111,7 @@ __global__ void global_avg_pool_kernel(PoolParams p) {
 
 int grid_for(int64_t threads, int block) {
   int64_t g = (threads + block - 1) / block;
-  return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+  return static_cast<int>(g < 148 * 32 ? (g < 1 ? 1 : g) : 148 * 32);
 }
 
 }  // namespace
@@ -121,6 +120,7 @@ int grid_for(int64_t threads, int block) {
 int launch_max_pool(const PoolParams& p, cudaStream_t st) {
   const int bytes = p.type == kBF16 ? 2 : p.type == kI8 ? 1 : 4;
   if ((p.c * bytes) % 16) return -1;
+  if (static_cast<int64_t>(p.n) * p.oh * p.ow * (p.c * bytes / 16) >= (int64_t(1) << 31)) return -1;
   const int64_t threads = static_cast<int64_t>(p.n) * p.oh * p.ow * (p.c * bytes / 16);
   const int block = 256, grid = grid_for(threads, block);
   switch (p.type) {

@@ -56,6 +56,8 @@ int launch_max_pool(const PoolParams& p, cudaStream_t st);
 bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t);
 int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
                   int prog, int sms, cudaStream_t st);
+int launch_pool_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
+                    int sms, cudaStream_t st);
 int launch_global_avg_pool(const PoolParams& p, cudaStream_t st);
 }  // namespace tec_sm100
 
@@ -379,6 +381,9 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
     if (hi.bn > 64 && hi.bn > d->k) continue;
     const int th = (int)std::min<int64_t>(pl.oh, (128 * hi.ms) / wp);
     if (th < 1 || th + d->r - 1 > 256) continue;
+    // Small images waste most MMA rows on junk virtual rows / padding: keep
+    // the halo form for tiles that are at least half real outputs.
+    if (!(kn && kn->tile_k == 2) && 2 * th * pl.ow < 128 * hi.ms) continue;
     const int halo_px = 128 * hi.ms + (int)((d->r - 1) * wp + d->s) + 8;
     const int bands = (int)((pl.oh + th - 1) / th);
     const int n_tiles = (int)((d->k + hi.bn - 1) / hi.bn);
@@ -1069,6 +1074,38 @@ tec_status tec_max_pool2d(const tec_pool_desc* d, const void* x, void* y, void* 
   p.ph = (int32_t)d->pad_h; p.pw = (int32_t)d->pad_w;
   p.type = p.out_type = elem_type_of(d->dtype);
   p.x = x; p.y = y;
+  // bf16 3x3 windows: TMA-tiled kernel (NaN out-of-bounds fill, skipped by
+  // the max), the depthwise tile planner sizes the halo tiles.
+  if (p.type == kBF16 && p.r == 3 && p.s == 3 && p.sh == p.sw && (p.sw == 1 || p.sw == 2) &&
+      p.pw <= 1 && p.ph <= 1) {
+    DepthwiseParams q{};
+    q.n = p.n; q.h = p.h; q.w = p.w; q.c = p.c; q.oh = p.oh; q.ow = p.ow;
+    q.r = 3; q.s = 3; q.sh = p.sh; q.sw = p.sw; q.ph = p.ph; q.pw = p.pw;
+    q.in_type = q.out_type = kBF16;
+    q.x = x; q.y = y;
+    DwTmaShape t{};
+    const DriverFns& fns = driver_fns();
+    if (fns.ok && dw_tma_plan(q, &t)) {
+      CUtensorMap tm{};
+      cuuint64_t dims[4] = {(cuuint64_t)d->c, (cuuint64_t)d->w, (cuuint64_t)d->h, (cuuint64_t)d->n};
+      cuuint64_t strides[3] = {(cuuint64_t)(d->c * 2), (cuuint64_t)(d->c * 2 * d->w),
+                               (cuuint64_t)(d->c * 2 * d->w * d->h)};
+      cuuint32_t box[4] = {(cuuint32_t)t.cb, (cuuint32_t)t.cols_in, (cuuint32_t)t.rows_in,
+                           (cuuint32_t)t.ni};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      CUresult r = fns.tiled(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
+      if (r == CUDA_SUCCESS) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int e = launch_pool_tma(q, tm, t, sm_count(dev), (cudaStream_t)stream);
+        if (e == 0) return TEC_OK;
+        if (e != -1) return cuda_fail(e, "max_pool2d (TMA) launch");
+      }
+    }
+  }
   const int e = launch_max_pool(p, (cudaStream_t)stream);
   if (e == -1) return fail(TEC_E_LOWERING, "max_pool2d: channels x element size must be a multiple of 16 B");
   if (e) return cuda_fail(e, "max_pool2d launch");
