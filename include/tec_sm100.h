@@ -186,6 +186,30 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
                                int32_t out_dtype, int32_t* err_flag,
                                void* stream);
 
+/* ---- lowering (target "sm100"): the kernel a descriptor + knobs lower to,
+ * without launching (LowerOptions::target, R/include/tec/lower.hpp:26-33;
+ * capacity checks replace check_target). LoweringError when no kernel fits. */
+typedef enum {
+  TEC_KERNEL_IM2COL = 1,     /* conv_tc.cu: TMA im2col implicit GEMM      */
+  TEC_KERNEL_HALO = 2,       /* conv_halo.cu: shifted-window implicit GEMM */
+  TEC_KERNEL_F32_EXACT = 3,  /* conv_f32_exact.cu: SIMT, reference order  */
+  TEC_KERNEL_DW_TMA = 4,     /* depthwise_tma.cu                           */
+  TEC_KERNEL_DW_DIRECT = 5   /* depthwise.cu                               */
+} tec_kernel_family;
+
+typedef struct {
+  int32_t family;                    /* tec_kernel_family */
+  int32_t tile_m, tile_n, stages;    /* rows / output channels per tile; stages
+                                        (halo: 1 streamed, 2 resident weights) */
+  int32_t split_k, cluster;          /* K splits; CTAs sharing weights       */
+  int32_t grid;                      /* persistent CTAs (0: data-dependent)  */
+  int32_t smem_bytes, tmem_cols;     /* per-CTA on-chip budget used          */
+  int32_t tma_store;                 /* 1: TMA-store epilogue                */
+} tec_kernel_plan;
+
+tec_status tec_conv_plan(const tec_conv_desc* d, const tec_epilogue* epi,
+                         const tec_knobs* knobs, tec_kernel_plan* out);
+
 /* ---- graph operators around the conv path (ResNet-18 graph).
  * The reference has no pooling operator; these are new registered ops
  * whose semantics oracle/tec_oracle.c restates (see pool.cu). NHWC device

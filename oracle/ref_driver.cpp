@@ -14,6 +14,10 @@
 //   fuse  <graph.json> <out.json>
 //         fuse_pass (R/src/graph_passes.cpp:196) + plan_memory (:285); writes
 //         {"graph": graph_to_json(fused), "plan": {...}}.
+//   fold  <graph.json> <out.json>
+//         fold_constants (R/src/graph_passes.cpp:41-73); writes graph_to_json.
+//   layouts <graph.json> <prefs.json> <out.json>
+//         apply_layouts (R/src/graph_passes.cpp:84-178) with {node: layout}.
 //   gen   <out_dir> <name> <dtype> <seed> <d0> [d1 ...]
 //         random_tensor (R/src/tensor.cpp:74) with mt19937_64(seed), saved
 //         with save_tensor -- the reference's own synthetic distributions.
@@ -60,6 +64,22 @@ static int cmd_fuse(const std::string& gpath, const std::string& out_path) {
                {"total_bytes", p.total_bytes},
                {"naive_bytes", p.naive_bytes}};
   write_text_file(out_path, j.dump(1) + "\n");
+  return 0;
+}
+
+static int cmd_fold(const std::string& gpath, const std::string& out_path) {
+  ComputeGraph g = graph_from_json(parse_json(read_text_file(gpath), gpath));
+  write_text_file(out_path, graph_to_json(fold_constants(g)).dump(1) + "\n");
+  return 0;
+}
+
+static int cmd_layouts(const std::string& gpath, const std::string& ppath,
+                       const std::string& out_path) {
+  ComputeGraph g = graph_from_json(parse_json(read_text_file(gpath), gpath));
+  nlohmann::json pj = parse_json(read_text_file(ppath), ppath);
+  std::map<std::string, std::string> prefs;
+  for (auto it = pj.begin(); it != pj.end(); ++it) prefs[it.key()] = it.value().get<std::string>();
+  write_text_file(out_path, graph_to_json(apply_layouts(g, prefs)).dump(1) + "\n");
   return 0;
 }
 
@@ -128,6 +148,8 @@ int main(int argc, char** argv) {
     std::string cmd = argv[1];
     if (cmd == "eval" && argc == 5) return cmd_eval(argv[2], argv[3], argv[4]);
     if (cmd == "fuse" && argc == 4) return cmd_fuse(argv[2], argv[3]);
+    if (cmd == "fold" && argc == 4) return cmd_fold(argv[2], argv[3]);
+    if (cmd == "layouts" && argc == 5) return cmd_layouts(argv[2], argv[3], argv[4]);
     if (cmd == "gen" && argc >= 7) return cmd_gen(argc, argv);
     if (cmd == "bench" && argc >= 12) return cmd_bench(argc, argv);
     std::fprintf(stderr, "bad arguments for '%s'\n", cmd.c_str());

@@ -74,6 +74,13 @@ class PoolDesc(C.Structure):
                [("dtype", C.c_int32), ("out_dtype", C.c_int32)]
 
 
+class KernelPlan(C.Structure):
+    """tec_kernel_plan (include/tec_sm100.h)."""
+    _fields_ = [(f, C.c_int32) for f in ("family", "tile_m", "tile_n", "stages", "split_k",
+                                         "cluster", "grid", "smem_bytes", "tmem_cols",
+                                         "tma_store")]
+
+
 class ConvLayout(C.Structure):
     _fields_ = [("oh", C.c_int64), ("ow", C.c_int64), ("cp", C.c_int64),
                 ("act_dtype", C.c_int32), ("acc_dtype", C.c_int32),
@@ -106,6 +113,7 @@ SIGNATURES = {
     "tec_measure": (C.c_int32, [_DESC, _EPI, _KN, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.POINTER(C.c_double)]),
     "tec_pool_infer": (C.c_int32, [C.POINTER(PoolDesc), C.POINTER(C.c_int64)]),
+    "tec_conv_plan": (C.c_int32, [_DESC, _EPI, _KN, C.POINTER(KernelPlan)]),
     "tec_max_pool2d": (C.c_int32, [C.POINTER(PoolDesc), _P, _P, _P]),
     "tec_global_avg_pool": (C.c_int32, [C.POINTER(PoolDesc), _P, _P, _P]),
 }

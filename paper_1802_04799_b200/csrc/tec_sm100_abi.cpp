@@ -66,6 +66,31 @@ using namespace tec_sm100;
 namespace {
 
 thread_local std::string g_last_error;
+// tec_conv_plan: when set, the launch paths record their decision here and
+// return before launching anything.
+thread_local tec_kernel_plan* g_plan = nullptr;
+
+bool plan_only(int family, int bn, int tile_m, int stages, int grid, int smem, int tmem_cols,
+               int tma_store, int splits, int cluster) {
+  if (!g_plan) return false;
+  g_plan->family = family;
+  g_plan->tile_n = bn;
+  g_plan->tile_m = tile_m;
+  g_plan->stages = stages;
+  g_plan->grid = grid;
+  g_plan->smem_bytes = smem;
+  g_plan->tmem_cols = tmem_cols;
+  g_plan->tma_store = tma_store;
+  g_plan->split_k = splits;
+  g_plan->cluster = cluster;
+  return true;
+}
+
+int tmem_cols_for(int cols) {
+  int c = 32;
+  while (c < cols) c *= 2;
+  return c;
+}
 
 tec_status fail(tec_status code, const std::string& msg) {
   g_last_error = msg;
@@ -543,6 +568,11 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
+  if (plan_only(TEC_KERNEL_HALO, hc.inst->bn, 128 * hc.inst->ms, hc.resident ? 2 : 1, grid,
+                conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px,
+                                     p.stage_bytes),
+                tmem_cols_for(2 * hc.inst->ms * hc.inst->bn), p.tma_store, 1, hc.cl))
+    return TEC_OK;
   const int e = hc.inst->fn(tm_x, tm_w, tm_y, p, grid, st);
   if (e) return cuda_fail(e, "conv_halo launch");
   if (prof) {
@@ -752,6 +782,9 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
+  if (plan_only(TEC_KERNEL_IM2COL, bn, 128, 0, grid, 0, tmem_cols_for(2 * bn), p.tma_store,
+                p.splits, 1))
+    return TEC_OK;
   const int e = launch(tm_a, tm_b, tm_y, p, grid, st);
   if (e) return cuda_fail(e, "conv_fprop_tc launch");
   if (prof) {
@@ -940,6 +973,7 @@ tec_status tec_conv2d_fused(const tec_conv_desc* d, const tec_epilogue* epi,
     p.y = y;
     p.err = err_flag;
     p.epi = ep;
+    if (plan_only(TEC_KERNEL_F32_EXACT, 64, 64, 0, 0, 0, 0, 0, 1, 1)) return TEC_OK;
     const int e = launch_conv_f32_exact(static_cast<const float*>(x_packed),
                                         static_cast<const float*>(w_packed), p,
                                         (cudaStream_t)stream);
@@ -1012,6 +1046,8 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
       if (r == CUDA_SUCCESS) {
         int dev = 0;
         cudaGetDevice(&dev);
+        if (plan_only(TEC_KERNEL_DW_TMA, t.cb, t.th, 2, 0, 2 * t.buf_bytes + 128, 0, 0, 1, 1))
+          return TEC_OK;
         const int e = launch_dw_tma(p, tm, t, prog, sm_count(dev), (cudaStream_t)stream);
         if (e == 0) return TEC_OK;
         if (e != -1) return cuda_fail(e, "depthwise (TMA) launch");
@@ -1019,6 +1055,7 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
     }
     if (tw == 8) return fail(TEC_E_LOWERING, "TMA depthwise kernel does not apply to this layer");
   }
+  if (plan_only(TEC_KERNEL_DW_DIRECT, 0, tw == 0 ? 4 : tw, 0, 0, 0, 0, 0, 1, 1)) return TEC_OK;
   const int e = launch_depthwise(p, tw == 0 ? 4 : tw, (cudaStream_t)stream);
   if (e == -1)
     return fail(TEC_E_LOWERING, "depthwise: unsupported dtype pair or C not a multiple of the vector width");
@@ -1049,6 +1086,32 @@ tec_status pool_check(const tec_pool_desc* d, bool window) {
   return TEC_OK;
 }
 }  // namespace
+
+tec_status tec_conv_plan(const tec_conv_desc* d, const tec_epilogue* epi,
+                         const tec_knobs* knobs, tec_kernel_plan* out) {
+  if (!out) return fail(TEC_E_INTERNAL, "null plan");
+  *out = tec_kernel_plan{};
+  cudaFree(nullptr);  // tensor-map encoding needs a current context
+  tec_conv_layout lay;
+  tec_status st = tec_conv_layout_of(d, &lay);
+  if (st) return st;
+  // Operand pointers only feed tensor-map encodes here (nothing launches):
+  // any aligned address works.
+  static char dummy[256] __attribute__((aligned(256)));
+  tec_epilogue e{};
+  if (epi) {
+    e = *epi;
+    if (e.bias) e.bias = dummy;
+    if (e.residual) e.residual = dummy;
+    if (e.mul_operand) e.mul_operand = dummy;
+  }
+  const int32_t out_t = d->compute == TEC_COMPUTE_I8 ? TEC_DT_I32
+                        : d->compute == TEC_COMPUTE_BF16 ? TEC_DT_BF16 : TEC_DT_F32;
+  g_plan = out;
+  st = tec_conv2d_fused(d, epi ? &e : nullptr, knobs, dummy, dummy, dummy, out_t, nullptr, nullptr);
+  g_plan = nullptr;
+  return st;
+}
 
 tec_status tec_pool_infer(const tec_pool_desc* d, int64_t out_shape[4]) {
   tec_status st = pool_check(d, true);

@@ -561,3 +561,210 @@ def load_tensor(directory: str, name: str) -> np.ndarray:
     if a.size != int(np.prod(shape)):
         _fail(E_IO, f"{name}.bin holds {a.size} elements, manifest says {shape}")
     return a.reshape(shape).astype({"f32": np.float32, "i32": np.int32, "i8": np.int8}[dt])
+
+
+# ------------------------------------------------------- fold_constants
+E_FOLD_OVERFLOW = 3
+_I32 = (np.iinfo(np.int32).min, np.iinfo(np.int32).max)
+
+
+def _check_i32(v: np.ndarray, what: str) -> np.ndarray:
+    if v.size and (v.min() < _I32[0] or v.max() > _I32[1]):
+        _fail(E_FOLD_OVERFLOW, f"value out of range for i32 folding {what}")
+    return v
+
+
+def _libm_expf(x: np.ndarray) -> np.ndarray:
+    """std::exp on float (the reference's kExp, R/src/expr.cpp:155-156) via
+    the C library itself, so folded results match it bit for bit."""
+    import ctypes
+    import ctypes.util
+    lib = ctypes.CDLL(ctypes.util.find_library("m") or "libm.so.6")
+    lib.expf.restype = ctypes.c_float
+    lib.expf.argtypes = [ctypes.c_float]
+    flat = np.ascontiguousarray(x, dtype=np.float32).ravel()
+    return np.array([lib.expf(float(v)) for v in flat], dtype=np.float32).reshape(x.shape)
+
+
+def _fold_eval(n: GraphNode, ins: List[np.ndarray]) -> np.ndarray:
+    """Compile-time evaluation of one node whose inputs are all constants.
+    Elementwise / reduction / layout ops follow the reference's host
+    semantics (float ops rounded per operation, integer ops in 64 bits with
+    the i32 range check, R/src/expr.cpp:95-167); conv / matmul / pool nodes
+    run through the device executor's bit-exact f32 path."""
+    op = n.op
+    isf = ins[0].dtype == np.float32 if ins else True
+    if op in ("add", "mul"):
+        a, b = ins
+        if isf:
+            return (a + b) if op == "add" else (a * b)
+        v = (a.astype(np.int64) + b) if op == "add" else (a.astype(np.int64) * b)
+        return _check_i32(v, n.id).astype(a.dtype if a.dtype == np.int32 else np.int32)
+    if op == "relu":
+        x = ins[0]
+        return np.where(x < 0, np.zeros_like(x), x)
+    if op == "exp":
+        return _libm_expf(ins[0])
+    if op == "sqrt":
+        return np.sqrt(ins[0].astype(np.float32))
+    if op == "scale":
+        c = float(n.attrs.get("scale", 1.0))
+        if isf:
+            return ins[0] * np.float32(c)
+        return _check_i32(ins[0].astype(np.int64) * int(c), n.id).astype(np.int32)
+    if op == "bias_add":
+        x, b = ins
+        ax = int(n.attrs.get("axis", 1 if x.ndim >= 2 else 0))
+        shape = [1] * x.ndim
+        shape[ax] = -1
+        if isf:
+            return x + b.reshape(shape)
+        return _check_i32(x.astype(np.int64) + b.reshape(shape), n.id).astype(np.int32)
+    if op == "sum":
+        x = ins[0]
+        ax = int(n.attrs.get("axis", x.ndim - 1))
+        if isf:  # sequential accumulation from 0, rounded per add
+            acc = np.zeros(np.delete(x.shape, ax), np.float32)
+            for i in range(x.shape[ax]):
+                acc = acc + np.take(x, i, axis=ax)
+            out = acc
+        else:
+            out = _check_i32(x.astype(np.int64).sum(axis=ax), n.id).astype(np.int32)
+        return out.reshape(n.out_type.shape)
+    if op == "layout_transform":
+        x = ins[0]
+        src, dst = n.attrs.get("src_layout", "row_major"), n.attrs.get("dst_layout", "row_major")
+        if src == dst:
+            return x.copy()
+        if src == "row_major":
+            h, w = x.shape
+            out = np.zeros(n.out_type.shape, x.dtype)
+            for i in range(h):
+                for j in range(w):
+                    out[i // 4, j // 4, i % 4, j % 4] = x[i, j]
+            return out
+        h, w = n.out_type.shape
+        return np.array([[x[i // 4, j // 4, i % 4, j % 4] for j in range(w)] for i in range(h)],
+                        dtype=x.dtype)
+    # conv / matmul / fused / pools: one-node graph on the device (f32 exact)
+    from .executor import DeviceGraph
+    names = [f"__c{i}" for i in range(len(ins))]
+    nodes = [GraphNode(nm, "input", out_type=TensorType(list(a.shape),
+                                                        {np.dtype(np.float32): "f32",
+                                                         np.dtype(np.int32): "i32",
+                                                         np.dtype(np.int8): "i8"}[a.dtype]))
+             for nm, a in zip(names, ins)]
+    node = copy.deepcopy(n)
+    node.inputs = names
+    if node.op == "fused":
+        ren = dict(zip(n.inputs, names))
+        for m in node.members:
+            m.inputs = [ren.get(i, i) for i in m.inputs]
+    g = ComputeGraph(nodes + [node], [node.id])
+    g.validate()
+    dg = DeviceGraph(g, compute="f32")
+    dg.bind_params({k: v for k, v in zip(names, ins) if k in dg.param_names})
+    return dg.run({k: v for k, v in zip(names, ins) if k in dg.feed_names})[node.id]
+
+
+def _strip_dead(g: ComputeGraph) -> ComputeGraph:
+    live = set(g.outputs)
+    for n in reversed(g.nodes):
+        if n.id in live:
+            live.update(n.inputs)
+    return ComputeGraph([n for n in g.nodes if n.id in live], list(g.outputs))
+
+
+def fold_constants(g: ComputeGraph) -> ComputeGraph:
+    """graph_passes.cpp:41-73: nodes whose inputs are all constants are
+    evaluated and replaced by const nodes; unreferenced nodes are dropped.
+    Folding through a const without payload is NotEnoughData; integer
+    overflow is FoldOverflow."""
+    out = ComputeGraph([], list(g.outputs))
+    consts: Dict[str, GraphNode] = {}
+    for n in g.nodes:
+        copy_n = copy.deepcopy(n)
+        foldable = n.op not in ("input", "const") and n.inputs and \
+            all(i in consts for i in n.inputs)
+        if foldable:
+            ins = []
+            for i in n.inputs:
+                c = consts[i]
+                if c.data is None:
+                    _fail(E_NOT_ENOUGH_DATA, f"cannot fold through const '{i}' with no data")
+                ins.append(c.data)
+            v = np.ascontiguousarray(_fold_eval(n, ins))
+            copy_n = GraphNode(n.id, "const", out_type=TensorType(list(v.shape), n.out_type.dtype),
+                               data=v)
+        out.nodes.append(copy_n)
+        if copy_n.op == "const":
+            consts[copy_n.id] = copy_n
+    out = _strip_dead(out)
+    out.validate()
+    return out
+
+
+# -------------------------------------------------------- apply_layouts
+_LAYOUT_ELEMWISE = ("add", "mul", "exp", "sqrt", "relu", "scale")
+
+
+def apply_layouts(g: ComputeGraph, prefs: Dict[str, str]) -> ComputeGraph:
+    """graph_passes.cpp:84-178: realise per-node layout preferences
+    ("row_major" | "tiled4x4") by inserting layout_transform nodes; graph
+    outputs stay row-major by contract."""
+    for nid, pf in prefs.items():
+        if pf not in ("row_major", "tiled4x4"):
+            _fail(E_SHAPE, f"unknown layout preference '{pf}'")
+        if pf == "row_major":
+            continue
+        n = g.node(nid)
+        if n.op not in _LAYOUT_ELEMWISE:
+            _fail(E_SHAPE, f"tiled4x4 preference on '{nid}' ({n.op}): only elementwise ops can carry it")
+        if n.out_type.rank() != 2:
+            _fail(E_SHAPE, f"tiled4x4 preference on '{nid}' needs a rank-2 tensor")
+    pref_of = lambda i: prefs.get(i, "row_major")  # noqa: E731
+    out = ComputeGraph([], list(g.outputs))
+    rm_type = {n.id: n.out_type for n in g.nodes}
+    realized: Dict[Tuple[str, str], str] = {}
+    for n in g.nodes:
+        pf = pref_of(n.id)
+        run_id = n.id + "#t" if pf == "tiled4x4" else n.id
+        c = copy.deepcopy(n)
+        c.id = run_id
+        c.out_type = TensorType()
+        if n.op in ("input", "const"):
+            c.out_type = copy.deepcopy(n.out_type)
+            out.nodes.append(c)
+            realized[(n.id, "row_major")] = n.id
+            continue
+        new_inputs = []
+        for i in c.inputs:
+            key = (i, pf)
+            if key in realized:
+                new_inputs.append(realized[key])
+                continue
+            rt = rm_type[i]
+            if pf == "tiled4x4":
+                tr = GraphNode(i + "#t", "layout_transform", [realized[(i, "row_major")]],
+                               {"src_layout": "row_major", "dst_layout": "tiled4x4"})
+            else:
+                tr = GraphNode(i + "#r", "layout_transform", [realized[(i, "tiled4x4")]],
+                               {"src_layout": "tiled4x4", "dst_layout": "row_major",
+                                "height": rt.shape[0], "width": rt.shape[1]})
+            realized[key] = tr.id
+            new_inputs.append(tr.id)
+            out.nodes.append(tr)
+        c.inputs = new_inputs
+        out.nodes.append(c)
+        realized[(n.id, pf)] = run_id
+    for o in out.outputs:
+        if (o, "row_major") in realized:
+            continue
+        rt = rm_type[o]
+        out.nodes.append(GraphNode(o, "layout_transform", [realized[(o, "tiled4x4")]],
+                                   {"src_layout": "tiled4x4", "dst_layout": "row_major",
+                                    "height": rt.shape[0], "width": rt.shape[1]}))
+        realized[(o, "row_major")] = o
+    out = _strip_dead(out)
+    out.validate()
+    return out

@@ -239,6 +239,96 @@ def build_graph_case(name, g, evaluate, seed=100):
     print(f"graphs/{name}: {'evaluated' if evaluate else 'passes only'}")
 
 
+# ----------------------------------------------------- graph passes
+# tests/golden/passes/<name>/: graph.json (+ prefs.json) and the reference's
+# fold_constants / apply_layouts result (fold.json / layouts.json, or
+# fold.status with the error when the reference throws).
+def _const(nid, arr, dtype):
+    import base64
+    raw = np.ascontiguousarray(arr).astype({"f32": "<f4", "i32": "<i4", "i8": "i1"}[dtype]).tobytes()
+    return {"id": nid, "op": "const", "shape": list(arr.shape), "dtype": dtype,
+            "data": base64.b64encode(raw).decode()}
+
+
+def pass_cases():
+    rng = np.random.default_rng(123)
+    f = lambda *s: rng.uniform(-2, 2, s).astype(np.float32)  # noqa: E731
+    i = lambda *s: rng.integers(-1000, 1000, s).astype(np.int32)  # noqa: E731
+    elem = {"nodes": [_const("c1", f(2, 3), "f32"), _const("c2", f(2, 3), "f32"),
+                      {"id": "x", "op": "input", "shape": [2, 3], "dtype": "f32"},
+                      {"id": "a", "op": "add", "inputs": ["c1", "c2"]},
+                      {"id": "m", "op": "mul", "inputs": ["a", "c2"]},
+                      {"id": "r", "op": "relu", "inputs": ["m"]},
+                      {"id": "s", "op": "scale", "inputs": ["r"], "attrs": {"scale": 0.3}},
+                      {"id": "e", "op": "exp", "inputs": ["s"]},
+                      {"id": "q", "op": "sqrt", "inputs": ["e"]},
+                      {"id": "y", "op": "add", "inputs": ["x", "q"]}], "outputs": ["y"]}
+    ints = {"nodes": [_const("k1", i(3, 4), "i32"), _const("k2", i(3, 4), "i32"),
+                      _const("kb", i(4), "i32"),
+                      {"id": "x", "op": "input", "shape": [3], "dtype": "i32"},
+                      {"id": "p", "op": "mul", "inputs": ["k1", "k2"]},
+                      {"id": "s", "op": "scale", "inputs": ["p"], "attrs": {"scale": 3.0}},
+                      {"id": "b", "op": "bias_add", "inputs": ["s", "kb"]},
+                      {"id": "t", "op": "sum", "inputs": ["b"], "attrs": {"axis": 1}},
+                      {"id": "y", "op": "add", "inputs": ["x", "t"]}], "outputs": ["y"]}
+    seq = {"nodes": [_const("v", f(4, 33) * 1000, "f32"),
+                     {"id": "x", "op": "input", "shape": [4], "dtype": "f32"},
+                     {"id": "t", "op": "sum", "inputs": ["v"], "attrs": {"axis": 1}},
+                     {"id": "y", "op": "mul", "inputs": ["x", "t"]}], "outputs": ["y"]}
+    ovf = {"nodes": [_const("k", np.full((2,), 2_000_000_000, np.int32), "i32"),
+                     {"id": "x", "op": "input", "shape": [2], "dtype": "i32"},
+                     {"id": "d", "op": "add", "inputs": ["k", "k"]},
+                     {"id": "y", "op": "add", "inputs": ["x", "d"]}], "outputs": ["y"]}
+    conv = {"nodes": [_const("w", f(4, 2, 3, 3), "f32"), _const("cx", f(1, 2, 5, 5), "f32"),
+                      _const("b", f(4), "f32"),
+                      {"id": "x", "op": "input", "shape": [1, 4, 5, 5], "dtype": "f32"},
+                      {"id": "c", "op": "conv2d", "inputs": ["cx", "w"],
+                       "attrs": {"strides": [1, 1], "padding": [1, 1]}},
+                      {"id": "cb", "op": "bias_add", "inputs": ["c", "b"]},
+                      {"id": "y", "op": "add", "inputs": ["x", "cb"]}], "outputs": ["y"]}
+    lay = {"nodes": [{"id": "x", "op": "input", "shape": [5, 6], "dtype": "f32"},
+                     {"id": "z", "op": "input", "shape": [5, 6], "dtype": "f32"},
+                     {"id": "r", "op": "relu", "inputs": ["x"]},
+                     {"id": "a", "op": "add", "inputs": ["r", "z"]},
+                     {"id": "s", "op": "scale", "inputs": ["a"], "attrs": {"scale": 2.0}}],
+           "outputs": ["s"]}
+    return [("fold_elemwise", elem, None), ("fold_int", ints, None), ("fold_seq_sum", seq, None),
+            ("fold_overflow", ovf, None), ("fold_conv", conv, None),
+            ("layouts_tiled", lay, {"r": "tiled4x4", "a": "tiled4x4"})]
+
+
+def build_pass_case(name, g, prefs, seed=500):
+    """fold cases: the reference's evaluate_graph of the ORIGINAL graph
+    (inputs + out/, or out.status when it throws). The reference's own
+    fold_constants is not used as a golden: it keeps pointers into the node
+    vector it is still appending to (R/src/graph_passes.cpp:46-70), so it
+    reads freed memory once the vector grows (reports NotEnoughData here).
+    layout cases: the reference's apply_layouts result (layouts.json)."""
+    d = os.path.join(HERE, "passes", name)
+    if os.path.exists(d):
+        shutil.rmtree(d)
+    os.makedirs(os.path.join(d, "out"))
+    gp = os.path.join(d, "graph.json")
+    with open(gp, "w") as fh:
+        json.dump(g, fh, indent=1)
+    if prefs is None:
+        for n in g["nodes"]:
+            if n["op"] == "input":
+                seed += 1
+                run([DRIVER, "gen", d, n["id"], n.get("dtype", "f32"), str(seed)] +
+                    [str(v) for v in n["shape"]])
+        pr = subprocess.run([DRIVER, "eval", gp, d, os.path.join(d, "out")],
+                            capture_output=True, text=True)
+        with open(os.path.join(d, "out.status"), "w") as fh:
+            fh.write(("ok" if pr.returncode == 0 else pr.stderr.strip()) + "\n")
+    else:
+        pp = os.path.join(d, "prefs.json")
+        with open(pp, "w") as fh:
+            json.dump(prefs, fh)
+        run([DRIVER, "layouts", gp, pp, os.path.join(d, "layouts.json")])
+    print(f"passes/{name}")
+
+
 def main():
     if not os.path.exists(DRIVER):
         sys.exit(f"{DRIVER} missing: run `make -C oracle ref` first")
@@ -249,6 +339,9 @@ def main():
     for name, g, ev in graph_cases():
         if not only or name in only:
             build_graph_case(name, g, ev)
+    for name, g, prefs in pass_cases():
+        if not only or name in only:
+            build_pass_case(name, g, prefs)
 
 
 if __name__ == "__main__":
