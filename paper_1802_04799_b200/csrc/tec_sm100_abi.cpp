@@ -422,9 +422,7 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
     // Epilogue term: the group-staged TMA-store path (run_conv_halo) moves
     // ~48 B/cycle of output, the SIMT fallback ~12 (measured, round 1).
     const int rowb = 32 * elem_bytes(out_dtype);
-    const bool tma_epi = 2 * hi.ms * 128 * rowb <= kStageMin && (wp * rowb) % 128 == 0;
-    const double epi = (double)th * pl.ow * std::min<int64_t>(hi.bn, d->k) *
-                       elem_bytes(out_dtype) / (tma_epi ? 48.0 : 12.0);
+    const int cbytes = hi.ms * 128 * rowb;  // one 32-column chunk of a tile
     // knob `stages`: 0 auto, 1 streamed weight ring, 2 resident weights
     for (int res = 0; res < 2; ++res) {
       if (kn && kn->stages == 1 && res) continue;
@@ -436,6 +434,13 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
                      hi.ms, hi.swz, res, th,
                      conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin));
       if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin) > kSmemMax) continue;
+      // The TMA-store epilogue needs one chunk per epilogue group in the stage.
+      const bool tma_epi =
+          (wp * rowb) % 128 == 0 &&
+          conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, std::max(kStageMin, 2 * cbytes)) <=
+              kSmemMax;
+      const double epi = (double)th * pl.ow * std::min<int64_t>(hi.bn, d->k) *
+                         elem_bytes(out_dtype) / (tma_epi ? 48.0 : 12.0);
       // knob cluster_n: 0 / 1 no multicast, 2 weight multicast over CTA
       // pairs. Not chosen automatically: measured slower on ResNet layers
       // (the pair runs in lockstep on the weight ring), so only the tuner
@@ -545,13 +550,16 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     const int rowb = 32 * elem_bytes(out_dtype);
     bool ok = false;
     const int cbytes = hc.inst->ms * 128 * rowb;
-    if (2 * cbytes <= kStageMin && (wp * rowb) % 128 == 0)
+    const int stage1 = std::max(kStageMin, 2 * cbytes);  // one chunk per group
+    if ((wp * rowb) % 128 == 0 &&
+        conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, stage1) <=
+            kSmemMax)
       make_store_map(&tm_y, y, out_dtype, 4, dims, (int)pl.ow, &ok);
     else std::memset(&tm_y, 0, sizeof(tm_y));
     // Room left in shared memory -> a 2-chunk ring per group, so one chunk
     // is written while the previous one's TMA stores drain.
-    p.stage_bytes = kStageMin;
-    if (ok && 4 * cbytes > kStageMin &&
+    p.stage_bytes = ok ? stage1 : kStageMin;
+    if (ok && 4 * cbytes > p.stage_bytes &&
         conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, 4 * cbytes) <=
             kSmemMax)
       p.stage_bytes = 4 * cbytes;
