@@ -229,6 +229,45 @@ tec_status tec_max_pool2d(const tec_pool_desc* d, const void* x, void* y, void* 
 tec_status tec_global_avg_pool(const tec_pool_desc* d, const void* x, void* y, void* stream);
 tec_status tec_pool_infer(const tec_pool_desc* d, int64_t out_shape[4]);
 
+/* ---- native launch plans: the executor's run loop (evaluate_graph for
+ * target sm100, R/src/graph.cpp:227-256). A compiled graph is a list of
+ * steps on caller-owned device buffers; the plan runs them in order or
+ * captures them ONCE into a CUDA graph and replays that. */
+typedef enum {
+  TEC_STEP_CONV = 1,       /* tec_conv2d_fused                              */
+  TEC_STEP_MAX_POOL = 2,   /* tec_max_pool2d                                */
+  TEC_STEP_AVG_POOL = 3,   /* tec_global_avg_pool                           */
+  TEC_STEP_PACK = 4,       /* tec_activation_pack(conv, src -> dst)         */
+  TEC_STEP_UNPACK = 5,     /* tec_output_unpack(src, src_dtype -> dst)      */
+  TEC_STEP_TO_NHWC = 6,    /* tec_nchw_to_nhwc(src, src_dtype -> dst)       */
+  TEC_STEP_DEPTHWISE = 7   /* tec_depthwise_fused                           */
+} tec_step_kind;
+
+typedef struct {
+  int32_t kind;            /* tec_step_kind */
+  int32_t src_dtype, dst_dtype;
+  tec_conv_desc conv;      /* CONV, DEPTHWISE, PACK */
+  tec_epilogue epi;        /* CONV, DEPTHWISE (device operand pointers)     */
+  tec_knobs knobs;         /* CONV, DEPTHWISE */
+  tec_pool_desc pool;      /* MAX_POOL, AVG_POOL */
+  const void* src;         /* input (x / NCHW source)                       */
+  const void* w;           /* CONV, DEPTHWISE: packed weights               */
+  void* dst;               /* output                                        */
+  int64_t n, c, h, w_;     /* UNPACK / TO_NHWC logical NCHW dims            */
+} tec_step;
+
+typedef struct tec_plan tec_plan;
+/* Copies the steps; LoweringError if a conv step has no kernel. */
+tec_status tec_plan_create(const tec_step* steps, int32_t n_steps, tec_plan** out);
+/* Enqueues the plan on `stream`: the captured CUDA graph when there is one,
+ * otherwise every step in order. */
+tec_status tec_plan_run(tec_plan* plan, void* stream);
+/* Runs the steps once eagerly (first-use setup), then captures them into a
+ * CUDA graph that later tec_plan_run calls replay. */
+tec_status tec_plan_capture(tec_plan* plan, void* stream);
+int32_t tec_plan_size(const tec_plan* plan);
+void tec_plan_destroy(tec_plan* plan);
+
 /* ---- host-level path: eval_graph_node / native_eval for target sm100 ----
  * x: NCHW f32 (i8 for I8); w: OIHW f32 (i8); epilogue operands NCHW f32
  * (i32); y: NCHW f32 (i32). All HOST pointers; copies included. */

@@ -88,6 +88,18 @@ class ConvLayout(C.Structure):
                 ("out_elems", C.c_int64)]
 
 
+STEP_CONV, STEP_MAX_POOL, STEP_AVG_POOL, STEP_PACK, STEP_UNPACK, STEP_TO_NHWC, STEP_DEPTHWISE = \
+    1, 2, 3, 4, 5, 6, 7
+
+
+class Step(C.Structure):
+    """tec_step (include/tec_sm100.h): one launch of a native plan."""
+    _fields_ = [("kind", C.c_int32), ("src_dtype", C.c_int32), ("dst_dtype", C.c_int32),
+                ("conv", ConvDesc), ("epi", Epilogue), ("knobs", Knobs), ("pool", PoolDesc),
+                ("src", C.c_void_p), ("w", C.c_void_p), ("dst", C.c_void_p),
+                ("n", C.c_int64), ("c", C.c_int64), ("h", C.c_int64), ("w_", C.c_int64)]
+
+
 # Every symbol include/tec_sm100.h declares, with its ctypes signature.
 _P = C.c_void_p
 _DESC = C.POINTER(ConvDesc)
@@ -116,6 +128,11 @@ SIGNATURES = {
     "tec_conv_plan": (C.c_int32, [_DESC, _EPI, _KN, C.POINTER(KernelPlan)]),
     "tec_max_pool2d": (C.c_int32, [C.POINTER(PoolDesc), _P, _P, _P]),
     "tec_global_avg_pool": (C.c_int32, [C.POINTER(PoolDesc), _P, _P, _P]),
+    "tec_plan_create": (C.c_int32, [C.POINTER(Step), C.c_int32, C.POINTER(C.c_void_p)]),
+    "tec_plan_run": (C.c_int32, [_P, _P]),
+    "tec_plan_capture": (C.c_int32, [_P, _P]),
+    "tec_plan_size": (C.c_int32, [_P]),
+    "tec_plan_destroy": (None, [_P]),
 }
 
 _lib = None

@@ -1341,3 +1341,116 @@ tec_status tec_measure(const tec_conv_desc* d, const tec_epilogue* epi,
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- native launch plans
+struct tec_plan {
+  std::vector<tec_step> steps;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+namespace {
+tec_status run_step(const tec_step& s, void* stream) {
+  switch (s.kind) {
+    case TEC_STEP_CONV:
+      return tec_conv2d_fused(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype, nullptr,
+                              stream);
+    case TEC_STEP_DEPTHWISE:
+      return tec_depthwise_fused(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype,
+                                 nullptr, stream);
+    case TEC_STEP_MAX_POOL:
+      return tec_max_pool2d(&s.pool, s.src, s.dst, stream);
+    case TEC_STEP_AVG_POOL:
+      return tec_global_avg_pool(&s.pool, s.src, s.dst, stream);
+    case TEC_STEP_PACK:
+      return tec_activation_pack(&s.conv, s.src, s.dst, stream);
+    case TEC_STEP_UNPACK:
+      return tec_output_unpack(s.src, s.src_dtype, s.dst, s.dst_dtype, s.n, s.c, s.h, s.w_, stream);
+    case TEC_STEP_TO_NHWC:
+      return tec_nchw_to_nhwc(s.src, s.src_dtype, s.dst, s.dst_dtype, s.n, s.c, s.h, s.w_, stream);
+    default:
+      return fail(TEC_E_INTERNAL, "unknown plan step kind " + std::to_string(s.kind));
+  }
+}
+
+tec_status run_steps(const tec_plan* p, void* stream) {
+  for (size_t i = 0; i < p->steps.size(); ++i) {
+    tec_status st = run_step(p->steps[i], stream);
+    if (st) {
+      g_last_error = "plan step " + std::to_string(i) + ": " + g_last_error;
+      return st;
+    }
+  }
+  return TEC_OK;
+}
+}  // namespace
+
+extern "C" {
+tec_status tec_plan_create(const tec_step* steps, int32_t n_steps, tec_plan** out) {
+  if (!out || (n_steps > 0 && !steps) || n_steps < 0) return fail(TEC_E_INTERNAL, "bad plan arguments");
+  auto* p = new tec_plan;
+  p->steps.assign(steps, steps + n_steps);
+  for (int32_t i = 0; i < n_steps; ++i) {
+    if (steps[i].kind != TEC_STEP_CONV && steps[i].kind != TEC_STEP_DEPTHWISE) continue;
+    tec_kernel_plan kp;
+    tec_status st = tec_conv_plan(&steps[i].conv, &steps[i].epi, &steps[i].knobs, &kp);
+    if (st) {
+      delete p;
+      g_last_error = "plan step " + std::to_string(i) + ": " + g_last_error;
+      return st;
+    }
+  }
+  *out = p;
+  return TEC_OK;
+}
+
+tec_status tec_plan_run(tec_plan* p, void* stream) {
+  if (!p) return fail(TEC_E_INTERNAL, "null plan");
+  if (p->exec) {
+    TEC_CUDA(cudaGraphLaunch(p->exec, (cudaStream_t)stream));
+    return TEC_OK;
+  }
+  return run_steps(p, stream);
+}
+
+tec_status tec_plan_capture(tec_plan* p, void* stream) {
+  if (!p) return fail(TEC_E_INTERNAL, "null plan");
+  if (p->exec) {
+    cudaGraphExecDestroy(p->exec);
+    cudaGraphDestroy(p->graph);
+    p->exec = nullptr;
+    p->graph = nullptr;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  tec_status st = run_steps(p, stream);  // eager pass: attributes, split-K workspace
+  if (st) return st;
+  TEC_CUDA(cudaStreamSynchronize(s));
+  TEC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  st = run_steps(p, stream);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s, &g);
+  if (st) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+  if (ie != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return cuda_fail(ie, "cudaGraphInstantiate");
+  }
+  p->graph = g;
+  p->exec = exec;
+  return TEC_OK;
+}
+
+int32_t tec_plan_size(const tec_plan* p) { return p ? (int32_t)p->steps.size() : 0; }
+
+void tec_plan_destroy(tec_plan* p) {
+  if (!p) return;
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  delete p;
+}
+}  // extern "C"

@@ -19,7 +19,10 @@ list of kernel launches on device buffers:
     kernels' NHWC layout between nodes -- a layout change (NHWC <-> the
     packed input of the next conv) is inserted only where a consumer needs
     one (the stem's space-to-depth pack; the f32 parity path's NCHW input);
-  * the launch list is replayed directly or captured into a CUDA graph.
+  * the launch list is a native plan (tec_plan_create, tec_sm100_abi.cpp):
+    an array of tec_step records the C++ runtime walks, or captures once
+    into a CUDA graph (tec_plan_capture) and replays -- no Python per
+    launch.
 
 Compute modes: "bf16" (activations bf16 NHWC, f32 accumulate; graph outputs
 f32) and "f32" (the bit-exact SIMT path: every conv equals the reference's
@@ -140,7 +143,7 @@ class DeviceGraph:
         self.g = _resolve_aliases(self.fused)
         self.outputs = list(self.g.outputs)
         self._classify_inputs()
-        self.steps: List[Callable[[int], None]] = []
+        self.steps: List[_abi.Step] = []
         self.tensors: Dict[str, DevTensor] = {}
         self.params: Dict[str, torch.Tensor] = {}
         self.param_prep: List[Callable[[int], None]] = []
@@ -148,7 +151,22 @@ class DeviceGraph:
         self.keep: list = []
         self._plan()
         self._compile()
-        self.cuda_graph = None
+        self._native = None
+        self._captured = False
+        self._make_plan()
+
+    def _make_plan(self):
+        arr = (_abi.Step * max(len(self.steps), 1))(*self.steps)
+        h = C.c_void_p()
+        with torch.cuda.device(self.dev):
+            _abi.check(self.lib.tec_plan_create(arr, len(self.steps), C.byref(h)))
+        self._native = h
+
+    def __del__(self):
+        h = getattr(self, "_native", None)
+        if h is not None and h.value:
+            self.lib.tec_plan_destroy(h)
+            self._native = None
 
     # ------------------------------------------------------------ analysis
     def _classify_inputs(self):
@@ -266,21 +284,14 @@ class DeviceGraph:
         else:
             n_, c_, h_, w_ = src.nchw4
             nchw = self._scratch(n_ * c_ * h_ * w_ * 4)
-            sdt, sp = src.dtype, src.ptr
-
-            def unpack(st, sp=sp, sdt=sdt, nchw=nchw, shp=(n_, c_, h_, w_)):
-                _abi.check(self.lib.tec_output_unpack(sp(), sdt, nchw.data_ptr(), _abi.DT_F32,
-                                                      *shp, st))
-            self.steps.append(unpack)
+            self.steps.append(_abi.Step(kind=_abi.STEP_UNPACK, src_dtype=src.dtype,
+                                        dst_dtype=_abi.DT_F32, src=src.ptr(),
+                                        dst=nchw.data_ptr(), n=n_, c=c_, h=h_, w_=w_))
         if self.cmode == _abi.COMPUTE_F32 and not d.depthwise:
             return nchw.data_ptr()  # the exact path reads NCHW f32 as is
         packed = self._scratch(lay.act_bytes)
-        dd = d
-
-        def pack(st, nchw=nchw, packed=packed, dd=dd):
-            _abi.check(self.lib.tec_activation_pack(C.byref(dd), nchw.data_ptr(),
-                                                    packed.data_ptr(), st))
-        self.steps.append(pack)
+        self.steps.append(_abi.Step(kind=_abi.STEP_PACK, conv=d, src=nchw.data_ptr(),
+                                    dst=packed.data_ptr()))
         return packed.data_ptr()
 
     def _compile_conv(self, n: GraphNode):
@@ -329,14 +340,9 @@ class DeviceGraph:
                     epi.mul_operand = r.ptr()
         epi.n_ops = len(items)
         kn = _abi.Knobs(**self.knobs.get(n.id, {}))
-        fn = self.lib.tec_depthwise_fused if d.depthwise else self.lib.tec_conv2d_fused
-        self.keep += [d, epi, kn]
-        yptr = y.data_ptr()
-
-        def launch(st, d=d, epi=epi, kn=kn, xptr=xptr, wpk=wpk, yptr=yptr, out_dt=out_dt):
-            _abi.check(fn(C.byref(d), C.byref(epi), C.byref(kn), xptr, wpk.data_ptr(), yptr,
-                          out_dt, None, st))
-        self.steps.append(launch)
+        self.steps.append(_abi.Step(kind=_abi.STEP_DEPTHWISE if d.depthwise else _abi.STEP_CONV,
+                                    dst_dtype=out_dt, conv=d, epi=epi, knobs=kn, src=xptr,
+                                    w=wpk.data_ptr(), dst=y.data_ptr()))
         shape = list(n.out_type.shape)
         self.tensors[n.id] = DevTensor(y, shape, out_dt, "nhwc")
 
@@ -375,9 +381,9 @@ class DeviceGraph:
         n_, c_, h_, w_ = src.nchw4
         out = self._scratch(n_ * c_ * h_ * w_ * _BYTES[self.act_dt]).view(_TORCH[self.act_dt])
 
-        def conv_(st, sp=src.ptr, out=out, shp=(n_, c_, h_, w_), sdt=src.dtype):
-            _abi.check(self.lib.tec_nchw_to_nhwc(sp(), sdt, out.data_ptr(), self.act_dt, *shp, st))
-        self.steps.append(conv_)
+        self.steps.append(_abi.Step(kind=_abi.STEP_TO_NHWC, src_dtype=src.dtype,
+                                    dst_dtype=self.act_dt, src=src.ptr(), dst=out.data_ptr(),
+                                    n=n_, c=c_, h=h_, w_=w_))
         return DevTensor(out, src.shape, self.act_dt, "nhwc")
 
     def _compile_maxpool(self, n: GraphNode):
@@ -392,11 +398,8 @@ class DeviceGraph:
         y = self._out_buffer(n, x.dtype, n.out_type.num_elements())
         if n.id in self.outputs:
             raise TecError(E_LOWERING, "max_pool2d as a graph output")
-        self.keep.append(pdsc)
-
-        def launch(st, pdsc=pdsc, xp=x.ptr, y=y):
-            _abi.check(self.lib.tec_max_pool2d(C.byref(pdsc), xp(), y.data_ptr(), st))
-        self.steps.append(launch)
+        self.steps.append(_abi.Step(kind=_abi.STEP_MAX_POOL, pool=pdsc, src=x.ptr(),
+                                    dst=y.data_ptr()))
         self.tensors[n.id] = DevTensor(y, list(n.out_type.shape), x.dtype, "nhwc")
 
     def _compile_avgpool(self, n: GraphNode, src: DevTensor):
@@ -406,11 +409,8 @@ class DeviceGraph:
         pdsc = _abi.PoolDesc(n=nn, c=c, h=h, w=w, r=1, s=1, stride_h=1, stride_w=1,
                              pad_h=0, pad_w=0, dtype=x.dtype, out_dtype=out_dt)
         y = self._out_buffer(n, out_dt, nn * c)
-        self.keep.append(pdsc)
-
-        def launch(st, pdsc=pdsc, xp=x.ptr, y=y):
-            _abi.check(self.lib.tec_global_avg_pool(C.byref(pdsc), xp(), y.data_ptr(), st))
-        self.steps.append(launch)
+        self.steps.append(_abi.Step(kind=_abi.STEP_AVG_POOL, pool=pdsc, src=x.ptr(),
+                                    dst=y.data_ptr()))
         self.tensors[n.id] = DevTensor(y, list(n.out_type.shape), out_dt, "nhwc")
 
     # ------------------------------------------------------------ execution
@@ -422,7 +422,6 @@ class DeviceGraph:
         with torch.cuda.device(self.dev):
             for prep in self.param_prep:
                 prep(params, st)
-        self.cuda_graph = None
 
     def set_feed(self, name: str, value, stream: Optional[torch.cuda.Stream] = None) -> None:
         t = self.feeds[name]
@@ -434,26 +433,24 @@ class DeviceGraph:
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Enqueue every step on `stream` (device-resident feeds)."""
         s = stream or torch.cuda.current_stream(self.dev)
-        if self.cuda_graph is not None:
-            with torch.cuda.stream(s):
-                self.cuda_graph.replay()
-            return
-        for step in self.steps:
-            step(s.cuda_stream)
+        with torch.cuda.device(self.dev):
+            _abi.check(self.lib.tec_plan_run(self._native, C.c_void_p(s.cuda_stream)))
 
     def capture(self) -> None:
-        """Capture the launch list into a CUDA graph (replayed by launch)."""
+        """Capture the launch list into a CUDA graph that launch() replays
+        (tec_plan_capture: one eager pass, then stream capture). Buffers and
+        parameters are bound by address, so re-binding parameters or feeds
+        keeps the captured graph valid."""
         s = torch.cuda.Stream(self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
-        with torch.cuda.stream(s):
-            for step in self.steps:  # warm-up outside capture (lazy init)
-                step(s.cuda_stream)
+        with torch.cuda.device(self.dev):
+            _abi.check(self.lib.tec_plan_capture(self._native, C.c_void_p(s.cuda_stream)))
         torch.cuda.current_stream(self.dev).wait_stream(s)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            for step in self.steps:
-                step(s.cuda_stream)
-        self.cuda_graph = g
+        self._captured = True
+
+    @property
+    def n_launches(self) -> int:
+        return int(self.lib.tec_plan_size(self._native))
 
     def output(self, name: str) -> torch.Tensor:
         """The device output in the reference layout (NCHW / [N, K]), f32."""

@@ -94,3 +94,46 @@ def test_layout_planning():
     d = _desc(compute=_abi.COMPUTE_I8)
     assert lib.tec_conv_layout_of(C.byref(d), C.byref(lay)) == 0
     assert lay.cp == 64 and lay.acc_dtype == _abi.DT_I32
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors have the C structs' sizes and field offsets
+    (compiled against include/tec_sm100.h with the host compiler)."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no host C compiler")
+    checks = {
+        "tec_conv_desc": (_abi.ConvDesc, []),
+        "tec_epilogue": (_abi.Epilogue, ["bias", "mul_operand"]),
+        "tec_knobs": (_abi.Knobs, ["grid"]),
+        "tec_pool_desc": (_abi.PoolDesc, ["out_dtype"]),
+        "tec_kernel_plan": (_abi.KernelPlan, ["tma_store"]),
+        "tec_step": (_abi.Step, ["conv", "epi", "knobs", "pool", "src", "w", "dst", "w_"]),
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tec_sm100.h"',
+             'int main(void) {']
+    for cname, (_, fields) in checks.items():
+        lines.append(f'  printf("%zu\\n", sizeof({cname}));')
+        for f in fields:
+            lines.append(f'  printf("%zu\\n", offsetof({cname}, {f}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = []
+    for _, (py, fields) in checks.items():
+        want.append(C.sizeof(py))
+        want += [getattr(py, f).offset for f in fields]
+    assert got == want
+
+
+def test_plan_create_rejects_bad_arguments():
+    lib = _abi.load()
+    h = C.c_void_p()
+    assert lib.tec_plan_create(None, -1, C.byref(h)) != 0
+    assert lib.tec_plan_size(None) == 0
+    lib.tec_plan_destroy(None)
