@@ -3,7 +3,7 @@
 //
 // Why it exists: the tcgen05 f32 accumulator does not round-to-nearest on
 // every add (measured on B200: a consistent negative bias that grows with
-// K; scratch/diag_accum.py), so tensor-core results
+// K), so tensor-core results
 // drift from evaluate_reference by more than 1e-4 at K = 4608. This kernel
 // instead performs, for every output, exactly the reference's sequence
 //   facc = 0.0f; for (ic, rh, rw) in order: facc = facc + x*w

@@ -14,7 +14,7 @@
 //
 // The SWIZZLE_128B K-major UMMA descriptor accepts any 128-B-row start
 // (the swizzle is a function of the absolute smem address; verified on
-// B200 by scratch/umma_shift_test.cu), so the shift is free. Virtual rows
+// B200 by tools/microbench/umma_shift_test.cu), so the shift is free. Virtual rows
 // with ow >= OW are junk and never stored (wp/OW extra work: 3.6% on C2).
 //
 // Pipelines (the paper's virtual-thread latency hiding, as mbarriers):
