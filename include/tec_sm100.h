@@ -265,6 +265,8 @@ tec_status tec_plan_run(tec_plan* plan, void* stream);
 /* Runs the steps once eagerly (first-use setup), then captures them into a
  * CUDA graph that later tec_plan_run calls replay. */
 tec_status tec_plan_capture(tec_plan* plan, void* stream);
+/* Runs steps [first, first + count) eagerly (per-launch profiling). */
+tec_status tec_plan_run_steps(tec_plan* plan, int32_t first, int32_t count, void* stream);
 int32_t tec_plan_size(const tec_plan* plan);
 void tec_plan_destroy(tec_plan* plan);
 

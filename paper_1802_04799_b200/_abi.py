@@ -131,6 +131,7 @@ SIGNATURES = {
     "tec_plan_create": (C.c_int32, [C.POINTER(Step), C.c_int32, C.POINTER(C.c_void_p)]),
     "tec_plan_run": (C.c_int32, [_P, _P]),
     "tec_plan_capture": (C.c_int32, [_P, _P]),
+    "tec_plan_run_steps": (C.c_int32, [_P, C.c_int32, C.c_int32, _P]),
     "tec_plan_size": (C.c_int32, [_P]),
     "tec_plan_destroy": (None, [_P]),
 }

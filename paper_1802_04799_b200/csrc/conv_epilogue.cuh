@@ -476,10 +476,41 @@ __device__ __forceinline__ uint32_t box_off(int row, int chunk) {
 // reference's i32 range check per member (DenseTensor::set_i,
 // R/include/tec/tensor.hpp:63-69); sets *ovf, stores i32 (ES == 4).
 // acc: this lane's row, 32 accumulator columns (raw f32 / s32 bits).
+// Residual operand of kProgBiasAddRelu (float kinds): the warp's 32 rows x
+// 32 columns of the output-shaped NHWC operand, read COALESCED (each load
+// instruction covers kRpi whole 32-column row segments) into this block's
+// output box -- the same swizzled slots the results go to -- and handed to
+// each lane as its own row. rrow = this lane's row (already offset to the
+// block's first column) or NULL for a row that is not stored (zeros).
+template <int ES>
+__device__ __forceinline__ void load_res_box(const uint8_t* rrow, int lane, uint32_t box,
+                                             uint32_t (&res)[kChunk]) {
+  constexpr int kCpr = 32 * ES / 16, kRpi = 32 / kCpr;
+#pragma unroll
+  for (int i = 0; i < kCpr; ++i) {
+    const int r = i * kRpi + lane / kCpr, c = lane % kCpr;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(__shfl_sync(
+        0xffffffffu, reinterpret_cast<unsigned long long>(rrow), r));
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (src) v = __ldg(reinterpret_cast<const uint4*>(src) + c);
+    sts128(box + box_off<ES>(r, c), v);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < kCpr; ++c) {
+    const uint4 v = lds128(box + box_off<ES>(lane, c));
+    res[4 * c] = v.x; res[4 * c + 1] = v.y; res[4 * c + 2] = v.z; res[4 * c + 3] = v.w;
+  }
+}
+
 template <int PROG, int ES, bool kInt = false>
 __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane,
                                                const uint32_t* bias_s, uint32_t box,
-                                               bool* ovf = nullptr) {
+                                               bool* ovf = nullptr,
+                                               const uint8_t* rrow = nullptr) {
+  static_assert(!(kInt && PROG == kProgBiasAddRelu), "int residual programs use the SIMT path");
+  uint32_t res[kChunk];
+  if constexpr (PROG == kProgBiasAddRelu) load_res_box<ES>(rrow, lane, box, res);
   uint32_t b[kChunk];
   if constexpr (PROG != kProgNone) load_bias32(bias_s, b);
   if constexpr (kInt) {
@@ -507,7 +538,10 @@ __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane
   for (int j = 0; j < kChunk; ++j) {
     float x = __uint_as_float(acc[j]);
     if constexpr (PROG != kProgNone) x = __fadd_rn(x, __uint_as_float(b[j]));
-    if constexpr (PROG == kProgBiasRelu) x = (x < 0.0f) ? 0.0f : x;
+    if constexpr (PROG == kProgBiasAddRelu)  // R/src/ops.cpp:216-223, member order
+      x = __fadd_rn(x, ES == 2 ? ((j & 1) ? bf16_hi(res[j >> 1]) : bf16_lo(res[j >> 1]))
+                               : __uint_as_float(res[j]));
+    if constexpr (PROG == kProgBiasRelu || PROG == kProgBiasAddRelu) x = (x < 0.0f) ? 0.0f : x;
     v[j] = x;
   }
   constexpr int kCpr = 32 * ES / 16;
@@ -529,11 +563,12 @@ __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane
 
 template <int PROG, int ES, bool kInt = false>
 __device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const uint32_t* bias_s,
-                                              uint32_t box, bool* ovf = nullptr) {
+                                              uint32_t box, bool* ovf = nullptr,
+                                              const uint8_t* rrow = nullptr) {
   uint32_t acc[kChunk];
   tmem_ld32(taddr, acc);
   tmem_ld_wait();
-  epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s, box, ovf);
+  epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s, box, ovf, rrow);
 }
 
 // One warp's 32 accumulator rows x BN columns through the TMA-store path.
@@ -545,7 +580,8 @@ __device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const ui
 template <int PROG, int ES, int BN, bool kInt, typename SrcFn, typename StoreFn>
 __device__ __forceinline__ void epi_rows_tma_src(SrcFn&& src, int lane, const uint32_t* bias_s,
                                                  uint32_t stage, int valid_cols, uint32_t& cnt,
-                                                 bool* ovf, StoreFn&& store) {
+                                                 bool* ovf, StoreFn&& store,
+                                                 const uint8_t* rrow = nullptr) {
   constexpr uint32_t kBox = 32 * 32 * ES;
   constexpr uint32_t kSlots = 4096 / kBox;
 #pragma unroll 1
@@ -555,7 +591,8 @@ __device__ __forceinline__ void epi_rows_tma_src(SrcFn&& src, int lane, const ui
     src(c0, acc);
     if (lane == 0) bulk_wait_read<kSlots - 1>();  // the box's previous store has read it
     __syncwarp();
-    epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s + c0, box, ovf);
+    epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s + c0, box, ovf,
+                                   rrow ? rrow + c0 * ES : nullptr);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -569,13 +606,14 @@ __device__ __forceinline__ void epi_rows_tma_src(SrcFn&& src, int lane, const ui
 template <int PROG, int ES, int BN, bool kInt, typename StoreFn>
 __device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const uint32_t* bias_s,
                                              uint32_t stage, int valid_cols, uint32_t& cnt,
-                                             bool* ovf, StoreFn&& store) {
+                                             bool* ovf, StoreFn&& store,
+                                             const uint8_t* rrow = nullptr) {
   epi_rows_tma_src<PROG, ES, BN, kInt>(
       [&](int c0, uint32_t (&acc)[kChunk]) {
         tmem_ld32(taddr0 + c0, acc);
         tmem_ld_wait();
       },
-      lane, bias_s, stage, valid_cols, cnt, ovf, store);
+      lane, bias_s, stage, valid_cols, cnt, ovf, store, rrow);
 }
 
 // Cooperative per-tile bias staging: `nthreads` epilogue threads copy the

@@ -164,6 +164,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int hs = 0, ws = 0;
       uint32_t hph = 0, wph = 0;
       int n_tile, band, img;
+      const int res_es = p.out_type == kBF16 ? 2 : 4;
+      const bool res_prefetch = KIND != MmaKind::kI8 && SWZ == 128 && p.n_tiles == 1 &&
+                                epi::classify_prog(p.epi) == epi::kProgBiasAddRelu &&
+                                (p.th * p.ow * p.oc * res_es) % 16 == 0 &&
+                                (p.ow * p.oc * res_es) % 16 == 0;
       if (p.resident && tile_at(0, &n_tile, &band, &img)) {
         // every (tap, channel block) weight tile of this CTA's N tile, once
         mbar_arrive_expect_tx(&wfull[0], static_cast<uint32_t>(taps * p.cblocks * Cfg::kWBytes));
@@ -186,6 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             // box {CB, wp, th + r - 1, 1} at (c, -pw, ih0, img); TMA fills
             // the out-of-image pixels with zeros (the select(..., 0) pad).
             tma_load_4d(sH + hs * hbytes, &tm_x, &hfull[hs], cb * kCB, -p.pw, ih0, img);
+            if (cb == 0 && res_prefetch) {
+              // the tile's residual rows are one contiguous NHWC block when
+              // the tile spans every output channel: into L2 two tiles ahead
+              const int oh0 = band * p.th, rows = min(p.th, p.oh - oh0);
+              bulk_prefetch_l2(static_cast<const uint8_t*>(p.epi.residual) +
+                                   static_cast<int64_t>(img * p.oh + oh0) * p.ow * p.oc * res_es,
+                               static_cast<uint32_t>(rows * p.ow * p.oc * res_es));
+            }
           }
           if (++hs == 2) { hs = 0; hph ^= 1; }
           if (p.resident) continue;
@@ -305,8 +318,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         ((KIND == MmaKind::kI8 || p.out_type != kBF16) ? (p.oc % 4) == 0 : (p.oc % 8) == 0);
     const epi::EpiProg prog = epi::make_prog(p.epi);
     const int fast = epi::classify_prog(p.epi);
-    const bool tma_epi = p.tma_store && p.epi_mode == 0 && fast != epi::kProgGeneric &&
-                         fast != epi::kProgBiasAddRelu;
+    // Residual programs compile into the 128-B-block float instances only
+    // (the stems / SW32 instances never carry a shortcut; keeping the extra
+    // path out of them keeps their register allocation unchanged).
+    constexpr bool kResTma = KIND != MmaKind::kI8 && SWZ == 128;
+    // bias + residual add + relu (the ResNet block) too, on the float kinds
+    // (residual read per row; oc % 32 == 0 keeps 32-column reads in the row)
+    const bool tma_epi =
+        p.tma_store && p.epi_mode == 0 && fast != epi::kProgGeneric &&
+        (fast != epi::kProgBiasAddRelu || (kResTma && p.oc % 32 == 0));
     uint32_t chunk_cnt = 0;
     int local = 0;
     int staged_n_tile = -1;
@@ -325,6 +345,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi::stage_bias(bias_s, p.epi.bias, n_tile * BN, BN, p.oc, gtid, 128);
         epi::named_bar_sync(1 + grp, 128);
         staged_n_tile = n_tile;
+      }
+      if (kResTma && tma_epi && fast == epi::kProgBiasAddRelu && !dummy) {
+        // The residual rows are read right after the accumulator lands: pull
+        // this lane's lines into L2 while the MMAs still run.
+        const int es = p.out_type == kBF16 ? 2 : 4;
+        for (int ms = 0; ms < MS; ++ms) {
+          const int v = ms * 128 + static_cast<int>(q * 32 + lane);
+          const int ohl = v / p.wp, ow = v - ohl * p.wp, oh = band * p.th + ohl;
+          if (ohl < p.th && oh < p.oh && ow < p.ow) {
+            const uint8_t* r = static_cast<const uint8_t*>(p.epi.residual) +
+                               ((static_cast<int64_t>(img * p.oh + oh) * p.ow + ow) * p.oc +
+                                n_tile * BN) * es;
+            for (int b = 0; b < BN * es && n_tile * BN + b / es < p.oc; b += 128)
+              prefetch_l2(r + b);
+          }
+        }
       }
       const long long tw0 = p.dbg ? clock64() : 0;
       mbar_wait(&tfull[acc], use & 1);
@@ -367,12 +403,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               epi::named_bar_sync(1 + grp, 128);
 #pragma unroll 1
-              for (int ms = 0; ms < MS; ++ms)
+              for (int ms = 0; ms < MS; ++ms) {
+                const uint8_t* rrow = nullptr;
+                if constexpr (kProg == epi::kProgBiasAddRelu) {
+                  // virtual row -> output pixel (junk rows: no residual, not stored)
+                  const int v = ms * 128 + static_cast<int>(q * 32 + lane);
+                  const int ohl = v / p.wp, ow = v - ohl * p.wp, oh = band * p.th + ohl;
+                  if (ohl < p.th && oh < p.oh && ow < p.ow)
+                    rrow = static_cast<const uint8_t*>(p.epi.residual) +
+                           ((static_cast<int64_t>(img * p.oh + oh) * p.ow + ow) * p.oc +
+                            n_tile * BN + c0) * kES;
+                }
                 epi::epi_block_box<kProg, kES, kInt>(
                     tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0,
                     static_cast<int>(lane), bias_s + c0,
                     gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB,
-                    &overflow);
+                    &overflow, rrow);
+              }
               fence_proxy_async_smem();
               epi::named_bar_sync(1 + grp, 128);
               if (issuer) {
@@ -386,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           using P0 = std::integral_constant<int, epi::kProgNone>;
           using P1 = std::integral_constant<int, epi::kProgBias>;
           using P2 = std::integral_constant<int, epi::kProgBiasRelu>;
+          using P3 = std::integral_constant<int, epi::kProgBiasAddRelu>;
           using E2 = std::integral_constant<int, 2>;
           using E4 = std::integral_constant<int, 4>;
           if constexpr (kInt) {
@@ -395,11 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (p.out_type == kBF16) {
             if (fast == epi::kProgNone) run(P0{}, E2{});
             else if (fast == epi::kProgBias) run(P1{}, E2{});
-            else run(P2{}, E2{});
+            else if (fast == epi::kProgBiasRelu || !kResTma) run(P2{}, E2{});
+            else if constexpr (kResTma) run(P3{}, E2{});
           } else {
             if (fast == epi::kProgNone) run(P0{}, E4{});
             else if (fast == epi::kProgBias) run(P1{}, E4{});
-            else run(P2{}, E4{});
+            else if (fast == epi::kProgBiasRelu || !kResTma) run(P2{}, E4{});
+            else if constexpr (kResTma) run(P3{}, E4{});
           }
           tc_fence_before();
           mbar_arrive(&tempty[acc]);

@@ -1445,6 +1445,19 @@ tec_status tec_plan_capture(tec_plan* p, void* stream) {
   return TEC_OK;
 }
 
+tec_status tec_plan_run_steps(tec_plan* p, int32_t first, int32_t count, void* stream) {
+  if (!p || first < 0 || count < 0 || (size_t)first + (size_t)count > p->steps.size())
+    return fail(TEC_E_INTERNAL, "plan step range out of bounds");
+  for (int32_t i = first; i < first + count; ++i) {
+    tec_status st = run_step(p->steps[i], stream);
+    if (st) {
+      g_last_error = "plan step " + std::to_string(i) + ": " + g_last_error;
+      return st;
+    }
+  }
+  return TEC_OK;
+}
+
 int32_t tec_plan_size(const tec_plan* p) { return p ? (int32_t)p->steps.size() : 0; }
 
 void tec_plan_destroy(tec_plan* p) {

@@ -448,6 +448,12 @@ class DeviceGraph:
         torch.cuda.current_stream(self.dev).wait_stream(s)
         self._captured = True
 
+    def launch_step(self, i: int, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Enqueue step i alone, eagerly (per-launch profiling)."""
+        s = stream or torch.cuda.current_stream(self.dev)
+        with torch.cuda.device(self.dev):
+            _abi.check(self.lib.tec_plan_run_steps(self._native, i, 1, C.c_void_p(s.cuda_stream)))
+
     @property
     def n_launches(self) -> int:
         return int(self.lib.tec_plan_size(self._native))

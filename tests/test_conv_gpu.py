@@ -270,3 +270,18 @@ def test_halo_weight_multicast_cluster(layer, batch):
     want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), attrs["strides"],
                        attrs["padding"], epi)
     assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("k", [64, 48])
+def test_residual_epilogue_both_paths(path, k):
+    """bias + add(shortcut) + relu on the im2col (1) and halo (2) kernels:
+    OC % 32 == 0 takes the TMA-store epilogue (per-row residual reads, junk
+    halo rows skipped: W=13 leaves padding columns), OC=48 the SIMT one."""
+    x, w, b = _inputs((2, 64, 20, 13), (k, 64, 3, 3), k, False, 21)
+    r = np.random.default_rng(22).uniform(-1, 1, (2, k, 20, 13)).astype(np.float32)
+    attrs = {"strides": (1, 1), "padding": (1, 1)}
+    epi = [("bias_add", b), ("add", r), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, knobs={"tile_k": path}, compute="bf16")
+    want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), (1, 1), (1, 1), epi)
+    assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"

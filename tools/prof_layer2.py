@@ -6,7 +6,7 @@ import sys
 
 import torch
 
-sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
+sys.path.insert(0, __import__('os').getcwd())
 from paper_1802_04799_b200.device import DeviceConv
 from paper_1802_04799_b200.workloads import resnet_layer
 
