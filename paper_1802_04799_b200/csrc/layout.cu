@@ -266,6 +266,88 @@ __global__ void pack_s2d_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
   }
 }
 
+// Row-staged variant (bf16, cp = 16, w % 4 == 0): one CTA per space-to-depth
+// row (image nn, row ii). The CTA reads the two input rows of every channel
+// with coalesced float4 loads into shared memory (zero padding included),
+// then each thread assembles s2d pixels from there. The per-pixel kernel
+// above reads 12 scattered floats per pixel (2.3 TB/s on ResNet-18 b256);
+// this one streams both directions.
+constexpr int kS2dMaxW2 = 128;
+constexpr int kS2dRows = 4;  // s2d rows per CTA
+__global__ void __launch_bounds__(256) pack_s2d_rows_bf16_kernel(
+    const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int c, int h, int w, int ph,
+    int pw, int h2, int w2) {
+  // [channel][input row of the CTA][staged column]
+  __shared__ float tile[4][2 * kS2dRows][2 * kS2dMaxW2];
+  const int ii0 = blockIdx.x * kS2dRows, nn = blockIdx.y;
+  const int wp2 = 2 * w2;  // staged columns: input x = col - pw
+  const int w4 = w >> 2;
+  const int nrows = c * 2 * kS2dRows;
+  // zero what the loads below do not write: padding columns and rows
+  // outside the image (one warp per staged row)
+  for (int rr = threadIdx.x >> 5; rr < nrows; rr += blockDim.x >> 5) {
+    const int cc = rr / (2 * kS2dRows), dy = rr - cc * 2 * kS2dRows;
+    const int y = 2 * ii0 + dy - ph;
+    float* row = tile[cc][dy];
+    if (y < 0 || y >= h) {
+      for (int col = threadIdx.x & 31; col < wp2; col += 32) row[col] = 0.0f;
+    } else {
+      for (int col = threadIdx.x & 31; col < pw; col += 32) row[col] = 0.0f;
+      for (int col = pw + w + (threadIdx.x & 31); col < wp2; col += 32) row[col] = 0.0f;
+    }
+  }
+  // Loads in batches of kB per thread, all in flight before any is used
+  // (one outstanding load per thread left the kernel latency bound).
+  constexpr int kB = 8;
+  const int nvec = nrows * w4;
+  for (int base = 0; base < nvec; base += kB * blockDim.x) {
+    float4 v[kB];
+    float* dst[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int idx = base + u * blockDim.x + threadIdx.x;
+      dst[u] = nullptr;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (idx < nvec) {
+        const int rr = idx / w4, k4 = idx - rr * w4;
+        const int cc = rr / (2 * kS2dRows), dy = rr - cc * 2 * kS2dRows;
+        const int y = 2 * ii0 + dy - ph;
+        if (y >= 0 && y < h) {
+          v[u] = __ldg(reinterpret_cast<const float4*>(
+                           in + ((static_cast<int64_t>(nn) * c + cc) * h + y) * w) + k4);
+          dst[u] = &tile[cc][dy][pw + 4 * k4];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (dst[u]) { dst[u][0] = v[u].x; dst[u][1] = v[u].y; dst[u][2] = v[u].z; dst[u][3] = v[u].w; }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kS2dRows * w2; t += blockDim.x) {
+    const int r = t / w2, jj = t - r * w2;
+    const int ii = ii0 + r;
+    if (ii >= h2) break;
+    uint32_t wd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wd[k] = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        if (cc >= c) break;
+        const float v = tile[cc][2 * r + (q >> 1)][2 * jj + (q & 1)];
+        const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        const int e = q * c + cc;  // channel (dy*2+dx)*C + c
+        wd[e >> 1] |= (e & 1) ? (b << 16) : b;
+      }
+    }
+    uint4* o = reinterpret_cast<uint4*>(out + ((static_cast<int64_t>(nn) * h2 + ii) * w2 + jj) * 16);
+    o[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    o[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+  }
+}
+
 // Matching weights: [K][R2][S2][cp], w2[k][ri][sj][(dy*2+dx)*C + c] =
 // w[k][c][2ri+dy][2sj+dx] (0 past the original R x S window).
 template <typename InT>
@@ -298,6 +380,17 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
 int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c, int64_t h,
                     int64_t w, int64_t ph, int64_t pw, int64_t h2, int64_t w2, int64_t cp,
                     int mode, cudaStream_t st) {
+  if (in_type != kI8 && mode == kPackBF16 && cp == 16 && c <= 4 && w % 4 == 0 &&
+      w2 <= kS2dMaxW2 && 2 * w2 >= w + pw && n <= 65535 && h2 <= (1 << 30)) {
+    pack_s2d_rows_bf16_kernel<<<dim3(static_cast<unsigned>((h2 + kS2dRows - 1) / kS2dRows),
+                                     static_cast<unsigned>(n)),
+                                256, 0, st>>>(static_cast<const float*>(in),
+                                         static_cast<__nv_bfloat16*>(out), static_cast<int>(c),
+                                         static_cast<int>(h), static_cast<int>(w),
+                                         static_cast<int>(ph), static_cast<int>(pw),
+                                         static_cast<int>(h2), static_cast<int>(w2));
+    return cudaGetLastError();
+  }
   if (in_type != kI8 && mode == kPackBF16 && cp == 16 && c <= 4 && n * h2 * w2 < (1ll << 31)) {
     const int64_t px = n * h2 * w2;
     const int blocks = static_cast<int>(std::min<int64_t>((px + 255) / 256, 148 * 32));
