@@ -830,6 +830,8 @@ tec_status ensure(DevBuf* b, size_t bytes) {
 struct HostWorkspace {
   std::mutex mu;
   cudaStream_t stream = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
+  std::vector<cudaEvent_t> ev;                 // [2 * chunk]: inputs landed, outputs ready
   DevBuf x_src, w_src, x_pack, w_pack, y_nhwc, y_nchw, bias, res_src, res_pack,
       mul_src, mul_pack, err;
 };
@@ -1232,7 +1234,6 @@ tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
   if ((st = ensure(&ws.y_nhwc, y_elems * 4))) return st;
   if ((st = ensure(&ws.y_nchw, y_elems * 4))) return st;
   if ((st = ensure(&ws.err, 4))) return st;
-  TEC_CUDA(cudaMemcpyAsync(ws.x_src.p, x, x_elems * in_es, cudaMemcpyHostToDevice, s));
   TEC_CUDA(cudaMemcpyAsync(ws.w_src.p, w, w_elems * in_es, cudaMemcpyHostToDevice, s));
   TEC_CUDA(cudaMemsetAsync(ws.err.p, 0, 4, s));
 
@@ -1260,6 +1261,62 @@ tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
       *dst[i] = pk[i]->p;
     }
   }
+  // Pipelined host path: without same-shape operands the batch is cut into
+  // chunks of whole images and H2D of chunk i+1, pack/conv/unpack of chunk i
+  // and D2H of chunk i-1 overlap on three streams (PCIe is full duplex). Each
+  // image's result is independent of the chunking (every output sums its K
+  // in the same order; tests check batch linearity bit for bit).
+  const bool same_shape_ops = epi && (epi->residual || epi->mul_operand);
+  const int64_t x_img = x_elems / d->n * in_es;
+  static const int64_t chunk_bytes = [] {
+    const char* e = std::getenv("TEC_SM100_CHUNK_KB");  // tuning override
+    return e ? std::max<int64_t>(64, std::atoll(e)) << 10 : int64_t(6) << 20;
+  }();
+  int64_t chunks = std::min<int64_t>(d->n, std::max<int64_t>(1, x_elems * in_es / chunk_bytes));
+  chunks = std::min<int64_t>(chunks, 32);
+  if (!same_shape_ops && chunks > 1 && lay.act_bytes % d->n == 0) {
+    if (!ws.h2d) TEC_CUDA(cudaStreamCreateWithFlags(&ws.h2d, cudaStreamNonBlocking));
+    if (!ws.d2h) TEC_CUDA(cudaStreamCreateWithFlags(&ws.d2h, cudaStreamNonBlocking));
+    while ((int64_t)ws.ev.size() < 2 * chunks) {
+      cudaEvent_t e;
+      TEC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ws.ev.push_back(e);
+    }
+    if ((st = tec_weight_pretransform(d, ws.w_src.p, ws.w_pack.p, s))) return st;
+    const int64_t per = (d->n + chunks - 1) / chunks;
+    const int64_t a_img = lay.act_bytes / d->n, y_img = y_elems / d->n * 4;
+    // the raw x copy above is replaced by per-chunk copies on the H2D stream
+    for (int64_t c = 0, n0 = 0; n0 < d->n; ++c, n0 += per) {
+      const int64_t nb = std::min<int64_t>(per, d->n - n0);
+      tec_conv_desc dc = *d;
+      dc.n = nb;
+      uint8_t* xs = static_cast<uint8_t*>(ws.x_src.p) + n0 * x_img;
+      TEC_CUDA(cudaMemcpyAsync(xs, static_cast<const uint8_t*>(x) + n0 * x_img, nb * x_img,
+                               cudaMemcpyHostToDevice, ws.h2d));
+      TEC_CUDA(cudaEventRecord(ws.ev[2 * c], ws.h2d));
+      TEC_CUDA(cudaStreamWaitEvent(s, ws.ev[2 * c], 0));
+      uint8_t* xp = static_cast<uint8_t*>(ws.x_pack.p) + n0 * a_img;
+      uint8_t* yn = static_cast<uint8_t*>(ws.y_nhwc.p) + n0 * y_img;
+      uint8_t* yc = static_cast<uint8_t*>(ws.y_nchw.p) + n0 * y_img;
+      if ((st = tec_activation_pack(&dc, xs, xp, s))) return st;
+      st = tec_conv2d_fused(&dc, epi ? &dev_epi : nullptr, knobs, xp, ws.w_pack.p, yn, acc_t,
+                            static_cast<int32_t*>(ws.err.p), s);
+      if (st) return st;
+      if ((st = tec_output_unpack(yn, acc_t, yc, acc_t, nb, d->k, pl.oh, pl.ow, s))) return st;
+      TEC_CUDA(cudaEventRecord(ws.ev[2 * c + 1], s));
+      TEC_CUDA(cudaStreamWaitEvent(ws.d2h, ws.ev[2 * c + 1], 0));
+      TEC_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(y) + n0 * y_img, yc, nb * y_img,
+                               cudaMemcpyDeviceToHost, ws.d2h));
+    }
+    int32_t err_host = 0;
+    TEC_CUDA(cudaMemcpyAsync(&err_host, ws.err.p, 4, cudaMemcpyDeviceToHost, s));
+    TEC_CUDA(cudaStreamSynchronize(s));
+    TEC_CUDA(cudaStreamSynchronize(ws.d2h));
+    if (err_host)
+      return fail(TEC_E_FOLD_OVERFLOW, "value out of range for i32 in the fused epilogue");
+    return TEC_OK;
+  }
+  TEC_CUDA(cudaMemcpyAsync(ws.x_src.p, x, x_elems * in_es, cudaMemcpyHostToDevice, s));
   if ((st = tec_activation_pack(d, ws.x_src.p, ws.x_pack.p, s))) return st;
   if ((st = tec_weight_pretransform(d, ws.w_src.p, ws.w_pack.p, s))) return st;
   st = tec_conv2d_fused(d, epi ? &dev_epi : nullptr, knobs, ws.x_pack.p, ws.w_pack.p,
