@@ -40,10 +40,11 @@ namespace {
 constexpr int kThreads = 384;     // 4 control warps + 8 epilogue warps
 constexpr int kEpiThreads = 256;
 
-template <int BN, int MS, int SWZ, int WSTAGES>
+template <int BN, int MS, int SWZ, int WSTAGES, bool kPair = false>
 struct HaloCfg {
   static constexpr int kWBytes = BN * SWZ;
-  static constexpr uint32_t kAccCols = MS * BN;
+  // kPair: every sub-tile accumulator is [lo BN | hi BN] columns (see below)
+  static constexpr uint32_t kAccCols = MS * BN * (kPair ? 2 : 1);
   static constexpr uint32_t kTmemCols = 2 * kAccCols <= 32    ? 32
                                         : 2 * kAccCols <= 64  ? 64
                                         : 2 * kAccCols <= 128 ? 128
@@ -57,13 +58,26 @@ __host__ __device__ inline int halo_bytes_aligned(int halo_px, int swz) {
   return (halo_px * swz + 1023) & ~1023;
 }
 
-template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
+// Paired taps (kPair, resident weights, BN = 64): the weight tiles of taps
+// (rh, rw) and (rh, rw + 1) sit next to each other in shared memory, i.e.
+// they ARE one 128-row B tile. One N=128 MMA at the A shift of (rh, rw)
+// computes  lo = X[v + s] * W(rh, rw)      -> output row v     (columns 0..63)
+//           hi = X[v + s] * W(rh, rw + 1)  -> output row v - 1 (columns 64..127)
+// because tap (rh, rw + 1) of output v - 1 reads exactly X[v + s]. The same
+// one-row offset holds for every pair, so one hi accumulator collects them
+// all and the epilogue adds hi of row v + 1 to lo of row v (a lane shuffle;
+// the last lane of each warp takes it from the next warp through shared
+// memory). An odd last tap runs as a plain N=64 MMA into lo. N=128 MMAs cost
+// 64 cycles vs 54 for N=64 (tools/microbench/RESULTS.md), so a 3x3 filter
+// row drops from 3 x 54 to 64 + 54 cycles and a 4-tap row to 2 x 64.
+template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES, bool kPair = false>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tm_x,
                      const __grid_constant__ CUtensorMap tm_w,
                      const __grid_constant__ CUtensorMap tm_y,
                      const ConvHaloParams p) {
-  using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
+  using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES, kPair>;
+  static_assert(!kPair || (BN == 64 && KIND == MmaKind::kF16), "paired taps: bf16, BN = 64");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -80,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* sBias = reinterpret_cast<uint32_t*>(
       reinterpret_cast<uint8_t*>(hfull) + 256);  // [2][BN] f32 / i32
+  float* sXchg = reinterpret_cast<float*>(sBias + 2 * BN);  // kPair: [2 grp][MS][4 warps][64]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -246,6 +261,56 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool dbg = p.dbg != nullptr;
       const int pr = p.r, ps = p.s, cblocks = p.cblocks;
       const uint32_t row_skip = static_cast<uint32_t>((p.wp - ps) * SWZ) >> 4;
+      if constexpr (kPair) {
+        // resident weights only (host guarantees); see the comment at the top
+        constexpr uint32_t idesc2 = make_idesc<KIND>(128, 2 * BN);
+        const int npair = ps >> 1;
+        const uint32_t odd_skip = static_cast<uint32_t>(((ps & 1) ? 1 : 0) * SWZ) >> 4;
+        for (int local = 0; tile_at(local, &n_tile, &band, &img); ++local) {
+          const int acc = local & 1;
+          const uint32_t use = static_cast<uint32_t>(local >> 1);
+          { const long long t0 = dbg ? clock64() : 0;
+            mbar_wait(&tempty[acc], (use & 1) ^ 1);
+            if (dbg) dbg_wait[2] += clock64() - t0; }
+          tc_fence_after();
+          const uint32_t d0 = tmem_base + acc * Cfg::kAccCols;
+          uint64_t bd = wdesc0;
+          for (int cb = 0; cb < cblocks; ++cb) {
+            { const long long t0 = dbg ? clock64() : 0;
+              mbar_wait(&hfull[hs], hph);
+              if (dbg) dbg_wait[1] += clock64() - t0; }
+            tc_fence_after();
+            uint64_t ad = make_smem_desc<SWZ>(smem_u32(sH + hs * hbytes), 8 * SWZ);
+            uint32_t accum = cb == 0 ? 0u : 1u;
+            for (int rh = 0; rh < pr; ++rh) {
+              for (int pp = 0; pp < npair; ++pp) {
+#pragma unroll
+                for (int ms = 0; ms < MS; ++ms)
+#pragma unroll
+                  for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk)
+                    tc_mma<KIND>(d0 + ms * 2 * BN, ad + ((ms * 128 * SWZ + kk * 32) >> 4),
+                                 bd + ((kk * 32) >> 4), idesc2, kk == 0 ? accum : 1u);
+                accum = 1u;
+                ad += (2 * SWZ) >> 4;
+                bd += (2 * Cfg::kWBytes) >> 4;
+              }
+              if (ps & 1) {  // the row's last tap alone, into lo
+#pragma unroll
+                for (int ms = 0; ms < MS; ++ms)
+#pragma unroll
+                  for (int kk = 0; kk < Cfg::kMmaPerTap; ++kk)
+                    tc_mma<KIND>(d0 + ms * 2 * BN, ad + ((ms * 128 * SWZ + kk * 32) >> 4),
+                                 bd + ((kk * 32) >> 4), idesc, 1u);
+                bd += Cfg::kWBytes >> 4;
+              }
+              ad += odd_skip + row_skip;
+            }
+            tc_commit(&hempty[hs]);
+            if (++hs == 2) { hs = 0; hph ^= 1; }
+          }
+          tc_commit(&tfull[acc]);
+        }
+      } else {
       auto issue = [&](auto resident_c) {
         constexpr bool kRes = decltype(resident_c)::value;
         for (int local = 0; tile_at(local, &n_tile, &band, &img); ++local) {
@@ -303,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue(std::true_type{});
       else
         issue(std::false_type{});
+      }  // !kPair
     }
   } else if (warp >= 4) {
     // ------------------------------------------------- epilogue warps
@@ -372,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&tempty[acc]);
         continue;
       }
+      if (kPair && !tma_epi) __trap();  // host guarantees the TMA-store program for kPair
       {
         if (tma_epi) {
           constexpr bool kInt = KIND == MmaKind::kI8;
@@ -414,11 +481,64 @@ __global__ void __launch_bounds__(kThreads, 1)
                            ((static_cast<int64_t>(img * p.oh + oh) * p.ow + ow) * p.oc +
                             n_tile * BN + c0) * kES;
                 }
-                epi::epi_block_box<kProg, kES, kInt>(
-                    tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0,
-                    static_cast<int>(lane), bias_s + c0,
-                    gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB,
-                    &overflow, rrow);
+                const uint32_t box =
+                    gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB;
+                if constexpr (kPair) {
+                  // output row v = lo(v) + hi(v + 1): hi of the next lane by
+                  // shuffle; lane 31's row needs the next warp's lane 0 and is
+                  // finished after the barrier below from the exchange slots.
+                  const uint32_t ta =
+                      tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * 2 * BN + c0;
+                  uint32_t lo[epi::kChunk], hi[epi::kChunk];
+                  tmem_ld32(ta, lo);
+                  tmem_ld32(ta + BN, hi);
+                  tmem_ld_wait();
+                  float* xs = sXchg + ((grp * MS + ms) * 4 + q) * 64;  // [hi of lane 0 | lo of lane 31]
+                  if (lane == 0 || lane == 31) {
+                    float4* x4 = reinterpret_cast<float4*>(xs + (lane == 0 ? 0 : 32));
+                    const uint32_t* src = lane == 0 ? hi : lo;
+#pragma unroll
+                    for (int j = 0; j < epi::kChunk / 4; ++j)
+                      x4[j] = make_float4(__uint_as_float(src[4 * j]), __uint_as_float(src[4 * j + 1]),
+                                          __uint_as_float(src[4 * j + 2]),
+                                          __uint_as_float(src[4 * j + 3]));
+                  }
+#pragma unroll
+                  for (int j = 0; j < epi::kChunk; ++j) {
+                    const float hn = __shfl_down_sync(0xffffffffu, __uint_as_float(hi[j]), 1);
+                    lo[j] = __float_as_uint(__fadd_rn(__uint_as_float(lo[j]), hn));
+                  }
+                  epi::epi_acc_to_box<kProg, kES, kInt>(lo, static_cast<int>(lane), bias_s + c0,
+                                                        box, &overflow, rrow);
+                } else {
+                  epi::epi_block_box<kProg, kES, kInt>(
+                      tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0,
+                      static_cast<int>(lane), bias_s + c0, box, &overflow, rrow);
+                }
+              }
+              if constexpr (kPair) {
+                epi::named_bar_sync(1 + grp, 128);  // exchange slots written
+                // the warp's last row, one column per lane
+#pragma unroll 1
+                for (int ms = 0; ms < MS; ++ms) {
+                  const float* mine = sXchg + ((grp * MS + ms) * 4 + q) * 64 + 32;
+                  const float* nx = q < 3 ? sXchg + ((grp * MS + ms) * 4 + q + 1) * 64
+                                    : ms + 1 < MS ? sXchg + ((grp * MS + ms + 1) * 4) * 64
+                                                  : nullptr;  // past the tile: a junk row
+                  const uint8_t* rrow = nullptr;
+                  if constexpr (kProg == epi::kProgBiasAddRelu) {
+                    const int v = ms * 128 + static_cast<int>(q * 32 + 31);
+                    const int ohl = v / p.wp, ow = v - ohl * p.wp, oh = band * p.th + ohl;
+                    if (ohl < p.th && oh < p.oh && ow < p.ow)
+                      rrow = static_cast<const uint8_t*>(p.epi.residual) +
+                             ((static_cast<int64_t>(img * p.oh + oh) * p.ow + ow) * p.oc +
+                              n_tile * BN + c0) * kES;
+                  }
+                  epi::row_col_to_box<kProg, kES>(
+                      mine, nx, bias_s + c0, rrow,
+                      gbuf + static_cast<uint32_t>(ms * 128 + static_cast<int>(q) * 32) * kRowB,
+                      31, static_cast<int>(lane));
+                }
               }
               fence_proxy_async_smem();
               epi::named_bar_sync(1 + grp, 128);
@@ -519,17 +639,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
+template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES, bool kPair>
 int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
                      const CUtensorMap& tm_y, const ConvHaloParams& p, int grid,
                      cudaStream_t stream) {
-  using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES>;
+  using Cfg = HaloCfg<BN, MS, SWZ, WSTAGES, kPair>;
   const int smem = 1024 + 2 * halo_bytes_aligned(p.halo_px, SWZ) +
-                   p.w_slots * Cfg::kWBytes + p.stage_bytes + 256 + 2 * BN * 4;
+                   p.w_slots * Cfg::kWBytes + p.stage_bytes + 256 + 2 * BN * 4 +
+                   (kPair ? 2 * MS * 4 * 64 * 4 : 0);
+  if (kPair && (!p.resident || p.s < 2 || !p.tma_store)) return cudaErrorInvalidValue;
   if (p.stage_bytes < 8 * 4096 || p.stage_bytes % 2048) return cudaErrorInvalidValue;
   if (!p.resident && p.w_slots != WSTAGES) return cudaErrorInvalidValue;
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES>;
+  auto kfn = conv_halo_kernel<KIND, BN, MS, SWZ, WSTAGES, kPair>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   e = launch_pdl_cluster(kfn, dim3(grid), dim3(kThreads), smem, stream,
@@ -539,13 +661,18 @@ int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
 }
 
 // Returns the dynamic smem a configuration needs (host-side planning).
-int conv_halo_smem_bytes(int bn, int swz, int w_slots, int halo_px, int stage_bytes) {
+int conv_halo_smem_bytes(int bn, int swz, int w_slots, int halo_px, int stage_bytes, int ms,
+                         bool pair) {
   return 1024 + 2 * halo_bytes_aligned(halo_px, swz) + w_slots * bn * swz + stage_bytes + 256 +
-         2 * bn * 4;
+         2 * bn * 4 + (pair ? 2 * ms * 4 * 64 * 4 : 0);
 }
 
 #define TEC_HALO(KIND, BN, MS, SWZ, WS)                                        \
-  template int launch_conv_halo<KIND, BN, MS, SWZ, WS>(                       \
+  template int launch_conv_halo<KIND, BN, MS, SWZ, WS, false>(                \
+      const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,           \
+      const ConvHaloParams&, int, cudaStream_t);
+#define TEC_HALO_PAIR(KIND, BN, MS, SWZ, WS)                                   \
+  template int launch_conv_halo<KIND, BN, MS, SWZ, WS, true>(                 \
       const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,           \
       const ConvHaloParams&, int, cudaStream_t);
 
@@ -570,6 +697,12 @@ TEC_HALO(MmaKind::kI8, 64, 4, 32, 8)
 TEC_HALO(MmaKind::kI8, 64, 2, 64, 6)
 TEC_HALO(MmaKind::kI8, 64, 4, 64, 6)
 
+TEC_HALO_PAIR(MmaKind::kF16, 64, 1, 128, 6)
+TEC_HALO_PAIR(MmaKind::kF16, 64, 2, 128, 6)
+TEC_HALO_PAIR(MmaKind::kF16, 64, 1, 32, 8)
+TEC_HALO_PAIR(MmaKind::kF16, 64, 2, 32, 8)
+
 #undef TEC_HALO
+#undef TEC_HALO_PAIR
 
 }  // namespace tec_sm100

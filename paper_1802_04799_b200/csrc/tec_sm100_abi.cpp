@@ -47,11 +47,12 @@ int launch_pack_weights_s2d(const void* w, int in_type, void* out, int64_t k, in
                             cudaStream_t st);
 int launch_conv_f32_exact(const float* x, const float* w,
                           const ConvGemmParams& p, cudaStream_t st);
-template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES>
+template <MmaKind KIND, int BN, int MS, int SWZ, int WSTAGES, bool kPair>
 int launch_conv_halo(const CUtensorMap& tm_x, const CUtensorMap& tm_w,
                      const CUtensorMap& tm_y, const ConvHaloParams& p, int grid,
                      cudaStream_t stream);
-int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px, int stage_bytes);
+int conv_halo_smem_bytes(int bn, int swz, int wstages, int halo_px, int stage_bytes, int ms,
+                         bool pair);
 int launch_max_pool(const PoolParams& p, cudaStream_t st);
 bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t);
 int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
@@ -363,8 +364,10 @@ struct HaloInst {
   MmaKind kind;
   int bn, ms, swz, wstages;
   HaloLauncher fn;
+  bool pair;  // paired taps (conv_halo.cu, kPair)
 };
-#define TEC_H(K, BN, MS, SW, WS) {K, BN, MS, SW, WS, &launch_conv_halo<K, BN, MS, SW, WS>}
+#define TEC_H(K, BN, MS, SW, WS) {K, BN, MS, SW, WS, &launch_conv_halo<K, BN, MS, SW, WS, false>, false}
+#define TEC_HP(K, BN, MS, SW, WS) {K, BN, MS, SW, WS, &launch_conv_halo<K, BN, MS, SW, WS, true>, true}
 const HaloInst kHaloInsts[] = {
     TEC_H(MmaKind::kF16, 64, 1, 128, 6),  TEC_H(MmaKind::kF16, 64, 2, 128, 6),
     TEC_H(MmaKind::kF16, 64, 4, 128, 4),  TEC_H(MmaKind::kF16, 128, 1, 128, 6),
@@ -376,8 +379,11 @@ const HaloInst kHaloInsts[] = {
     TEC_H(MmaKind::kI8, 64, 2, 64, 6),    TEC_H(MmaKind::kI8, 64, 4, 64, 6),
     TEC_H(MmaKind::kI8, 64, 1, 32, 8),    TEC_H(MmaKind::kI8, 64, 1, 64, 6),
     TEC_H(MmaKind::kI8, 64, 2, 32, 8),    TEC_H(MmaKind::kI8, 64, 4, 32, 8),
+    TEC_HP(MmaKind::kF16, 64, 1, 128, 6), TEC_HP(MmaKind::kF16, 64, 2, 128, 6),
+    TEC_HP(MmaKind::kF16, 64, 1, 32, 8),  TEC_HP(MmaKind::kF16, 64, 2, 32, 8),
 };
 #undef TEC_H
+#undef TEC_HP
 
 constexpr int kStageMin = 8 * 4096;  // epilogue stage: 8 warps x 4 KB
 constexpr int kSmemMax = 227 * 1024;
@@ -392,8 +398,10 @@ struct HaloChoice {
 // Picks (BN, MS, rows per tile) by a two-term model per tile --
 // max(MMA cycles, L2->SM bytes / 40 B/cycle) -- times the number of waves
 // over the SMs. Returns false when no halo instance fits.
+// pair_ok: the epilogue program has the TMA-store path the paired-tap
+// instances need (kPair). Knob tile_k: 2 = halo without pairing, 4 = paired.
 bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int sms,
-               int32_t out_dtype, HaloChoice* out) {
+               int32_t out_dtype, bool pair_ok, HaloChoice* out) {
   if (d->stride_h != 1 || d->stride_w != 1) return false;
   const int wp = (int)((d->w + 2 * d->pad_w + 1) & ~int64_t(1));  // even: 128-B aligned output rows in the TMA epilogue
   const int es = elem_bytes(pl.act);
@@ -404,11 +412,19 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
     if (kn && kn->tile_n && kn->tile_n != hi.bn) continue;
     if (kn && kn->tile_m && kn->tile_m != 128 * hi.ms) continue;
     if (hi.bn > 64 && hi.bn > d->k) continue;
+    // Paired taps only on request (knob tile_k = 4): they cut the MMA time
+    // (C2: 54 -> 39 cycles per tap-equivalent) but double the accumulator the
+    // epilogue reads from TMEM, and the epilogue then bounds the ResNet
+    // layers (C2 b64: 25.0 us paired vs 23.8 us plain, C1: 58 vs 43).
+    if (hi.pair && (!pair_ok || d->s < 2 || !(kn && kn->tile_k == 4) ||
+                    (kn && (kn->stages == 1 || kn->cluster_n > 1))))
+      continue;
+    if (!hi.pair && kn && kn->tile_k == 4) continue;
     const int th = (int)std::min<int64_t>(pl.oh, (128 * hi.ms) / wp);
     if (th < 1 || th + d->r - 1 > 256) continue;
     // Small images waste most MMA rows on junk virtual rows / padding: keep
     // the halo form for tiles that are at least half real outputs.
-    if (!(kn && kn->tile_k == 2) && 2 * th * pl.ow < 128 * hi.ms) continue;
+    if (!(kn && (kn->tile_k == 2 || kn->tile_k == 4)) && 2 * th * pl.ow < 128 * hi.ms) continue;
     const int halo_px = 128 * hi.ms + (int)((d->r - 1) * wp + d->s) + 8;
     const int bands = (int)((pl.oh + th - 1) / th);
     const int n_tiles = (int)((d->k + hi.bn - 1) / hi.bn);
@@ -416,8 +432,10 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
     const int64_t tiles = spatial * n_tiles;
     const int taps_cb = (int)(d->r * d->s * (pl.cp * es / hi.swz));
     const double ktot = (double)d->r * d->s * pl.cp;
-    const double mma = 128.0 * hi.ms * hi.bn * ktot * 2 / 8192.0 *
-                       (pl.kind == MmaKind::kTF32 ? 2 : pl.kind == MmaKind::kI8 ? 0.5 : 1);
+    double mma = 128.0 * hi.ms * hi.bn * ktot * 2 / 8192.0 *
+                 (pl.kind == MmaKind::kTF32 ? 2 : pl.kind == MmaKind::kI8 ? 0.5 : 1);
+    if (hi.pair)  // measured N=128 64 cycles vs N=64 54 (tools/microbench/RESULTS.md)
+      mma *= ((d->s / 2) * 64.0 + (d->s % 2) * 54.0) / (d->s * 54.0);
     const double halo_bytes = (double)(th + d->r - 1) * wp * pl.cp * es;
     // Epilogue term: the group-staged TMA-store path (run_conv_halo) moves
     // ~48 B/cycle of output, the SIMT fallback ~12 (measured, round 1).
@@ -432,12 +450,12 @@ bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int 
       if (dbg)
         std::fprintf(stderr, "[tec-plan] halo bn=%d ms=%d swz=%d res=%d th=%d smem=%d\n", hi.bn,
                      hi.ms, hi.swz, res, th,
-                     conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin));
-      if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin) > kSmemMax) continue;
+                     conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin, hi.ms, hi.pair));
+      if (conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, kStageMin, hi.ms, hi.pair) > kSmemMax) continue;
       // The TMA-store epilogue needs one chunk per epilogue group in the stage.
       const bool tma_epi =
           (wp * rowb) % 128 == 0 &&
-          conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, std::max(kStageMin, 2 * cbytes)) <=
+          conv_halo_smem_bytes(hi.bn, hi.swz, w_slots, halo_px, std::max(kStageMin, 2 * cbytes), hi.ms, hi.pair) <=
               kSmemMax;
       const double epi = (double)th * pl.ow * std::min<int64_t>(hi.bn, d->k) *
                          elem_bytes(out_dtype) / (tma_epi ? 48.0 : 12.0);
@@ -552,7 +570,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     const int cbytes = hc.inst->ms * 128 * rowb;
     const int stage1 = std::max(kStageMin, 2 * cbytes);  // one chunk per group
     if ((wp * rowb) % 128 == 0 &&
-        conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, stage1) <=
+        conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, stage1, hc.inst->ms, hc.inst->pair) <=
             kSmemMax)
       make_store_map(&tm_y, y, out_dtype, 4, dims, (int)pl.ow, &ok);
     else std::memset(&tm_y, 0, sizeof(tm_y));
@@ -560,7 +578,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     // is written while the previous one's TMA stores drain.
     p.stage_bytes = ok ? stage1 : kStageMin;
     if (ok && 4 * cbytes > p.stage_bytes &&
-        conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, 4 * cbytes) <=
+        conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px, 4 * cbytes, hc.inst->ms, hc.inst->pair) <=
             kSmemMax)
       p.stage_bytes = 4 * cbytes;
     p.tma_store = ok && !(kn && kn->vec == 3) ? 1 : 0;  // vec 3: SIMT stores
@@ -576,10 +594,13 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
+  if (hc.inst->pair && !p.tma_store)
+    return fail(TEC_E_INTERNAL, "paired-tap halo instance without its TMA-store epilogue");
   if (plan_only(TEC_KERNEL_HALO, hc.inst->bn, 128 * hc.inst->ms, hc.resident ? 2 : 1, grid,
                 conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px,
-                                     p.stage_bytes),
-                tmem_cols_for(2 * hc.inst->ms * hc.inst->bn), p.tma_store, 1, hc.cl))
+                                     p.stage_bytes, hc.inst->ms, hc.inst->pair),
+                tmem_cols_for(2 * hc.inst->ms * hc.inst->bn * (hc.inst->pair ? 2 : 1)),
+                p.tma_store, 1, hc.cl))
     return TEC_OK;
   const int e = hc.inst->fn(tm_x, tm_w, tm_y, p, grid, st);
   if (e) return cuda_fail(e, "conv_halo launch");
@@ -660,17 +681,23 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   cudaGetDevice(&dev);
   const int sms = sm_count(dev);
   // Path: knob tile_k selects the A-operand strategy -- 0 auto, 1 im2col
-  // TMA (conv_tc.cu), 2 shifted-window halo (conv_halo.cu, stride 1 only).
+  // TMA (conv_tc.cu), 2 shifted-window halo (conv_halo.cu, stride 1 only),
+  // 4 halo with paired filter taps (N=128 MMAs, conv_halo.cu kPair).
   const int64_t path = kn ? kn->tile_k : 0;
   if (path == 1 && kn && kn->cluster_n > 1)
     return fail(TEC_E_LOWERING, "cluster_n (weight multicast) applies to the halo path");
-  if (path == 2 && kn && kn->split_k > 1)
+  if ((path == 2 || path == 4) && kn && kn->split_k > 1)
     return fail(TEC_E_LOWERING, "split_k applies to the im2col path (tile_k=1)");
   if (path != 1 && !(kn && kn->split_k > 1)) {
+    // paired taps need the TMA-store epilogue program (conv_halo.cu tma_epi)
+    const bool res_prog = epi.n_ops == 3 && epi.ops[0] == kEpiBias && epi.ops[1] == kEpiAdd &&
+                          epi.ops[2] == kEpiRelu;
+    const bool pair_ok = pl.kind == MmaKind::kF16 && !(kn && kn->vec != 0) &&
+                         (fast_program(epi) || (res_prog && pl.swz == 128 && d->k % 32 == 0));
     HaloChoice hc;
-    if (plan_halo(d, pl, kn, sms, out_dtype, &hc))
+    if (plan_halo(d, pl, kn, sms, out_dtype, pair_ok, &hc))
       return run_conv_halo(d, pl, hc, epi, kn, x, w, y, out_dtype, err, st, sms);
-    if (path == 2) return fail(TEC_E_LOWERING, "no halo configuration for this conv");
+    if (path == 2 || path == 4) return fail(TEC_E_LOWERING, "no halo configuration for this conv");
   }
   const int64_t m_tiles = (pl.m + 127) / 128;
 

@@ -285,3 +285,36 @@ def test_residual_epilogue_both_paths(path, k):
     y = fused_conv("conv2d", x, w, attrs, epi, knobs={"tile_k": path}, compute="bf16")
     want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), (1, 1), (1, 1), epi)
     assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
+
+
+@pytest.mark.parametrize("case", [
+    ("C1", None), ("C2", None), ("C2", "residual"), ("odd", None), ("odd", "residual")])
+def test_paired_taps_agree_with_oracle(case):
+    """tile_k=4: the halo kernel with paired filter taps (N=128 MMAs, the hi
+    half shifted one output row and added back in the epilogue). C1 runs on
+    its space-to-depth form (4x4 taps: two pairs per row), C2 3x3 (a pair and
+    a single); 'odd' has junk virtual rows (W=13) and a 2-image batch."""
+    from paper_1802_04799_b200.lower import lower
+    from paper_1802_04799_b200.ops import conv_desc
+    name, kind = case
+    if name == "odd":
+        shape_x, shape_w, s = (2, 64, 20, 13), (64, 64, 3, 3), 1
+    else:
+        hw, c, k, r, s = RESNET18_CONVS[name]
+        shape_x, shape_w = (2, c, hw, hw), (k, c, r, r)
+    x, w, b = _inputs(shape_x, shape_w, shape_w[0], False, 31)
+    attrs = {"strides": (s, s), "padding": (shape_w[2] // 2, shape_w[2] // 2)}
+    epi = [("bias_add", b), ("relu",)]
+    if kind == "residual":
+        oh = (shape_x[2] + 2 * attrs["padding"][0] - shape_w[2]) // s + 1
+        r_ = np.random.default_rng(32).uniform(-1, 1, (shape_x[0], shape_w[0], oh, oh if name != "odd" else 13)).astype(np.float32)
+        epi = [("bias_add", b), ("add", r_), ("relu",)]
+    kn = {"tile_k": 4}
+    from paper_1802_04799_b200 import _abi
+    d = conv_desc("conv2d", list(shape_x), list(shape_w), attrs, _abi.COMPUTE_BF16)
+    plan = lower(d, kn, [{"bias_add": 2, "add": 3, "relu": 5}[m[0]] for m in epi])
+    assert plan.family == "halo" and plan.tmem_cols == 4 * plan.tile_n * plan.tile_m // 128
+    y = fused_conv("conv2d", x, w, attrs, epi, knobs=kn, compute="bf16")
+    want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), attrs["strides"],
+                       attrs["padding"], epi)
+    assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
