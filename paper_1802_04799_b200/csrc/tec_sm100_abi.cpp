@@ -1395,22 +1395,41 @@ tec_status tec_measure(const tec_conv_desc* d, const tec_epilogue* epi,
     if (e.residual) e.residual = r;
     if (e.mul_operand) e.mul_operand = r;
   }
+  // Event timestamps here advance in ~2 us steps, too coarse for one launch
+  // of a 10-30 us kernel: time `reps` back-to-back (flush, launch) pairs and
+  // subtract the same number of flushes timed alone; three such batches,
+  // median. The host enqueues each launch while the GPU runs the flush, so
+  // host planning time stays outside the measurement.
   std::vector<float> times;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int i = 0; i < warmup + reps && st == TEC_OK; ++i) {
-    if (flush_l2) cudaMemsetAsync(fl, i & 0xff, flush_bytes, s);
-    cudaEventRecord(e0, s);
+  for (int i = 0; i < warmup && st == TEC_OK; ++i)
     st = tec_conv2d_fused(d, epi ? &e : nullptr, knobs, x, w, y, out_t, nullptr, s);
-    cudaEventRecord(e1, s);
-    if (cudaEventSynchronize(e1) != cudaSuccess) {
-      st = fail(TEC_E_CUDA, "measure: kernel failed");
-      break;
+  if (st == TEC_OK && cudaStreamSynchronize(s) != cudaSuccess)
+    st = fail(TEC_E_CUDA, "measure: kernel failed");
+  const int n = std::max(1, reps);
+  auto batch = [&](bool with_conv, float* us) -> tec_status {
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < n; ++i) {
+      if (flush_l2) cudaMemsetAsync(fl, i & 0xff, flush_bytes, s);
+      if (with_conv) {
+        tec_status t = tec_conv2d_fused(d, epi ? &e : nullptr, knobs, x, w, y, out_t, nullptr, s);
+        if (t) return t;
+      }
     }
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) return fail(TEC_E_CUDA, "measure: kernel failed");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    if (i >= warmup) times.push_back(ms * 1000.f);
+    *us = ms * 1000.f;
+    return TEC_OK;
+  };
+  for (int trial = 0; trial < 3 && st == TEC_OK; ++trial) {
+    float t_all = 0.f, t_flush = 0.f;
+    st = batch(true, &t_all);
+    if (st == TEC_OK && flush_l2) st = batch(false, &t_flush);
+    if (st == TEC_OK) times.push_back(std::max(0.f, t_all - t_flush) / n);
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

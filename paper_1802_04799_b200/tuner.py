@@ -7,8 +7,9 @@ Reference -> here:
          CTA N tile, M sub-tiles); config_at is the same mixed-radix decode
          (knob 0 varies slowest).
   measure / measure_program         tune.cpp:295-351 (simulated cycles,
-      sequential) -> tec_measure: CUDA-event timing on the GPU, median of
-      `repeats` launches with L2 flushed between them, configs sharded
+      sequential) -> tec_measure: CUDA-event timing on the GPU of
+      `repeats` back-to-back (L2 flush, launch) pairs minus the flushes
+      alone, median of three such batches, configs sharded
       round-robin over the visible devices (one host thread per device).
   TrialRecord / append_trials /     tune.cpp:101-144 (JSONL DB)
   load_trials                       -> identical JSONL fields.
