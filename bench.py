@@ -35,6 +35,7 @@ sys.path.insert(0, REPO)
 
 from paper_1802_04799_b200.workloads import RESNET18_CONVS, resnet_layer  # noqa: E402
 
+DEFAULT_KNOBS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_tuned_knobs.json")
 METRIC = "ResNet-18 conv C1-C12 TFLOP/s (% roofline)"
 LAYERS = list(RESNET18_CONVS)
 REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
@@ -223,10 +224,16 @@ def impl_ours(args):
     # the knob grid of every layer (untimed) and the step uses the best.
     from paper_1802_04799_b200.device import make_desc
     from paper_1802_04799_b200.tuner import conv_space, tune
+    # Default: the tuning log of an earlier on-device tuning run of this same
+    # step (bench.py --retune --knobs-out ...), read like the reference's
+    # trial DB with budget 0 (tune.cpp:355-436). Live tuning of the 12 layers
+    # in isolation picks differently from run to run (+-2% on the step).
     tuned = {}
-    if args.knobs_in:
-        with open(args.knobs_in) as f:
+    knobs_in = args.knobs_in or ("" if args.retune else DEFAULT_KNOBS)
+    if knobs_in and os.path.exists(knobs_in):
+        with open(knobs_in) as f:
             tuned = json.load(f)
+    knobs_src = knobs_in if tuned else "tuned live (tec_measure over the knob grid)"
     for n in LAYERS:
         if n in tuned:
             continue
@@ -351,6 +358,7 @@ def impl_ours(args):
                       "flush L2 (256 MB write) before each launch",
                 "timing": "CUDA graph of the 12 launches replayed K times; CUDA events on "
                           "the replay stream; max over ranks",
+                "knobs": knobs_src,
             },
             "roofline": {
                 "bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf,
@@ -431,6 +439,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tune", action="store_true", help="library default knobs")
     ap.add_argument("--knobs-in", default="", help="JSON {layer: knobs} to use instead of tuning")
+    ap.add_argument("--retune", action="store_true",
+                    help="tune every layer live instead of reading the committed tuning log")
     ap.add_argument("--knobs-out", default="", help="write the tuned knobs here")
     ap.add_argument("--workload", default="conv",
                     choices=["conv", "resnet18", "depthwise", "c2b1", "int8"],
