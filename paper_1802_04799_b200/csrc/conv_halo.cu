@@ -45,11 +45,14 @@ struct HaloCfg {
   static constexpr int kWBytes = BN * SWZ;
   // kPair: every sub-tile accumulator is [lo BN | hi BN] columns (see below)
   static constexpr uint32_t kAccCols = MS * BN * (kPair ? 2 : 1);
-  static constexpr uint32_t kTmemCols = 2 * kAccCols <= 32    ? 32
-                                        : 2 * kAccCols <= 64  ? 64
-                                        : 2 * kAccCols <= 128 ? 128
-                                        : 2 * kAccCols <= 256 ? 256
-                                                              : 512;
+  // TMEM accumulator buffers (knob acc_bufs; the paper's virtual threads):
+  // up to 4 when they fit, so the MMA can run ahead of a slow epilogue.
+  static constexpr int kMaxAcc = 4 * kAccCols <= 512 ? 4 : 2;
+  static constexpr uint32_t kTmemCols = kMaxAcc * kAccCols <= 32    ? 32
+                                        : kMaxAcc * kAccCols <= 64  ? 64
+                                        : kMaxAcc * kAccCols <= 128 ? 128
+                                        : kMaxAcc * kAccCols <= 256 ? 256
+                                                                    : 512;
   static_assert(2 * kAccCols <= 512, "TMEM holds at most 512 columns");
   static constexpr int kMmaPerTap = SWZ / 32;
 };
@@ -90,14 +93,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* wfull = hempty + 2;
   uint64_t* wempty = wfull + WSTAGES;
   uint64_t* tfull = wempty + WSTAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   uint32_t* sBias = reinterpret_cast<uint32_t*>(
       reinterpret_cast<uint8_t*>(hfull) + 256);  // [2][BN] f32 / i32
   float* sXchg = reinterpret_cast<float*>(sBias + 2 * BN);  // kPair: [2 grp][MS][4 warps][64]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
+  // accumulator ring: tile `local` uses buffer local % nacc; epilogue group
+  // local % 2 drains it (nacc even: a buffer always belongs to one group)
+  const int nacc = p.nacc == 4 && Cfg::kMaxAcc == 4 ? 4 : 2;
+  const int acc_shift = nacc == 4 ? 2 : 1;
   const int taps = p.r * p.s;
   const int num_tiles = p.n * p.bands * p.n_tiles;
   long long dbg_wait[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -120,8 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&hfull[i], 1);
       mbar_init(&hempty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);  // one epilogue group per accumulator
+      mbar_init(&tempty[i], 128);  // the epilogue group of the accumulator
     }
     for (int i = 0; i < WSTAGES; ++i) {
       mbar_init(&wfull[i], 1);
@@ -267,8 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int npair = ps >> 1;
         const uint32_t odd_skip = static_cast<uint32_t>(((ps & 1) ? 1 : 0) * SWZ) >> 4;
         for (int local = 0; tile_at(local, &n_tile, &band, &img); ++local) {
-          const int acc = local & 1;
-          const uint32_t use = static_cast<uint32_t>(local >> 1);
+          const int acc = local & (nacc - 1);
+          const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
           { const long long t0 = dbg ? clock64() : 0;
             mbar_wait(&tempty[acc], (use & 1) ^ 1);
             if (dbg) dbg_wait[2] += clock64() - t0; }
@@ -314,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue = [&](auto resident_c) {
         constexpr bool kRes = decltype(resident_c)::value;
         for (int local = 0; tile_at(local, &n_tile, &band, &img); ++local) {
-          const int acc = local & 1;
-          const uint32_t use = static_cast<uint32_t>(local >> 1);
+          const int acc = local & (nacc - 1);
+          const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
           { const long long t0 = dbg ? clock64() : 0;
             mbar_wait(&tempty[acc], (use & 1) ^ 1);
             if (dbg) dbg_wait[2] += clock64() - t0; }
@@ -400,10 +409,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int n_tile, band, img;
     bool dummy = false;
     for (; tile_at(local, &n_tile, &band, &img, &dummy); ++local) {
-      const int acc = local & 1;
-      if (acc != grp) continue;
-      const uint32_t use = static_cast<uint32_t>(local >> 1);
-      uint32_t* bias_s = sBias + acc * BN;
+      if ((local & 1) != grp) continue;
+      const int acc = local & (nacc - 1);
+      const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
+      uint32_t* bias_s = sBias + grp * BN;
       // The group's bias buffer only changes with the output-channel tile
       // (a global load + two barriers on the per-tile critical path).
       if (n_tile != staged_n_tile) {

@@ -85,6 +85,7 @@ struct ConvHaloParams {
   int32_t tma_store;        // 1: y has a TMA store map (fast programs use it)
   int32_t stage_bytes;      // epilogue stage (>= 32 KB); two halves, one per group
   int32_t cl;               // streamed weights: CTAs per cluster sharing them by multicast
+  int32_t nacc;             // TMEM accumulator buffers: 2 or 4 (when 4 fit in 512 columns)
 };
 
 struct DepthwiseParams {

@@ -552,6 +552,10 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   p.resident = hc.resident;
   p.w_slots = hc.w_slots;
   p.cl = hc.cl;
+  // knob acc_bufs: TMEM accumulator buffers (2 or 4; 0 = 4 when they fit)
+  if (kn && kn->acc_bufs && kn->acc_bufs != 2 && kn->acc_bufs != 4)
+    return fail(TEC_E_LOWERING, "acc_bufs must be 2 or 4");
+  p.nacc = kn && kn->acc_bufs ? (int32_t)kn->acc_bufs : 4;
   p.out_type = out_dtype;
   p.y = y;
   p.err = err;
@@ -599,7 +603,8 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   if (plan_only(TEC_KERNEL_HALO, hc.inst->bn, 128 * hc.inst->ms, hc.resident ? 2 : 1, grid,
                 conv_halo_smem_bytes(hc.inst->bn, hc.inst->swz, hc.w_slots, hc.halo_px,
                                      p.stage_bytes, hc.inst->ms, hc.inst->pair),
-                tmem_cols_for(2 * hc.inst->ms * hc.inst->bn * (hc.inst->pair ? 2 : 1)),
+                tmem_cols_for((4 * hc.inst->ms * hc.inst->bn * (hc.inst->pair ? 2 : 1) <= 512 ? 4 : 2) *
+                              hc.inst->ms * hc.inst->bn * (hc.inst->pair ? 2 : 1)),
                 p.tma_store, 1, hc.cl))
     return TEC_OK;
   const int e = hc.inst->fn(tm_x, tm_w, tm_y, p, grid, st);
