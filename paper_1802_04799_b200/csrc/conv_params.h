@@ -54,6 +54,7 @@ struct ConvGemmParams {
   // tile to ws, and the last split to arrive (tile_cnt) sums the partials in
   // split order and runs the epilogue. Requires the TMA-store fast path.
   int32_t splits, kps;
+  int32_t nacc;         // TMEM accumulator buffers: 2 or 4 (when 4 fit in 512 columns)
   float* ws;            // [m_tiles*n_tiles][splits][128][BN]
   int32_t* tile_cnt;    // [m_tiles*n_tiles], zero between launches
 };

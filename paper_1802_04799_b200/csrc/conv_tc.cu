@@ -51,11 +51,13 @@ struct ConvCfg {
   static constexpr int kBBytes = BN * SWZ;   // one stage of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kMmaPerStage = SWZ / 32;  // each MMA eats 32 B of K
-  static constexpr uint32_t kTmemCols = 2 * BN <= 32    ? 32
-                                        : 2 * BN <= 64  ? 64
-                                        : 2 * BN <= 128 ? 128
-                                        : 2 * BN <= 256 ? 256
-                                                        : 512;
+  // TMEM accumulator ring: 4 buffers when they fit (knob acc_bufs), else 2
+  static constexpr int kMaxAcc = 4 * BN <= 512 ? 4 : 2;
+  static constexpr uint32_t kTmemCols = kMaxAcc * BN <= 32    ? 32
+                                        : kMaxAcc * BN <= 64  ? 64
+                                        : kMaxAcc * BN <= 128 ? 128
+                                        : kMaxAcc * BN <= 256 ? 256
+                                                              : 512;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + STAGES * kStageBytes +
                                     8 * 4096 /*epilogue stage*/ + 256 /*barriers*/ +
                                     2 * BN * 4 /*bias*/;
@@ -78,13 +80,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   uint32_t* sBias = reinterpret_cast<uint32_t*>(
       reinterpret_cast<uint8_t*>(full) + 256);  // [2][BN] f32 / i32
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
+  // tile `local` -> accumulator local % nacc, drained by epilogue group local % 2
+  const int nacc = p.nacc == 4 && Cfg::kMaxAcc == 4 ? 4 : 2;
+  const int acc_shift = nacc == 4 ? 2 : 1;
   const int splits = p.splits > 1 ? p.splits : 1;
   const int num_tiles = p.m_tiles * p.n_tiles * splits;  // work items
   const int k_iters = p.r * p.s * p.cblocks;
@@ -104,9 +109,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);  // one epilogue group (4 warps) per accumulator
+      mbar_init(&tempty[i], 128);  // the epilogue group (4 warps) of the accumulator
     }
     fence_barrier_init();
   }
@@ -173,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int local = 0;
       for (int tile = blockIdx.x; tile < num_tiles;
            tile += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        const int acc = local & (nacc - 1);
+        const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
         { const long long t0 = p.dbg ? clock64() : 0;
           mbar_wait(&tempty[acc], (use & 1) ^ 1);
           if (p.dbg) dbg_wait[2] += clock64() - t0; }
@@ -226,9 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool overflow = false;
     for (int tile = blockIdx.x; tile < num_tiles;
          tile += gridDim.x, ++local) {
-      const int acc = local & 1;
-      if (acc != grp) continue;
-      const uint32_t use = static_cast<uint32_t>(local >> 1);
+      if ((local & 1) != grp) continue;
+      const int acc = local & (nacc - 1);
+      const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
       const int mn = tile / splits;
       const int split = tile - mn * splits;
       const int m_tile = mn / p.n_tiles;
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = row0 + static_cast<int>(lane);
       const bool row_ok = row < p.m;
       // Per-tile bias copy in smem (one buffer per group).
-      uint32_t* bias_s = sBias + acc * BN;
+      uint32_t* bias_s = sBias + grp * BN;
       // The group's bias buffer only changes with the output-channel tile
       // (a global load + two barriers on the per-tile critical path).
       if (n_tile != staged_n_tile) {

@@ -781,6 +781,10 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   p.epi = epi;
   // knob vec: 1 = per-thread epilogue rows, 2 = no epilogue (diagnostic only)
   p.epi_mode = kn && (kn->vec == 1 || kn->vec == 2) ? (int32_t)kn->vec : 0;
+  // knob acc_bufs: TMEM accumulator buffers (2 or 4; 0 = 4 when they fit)
+  if (kn && kn->acc_bufs && kn->acc_bufs != 2 && kn->acc_bufs != 4)
+    return fail(TEC_E_LOWERING, "acc_bufs must be 2 or 4");
+  p.nacc = kn && kn->acc_bufs ? (int32_t)kn->acc_bufs : 4;
   CUtensorMap tm_y;
   {
     cuuint64_t dims[2] = {(cuuint64_t)d->k, (cuuint64_t)pl.m};
@@ -822,7 +826,7 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
-  if (plan_only(TEC_KERNEL_IM2COL, bn, 128, 0, grid, 0, tmem_cols_for(2 * bn), p.tma_store,
+  if (plan_only(TEC_KERNEL_IM2COL, bn, 128, 0, grid, 0, tmem_cols_for((4 * bn <= 512 ? 4 : 2) * bn), p.tma_store,
                 p.splits, 1))
     return TEC_OK;
   const int e = launch(tm_a, tm_b, tm_y, p, grid, st);
