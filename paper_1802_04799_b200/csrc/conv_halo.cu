@@ -143,8 +143,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_launch_dependents();  // see conv_tc.cu
-  pdl_wait();
+  // Let the next layer launch. Only the producer waits for the previous one
+  // (pdl_wait below), after issuing the resident weights (parameters): the
+  // halo loads follow the wait, and every later step -- MMAs, epilogue reads
+  // of the residual, output writes -- is ordered after them by mbarriers.
+  pdl_launch_dependents();
 
   // Tile order. Streamed weights: tiles strided over the grid, N fastest.
   // Resident weights (p.resident): each CTA keeps ONE output-channel tile
@@ -201,6 +204,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sW + (cb * taps + t) * Cfg::kWBytes, &tm_w, &wfull[0],
                         t * p.cp + cb * kCB, n_tile * BN);
       }
+      // streamed weights (no cluster): the first ring pass before the wait too
+      int wpre = 0;
+      if (!p.resident && cl == 1 && tile_at(0, &n_tile, &band, &img)) {
+        for (int j = 0; j < taps * p.cblocks && wpre < WSTAGES; ++j, ++wpre) {
+          const int cb = j / taps, t = j - cb * taps;
+          mbar_arrive_expect_tx(&wfull[wpre], Cfg::kWBytes);
+          tma_load_2d(sW + wpre * Cfg::kWBytes, &tm_w, &wfull[wpre], t * p.cp + cb * kCB,
+                      n_tile * BN);
+        }
+      }
+      pdl_wait();
       bool dummy = false;
       for (int i = 0; tile_at(i, &n_tile, &band, &img, &dummy); ++i) {
         const int ih0 = band * p.th - p.ph;
@@ -227,6 +241,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++hs == 2) { hs = 0; hph ^= 1; }
           if (p.resident) continue;
           for (int t = 0; t < taps; ++t) {
+            if (wpre > 0) {  // issued before the wait
+              --wpre;
+              if (++ws == WSTAGES) { ws = 0; wph ^= 1; }
+              continue;
+            }
             { const long long t0 = p.dbg ? clock64() : 0;
               mbar_wait(&wempty[ws], wph ^ 1);
               if (p.dbg) dbg_wait[0] += clock64() - t0; }

@@ -120,14 +120,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // Prologue done: let the next layer launch, then wait for the previous
-  // layer's outputs (our inputs) to be complete and visible.
+  // Prologue done: let the next layer launch. Only the producer waits for
+  // the previous layer (pdl_wait below), after issuing the weight (B) boxes
+  // of the first ring pass -- parameters; the activation loads follow the
+  // wait and every later step is ordered after them by mbarriers.
   pdl_launch_dependents();
-  pdl_wait();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer warp
     if (elect_one()) {
+      int pre = 0;  // stages whose B box went out before the wait
+      if (static_cast<int>(blockIdx.x) < num_tiles) {
+        const int mn = static_cast<int>(blockIdx.x) / splits;
+        const int n_tile0 = mn % p.n_tiles;
+        const int kb = (static_cast<int>(blockIdx.x) - mn * splits) * kps;
+        const int ke = min(k_iters, kb + kps);
+        for (int k = kb; k < ke && pre < STAGES; ++k, ++pre) {
+          mbar_arrive_expect_tx(&full[pre], Cfg::kStageBytes);
+          // k = (r * S + s) * cblocks + cb -> weight column k * kCB
+          tma_load_2d(sB + pre * Cfg::kBBytes, &tm_b, &full[pre], k * kCB, n_tile0 * BN);
+        }
+      }
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       const int ohw = p.oh * p.ow;
@@ -148,6 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         int r = kb / sc, rem_k = kb - r * sc;
         int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
         for (int k = kb; k < ke; ++k) {
+          if (pre > 0) {  // B already in flight, the stage known free
+            --pre;
+            tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a,
+                               &full[stage], cb * kCB, w0, h0, img,
+                               static_cast<uint16_t>(s),
+                               static_cast<uint16_t>(r));
+          } else {
           { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&empty[stage], phase ^ 1);
             if (p.dbg) dbg_wait[0] += clock64() - t0; }
@@ -158,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              static_cast<uint16_t>(r));
           tma_load_2d(sB + stage * Cfg::kBBytes, &tm_b, &full[stage],
                       (r * p.s + s) * p.cp + cb * kCB, n_tile * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
