@@ -94,8 +94,11 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  // Only the TMA-issuing thread waits for the previous layer: every other
+  // thread reads activations from the smem tiles it lands (mbarrier-ordered)
+  // and meanwhile loads its taps and bias (parameters) early.
   pdl_launch_dependents();
-  pdl_wait();
+  if (tid == 0) pdl_wait();
 
   // tile -> (cblk slowest, so a CTA's consecutive tiles mostly share taps)
   auto decode = [&](int tile, int* n, int* band, int* cblk) {
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
   }
   __syncthreads();
   pdl_launch_dependents();
-  pdl_wait();
+  if (tid == 0) pdl_wait();  // only the TMA issuer touches the previous layer's output
   auto decode = [&](int tile, int* n, int* band, int* cblk) {
     const int per_c = ngroups * t.bands;
     *cblk = tile / per_c;
