@@ -8,15 +8,16 @@
 #include "sm100_ptx.cuh"
 using namespace tec_sm100;
 template <int SWZ, int MS, int KK, int R, int BN, bool kCommit, bool kKOuter = false, bool kResetB = true, int ACCS = BN>
-__global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, int boff) {
+__global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, int boff, int aoff, int bstride) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = sm;                 // halo: up to 96 KB
+  uint8_t* sA = sm + aoff;          // halo: up to 96 KB (aoff: base shift)
   uint8_t* sB = sm + 96 * 1024 + boff;  // weights: R*R*BN*SWZ (boff: base shift, bytes)
   uint64_t* bar = (uint64_t*)(sm + 200 * 1024);
   uint32_t* slot = (uint32_t*)(bar + 2);
   static_assert((kResetB ? R : R * R) * BN * SWZ <= 72 * 1024, "B tiles must fit the B region");
-  if (boff > 32 * 1024) return;
+  if (boff > 32 * 1024 || aoff > 32 * 1024) return;
+  if (bstride && (kResetB ? R : R * R) * bstride + boff > 104 * 1024) return;
   for (int i = threadIdx.x; i < 200 * 1024 / 16; i += blockDim.x)
     ((uint4*)sm)[i] = make_uint4(0x3f803f80u, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;");
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, i
           }
           accum = 1;
           ad += SWZ >> 4;
-          bd += (BN * SWZ) >> 4;
+          bd += (bstride ? bstride : BN * SWZ) >> 4;
         }
         ad += row_skip;
         if (kResetB) bd = b0;  // one filter row of weight tiles, reused
@@ -70,31 +71,31 @@ __global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, i
   if (threadIdx.x / 32 == 1) tmem_dealloc<512>(tmem);
 }
 template <int SWZ, int MS, int KK, int R, int BN, bool kC, bool kKO = false, bool kRB = true, int ACCS = BN>
-void run(const char* name, int wp, int boff = 0) {
+void run(const char* name, int wp, int boff = 0, int aoff = 0, int bstride = 0) {
   long long* d; cudaMalloc(&d, 148 * 8);
   auto f = k<SWZ, MS, KK, R, BN, kC, kKO, kRB, ACCS>;
   const int smem = 200 * 1024 + 2048;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int tiles = 400;
-  f<<<148, 128, smem>>>(tiles, wp, d, boff);
+  f<<<148, 128, smem>>>(tiles, wp, d, boff, aoff, bstride);
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("%s: kernel failed\n", name); exit(1); }
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  f<<<148, 128, smem>>>(tiles, wp, d, boff);
+  f<<<148, 128, smem>>>(tiles, wp, d, boff, aoff, bstride);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   const double mmas = (double)tiles * R * R * MS * KK;
-  printf("%s boff=%d: %.1f us, %.1f ns/MMA/SM -> %.2f GHz-equiv at 54 cyc  (%s)\n", name, boff, ms * 1e3,
+  printf("%s boff=%d aoff=%d bstride=%d: %.1f us, %.1f ns/MMA/SM -> %.2f GHz-equiv at 54 cyc  (%s)\n", name, boff, aoff, bstride, ms * 1e3,
          ms * 1e6 / mmas, 54.0 / (ms * 1e6 / mmas), cudaGetErrorString(cudaGetLastError()));
   long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   printf("   issue-side cycles/MMA (thread 0 loop) %.1f\n", (double)h[0] / mmas);
   cudaFree(d);
 }
 int main() {
-  run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB acc stride 64", 58);
-  run<128, 2, 4, 3, 64, true, false, false, 128>("C2 MS2 B72KB acc stride 128", 58);
-  run<128, 3, 4, 3, 64, true, false, false>("C2 MS3 B72KB", 58);
-  run<128, 2, 4, 3, 64, false, false, false>("C2 MS2 B72KB no per-tile commit", 58);
-  run<128, 2, 4, 3, 64, true, false, true>("C2 MS2 B24KB", 58);
+  run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB", 58, 0, 0, 0);
+  for (int aoff : {1024, 4096, 8192, 16384})
+    run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB", 58, 0, aoff, 0);
+  for (int bstride : {9216, 10240, 11264})
+    run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB", 58, 0, 0, bstride);
   return 0;
 }
