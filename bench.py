@@ -132,7 +132,10 @@ def impl_reference(args):
         kind = "reference"
     vals = []
     sample = None
-    for i in range(args.warmup + args.steps):
+    # each step is a ~1 s bounded CPU sample: at most 20 timed steps keep the
+    # reference arm within a few minutes whatever K the caller asks for
+    steps = min(args.steps, 20)
+    for i in range(args.warmup + steps):
         if kind == "reference":
             flops, wall, sample = run_reference_sample(threads, seed=i)
         else:
@@ -144,7 +147,7 @@ def impl_reference(args):
     value = tot_f / tot_t / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_t / max(1, len(vals)) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C1-C12 fused conv2d+bias_add+relu (bounded CPU sample)",
@@ -168,6 +171,7 @@ class ClockSampler:
         self.device = device
         self.sm, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
+        self._ready = threading.Event()  # NVML initialised, first sample taken
 
     def _run(self):
         try:
@@ -175,6 +179,7 @@ class ClockSampler:
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._ready.set()
             while not self._stop.is_set():
                 self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
                 r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
@@ -184,11 +189,15 @@ class ClockSampler:
                 time.sleep(0.001)
         except Exception as e:  # pragma: no cover
             self.error = repr(e)
+        finally:
+            self._ready.set()
 
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
-        time.sleep(0.05)
+        # NVML start-up can take longer than a short timed region: start the
+        # region only once the sampler runs
+        self._ready.wait(timeout=10.0)
         return self
 
     def __exit__(self, *a):
@@ -431,7 +440,7 @@ def run_e2e(args, batch, device):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
