@@ -453,21 +453,21 @@ int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
 
 // bf16: 128 B channel blocks (64 ch) for Cp % 64 == 0, 32 B (16 ch) for
 // the stem (C1, 3 -> 16 padded channels).
-TEC_INST(MmaKind::kF16, 64, 7, 128)
-TEC_INST(MmaKind::kF16, 128, 5, 128)
+TEC_INST(MmaKind::kF16, 64, 8, 128)
+TEC_INST(MmaKind::kF16, 128, 6, 128)
 TEC_INST(MmaKind::kF16, 256, 3, 128)
 TEC_INST(MmaKind::kF16, 64, 8, 32)
 // int8: 128 B blocks (128 ch), 64 B (64 ch), 32 B (32 ch, the stem).
-TEC_INST(MmaKind::kI8, 64, 7, 128)
-TEC_INST(MmaKind::kI8, 128, 5, 128)
+TEC_INST(MmaKind::kI8, 64, 8, 128)
+TEC_INST(MmaKind::kI8, 128, 6, 128)
 TEC_INST(MmaKind::kI8, 256, 3, 128)
 TEC_INST(MmaKind::kI8, 64, 8, 64)
 TEC_INST(MmaKind::kI8, 128, 6, 64)
 TEC_INST(MmaKind::kI8, 64, 8, 32)
 // tf32 (approximate-f32 3xTF32 path, K = [hi|hi|lo] x [hi|lo|hi]): 128 B
 // blocks (32 ch), 64 B (16 ch, the stem: 3*3 -> 16 padded channels).
-TEC_INST(MmaKind::kTF32, 64, 7, 128)
-TEC_INST(MmaKind::kTF32, 128, 5, 128)
+TEC_INST(MmaKind::kTF32, 64, 8, 128)
+TEC_INST(MmaKind::kTF32, 128, 6, 128)
 TEC_INST(MmaKind::kTF32, 256, 3, 128)
 TEC_INST(MmaKind::kTF32, 64, 8, 64)
 

@@ -339,18 +339,18 @@ using Launcher = int (*)(const CUtensorMap&, const CUtensorMap&, const CUtensorM
 Launcher pick_launcher(MmaKind kind, int bn, int swz) {
 #define TEC_CASE(K, BN, ST, SW) \
   if (kind == K && bn == BN && swz == SW) return &launch_conv_fprop_tc<K, BN, ST, SW>;
-  TEC_CASE(MmaKind::kF16, 64, 7, 128)
-  TEC_CASE(MmaKind::kF16, 128, 5, 128)
+  TEC_CASE(MmaKind::kF16, 64, 8, 128)
+  TEC_CASE(MmaKind::kF16, 128, 6, 128)
   TEC_CASE(MmaKind::kF16, 256, 3, 128)
   TEC_CASE(MmaKind::kF16, 64, 8, 32)
-  TEC_CASE(MmaKind::kI8, 64, 7, 128)
-  TEC_CASE(MmaKind::kI8, 128, 5, 128)
+  TEC_CASE(MmaKind::kI8, 64, 8, 128)
+  TEC_CASE(MmaKind::kI8, 128, 6, 128)
   TEC_CASE(MmaKind::kI8, 256, 3, 128)
   TEC_CASE(MmaKind::kI8, 64, 8, 64)
   TEC_CASE(MmaKind::kI8, 128, 6, 64)
   TEC_CASE(MmaKind::kI8, 64, 8, 32)
-  TEC_CASE(MmaKind::kTF32, 64, 7, 128)
-  TEC_CASE(MmaKind::kTF32, 128, 5, 128)
+  TEC_CASE(MmaKind::kTF32, 64, 8, 128)
+  TEC_CASE(MmaKind::kTF32, 128, 6, 128)
   TEC_CASE(MmaKind::kTF32, 256, 3, 128)
   TEC_CASE(MmaKind::kTF32, 64, 8, 64)
 #undef TEC_CASE
