@@ -373,7 +373,9 @@ def impl_ours(args):
                 "bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf,
                 "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 3),
                 "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src})",
-                "kernel": "conv_fprop_tc_kernel (tcgen05 implicit GEMM), all 12 launches",
+                "kernel": "fused conv kernels (conv_halo_kernel / conv_fprop_tc_kernel, tcgen05 "
+                          "implicit GEMM), all 12 launches: sum of flops / sum of per-layer "
+                          "kernel times",
             },
             "layers": per_layer,
             "gpu_launches": len(layers) * args.steps,
