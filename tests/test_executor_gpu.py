@@ -172,3 +172,34 @@ def test_unsupported_node_raises_lowering_error():
     with pytest.raises(TecError) as e:
         DeviceGraph(g)
     assert e.value.code == "LoweringError"
+
+
+def test_native_plan_runtime_steps_and_errors():
+    """The executor's launch list is a native tec_plan: its size is the
+    compiled step count, running steps one by one (tec_plan_run_steps) gives
+    the same bytes as tec_plan_run, and a conv step without a kernel is
+    rejected at tec_plan_create (LoweringError), not at run time."""
+    import ctypes as C
+
+    from paper_1802_04799_b200 import _abi
+    g = resnet18_graph(1, width=8, head=False, maxpool=False)
+    dg = DeviceGraph(g, compute="bf16")
+    vals = _resnet_inputs(g, seed=5)
+    feeds, params = _split(dg, vals)
+    dg.bind_params(params)
+    assert dg.n_launches == len(dg.steps) > 0
+    out = dg.run(feeds)
+    for name in dg.feed_names:
+        dg.set_feed(name, feeds[name])
+    for i in range(dg.n_launches):
+        dg.launch_step(i)
+    torch.cuda.synchronize()
+    for o in dg.outputs:
+        assert np.array_equal(dg.output(o).cpu().numpy(), out[o])
+    lib = _abi.load()
+    bad = _abi.Step(kind=_abi.STEP_CONV, dst_dtype=_abi.DT_BF16, conv=dg.steps[0].conv)
+    bad.conv.compute = 99  # no such compute mode
+    h = C.c_void_p()
+    st = lib.tec_plan_create((_abi.Step * 1)(bad), 1, C.byref(h))
+    assert st != 0 and not h.value
+    assert lib.tec_plan_run_steps(dg._native, dg.n_launches, 1, None) != 0  # out of range
