@@ -7,7 +7,7 @@
 #include <cstdio>
 #include "sm100_ptx.cuh"
 using namespace tec_sm100;
-template <int SWZ, int MS, int KK, int R, int BN, bool kCommit, bool kKOuter = false, bool kResetB = true, int ACCS = BN>
+template <int SWZ, int MS, int KK, int R, int BN, bool kCommit, bool kKOuter = false, bool kResetB = true, int ACCS = BN, bool kMsOuter = false>
 __global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, int boff, int aoff, int bstride) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -33,6 +33,27 @@ __global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, i
     long long t0 = clock64();
     for (int t = 0; t < tiles; ++t) {
       const uint32_t d0 = tmem + (t & 1) * MS * ACCS;
+      if constexpr (kMsOuter) {
+        for (int ms = 0; ms < MS; ++ms) {
+          uint64_t ad = a0 + ((ms * 128 * SWZ) >> 4), bd = b0;
+          uint32_t accum = 0;
+          for (int rh = 0; rh < R; ++rh) {
+            for (int rw = 0; rw < R; ++rw) {
+#pragma unroll
+              for (int kk = 0; kk < KK; ++kk)
+                tc_mma<MmaKind::kF16>(d0 + ms * ACCS, ad + ((kk * 32) >> 4), bd + ((kk * 32) >> 4),
+                                      idesc, kk == 0 ? accum : 1u);
+              accum = 1;
+              ad += SWZ >> 4;
+              bd += (bstride ? bstride : BN * SWZ) >> 4;
+            }
+            ad += row_skip;
+            if (kResetB) bd = b0;
+          }
+        }
+        if (kCommit) tc_commit(&bar[t & 1]);
+        continue;
+      }
       uint64_t ad = a0, bd = b0;
       uint32_t accum = 0;
       for (int rh = 0; rh < R; ++rh) {
@@ -70,10 +91,10 @@ __global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, i
   tc_fence_before(); __syncthreads(); tc_fence_after();
   if (threadIdx.x / 32 == 1) tmem_dealloc<512>(tmem);
 }
-template <int SWZ, int MS, int KK, int R, int BN, bool kC, bool kKO = false, bool kRB = true, int ACCS = BN>
+template <int SWZ, int MS, int KK, int R, int BN, bool kC, bool kKO = false, bool kRB = true, int ACCS = BN, bool kMO = false>
 void run(const char* name, int wp, int boff = 0, int aoff = 0, int bstride = 0) {
   long long* d; cudaMalloc(&d, 148 * 8);
-  auto f = k<SWZ, MS, KK, R, BN, kC, kKO, kRB, ACCS>;
+  auto f = k<SWZ, MS, KK, R, BN, kC, kKO, kRB, ACCS, kMO>;
   const int smem = 200 * 1024 + 2048;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int tiles = 400;
@@ -92,10 +113,10 @@ void run(const char* name, int wp, int boff = 0, int aoff = 0, int bstride = 0) 
   cudaFree(d);
 }
 int main() {
-  run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB", 58, 0, 0, 0);
-  for (int aoff : {1024, 4096, 8192, 16384})
-    run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB", 58, 0, aoff, 0);
-  for (int bstride : {9216, 10240, 11264})
-    run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB", 58, 0, 0, bstride);
+  run<128, 2, 4, 3, 64, true, false, false>("C2 MS2 B72KB (ms inside the tap loop)", 58);
+  run<128, 2, 4, 3, 64, true, false, false, 64, true>("C2 MS2 B72KB (ms outermost)", 58);
+  run<128, 1, 4, 3, 64, true, false, false>("C2 MS1 B72KB", 58);
+  run<32, 4, 1, 4, 64, true, false, false>("C1 MS4 SW32 B32KB (ms inside)", 116);
+  run<32, 4, 1, 4, 64, true, false, false, 64, true>("C1 MS4 SW32 B32KB (ms outermost)", 116);
   return 0;
 }
