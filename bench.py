@@ -304,23 +304,43 @@ def impl_ours(args):
     max_ms = float(t.item())
     value = world * step_flops * args.steps / (max_ms / 1e3) / 1e12
 
-    # ---- per-layer kernel durations (same stream, L2 flushed before each).
+    # ---- per-layer kernel durations, L2 flushed before each launch. Event
+    # timestamps here move in ~2 us steps, too coarse for one 6-45 us launch:
+    # a CUDA graph of R x (flush, launch) is timed against R x flush alone
+    # (median of 3 each) and the difference / R is the launch's device time.
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     per_layer = []
-    reps = max(5, min(20, args.steps))
-    for l, fl in zip(layers, flops):
-        times = []
+    reps = 10
+
+    def graph_of(fn):
         with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        return g
+
+    def median_ms(g):
+        ts = []
+        for _ in range(3):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    flush_ms = median_ms(graph_of(lambda: [flush.zero_() for _ in range(reps)]))
+    for l, fl in zip(layers, flops):
+        def body(l=l):
             for _ in range(reps):
                 flush.zero_()
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
                 l.launch(stream)
-                b.record(stream)
-                times.append((a, b))
-        torch.cuda.synchronize()
-        us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in times)
+        us = max(1e-3, (median_ms(graph_of(body)) - flush_ms) * 1e3 / reps)
         byts = l.algorithmic_bytes()
         ai = fl / byts
         bound_tf = min(peak_tf, ai * hbm_gbs / 1e3)
@@ -364,7 +384,8 @@ def impl_ours(args):
                             f"batch {batch} per GPU, bf16 in / f32 accumulate / bf16 out",
                 "global_batch": batch * world, "parallelism": f"replicas x{world} (no collective)",
                 "l2": "step working set (all 12 layers) > 126 MB L2; per-layer timings "
-                      "flush L2 (256 MB write) before each launch",
+                      "flush L2 (256 MB write) before each launch (graph of 10 x (flush, "
+                      "launch) minus 10 x flush)",
                 "timing": "CUDA graph of the 12 launches replayed K times; CUDA events on "
                           "the replay stream; max over ranks",
                 "knobs": knobs_src,
