@@ -321,9 +321,23 @@ def int8(args, bench):
     from paper_1802_04799_b200.device import DeviceConv, make_desc
     from paper_1802_04799_b200.tuner import conv_space, measure
     from paper_1802_04799_b200.workloads import RESNET18_CONVS, resnet_layer
+    from paper_1802_04799_b200.tuner import tune
     rank, ws, local = _dist()
     batch = args.batch
-    layers = [DeviceConv(resnet_layer(n, batch), compute="i8", device=local, seed=i)
+    # per-layer knobs from the on-device tuner (the same exhaustive grid the
+    # bf16 headline uses), untimed; --no-tune keeps the library defaults
+    knobs = {}
+    t_tune = time.perf_counter()
+    for n in RESNET18_CONVS:
+        if args.no_tune:
+            break
+        sp = conv_space(f"{n}_b{batch}_i8", make_desc(resnet_layer(n, batch), "i8"))
+        best = tune(sp, budget=sp.size(), batch_size=sp.size(), method="random",
+                    devices=[local], repeats=5)
+        knobs[n] = best.config if best else {}
+    t_tune = time.perf_counter() - t_tune
+    layers = [DeviceConv(resnet_layer(n, batch), compute="i8", device=local, seed=i,
+                         knobs=knobs.get(n) or None)
               for i, n in enumerate(RESNET18_CONVS)]
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -354,7 +368,9 @@ def int8(args, bench):
             "scaling": "weak", "vs_baseline": None, "dtype": "i8", "data": "synthetic",
             "config": {"workload": f"configs[5]: C1-C12 int8 x int8 -> i32 + bias + relu, batch "
                                    f"{batch} (bit-exact path)", "global_batch": batch * ws,
-                       "parallelism": f"replicas x{ws}"},
+                       "parallelism": f"replicas x{ws}",
+                       "knobs": knobs or "library defaults",
+                       "tuning_seconds": round(t_tune, 1)},
             "tuning": {"trials": len(recs), "ok": len(ok), "seconds": round(dt, 2),
                        "trials_per_s": round(len(recs) / dt, 1),
                        "best_us": round(min(r.cost for r in ok), 2) if ok else None},

@@ -141,6 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  // Weight multicast: peers write into this CTA's shared memory and arrive
+  // on its barriers, so every CTA of the cluster must have initialised its
+  // barriers before any of them issues a load (cluster-scope release/acquire).
+  if (p.cl > 1 && !p.resident) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Let the next layer launch. Only the producer waits for the previous one
