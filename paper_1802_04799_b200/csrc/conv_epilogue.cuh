@@ -561,49 +561,9 @@ __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane
   }
 }
 
-// One row of a box, computed by a single thread (the paired-tap halo
-// kernel's last row per warp): v = lo + hi_next (f32, NULL hi = 0), then
-// the program (bias, residual from global, relu) into row `row` of `box`.
-template <int PROG, int ES>
-__device__ __forceinline__ void row_to_box(const float* lo, const float* hi_next,
-                                           const uint32_t* bias_s, const uint8_t* rrow,
-                                           uint32_t box, int row) {
-  float v[kChunk];
-#pragma unroll
-  for (int j = 0; j < kChunk; ++j) {
-    float x = __fadd_rn(lo[j], hi_next ? hi_next[j] : 0.0f);
-    if constexpr (PROG != kProgNone) x = __fadd_rn(x, __uint_as_float(bias_s[j]));
-    if constexpr (PROG == kProgBiasAddRelu) {
-      float r = 0.0f;
-      if (rrow) {
-        if constexpr (ES == 2)
-          r = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rrow)[j]);
-        else
-          r = reinterpret_cast<const float*>(rrow)[j];
-      }
-      x = __fadd_rn(x, r);
-    }
-    if constexpr (PROG == kProgBiasRelu || PROG == kProgBiasAddRelu) x = (x < 0.0f) ? 0.0f : x;
-    v[j] = x;
-  }
-  constexpr int kCpr = 32 * ES / 16;
-  if constexpr (ES == 2) {
-#pragma unroll
-    for (int c = 0; c < kCpr; ++c)
-      sts128(box + box_off<2>(row, c),
-             make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
-                        pack_bf16x2(v[8 * c + 4], v[8 * c + 5]),
-                        pack_bf16x2(v[8 * c + 6], v[8 * c + 7])));
-  } else {
-#pragma unroll
-    for (int c = 0; c < kCpr; ++c)
-      sts128(box + box_off<4>(row, c),
-             make_uint4(__float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]),
-                        __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3])));
-  }
-}
-
-// Same, one column per lane (j = lane): the whole warp finishes the row.
+// One row of a box (the paired-tap halo kernel's last row per warp), one
+// column per lane (j = lane): v = lo + hi_next (f32, NULL hi = 0), then the
+// program (bias, residual from global, relu) into row `row` of `box`.
 template <int PROG, int ES>
 __device__ __forceinline__ void row_col_to_box(const float* lo, const float* hi_next,
                                                const uint32_t* bias_s, const uint8_t* rrow,
