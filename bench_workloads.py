@@ -213,17 +213,65 @@ def _resnet_cpu_baseline(bench):
             "sample": desc + "; extrapolated to ResNet-18 conv MACs per image"}
 
 
+def _flushed_launch_us(launch, flush, stream, reps=10):
+    """Device time of one launch after an L2 flush: a CUDA graph of reps x
+    (flush, launch) minus reps x flush (median of 3 each); single-launch
+    events here move in ~2 us steps."""
+    import torch
+
+    def graph_of(fn):
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        return g
+
+    def med(g):
+        ts = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    def both():
+        for _ in range(reps):
+            flush.zero_()
+            launch()
+
+    t_f = med(graph_of(lambda: [flush.zero_() for _ in range(reps)]))
+    return max(1e-3, (med(graph_of(both)) - t_f) * 1e3 / reps)
+
+
 # ----------------------------------------------------------------- depthwise
 def depthwise(args, bench):
     import torch
 
     from paper_1802_04799_b200.device import DeviceConv
     from paper_1802_04799_b200.workloads import MOBILENET_DW, mobilenet_layer
+    from paper_1802_04799_b200.device import make_desc
+    from paper_1802_04799_b200.tuner import dw_space, tune
     rank, ws, local = _dist()
     batch = args.batch
     compute = args.dw_compute
+    # per-layer kernel choice (dw_space: the unroll knob selects the kernel
+    # variant) from the on-device tuner, untimed
+    knobs = {}
+    for n in MOBILENET_DW:
+        if args.no_tune:
+            break
+        sp = dw_space(f"{n}_b{batch}_{compute}", make_desc(mobilenet_layer(n, batch), compute))
+        best = tune(sp, budget=sp.size(), batch_size=sp.size(), method="random",
+                    devices=[local], repeats=5)
+        knobs[n] = best.config if best else {}
     layers = [DeviceConv(mobilenet_layer(n, batch), compute=compute, device=local, seed=i,
-                         out_dtype=0 if compute == "f32" else None)
+                         out_dtype=0 if compute == "f32" else None, knobs=knobs.get(n) or None)
               for i, n in enumerate(MOBILENET_DW)]
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -242,17 +290,7 @@ def depthwise(args, bench):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     per = []
     for l in layers:
-        ts = []
-        with torch.cuda.stream(stream):
-            for _ in range(10):
-                flush.zero_()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                l.launch(stream)
-                b.record(stream)
-                ts.append((a, b))
-        torch.cuda.synchronize()
-        us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ts)
+        us = _flushed_launch_us(lambda l=l: l.launch(stream), flush, stream)
         byts = l.algorithmic_bytes()
         per.append({"layer": l.wl.name, "us": round(us, 2), "mbytes": round(byts / 1e6, 2),
                     "gbs": round(byts / us / 1e3, 1)})
