@@ -1352,9 +1352,12 @@ tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
       return fail(TEC_E_FOLD_OVERFLOW, "value out of range for i32 in the fused epilogue");
     return TEC_OK;
   }
+  // Weights first: the conv kernel reads them BEFORE griddepcontrol.wait
+  // (they are parameters), so the kernel right before it must not be the
+  // one producing them -- the activation pack sits in between.
+  if ((st = tec_weight_pretransform(d, ws.w_src.p, ws.w_pack.p, s))) return st;
   TEC_CUDA(cudaMemcpyAsync(ws.x_src.p, x, x_elems * in_es, cudaMemcpyHostToDevice, s));
   if ((st = tec_activation_pack(d, ws.x_src.p, ws.x_pack.p, s))) return st;
-  if ((st = tec_weight_pretransform(d, ws.w_src.p, ws.w_pack.p, s))) return st;
   st = tec_conv2d_fused(d, epi ? &dev_epi : nullptr, knobs, ws.x_pack.p, ws.w_pack.p,
                         ws.y_nhwc.p, acc_t, static_cast<int32_t*>(ws.err.p), s);
   if (st) return st;

@@ -92,6 +92,9 @@ class DeviceConv:
         self.epi.n_ops = len(ops)
         self.epi.bias = self.bias.data_ptr()
         self.knobs = _abi.Knobs(**(knobs or {}))
+        # the packed operands are ready before any launch, on any stream (the
+        # conv kernels read weights before their PDL wait)
+        torch.cuda.synchronize(self.dev)
         del x_src, w_src
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
