@@ -19,8 +19,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
+#include <vector>
 
 #include "conv_params.h"
 #include "sm100_ptx.cuh"
@@ -350,8 +352,32 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
   t->cols_in = (((p.ow + kTW - 1) / kTW) * kTW - 1) * p.sw + 3;
   if (t->cols_in > 256) return false;
   const int budget = 100 * 1024;  // per buffer (two buffers + slack < 227 KB)
-  int th = p.oh;
-  while (th > 1 && ((th - 1) * p.sw + 3) * t->cols_in * cb * es > budget) --th;
+  int th_max = p.oh;
+  while (th_max > 1 && ((th_max - 1) * p.sw + 3) * t->cols_in * cb * es > budget) --th_max;
+  // Band height: tiles go to CTAs round-robin (tile = cta + k * grid, band
+  // fastest), so bands of unequal height can land all the tall ones on the
+  // same CTAs -- D5 with th = 24 (+ a 4-row band) put every 24-row band on
+  // the even CTAs (148 is even): half the SMs did 6x the work of the other
+  // half. Pick the height whose round-robin makespan is smallest, in rows
+  // (+ 2 per tile for the halo rows / pipeline step); ties keep the taller.
+  int th = th_max;
+  if (th_max < p.oh) {
+    const int sms = 148;
+    long best = -1;
+    std::vector<long> load(sms);
+    for (int h = th_max; h >= 1 && h * 4 >= th_max; --h) {
+      const int bands = (p.oh + h - 1) / h;
+      const long tiles = static_cast<long>(p.n) * bands * t->cblocks;
+      const int grid = tiles < sms ? static_cast<int>(tiles) : sms;
+      std::fill(load.begin(), load.end(), 0L);
+      for (long tile = 0; tile < tiles; ++tile) {
+        const int band = static_cast<int>(tile % bands);
+        load[tile % grid] += std::min(h, p.oh - band * h) + 2;
+      }
+      const long span = *std::max_element(load.begin(), load.begin() + grid);
+      if (best < 0 || span < best) { best = span; th = h; }
+    }
+  }
   t->th = th;
   t->rows_in = (th - 1) * p.sw + 3;
   if (t->rows_in > 256) return false;

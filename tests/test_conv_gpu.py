@@ -256,6 +256,23 @@ def test_depthwise_multi_image_tiles(layer, compute):
     assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
 
 
+@pytest.mark.parametrize("unroll", [8])
+@pytest.mark.parametrize("compute", ["bf16", "f32"])
+@pytest.mark.parametrize("layer", list(MOBILENET_DW))
+def test_depthwise_tma_variants(layer, compute, unroll):
+    # the TMA-tiled kernel on every layer at batch 3 (bands, channel blocks,
+    # multi-image tiles), with and without the bias+relu members
+    hw, c, s = MOBILENET_DW[layer]
+    x, w, b = _inputs((3, c, hw, hw), (c, 1, 3, 3), c, False, seed=91)
+    attrs = {"strides": (s, s), "padding": (1, 1)}
+    for epi in ([("bias_add", b), ("relu",)], []):
+        y = fused_conv("depthwise_conv2d", x, w, attrs, epi, compute=compute,
+                       knobs={"unroll": unroll})
+        xr, wr = (bf16_round(x), bf16_round(w)) if compute == "bf16" else (x, w)
+        want = oracle_conv("depthwise_conv2d", xr, wr, attrs["strides"], attrs["padding"], epi)
+        assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
+
+
 @pytest.mark.parametrize("batch", [3, 4])
 @pytest.mark.parametrize("layer", ["C2", "C6", "C9"])
 def test_halo_weight_multicast_cluster(layer, batch):
