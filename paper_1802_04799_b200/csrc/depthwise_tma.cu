@@ -155,14 +155,23 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
     const int rows = min(t.th, p.oh - oh0);
     const int strips = (p.ow + kTW - 1) / kTW;
     const int nimg = min(t.ni, p.n - n);
-    const int per_img = rows * strips;
-    const int items = nimg * per_img;
+    const int items = nimg * rows * strips;
     // kTW consecutive output columns per item: each loaded (and unpacked)
     // input column serves up to 3 taps of neighbouring outputs.
-    for (int it2 = lane_pix; it2 < items; it2 += pix_step) {
-      const int im = it2 / per_img;
-      const int rem_i = it2 - im * per_img;
-      const int r = rem_i / strips, ow0 = (rem_i - r * strips) * kTW;
+    // (image, row, strip) of item it2, stepped by pix_step with carries:
+    // the divisions run once per tile instead of twice per item.
+    const int ds = pix_step % strips, dq = pix_step / strips;
+    const int dr = dq % rows, dim = dq / rows;
+    int s_i = lane_pix % strips, r_i = (lane_pix / strips) % rows, im_i = lane_pix / strips / rows;
+    auto advance = [&]() {
+      s_i += ds;
+      if (s_i >= strips) { s_i -= strips; ++r_i; }
+      r_i += dr;
+      if (r_i >= rows) { r_i -= rows; ++im_i; }
+      im_i += dim;
+    };
+    for (int it2 = lane_pix; it2 < items; it2 += pix_step, advance()) {
+      const int im = im_i, r = r_i, ow0 = s_i * kTW;
       float2 acc2[kTW][V2];
 #pragma unroll
       for (int i = 0; i < kTW; ++i)
