@@ -242,7 +242,8 @@ def impl_ours(args):
     if knobs_in and os.path.exists(knobs_in):
         with open(knobs_in) as f:
             tuned = json.load(f)
-    knobs_src = knobs_in if tuned else "tuned live (tec_measure over the knob grid)"
+    knobs_src = (os.path.relpath(knobs_in, REPO) if knobs_in.startswith(REPO) else knobs_in) if tuned \
+        else "tuned live (tec_measure over the knob grid)"
     for n in LAYERS:
         if n in tuned:
             continue
