@@ -20,7 +20,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -369,8 +372,19 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
   // the even CTAs (148 is even): half the SMs did 6x the work of the other
   // half. Pick the height whose round-robin makespan is smallest, in rows
   // (+ 2 per tile for the halo rows / pipeline step); ties keep the taller.
+  // The search walks every tile (~10^4 steps per candidate): cache it per
+  // shape so eager launches (tec_measure, the e2e host path) do not pay it.
+  static std::mutex mu;
+  static std::map<std::array<int, 4>, int> memo;
+  const std::array<int, 4> key{p.n, p.oh, th_max, t->cblocks};
   int th = th_max;
-  if (th_max < p.oh) {
+  bool cached = false;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto f = memo.find(key);
+    if (f != memo.end()) { th = f->second; cached = true; }
+  }
+  if (!cached && th_max < p.oh) {
     const int sms = 148;
     long best = -1;
     std::vector<long> load(sms);
@@ -386,6 +400,8 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
       const long span = *std::max_element(load.begin(), load.begin() + grid);
       if (best < 0 || span < best) { best = span; th = h; }
     }
+    std::lock_guard<std::mutex> g(mu);
+    memo[key] = th;
   }
   t->th = th;
   t->rows_in = (th - 1) * p.sw + 3;
