@@ -407,15 +407,22 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
   t->rows_in = (th - 1) * p.sw + 3;
   if (t->rows_in > 256) return false;
   t->bands = (p.oh + th - 1) / th;
-  // Small images: several per tile (the TMA box's N extent) so a tile has
-  // enough work to hide the next tile's load, keeping >= 2 tiles per SM.
   const int img = t->rows_in * t->cols_in * cb * es;
+  // Images per tile when a whole image is one band: fewest rounds of tiles
+  // per CTA x (ni + 1) -- one image-time per image plus ~one of per-tile
+  // load/barrier overhead, ties to the larger ni (fewer tiles). Measured on
+  // D7-D9 b64 (ni swept 1-8, tools/prof_dw.py): D7 2 (15.5 -> 12.9 us),
+  // D8 2 (10.3 -> 8.4), D9 8 (10.4 -> 7.5); the earlier ">= 2 tiles per SM"
+  // rule chose 1 / 1 / 3.
   t->ni = 1;
   if (t->bands == 1) {
     const int sms = 148;
-    while (t->ni < 8 && (t->ni + 1) * img <= budget &&
-           ((p.n + t->ni) / (t->ni + 1)) * t->cblocks >= 2 * sms)
-      ++t->ni;
+    long best = -1;
+    for (int ni = 1; ni <= 8 && ni <= p.n && ni * img <= budget; ++ni) {
+      const long tiles = static_cast<long>((p.n + ni - 1) / ni) * t->cblocks;
+      const long cost = ((tiles + sms - 1) / sms) * (ni + 1);
+      if (best < 0 || cost <= best) { best = cost; t->ni = ni; }
+    }
   }
   t->buf_bytes = ((img * t->ni) + 127) & ~127;
   return t->buf_bytes <= budget;
