@@ -13,8 +13,10 @@
 // Arithmetic is the oracle's per-output sequence (taps (rh, rw) in order,
 // facc = facc + x*w rounded to float; out-of-image taps contribute x = 0
 // exactly like the reference's select): bf16 x bf16 products are exact in
-// f32, so one FMA rounds like the reference's add; f32 operands keep the
-// separate multiply and add.
+// f32, so one FMA rounds like the reference's add -- for bf16 the mixed
+// fma.rn.f32.bf16 (SASS FHFMA.BF16) reads both operands as halves of the
+// packed smem / tap registers, so nothing is unpacked (-10 % on D1-D9 vs
+// unpack + FFMA2); f32 operands keep the separate multiply and add.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -124,7 +126,9 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
   int first = blockIdx.x;
   if (tid == 0 && first < tiles) issue(first, 0);
   constexpr int V2 = VEC / 2;  // float2 lanes: packed f32x2 FMA (FFMA2)
-  float2 w2[9][V2];
+  constexpr bool kBF = std::is_same<InT, __nv_bfloat16>::value;
+  float2 w2[kBF ? 1 : 9][V2];
+  uint32_t wb[kBF ? 9 : 1][4];  // bf16: the taps stay packed (FHFMA.BF16 reads halves)
   float bias[VEC];
   int cur_cblk = -1;
   int it = 0;
@@ -139,10 +143,15 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
       cur_cblk = cblk;
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
-        float wk[VEC];
-        load8<InT>(static_cast<const InT*>(p.wt) + k * p.c + c0, wk);
+        if constexpr (kBF) {
+          const uint4 q = *reinterpret_cast<const uint4*>(static_cast<const InT*>(p.wt) + k * p.c + c0);
+          wb[k][0] = q.x; wb[k][1] = q.y; wb[k][2] = q.z; wb[k][3] = q.w;
+        } else {
+          float wk[VEC];
+          load8<InT>(static_cast<const InT*>(p.wt) + k * p.c + c0, wk);
 #pragma unroll
-        for (int j = 0; j < V2; ++j) w2[k][j] = make_float2(wk[2 * j], wk[2 * j + 1]);
+          for (int j = 0; j < V2; ++j) w2[k][j] = make_float2(wk[2 * j], wk[2 * j + 1]);
+        }
       }
       if constexpr (PROG != kDwtNone) {
 #pragma unroll
@@ -186,8 +195,15 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
             static_cast<uint32_t>(((r * SW + rh) * t.cols_in + ow0 * SW) * t.cb * ES);
 #pragma unroll
         for (int jc = 0; jc < (kTW - 1) * SW + 3; ++jc) {
-          float x[VEC];
-          lds_vec(rowa + static_cast<uint32_t>(jc * t.cb * ES), x);
+          float x[kBF ? 1 : VEC];
+          uint32_t xb[4];
+          if constexpr (kBF) {
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(xb[0]), "=r"(xb[1]), "=r"(xb[2]), "=r"(xb[3])
+                         : "r"(rowa + static_cast<uint32_t>(jc * t.cb * ES)));
+          } else {
+            lds_vec(rowa + static_cast<uint32_t>(jc * t.cb * ES), x);
+          }
 #pragma unroll
           for (int i = 0; i < kTW; ++i) {
 #pragma unroll
@@ -195,9 +211,16 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
               if (jc == i * SW + rw) {  // taps arrive in rw order per output
 #pragma unroll
                 for (int j = 0; j < V2; ++j) {
-                  if constexpr (std::is_same<InT, __nv_bfloat16>::value) {
-                    acc2[i][j] = __ffma2_rn(make_float2(x[2 * j], x[2 * j + 1]),
-                                            w2[rh * 3 + rw][j], acc2[i][j]);
+                  if constexpr (kBF) {
+                    // f32 += bf16 x bf16, the product exact, one rounding:
+                    // the reference's facc + x*w
+                    asm("{.reg .b16 xl, xh, wl, wh;\n\t"
+                        "mov.b32 {xl, xh}, %2;\n\t"
+                        "mov.b32 {wl, wh}, %3;\n\t"
+                        "fma.rn.f32.bf16 %0, xl, wl, %0;\n\t"
+                        "fma.rn.f32.bf16 %1, xh, wh, %1;}"
+                        : "+f"(acc2[i][j].x), "+f"(acc2[i][j].y)
+                        : "r"(xb[j]), "r"(wb[rh * 3 + rw][j]));
                   } else {
                     acc2[i][j].x = __fadd_rn(acc2[i][j].x, __fmul_rn(x[2 * j], w2[rh * 3 + rw][j].x));
                     acc2[i][j].y = __fadd_rn(acc2[i][j].y, __fmul_rn(x[2 * j + 1], w2[rh * 3 + rw][j].y));
