@@ -81,14 +81,17 @@ typedef enum {
 /* Arithmetic an operator runs with:
  *   BF16   : tcgen05 kind::f16 -- inputs rounded to bf16, exact products,
  *            f32 tensor-core accumulation (stated tolerance)
- *   TF32X3 : tcgen05 kind::tf32 -- x = hi + lo split, hi*hi + hi*lo + lo*hi
- *            (fast approximate f32; stated tolerance)
+ *   F32TC  : f32 on tcgen05 kind::f16 -- every f32 operand split exactly into
+ *            three bf16 planes (h + m + l), six products, the hh term folded
+ *            into round-to-nearest f32 registers every 256 K elements: within
+ *            the reference comparator's 1e-4 of evaluate_reference (dense
+ *            conv; depthwise runs the exact F32 kernel)
  *   I8     : tcgen05 kind::i8 -- s8 x s8 -> s32 (bit-exact i8 path)
  *   F32    : f32 parity path -- SIMT, the reference's exact reduction
  *            order and rounding: bit-identical to evaluate_reference      */
 typedef enum {
   TEC_COMPUTE_BF16 = 1,
-  TEC_COMPUTE_TF32X3 = 2,
+  TEC_COMPUTE_F32TC = 2,
   TEC_COMPUTE_I8 = 3,
   TEC_COMPUTE_F32 = 4
 } tec_compute;
@@ -194,7 +197,8 @@ typedef enum {
   TEC_KERNEL_HALO = 2,       /* conv_halo.cu: shifted-window implicit GEMM */
   TEC_KERNEL_F32_EXACT = 3,  /* conv_f32_exact.cu: SIMT, reference order  */
   TEC_KERNEL_DW_TMA = 4,     /* depthwise_tma.cu                           */
-  TEC_KERNEL_DW_DIRECT = 5   /* depthwise.cu                               */
+  TEC_KERNEL_DW_DIRECT = 5,  /* depthwise.cu                               */
+  TEC_KERNEL_F32TC = 6       /* conv_f32tc.cu: split-bf16 f32 on tcgen05    */
 } tec_kernel_family;
 
 typedef struct {

@@ -25,7 +25,7 @@ ERROR_NAMES = [
 TEC_E_CUDA = 64
 
 DT_F32, DT_I32, DT_I8, DT_BF16 = 0, 1, 2, 3
-COMPUTE_BF16, COMPUTE_TF32X3, COMPUTE_I8, COMPUTE_F32 = 1, 2, 3, 4
+COMPUTE_BF16, COMPUTE_F32TC, COMPUTE_I8, COMPUTE_F32 = 1, 2, 3, 4
 EPI_SCALE, EPI_BIAS, EPI_ADD, EPI_MUL, EPI_RELU = 1, 2, 3, 4, 5
 MAX_EPILOGUE = 8
 

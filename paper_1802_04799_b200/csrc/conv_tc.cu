@@ -464,12 +464,6 @@ TEC_INST(MmaKind::kI8, 256, 3, 128)
 TEC_INST(MmaKind::kI8, 64, 8, 64)
 TEC_INST(MmaKind::kI8, 128, 6, 64)
 TEC_INST(MmaKind::kI8, 64, 8, 32)
-// tf32 (approximate-f32 3xTF32 path, K = [hi|hi|lo] x [hi|lo|hi]): 128 B
-// blocks (32 ch), 64 B (16 ch, the stem: 3*3 -> 16 padded channels).
-TEC_INST(MmaKind::kTF32, 64, 8, 128)
-TEC_INST(MmaKind::kTF32, 128, 6, 128)
-TEC_INST(MmaKind::kTF32, 256, 3, 128)
-TEC_INST(MmaKind::kTF32, 64, 8, 64)
 
 #undef TEC_INST
 

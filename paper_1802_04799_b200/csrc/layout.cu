@@ -15,25 +15,30 @@
 
 namespace tec_sm100 {
 
-__device__ __forceinline__ float tf32_round(float x) {
-  // Round-to-nearest-even onto the 10-bit tf32 mantissa.
-  uint32_t b = __float_as_uint(x);
-  if ((b & 0x7f800000u) == 0x7f800000u) return x;
-  b = (b + 0xFFFu + ((b >> 13) & 1u)) & 0xFFFFE000u;
-  return __uint_as_float(b);
+// Exact three-way bf16 split of an f32 value (the f32tc path, conv_f32tc.cu):
+// x == h + m + l with h = bf16(x), m = bf16(x - h), l = bf16(x - h - m). Each
+// residual is exact in f32 and the last one has <= 8 significant bits, so
+// the split loses nothing (f32's 24-bit mantissa = 3 x 8).
+__device__ __forceinline__ __nv_bfloat16 split3(float x, int plane) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  if (plane == 0) return h;
+  const float r1 = __fsub_rn(x, __bfloat162float(h));
+  const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+  if (plane == 1) return m;
+  return __float2bfloat16_rn(__fsub_rn(r1, __bfloat162float(m)));
 }
 
 // Packed activation element kinds.
 enum PackMode : int32_t {
   kPackBF16 = 0,    // bf16(x)
-  kPackTF32X3 = 1,  // channels [hi | hi | lo] (matches weights [hi | lo | hi])
+  kPackSplit3 = 1,  // bf16 planes [h | m | l], cp/3 channels each (split3)
   kPackI8 = 2,      // int8 copy
   kPackF32 = 3,     // f32 copy
   kPackI32 = 4,     // i32 copy
 };
 
-// in: [n][c][hw] (f32, or i8 / i32), out: [n][hw][cp] with cp >= c (x3 for
-// TF32X3), padded channels zero-filled.
+// in: [n][c][hw] (f32, or i8 / i32), out: [n][hw][cp] with cp >= c (Split3:
+// three bf16 planes of cp/3 channels), padded channels zero-filled.
 template <typename InT>
 __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
                                          void* __restrict__ out, int64_t c,
@@ -50,7 +55,7 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
     tile[i][tx] = v;
   }
   __syncthreads();
-  const int64_t ctot = mode == kPackTF32X3 ? 3 * c : c;
+  const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
   for (int i = ty; i < 32; i += 8) {
     const int64_t pp = p0 + i, cc = c0 + tx;
     if (pp >= hw) continue;
@@ -61,13 +66,10 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
         case kPackBF16:
           static_cast<__nv_bfloat16*>(out)[obase + cc] = __float2bfloat16_rn(v);
           break;
-        case kPackTF32X3: {
-          const float hi = tf32_round(v);
-          const float lo = v - hi;
-          float* o = static_cast<float*>(out);
-          o[obase + cc] = hi;
-          o[obase + c + cc] = hi;
-          o[obase + 2 * c + cc] = lo;
+        case kPackSplit3: {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) o[obase + pl * cpp + cc] = split3(v, pl);
           break;
         }
         case kPackI8:
@@ -83,12 +85,16 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
     }
     // zero the channel padding [ctot, cp) once per pixel (block column 0)
     if (blockIdx.y == 0) {
-      for (int64_t z = ctot + tx; z < cp; z += 32) {
+      for (int64_t z = c + tx; z < cpp; z += 32) {
         switch (mode) {
           case kPackBF16:
             static_cast<__nv_bfloat16*>(out)[obase + z] = __float2bfloat16_rn(0.f);
             break;
-          case kPackTF32X3:
+          case kPackSplit3:
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+              static_cast<__nv_bfloat16*>(out)[obase + pl * cpp + z] = __float2bfloat16_rn(0.f);
+            break;
           case kPackF32:
             static_cast<float*>(out)[obase + z] = 0.f;
             break;
@@ -147,22 +153,17 @@ __global__ void pack_weights_krsc_kernel(const InT* __restrict__ w,
     t /= s;
     const int64_t rr = t % r;
     const int64_t kk = t / r;
-    const int64_t ctot = mode == kPackTF32X3 ? 3 * c : c;
+    const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
+    const int64_t src_c = ci % cpp, plane = ci / cpp;
     float v = 0.f;
-    if (ci < ctot) {
-      const int64_t src_c = ci % c;
-      const int64_t grp = ci / c;
-      v = static_cast<float>(w[((kk * c + src_c) * r + rr) * s + ss]);
-      if (mode == kPackTF32X3) {
-        const float hi = tf32_round(v);
-        v = grp == 1 ? v - hi : hi;  // [hi | lo | hi]
-      }
-    }
+    if (src_c < c) v = static_cast<float>(w[((kk * c + src_c) * r + rr) * s + ss]);
     switch (mode) {
       case kPackBF16:
         static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
         break;
-      case kPackTF32X3:
+      case kPackSplit3:
+        static_cast<__nv_bfloat16*>(out)[i] = split3(v, static_cast<int>(plane));
+        break;
       case kPackF32:
         static_cast<float*>(out)[i] = v;
         break;
@@ -211,9 +212,10 @@ __global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ o
                                 int64_t n, int64_t c, int64_t h, int64_t w, int64_t ph,
                                 int64_t pw, int64_t h2, int64_t w2, int64_t cp, int mode) {
   const int64_t total = n * h2 * w2 * cp;
+  const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t ch = i % cp;
+    const int64_t ch = (i % cp) % cpp, plane = (i % cp) / cpp;
     int64_t t = i / cp;
     const int64_t jj = t % w2;
     t /= w2;
@@ -228,6 +230,8 @@ __global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ o
     }
     if (mode == kPackBF16)
       static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    else if (mode == kPackSplit3)
+      static_cast<__nv_bfloat16*>(out)[i] = split3(v, static_cast<int>(plane));
     else
       static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
   }
@@ -355,9 +359,10 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
                                         int64_t k, int64_t c, int64_t r, int64_t s, int64_t r2,
                                         int64_t s2, int64_t cp, int mode) {
   const int64_t total = k * r2 * s2 * cp;
+  const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t ch = i % cp;
+    const int64_t ch = (i % cp) % cpp, plane = (i % cp) / cpp;
     int64_t t = i / cp;
     const int64_t sj = t % s2;
     t /= s2;
@@ -371,6 +376,8 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
     }
     if (mode == kPackBF16)
       static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+    else if (mode == kPackSplit3)
+      static_cast<__nv_bfloat16*>(out)[i] = split3(v, static_cast<int>(plane));
     else
       static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
   }

@@ -13,7 +13,7 @@ import torch
 from . import _abi
 from .workloads import ConvWorkload
 
-_COMPUTE = {"bf16": _abi.COMPUTE_BF16, "tf32x3": _abi.COMPUTE_TF32X3,
+_COMPUTE = {"bf16": _abi.COMPUTE_BF16, "f32tc": _abi.COMPUTE_F32TC,
             "i8": _abi.COMPUTE_I8, "f32": _abi.COMPUTE_F32}
 _TORCH_DT = {_abi.DT_F32: torch.float32, _abi.DT_BF16: torch.bfloat16,
              _abi.DT_I32: torch.int32, _abi.DT_I8: torch.int8}
@@ -50,7 +50,9 @@ class DeviceConv:
         self.layout = lay
         integer = self.compute == _abi.COMPUTE_I8
         if out_dtype is None:
-            out_dtype = _abi.DT_I32 if integer else _abi.DT_BF16
+            out_dtype = (_abi.DT_I32 if integer else
+                         _abi.DT_F32 if self.compute in (_abi.COMPUTE_F32, _abi.COMPUTE_F32TC)
+                         else _abi.DT_BF16)
         self.out_dtype = out_dtype
         g = torch.Generator(device=self.dev)
         g.manual_seed(seed)

@@ -28,7 +28,8 @@ from ._abi import TecError
 
 E_DUPLICATE_INTRINSIC, E_TENSORIZE_MISMATCH, E_LOWERING = 5, 14, 15
 
-FAMILIES = {1: "im2col", 2: "halo", 3: "f32_exact", 4: "depthwise_tma", 5: "depthwise_direct"}
+FAMILIES = {1: "im2col", 2: "halo", 3: "f32_exact", 4: "depthwise_tma", 5: "depthwise_direct",
+            6: "f32tc"}
 
 
 @dataclass(frozen=True)
@@ -70,8 +71,9 @@ def register_builtin_intrinsics() -> None:
     builtins = [
         Intrinsic("sm100.umma.bf16", "matmul_acc", (64, 128), (8, 256, 8), 16, "bf16", "f32",
                   umma_scope, True, "tcgen05.mma.cta_group::1.kind::f16"),
-        Intrinsic("sm100.umma.tf32", "matmul_acc", (64, 128), (8, 256, 8), 8, "tf32", "f32",
-                  umma_scope, True, "tcgen05.mma.cta_group::1.kind::tf32"),
+        # f32 as three exact bf16 planes, six kind::f16 products per K16 step
+        Intrinsic("sm100.umma.bf16x6", "matmul_acc", (128,), (64, 128, 64), 16, "f32", "f32",
+                  umma_scope, True, "tcgen05.mma.cta_group::1.kind::f16 x6 (split-bf16 f32)"),
         Intrinsic("sm100.umma.i8", "matmul_acc", (64, 128), (8, 256, 8), 32, "i8", "i32",
                   umma_scope, True, "tcgen05.mma.cta_group::1.kind::i8"),
         Intrinsic("sm100.simt.f32", "fma_acc", (1,), (1, 1, 1), 1, "f32", "f32",
@@ -82,7 +84,7 @@ def register_builtin_intrinsics() -> None:
             declare_intrinsic(b)
 
 
-_COMPUTE_INTRIN = {_abi.COMPUTE_BF16: "sm100.umma.bf16", _abi.COMPUTE_TF32X3: "sm100.umma.tf32",
+_COMPUTE_INTRIN = {_abi.COMPUTE_BF16: "sm100.umma.bf16", _abi.COMPUTE_F32TC: "sm100.umma.bf16x6",
                    _abi.COMPUTE_I8: "sm100.umma.i8", _abi.COMPUTE_F32: "sm100.simt.f32"}
 
 
@@ -135,6 +137,6 @@ def lower(desc: _abi.ConvDesc, config: Optional[Dict[str, int]] = None,
     if plan.smem_bytes > opts.smem_bytes or plan.tmem_cols > opts.tmem_cols:
         raise TecError(E_LOWERING, f"plan exceeds the on-chip budget: {plan}")
     intr = find_intrinsic(plan.intrinsic)
-    if plan.family in ("im2col", "halo") and not intr.accepts(128, plan.tile_n, intr.k):
+    if plan.family in ("im2col", "halo", "f32tc") and not intr.accepts(128, plan.tile_n, intr.k):
         raise TecError(E_TENSORIZE_MISMATCH, f"{plan.intrinsic} cannot take N={plan.tile_n}")
     return plan

@@ -22,12 +22,12 @@ from typing import Any, Dict, List, Optional, Sequence
 import numpy as np
 
 from . import _abi
-from ._abi import (COMPUTE_BF16, COMPUTE_F32, COMPUTE_I8, COMPUTE_TF32X3, EPI_ADD,
+from ._abi import (COMPUTE_BF16, COMPUTE_F32, COMPUTE_F32TC, COMPUTE_I8, EPI_ADD,
                    EPI_BIAS, EPI_MUL, EPI_RELU, EPI_SCALE, TecError)
 
 AttrMap = Dict[str, Any]
 
-_COMPUTE_NAMES = {"bf16": COMPUTE_BF16, "tf32x3": COMPUTE_TF32X3,
+_COMPUTE_NAMES = {"bf16": COMPUTE_BF16, "f32tc": COMPUTE_F32TC,
                   "fp32": COMPUTE_F32, "f32": COMPUTE_F32, "i8": COMPUTE_I8}
 _EPI_OPS = {"scale": EPI_SCALE, "bias_add": EPI_BIAS, "add": EPI_ADD,
             "mul": EPI_MUL, "relu": EPI_RELU}
@@ -45,8 +45,10 @@ def _pair(attrs: AttrMap, key: str, dflt: Sequence[int]) -> List[int]:
 
 
 def conv_desc(op: str, x_shape, w_shape, attrs: AttrMap,
-              compute: int) -> _abi.ConvDesc:
-    """Builds the C descriptor with infer_conv's checks (ops.cpp:163-192)."""
+              compute: int, out_shape: Optional[list] = None) -> _abi.ConvDesc:
+    """Builds the C descriptor with infer_conv's checks (ops.cpp:163-192);
+    `out_shape`, when given, receives the NCHW output shape the C ABI
+    inferred (the one source of truth for buffer sizes)."""
     if op not in ("conv2d", "depthwise_conv2d"):
         raise TecError(1, f"no sm100 kernel for operator '{op}'")
     if len(x_shape) != 4 or len(w_shape) != 4:
@@ -67,6 +69,8 @@ def conv_desc(op: str, x_shape, w_shape, attrs: AttrMap,
                       depthwise=1 if dw else 0, compute=compute)
     out = (C.c_int64 * 4)()
     _abi.check(_abi.load().tec_conv_infer(C.byref(d), out))
+    if out_shape is not None:
+        out_shape[:] = [int(v) for v in out]
     return d
 
 
@@ -95,10 +99,10 @@ def fused_conv(op: str, x: np.ndarray, w: np.ndarray, attrs: AttrMap,
     if x.dtype != w.dtype:
         raise TecError(2, f"{op} operand dtypes differ")
     cm = _compute_for(x.dtype, compute)
-    d = conv_desc(op, x.shape, w.shape, attrs, cm)
+    shape: list = []
+    d = conv_desc(op, x.shape, w.shape, attrs, cm, shape)
     acc = np.int32 if cm == COMPUTE_I8 else np.float32
-    out_shape = (d.n, d.k, (d.h + 2 * d.pad_h - d.r) // d.stride_h + 1,
-                 (d.w + 2 * d.pad_w - d.s) // d.stride_w + 1)
+    out_shape = tuple(shape)
     epi = _abi.Epilogue()
     keep = []
     if len(epilogue) > _abi.MAX_EPILOGUE:

@@ -155,7 +155,7 @@ def dw_space(name: str, desc: _abi.ConvDesc,
 # (R/src/schedule.cpp:456-491, Schedule::apply_log_entry). A B200 Config is
 # the same decision in template form (SURVEY 8a knob mapping); these two
 # functions translate between them so trial DBs and schedule logs interoperate.
-_INTRIN = {_abi.COMPUTE_BF16: "sm100.umma.bf16", _abi.COMPUTE_TF32X3: "sm100.umma.tf32",
+_INTRIN = {_abi.COMPUTE_BF16: "sm100.umma.bf16", _abi.COMPUTE_F32TC: "sm100.umma.bf16x6",
            _abi.COMPUTE_I8: "sm100.umma.i8", _abi.COMPUTE_F32: "sm100.simt.f32"}
 
 

@@ -11,7 +11,9 @@ Bars (comparator = DenseTensor::same_values, R/src/tensor.cpp:56-72:
     and w; products are exact, only the f32 accumulation differs. Stated
     tolerance TOL_BF16 = 2e-3: the tensor-core accumulator truncates, error
     grows with K (measured 5.7e-4 abs at K = 4608, |y| <= 85).
-  * tf32x3 (fast approximate f32): stated tolerance TOL_TF32X3 = 1e-2.
+  * f32tc (f32 on tcgen05, conv_f32tc.cu: exact 3-way bf16 split, six
+    products, hh folded in RN registers every 256 K): the north_star bar,
+    TOL_F32TC = 1e-4 against the f32 oracle on the ORIGINAL f32 inputs.
 """
 import numpy as np
 import pytest
@@ -26,7 +28,9 @@ from paper_1802_04799_b200.workloads import MOBILENET_DW, RESNET18_CONVS
 pytestmark = pytest.mark.gpu
 
 TOL_BF16 = 2e-3
-TOL_TF32X3 = 1e-2
+TOL_F32TC = 1e-4
+# fused programs the f32tc kernel runs; others are a LoweringError there
+F32TC_PROGRAMS = ([], ["bias_add"], ["bias_add", "relu"], ["bias_add", "add", "relu"])
 
 
 def bits(a):
@@ -55,13 +59,18 @@ def test_golden_bit_identical_to_reference(name):
 
 @pytest.mark.parametrize("name", [n for n in golden_cases.names()
                                   if not n.startswith("i8")])
-@pytest.mark.parametrize("compute", ["bf16", "tf32x3"])
+@pytest.mark.parametrize("compute", ["bf16", "f32tc"])
 def test_golden_tensor_core_float_paths(name, compute):
     c = golden_cases.load(name)
     if compute == "bf16":
         xr, wr, tol = bf16_round(c.x), bf16_round(c.w), TOL_BF16
     else:
-        xr, wr, tol = c.x, c.w, TOL_TF32X3
+        xr, wr, tol = c.x, c.w, TOL_F32TC
+        if c.op == "conv2d" and [m[0] for m in c.epilogue] not in F32TC_PROGRAMS:
+            with pytest.raises(TecError) as ei:
+                _gpu(c, compute)
+            assert ei.value.code == "LoweringError"
+            return
     want = oracle_conv(c.op, xr, wr, c.strides, c.padding, c.epilogue)
     y = _gpu(c, compute)
     assert same_values(y, want, tol), f"{compute} max rel err {max_rel_err(y, want)}"
@@ -88,11 +97,11 @@ def _check(op, x, w, attrs, epi, compute):
     if compute in ("i8", "f32"):
         assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
     else:
-        tol = TOL_BF16 if compute == "bf16" else TOL_TF32X3
+        tol = TOL_BF16 if compute == "bf16" else TOL_F32TC
         assert same_values(y, want, tol), f"max rel err {max_rel_err(y, want)}"
 
 
-@pytest.mark.parametrize("compute", ["bf16", "f32", "i8", "tf32x3"])
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8", "f32tc"])
 @pytest.mark.parametrize("layer", list(RESNET18_CONVS))
 def test_resnet_layer_batch1(layer, compute):
     hw, c, k, r, s = RESNET18_CONVS[layer]
@@ -119,7 +128,7 @@ def test_mobilenet_depthwise_batch1(layer, compute):
     assert np.array_equal(bits(y), bits(want)), f"max rel err {max_rel_err(y, want)}"
 
 
-@pytest.mark.parametrize("compute", ["bf16", "f32", "i8"])
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8", "f32tc"])
 def test_batch_tail_and_multi_image(compute):
     # M not a multiple of the 128-row tile; tiles spanning several images.
     x, w, b = _inputs((3, 64, 9, 11), (64, 64, 3, 3), 64, compute == "i8", 5)
@@ -127,7 +136,7 @@ def test_batch_tail_and_multi_image(compute):
            [("bias_add", b), ("relu",)], compute)
 
 
-@pytest.mark.parametrize("compute", ["bf16", "f32", "i8"])
+@pytest.mark.parametrize("compute", ["bf16", "f32", "i8", "f32tc"])
 def test_resnet_block_residual_epilogue(compute):
     # conv -> bias_add -> add(shortcut) -> relu: the fused node of every
     # ResNet basic block's second conv.
@@ -335,3 +344,56 @@ def test_paired_taps_agree_with_oracle(case):
     want = oracle_conv("conv2d", bf16_round(x), bf16_round(w), attrs["strides"],
                        attrs["padding"], epi)
     assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
+
+
+def f32tc_within_bar(y, ref, exact, tol=TOL_F32TC):
+    """The f32tc bar, element-wise: |y - ref| <= tol * max(|y|, |ref|, 1)
+    (the reference comparator, R/src/tensor.cpp:56-72) PLUS the reference's
+    own distance from the exact result. At K = 4608 the reference's
+    sequential f32 sum is itself up to ~1.5e-4 from the exact value on a few
+    near-zero outputs (std 2.8e-5, tools/microbench/acc_precision.cu), so no
+    result -- not even the exactly rounded one -- is within 1e-4 of it there;
+    everywhere else the plain comparator must hold. Returns (ok, n_explained)."""
+    d = np.abs(y.astype(np.float64) - ref)
+    t = tol * np.maximum(np.maximum(np.abs(y), np.abs(ref)), 1.0)
+    own = np.abs(ref.astype(np.float64) - exact)
+    ok = bool(np.all(d <= t + own))
+    return ok, int(np.count_nonzero(d > t))
+
+
+def _exact_conv(x, w, s, p):
+    import torch
+    return torch.nn.functional.conv2d(torch.from_numpy(x).double(), torch.from_numpy(w).double(),
+                                      stride=s, padding=p).numpy()
+
+
+@pytest.mark.parametrize("layer", ["C2", "C9", "C12"])
+def test_f32tc_error_well_below_reference_rounding(layer):
+    """f32tc vs the exact (f64) conv: its error must be a small fraction of
+    the reference's OWN f32 rounding error, so the 1e-4 comparison against
+    the oracle measures the oracle's rounding, not ours (conv_f32tc.cu)."""
+    hw, c, k, r, s = RESNET18_CONVS[layer]
+    x, w, b = _inputs((2, c, hw, hw), (k, c, r, r), k, False, seed=5)
+    attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+    y = fused_conv("conv2d", x, w, attrs, [], compute="f32tc")
+    ref = oracle_conv("conv2d", x, w, (s, s), (r // 2, r // 2), [])
+    exact = _exact_conv(x, w, s, r // 2)
+    e_gpu = np.abs(y - exact).max()
+    e_ref = np.abs(ref - exact).max()
+    assert e_gpu < 0.5 * e_ref, (e_gpu, e_ref)
+    # the 1e-4 comparator against the EXACT result holds everywhere
+    assert same_values(y, exact.astype(np.float32), TOL_F32TC)
+    ok, n = f32tc_within_bar(y, ref, exact)
+    assert ok, n
+
+
+@pytest.mark.parametrize("tile_n", [64, 128])
+def test_f32tc_tiles_and_unsupported_program(tile_n):
+    x, w, b = _inputs((3, 128, 9, 11), (128, 128, 3, 3), 128, False, 6)
+    attrs = {"strides": (1, 1), "padding": (1, 1)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc", knobs={"tile_n": tile_n})
+    assert same_values(y, oracle_conv("conv2d", x, w, (1, 1), (1, 1), epi), TOL_F32TC)
+    with pytest.raises(TecError) as ei:
+        fused_conv("conv2d", x, w, attrs, [("scale", 2.0)], compute="f32tc")
+    assert ei.value.code == "LoweringError"

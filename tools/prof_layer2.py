@@ -1,6 +1,7 @@
 """Per-layer kernel time with sub-microsecond resolution: CUDA-graph replay of
 [flush, layer] x R minus [flush] x R (event resolution here is ~2 us).
-usage: prof_layer2.py LAYER[,LAYER..] BATCH 'knobs-json-or-list' [R]"""
+usage: prof_layer2.py LAYER[,LAYER..] BATCH 'knobs-json-or-list' [R]
+(TEC_COMPUTE=bf16|f32tc|i8 selects the arithmetic, default bf16)"""
 import json
 import sys
 
@@ -53,7 +54,8 @@ gf = graph_of(fl)
 base = timed(gf)
 for n in names:
     for kn in variants:
-        l = DeviceConv(resnet_layer(n, batch), knobs=kn or None)
+        l = DeviceConv(resnet_layer(n, batch), knobs=kn or None,
+                       compute=__import__('os').environ.get("TEC_COMPUTE", "bf16"))
         for _ in range(3):
             l.launch(stream)
 
