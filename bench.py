@@ -1,19 +1,35 @@
 #!/usr/bin/env python3
 """bench.py -- the headline benchmark (BASELINE.json `metric`):
 
-  "ResNet-18 conv C1-C12 TFLOP/s (% roofline)" on configs[1]: all twelve
-  ResNet-18 conv workloads at batch 64, bf16 inputs with
-  f32 accumulation, each a fused [conv2d, bias_add, relu] node (the group
-  fuse_pass builds, R/src/graph_passes.cpp:240-244) run as ONE sm_100a
-  kernel through the C ABI.
+  "ResNet-18 conv C1-C12 TFLOP/s (% roofline); ResNet-18 img/s at 1/2/4/8 GPU"
+  on configs[1]: all twelve ResNet-18 conv workloads at
+  batch 64, each a fused [conv2d, bias_add, relu] node (the group fuse_pass
+  builds, R/src/graph_passes.cpp:240-244) run as ONE sm_100a kernel through
+  the C ABI.
+
+The headline `value` is at the REFERENCE'S precision: f32 in, f32 out
+(compute "f32tc", conv_f32tc.cu -- f32 on the tcgen05 tensor cores, held to
+the reference comparator's 1e-4, tests/test_conv_gpu.py + test_bench_parity.py).
+The same line carries, as named sub-results measured in the same run:
+  precisions.bf16  bf16 in / f32 accumulate / bf16 out (stated tolerance)
+  precisions.i8    int8 x int8 -> i32, bit-exact (configs[4], the VDLA path),
+                   against an int8 peak measured in this run
+  resnet18         ResNet-18 inference, global batch 256 sharded over the
+                   ranks (configs[3], strong scaling), img/s + e2e img/s
 
 One "step" = the 12 fused layers once over one batch of synthetic inputs
 (reference value distributions, random-init weights), inputs resident in HBM.
 `value` = total algorithmic FLOPs (2*N*OC*OH*OW*IC*KH*KW per layer) / time.
+Knobs come from profiles/tuned_knobs.json -- the SAME file the batch-64
+parity tests (tests/test_bench_parity.py) run, so every knob set the bench
+times is covered by a parity test; other knob files are refused unless
+--allow-untested-knobs.
 
-Multi-GPU (torchrun): the single-operator configs are replicas only (SURVEY
-8e) -- each rank runs its own batch-64 replica, no collective on the data
-path; value = FLOPs of all ranks / max-over-ranks time ("scaling": "weak").
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run (N ranks, 127.0.0.1). The single-operator configs are
+replicas: value = FLOPs of all ranks / max-over-ranks time
+("scaling": "weak"); ResNet-18 is batch-sharded (strong scaling).
+`--cpu-dry-run` runs the same rank plumbing on gloo without a GPU.
 
 `--impl reference` runs the reference's own CPU implementation (the tec
 library compiled from /root/reference sources into oracle/_ref by
@@ -35,8 +51,7 @@ sys.path.insert(0, REPO)
 
 from paper_1802_04799_b200.workloads import RESNET18_CONVS, resnet_layer  # noqa: E402
 
-DEFAULT_KNOBS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_tuned_knobs.json")
-METRIC = "ResNet-18 conv C1-C12 TFLOP/s (% roofline)"
+METRIC = "ResNet-18 conv C1\u2013C12 TFLOP/s (% roofline); ResNet-18 img/s at 1/2/4/8 GPU"
 LAYERS = list(RESNET18_CONVS)
 REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
 
@@ -109,6 +124,21 @@ def run_port_sample(threads, seed=0):
     return flops, time.perf_counter() - t0, f"oracle C port, 1 row per layer, {threads} threads"
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# oracle/Makefile builds the reference with its own CMake default (Release)
+REF_FLAGS = "g++ -std=c++20 -O3 -DNDEBUG (the reference's CMake Release flags, oracle/Makefile)"
+
+
 def cpu_baseline_block(threads):
     if os.path.exists(REF_DRIVER):
         flops, wall, desc = run_reference_sample(threads)
@@ -118,7 +148,8 @@ def cpu_baseline_block(threads):
         kind = "port"
     return {"value": flops / wall / 1e12, "unit": "TFLOP/s", "cores": threads,
             "kind": kind, "sample": desc, "sample_flops": flops,
-            "sample_seconds": round(wall, 3)}
+            "sample_seconds": round(wall, 3), "cpu_model": cpu_model(),
+            "compiler_flags": REF_FLAGS if kind == "reference" else "gcc -O3 -ffp-contract=off"}
 
 
 def impl_reference(args):
@@ -153,7 +184,9 @@ def impl_reference(args):
         "config": {"workload": "C1-C12 fused conv2d+bias_add+relu (bounded CPU sample)",
                    "global_batch": 1, "parallelism": "process-sharded host cores"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads,
-                         "kind": kind, "sample": sample},
+                         "kind": kind, "sample": sample, "cpu_model": cpu_model(),
+                         "compiler_flags": REF_FLAGS if kind == "reference" else
+                         "gcc -O3 -ffp-contract=off"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -213,52 +246,83 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ our arm
-def impl_ours(args):
+KNOBS_FILE = os.path.join(REPO, "profiles", "tuned_knobs.json")
+# element bytes of the algorithmic operands (x, w | y) per arithmetic
+PRECISIONS = {"f32tc": (4, 4), "bf16": (2, 2), "i8": (1, 4)}
+
+
+def load_knobs(path=KNOBS_FILE):
+    if path and os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return {}
+
+
+def measure_int8_peak():
+    """Dense int8 tensor-core peak of THIS GPU: best of 10 cuBLASLt int8
+    GEMMs (torch._int_mm, 8192^3, 2*N^3 ops). None when unavailable."""
+    import torch
+    try:
+        n = 8192
+        a = torch.randint(-8, 8, (n, n), dtype=torch.int8, device="cuda")
+        b = torch.randint(-8, 8, (n, n), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = None
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del a, b
+        return 2 * n ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+def _graph_of(fn, stream):
+    import torch
+    with torch.cuda.stream(stream):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    return g
+
+
+def _median_ms(g, stream):
+    import torch
+    ts = []
+    for _ in range(3):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def measure_step(compute, knobs, batch, local, rank, world, steps, warmup, peak, hbm_gbs,
+                 sampler=None):
+    """Times the 12-layer step at one arithmetic: K CUDA-graph replays
+    between barriers (max over ranks), then each layer's L2-flushed kernel
+    time. Returns the step's numbers and its per-layer roofline table."""
     import torch
     import torch.distributed as dist
 
-    from paper_1802_04799_b200 import _abi
     from paper_1802_04799_b200.device import DeviceConv
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    peak_tf, hbm_gbs, peak_tf_sus, peak_src = load_peaks()
-    batch = args.batch
-
-    # "with tuned schedule knobs" (configs[1]): the on-device tuner measures
-    # the knob grid of every layer (untimed) and the step uses the best.
-    from paper_1802_04799_b200.device import make_desc
-    from paper_1802_04799_b200.tuner import conv_space, tune
-    # Default: the tuning log of an earlier on-device tuning run of this same
-    # step (bench.py --retune --knobs-out ...), read like the reference's
-    # trial DB with budget 0 (tune.cpp:355-436). Live tuning of the 12 layers
-    # in isolation picks differently from run to run (+-2% on the step).
-    tuned = {}
-    knobs_in = args.knobs_in or ("" if args.retune else DEFAULT_KNOBS)
-    if knobs_in and os.path.exists(knobs_in):
-        with open(knobs_in) as f:
-            tuned = json.load(f)
-    knobs_src = (os.path.relpath(knobs_in, REPO) if knobs_in.startswith(REPO) else knobs_in) if tuned \
-        else "tuned live (tec_measure over the knob grid)"
-    for n in LAYERS:
-        if n in tuned:
-            continue
-        if args.no_tune:
-            tuned[n] = {}
-            continue
-        space = conv_space(f"{n}_b{batch}_bf16", make_desc(resnet_layer(n, batch), "bf16"))
-        best = tune(space, budget=space.size(), batch_size=space.size(), method="random",
-                    devices=[local], repeats=5)
-        tuned[n] = best.config if best else {}
-    if args.knobs_out and rank == 0:
-        with open(args.knobs_out, "w") as f:
-            json.dump(tuned, f)
-    layers = [DeviceConv(resnet_layer(n, batch), compute="bf16", device=local,
-                         seed=1000 * rank + i, knobs=tuned[n]) for i, n in enumerate(LAYERS)]
+    in_b, out_b = PRECISIONS[compute]
+    layers = [DeviceConv(resnet_layer(n, batch), compute=compute, device=local,
+                         seed=1000 * rank + i, knobs=knobs.get(n) or None)
+              for i, n in enumerate(LAYERS)]
     flops = [l.wl.flops for l in layers]
     step_flops = sum(flops)
     stream = torch.cuda.Stream()
@@ -268,13 +332,10 @@ def impl_ours(args):
         for l in layers:
             l.launch(stream)
 
-    # Warm-up (also first-call TMA descriptor / attribute setup).
     with torch.cuda.stream(stream):
-        for _ in range(max(1, args.warmup)):
+        for _ in range(max(1, warmup)):
             step()
     torch.cuda.synchronize()
-
-    # Capture one step in a CUDA graph: 12 kernel launches, no host gaps.
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         step()
@@ -289,100 +350,163 @@ def impl_ours(args):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    import contextlib
+    with (sampler if sampler is not None else contextlib.nullcontext()):
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for _ in range(args.steps):
+            for _ in range(steps):
                 graph.replay()
             ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    elapsed_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([elapsed_ms], device="cuda")
+    t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    value = world * step_flops * args.steps / (max_ms / 1e3) / 1e12
+    value = world * step_flops * steps / (max_ms / 1e3) / 1e12
 
     # ---- per-layer kernel durations, L2 flushed before each launch. Event
     # timestamps here move in ~2 us steps, too coarse for one 6-45 us launch:
     # a CUDA graph of R x (flush, launch) is timed against R x flush alone
     # (median of 3 each) and the difference / R is the launch's device time.
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    per_layer = []
     reps = 10
-
-    def graph_of(fn):
-        with torch.cuda.stream(stream):
-            fn()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            fn()
-        return g
-
-    def median_ms(g):
-        ts = []
-        for _ in range(3):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                a.record(stream)
-                g.replay()
-                b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
-
-    flush_ms = median_ms(graph_of(lambda: [flush.zero_() for _ in range(reps)]))
+    flush_ms = _median_ms(_graph_of(lambda: [flush.zero_() for _ in range(reps)], stream), stream)
+    per_layer = []
     for l, fl in zip(layers, flops):
         def body(l=l):
             for _ in range(reps):
                 flush.zero_()
                 l.launch(stream)
-        us = max(1e-3, (median_ms(graph_of(body)) - flush_ms) * 1e3 / reps)
-        byts = l.algorithmic_bytes()
+        us = max(1e-3, (_median_ms(_graph_of(body, stream), stream) - flush_ms) * 1e3 / reps)
+        byts = l.wl.bytes(in_b, out_b)
         ai = fl / byts
-        bound_tf = min(peak_tf, ai * hbm_gbs / 1e3)
+        bound_tf = min(peak, ai * hbm_gbs / 1e3)
         achieved = fl / (us * 1e-6) / 1e12
         per_layer.append({
-            "layer": l.wl.name, "knobs": tuned[l.wl.name],
+            "layer": l.wl.name, "knobs": knobs.get(l.wl.name) or {},
             "us": round(us, 2), "tflops": round(achieved, 1),
             "gflop": round(fl / 1e9, 3), "mbytes": round(byts / 1e6, 2),
             "ai_flop_per_byte": round(ai, 1),
-            "bound": "tensor" if bound_tf >= peak_tf else "hbm",
+            "bound": "tensor" if bound_tf >= peak else "hbm",
             "roof_tflops": round(bound_tf, 1), "frac_of_roof": round(achieved / bound_tf, 3),
         })
     kern_s = sum(p["us"] for p in per_layer) * 1e-6
-    achieved_tf = step_flops / kern_s / 1e12
-    traffic = None
-    tp = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_step")
-        except Exception:
-            traffic = None
+    # attainable step time: every layer at its own min(peak, AI x HBM) roof
+    roof_s = sum(p["gflop"] * 1e9 / (p["roof_tflops"] * 1e12) for p in per_layer)
+    out = {"value": value, "ms_per_step": max_ms / steps, "step_flops": step_flops,
+           "kernel_tflops": step_flops / kern_s / 1e12, "kernel_us": kern_s * 1e6,
+           "frac_of_attainable": roof_s / kern_s, "layers": per_layer,
+           "launches": len(layers) * steps}
+    del graph, layers, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def impl_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak_tf, hbm_gbs, peak_tf_sus, peak_src = load_peaks()
+    batch = args.batch
+
+    knobs_path = args.knobs_in or KNOBS_FILE
+    knobs = load_knobs(knobs_path)
+    knobs_src = os.path.relpath(knobs_path, REPO) if os.path.exists(knobs_path) else "library defaults"
+
+    int8_peak = measure_int8_peak()
+    peaks = {"f32tc": peak_tf / 6.0, "bf16": peak_tf,
+             "i8": int8_peak if int8_peak else 2.0 * peak_tf}
+    peak_notes = {
+        "f32tc": f"MEASURED_PEAKS.json bf16_tflops ({peak_src}) / 6: every f32 multiply-add is "
+                 "six bf16 tensor-core products (h*h, h*m, m*h, h*l, l*h, m*m)",
+        "bf16": f"MEASURED_PEAKS.json bf16_tflops ({peak_src})",
+        "i8": ("measured in this run: best of 10 cuBLASLt int8 GEMMs 8192^3 (torch._int_mm)"
+               if int8_peak else "2 x bf16_tflops (no int8 GEMM available to measure)"),
+    }
+    headline = args.precision
+    clk = ClockSampler(local)
+    res = {}
+    order = [headline] + [p for p in ("bf16", "i8", "f32tc") if p != headline and
+                          p in args.also.split(",")]
+    for prec in order:
+        res[prec] = measure_step(prec, knobs.get(prec, {}), batch, local, rank, world,
+                                 args.steps, args.warmup, peaks[prec], hbm_gbs,
+                                 sampler=clk if prec == headline else None)
+    h = res[headline]
+
+    # ---- ResNet-18, global batch 256 sharded over the ranks (strong scaling)
+    resnet = None
+    if not args.no_resnet18:
+        import bench_workloads
+        rargs = argparse.Namespace(**vars(args))
+        rargs.global_batch = args.global_batch or 256
+        rargs.no_cpu_baseline = True
+        rargs.steps = min(args.steps, 50)
+        rl = bench_workloads.resnet18_line(rargs, sys.modules[__name__], knobs_file=knobs_path)
+        if rl is not None:
+            resnet = {"img_s": rl["value"], "unit": "img/s", "global_batch": rargs.global_batch,
+                      "n_gpus": rl["n_gpus"], "ms_per_step": rl["ms_per_step"],
+                      "scaling": "strong", "dtype": "bf16", "e2e_img_s": rl["e2e"]["value"],
+                      "roofline_frac": rl["roofline"]["frac"],
+                      "config": rl["config"]["workload"]}
 
     # ---- e2e through the reference-facing host API (tec_eval_fused_conv):
     # pinned host NCHW f32 inputs -> H2D -> pack -> fused kernel -> unpack -> D2H.
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, batch, local)
+        e2e = run_e2e(args, batch, local, headline, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_block(os.cpu_count() or 1)
 
+    traffic, traffic_src = None, None
+    tp = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp)).get(headline) or {}
+            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
+        except Exception:
+            traffic = None
+
+    def sub(prec):
+        r = res[prec]
+        unit = "TOPS" if prec == "i8" else "TFLOP/s"
+        return {"value": round(r["value"], 2), "unit": unit, "dtype": prec,
+                "ms_per_step": round(r["ms_per_step"], 4),
+                "roofline": {"bound": "tensor", "achieved": round(r["kernel_tflops"], 1),
+                             "peak": round(peaks[prec], 1), "unit": unit,
+                             "frac": round(r["kernel_tflops"] / peaks[prec], 3),
+                             "frac_of_attainable": round(r["frac_of_attainable"], 3),
+                             "peak_source": peak_notes[prec]},
+                "parity": {"f32tc": "1e-4 comparator vs the f32 oracle (tests/test_bench_parity.py)",
+                           "bf16": "2e-3 comparator vs the oracle on bf16-rounded inputs",
+                           "i8": "bit-exact vs the oracle"}[prec],
+                "layers": r["layers"]}
+
     if rank == 0:
+        dtype = {"f32tc": "f32", "bf16": "bf16", "i8": "i8"}[headline]
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s",
+            "metric": METRIC, "value": round(h["value"], 2),
+            "unit": "TOPS" if headline == "i8" else "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "ms_per_step": round(h["ms_per_step"], 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {
-                "workload": "configs[1]: ResNet-18 C1-C12 fused conv2d+bias_add+relu, "
-                            f"batch {batch} per GPU, bf16 in / f32 accumulate / bf16 out",
+                "workload": f"configs[1]: ResNet-18 C1-C12 fused conv2d+bias_add+relu, batch "
+                            f"{batch} per GPU, " + {
+                                "f32tc": "f32 in / f32 out (f32 on tcgen05: exact 3-way bf16 "
+                                         "split, six products, RN-folded K chunks; 1e-4 parity)",
+                                "bf16": "bf16 in / f32 accumulate / bf16 out",
+                                "i8": "int8 in / i32 out (bit-exact)"}[headline],
                 "global_batch": batch * world, "parallelism": f"replicas x{world} (no collective)",
                 "l2": "step working set (all 12 layers) > 126 MB L2; per-layer timings "
                       "flush L2 (256 MB write) before each launch (graph of 10 x (flush, "
@@ -392,15 +516,19 @@ def impl_ours(args):
                 "knobs": knobs_src,
             },
             "roofline": {
-                "bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf,
-                "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 3),
-                "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src})",
-                "kernel": "fused conv kernels (conv_halo_kernel / conv_fprop_tc_kernel, tcgen05 "
-                          "implicit GEMM), all 12 launches: sum of flops / sum of per-layer "
-                          "kernel times",
+                "bound": "tensor", "achieved": round(h["kernel_tflops"], 1),
+                "peak": round(peaks[headline], 1), "unit": "TFLOP/s",
+                "frac": round(h["kernel_tflops"] / peaks[headline], 3),
+                "frac_of_attainable": round(h["frac_of_attainable"], 3),
+                "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_notes[headline],
+                "kernel": "the 12 fused conv launches: sum of algorithmic flops / sum of "
+                          "per-layer L2-flushed kernel times",
             },
-            "layers": per_layer,
-            "gpu_launches": len(layers) * args.steps,
+            "layers": h["layers"],
+            "precisions": {p: sub(p) for p in res if p != headline},
+            "resnet18": resnet,
+            "gpu_launches": h["launches"],
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -410,10 +538,14 @@ def impl_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, batch, device):
+def run_e2e(args, batch, device, compute, world):
+    """The headline metric through the public C ABI a reference user calls
+    (tec_eval_fused_conv: host NCHW f32 buffers), H2D + pack + kernel +
+    unpack + D2H inside the timed region, max over ranks."""
     import ctypes as C
 
     import torch
+    import torch.distributed as dist
 
     from paper_1802_04799_b200 import _abi
     lib = _abi.load()
@@ -422,22 +554,30 @@ def run_e2e(args, batch, device):
     prepared = []
     h2d = d2h = 0
     flops = 0
+    cm = {"f32tc": _abi.COMPUTE_F32TC, "bf16": _abi.COMPUTE_BF16, "i8": _abi.COMPUTE_I8}[compute]
     for name in LAYERS:
         wl = resnet_layer(name, batch)
-        x = (torch.rand((wl.n, wl.c, wl.h, wl.w), generator=g) * 2 - 1).pin_memory()
-        w = (torch.rand((wl.k, wl.c, wl.r, wl.s), generator=g) * 2 - 1).pin_memory()
-        b = (torch.rand((wl.k,), generator=g) * 2 - 1).pin_memory()
-        y = torch.empty((wl.n, wl.k, wl.oh, wl.ow)).pin_memory()
+        if compute == "i8":
+            x = torch.randint(-8, 8, (wl.n, wl.c, wl.h, wl.w), dtype=torch.int8, generator=g)
+            w = torch.randint(-8, 8, (wl.k, wl.c, wl.r, wl.s), dtype=torch.int8, generator=g)
+            b = torch.randint(-100, 101, (wl.k,), dtype=torch.int32, generator=g)
+            y = torch.empty((wl.n, wl.k, wl.oh, wl.ow), dtype=torch.int32)
+        else:
+            x = torch.rand((wl.n, wl.c, wl.h, wl.w), generator=g) * 2 - 1
+            w = torch.rand((wl.k, wl.c, wl.r, wl.s), generator=g) * 2 - 1
+            b = torch.rand((wl.k,), generator=g) * 2 - 1
+            y = torch.empty((wl.n, wl.k, wl.oh, wl.ow))
+        x, w, b, y = x.pin_memory(), w.pin_memory(), b.pin_memory(), y.pin_memory()
         d = _abi.ConvDesc(n=wl.n, c=wl.c, h=wl.h, w=wl.w, k=wl.k, r=wl.r, s=wl.s,
                           stride_h=wl.stride, stride_w=wl.stride, pad_h=wl.pad,
-                          pad_w=wl.pad, depthwise=0, compute=_abi.COMPUTE_BF16)
+                          pad_w=wl.pad, depthwise=0, compute=cm)
         e = _abi.Epilogue()
         e.n_ops = 2
         e.ops[0] = _abi.EPI_BIAS
         e.ops[1] = _abi.EPI_RELU
         e.bias = b.data_ptr()
         prepared.append((d, e, x, w, y, b))
-        h2d += x.numel() * 4 + w.numel() * 4 + b.numel() * 4
+        h2d += x.numel() * x.element_size() + w.numel() * w.element_size() + b.numel() * 4
         d2h += y.numel() * 4
         flops += wl.flops
     kn = _abi.Knobs()
@@ -449,16 +589,81 @@ def run_e2e(args, batch, device):
                                                device))
     one()  # warm-up: workspace allocation
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         one()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / steps
-    return {"value": round(flops / dt / 1e12, 3), "unit": "TFLOP/s",
+    if world > 1:
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": round(world * flops / dt / 1e12, 3),
+            "unit": "TOPS" if compute == "i8" else "TFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": round(dt * 1e3, 2),
-            "path": "tec_eval_fused_conv (C ABI, host NCHW f32 buffers, pinned), "
-                    "wall clock incl. H2D, layout packing, kernel, unpack, D2H"}
+            "ms_per_step": round(dt * 1e3, 2), "compute": compute,
+            "path": "tec_eval_fused_conv (C ABI, host NCHW buffers, pinned), wall clock incl. "
+                    "H2D, layout packing, kernel, unpack, D2H; max over ranks"}
+
+
+# ------------------------------------------------------------ multi-rank plumbing
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks
+    (torch.distributed.run, one node, 127.0.0.1) and pass rank 0's output
+    through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def impl_cpu_dry_run(args):
+    """The rank plumbing of the multi-GPU bench on gloo, no GPU: every rank
+    shards the ResNet-18 global batch, times its (tiny, oracle-free numpy)
+    stand-in step between barriers, the max over ranks is reduced, and the
+    logits slices are gathered in rank order -- what the GPU run does, with
+    the kernels replaced by a host matmul."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1802_04799_b200.parallel import gather_rows, shard_batch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    gb = args.global_batch or 256
+    start, cnt = shard_batch(gb, world, rank)
+    rng = np.random.default_rng(rank)
+    a = rng.standard_normal((cnt, 512)).astype(np.float32)
+    w = rng.standard_normal((512, 10)).astype(np.float32)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        logits = a @ w
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64)
+    ranks = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_gather(ranks, torch.tensor([rank], dtype=torch.int64))
+    full = gather_rows(torch.from_numpy(logits), gb)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "dry_run": True, "backend": "gloo" if world > 1 else "none",
+            "n_gpus": world, "ranks": [int(r.item()) for r in ranks] if world > 1 else [0],
+            "global_batch": gb, "gathered_rows": int(full.shape[0]),
+            "max_rank_seconds": float(t.item()), "steps": args.steps}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -470,11 +675,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-tune", action="store_true", help="library default knobs")
-    ap.add_argument("--knobs-in", default="", help="JSON {layer: knobs} to use instead of tuning")
-    ap.add_argument("--retune", action="store_true",
-                    help="tune every layer live instead of reading the committed tuning log")
-    ap.add_argument("--knobs-out", default="", help="write the tuned knobs here")
+    ap.add_argument("--no-tune", action="store_true", help="library default knobs (workloads)")
+    ap.add_argument("--knobs-in", default="",
+                    help="knob file {precision: {layer: knobs}} instead of profiles/tuned_knobs.json")
+    ap.add_argument("--allow-untested-knobs", action="store_true",
+                    help="accept a knob file the parity tests do not cover")
+    ap.add_argument("--precision", default="f32tc", choices=["f32tc", "bf16", "i8"],
+                    help="headline arithmetic (default: f32, the reference's precision)")
+    ap.add_argument("--also", default="bf16,i8", help="sub-result precisions in the same line")
+    ap.add_argument("--no-resnet18", action="store_true")
+    ap.add_argument("--cpu-dry-run", action="store_true",
+                    help="multi-rank plumbing on gloo without a GPU (tests)")
     ap.add_argument("--workload", default="conv",
                     choices=["conv", "resnet18", "depthwise", "c2b1", "int8"],
                     help="conv = the headline configs[1]; others: bench_workloads.py")
@@ -483,7 +694,15 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
-    if args.impl == "reference":
+    if args.knobs_in and os.path.abspath(args.knobs_in) != os.path.abspath(KNOBS_FILE) and \
+            not args.allow_untested_knobs:
+        raise SystemExit(f"bench.py: {args.knobs_in} is not the knob file the parity tests cover "
+                         f"({os.path.relpath(KNOBS_FILE, REPO)}); pass --allow-untested-knobs")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    if args.cpu_dry_run:
+        impl_cpu_dry_run(args)
+    elif args.impl == "reference":
         impl_reference(args)
     elif args.workload != "conv":
         import bench_workloads

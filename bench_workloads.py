@@ -9,7 +9,7 @@ C1-C12 conv step). Each prints ONE JSON line in bench.py's format.
   depthwise  config 3: MobileNet D1-D9 fused depthwise+bias+relu, batch 64,
              bf16 (default) or f32; GB/s vs the HBM roofline (replicas).
   c2b1       config 1: C2 at batch 1, fp32 -- the bit-exact SIMT path and
-             the 3xTF32 tensor-core path; latency (us) per fused layer.
+             the f32tc tensor-core path; latency (us) per fused layer.
   int8       config 5: C1-C12 int8 -> i32 at batch 64 (TOPS) plus the
              sharded tuner's trial throughput.
 """
@@ -68,6 +68,16 @@ def _time_replays(fn, steps, stream):
 
 # ------------------------------------------------------------------ resnet18
 def resnet18(args, bench):
+    line = resnet18_line(args, bench)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def resnet18_line(args, bench, knobs_file=None):
+    """ResNet-18 b256 strong-scaling measurement; returns rank 0's JSON
+    line (None on other ranks). Knobs: `knobs_file`'s "resnet18_bf16" entry
+    ({fused node id: knobs}) when present, else tuned live (or defaults
+    with --no-tune)."""
     import torch
 
     from paper_1802_04799_b200.executor import DeviceGraph
@@ -78,7 +88,12 @@ def resnet18(args, bench):
     gb = args.global_batch or 256
     start, cnt = shard_batch(gb, ws, rank)
     g = resnet18_graph(cnt)
-    knobs = _tune_graph_convs(g, local, args) if not args.no_tune else {}
+    knobs = None
+    if knobs_file and os.path.exists(knobs_file):
+        with open(knobs_file) as f:
+            knobs = json.load(f).get("resnet18_bf16")
+    if knobs is None:
+        knobs = _tune_graph_convs(g, local, args) if not args.no_tune else {}
     dg = DeviceGraph(g, compute="bf16", device=local, knobs=knobs)
     rng = np.random.default_rng(1234)  # same weights on every rank (replicated)
     params = {}
@@ -169,9 +184,10 @@ def resnet18(args, bench):
                         "gathered (all_gather) and copied to host"},
         "cpu_baseline": _resnet_cpu_baseline(bench) if rank == 0 and ws == 1 and
         not args.no_cpu_baseline else None,
+        "knobs": knobs,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    del dg
+    return line if rank == 0 else None
 
 
 def _tune_graph_convs(g, device, args):
@@ -340,7 +356,7 @@ def c2b1(args, bench):
     res = {}
     stream = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for compute in ("f32", "tf32x3", "bf16"):
+    for compute in ("f32", "f32tc", "bf16"):
         l = DeviceConv(wl, compute=compute, device=local,
                        out_dtype=None if compute == "bf16" else 0)
         with torch.cuda.stream(stream):

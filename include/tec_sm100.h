@@ -188,6 +188,21 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
                                const void* w_packed, void* y,
                                int32_t out_dtype, int32_t* err_flag,
                                void* stream);
+/* Device scratch a tec_conv2d_fused_ws launch of this desc + knobs needs
+ * (split-K partial tiles + tile counters; 0 for every other schedule). */
+tec_status tec_workspace_bytes(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, size_t* bytes);
+/* tec_conv2d_fused on a CALLER-OWNED workspace of >= tec_workspace_bytes
+ * bytes, zero-filled before its first use (every launch leaves it zeroed).
+ * Nothing is allocated on this path; a workspace may be shared by launches
+ * that are ordered on one stream. CapacityError if ws_bytes is too small.
+ * (tec_conv2d_fused without a workspace uses a grow-only internal scratch
+ * per (device, stream), never freed while the library is loaded.) */
+tec_status tec_conv2d_fused_ws(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, const void* x_packed,
+                               const void* w_packed, void* y, int32_t out_dtype,
+                               int32_t* err_flag, void* ws, size_t ws_bytes,
+                               void* stream);
 
 /* ---- lowering (target "sm100"): the kernel a descriptor + knobs lower to,
  * without launching (LowerOptions::target, R/include/tec/lower.hpp:26-33;
@@ -209,6 +224,8 @@ typedef struct {
   int32_t grid;                      /* persistent CTAs (0: data-dependent)  */
   int32_t smem_bytes, tmem_cols;     /* per-CTA on-chip budget used          */
   int32_t tma_store;                 /* 1: TMA-store epilogue                */
+  int64_t workspace_bytes;           /* device scratch the launch needs (split-K
+                                        partials + tile counters); 0 = none  */
 } tec_kernel_plan;
 
 tec_status tec_conv_plan(const tec_conv_desc* d, const tec_epilogue* epi,

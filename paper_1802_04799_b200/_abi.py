@@ -78,7 +78,7 @@ class KernelPlan(C.Structure):
     """tec_kernel_plan (include/tec_sm100.h)."""
     _fields_ = [(f, C.c_int32) for f in ("family", "tile_m", "tile_n", "stages", "split_k",
                                          "cluster", "grid", "smem_bytes", "tmem_cols",
-                                         "tma_store")]
+                                         "tma_store")] + [("workspace_bytes", C.c_int64)]
 
 
 class ConvLayout(C.Structure):
@@ -121,6 +121,9 @@ SIGNATURES = {
                                      _P, _P]),
     "tec_depthwise_fused": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P,
                                         C.c_int32, _P, _P]),
+    "tec_workspace_bytes": (C.c_int32, [_DESC, _EPI, _KN, C.POINTER(C.c_size_t)]),
+    "tec_conv2d_fused_ws": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P, C.c_int32, _P, _P,
+                                        C.c_size_t, _P]),
     "tec_eval_fused_conv": (C.c_int32, [_DESC, _EPI, _KN, _P, _P, _P, C.c_int]),
     "tec_measure": (C.c_int32, [_DESC, _EPI, _KN, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.POINTER(C.c_double)]),

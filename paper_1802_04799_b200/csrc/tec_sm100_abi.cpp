@@ -74,6 +74,10 @@ thread_local std::string g_last_error;
 // tec_conv_plan: when set, the launch paths record their decision here and
 // return before launching anything.
 thread_local tec_kernel_plan* g_plan = nullptr;
+// Caller-owned workspace of the current tec_conv2d_fused_ws call (null:
+// the per-(device, stream) internal pool of tec_conv2d_fused).
+thread_local void* g_ws = nullptr;
+thread_local size_t g_ws_bytes = 0;
 
 bool plan_only(int family, int bn, int tile_m, int stages, int grid, int smem, int tmem_cols,
                int tma_store, int splits, int cluster) {
@@ -314,6 +318,15 @@ tec_status build_epilogue(const tec_epilogue* e, bool integer, EpilogueParams* o
   if (e->n_ops < 0 || e->n_ops > kMaxEpi)
     return fail(TEC_E_LOWERING, "too many fused epilogue members");
   out->n_ops = e->n_ops;
+  int n_bias = 0, n_add = 0, n_mul = 0;
+  for (int i = 0; i < e->n_ops; ++i) {
+    n_bias += e->ops[i] == TEC_EPI_BIAS;
+    n_add += e->ops[i] == TEC_EPI_ADD;
+    n_mul += e->ops[i] == TEC_EPI_MUL;
+  }
+  // one operand pointer per kind: a repeated member would read the same operand
+  if (n_bias > 1 || n_add > 1 || n_mul > 1)
+    return fail(TEC_E_LOWERING, "more than one bias_add / add / mul member in one fused conv");
   for (int i = 0; i < e->n_ops; ++i) {
     const int op = e->ops[i];
     if (op < TEC_EPI_SCALE || op > TEC_EPI_RELU)
@@ -643,37 +656,52 @@ bool fast_program(const EpilogueParams& e) {
   return e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu;
 }
 
-// Per-device split-K scratch: f32 partial tiles + per-tile arrival counters
-// (zeroed once; the kernel resets each counter after use). Grows on demand;
-// growing is a synchronous allocation, so it must happen outside a CUDA-graph
-// capture (the first eager launch of a shape takes care of that).
-tec_status splitk_workspace(int dev, size_t bytes, size_t tiles, cudaStream_t st, float** ws,
-                            int32_t** cnt) {
-  struct Scratch { float* ws = nullptr; size_t bytes = 0; int32_t* cnt = nullptr; size_t n = 0; };
-  static std::mutex mu;
-  static std::map<int, Scratch> per_dev;
-  std::lock_guard<std::mutex> lock(mu);
-  Scratch& sc = per_dev[dev];
-  if (sc.bytes < bytes || sc.n < tiles) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs != cudaStreamCaptureStatusNone)
-      return fail(TEC_E_LOWERING, "split-K workspace must be sized by an eager launch before capture");
-    TEC_CUDA(cudaStreamSynchronize(st));
-    if (sc.bytes < bytes) {
-      if (sc.ws) cudaFree(sc.ws);
-      TEC_CUDA(cudaMalloc(&sc.ws, bytes));
-      sc.bytes = bytes;
+// Split-K scratch layout: [f32 partial tiles][per-tile arrival counters],
+// the counters zero before the first launch (every launch leaves them zero:
+// the last split of a tile resets its counter).
+size_t splitk_partials_bytes(size_t partial_bytes) { return (partial_bytes + 255) & ~size_t(255); }
+size_t splitk_bytes(size_t partial_bytes, size_t tiles) {
+  return splitk_partials_bytes(partial_bytes) + tiles * sizeof(int32_t);
+}
+
+// The scratch a split-K launch uses: the caller's (tec_conv2d_fused_ws /
+// a tec_plan's own buffer), else an internal pool per (device, stream) --
+// grow-only: a buffer a captured CUDA graph may still reference is never
+// freed, and launches on different streams never share tile counters.
+// Growing is a synchronous allocation, refused during stream capture.
+tec_status splitk_workspace(int dev, size_t partial_bytes, size_t tiles, cudaStream_t st,
+                            float** ws, int32_t** cnt) {
+  const size_t need = splitk_bytes(partial_bytes, tiles);
+  uint8_t* base = nullptr;
+  if (g_ws) {
+    if (g_ws_bytes < need)
+      return fail(TEC_E_CAPACITY, "workspace too small: " + std::to_string(g_ws_bytes) + " < " +
+                                      std::to_string(need) + " bytes (tec_workspace_bytes)");
+    base = static_cast<uint8_t*>(g_ws);
+  } else {
+    struct Pool { void* p = nullptr; size_t bytes = 0; };
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, Pool> pools;
+    static std::vector<void*> retired;  // kept alive: captured graphs may use them
+    std::lock_guard<std::mutex> lock(mu);
+    Pool& pool = pools[{dev, st}];
+    if (pool.bytes < need) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone)
+        return fail(TEC_E_LOWERING, "split-K workspace must be sized by an eager launch before "
+                                    "capture (or pass one: tec_conv2d_fused_ws)");
+      void* p = nullptr;
+      TEC_CUDA(cudaMalloc(&p, need));
+      TEC_CUDA(cudaMemsetAsync(p, 0, need, st));
+      if (pool.p) retired.push_back(pool.p);
+      pool.p = p;
+      pool.bytes = need;
     }
-    if (sc.n < tiles) {
-      if (sc.cnt) cudaFree(sc.cnt);
-      TEC_CUDA(cudaMalloc(&sc.cnt, tiles * sizeof(int32_t)));
-      TEC_CUDA(cudaMemset(sc.cnt, 0, tiles * sizeof(int32_t)));
-      sc.n = tiles;
-    }
+    base = static_cast<uint8_t*>(pool.p);
   }
-  *ws = sc.ws;
-  *cnt = sc.cnt;
+  *ws = reinterpret_cast<float*>(base);
+  *cnt = reinterpret_cast<int32_t*>(base + splitk_partials_bytes(partial_bytes));
   return TEC_OK;
 }
 
@@ -819,10 +847,13 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
       if (want > k_iters) want = k_iters;
       p.splits = want;
       p.kps = (k_iters + want - 1) / want;
-      tec_status wst = splitk_workspace(dev, (size_t)tiles * want * 128 * bn * sizeof(float),
-                                        (size_t)tiles, st, &p.ws, &p.tile_cnt);
-      if (wst) return wst;
     }
+  }
+  const size_t partials = (size_t)tiles * p.splits * 128 * bn * sizeof(float);
+  if (g_plan) g_plan->workspace_bytes = p.splits > 1 ? (int64_t)splitk_bytes(partials, tiles) : 0;
+  if (p.splits > 1 && !g_plan) {  // sized without allocating when only planning
+    tec_status wst = splitk_workspace(dev, partials, (size_t)tiles, st, &p.ws, &p.tile_cnt);
+    if (wst) return wst;
   }
   int grid = (int)std::min<int64_t>(tiles * p.splits, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
@@ -1168,6 +1199,29 @@ tec_status tec_conv2d_fused(const tec_conv_desc* d, const tec_epilogue* epi,
                   (cudaStream_t)stream);
 }
 
+tec_status tec_conv2d_fused_ws(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, const void* x_packed,
+                               const void* w_packed, void* y, int32_t out_dtype,
+                               int32_t* err_flag, void* ws, size_t ws_bytes, void* stream) {
+  g_ws = ws;
+  g_ws_bytes = ws ? ws_bytes : 0;
+  const tec_status st = tec_conv2d_fused(d, epi, knobs, x_packed, w_packed, y, out_dtype,
+                                         err_flag, stream);
+  g_ws = nullptr;
+  g_ws_bytes = 0;
+  return st;
+}
+
+tec_status tec_workspace_bytes(const tec_conv_desc* d, const tec_epilogue* epi,
+                               const tec_knobs* knobs, size_t* bytes) {
+  if (!bytes) return fail(TEC_E_INTERNAL, "null output");
+  tec_kernel_plan kp;
+  const tec_status st = tec_conv_plan(d, epi, knobs, &kp);
+  if (st) return st;
+  *bytes = (size_t)kp.workspace_bytes;
+  return TEC_OK;
+}
+
 tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
                                const tec_knobs* knobs, const void* x_packed,
                                const void* w_packed, void* y, int32_t out_dtype,
@@ -1377,6 +1431,15 @@ tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
   TEC_CUDA(cudaSetDevice(device));
   HostWorkspace& ws = workspace(device);
   std::lock_guard<std::mutex> lock(ws.mu);
+  // Every exit -- errors included -- waits for the call's copy and compute
+  // streams, so no DMA into the caller's host buffers outlives the call.
+  struct Drain {
+    HostWorkspace& w;
+    ~Drain() {
+      for (cudaStream_t t : {w.stream, w.h2d, w.d2h})
+        if (t) cudaStreamSynchronize(t);
+    }
+  } drain{ws};
   if (!ws.stream) TEC_CUDA(cudaStreamCreateWithFlags(&ws.stream, cudaStreamNonBlocking));
   cudaStream_t s = ws.stream;
 
@@ -1588,14 +1651,18 @@ struct tec_plan {
   std::vector<tec_step> steps;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  // the plan's own split-K scratch (steps run in order on one stream, so
+  // they share it; zero-filled once, left zeroed by every launch)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
 };
 
 namespace {
-tec_status run_step(const tec_step& s, void* stream) {
+tec_status run_step(const tec_plan* p, const tec_step& s, void* stream) {
   switch (s.kind) {
     case TEC_STEP_CONV:
-      return tec_conv2d_fused(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype, nullptr,
-                              stream);
+      return tec_conv2d_fused_ws(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype,
+                                 nullptr, p->ws, p->ws_bytes, stream);
     case TEC_STEP_DEPTHWISE:
       return tec_depthwise_fused(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype,
                                  nullptr, stream);
@@ -1616,7 +1683,7 @@ tec_status run_step(const tec_step& s, void* stream) {
 
 tec_status run_steps(const tec_plan* p, void* stream) {
   for (size_t i = 0; i < p->steps.size(); ++i) {
-    tec_status st = run_step(p->steps[i], stream);
+    tec_status st = run_step(p, p->steps[i], stream);
     if (st) {
       g_last_error = "plan step " + std::to_string(i) + ": " + g_last_error;
       return st;
@@ -1639,6 +1706,15 @@ tec_status tec_plan_create(const tec_step* steps, int32_t n_steps, tec_plan** ou
       delete p;
       g_last_error = "plan step " + std::to_string(i) + ": " + g_last_error;
       return st;
+    }
+    p->ws_bytes = std::max(p->ws_bytes, (size_t)kp.workspace_bytes);
+  }
+  if (p->ws_bytes) {
+    if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess ||
+        cudaMemset(p->ws, 0, p->ws_bytes) != cudaSuccess) {
+      if (p->ws) cudaFree(p->ws);
+      delete p;
+      return fail(TEC_E_CUDA, "plan workspace allocation failed");
     }
   }
   *out = p;
@@ -1690,7 +1766,7 @@ tec_status tec_plan_run_steps(tec_plan* p, int32_t first, int32_t count, void* s
   if (!p || first < 0 || count < 0 || (size_t)first + (size_t)count > p->steps.size())
     return fail(TEC_E_INTERNAL, "plan step range out of bounds");
   for (int32_t i = first; i < first + count; ++i) {
-    tec_status st = run_step(p->steps[i], stream);
+    tec_status st = run_step(p, p->steps[i], stream);
     if (st) {
       g_last_error = "plan step " + std::to_string(i) + ": " + g_last_error;
       return st;
@@ -1705,6 +1781,7 @@ void tec_plan_destroy(tec_plan* p) {
   if (!p) return;
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->graph) cudaGraphDestroy(p->graph);
+  if (p->ws) cudaFree(p->ws);
   delete p;
 }
 }  // extern "C"

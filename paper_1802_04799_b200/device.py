@@ -94,16 +94,28 @@ class DeviceConv:
         self.epi.n_ops = len(ops)
         self.epi.bias = self.bias.data_ptr()
         self.knobs = _abi.Knobs(**(knobs or {}))
+        # caller-owned split-K scratch (tec_workspace_bytes), zeroed once
+        nbytes = C.c_size_t(0)
+        if not wl.depthwise:
+            _abi.check(self.lib.tec_workspace_bytes(C.byref(self.desc), C.byref(self.epi),
+                                                    C.byref(self.knobs), C.byref(nbytes)))
+        self.ws = torch.zeros(max(1, nbytes.value), dtype=torch.uint8, device=self.dev)
+        self.ws_bytes = nbytes.value
         # the packed operands are ready before any launch, on any stream (the
         # conv kernels read weights before their PDL wait)
         torch.cuda.synchronize(self.dev)
         del x_src, w_src
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
-        fn = self.lib.tec_depthwise_fused if self.wl.depthwise else self.lib.tec_conv2d_fused
-        _abi.check(fn(C.byref(self.desc), C.byref(self.epi), C.byref(self.knobs),
-                      self.x.data_ptr(), self.w.data_ptr(), self.y.data_ptr(),
-                      self.out_dtype, None, _stream_ptr(stream)))
+        if self.wl.depthwise:
+            _abi.check(self.lib.tec_depthwise_fused(
+                C.byref(self.desc), C.byref(self.epi), C.byref(self.knobs), self.x.data_ptr(),
+                self.w.data_ptr(), self.y.data_ptr(), self.out_dtype, None, _stream_ptr(stream)))
+            return
+        _abi.check(self.lib.tec_conv2d_fused_ws(
+            C.byref(self.desc), C.byref(self.epi), C.byref(self.knobs), self.x.data_ptr(),
+            self.w.data_ptr(), self.y.data_ptr(), self.out_dtype, None, self.ws.data_ptr(),
+            self.ws_bytes, _stream_ptr(stream)))
 
     @property
     def act_elem_bytes(self) -> int:

@@ -267,6 +267,11 @@ class DeviceGraph:
                 raise TecError(E_LOWERING, "bias_add must broadcast over channels")
             items.append((m.op, others[0] if others else None, m))
             prev = m.id
+        for op in ("bias_add", "add", "mul"):
+            # one operand slot each in tec_epilogue: a second member of the
+            # same kind would silently read the first one's operand
+            if sum(1 for it in items if it[0] == op) > 1:
+                raise TecError(E_LOWERING, f"fused node '{n.id}' has more than one '{op}' member")
         return root, items
 
     def _conv_input(self, d: _abi.ConvDesc, src: DevTensor) -> int:
@@ -424,11 +429,15 @@ class DeviceGraph:
                 prep(params, st)
 
     def set_feed(self, name: str, value, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Copies a feed into its device buffer ON `stream` (default: the
+        current stream), so a later launch(stream) is ordered after it."""
         t = self.feeds[name]
         v = value if isinstance(value, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(value))
         if list(v.shape) != t.shape:
             raise TecError(E_SHAPE, f"input {name} is {list(v.shape)}, expected {t.shape}")
-        t.buf.copy_(v.reshape(-1).to(t.buf.dtype), non_blocking=True)
+        s = stream or torch.cuda.current_stream(self.dev)
+        with torch.cuda.stream(s):
+            t.buf.copy_(v.reshape(-1).to(t.buf.dtype), non_blocking=True)
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Enqueue every step on `stream` (device-resident feeds)."""

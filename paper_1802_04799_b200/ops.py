@@ -130,6 +130,10 @@ def fused_conv(op: str, x: np.ndarray, w: np.ndarray, attrs: AttrMap,
             else:
                 epi.mul_operand = r.ctypes.data
     epi.n_ops = len(epilogue)
+    names = [it[0] for it in epilogue]
+    for op in ("bias_add", "add", "mul"):
+        if names.count(op) > 1:  # one operand slot each in tec_epilogue
+            raise TecError(15, f"more than one '{op}' member in one fused conv")
     kn = _abi.Knobs(**(knobs or {}))
     x = np.ascontiguousarray(x)
     w = np.ascontiguousarray(w)

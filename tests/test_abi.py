@@ -87,10 +87,11 @@ def test_layout_planning():
     # stem: 3 channels padded to one 32-byte block
     assert lib.tec_conv_layout_of(C.byref(_desc(c=3)), C.byref(lay)) == 0
     assert lay.cp == 16
-    # fp32 parity path stores [hi | hi | lo] channel triplets
-    d = _desc(compute=_abi.COMPUTE_TF32X3)
+    # f32 on tensor cores stores three exact bf16 planes [h | m | l]
+    d = _desc(compute=_abi.COMPUTE_F32TC)
     assert lib.tec_conv_layout_of(C.byref(d), C.byref(lay)) == 0
-    assert lay.cp == 192 and lay.act_dtype == _abi.DT_F32
+    assert lay.cp == 192 and lay.act_dtype == _abi.DT_BF16
+    assert lay.act_bytes == 56 * 56 * 192 * 2
     d = _desc(compute=_abi.COMPUTE_I8)
     assert lib.tec_conv_layout_of(C.byref(d), C.byref(lay)) == 0
     assert lay.cp == 64 and lay.acc_dtype == _abi.DT_I32
@@ -108,7 +109,7 @@ def test_struct_layouts_match_header(tmp_path):
         "tec_epilogue": (_abi.Epilogue, ["bias", "mul_operand"]),
         "tec_knobs": (_abi.Knobs, ["grid"]),
         "tec_pool_desc": (_abi.PoolDesc, ["out_dtype"]),
-        "tec_kernel_plan": (_abi.KernelPlan, ["tma_store"]),
+        "tec_kernel_plan": (_abi.KernelPlan, ["tma_store", "workspace_bytes"]),
         "tec_step": (_abi.Step, ["conv", "epi", "knobs", "pool", "src", "w", "dst", "w_"]),
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tec_sm100.h"',
@@ -137,3 +138,16 @@ def test_plan_create_rejects_bad_arguments():
     assert lib.tec_plan_create(None, -1, C.byref(h)) != 0
     assert lib.tec_plan_size(None) == 0
     lib.tec_plan_destroy(None)
+
+
+def test_window_larger_than_padded_input_is_rejected():
+    """-stride < h + 2p - r < 0: C++ truncation would give OH = 1 (the
+    reference's infer_conv accepts it and then reads out of bounds); the ABI
+    rejects it and Python sizes outputs from the ABI's shape."""
+    from paper_1802_04799_b200.ops import conv_desc
+    with pytest.raises(_abi.TecError) as ei:
+        conv_desc("conv2d", (1, 4, 2, 2), (4, 4, 3, 3), {"strides": (2, 2)}, 1)
+    assert ei.value.code == "ShapeMismatch"
+    shape = []
+    conv_desc("conv2d", (1, 4, 3, 3), (4, 4, 3, 3), {"strides": (2, 2)}, 1, shape)
+    assert shape == [1, 4, 1, 1]
