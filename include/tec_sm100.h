@@ -193,7 +193,8 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
 tec_status tec_workspace_bytes(const tec_conv_desc* d, const tec_epilogue* epi,
                                const tec_knobs* knobs, size_t* bytes);
 /* tec_conv2d_fused on a CALLER-OWNED workspace of >= tec_workspace_bytes
- * bytes, zero-filled before its first use (every launch leaves it zeroed).
+ * bytes, zero-filled before its first use (every launch leaves its counter
+ * region zeroed; one workspace may serve launches of different shapes).
  * Nothing is allocated on this path; a workspace may be shared by launches
  * that are ordered on one stream. CapacityError if ws_bytes is too small.
  * (tec_conv2d_fused without a workspace uses a grow-only internal scratch

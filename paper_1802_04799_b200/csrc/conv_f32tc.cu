@@ -35,6 +35,19 @@
 //              rounded separately, R/src/graph.cpp:209-222) and stores
 //              through 32x32 f32 boxes with TMA.
 // TMEM: S0 S1 T0 T1, BN columns each (4 x BN <= 512).
+//
+// Plane layouts: 64+ channels per plane -> the three planes are separate
+// 128-B channel blocks ([h | m | l], one TMA box each per k-iteration);
+// <= 16 channels per plane (the space-to-depth stem C1) -> INTERLEAVED: one
+// 64-channel pixel [h16 | m16 | l16 | 0], one box per k-iteration, and the
+// planes are the three K16 slices (32-B offsets) of the same swizzled row --
+// a third of the im2col requests.
+//
+// Split-K (deep layers whose output has too few tiles for 148 SMs): work
+// item = (tile, split); a split folds its own hh chunks and cross terms into
+// an f32 partial, the last split to arrive sums the partials IN SPLIT ORDER
+// with RN adds (the same promotion as the chunk fold -- deterministic and
+// independent of scheduling) and runs the fused members.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -52,26 +65,32 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 
-template <int BN, int SWZ, int STAGES>
+template <int BN, int SWZ, int STAGES, bool INTER>
 struct F32tcCfg {
-  static constexpr int kA = kBM * SWZ;         // one plane of A per stage
-  static constexpr int kB = BN * SWZ;          // one plane of B per stage
-  static constexpr int kStage = 3 * (kA + kB);
-  static constexpr int kKSteps = SWZ / 32;     // K16 MMAs per plane per stage
+  static constexpr int kPlanes = INTER ? 1 : 3;  // TMA boxes per operand per k-iteration
+  static constexpr int kA = kBM * SWZ;           // one box of A
+  static constexpr int kB = BN * SWZ;            // one box of B
+  static constexpr int kStage = kPlanes * (kA + kB);
+  static constexpr int kKSteps = INTER ? 1 : SWZ / 32;  // K16 steps per plane per stage
   static constexpr uint32_t kTmemCols = 4 * BN <= 256 ? 256 : 512;
   static constexpr int kSmem = 1024 + STAGES * kStage + 8 * 4096 + 256 + BN * 4;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   static_assert(4 * BN <= 512, "TMEM budget");
+  static_assert(!INTER || SWZ == 128, "interleaved planes live in one 128-B row");
 };
 
-template <int BN, int SWZ, int STAGES, int PROG>
+template <int BN, int SWZ, int STAGES, bool INTER, int PROG>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_f32tc_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvGemmParams p) {
-  using Cfg = F32tcCfg<BN, SWZ, STAGES>;
-  constexpr int kCB = SWZ / 2;  // bf16 channels per block
+  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER>;
+  constexpr int kCB = SWZ / 2;  // bf16 channels per box row
   constexpr int HB = BN / 2;    // columns per epilogue warp
+  // byte offset of plane q inside an operand stage: its own box, or its
+  // K16 slice of the interleaved row
+  constexpr int kPlaneA = INTER ? 32 : Cfg::kA;
+  constexpr int kPlaneB = INTER ? 32 : Cfg::kB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -83,14 +102,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = sempty + 2;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
   uint32_t* sBias = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int num_tiles = p.m_tiles * p.n_tiles;
+  const int splits = p.splits > 1 ? p.splits : 1;
+  const int num_items = p.m_tiles * p.n_tiles * splits;
   const int k_iters = p.r * p.s * p.cblocks;
-  const int kps = p.kps;  // k-iterations per hh chunk
-  const int cpp = p.cp;   // channels per plane
+  const int kps = splits > 1 ? p.kps : k_iters;  // k-iterations per split
+  const int chunk = p.chunk_iters;               // k-iterations per hh chunk
+  const int cpp = p.cp;                          // channels per plane
+  const int pix = INTER ? 64 : 3 * cpp;          // packed channels per pixel
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_a);
@@ -122,10 +145,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int ohw = p.oh * p.ow;
-      const int wrow = 3 * cpp * p.s;  // weight columns per filter row
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_tile = tile / p.n_tiles;
-        const int n_tile = tile - m_tile * p.n_tiles;
+      const int sc = p.s * p.cblocks;
+      for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
+        const int mn = item / splits;
+        const int split = item - mn * splits;
+        const int m_tile = mn / p.n_tiles;
+        const int n_tile = mn - m_tile * p.n_tiles;
         const int m0 = m_tile * kBM;
         const int img = m0 / ohw;
         const int rem = m0 - img * ohw;
@@ -133,17 +158,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ow = rem - oh * p.ow;
         const int w0 = ow * p.sw - p.pw;
         const int h0 = oh * p.sh - p.ph;
-        int r = 0, s = 0, cb = 0;
-        for (int k = 0; k < k_iters; ++k) {
+        const int kb = split * kps, ke = min(k_iters, kb + kps);
+        int r = kb / sc, rem_k = kb - r * sc;
+        int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
+        for (int k = kb; k < ke; ++k) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
           uint8_t* base = smem + stage * Cfg::kStage;
-          const int wcol = r * wrow + s * 3 * cpp + cb * kCB;
+          const int wcol = (r * p.s + s) * pix + cb * kCB;
 #pragma unroll
-          for (int pl = 0; pl < 3; ++pl) {
+          for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
             tma_load_im2col_4d(base + pl * Cfg::kA, &tm_a, &full[stage], pl * cpp + cb * kCB, w0,
                                h0, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-            tma_load_2d(base + 3 * Cfg::kA + pl * Cfg::kB, &tm_b, &full[stage],
+            tma_load_2d(base + Cfg::kPlanes * Cfg::kA + pl * Cfg::kB, &tm_b, &full[stage],
                         wcol + pl * cpp, n_tile * BN);
           }
           if (++stage == STAGES) {
@@ -165,14 +192,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int g = 0;  // hh chunks issued so far (S ring position)
       int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
         const int tb = local & 1;
         mbar_wait(&tempty[tb], ((local >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t t_tmem = tmem_base + (2 + tb) * BN;
         uint32_t s_tmem = tmem_base;
+        const int kb = (item % splits) * kps, ke = min(k_iters, kb + kps);
         int in_chunk = 0;
-        for (int k = 0; k < k_iters; ++k) {
+        for (int k = kb; k < ke; ++k) {
           if (in_chunk == 0) {
             const int sb = g & 1;
             mbar_wait(&sempty[sb], ((g >> 1) & 1) ^ 1);
@@ -184,15 +212,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t base = smem_u32(smem + stage * Cfg::kStage);
 #pragma unroll
           for (int kk = 0; kk < Cfg::kKSteps; ++kk) {
-            const uint32_t a0 = base + kk * 32, b0 = base + 3 * Cfg::kA + kk * 32;
+            const uint32_t a0 = base + kk * 32, b0 = base + Cfg::kPlanes * Cfg::kA + kk * 32;
             const uint64_t ah = make_smem_desc<SWZ>(a0, 8 * SWZ);
-            const uint64_t am = make_smem_desc<SWZ>(a0 + Cfg::kA, 8 * SWZ);
-            const uint64_t al = make_smem_desc<SWZ>(a0 + 2 * Cfg::kA, 8 * SWZ);
+            const uint64_t am = make_smem_desc<SWZ>(a0 + kPlaneA, 8 * SWZ);
+            const uint64_t al = make_smem_desc<SWZ>(a0 + 2 * kPlaneA, 8 * SWZ);
             const uint64_t bh = make_smem_desc<SWZ>(b0, 8 * SWZ);
-            const uint64_t bm = make_smem_desc<SWZ>(b0 + Cfg::kB, 8 * SWZ);
-            const uint64_t bl = make_smem_desc<SWZ>(b0 + 2 * Cfg::kB, 8 * SWZ);
+            const uint64_t bm = make_smem_desc<SWZ>(b0 + kPlaneB, 8 * SWZ);
+            const uint64_t bl = make_smem_desc<SWZ>(b0 + 2 * kPlaneB, 8 * SWZ);
             tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc, (in_chunk | kk) != 0 ? 1u : 0u);
-            tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, (k | kk) != 0 ? 1u : 0u);
+            tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, (k != kb || kk != 0) ? 1u : 0u);
             tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
             tc_mma<MmaKind::kF16>(t_tmem, ah, bl, idesc, 1u);
             tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
@@ -203,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage = 0;
             phase ^= 1;
           }
-          if (++in_chunk == kps || k + 1 == k_iters) {
+          if (++in_chunk == chunk || k + 1 == ke) {
             tc_commit(&sfull[g & 1]);  // chunk ready to fold
             ++g;
             in_chunk = 0;
@@ -215,26 +243,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------- epilogue warps
     const uint32_t q = warp & 3;
-    const int hf = static_cast<int>(warp - 4) >> 2;
+    const int ew = static_cast<int>(warp) - 4;
+    const int hf = ew >> 2;
     const int etid = static_cast<int>(threadIdx.x) - 128;
-    const uint32_t stage_u32 = smem_u32(sStage + (warp - 4) * 4096);
-    const int nch = (k_iters + kps - 1) / kps;
+    const uint32_t stage_u32 = smem_u32(sStage + ew * 4096);
     const uint32_t lane_base = tmem_base + ((q * 32) << 16) + hf * HB;
     bool overflow = false;
     int g = 0;
     int local = 0;
     int staged_n = -1;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int m_tile = tile / p.n_tiles;
-      const int n_tile = tile - m_tile * p.n_tiles;
+    for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
+      const int mn = item / splits;
+      const int split = item - mn * splits;
+      const int m_tile = mn / p.n_tiles;
+      const int n_tile = mn - m_tile * p.n_tiles;
       const int row0 = m_tile * kBM + static_cast<int>(q * 32);
       const int row = row0 + static_cast<int>(lane);
-      if (PROG != epi::kProgNone && n_tile != staged_n) {
-        epi::named_bar_sync(1, 256);  // previous tile's bias readers are done
-        epi::stage_bias(sBias, p.epi.bias, n_tile * BN, BN, p.oc, etid, 256);
-        epi::named_bar_sync(1, 256);
-        staged_n = n_tile;
-      }
+      const int kb = split * kps, ke = min(k_iters, kb + kps);
+      const int nch = (ke - kb + chunk - 1) / chunk;
       float sum[HB];
 #pragma unroll
       for (int j = 0; j < HB; ++j) sum[j] = 0.0f;
@@ -269,6 +295,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[tb]);
+      if (splits > 1) {
+        // publish this split's partial ([item][warp][column][lane]: one
+        // 128-B line per column); the last split of the tile sums them all
+        // in split order
+        float* mine = p.ws + ((static_cast<size_t>(mn) * splits + split) * 8 + ew) * HB * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < HB; ++j) __stcg(mine + j * 32, sum[j]);
+        __threadfence();
+        epi::named_bar_sync(1, 256);
+        if (etid == 0) *s_last = atomicAdd(&p.tile_cnt[mn], 1) == splits - 1;
+        epi::named_bar_sync(1, 256);
+        if (!*s_last) continue;
+        __threadfence();
+        const float* part = p.ws + (static_cast<size_t>(mn) * splits * 8 + ew) * HB * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < HB; ++j) sum[j] = __ldcg(part + j * 32);
+#pragma unroll 1
+        for (int sp = 1; sp < splits; ++sp) {
+          const float* ps = part + static_cast<size_t>(sp) * 8 * HB * 32;
+#pragma unroll
+          for (int j = 0; j < HB; ++j) sum[j] = __fadd_rn(sum[j], __ldcg(ps + j * 32));
+        }
+        if (etid == 0) p.tile_cnt[mn] = 0;  // ready for the next launch
+      }
+      if (PROG != epi::kProgNone && n_tile != staged_n) {
+        // only the tiles this CTA finishes stage their bias (uniform over the
+        // 256 epilogue threads: s_last is shared)
+        epi::named_bar_sync(2, 256);  // previous tile's bias readers are done
+        epi::stage_bias(sBias, p.epi.bias, n_tile * BN, BN, p.oc, etid, 256);
+        epi::named_bar_sync(2, 256);
+        staged_n = n_tile;
+      }
       if (!p.tma_store) {
         // OC not a multiple of 32: per-element stores (small odd shapes)
         const float* bias = static_cast<const float*>(p.epi.bias);
@@ -322,19 +380,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
 }
 
-}  // namespace
-
-int conv_f32tc_smem_bytes(int bn, int swz) {
-  if (swz == 128) return bn == 64 ? F32tcCfg<64, 128, 2>::kSmem : F32tcCfg<128, 128, 2>::kSmem;
-  return bn == 64 ? F32tcCfg<64, 32, 8>::kSmem : F32tcCfg<128, 32, 6>::kSmem;
-}
-
-template <int BN, int SWZ, int STAGES, int PROG>
-static int launch_f32tc_inst(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
-                             const CUtensorMap& tm_y, const ConvGemmParams& p, int grid,
-                             cudaStream_t stream) {
-  using Cfg = F32tcCfg<BN, SWZ, STAGES>;
-  auto kfn = conv_f32tc_kernel<BN, SWZ, STAGES, PROG>;
+template <int BN, int SWZ, int STAGES, bool INTER, int PROG>
+int launch_f32tc_inst(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
+                      const ConvGemmParams& p, int grid, cudaStream_t stream) {
+  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER>;
+  auto kfn = conv_f32tc_kernel<BN, SWZ, STAGES, INTER, PROG>;
   cudaError_t e =
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
   if (e != cudaSuccess) return e;
@@ -343,27 +393,54 @@ static int launch_f32tc_inst(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
   return cudaGetLastError();
 }
 
-template <int BN, int SWZ, int STAGES>
-static int launch_f32tc_prog(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
-                             const CUtensorMap& tm_y, const ConvGemmParams& p, int prog,
-                             int grid, cudaStream_t st) {
+template <int BN, int SWZ, int STAGES, bool INTER>
+int launch_f32tc_prog(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
+                      const ConvGemmParams& p, int prog, int grid, cudaStream_t st) {
   switch (prog) {
-    case epi::kProgNone: return launch_f32tc_inst<BN, SWZ, STAGES, epi::kProgNone>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBias: return launch_f32tc_inst<BN, SWZ, STAGES, epi::kProgBias>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBiasRelu: return launch_f32tc_inst<BN, SWZ, STAGES, epi::kProgBiasRelu>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBiasAddRelu: return launch_f32tc_inst<BN, SWZ, STAGES, epi::kProgBiasAddRelu>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgNone: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgNone>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBias: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgBias>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBiasRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgBiasRelu>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBiasAddRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgBiasAddRelu>(tm_a, tm_b, tm_y, p, grid, st);
     default: return -1;
   }
 }
 
+// The instantiated (BN, block, stages, interleaved) set.
+#define TEC_F32TC_INSTANCES(X) \
+  X(64, 128, 2, false)         \
+  X(128, 128, 2, false)        \
+  X(64, 32, 8, false)          \
+  X(128, 32, 6, false)         \
+  X(64, 128, 6, true)          \
+  X(128, 128, 5, true)
+
+}  // namespace
+
+int conv_f32tc_smem_bytes(int bn, int swz, bool inter) {
+#define TEC_X(BN, SW, ST, IN) \
+  if (bn == BN && swz == SW && inter == IN) return F32tcCfg<BN, SW, ST, IN>::kSmem;
+  TEC_F32TC_INSTANCES(TEC_X)
+#undef TEC_X
+  return -1;
+}
+
+int conv_f32tc_stages(int bn, int swz, bool inter) {
+#define TEC_X(BN, SW, ST, IN) \
+  if (bn == BN && swz == SW && inter == IN) return ST;
+  TEC_F32TC_INSTANCES(TEC_X)
+#undef TEC_X
+  return -1;
+}
+
 // Returns a cudaError_t, or -1 for an unsupported (bn, swz, program).
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
-                      const ConvGemmParams& p, int bn, int swz, int prog, int grid,
+                      const ConvGemmParams& p, int bn, int swz, bool inter, int prog, int grid,
                       cudaStream_t st) {
-  if (swz == 128 && bn == 64) return launch_f32tc_prog<64, 128, 2>(tm_a, tm_b, tm_y, p, prog, grid, st);
-  if (swz == 128 && bn == 128) return launch_f32tc_prog<128, 128, 2>(tm_a, tm_b, tm_y, p, prog, grid, st);
-  if (swz == 32 && bn == 64) return launch_f32tc_prog<64, 32, 8>(tm_a, tm_b, tm_y, p, prog, grid, st);
-  if (swz == 32 && bn == 128) return launch_f32tc_prog<128, 32, 6>(tm_a, tm_b, tm_y, p, prog, grid, st);
+#define TEC_X(BN, SW, ST, IN)   \
+  if (bn == BN && swz == SW && inter == IN) \
+    return launch_f32tc_prog<BN, SW, ST, IN>(tm_a, tm_b, tm_y, p, prog, grid, st);
+  TEC_F32TC_INSTANCES(TEC_X)
+#undef TEC_X
   return -1;
 }
 

@@ -57,6 +57,7 @@ struct ConvGemmParams {
   int32_t nacc;         // TMEM accumulator buffers: 2 or 4 (when 4 fit in 512 columns)
   float* ws;            // [m_tiles*n_tiles][splits][128][BN]
   int32_t* tile_cnt;    // [m_tiles*n_tiles], zero between launches
+  int32_t chunk_iters;  // f32tc: k-iterations per hh promotion chunk
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA

@@ -35,7 +35,16 @@ enum PackMode : int32_t {
   kPackI8 = 2,      // int8 copy
   kPackF32 = 3,     // f32 copy
   kPackI32 = 4,     // i32 copy
+  kPackSplit3I = 5, // split3 interleaved: [h16 | m16 | l16 | 0] per 64-channel pixel
 };
+
+// Channels per plane of the split layouts (cp = stored channels per pixel).
+__host__ __device__ __forceinline__ int64_t plane_channels(int mode, int64_t cp) {
+  return mode == kPackSplit3I ? 16 : mode == kPackSplit3 ? cp / 3 : cp;
+}
+__host__ __device__ __forceinline__ bool split_mode(int mode) {
+  return mode == kPackSplit3 || mode == kPackSplit3I;
+}
 
 // in: [n][c][hw] (f32, or i8 / i32), out: [n][hw][cp] with cp >= c (Split3:
 // three bf16 planes of cp/3 channels), padded channels zero-filled.
@@ -55,7 +64,7 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
     tile[i][tx] = v;
   }
   __syncthreads();
-  const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
+  const int64_t cpp = plane_channels(mode, cp);  // channels per plane
   for (int i = ty; i < 32; i += 8) {
     const int64_t pp = p0 + i, cc = c0 + tx;
     if (pp >= hw) continue;
@@ -66,7 +75,8 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
         case kPackBF16:
           static_cast<__nv_bfloat16*>(out)[obase + cc] = __float2bfloat16_rn(v);
           break;
-        case kPackSplit3: {
+        case kPackSplit3:
+        case kPackSplit3I: {
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out);
 #pragma unroll
           for (int pl = 0; pl < 3; ++pl) o[obase + pl * cpp + cc] = split3(v, pl);
@@ -91,6 +101,7 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
             static_cast<__nv_bfloat16*>(out)[obase + z] = __float2bfloat16_rn(0.f);
             break;
           case kPackSplit3:
+          case kPackSplit3I:
 #pragma unroll
             for (int pl = 0; pl < 3; ++pl)
               static_cast<__nv_bfloat16*>(out)[obase + pl * cpp + z] = __float2bfloat16_rn(0.f);
@@ -106,6 +117,9 @@ __global__ void pack_nchw_to_nhwc_kernel(const InT* __restrict__ in,
             break;
         }
       }
+      if (mode == kPackSplit3I)  // the 4th (zero) slice of an interleaved pixel
+        for (int64_t z = 3 * cpp + tx; z < cp; z += 32)
+          static_cast<__nv_bfloat16*>(out)[obase + z] = __float2bfloat16_rn(0.f);
     }
   }
 }
@@ -153,15 +167,16 @@ __global__ void pack_weights_krsc_kernel(const InT* __restrict__ w,
     t /= s;
     const int64_t rr = t % r;
     const int64_t kk = t / r;
-    const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
+    const int64_t cpp = plane_channels(mode, cp);  // channels per plane
     const int64_t src_c = ci % cpp, plane = ci / cpp;
     float v = 0.f;
-    if (src_c < c) v = static_cast<float>(w[((kk * c + src_c) * r + rr) * s + ss]);
+    if (src_c < c && plane < 3) v = static_cast<float>(w[((kk * c + src_c) * r + rr) * s + ss]);
     switch (mode) {
       case kPackBF16:
         static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
         break;
       case kPackSplit3:
+      case kPackSplit3I:
         static_cast<__nv_bfloat16*>(out)[i] = split3(v, static_cast<int>(plane));
         break;
       case kPackF32:
@@ -212,7 +227,7 @@ __global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ o
                                 int64_t n, int64_t c, int64_t h, int64_t w, int64_t ph,
                                 int64_t pw, int64_t h2, int64_t w2, int64_t cp, int mode) {
   const int64_t total = n * h2 * w2 * cp;
-  const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
+  const int64_t cpp = plane_channels(mode, cp);  // channels per plane
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t ch = (i % cp) % cpp, plane = (i % cp) / cpp;
@@ -222,7 +237,7 @@ __global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ o
     const int64_t ii = t % h2;
     const int64_t nn = t / h2;
     float v = 0.f;
-    if (ch < 4 * c) {
+    if (ch < 4 * c && plane < 3) {
       const int64_t q = ch / c, cc = ch % c;
       const int64_t y = 2 * ii + q / 2 - ph, x = 2 * jj + q % 2 - pw;
       if (y >= 0 && y < h && x >= 0 && x < w)
@@ -230,7 +245,7 @@ __global__ void pack_s2d_kernel(const InT* __restrict__ in, void* __restrict__ o
     }
     if (mode == kPackBF16)
       static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
-    else if (mode == kPackSplit3)
+    else if (split_mode(mode))
       static_cast<__nv_bfloat16*>(out)[i] = split3(v, static_cast<int>(plane));
     else
       static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);
@@ -359,7 +374,7 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
                                         int64_t k, int64_t c, int64_t r, int64_t s, int64_t r2,
                                         int64_t s2, int64_t cp, int mode) {
   const int64_t total = k * r2 * s2 * cp;
-  const int64_t cpp = mode == kPackSplit3 ? cp / 3 : cp;  // channels per plane
+  const int64_t cpp = plane_channels(mode, cp);  // channels per plane
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t ch = (i % cp) % cpp, plane = (i % cp) / cpp;
@@ -369,14 +384,14 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
     const int64_t ri = t % r2;
     const int64_t kk = t / r2;
     float v = 0.f;
-    if (ch < 4 * c) {
+    if (ch < 4 * c && plane < 3) {
       const int64_t q = ch / c, cc = ch % c;
       const int64_t rr = 2 * ri + q / 2, ss = 2 * sj + q % 2;
       if (rr < r && ss < s) v = static_cast<float>(w[((kk * c + cc) * r + rr) * s + ss]);
     }
     if (mode == kPackBF16)
       static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
-    else if (mode == kPackSplit3)
+    else if (split_mode(mode))
       static_cast<__nv_bfloat16*>(out)[i] = split3(v, static_cast<int>(plane));
     else
       static_cast<int8_t*>(out)[i] = static_cast<int8_t>(v);

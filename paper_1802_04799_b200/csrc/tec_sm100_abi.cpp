@@ -61,9 +61,10 @@ int launch_pool_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwT
                     int sms, cudaStream_t st);
 int launch_global_avg_pool(const PoolParams& p, cudaStream_t st);
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
-                      const ConvGemmParams& p, int bn, int swz, int prog, int grid,
+                      const ConvGemmParams& p, int bn, int swz, bool inter, int prog, int grid,
                       cudaStream_t st);
-int conv_f32tc_smem_bytes(int bn, int swz);
+int conv_f32tc_smem_bytes(int bn, int swz, bool inter);
+int conv_f32tc_stages(int bn, int swz, bool inter);
 }  // namespace tec_sm100
 
 using namespace tec_sm100;
@@ -199,7 +200,8 @@ int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 struct Plan {
   int64_t oh, ow, m;
   int64_t cp;       // stored channels of the packed activation (all planes)
-  int64_t cpp = 0;  // channels per plane (F32TC: cp = 3 * cpp; else cp)
+  int64_t cpp = 0;  // channels per plane (F32TC: cp = 3 * cpp, or 64 interleaved)
+  bool inter = false;  // F32TC with <= 16 channels per plane: [h16|m16|l16|0] pixels
   int32_t act;      // packed element type (tec_dtype)
   int32_t acc;      // accumulator type
   int pack_mode;    // layout.cu PackMode
@@ -261,12 +263,14 @@ tec_status make_plan(const tec_conv_desc* d, Plan* p) {
         p->pack_mode = 3;
         p->cp = d->c;
       } else {
-        // three exact bf16 planes [h | m | l] (conv_f32tc.cu)
+        // three exact bf16 planes [h | m | l] (conv_f32tc.cu); <= 16
+        // channels per plane: interleaved in one 64-channel pixel
         p->act = TEC_DT_BF16;
-        p->pack_mode = 1;
         p->cpp = round_up(d->c, 16);
-        p->cp = 3 * p->cpp;
-        p->swz = p->cpp % 64 == 0 ? 128 : 32;
+        p->inter = p->cpp == 16;
+        p->pack_mode = p->inter ? 5 : 1;
+        p->cp = p->inter ? 64 : 3 * p->cpp;
+        p->swz = p->inter || p->cpp % 64 == 0 ? 128 : 32;
       }
       break;
     case TEC_COMPUTE_F32:
@@ -305,8 +309,15 @@ tec_status make_plan(const tec_conv_desc* d, Plan* p) {
       p->s2d = true;
       p->h2 = h2; p->w2 = w2; p->r2 = r2; p->s2 = s2;
       p->cpp = s2d_c;
-      p->cp = d->compute == TEC_COMPUTE_F32TC ? 3 * s2d_c : s2d_c;
       p->swz = 32;
+      if (d->compute == TEC_COMPUTE_F32TC) {  // interleaved planes
+        p->inter = true;
+        p->pack_mode = 5;
+        p->cp = 64;
+        p->swz = 128;
+      } else {
+        p->cp = s2d_c;
+      }
     }
   }
   return TEC_OK;
@@ -656,12 +667,16 @@ bool fast_program(const EpilogueParams& e) {
   return e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu;
 }
 
-// Split-K scratch layout: [f32 partial tiles][per-tile arrival counters],
-// the counters zero before the first launch (every launch leaves them zero:
-// the last split of a tile resets its counter).
-size_t splitk_partials_bytes(size_t partial_bytes) { return (partial_bytes + 255) & ~size_t(255); }
-size_t splitk_bytes(size_t partial_bytes, size_t tiles) {
-  return splitk_partials_bytes(partial_bytes) + tiles * sizeof(int32_t);
+// Split-K scratch layout: [per-tile arrival counters: a FIXED kSplitKTiles
+// slots][f32 partial tiles]. The counters are zero before the first launch
+// and every launch leaves them zero (the last split of a tile resets its
+// counter); because their region has the same size for every shape, one
+// scratch can serve launches of different shapes (a plan's steps, the
+// per-stream pool) without a counter ever landing on stale partial sums.
+constexpr size_t kSplitKTiles = 1 << 16;
+constexpr size_t kSplitKCounterBytes = kSplitKTiles * sizeof(int32_t);
+size_t splitk_bytes(size_t partial_bytes, size_t /*tiles*/) {
+  return kSplitKCounterBytes + ((partial_bytes + 255) & ~size_t(255));
 }
 
 // The scratch a split-K launch uses: the caller's (tec_conv2d_fused_ws /
@@ -671,6 +686,8 @@ size_t splitk_bytes(size_t partial_bytes, size_t tiles) {
 // Growing is a synchronous allocation, refused during stream capture.
 tec_status splitk_workspace(int dev, size_t partial_bytes, size_t tiles, cudaStream_t st,
                             float** ws, int32_t** cnt) {
+  if (tiles > kSplitKTiles)
+    return fail(TEC_E_LOWERING, "split-K over more than 65536 output tiles");
   const size_t need = splitk_bytes(partial_bytes, tiles);
   uint8_t* base = nullptr;
   if (g_ws) {
@@ -700,8 +717,8 @@ tec_status splitk_workspace(int dev, size_t partial_bytes, size_t tiles, cudaStr
     }
     base = static_cast<uint8_t*>(pool.p);
   }
-  *ws = reinterpret_cast<float*>(base);
-  *cnt = reinterpret_cast<int32_t*>(base + splitk_partials_bytes(partial_bytes));
+  *cnt = reinterpret_cast<int32_t*>(base);
+  *ws = reinterpret_cast<float*>(base + kSplitKCounterBytes);
   return TEC_OK;
 }
 
@@ -907,10 +924,11 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
            epi.ops[2] == kEpiRelu) prog = 4;
   else return fail(TEC_E_LOWERING, "f32tc: fused program not supported (compute f32 runs it)");
   if (kn && kn->tile_m && kn->tile_m != 128) return fail(TEC_E_LOWERING, "tile_m must be 128 (tcgen05 M)");
-  if (kn && (kn->split_k > 1 || kn->cluster_n > 1 || (kn->tile_k && kn->tile_k != 1)))
-    return fail(TEC_E_LOWERING, "f32tc: im2col kernel only (no split_k / cluster / halo knobs)");
+  if (kn && (kn->cluster_n > 1 || (kn->tile_k && kn->tile_k != 1)))
+    return fail(TEC_E_LOWERING, "f32tc: im2col kernel only (no cluster / halo knobs)");
   const int swz = pl.swz;
-  const int cb = swz / 2;
+  const bool inter = pl.inter;
+  const int cb = inter ? 16 : swz / 2;  // channels per plane per k-iteration
   if (pl.cpp % cb) return fail(TEC_E_INTERNAL, "channel padding does not match block");
   int dev = 0;
   cudaGetDevice(&dev);
@@ -934,7 +952,7 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
         d->stride_w > 8 || d->stride_h > 8)
       return fail(TEC_E_LOWERING, "window outside the TMA im2col range");
     CUresult r = fns.im2col(&tm_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x),
-                            dims, strides, lower, upper, (cuuint32_t)cb, 128, estr,
+                            dims, strides, lower, upper, (cuuint32_t)(swz / 2), 128, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(swz),
                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
@@ -947,7 +965,7 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     const int64_t ktot = d->r * d->s * pl.cp;
     cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)d->k};
     cuuint64_t strides[1] = {(cuuint64_t)(ktot * 2)};
-    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)bn};
+    cuuint32_t box[2] = {(cuuint32_t)(swz / 2), (cuuint32_t)bn};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fns.tiled(&tm_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(swz),
@@ -977,21 +995,46 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   p.y = y;
   p.epi = epi;
   p.tma_store = tma_ok ? 1 : 0;
-  p.splits = 1;
   // hh promotion chunk: 256 K elements per plane (TEC_SM100_F32TC_CHUNK
   // overrides, for the accuracy experiments only)
   static const int chunk_k = [] {
     const char* e = std::getenv("TEC_SM100_F32TC_CHUNK");
     return e ? std::max(16, std::atoi(e)) : 256;
   }();
-  p.kps = std::max(1, chunk_k / cb);
+  p.chunk_iters = std::max(1, chunk_k / cb);
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
-  int grid = (int)std::min<int64_t>(tiles, sms);
+  const int k_iters = (int)(d->r * d->s * p.cblocks);
+  // Split-K (knob split_k; 0 = auto): for outputs with few tiles, pick the
+  // split count with the smallest makespan waves x (k-iterations per split +
+  // ~2 k-iterations of partial write/read per item).
+  int splits = kn && kn->split_k > 0 ? (int)kn->split_k : 0;
+  if (!splits) {
+    double best = 1e30;
+    for (int sp : {1, 2, 3, 4, 6, 8}) {
+      if (sp > 1 && k_iters / sp < 4) break;
+      const int64_t waves = (tiles * sp + sms - 1) / sms;
+      const double cost = (double)waves * ((k_iters + sp - 1) / sp + (sp > 1 ? 2 : 0));
+      if (cost < best - 1e-9) { best = cost; splits = sp; }
+    }
+  }
+  splits = std::max(1, std::min(splits, k_iters));
+  p.splits = splits;
+  p.kps = (k_iters + splits - 1) / splits;
+  p.splits = (k_iters + p.kps - 1) / p.kps;  // no empty split
+  const size_t partials = (size_t)tiles * p.splits * 128 * bn * sizeof(float);
+  if (g_plan) g_plan->workspace_bytes = p.splits > 1 ? (int64_t)splitk_bytes(partials, tiles) : 0;
+  int grid = (int)std::min<int64_t>(tiles * p.splits, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
-  if (plan_only(TEC_KERNEL_F32TC, bn, 128, swz == 128 ? 2 : (bn == 64 ? 8 : 6), grid,
-                conv_f32tc_smem_bytes(bn, swz), 4 * bn <= 256 ? 256 : 512, p.tma_store, 1, 1))
+  const int stages = conv_f32tc_stages(bn, swz, inter);
+  if (stages < 0) return fail(TEC_E_LOWERING, "f32tc: no instance for this tile / block");
+  if (plan_only(TEC_KERNEL_F32TC, bn, 128, stages, grid, conv_f32tc_smem_bytes(bn, swz, inter),
+                4 * bn <= 256 ? 256 : 512, p.tma_store, p.splits, 1))
     return TEC_OK;
-  const int e = launch_conv_f32tc(tm_a, tm_b, tm_y, p, bn, swz, prog, grid, st);
+  if (p.splits > 1) {
+    tec_status wst = splitk_workspace(dev, partials, (size_t)tiles, st, &p.ws, &p.tile_cnt);
+    if (wst) return wst;
+  }
+  const int e = launch_conv_f32tc(tm_a, tm_b, tm_y, p, bn, swz, inter, prog, grid, st);
   if (e == -1) return fail(TEC_E_LOWERING, "f32tc: no instance for this tile / block");
   if (e) return cuda_fail(e, "conv_f32tc launch");
   return TEC_OK;

@@ -397,3 +397,21 @@ def test_f32tc_tiles_and_unsupported_program(tile_n):
     with pytest.raises(TecError) as ei:
         fused_conv("conv2d", x, w, attrs, [("scale", 2.0)], compute="f32tc")
     assert ei.value.code == "LoweringError"
+
+
+def test_split_k_scratch_shared_across_shapes():
+    """One split-K scratch (the per-stream pool here, a plan's buffer in the
+    executor) serves launches of different shapes back to back: the tile
+    counters live in a fixed region, so a launch never counts on another
+    shape's stale partial sums (regression: f32tc C9 then C12 then C7)."""
+    for layer, sk in (("C9", 3), ("C12", 4), ("C7", 2), ("C12", 3), ("C9", 2)):
+        hw, c, k, r, s = RESNET18_CONVS[layer]
+        x, w, b = _inputs((1, c, hw, hw), (k, c, r, r), k, False, seed=sk)
+        attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+        epi = [("bias_add", b), ("relu",)]
+        for compute, tol in (("f32tc", TOL_F32TC), ("bf16", TOL_BF16)):
+            kn = {"split_k": sk} if compute == "f32tc" else {"split_k": sk, "tile_k": 1}
+            y = fused_conv("conv2d", x, w, attrs, epi, compute=compute, knobs=kn)
+            xr, wr = (bf16_round(x), bf16_round(w)) if compute == "bf16" else (x, w)
+            want = oracle_conv("conv2d", xr, wr, (s, s), (r // 2, r // 2), epi)
+            assert same_values(y, want, tol), (layer, sk, compute, max_rel_err(y, want))
