@@ -21,6 +21,10 @@
 //   gen   <out_dir> <name> <dtype> <seed> <d0> [d1 ...]
 //         random_tensor (R/src/tensor.cpp:74) with mt19937_64(seed), saved
 //         with save_tensor -- the reference's own synthetic distributions.
+//   gbt   <in.json> <out.json>
+//         CostModel::train / predict / pairwise_rank_accuracy
+//         (R/src/gbt.cpp:119-246) on {"feats", "costs", "query", "params"};
+//         writes {"pred", "acc", "model"} -- pins the tuner's restatement.
 //   bench <op> <C> <H> <W> <OC> <K> <stride> <pad> <rows> <seed> [dtype]
 //         times eval_graph_node (R/src/graph.cpp:209) on the fused node
 //         [conv2d|depthwise_conv2d, bias_add, relu] built exactly as
@@ -33,6 +37,7 @@
 #include <string>
 #include <vector>
 
+#include "tec/autotune.hpp"
 #include "tec/graph.hpp"
 #include "tec/graph_passes.hpp"
 #include "tec/io.hpp"
@@ -80,6 +85,31 @@ static int cmd_layouts(const std::string& gpath, const std::string& ppath,
   std::map<std::string, std::string> prefs;
   for (auto it = pj.begin(); it != pj.end(); ++it) prefs[it.key()] = it.value().get<std::string>();
   write_text_file(out_path, graph_to_json(apply_layouts(g, prefs)).dump(1) + "\n");
+  return 0;
+}
+
+static int cmd_gbt(const std::string& in_path, const std::string& out_path) {
+  nlohmann::json j = parse_json(read_text_file(in_path), in_path);
+  GbtParams prm;
+  if (j.contains("params")) {
+    const auto& p = j["params"];
+    prm.max_depth = p.value("max_depth", prm.max_depth);
+    prm.rounds = p.value("rounds", prm.rounds);
+    prm.learning_rate = p.value("learning_rate", prm.learning_rate);
+    prm.reg_lambda = p.value("reg_lambda", prm.reg_lambda);
+  }
+  std::vector<FeatureVector> feats;
+  for (const auto& r : j.at("feats")) feats.push_back(r.get<std::vector<double>>());
+  std::vector<double> costs = j.at("costs").get<std::vector<double>>();
+  CostModel m(prm);
+  m.train(feats, costs);
+  nlohmann::json out;
+  std::vector<double> pred;
+  for (const auto& r : j.at("query")) pred.push_back(m.predict(r.get<std::vector<double>>()));
+  out["pred"] = pred;
+  out["acc"] = pairwise_rank_accuracy(m, feats, costs);
+  out["model"] = m.to_json();
+  write_text_file(out_path, out.dump(1) + "\n");
   return 0;
 }
 
@@ -151,6 +181,7 @@ int main(int argc, char** argv) {
     if (cmd == "fold" && argc == 4) return cmd_fold(argv[2], argv[3]);
     if (cmd == "layouts" && argc == 5) return cmd_layouts(argv[2], argv[3], argv[4]);
     if (cmd == "gen" && argc >= 7) return cmd_gen(argc, argv);
+    if (cmd == "gbt" && argc == 4) return cmd_gbt(argv[2], argv[3]);
     if (cmd == "bench" && argc >= 12) return cmd_bench(argc, argv);
     std::fprintf(stderr, "bad arguments for '%s'\n", cmd.c_str());
     return 2;

@@ -146,8 +146,8 @@ def test_schedule_log_round_trip():
     from paper_1802_04799_b200.tuner import config_from_schedule_log, conv_space, schedule_log
     from paper_1802_04799_b200.workloads import resnet_layer
     s = conv_space("C6", make_desc(resnet_layer("C6", 1)))
-    for i in range(0, s.size(), 7):
-        cfg = s.config_at(i)
+    for i in range(0, s.grid_size(), 7):  # the whole grid: no lowering needed
+        cfg = s.grid_at(i)
         log = schedule_log(cfg, s.desc)
         json.dumps(log)
         back = config_from_schedule_log(log)
