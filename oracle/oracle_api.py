@@ -166,6 +166,14 @@ def load_tensor(d: str, name: str) -> np.ndarray:
     return raw.reshape(m["shape"])
 
 
+def save_tensor(d: str, name: str, a: np.ndarray) -> None:
+    """save_tensor (R/src/io.cpp:111-119): raw row-major bytes + a JSON header."""
+    dt = {np.dtype(np.float32): "f32", np.dtype(np.int32): "i32", np.dtype(np.int8): "i8"}[a.dtype]
+    np.ascontiguousarray(a).tofile(os.path.join(d, name + ".bin"))
+    with open(os.path.join(d, name + ".json"), "w") as f:
+        json.dump({"dtype": dt, "name": name, "shape": list(a.shape)}, f)
+
+
 def bf16_round(a: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even onto bf16, returned as f32 (what the bf16 path
     feeds the tensor cores)."""
