@@ -294,7 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 32; ++j) sum[c0 + j] = __fadd_rn(sum[c0 + j], __uint_as_float(v[j]));
       }
       tc_fence_before();
-      mbar_arrive(&tempty[tb]);
+      // p.fault == 1 (tests only): lose one arrive -- the MMA warp then waits
+      // for this accumulator forever and the mbarrier watchdog must trap
+      if (!(p.fault == 1 && local == 0)) mbar_arrive(&tempty[tb]);
       if (splits > 1) {
         // publish this split's partial ([item][warp][column][lane]: one
         // 128-B line per column); the last split of the tile sums them all

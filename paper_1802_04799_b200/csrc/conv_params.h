@@ -58,6 +58,8 @@ struct ConvGemmParams {
   float* ws;            // [m_tiles*n_tiles][splits][128][BN]
   int32_t* tile_cnt;    // [m_tiles*n_tiles], zero between launches
   int32_t chunk_iters;  // f32tc: k-iterations per hh promotion chunk
+  int32_t fault;        // test-only fault injection (TEC_SM100_FAULT): 1 = the
+                        // epilogue drops its first accumulator-free arrive
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA

@@ -63,12 +63,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Blocking wait with a watchdog: a pipeline bug (lost arrive, bad tx count)
-// traps the kernel after seconds instead of hanging the GPU.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Blocking wait with a watchdog on the GLOBAL TIMER: a pipeline bug (lost
+// arrive, bad tx count) traps the kernel after kWatchdogNs instead of hanging
+// the GPU. (A spin count is no bound: each try_wait may suspend up to its
+// 1 ms hint.) The clock is read only once a wait has spun a while, so the
+// fast path costs nothing.
+constexpr uint64_t kWatchdogNs = 10ull * 1000 * 1000 * 1000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins == (1u << 22)) __trap();
+    if (++spins == 16) {
+      t0 = global_ns();
+    } else if (spins > 16 && (spins & 15) == 0 && global_ns() - t0 > kWatchdogNs) {
+      __trap();
+    }
   }
 }
 

@@ -1002,6 +1002,11 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     return e ? std::max(16, std::atoi(e)) : 256;
   }();
   p.chunk_iters = std::max(1, chunk_k / cb);
+  static const int fault = [] {  // test-only: the watchdog mutation test
+    const char* e = std::getenv("TEC_SM100_FAULT");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.fault = fault;
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
   const int k_iters = (int)(d->r * d->s * p.cblocks);
   // Split-K (knob split_k; 0 = auto): for outputs with few tiles, pick the
