@@ -214,7 +214,8 @@ typedef enum {
   TEC_KERNEL_F32_EXACT = 3,  /* conv_f32_exact.cu: SIMT, reference order  */
   TEC_KERNEL_DW_TMA = 4,     /* depthwise_tma.cu                           */
   TEC_KERNEL_DW_DIRECT = 5,  /* depthwise.cu                               */
-  TEC_KERNEL_F32TC = 6       /* conv_f32tc.cu: split-bf16 f32 on tcgen05    */
+  TEC_KERNEL_F32TC = 6,      /* conv_f32tc.cu: split-bf16 f32 on tcgen05    */
+  TEC_KERNEL_F32TC_HALO = 7  /* conv_f32tc.cu, shifted-window (stride 1)    */
 } tec_kernel_family;
 
 typedef struct {

@@ -65,43 +65,76 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 
-template <int BN, int SWZ, int STAGES, bool INTER>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES = false, bool HALO = false>
 struct F32tcCfg {
-  static constexpr int kPlanes = INTER ? 1 : 3;  // TMA boxes per operand per k-iteration
-  static constexpr int kA = kBM * SWZ;           // one box of A
-  static constexpr int kB = BN * SWZ;            // one box of B
-  static constexpr int kStage = kPlanes * (kA + kB);
+  static constexpr int kAPlanes = INTER ? 1 : 3;  // A boxes per k-iteration
+  static constexpr int kA = kBM * SWZ;            // one A box
+  // B: three boxes of BN rows (one per plane), or -- interleaved -- one 3-D
+  // box [plane][BN rows][16 ch] with the 32-B swizzle. Either way the planes
+  // are consecutive row blocks: [B_h; B_m; B_l] is one N-concatenated operand.
+  static constexpr int kBSW = INTER ? 32 : SWZ;      // B row bytes / swizzle
+  static constexpr int kBPlane = BN * kBSW;          // bytes per B plane
+  static constexpr int kBBoxes = INTER ? 1 : 3;
+  static constexpr int kBBox = INTER ? 3 * kBPlane : kBPlane;
+  static constexpr int kBStage = 3 * kBPlane;       // B bytes per k-iteration
+  // RES: every k-iteration's B tile of the CTA's output-channel tile stays
+  // in shared memory (loaded once per CTA, p.res_bytes); the ring carries A only
+  // HALO: A lives in the halo buffers (runtime-sized), the ring carries B
+  static constexpr int kStage = (HALO ? 0 : kAPlanes * kA) + (RES ? 0 : kBStage);
   static constexpr int kKSteps = INTER ? 1 : SWZ / 32;  // K16 steps per plane per stage
-  static constexpr uint32_t kTmemCols = 4 * BN <= 256 ? 256 : 512;
+  // GRP (BN = 64): the products sharing an operand run as ONE MMA on the
+  // N-concatenated planes -- A_h x [B_h|B_m|B_l] (N=192), A_m x [B_h|B_m]
+  // (N=128), A_l x B_h (N=64): 3 MMAs instead of 6 N=64 ones, whose rate is
+  // bound by re-reading A from shared memory (54 vs 32 cycles each,
+  // tools/microbench/RESULTS.md). TMEM: chunk ring X 2 x 192 (hh|hm|hl) +
+  // one tile accumulator Y 128 (mh+lh | mm) = 512 columns. (Measured: C2 b64
+  // 98 -> 86 us; a 4-MMA form with a double-buffered Y -- X = A_h x
+  // [B_h|B_m], A_h x B_l into Y -- was slower, C1 197 vs 169 us.)
+  // Otherwise (BN = 128): six N=128 MMAs; chunk ring S 2 x BN + tile
+  // accumulators T 2 x BN.
+  static constexpr bool kGrp = BN == 64;
+  static constexpr int kXCols = kGrp ? 3 * BN : BN;     // chunk accumulator width
+  static constexpr int kYCols = kGrp ? 2 * BN : BN;     // tile accumulator width
+  static constexpr int kYBufs = kGrp ? 1 : 2;
+  static constexpr int kYBase = 2 * kXCols;
+  static constexpr uint32_t kTmemCols = 2 * kXCols + kYBufs * kYCols <= 256 ? 256 : 512;
+  // + res_bytes (RES) + hbuf x kAPlanes x halo_bytes (HALO)
   static constexpr int kSmem = 1024 + STAGES * kStage + 8 * 4096 + 256 + BN * 4;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
-  static_assert(4 * BN <= 512, "TMEM budget");
+  static_assert(2 * kXCols + kYBufs * kYCols <= 512, "TMEM budget");
   static_assert(!INTER || SWZ == 128, "interleaved planes live in one 128-B row");
 };
 
-template <int BN, int SWZ, int STAGES, bool INTER, int PROG>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_f32tc_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvGemmParams p) {
-  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER>;
+  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER, RES, HALO>;
   constexpr int kCB = SWZ / 2;  // bf16 channels per box row
   constexpr int HB = BN / 2;    // columns per epilogue warp
-  // byte offset of plane q inside an operand stage: its own box, or its
-  // K16 slice of the interleaved row
+  constexpr int kBSW = Cfg::kBSW;
+  // byte offset of A plane q inside a stage: its own box, or its K16 slice
+  // of the interleaved row
   constexpr int kPlaneA = INTER ? 32 : Cfg::kA;
-  constexpr int kPlaneB = INTER ? 32 : Cfg::kB;
+  constexpr int kPlaneB = Cfg::kBPlane;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sStage = smem + STAGES * Cfg::kStage;  // 8 warps x 4 KB
+  uint8_t* sHalo = smem;  // HALO: hbuf x kAPlanes halo buffers of halo_bytes
+  uint8_t* sRing = sHalo + (HALO ? p.hbuf * Cfg::kAPlanes * p.halo_bytes : 0);
+  uint8_t* sRes = sRing + STAGES * Cfg::kStage;  // RES: resident B, k_iters x kBStage
+  uint8_t* sStage = sRes + (RES ? p.res_bytes : 0);  // 8 warps x 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 8 * 4096);
   uint64_t* empty = full + STAGES;
   uint64_t* sfull = empty + STAGES;
   uint64_t* sempty = sfull + 2;
   uint64_t* tfull = sempty + 2;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wfull = tempty + 2;  // RES: the resident B tiles landed
+  uint64_t* hfull = wfull + 1;   // HALO: halo buffer landed / free
+  uint64_t* hempty = hfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
   uint32_t* sBias = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
 
@@ -129,6 +162,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 256);
     }
+    mbar_init(wfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hfull[i], 1);
+      mbar_init(&hempty[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -138,14 +176,90 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+  if (warp == 0 || (warp == 3 && p.producers == 2)) {
+    // ------------------------------------------------ TMA producers
+    // warp 0 issues the activation boxes (and arms the stage's transaction
+    // count); with two producers warp 3 issues the weight boxes of the same
+    // stage, so the two TMA streams are not serialised behind one thread
+    const bool issue_a = warp == 0;
+    const bool issue_b = warp == 3 || p.producers != 2;
     if (elect_one()) {
+      const int sc = p.s * p.cblocks;
+      if (RES && issue_b && static_cast<int>(blockIdx.x) < num_items) {
+        // the CTA's output-channel tile is fixed (grid % n_tiles == 0, no
+        // split): its B tiles for all k-iterations, once -- parameters, so
+        // before the wait on the previous layer
+        const int n_tile = static_cast<int>(blockIdx.x) % p.n_tiles;
+        mbar_arrive_expect_tx(wfull, static_cast<uint32_t>(k_iters * Cfg::kBStage));
+        int r = 0, s = 0, cb = 0;
+        for (int k = 0; k < k_iters; ++k) {
+          uint8_t* bb = sRes + k * Cfg::kBStage;
+          if constexpr (INTER) {
+            tma_load_3d(bb, &tm_b, wfull, 0, n_tile * BN, 3 * (r * p.s + s));
+          } else {
+            const int wcol = (r * p.s + s) * pix + cb * kCB;
+#pragma unroll
+            for (int pl = 0; pl < 3; ++pl)
+              tma_load_2d(bb + pl * kPlaneB, &tm_b, wfull, wcol + pl * cpp, n_tile * BN);
+          }
+          if (++cb == p.cblocks) {
+            cb = 0;
+            if (++s == p.s) { s = 0; ++r; }
+          }
+        }
+      }
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       const int ohw = p.oh * p.ow;
-      const int sc = p.s * p.cblocks;
+      if constexpr (HALO) {
+        // per tile and channel block: ONE halo box per plane (the A thread),
+        // then one weight stage per filter tap (the B thread)
+        int hb = 0;
+        uint32_t hphase = 0;
+        for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
+          const int m_tile = item / p.n_tiles;
+          const int n_tile = item - m_tile * p.n_tiles;
+          const int img = m_tile / p.bands;
+          const int oh0 = (m_tile - img * p.bands) * p.th;
+          for (int cb = 0; cb < p.cblocks; ++cb) {
+            if (issue_a) {
+              mbar_wait(&hempty[hb], hphase ^ 1);
+              mbar_arrive_expect_tx(&hfull[hb],
+                                    static_cast<uint32_t>(Cfg::kAPlanes * p.halo_box_bytes));
+#pragma unroll
+              for (int pl = 0; pl < Cfg::kAPlanes; ++pl)
+                tma_load_4d(sHalo + (hb * Cfg::kAPlanes + pl) * p.halo_bytes, &tm_a, &hfull[hb],
+                            pl * cpp + cb * kCB, -p.pw, oh0 - p.ph, img);
+              if (++hb == p.hbuf) {
+                hb = 0;
+                hphase ^= 1;
+              }
+            }
+            if (issue_b && !RES) {
+              for (int r = 0; r < p.r; ++r)
+                for (int s = 0; s < p.s; ++s) {
+                  mbar_wait(&empty[stage], phase ^ 1);
+                  mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
+                  uint8_t* bbase = sRing + stage * Cfg::kStage;
+                  if constexpr (INTER) {
+                    tma_load_3d(bbase, &tm_b, &full[stage], 0, n_tile * BN, 3 * (r * p.s + s));
+                  } else {
+                    const int wcol = (r * p.s + s) * pix + cb * kCB;
+#pragma unroll
+                    for (int pl = 0; pl < 3; ++pl)
+                      tma_load_2d(bbase + pl * kPlaneB, &tm_b, &full[stage], wcol + pl * cpp,
+                                  n_tile * BN);
+                  }
+                  if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                  }
+                }
+            }
+          }
+        }
+      } else
       for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
         const int mn = item / splits;
         const int split = item - mn * splits;
@@ -163,15 +277,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
         for (int k = kb; k < ke; ++k) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
-          uint8_t* base = smem + stage * Cfg::kStage;
-          const int wcol = (r * p.s + s) * pix + cb * kCB;
+          if (issue_a) mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
+          uint8_t* base = sRing + stage * Cfg::kStage;
+          uint8_t* bbase = base + Cfg::kAPlanes * Cfg::kA;
 #pragma unroll
-          for (int pl = 0; pl < Cfg::kPlanes; ++pl) {
-            tma_load_im2col_4d(base + pl * Cfg::kA, &tm_a, &full[stage], pl * cpp + cb * kCB, w0,
-                               h0, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-            tma_load_2d(base + Cfg::kPlanes * Cfg::kA + pl * Cfg::kB, &tm_b, &full[stage],
-                        wcol + pl * cpp, n_tile * BN);
+          for (int pl = 0; pl < Cfg::kAPlanes; ++pl)
+            if (issue_a)
+              tma_load_im2col_4d(base + pl * Cfg::kA, &tm_a, &full[stage], pl * cpp + cb * kCB,
+                                 w0, h0, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+          if (issue_b && !RES) {
+            if constexpr (INTER) {
+              tma_load_3d(bbase, &tm_b, &full[stage], 0, n_tile * BN, 3 * (r * p.s + s));
+            } else {
+              const int wcol = (r * p.s + s) * pix + cb * kCB;
+#pragma unroll
+              for (int pl = 0; pl < 3; ++pl)
+                tma_load_2d(bbase + pl * kPlaneB, &tm_b, &full[stage], wcol + pl * cpp,
+                            n_tile * BN);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -188,53 +311,117 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------ single-thread MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc = make_idesc<MmaKind::kF16>(kBM, BN);
+      constexpr uint32_t idesc3 = make_idesc<MmaKind::kF16>(kBM, 3 * BN);
+      constexpr uint32_t idesc2 = make_idesc<MmaKind::kF16>(kBM, 2 * BN);
       int stage = 0;
       uint32_t phase = 0;
       int g = 0;  // hh chunks issued so far (S ring position)
       int local = 0;
-      for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
-        const int tb = local & 1;
-        mbar_wait(&tempty[tb], ((local >> 1) & 1) ^ 1);
+      if (RES) {
+        mbar_wait(wfull, 0);
         tc_fence_after();
-        const uint32_t t_tmem = tmem_base + (2 + tb) * BN;
+      }
+      int hb = 0;
+      uint32_t hphase = 0;
+      for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
+        const int tb = local % Cfg::kYBufs;
+        const int tuse = local / Cfg::kYBufs;
+        mbar_wait(&tempty[tb], (tuse & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t t_tmem = tmem_base + Cfg::kYBase + tb * Cfg::kYCols;
         uint32_t s_tmem = tmem_base;
-        const int kb = (item % splits) * kps, ke = min(k_iters, kb + kps);
         int in_chunk = 0;
-        for (int k = kb; k < ke; ++k) {
+        bool first = true;
+        // one k-step: the 3 (GRP) or 6 products of every K16 slice of the
+        // stage; A planes `a_plane` bytes apart (boxes, or K16 slices)
+        auto step = [&](uint32_t abase, uint32_t bbase, uint32_t a_plane, bool last_of_tile) {
           if (in_chunk == 0) {
             const int sb = g & 1;
             mbar_wait(&sempty[sb], ((g >> 1) & 1) ^ 1);
             tc_fence_after();
-            s_tmem = tmem_base + sb * BN;
+            s_tmem = tmem_base + sb * Cfg::kXCols;
           }
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t base = smem_u32(smem + stage * Cfg::kStage);
 #pragma unroll
           for (int kk = 0; kk < Cfg::kKSteps; ++kk) {
-            const uint32_t a0 = base + kk * 32, b0 = base + Cfg::kPlanes * Cfg::kA + kk * 32;
+            const uint32_t a0 = abase + kk * 32;
+            const uint32_t b0 = bbase + kk * 32;
             const uint64_t ah = make_smem_desc<SWZ>(a0, 8 * SWZ);
-            const uint64_t am = make_smem_desc<SWZ>(a0 + kPlaneA, 8 * SWZ);
-            const uint64_t al = make_smem_desc<SWZ>(a0 + 2 * kPlaneA, 8 * SWZ);
-            const uint64_t bh = make_smem_desc<SWZ>(b0, 8 * SWZ);
-            const uint64_t bm = make_smem_desc<SWZ>(b0 + kPlaneB, 8 * SWZ);
-            const uint64_t bl = make_smem_desc<SWZ>(b0 + 2 * kPlaneB, 8 * SWZ);
-            tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc, (in_chunk | kk) != 0 ? 1u : 0u);
-            tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, (k != kb || kk != 0) ? 1u : 0u);
-            tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
-            tc_mma<MmaKind::kF16>(t_tmem, ah, bl, idesc, 1u);
-            tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
-            tc_mma<MmaKind::kF16>(t_tmem, am, bm, idesc, 1u);
+            const uint64_t am = make_smem_desc<SWZ>(a0 + a_plane, 8 * SWZ);
+            const uint64_t al = make_smem_desc<SWZ>(a0 + 2 * a_plane, 8 * SWZ);
+            const uint64_t bh = make_smem_desc<kBSW>(b0, 8 * kBSW);
+            const uint32_t t_acc = (first && kk == 0) ? 0u : 1u;
+            const uint32_t s_acc = (in_chunk | kk) != 0 ? 1u : 0u;
+            if constexpr (Cfg::kGrp) {
+              // X[0:192] += A_h x [B_h|B_m|B_l]; Y[0:128] += A_m x [B_h|B_m];
+              // Y[0:64] += A_l x B_h
+              tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc3, s_acc);
+              tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc2, t_acc);
+              tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
+            } else {
+              const uint64_t bm = make_smem_desc<kBSW>(b0 + kPlaneB, 8 * kBSW);
+              const uint64_t bl = make_smem_desc<kBSW>(b0 + 2 * kPlaneB, 8 * kBSW);
+              tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc, s_acc);
+              tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, t_acc);
+              tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
+              tc_mma<MmaKind::kF16>(t_tmem, ah, bl, idesc, 1u);
+              tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
+              tc_mma<MmaKind::kF16>(t_tmem, am, bm, idesc, 1u);
+            }
           }
-          tc_commit(&empty[stage]);  // frees the smem slot when the MMAs land
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-          if (++in_chunk == chunk || k + 1 == ke) {
+          first = false;
+          if (++in_chunk == chunk || last_of_tile) {
             tc_commit(&sfull[g & 1]);  // chunk ready to fold
             ++g;
             in_chunk = 0;
+          }
+        };
+        if constexpr (HALO) {
+          const uint32_t a_plane = INTER ? 32u : static_cast<uint32_t>(p.halo_bytes);
+          for (int cb = 0; cb < p.cblocks; ++cb) {
+            mbar_wait(&hfull[hb], hphase);
+            tc_fence_after();
+            const uint32_t halo = smem_u32(sHalo + hb * Cfg::kAPlanes * p.halo_bytes);
+            for (int r = 0; r < p.r; ++r)
+              for (int s = 0; s < p.s; ++s) {
+                const int k = (r * p.s + s) * p.cblocks + cb;
+                uint32_t bbase;
+                if (RES) {
+                  bbase = smem_u32(sRes) + k * Cfg::kBStage;
+                } else {
+                  mbar_wait(&full[stage], phase);
+                  tc_fence_after();
+                  bbase = smem_u32(sRing + stage * Cfg::kStage);
+                }
+                // tap (r, s) of output virtual row v reads halo row v + r*wp + s
+                step(halo + (r * p.wp + s) * SWZ, bbase, a_plane,
+                     cb + 1 == p.cblocks && r + 1 == p.r && s + 1 == p.s);
+                if (!RES) {
+                  tc_commit(&empty[stage]);
+                  if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                  }
+                }
+              }
+            tc_commit(&hempty[hb]);  // halo free once these MMAs land
+            if (++hb == p.hbuf) {
+              hb = 0;
+              hphase ^= 1;
+            }
+          }
+        } else {
+          const int kb = (item % splits) * kps, ke = min(k_iters, kb + kps);
+          for (int k = kb; k < ke; ++k) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t base = smem_u32(sRing + stage * Cfg::kStage);
+            step(base, RES ? smem_u32(sRes) + k * Cfg::kBStage : base + Cfg::kAPlanes * Cfg::kA,
+                 kPlaneA, k + 1 == ke);
+            tc_commit(&empty[stage]);  // frees the smem slot when the MMAs land
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
         tc_commit(&tfull[tb]);
@@ -258,45 +445,74 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m_tile = mn / p.n_tiles;
       const int n_tile = mn - m_tile * p.n_tiles;
       const int row0 = m_tile * kBM + static_cast<int>(q * 32);
-      const int row = row0 + static_cast<int>(lane);
+      // this lane's output row (NHWC row index), or -1: past M, or (HALO) a
+      // junk virtual row of the shifted window
+      int orow;
+      int img = 0, oh0 = 0;
+      if constexpr (HALO) {
+        img = m_tile / p.bands;
+        oh0 = (m_tile - img * p.bands) * p.th;
+        const int v = static_cast<int>(q * 32 + lane);
+        const int ohl = v / p.wp, ow = v - ohl * p.wp;
+        orow = ow < p.ow && ohl < p.th && oh0 + ohl < p.oh ? (img * p.oh + oh0 + ohl) * p.ow + ow
+                                                          : -1;
+      } else {
+        const int row = row0 + static_cast<int>(lane);
+        orow = row < p.m ? row : -1;
+      }
       const int kb = split * kps, ke = min(k_iters, kb + kps);
       const int nch = (ke - kb + chunk - 1) / chunk;
       float sum[HB];
+      float cross[Cfg::kGrp ? HB : 1];  // GRP: the cross terms of the X chunks
 #pragma unroll
       for (int j = 0; j < HB; ++j) sum[j] = 0.0f;
-      // hh chunks, folded in K order with round-to-nearest adds
+#pragma unroll
+      for (int j = 0; j < (Cfg::kGrp ? HB : 1); ++j) cross[j] = 0.0f;
+      auto fold = [&](float* acc, uint32_t taddr) {
+#pragma unroll
+        for (int c0 = 0; c0 < HB; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(v[j]));
+        }
+      };
+      // hh chunks, folded in K order with round-to-nearest adds (GRP: the
+      // chunk also carries hm | hl, folded into the cross-term registers)
 #pragma unroll 1
       for (int c = 0; c < nch; ++c, ++g) {
         const int sb = g & 1;
         mbar_wait(&sfull[sb], (g >> 1) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int c0 = 0; c0 < HB; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(lane_base + sb * BN + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sum[c0 + j] = __fadd_rn(sum[c0 + j], __uint_as_float(v[j]));
+        const uint32_t xb = lane_base + sb * Cfg::kXCols;
+        fold(sum, xb);
+        if constexpr (Cfg::kGrp) {
+          fold(cross, xb + BN);
+          fold(cross, xb + 2 * BN);
         }
         tc_fence_before();
         mbar_arrive(&sempty[sb]);
       }
-      // + the cross terms
-      const int tb = local & 1;
-      mbar_wait(&tfull[tb], (local >> 1) & 1);
+      // + the tile's cross-term accumulator
+      const int tb = local % Cfg::kYBufs;
+      mbar_wait(&tfull[tb], (local / Cfg::kYBufs) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < HB; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(lane_base + (2 + tb) * BN + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) sum[c0 + j] = __fadd_rn(sum[c0 + j], __uint_as_float(v[j]));
+      const uint32_t yb = lane_base + Cfg::kYBase + tb * Cfg::kYCols;
+      if constexpr (Cfg::kGrp) {
+        fold(cross, yb);
+        fold(cross, yb + BN);
+      } else {
+        fold(sum, yb);
       }
       tc_fence_before();
       // p.fault == 1 (tests only): lose one arrive -- the MMA warp then waits
       // for this accumulator forever and the mbarrier watchdog must trap
       if (!(p.fault == 1 && local == 0)) mbar_arrive(&tempty[tb]);
+      if constexpr (Cfg::kGrp) {
+#pragma unroll
+        for (int j = 0; j < HB; ++j) sum[j] = __fadd_rn(sum[j], cross[j]);
+      }
       if (splits > 1) {
         // publish this split's partial ([item][warp][column][lane]: one
         // 128-B line per column); the last split of the tile sums them all
@@ -337,8 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < HB; ++j) {
           const int col = n_tile * BN + hf * HB + j;
-          if (row >= p.m || col >= p.oc) continue;
-          const int64_t o = static_cast<int64_t>(row) * p.oc + col;
+          if (orow < 0 || col >= p.oc) continue;
+          const int64_t o = static_cast<int64_t>(orow) * p.oc + col;
           float v = sum[j];
           if constexpr (PROG != epi::kProgNone) v = __fadd_rn(v, bias[col]);
           if constexpr (PROG == epi::kProgBiasAddRelu) v = __fadd_rn(v, res[o]);
@@ -351,9 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // fused members -> 32x32 f32 boxes -> TMA stores (rows >= M and
       // columns >= OC are clipped by the tensor map)
       const uint8_t* rrow = nullptr;
-      if (PROG == epi::kProgBiasAddRelu && row < p.m)
+      if (PROG == epi::kProgBiasAddRelu && orow >= 0)
         rrow = static_cast<const uint8_t*>(p.epi.residual) +
-               (static_cast<int64_t>(row) * p.oc + n_tile * BN + hf * HB) * 4;
+               (static_cast<int64_t>(orow) * p.oc + n_tile * BN + hf * HB) * 4;
 #pragma unroll
       for (int c0 = 0; c0 < HB; c0 += 32) {
         if (n_tile * BN + hf * HB + c0 < p.oc) {
@@ -367,7 +583,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tm_y, stage_u32, n_tile * BN + hf * HB + c0, row0);
+            if constexpr (HALO)  // one output row per tile: (OC, OW, N*OH) map
+              tma_store_3d(&tm_y, stage_u32, n_tile * BN + hf * HB + c0, static_cast<int>(q * 32),
+                           img * p.oh + oh0);
+            else
+              tma_store_2d(&tm_y, stage_u32, n_tile * BN + hf * HB + c0, row0);
             bulk_commit();
           }
         }
@@ -382,65 +602,83 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
 }
 
-template <int BN, int SWZ, int STAGES, bool INTER, int PROG>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG>
 int launch_f32tc_inst(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int grid, cudaStream_t stream) {
-  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER>;
-  auto kfn = conv_f32tc_kernel<BN, SWZ, STAGES, INTER, PROG>;
-  cudaError_t e =
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER, RES, HALO>;
+  auto kfn = conv_f32tc_kernel<BN, SWZ, STAGES, INTER, RES, HALO, PROG>;
+  const int smem = Cfg::kSmem + (RES ? p.res_bytes : 0) +
+                   (HALO ? p.hbuf * Cfg::kAPlanes * p.halo_bytes : 0);
+  if (smem > 227 * 1024) return -1;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), Cfg::kSmem, stream, tm_a, tm_b, tm_y, p);
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_a, tm_b, tm_y, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-template <int BN, int SWZ, int STAGES, bool INTER>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO>
 int launch_f32tc_prog(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int prog, int grid, cudaStream_t st) {
   switch (prog) {
-    case epi::kProgNone: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgNone>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBias: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgBias>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBiasRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgBiasRelu>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBiasAddRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, epi::kProgBiasAddRelu>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgNone: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgNone>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBias: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBias>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBiasRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBiasRelu>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBiasAddRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBiasAddRelu>(tm_a, tm_b, tm_y, p, grid, st);
     default: return -1;
   }
 }
 
-// The instantiated (BN, block, stages, interleaved) set.
-#define TEC_F32TC_INSTANCES(X) \
-  X(64, 128, 2, false)         \
-  X(128, 128, 2, false)        \
-  X(64, 32, 8, false)          \
-  X(128, 32, 6, false)         \
-  X(64, 128, 6, true)          \
-  X(128, 128, 5, true)
+// The instantiated (BN, block, stages, interleaved, resident weights, halo)
+// set. Halo instances: the ring carries weights only (STAGES = its depth,
+// 0 with resident weights).
+#define TEC_F32TC_INSTANCES(X)         \
+  X(64, 128, 2, false, false, false)   \
+  X(128, 128, 2, false, false, false)  \
+  X(64, 32, 8, false, false, false)    \
+  X(128, 32, 6, false, false, false)   \
+  X(64, 128, 6, true, false, false)    \
+  X(128, 128, 5, true, false, false)   \
+  X(64, 128, 3, false, true, false)    \
+  X(128, 128, 2, false, true, false)   \
+  X(64, 128, 6, true, true, false)     \
+  X(128, 128, 4, true, true, false)    \
+  X(64, 128, 1, true, true, true)      \
+  X(64, 128, 3, false, false, true)    \
+  X(128, 128, 2, false, false, true)
 
 }  // namespace
 
-int conv_f32tc_smem_bytes(int bn, int swz, bool inter) {
-#define TEC_X(BN, SW, ST, IN) \
-  if (bn == BN && swz == SW && inter == IN) return F32tcCfg<BN, SW, ST, IN>::kSmem;
+// Fixed shared memory of an instance (resident weights come on top), its
+// ring depth, and B bytes per k-iteration; -1 when not instantiated.
+int conv_f32tc_smem_bytes(int bn, int swz, bool inter, bool res, bool halo) {
+#define TEC_X(BN, SW, ST, IN, RS, HA)                                     \
+  if (bn == BN && swz == SW && inter == IN && res == RS && halo == HA) \
+    return F32tcCfg<BN, SW, ST, IN, RS, HA>::kSmem;
   TEC_F32TC_INSTANCES(TEC_X)
 #undef TEC_X
   return -1;
 }
 
-int conv_f32tc_stages(int bn, int swz, bool inter) {
-#define TEC_X(BN, SW, ST, IN) \
-  if (bn == BN && swz == SW && inter == IN) return ST;
+int conv_f32tc_stages(int bn, int swz, bool inter, bool res, bool halo) {
+#define TEC_X(BN, SW, ST, IN, RS, HA) \
+  if (bn == BN && swz == SW && inter == IN && res == RS && halo == HA) return ST;
   TEC_F32TC_INSTANCES(TEC_X)
 #undef TEC_X
   return -1;
+}
+
+int conv_f32tc_b_stage_bytes(int bn, int swz, bool inter) {
+  return 3 * bn * (inter ? 32 : swz);
 }
 
 // Returns a cudaError_t, or -1 for an unsupported (bn, swz, program).
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
-                      const ConvGemmParams& p, int bn, int swz, bool inter, int prog, int grid,
-                      cudaStream_t st) {
-#define TEC_X(BN, SW, ST, IN)   \
-  if (bn == BN && swz == SW && inter == IN) \
-    return launch_f32tc_prog<BN, SW, ST, IN>(tm_a, tm_b, tm_y, p, prog, grid, st);
+                      const ConvGemmParams& p, int bn, int swz, bool inter, bool res, bool halo,
+                      int prog, int grid, cudaStream_t st) {
+#define TEC_X(BN, SW, ST, IN, RS, HA)                                     \
+  if (bn == BN && swz == SW && inter == IN && res == RS && halo == HA) \
+    return launch_f32tc_prog<BN, SW, ST, IN, RS, HA>(tm_a, tm_b, tm_y, p, prog, grid, st);
   TEC_F32TC_INSTANCES(TEC_X)
 #undef TEC_X
   return -1;

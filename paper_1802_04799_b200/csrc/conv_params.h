@@ -60,6 +60,16 @@ struct ConvGemmParams {
   int32_t chunk_iters;  // f32tc: k-iterations per hh promotion chunk
   int32_t fault;        // test-only fault injection (TEC_SM100_FAULT): 1 = the
                         // epilogue drops its first accumulator-free arrive
+  int32_t producers;    // f32tc: TMA issuing threads (1, or 2: A and B split)
+  int32_t res_bytes;    // f32tc resident weights: shared-memory bytes of all B tiles
+  // f32tc shifted-window mode (stride 1): a tile is th output rows of one
+  // image; its (th + r - 1) x wp input rows are loaded ONCE per channel
+  // block (tiled TMA, zero padding by OOB fill) and every filter tap is a
+  // row shift of that halo (see conv_halo.cu); m_tiles = n * bands.
+  int32_t th, wp, bands;
+  int32_t halo_bytes;      // smem bytes per halo plane buffer (1024-aligned)
+  int32_t halo_box_bytes;  // bytes one halo box lands (th + r - 1) * wp * 128
+  int32_t hbuf;            // halo buffers (1 or 2)
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA

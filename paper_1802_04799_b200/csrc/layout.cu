@@ -398,7 +398,50 @@ __global__ void pack_weights_s2d_kernel(const InT* __restrict__ w, void* __restr
   }
 }
 
+// Weights of the interleaved f32tc path (<= 16 channels per plane, incl.
+// the space-to-depth stem): [tap][plane][K][16] bf16 -- per tap the three
+// planes are consecutive 16-channel row blocks, so one 3-D TMA box lands
+// them as [B_h; B_m; B_l] rows (one N-concatenated MMA operand).
+// s2d: tap = (ri, sj) over (r2, s2), channel (dy*2+dx)*C + c of w[k][c][2ri+dy][2sj+dx];
+// else tap = (rr, ss) over (r, s), channel c.
+template <typename InT>
+__global__ void pack_weights_split3i_kernel(const InT* __restrict__ w, __nv_bfloat16* __restrict__ out,
+                                            int64_t k, int64_t c, int64_t r, int64_t s,
+                                            int64_t r2, int64_t s2, int s2d) {
+  const int64_t taps = s2d ? r2 * s2 : r * s;
+  const int64_t total = taps * 3 * k * 16;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ch = i % 16;
+    int64_t t = i / 16;
+    const int64_t kk = t % k;
+    t /= k;
+    const int plane = static_cast<int>(t % 3);
+    const int64_t tap = t / 3;
+    float v = 0.f;
+    if (s2d) {
+      if (ch < 4 * c) {
+        const int64_t q = ch / c, cc = ch % c;
+        const int64_t rr = 2 * (tap / s2) + q / 2, ss = 2 * (tap % s2) + q % 2;
+        if (rr < r && ss < s) v = static_cast<float>(w[((kk * c + cc) * r + rr) * s + ss]);
+      }
+    } else if (ch < c) {
+      v = static_cast<float>(w[((kk * c + ch) * r + tap / s) * s + tap % s]);
+    }
+    out[i] = split3(v, plane);
+  }
+}
+
 // ----------------------------------------------------------- launchers
+int launch_pack_weights_split3i(const void* w, void* out, int64_t k, int64_t c, int64_t r,
+                                int64_t s, int64_t r2, int64_t s2, int s2d, cudaStream_t st) {
+  const int64_t taps = s2d ? r2 * s2 : r * s;
+  const int64_t total = taps * 3 * k * 16;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 4096)));
+  pack_weights_split3i_kernel<float><<<blocks, 256, 0, st>>>(
+      static_cast<const float*>(w), static_cast<__nv_bfloat16*>(out), k, c, r, s, r2, s2, s2d);
+  return cudaGetLastError();
+}
 int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c, int64_t h,
                     int64_t w, int64_t ph, int64_t pw, int64_t h2, int64_t w2, int64_t cp,
                     int mode, cudaStream_t st) {

@@ -29,7 +29,7 @@ from ._abi import TecError
 E_DUPLICATE_INTRINSIC, E_TENSORIZE_MISMATCH, E_LOWERING = 5, 14, 15
 
 FAMILIES = {1: "im2col", 2: "halo", 3: "f32_exact", 4: "depthwise_tma", 5: "depthwise_direct",
-            6: "f32tc"}
+            6: "f32tc", 7: "f32tc_halo"}
 
 
 @dataclass(frozen=True)
@@ -137,6 +137,6 @@ def lower(desc: _abi.ConvDesc, config: Optional[Dict[str, int]] = None,
     if plan.smem_bytes > opts.smem_bytes or plan.tmem_cols > opts.tmem_cols:
         raise TecError(E_LOWERING, f"plan exceeds the on-chip budget: {plan}")
     intr = find_intrinsic(plan.intrinsic)
-    if plan.family in ("im2col", "halo", "f32tc") and not intr.accepts(128, plan.tile_n, intr.k):
+    if plan.family in ("im2col", "halo", "f32tc", "f32tc_halo") and not intr.accepts(128, plan.tile_n, intr.k):
         raise TecError(E_TENSORIZE_MISMATCH, f"{plan.intrinsic} cannot take N={plan.tile_n}")
     return plan

@@ -226,7 +226,8 @@ def conv_space(name: str, desc: _abi.ConvDesc,
         weight tiles by TMA multicast);
       f32tc: tile_n and split_k of the split-bf16 f32 kernel."""
     if desc.compute == _abi.COMPUTE_F32TC:
-        knobs = [KnobDef("tile_n", [64, 128]), KnobDef("split_k", [1, 2, 3, 4, 6, 8])]
+        knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128]),
+                 KnobDef("stages", [1, 2]), KnobDef("split_k", [1, 2, 3, 4, 6, 8])]
     else:
         knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
                  KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2]),
@@ -363,6 +364,7 @@ def measure(space: KnobSpace, configs: Sequence[Config], devices: Sequence[int] 
 FEATURE_NAMES = (
     # kernel family one-hot (lower.FAMILIES)
     "fam_im2col", "fam_halo", "fam_f32_exact", "fam_dw_tma", "fam_dw_direct", "fam_f32tc",
+    "fam_f32tc_halo",
     # loop structure: extents of the tile loop and the reduction loop
     "log_tiles", "log_items", "log_grid", "log_waves", "log_k_iters", "tail_frac",
     # annotations (the reference's vectorize / unroll / parallel / vthread slots)
@@ -383,7 +385,7 @@ def kernel_features(desc: _abi.ConvDesc, plan) -> List[float]:
     from .lower import FAMILIES
     lg = lambda v: math.log2(max(1.0, float(v)))  # noqa: E731
     fam = {v: k for k, v in FAMILIES.items()}.get(plan.family, 0)
-    onehot = [1.0 if fam == i else 0.0 for i in range(1, 7)]
+    onehot = [1.0 if fam == i else 0.0 for i in range(1, 8)]
     es = {_abi.COMPUTE_BF16: 2, _abi.COMPUTE_I8: 1}.get(desc.compute, 4)
     a_es = 6 if desc.compute == _abi.COMPUTE_F32TC else es   # three bf16 planes
     oh = (desc.h + 2 * desc.pad_h - desc.r) // desc.stride_h + 1
@@ -404,7 +406,7 @@ def kernel_features(desc: _abi.ConvDesc, plan) -> List[float]:
     hbm_out = m * desc.k * 4
     l2_act = tm * kdim * a_es / split          # A operand per work item
     l2_wt = tn * kdim * a_es / split            # B operand per work item
-    if plan.family == "halo":                   # each input row loaded once per tile
+    if plan.family in ("halo", "f32tc_halo"):   # each input row loaded once per tile
         l2_act /= max(1, desc.r * desc.s)
     l2_sm = (l2_act + l2_wt) * items / grid
     flops = 2.0 * m * desc.k * kdim

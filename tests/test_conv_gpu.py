@@ -415,3 +415,32 @@ def test_split_k_scratch_shared_across_shapes():
             xr, wr = (bf16_round(x), bf16_round(w)) if compute == "bf16" else (x, w)
             want = oracle_conv("conv2d", xr, wr, (s, s), (r // 2, r // 2), epi)
             assert same_values(y, want, tol), (layer, sk, compute, max_rel_err(y, want))
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("case", ["C1", "C2", "C6", "C9", "odd5x5", "odd_res"])
+def test_f32tc_im2col_and_shifted_window(case, path):
+    """f32tc A-operand paths (knob tile_k): 1 = im2col TMA, 2 = shifted
+    window (one halo load per tile and channel block, every tap a row
+    shift; th = 1 rows store by TMA, th > 1 per element). 'odd*': 5x5,
+    padding 2, W not a multiple of anything, a batch tail, residual."""
+    if case.startswith("odd"):
+        shape_x, shape_w, s, pad = (3, 64, 11, 13), (64, 64, 5, 5), 1, 2
+    else:
+        hw, c, k, r, s = RESNET18_CONVS[case]
+        shape_x, shape_w, pad = (2, c, hw, hw), (k, c, r, r), r // 2
+    x, w, b = _inputs(shape_x, shape_w, shape_w[0], False, 17)
+    attrs = {"strides": (s, s), "padding": (pad, pad)}
+    epi = [("bias_add", b), ("relu",)]
+    if case == "odd_res":
+        oh = (shape_x[2] + 2 * pad - shape_w[2]) // s + 1
+        ow = (shape_x[3] + 2 * pad - shape_w[3]) // s + 1
+        r_ = np.random.default_rng(18).uniform(-1, 1, (shape_x[0], shape_w[0], oh, ow)).astype(np.float32)
+        epi = [("bias_add", b), ("add", r_), ("relu",)]
+    try:
+        y = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc", knobs={"tile_k": path})
+    except TecError as e:
+        assert e.code == "LoweringError" and path == 2
+        pytest.skip(str(e))
+    want = oracle_conv("conv2d", x, w, (s, s), (pad, pad), epi)
+    assert same_values(y, want, TOL_F32TC), f"max rel err {max_rel_err(y, want)}"
