@@ -105,6 +105,17 @@ struct F32tcCfg {
   static_assert(!INTER || SWZ == 128, "interleaved planes live in one 128-B row");
 };
 
+// mbar_wait that adds its waiting cycles to *acc when profiling (p.dbg)
+__device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool prof, long long* acc) {
+  if (!prof) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  *acc += clock64() - t0;
+}
+
 template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_f32tc_kernel(const __grid_constant__ CUtensorMap tm_a,
@@ -142,6 +153,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = threadIdx.x & 31;
   const int splits = p.splits > 1 ? p.splits : 1;
   const int num_items = p.m_tiles * p.n_tiles * splits;
+  // TEC_SM100_PROFILE: per-role waiting cycles, summed over CTAs into p.dbg --
+  // [0] producer A (halo/ring) free, [1] producer B ring free, [2] MMA
+  // tile accumulator free, [3] MMA chunk accumulator free, [4] MMA operands
+  // landed, [5] epilogue chunk ready, [6] epilogue tile ready, [7] epilogue
+  // busy, [8] CTA cycles, [9] items
+  const bool prof = p.dbg != nullptr;
+  long long dw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = prof ? clock64() : 0;
   const int k_iters = p.r * p.s * p.cblocks;
   const int kps = splits > 1 ? p.kps : k_iters;  // k-iterations per split
   const int chunk = p.chunk_iters;               // k-iterations per hh chunk
@@ -224,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int oh0 = (m_tile - img * p.bands) * p.th;
           for (int cb = 0; cb < p.cblocks; ++cb) {
             if (issue_a) {
-              mbar_wait(&hempty[hb], hphase ^ 1);
+              twait(&hempty[hb], hphase ^ 1, prof, &dw[0]);
               mbar_arrive_expect_tx(&hfull[hb],
                                     static_cast<uint32_t>(Cfg::kAPlanes * p.halo_box_bytes));
 #pragma unroll
@@ -239,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (issue_b && !RES) {
               for (int r = 0; r < p.r; ++r)
                 for (int s = 0; s < p.s; ++s) {
-                  mbar_wait(&empty[stage], phase ^ 1);
+                  twait(&empty[stage], phase ^ 1, prof, &dw[1]);
                   mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
                   uint8_t* bbase = sRing + stage * Cfg::kStage;
                   if constexpr (INTER) {
@@ -276,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int r = kb / sc, rem_k = kb - r * sc;
         int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
         for (int k = kb; k < ke; ++k) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          twait(&empty[stage], phase ^ 1, prof, &dw[0]);
           if (issue_a) mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
           uint8_t* base = sRing + stage * Cfg::kStage;
           uint8_t* bbase = base + Cfg::kAPlanes * Cfg::kA;
@@ -326,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
         const int tb = local % Cfg::kYBufs;
         const int tuse = local / Cfg::kYBufs;
-        mbar_wait(&tempty[tb], (tuse & 1) ^ 1);
+        twait(&tempty[tb], (tuse & 1) ^ 1, prof, &dw[2]);
         tc_fence_after();
         const uint32_t t_tmem = tmem_base + Cfg::kYBase + tb * Cfg::kYCols;
         uint32_t s_tmem = tmem_base;
@@ -337,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto step = [&](uint32_t abase, uint32_t bbase, uint32_t a_plane, bool last_of_tile) {
           if (in_chunk == 0) {
             const int sb = g & 1;
-            mbar_wait(&sempty[sb], ((g >> 1) & 1) ^ 1);
+            twait(&sempty[sb], ((g >> 1) & 1) ^ 1, prof, &dw[3]);
             tc_fence_after();
             s_tmem = tmem_base + sb * Cfg::kXCols;
           }
@@ -378,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (HALO) {
           const uint32_t a_plane = INTER ? 32u : static_cast<uint32_t>(p.halo_bytes);
           for (int cb = 0; cb < p.cblocks; ++cb) {
-            mbar_wait(&hfull[hb], hphase);
+            twait(&hfull[hb], hphase, prof, &dw[4]);
             tc_fence_after();
             const uint32_t halo = smem_u32(sHalo + hb * Cfg::kAPlanes * p.halo_bytes);
             for (int r = 0; r < p.r; ++r)
@@ -388,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (RES) {
                   bbase = smem_u32(sRes) + k * Cfg::kBStage;
                 } else {
-                  mbar_wait(&full[stage], phase);
+                  twait(&full[stage], phase, prof, &dw[4]);
                   tc_fence_after();
                   bbase = smem_u32(sRing + stage * Cfg::kStage);
                 }
@@ -412,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           const int kb = (item % splits) * kps, ke = min(k_iters, kb + kps);
           for (int k = kb; k < ke; ++k) {
-            mbar_wait(&full[stage], phase);
+            twait(&full[stage], phase, prof, &dw[4]);
             tc_fence_after();
             const uint32_t base = smem_u32(sRing + stage * Cfg::kStage);
             step(base, RES ? smem_u32(sRes) + k * Cfg::kBStage : base + Cfg::kAPlanes * Cfg::kA,
@@ -483,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < nch; ++c, ++g) {
         const int sb = g & 1;
-        mbar_wait(&sfull[sb], (g >> 1) & 1);
+        twait(&sfull[sb], (g >> 1) & 1, prof, &dw[5]);
         tc_fence_after();
         const uint32_t xb = lane_base + sb * Cfg::kXCols;
         fold(sum, xb);
@@ -496,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // + the tile's cross-term accumulator
       const int tb = local % Cfg::kYBufs;
-      mbar_wait(&tfull[tb], (local / Cfg::kYBufs) & 1);
+      twait(&tfull[tb], (local / Cfg::kYBufs) & 1, prof, &dw[6]);
       tc_fence_after();
       const uint32_t yb = lane_base + Cfg::kYBase + tb * Cfg::kYCols;
       if constexpr (Cfg::kGrp) {
@@ -594,12 +613,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) bulk_wait_all();  // TMA stores done before smem goes away
+    if (prof) dw[7] = clock64() - t_start - dw[5] - dw[6];
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  if (prof) {
+    // one representative thread per role: producer warps 0 / 3, MMA warp 1,
+    // the first epilogue thread
+    const bool rep = ((warp == 0 || warp == 1 || warp == 3) && lane == 0) || threadIdx.x == 128;
+    if (rep)
+      for (int i = 0; i < 8; ++i)
+        if (dw[i]) atomicAdd(&p.dbg[i], static_cast<unsigned long long>(dw[i]));
+    if (threadIdx.x == 0) {
+      atomicAdd(&p.dbg[8], static_cast<unsigned long long>(clock64() - t_start));
+      atomicAdd(&p.dbg[9], static_cast<unsigned long long>(
+                               (num_items - blockIdx.x + gridDim.x - 1) / gridDim.x));
+    }
+  }
 }
 
 template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG>

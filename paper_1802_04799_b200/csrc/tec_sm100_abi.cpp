@@ -1143,9 +1143,30 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     tec_status wst = splitk_workspace(dev, partials, (size_t)tiles, st, &p.ws, &p.tile_cnt);
     if (wst) return wst;
   }
+  static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
+  unsigned long long* dbg = nullptr;
+  if (prof) {  // diagnostics only: synchronises the stream
+    TEC_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    TEC_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st));
+    p.dbg = dbg;
+  }
   const int e = launch_conv_f32tc(tm_a, tm_b, tm_y, p, bn, swz, inter, res, halo, prog, grid, st);
   if (e == -1) return fail(TEC_E_LOWERING, "f32tc: no instance for this tile / block");
   if (e) return cuda_fail(e, "conv_f32tc launch");
+  if (prof) {
+    unsigned long long h[16];
+    TEC_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TEC_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dbg);
+    const double c = (double)grid;
+    std::fprintf(stderr,
+                 "[tec-prof] f32tc halo=%d res=%d bn=%d inter=%d splits=%d items/cta=%.2f "
+                 "cta_cycles=%.0f | prodA_wait=%.0f prodB_wait=%.0f mma_wait_tile=%.0f "
+                 "mma_wait_chunk=%.0f mma_wait_data=%.0f epi_wait_chunk=%.0f epi_wait_tile=%.0f "
+                 "epi_busy=%.0f (per CTA)\n",
+                 (int)halo, (int)res, bn, (int)inter, p.splits, h[9] / c, h[8] / c, h[0] / c, h[1] / c,
+                 h[2] / c, h[3] / c, h[4] / c, h[5] / c, h[6] / c, h[7] / c);
+  }
   return TEC_OK;
 }
 
