@@ -16,6 +16,8 @@ The same line carries, as named sub-results measured in the same run:
                    against an int8 peak measured in this run
   resnet18         ResNet-18 inference, global batch 256 sharded over the
                    ranks (configs[3], strong scaling), img/s + e2e img/s
+  depthwise        MobileNet D1-D9 depthwise + bias + relu, batch 64, bf16 and
+                   f32 (configs[2]), GB/s against the HBM roofline
 
 One "step" = the 12 fused layers once over one batch of synthetic inputs
 (reference value distributions, random-init weights), inputs resident in HBM.
@@ -458,6 +460,21 @@ def impl_ours(args):
                       "roofline_frac": rl["roofline"]["frac"],
                       "config": rl["config"]["workload"]}
 
+    # ---- configs[2]: MobileNet D1-D9 depthwise + bias + relu, batch 64
+    # (HBM-bound; GB/s against the HBM roofline), bf16 and f32
+    depthwise = {}
+    if not args.no_depthwise:
+        import bench_workloads
+        for dc in ("bf16", "f32"):
+            dargs = argparse.Namespace(**vars(args))
+            dargs.steps = min(args.steps, 100)
+            dl = bench_workloads.depthwise_line(dargs, sys.modules[__name__], dc)
+            if dl is not None:
+                depthwise[dc] = {"value": dl["value"], "unit": "GB/s",
+                                 "ms_per_step": dl["ms_per_step"], "roofline": dl["roofline"],
+                                 "parity": "bit-identical to the oracle (tests/test_bench_parity.py)",
+                                 "layers": dl["layers"]}
+
     # ---- e2e through the reference-facing host API (tec_eval_fused_conv):
     # pinned host NCHW f32 inputs -> H2D -> pack -> fused kernel -> unpack -> D2H.
     e2e = None
@@ -528,6 +545,7 @@ def impl_ours(args):
             "layers": h["layers"],
             "precisions": {p: sub(p) for p in res if p != headline},
             "resnet18": resnet,
+            "depthwise": depthwise or None,
             "gpu_launches": h["launches"],
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -684,6 +702,7 @@ def main():
                     help="headline arithmetic (default: f32, the reference's precision)")
     ap.add_argument("--also", default="bf16,i8", help="sub-result precisions in the same line")
     ap.add_argument("--no-resnet18", action="store_true")
+    ap.add_argument("--no-depthwise", action="store_true")
     ap.add_argument("--cpu-dry-run", action="store_true",
                     help="multi-rank plumbing on gloo without a GPU (tests)")
     ap.add_argument("--workload", default="conv",
