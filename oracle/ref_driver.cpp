@@ -25,6 +25,14 @@
 //         CostModel::train / predict / pairwise_rank_accuracy
 //         (R/src/gbt.cpp:119-246) on {"feats", "costs", "query", "params"};
 //         writes {"pred", "acc", "model"} -- pins the tuner's restatement.
+//   sched <in.json> <out_dir>
+//         a B200 Config's schedule log (tuner.schedule_log) replayed on the
+//         reference: conv2d compute "conv" over placeholders D / W
+//         (make_conv), Schedule::replay (R/src/schedule.cpp:486-491) ->
+//         lower(target "interp") -> interpret (R/src/interp.cpp:501-546) on
+//         random_tensor feeds; saves D, W, interp and reference outputs;
+//         prints {"features": extract_features, "log", "cost", "matches"} --
+//         the legality check, the reference features and the second oracle.
 //   bench <op> <C> <H> <W> <OC> <K> <stride> <pad> <rows> <seed> [dtype]
 //         times eval_graph_node (R/src/graph.cpp:209) on the fused node
 //         [conv2d|depthwise_conv2d, bias_add, relu] built exactly as
@@ -39,6 +47,10 @@
 
 #include "tec/autotune.hpp"
 #include "tec/graph.hpp"
+#include "tec/interp.hpp"
+#include "tec/lower.hpp"
+#include "tec/schedule.hpp"
+#include "tec/texpr.hpp"
 #include "tec/graph_passes.hpp"
 #include "tec/io.hpp"
 #include "tec/ops.hpp"
@@ -113,6 +125,38 @@ static int cmd_gbt(const std::string& in_path, const std::string& out_path) {
   return 0;
 }
 
+static int cmd_sched(const std::string& in_path, const std::string& out_dir) {
+  nlohmann::json j = parse_json(read_text_file(in_path), in_path);
+  auto xs = j.at("x_shape").get<std::vector<int64_t>>();
+  auto ws = j.at("w_shape").get<std::vector<int64_t>>();
+  Tensor d = placeholder("D", TensorType(xs, DType::kF32));
+  Tensor w = placeholder("W", TensorType(ws, DType::kF32));
+  AttrMap a;
+  a["strides"] = j.at("strides").get<std::vector<int64_t>>();
+  a["padding"] = j.at("padding").get<std::vector<int64_t>>();
+  Tensor conv = op_def("conv2d").make_compute("conv", {d, w}, a);
+  Schedule s = Schedule::replay({conv}, j.at("log"));
+  LoopProgram prog = lower(s, "conv");
+  std::mt19937_64 rng(j.value("seed", 0));
+  std::map<std::string, DenseTensor> feeds;
+  feeds.emplace("D", random_tensor(d->type, rng));
+  feeds.emplace("W", random_tensor(w->type, rng));
+  InterpResult r = interpret(prog, feeds);
+  DenseTensor want = evaluate_reference(conv, feeds);
+  const DenseTensor& got = r.outputs.at("conv");
+  save_tensor(out_dir, "D", feeds.at("D"));
+  save_tensor(out_dir, "W", feeds.at("W"));
+  save_tensor(out_dir, "interp", got);
+  save_tensor(out_dir, "ref", want);
+  nlohmann::json out;
+  out["features"] = extract_features(prog);
+  out["log"] = s.log();
+  out["cost"] = r.cost();
+  out["matches_1e5"] = got.same_values(want, 1e-5);
+  std::printf("%s\n", out.dump().c_str());
+  return 0;
+}
+
 static int cmd_gen(int argc, char** argv) {
   std::string dir = argv[2], name = argv[3];
   DType dt = dtype_from_name(argv[4]);
@@ -182,6 +226,7 @@ int main(int argc, char** argv) {
     if (cmd == "layouts" && argc == 5) return cmd_layouts(argv[2], argv[3], argv[4]);
     if (cmd == "gen" && argc >= 7) return cmd_gen(argc, argv);
     if (cmd == "gbt" && argc == 4) return cmd_gbt(argv[2], argv[3]);
+    if (cmd == "sched" && argc == 4) return cmd_sched(argv[2], argv[3]);
     if (cmd == "bench" && argc >= 12) return cmd_bench(argc, argv);
     std::fprintf(stderr, "bad arguments for '%s'\n", cmd.c_str());
     return 2;

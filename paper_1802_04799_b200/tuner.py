@@ -251,68 +251,103 @@ def dw_space(name: str, desc: _abi.ConvDesc,
 
 
 # ------------------------------------------------ Config <-> schedule log
-# The reference records a schedule as a JSON list of primitive applications
-# (R/src/schedule.cpp:456-491, Schedule::apply_log_entry). A B200 Config is
-# the same decision in template form (SURVEY 8a knob mapping); these two
-# functions translate between them so trial DBs and schedule logs interoperate.
+# A Config as a schedule of the reference's conv2d compute (R/src/ops.cpp:
+# 120-161, stage "conv", axes n, oc, oh, ow / reduce ic, rh, rw), in the
+# reference's own transformation-log format (R/src/schedule.cpp:164-453,
+# replayed by Schedule::replay / apply_log_entry :456-491). The template
+# mirrors the kernel's decomposition:
+#   split oc by tile_n, oh by the tile's output rows, ic by the channel block
+#   of one k-step; blockIdx.x/y = (row tile, N tile); the tile's rows and
+#   channels as threadIdx.y/x (the tensor core's lanes); the reduction walks
+#   (rh, rw, channel block) -- im2col -- or (channel block, rh, rw) -- the
+#   shifted window, one activation load per channel block; split-K fuses the
+#   reduce-outer axes and splits them; the weight tile is a shared-memory
+#   cache computed per k-step, or once per output-channel tile (resident).
+# The reference lowers such a log (legality), featurises it (features.cpp)
+# and interprets it -- a second oracle (tests/test_schedule_template.py).
+# Not expressible: the activation staging (a padded conv's clamp defeats the
+# reference's footprint inference for a cached D), cluster multicast.
 _INTRIN = {_abi.COMPUTE_BF16: "sm100.umma.bf16", _abi.COMPUTE_F32TC: "sm100.umma.bf16x6",
            _abi.COMPUTE_I8: "sm100.umma.i8", _abi.COMPUTE_F32: "sm100.simt.f32"}
 
 
+def _geom(desc: _abi.ConvDesc):
+    oh = (desc.h + 2 * desc.pad_h - desc.r) // desc.stride_h + 1
+    ow = (desc.w + 2 * desc.pad_w - desc.s) // desc.stride_w + 1
+    kcb = {_abi.COMPUTE_I8: 128}.get(desc.compute, 64)  # channels per k-step
+    return oh, ow, min(kcb, desc.c)
+
+
 def schedule_log(cfg: Config, desc: _abi.ConvDesc, stage: str = "conv") -> List[dict]:
-    log = []
-    if cfg.get("tile_n"):
-        log.append({"prim": "split", "stage": stage, "axis": "ff", "factor": int(cfg["tile_n"])})
-    if cfg.get("tile_m"):
-        log.append({"prim": "split", "stage": stage, "axis": "nyx", "factor": int(cfg["tile_m"])})
-    if cfg.get("split_k", 1) > 1:
-        log.append({"prim": "split", "stage": stage, "axis": "rc", "factor": int(cfg["split_k"])})
-    src = {1: "im2col", 2: "halo"}.get(int(cfg.get("tile_k", 0)), "auto")
-    log.append({"prim": "cache_read", "src": f"data.{src}", "scope": "shared", "readers": [stage]})
-    if cfg.get("stages"):
-        log.append({"prim": "cache_read", "src": "weight." + ("resident" if cfg["stages"] == 2
-                                                           else "streamed"),
-                    "scope": "shared", "readers": [stage]})
-    log.append({"prim": "set_scope", "stage": stage, "scope": "accel.accum"})
-    log.append({"prim": "tensorize", "stage": stage, "axis": "nyx.inner",
-                "intrin": _INTRIN.get(desc.compute, "sm100.umma.bf16")})
-    if cfg.get("unroll"):
-        log.append({"prim": "unroll", "stage": stage, "axis": f"xx.{int(cfg['unroll'])}"})
-    if cfg.get("grid"):
-        log.append({"prim": "bind", "stage": stage, "axis": f"nyx.outer.{int(cfg['grid'])}",
-                    "tag": "blockIdx.x"})
-    if cfg.get("cluster_n", 1) > 1:
-        log.append({"prim": "bind", "stage": stage, "axis": f"nyx.cluster.{int(cfg['cluster_n'])}",
-                    "tag": "cluster"})
+    oh, ow, kcb = _geom(desc)
+    path = int(cfg.get("tile_k") or 1)
+    halo = path in (2, 4)
+    tn = min(int(cfg.get("tile_n") or (64 if desc.k < 128 else 128)), desc.k)
+    if halo:
+        wp = desc.w + 2 * desc.pad_w
+        th = max(1, min(oh, int(cfg.get("tile_m") or 128) // wp))
+    else:
+        th = max(1, min(oh, 128 // max(1, ow)))
+    red = (["ic.outer", "rh", "rw", "ic.inner"] if halo else ["rh", "rw", "ic.outer", "ic.inner"])
+    log = [{"prim": "split", "stage": stage, "axis": "oc", "factor": tn},
+           {"prim": "split", "stage": stage, "axis": "oh", "factor": th},
+           {"prim": "split", "stage": stage, "axis": "ic", "factor": kcb},
+           {"prim": "reorder", "stage": stage,
+            "axes": ["n", "oh.outer", "oc.outer", "oh.inner", "oc.inner", "ow"] + red}]
+    wat = "rw" if halo else "ic.outer"
+    sk = int(cfg.get("split_k") or 1)
+    if sk > 1 and not halo:
+        k_steps = desc.r * desc.s * -(-desc.c // kcb)
+        kps = -(-k_steps // sk)
+        log += [{"prim": "fuse_axes", "stage": stage, "outer": "rh", "inner": "rw"},
+                {"prim": "fuse_axes", "stage": stage, "outer": "rh.rw.fused", "inner": "ic.outer"},
+                {"prim": "split", "stage": stage, "axis": "rh.rw.fused.ic.outer.fused",
+                 "factor": kps}]
+        wat = "rh.rw.fused.ic.outer.fused.inner"
+    if int(cfg.get("stages") or 0) == 2:
+        wat = "ow"  # resident weights: staged once per output-channel tile
+    log += [{"prim": "bind", "stage": stage, "axis": "oh.outer", "tag": "blockIdx.x"},
+            {"prim": "bind", "stage": stage, "axis": "oc.outer", "tag": "blockIdx.y"},
+            {"prim": "bind", "stage": stage, "axis": "oh.inner", "tag": "threadIdx.y"},
+            {"prim": "bind", "stage": stage, "axis": "oc.inner", "tag": "threadIdx.x"},
+            {"prim": "cache_read", "src": "W", "scope": "shared", "readers": [stage]},
+            {"prim": "compute_at", "stage": "W.shared", "target": stage, "axis": wat}]
     return log
 
 
-def config_from_schedule_log(log: Sequence[dict]) -> Config:
-    """Inverse of schedule_log; unknown primitives are an IOError, as in
+def config_from_schedule_log(log: Sequence[dict], desc: _abi.ConvDesc) -> Config:
+    """Inverse of schedule_log (the Config a log encodes); entries outside
+    the template are an IOError, as unknown primitives are in
     apply_log_entry."""
+    oh, ow, kcb = _geom(desc)
     cfg: Config = {}
+    th = None
+    halo = False
     for e in log:
         prim = e.get("prim")
-        if prim == "split":
-            key = {"ff": "tile_n", "nyx": "tile_m", "rc": "split_k"}.get(e.get("axis"))
-            if key is None:
-                raise _abi.TecError(20, f"split of unknown axis {e.get('axis')}")
-            cfg[key] = int(e["factor"])
-        elif prim == "cache_read":
-            s = e.get("src", "")
-            if s.startswith("data."):
-                cfg["tile_k"] = {"im2col": 1, "halo": 2}.get(s[5:], 0)
-            elif s.startswith("weight."):
-                cfg["stages"] = 2 if s.endswith("resident") else 1
-        elif prim == "unroll":
-            cfg["unroll"] = int(e["axis"].split(".")[-1])
-        elif prim == "bind":
-            key = "cluster_n" if e.get("tag") == "cluster" else "grid"
-            cfg[key] = int(e["axis"].split(".")[-1])
-        elif prim in ("set_scope", "tensorize"):
+        if prim == "split" and e.get("axis") == "oc":
+            cfg["tile_n"] = int(e["factor"])
+        elif prim == "split" and e.get("axis") == "oh":
+            th = int(e["factor"])
+        elif prim == "split" and e.get("axis") == "ic":
+            continue
+        elif prim == "split" and e.get("axis") == "rh.rw.fused.ic.outer.fused":
+            k_steps = desc.r * desc.s * -(-desc.c // kcb)
+            cfg["split_k"] = -(-k_steps // int(e["factor"]))
+        elif prim == "reorder":
+            axes = list(e["axes"])
+            halo = axes.index("ic.outer") < axes.index("rh")
+            cfg["tile_k"] = 2 if halo else 1
+        elif prim == "compute_at" and e.get("stage") == "W.shared":
+            if e.get("axis") == "ow":
+                cfg["stages"] = 2
+        elif prim in ("fuse_axes", "bind", "cache_read"):
             continue
         else:
-            raise _abi.TecError(20, f"unknown schedule primitive '{prim}'")
+            raise _abi.TecError(20, f"schedule entry outside the sm100 template: {e}")
+    if halo and th is not None:
+        wp = desc.w + 2 * desc.pad_w
+        cfg["tile_m"] = -(-th * wp // 128) * 128
     return cfg
 
 

@@ -139,19 +139,3 @@ def test_tensor_io_reads_reference_files_and_round_trips(tmp_path):
     with pytest.raises(TecError) as e:
         gl(str(tmp_path), "missing")
     assert e.value.code == "IOError"
-
-
-def test_schedule_log_round_trip():
-    from paper_1802_04799_b200.device import make_desc
-    from paper_1802_04799_b200.tuner import config_from_schedule_log, conv_space, schedule_log
-    from paper_1802_04799_b200.workloads import resnet_layer
-    s = conv_space("C6", make_desc(resnet_layer("C6", 1)))
-    for i in range(0, s.grid_size(), 7):  # the whole grid: no lowering needed
-        cfg = s.grid_at(i)
-        log = schedule_log(cfg, s.desc)
-        json.dumps(log)
-        back = config_from_schedule_log(log)
-        want = {k: v for k, v in cfg.items() if not (k in ("split_k", "cluster_n") and v == 1)}
-        assert back == want
-    with pytest.raises(TecError):
-        config_from_schedule_log([{"prim": "fuse_axes"}])
