@@ -452,13 +452,18 @@ def impl_ours(args):
         rargs.global_batch = args.global_batch or 256
         rargs.no_cpu_baseline = True
         rargs.steps = min(args.steps, 50)
-        rl = bench_workloads.resnet18_line(rargs, sys.modules[__name__], knobs_file=knobs_path)
-        if rl is not None:
-            resnet = {"img_s": rl["value"], "unit": "img/s", "global_batch": rargs.global_batch,
-                      "n_gpus": rl["n_gpus"], "ms_per_step": rl["ms_per_step"],
-                      "scaling": "strong", "dtype": "bf16", "e2e_img_s": rl["e2e"]["value"],
-                      "roofline_frac": rl["roofline"]["frac"],
-                      "config": rl["config"]["workload"]}
+        resnet = {}
+        for rc in ("bf16", "f32tc"):
+            rl = bench_workloads.resnet18_line(rargs, sys.modules[__name__], knobs_file=knobs_path,
+                                               compute=rc)
+            if rl is not None:
+                resnet[rc] = {"img_s": rl["value"], "unit": "img/s",
+                              "global_batch": rargs.global_batch, "n_gpus": rl["n_gpus"],
+                              "ms_per_step": rl["ms_per_step"], "scaling": "strong",
+                              "dtype": rl["dtype"], "e2e_img_s": rl["e2e"]["value"],
+                              "roofline_frac": rl["roofline"]["frac"],
+                              "config": rl["config"]["workload"]}
+        resnet = resnet or None
 
     # ---- configs[2]: MobileNet D1-D9 depthwise + bias + relu, batch 64
     # (HBM-bound; GB/s against the HBM roofline), bf16 and f32

@@ -73,7 +73,7 @@ def resnet18(args, bench):
         print(json.dumps(line), flush=True)
 
 
-def resnet18_line(args, bench, knobs_file=None):
+def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
     """ResNet-18 b256 strong-scaling measurement; returns rank 0's JSON
     line (None on other ranks). Knobs: `knobs_file`'s "resnet18_bf16" entry
     ({fused node id: knobs}) when present, else tuned live (or defaults
@@ -91,10 +91,10 @@ def resnet18_line(args, bench, knobs_file=None):
     knobs = None
     if knobs_file and os.path.exists(knobs_file):
         with open(knobs_file) as f:
-            knobs = json.load(f).get("resnet18_bf16")
+            knobs = json.load(f).get(f"resnet18_{compute}")
     if knobs is None:
-        knobs = _tune_graph_convs(g, local, args) if not args.no_tune else {}
-    dg = DeviceGraph(g, compute="bf16", device=local, knobs=knobs)
+        knobs = _tune_graph_convs(g, local, args, compute) if not args.no_tune else {}
+    dg = DeviceGraph(g, compute=compute, device=local, knobs=knobs)
     rng = np.random.default_rng(1234)  # same weights on every rank (replicated)
     params = {}
     for n in g.nodes:
@@ -160,13 +160,14 @@ def resnet18_line(args, bench, knobs_file=None):
         e2e_step()
     torch.cuda.synchronize()
     e2e_ms = _max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps)
-    peak_tf = bench.load_peaks()[0]
+    peak_tf = bench.load_peaks()[0] / (6.0 if compute == "f32tc" else 1.0)
     line = {
         "metric": "ResNet-18 inference img/s (config 4)", "value": round(img_s, 1),
         "unit": "img/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"configs[4]: ResNet-18 224x224 inference, global batch {gb} "
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": {"bf16": "bf16", "f32tc": "f32"}[compute], "data": "synthetic",
+        "config": {"workload": f"configs[3]: ResNet-18 224x224 inference ({compute}), global batch {gb} "
                                f"sharded {cnt}/rank, random-init weights, BN folded",
                    "global_batch": gb, "parallelism": f"batch-sharded x{ws}, logits gathered",
                    "timing": "CUDA graph of the whole network per rank, events, max over ranks"},
@@ -190,9 +191,9 @@ def resnet18_line(args, bench, knobs_file=None):
     return line if rank == 0 else None
 
 
-def _tune_graph_convs(g, device, args):
-    """Tune each distinct conv shape of the graph once (bf16, bias+relu
-    epilogue as the stand-in cost); returns knobs keyed by fused node id."""
+def _tune_graph_convs(g, device, args, compute="bf16"):
+    """Tune each distinct conv shape of the graph once (bias+relu epilogue
+    as the stand-in cost); returns knobs keyed by fused node id."""
     from paper_1802_04799_b200 import _abi
     from paper_1802_04799_b200.graph import fuse_pass
     from paper_1802_04799_b200.ops import conv_desc
@@ -205,11 +206,12 @@ def _tune_graph_convs(g, device, args):
         root = n.members[0]
         xs = f.node(root.inputs[0]).out_type.shape if f.find(root.inputs[0]) else None
         ws_ = f.node(root.inputs[1]).out_type.shape
-        d = conv_desc("conv2d", xs, ws_, root.attrs, _abi.COMPUTE_BF16)
+        d = conv_desc("conv2d", xs, ws_, root.attrs,
+                      {"bf16": _abi.COMPUTE_BF16, "f32tc": _abi.COMPUTE_F32TC}[compute])
         key = (tuple(xs), tuple(ws_), tuple(root.attrs.get("strides", (1, 1))))
         if key not in best:
             space = conv_space(str(key), d)
-            rec = tune(space, budget=space.size(), batch_size=space.size(), method="random",
+            rec = tune(space, budget=min(space.size(), 16), batch_size=8, method="ml",
                        devices=[device], repeats=3)
             best[key] = rec.config if rec else {}
         out[n.id] = best[key]

@@ -166,6 +166,10 @@ tec_status tec_activation_pack(const tec_conv_desc* d, const void* x_nchw,
 /* OIHW f32 (or i8) -> packed weights (KRSC, or [R][S][C] for depthwise). */
 tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
                                    void* w_packed, void* stream);
+/* f32 NHWC [n*h*w][c] (an f32tc layer's output) -> the packed input of an
+ * f32tc dense conv (its three exact bf16 planes), without the NCHW detour. */
+tec_status tec_activation_pack_nhwc(const tec_conv_desc* d, const void* x_nhwc_f32,
+                                    void* x_packed, void* stream);
 /* NCHW (f32 / i32) -> NHWC in out_dtype (residual/mul operands). */
 tec_status tec_nchw_to_nhwc(const void* src, int32_t src_dtype, void* dst,
                             int32_t dst_dtype, int64_t n, int64_t c,
@@ -263,7 +267,8 @@ typedef enum {
   TEC_STEP_PACK = 4,       /* tec_activation_pack(conv, src -> dst)         */
   TEC_STEP_UNPACK = 5,     /* tec_output_unpack(src, src_dtype -> dst)      */
   TEC_STEP_TO_NHWC = 6,    /* tec_nchw_to_nhwc(src, src_dtype -> dst)       */
-  TEC_STEP_DEPTHWISE = 7   /* tec_depthwise_fused                           */
+  TEC_STEP_DEPTHWISE = 7,  /* tec_depthwise_fused                           */
+  TEC_STEP_PACK_NHWC = 8   /* tec_activation_pack_nhwc(conv, src -> dst)    */
 } tec_step_kind;
 
 typedef struct {

@@ -88,8 +88,8 @@ class ConvLayout(C.Structure):
                 ("out_elems", C.c_int64)]
 
 
-STEP_CONV, STEP_MAX_POOL, STEP_AVG_POOL, STEP_PACK, STEP_UNPACK, STEP_TO_NHWC, STEP_DEPTHWISE = \
-    1, 2, 3, 4, 5, 6, 7
+STEP_CONV, STEP_MAX_POOL, STEP_AVG_POOL, STEP_PACK, STEP_UNPACK, STEP_TO_NHWC, STEP_DEPTHWISE, \
+    STEP_PACK_NHWC = 1, 2, 3, 4, 5, 6, 7, 8
 
 
 class Step(C.Structure):
@@ -112,6 +112,7 @@ SIGNATURES = {
     "tec_conv_infer": (C.c_int32, [_DESC, C.POINTER(C.c_int64)]),
     "tec_conv_layout_of": (C.c_int32, [_DESC, C.POINTER(ConvLayout)]),
     "tec_activation_pack": (C.c_int32, [_DESC, _P, _P, _P]),
+    "tec_activation_pack_nhwc": (C.c_int32, [_DESC, _P, _P, _P]),
     "tec_weight_pretransform": (C.c_int32, [_DESC, _P, _P, _P]),
     "tec_nchw_to_nhwc": (C.c_int32, [_P, C.c_int32, _P, C.c_int32, C.c_int64,
                                      C.c_int64, C.c_int64, C.c_int64, _P]),

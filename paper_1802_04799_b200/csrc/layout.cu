@@ -432,7 +432,63 @@ __global__ void pack_weights_split3i_kernel(const InT* __restrict__ w, __nv_bflo
   }
 }
 
+// f32 NHWC [pixels][c] (an f32tc layer's output) -> the next f32tc conv's
+// packed input: three exact bf16 planes per pixel, [h | m | l] blocks of cpp
+// channels (cp = 3 * cpp) or interleaved [h16 | m16 | l16 | 0] (cp = 64).
+__global__ void split3_nhwc_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   int64_t pixels, int64_t c, int64_t cp, int64_t cpp) {
+  const int64_t total = pixels * cp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t px = i / cp, ch = i - px * cp;
+    const int64_t plane = ch / cpp, cc = ch - plane * cpp;
+    const float v = plane < 3 && cc < c ? in[px * c + cc] : 0.0f;
+    out[i] = split3(v, static_cast<int>(plane < 3 ? plane : 0));
+  }
+}
+
+// Vector form (c == cpp, c % 4 == 0, planes in blocks): a thread reads 4
+// channels (16 B) and writes 4 bf16 (8 B) into each plane.
+__global__ void split3_nhwc_vec_kernel(const float4* __restrict__ in, uint2* __restrict__ out,
+                                       int64_t pixels, int c4) {
+  const int64_t total = pixels * c4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t px = i / c4;
+    const int q = static_cast<int>(i - px * c4);
+    const float4 v = in[i];
+    const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl) {
+      uint32_t h[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t lo = __bfloat16_as_ushort(split3(f[2 * j], pl));
+        const uint32_t hi = __bfloat16_as_ushort(split3(f[2 * j + 1], pl));
+        h[j] = lo | (hi << 16);
+      }
+      out[(px * 3 + pl) * c4 + q] = make_uint2(h[0], h[1]);
+    }
+  }
+}
+
 // ----------------------------------------------------------- launchers
+int launch_split3_nhwc(const float* in, void* out, int64_t pixels, int64_t c, int64_t cp,
+                       int64_t cpp, cudaStream_t st) {
+  if (c == cpp && cp == 3 * cpp && c % 4 == 0) {
+    const int64_t total = pixels * (c / 4);
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 32)));
+    split3_nhwc_vec_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in),
+                                                   static_cast<uint2*>(out), pixels,
+                                                   static_cast<int>(c / 4));
+    return cudaGetLastError();
+  }
+  const int64_t total = pixels * cp;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 32)));
+  split3_nhwc_kernel<<<blocks, 256, 0, st>>>(in, static_cast<__nv_bfloat16*>(out), pixels, c, cp,
+                                             cpp);
+  return cudaGetLastError();
+}
 int launch_pack_weights_split3i(const void* w, void* out, int64_t k, int64_t c, int64_t r,
                                 int64_t s, int64_t r2, int64_t s2, int s2d, cudaStream_t st) {
   const int64_t taps = s2d ? r2 * s2 : r * s;

@@ -42,6 +42,8 @@ int launch_depthwise(const DepthwiseParams& p, int tw, cudaStream_t st);
 int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c, int64_t h,
                     int64_t w, int64_t ph, int64_t pw, int64_t h2, int64_t w2, int64_t cp,
                     int mode, cudaStream_t st);
+int launch_split3_nhwc(const float* in, void* out, int64_t pixels, int64_t c, int64_t cp,
+                       int64_t cpp, cudaStream_t st);
 int launch_pack_weights_split3i(const void* w, void* out, int64_t k, int64_t c, int64_t r,
                                 int64_t s, int64_t r2, int64_t s2, int s2d, cudaStream_t st);
 int launch_pack_weights_s2d(const void* w, int in_type, void* out, int64_t k, int64_t c,
@@ -136,11 +138,94 @@ using EncodeIm2colFn = CUresult (*)(
     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 struct DriverFns {
-  EncodeTiledFn tiled = nullptr;
-  EncodeIm2colFn im2col = nullptr;
+  EncodeTiledFn tiled = nullptr;    // cached (tensor-map cache below)
+  EncodeIm2colFn im2col = nullptr;  // cached
+  EncodeTiledFn raw_tiled = nullptr;
+  EncodeIm2colFn raw_im2col = nullptr;
   int driver_version = 0;
   bool ok = false;
 };
+
+const DriverFns& driver_fns();
+
+// Tensor-map cache (the library-owned state of SURVEY 8b): an encoded
+// CUtensorMap is a pure function of its arguments (address, dims, strides,
+// box, swizzle, ...), so eager launches reuse it instead of re-encoding on
+// every call. Keyed by the argument bytes; a mutex on the map, bounded.
+struct MapCache {
+  std::mutex mu;
+  std::map<std::string, CUtensorMap> maps;
+};
+MapCache& map_cache() {
+  static MapCache c;
+  return c;
+}
+template <typename T>
+void key_add(std::string* k, const T* p, size_t n) {
+  k->append(reinterpret_cast<const char*>(p), n * sizeof(T));
+}
+CUresult cached_tiled(CUtensorMap* tm, CUtensorMapDataType dt, cuuint32_t rank, void* addr,
+                      const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                      const cuuint32_t* estr, CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                      CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob) {
+  std::string k("T");
+  const int64_t scal[7] = {(int64_t)dt, (int64_t)rank, (int64_t)(uintptr_t)addr, (int64_t)il,
+                           (int64_t)sw, (int64_t)l2, (int64_t)oob};
+  key_add(&k, scal, 7);
+  key_add(&k, dims, rank);
+  key_add(&k, strides, rank > 0 ? rank - 1 : 0);
+  key_add(&k, box, rank);
+  key_add(&k, estr, rank);
+  MapCache& c = map_cache();
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.maps.find(k);
+    if (it != c.maps.end()) {
+      *tm = it->second;
+      return CUDA_SUCCESS;
+    }
+  }
+  const CUresult r =
+      driver_fns().raw_tiled(tm, dt, rank, addr, dims, strides, box, estr, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) {
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (c.maps.size() >= 4096) c.maps.clear();
+    c.maps.emplace(std::move(k), *tm);
+  }
+  return r;
+}
+CUresult cached_im2col(CUtensorMap* tm, CUtensorMapDataType dt, cuuint32_t rank, void* addr,
+                       const cuuint64_t* dims, const cuuint64_t* strides, const int* lower,
+                       const int* upper, cuuint32_t ch, cuuint32_t px, const cuuint32_t* estr,
+                       CUtensorMapInterleave il, CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                       CUtensorMapFloatOOBfill oob) {
+  std::string k("I");
+  const int64_t scal[9] = {(int64_t)dt, (int64_t)rank, (int64_t)(uintptr_t)addr, (int64_t)ch,
+                           (int64_t)px, (int64_t)il, (int64_t)sw, (int64_t)l2, (int64_t)oob};
+  key_add(&k, scal, 9);
+  key_add(&k, dims, rank);
+  key_add(&k, strides, rank > 0 ? rank - 1 : 0);
+  key_add(&k, lower, rank > 2 ? rank - 2 : 0);
+  key_add(&k, upper, rank > 2 ? rank - 2 : 0);
+  key_add(&k, estr, rank);
+  MapCache& c = map_cache();
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.maps.find(k);
+    if (it != c.maps.end()) {
+      *tm = it->second;
+      return CUDA_SUCCESS;
+    }
+  }
+  const CUresult r = driver_fns().raw_im2col(tm, dt, rank, addr, dims, strides, lower, upper,
+                                             ch, px, estr, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) {
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (c.maps.size() >= 4096) c.maps.clear();
+    c.maps.emplace(std::move(k), *tm);
+  }
+  return r;
+}
 
 const DriverFns& driver_fns() {
   static DriverFns fns;
@@ -154,10 +239,12 @@ const DriverFns& driver_fns() {
         cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p2,
                                 cudaEnableDefault, &q2) != cudaSuccess)
       return;
-    fns.tiled = reinterpret_cast<EncodeTiledFn>(p1);
-    fns.im2col = reinterpret_cast<EncodeIm2colFn>(p2);
+    fns.raw_tiled = reinterpret_cast<EncodeTiledFn>(p1);
+    fns.raw_im2col = reinterpret_cast<EncodeIm2colFn>(p2);
+    fns.tiled = &cached_tiled;
+    fns.im2col = &cached_im2col;
     cudaDriverGetVersion(&fns.driver_version);
-    fns.ok = fns.tiled && fns.im2col;
+    fns.ok = fns.raw_tiled && fns.raw_im2col;
   });
   return fns;
 }
@@ -1298,6 +1385,20 @@ tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
   return TEC_OK;
 }
 
+tec_status tec_activation_pack_nhwc(const tec_conv_desc* d, const void* x_nhwc_f32,
+                                    void* x_packed, void* stream) {
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  if (d->compute != TEC_COMPUTE_F32TC || d->depthwise || pl.s2d)
+    return fail(TEC_E_LOWERING, "NHWC packing is the f32tc dense-conv input (no space-to-depth)");
+  const int e = launch_split3_nhwc(static_cast<const float*>(x_nhwc_f32), x_packed,
+                                   d->n * d->h * d->w, d->c, pl.cp, pl.inter ? 16 : pl.cpp,
+                                   (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "split3_nhwc");
+  return TEC_OK;
+}
+
 tec_status tec_nchw_to_nhwc(const void* src, int32_t src_dtype, void* dst,
                             int32_t dst_dtype, int64_t n, int64_t c, int64_t h,
                             int64_t w, void* stream) {
@@ -1857,6 +1958,8 @@ tec_status run_step(const tec_plan* p, const tec_step& s, void* stream) {
       return tec_output_unpack(s.src, s.src_dtype, s.dst, s.dst_dtype, s.n, s.c, s.h, s.w_, stream);
     case TEC_STEP_TO_NHWC:
       return tec_nchw_to_nhwc(s.src, s.src_dtype, s.dst, s.dst_dtype, s.n, s.c, s.h, s.w_, stream);
+    case TEC_STEP_PACK_NHWC:
+      return tec_activation_pack_nhwc(&s.conv, s.src, s.dst, stream);
     default:
       return fail(TEC_E_INTERNAL, "unknown plan step kind " + std::to_string(s.kind));
   }

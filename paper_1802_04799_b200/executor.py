@@ -131,12 +131,16 @@ def f32_output(n: GraphNode) -> bool:
 class DeviceGraph:
     def __init__(self, g: ComputeGraph, compute: str = "bf16", device: int = 0,
                  knobs: Optional[Dict[str, dict]] = None):
-        if compute not in ("bf16", "f32"):
-            raise TecError(E_LOWERING, f"executor compute mode '{compute}' (bf16 | f32)")
+        if compute not in ("bf16", "f32", "f32tc"):
+            raise TecError(E_LOWERING, f"executor compute mode '{compute}' (bf16 | f32 | f32tc)")
         self.lib = _abi.load()
         self.dev = torch.device("cuda", device)
         self.compute = compute
-        self.cmode = _abi.COMPUTE_BF16 if compute == "bf16" else _abi.COMPUTE_F32
+        # f32tc: every conv on the tensor cores at f32 (conv_f32tc.cu), f32
+        # NHWC activations between layers, each conv's input packed into its
+        # three bf16 planes by a layout step
+        self.cmode = {"bf16": _abi.COMPUTE_BF16, "f32": _abi.COMPUTE_F32,
+                      "f32tc": _abi.COMPUTE_F32TC}[compute]
         self.act_dt = _abi.DT_BF16 if compute == "bf16" else _abi.DT_F32
         self.knobs = knobs or {}
         self.fused = fuse_pass(g)
@@ -283,6 +287,14 @@ class DeviceGraph:
                   and not (self.cmode == _abi.COMPUTE_F32 and not d.depthwise))
         if direct:
             return src.ptr()
+        if (self.cmode == _abi.COMPUTE_F32TC and not d.depthwise and src.layout == "nhwc"
+                and src.dtype == _abi.DT_F32
+                and not (d.stride_h == 2 and d.stride_w == 2 and 4 * d.c <= 16)):  # not s2d
+            # f32 NHWC -> the conv's three bf16 planes in one pass
+            packed = self._scratch(lay.act_bytes)
+            self.steps.append(_abi.Step(kind=_abi.STEP_PACK_NHWC, conv=d, src=src.ptr(),
+                                        dst=packed.data_ptr()))
+            return packed.data_ptr()
         # src -> NCHW f32 (the reference layout) -> tec_activation_pack
         if src.layout == "nchw" and src.dtype == _abi.DT_F32:
             nchw = src.buf

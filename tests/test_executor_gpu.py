@@ -203,3 +203,39 @@ def test_native_plan_runtime_steps_and_errors():
     st = lib.tec_plan_create((_abi.Step * 1)(bad), 1, C.byref(h))
     assert st != 0 and not h.value
     assert lib.tec_plan_run_steps(dg._native, dg.n_launches, 1, None) != 0  # out of range
+
+
+# f32tc whole-network bar: per conv the 1e-4 comparator holds (node by node,
+# tests/test_integration_gpu.py); through a network the differences compound
+TOL_NET_F32TC = 1e-3
+
+
+@pytest.mark.parametrize("name", ["fc_head", "tiny_resnet_body"])
+def test_executor_f32tc_vs_reference(name):
+    """Reference precision on the tensor cores: every conv of the graph in
+    f32tc, against the reference's own evaluate_graph output."""
+    from oracle.oracle_api import same_values
+    d, g, inputs = _golden(name)
+    dg = DeviceGraph(g, compute="f32tc")
+    feeds, params = _split(dg, inputs)
+    dg.bind_params(params)
+    out = dg.run(feeds)
+    for o in g.outputs:
+        want = load_tensor(os.path.join(d, "out"), o)
+        assert same_values(out[o].reshape(want.shape), want, TOL_NET_F32TC), o
+
+
+def test_resnet18_f32tc_end_to_end():
+    """Full ResNet-18 at batch 2, f32 on the tensor cores, vs the f32 graph
+    oracle (the reference's arithmetic), captured replay bit-stable."""
+    from oracle.oracle_api import same_values
+    g = resnet18_graph(2)
+    dg = DeviceGraph(g, compute="f32tc")
+    vals = _resnet_inputs(g)
+    feeds, params = _split(dg, vals)
+    dg.bind_params(params)
+    out = dg.run(feeds)["logits"]
+    want = graph_oracle.evaluate(fuse_pass(g), feeds, params, "f32")["logits"]
+    assert same_values(out, want, TOL_NET_F32TC)
+    dg.capture()
+    assert np.array_equal(out, dg.run(feeds)["logits"])
