@@ -495,7 +495,9 @@ def impl_ours(args):
     if os.path.exists(tp):
         try:
             tj = json.load(open(tp)).get(headline) or {}
-            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
+            # the roofline covers the 12 launches of a step: their DRAM bytes
+            # (ncu launch list of this same step, cold caches)
+            traffic, traffic_src = tj.get("dram_bytes_per_step"), tj.get("source")
         except Exception:
             traffic = None
 
