@@ -83,18 +83,23 @@ struct F32tcCfg {
   static constexpr int kStage = (HALO ? 0 : kAPlanes * kA) + (RES ? 0 : kBStage);
   static constexpr int kKSteps = INTER ? 1 : SWZ / 32;  // K16 steps per plane per stage
   // GRP (BN = 64): the products sharing an operand run as ONE MMA on the
-  // N-concatenated planes -- A_h x [B_h|B_m|B_l] (N=192), A_m x [B_h|B_m]
-  // (N=128), A_l x B_h (N=64): 3 MMAs instead of 6 N=64 ones, whose rate is
-  // bound by re-reading A from shared memory (54 vs 32 cycles each,
-  // tools/microbench/RESULTS.md). TMEM: chunk ring X 2 x 192 (hh|hm|hl) +
-  // one tile accumulator Y 128 (mh+lh | mm) = 512 columns. (Measured: C2 b64
-  // 98 -> 86 us; a 4-MMA form with a double-buffered Y -- X = A_h x
-  // [B_h|B_m], A_h x B_l into Y -- was slower, C1 197 vs 169 us.)
-  // Otherwise (BN = 128): six N=128 MMAs; chunk ring S 2 x BN + tile
-  // accumulators T 2 x BN.
+  // N-concatenated planes -- A_h x [B_h|B_m|B_l] (N=192) into the chunk
+  // accumulator X = [hh | hm | hl]; A_m x [B_h|B_m] (N=128) into X[64:192]
+  // (mh onto hm, mm onto hl: all cross terms) and A_l x B_h (N=64) into
+  // X[64:128] -- 3 MMAs instead of 6 N=64 ones, whose rate is bound by
+  // re-reading A from shared memory (54 vs 32 cycles each,
+  // tools/microbench/RESULTS.md). Everything folds per chunk, so there is no
+  // tile accumulator and no tile-boundary wait for the epilogue: TMEM = X
+  // ring 2 x 192. (Measured before: with the cross terms of A_m / A_l in a
+  // single-buffered tile accumulator the MMA waited for the epilogue at every
+  // tile start -- 17 % of C1; a 4-MMA form with a double-buffered one was
+  // slower still, C1 197 vs 169 us.)
+  // Otherwise (BN = 128): six N=128 MMAs; chunk ring S 2 x BN (hh) + tile
+  // accumulators T 2 x BN (cross terms over the whole tile).
   static constexpr bool kGrp = BN == 64;
+  static constexpr bool kHasY = !kGrp;
   static constexpr int kXCols = kGrp ? 3 * BN : BN;     // chunk accumulator width
-  static constexpr int kYCols = kGrp ? 2 * BN : BN;     // tile accumulator width
+  static constexpr int kYCols = kGrp ? 0 : BN;          // tile accumulator width
   static constexpr int kYBufs = kGrp ? 1 : 2;
   static constexpr int kYBase = 2 * kXCols;
   static constexpr uint32_t kTmemCols = 2 * kXCols + kYBufs * kYCols <= 256 ? 256 : 512;
@@ -345,8 +350,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
         const int tb = local % Cfg::kYBufs;
         const int tuse = local / Cfg::kYBufs;
-        twait(&tempty[tb], (tuse & 1) ^ 1, prof, &dw[2]);
-        tc_fence_after();
+        if (Cfg::kHasY) {
+          twait(&tempty[tb], (tuse & 1) ^ 1, prof, &dw[2]);
+          tc_fence_after();
+        }
         const uint32_t t_tmem = tmem_base + Cfg::kYBase + tb * Cfg::kYCols;
         uint32_t s_tmem = tmem_base;
         int in_chunk = 0;
@@ -371,11 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_acc = (first && kk == 0) ? 0u : 1u;
             const uint32_t s_acc = (in_chunk | kk) != 0 ? 1u : 0u;
             if constexpr (Cfg::kGrp) {
-              // X[0:192] += A_h x [B_h|B_m|B_l]; Y[0:128] += A_m x [B_h|B_m];
-              // Y[0:64] += A_l x B_h
+              // X[0:192] += A_h x [B_h|B_m|B_l]; X[64:192] += A_m x [B_h|B_m];
+              // X[64:128] += A_l x B_h
               tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc3, s_acc);
-              tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc2, t_acc);
-              tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
+              tc_mma<MmaKind::kF16>(s_tmem + BN, am, bh, idesc2, 1u);
+              tc_mma<MmaKind::kF16>(s_tmem + BN, al, bh, idesc, 1u);
             } else {
               const uint64_t bm = make_smem_desc<kBSW>(b0 + kPlaneB, 8 * kBSW);
               const uint64_t bl = make_smem_desc<kBSW>(b0 + 2 * kPlaneB, 8 * kBSW);
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        tc_commit(&tfull[tb]);
+        if (Cfg::kHasY) tc_commit(&tfull[tb]);
       }
     }
   } else if (warp >= 4) {
@@ -511,23 +518,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           fold(cross, xb + 2 * BN);
         }
         tc_fence_before();
-        mbar_arrive(&sempty[sb]);
+        // GRP (no tile accumulator): the fault test drops a chunk arrive
+        if (!(Cfg::kGrp && p.fault == 1 && local == 0 && c == 0)) mbar_arrive(&sempty[sb]);
       }
-      // + the tile's cross-term accumulator
-      const int tb = local % Cfg::kYBufs;
-      twait(&tfull[tb], (local / Cfg::kYBufs) & 1, prof, &dw[6]);
-      tc_fence_after();
-      const uint32_t yb = lane_base + Cfg::kYBase + tb * Cfg::kYCols;
-      if constexpr (Cfg::kGrp) {
-        fold(cross, yb);
-        fold(cross, yb + BN);
-      } else {
-        fold(sum, yb);
+      if constexpr (Cfg::kHasY) {
+        // + the tile's cross-term accumulator
+        const int tb = local % Cfg::kYBufs;
+        twait(&tfull[tb], (local / Cfg::kYBufs) & 1, prof, &dw[6]);
+        tc_fence_after();
+        fold(sum, lane_base + Cfg::kYBase + tb * Cfg::kYCols);
+        tc_fence_before();
+        // p.fault == 1 (tests only): lose one arrive -- the MMA warp then
+        // waits for this accumulator forever and the mbarrier watchdog must trap
+        if (!(p.fault == 1 && local == 0)) mbar_arrive(&tempty[tb]);
       }
-      tc_fence_before();
-      // p.fault == 1 (tests only): lose one arrive -- the MMA warp then waits
-      // for this accumulator forever and the mbarrier watchdog must trap
-      if (!(p.fault == 1 && local == 0)) mbar_arrive(&tempty[tb]);
       if constexpr (Cfg::kGrp) {
 #pragma unroll
         for (int j = 0; j < HB; ++j) sum[j] = __fadd_rn(sum[j], cross[j]);
