@@ -33,6 +33,10 @@
 //         random_tensor feeds; saves D, W, interp and reference outputs;
 //         prints {"features": extract_features, "log", "cost", "matches"} --
 //         the legality check, the reference features and the second oracle.
+//   serve <seconds>
+//         the reference's own WorkerServer (R/src/rpc.cpp:129-181) on an
+//         ephemeral 127.0.0.1 port, printed as {"port": p}; stops after
+//         <seconds> -- pins the RPC framing of paper_1802_04799_b200/rpc.py.
 //   bench <op> <C> <H> <W> <OC> <K> <stride> <pad> <rows> <seed> [dtype]
 //         times eval_graph_node (R/src/graph.cpp:209) on the fused node
 //         [conv2d|depthwise_conv2d, bias_add, relu] built exactly as
@@ -49,7 +53,9 @@
 #include "tec/graph.hpp"
 #include "tec/interp.hpp"
 #include "tec/lower.hpp"
+#include "tec/rpc.hpp"
 #include "tec/schedule.hpp"
+#include <thread>
 #include "tec/texpr.hpp"
 #include "tec/graph_passes.hpp"
 #include "tec/io.hpp"
@@ -157,6 +163,15 @@ static int cmd_sched(const std::string& in_path, const std::string& out_dir) {
   return 0;
 }
 
+static int cmd_serve(int seconds) {
+  WorkerServer srv(0);
+  std::printf("{\"port\": %d}\n", srv.port());
+  std::fflush(stdout);
+  std::this_thread::sleep_for(std::chrono::seconds(seconds));
+  srv.stop();
+  return 0;
+}
+
 static int cmd_gen(int argc, char** argv) {
   std::string dir = argv[2], name = argv[3];
   DType dt = dtype_from_name(argv[4]);
@@ -227,6 +242,7 @@ int main(int argc, char** argv) {
     if (cmd == "gen" && argc >= 7) return cmd_gen(argc, argv);
     if (cmd == "gbt" && argc == 4) return cmd_gbt(argv[2], argv[3]);
     if (cmd == "sched" && argc == 4) return cmd_sched(argv[2], argv[3]);
+    if (cmd == "serve" && argc == 3) return cmd_serve(std::stoi(argv[2]));
     if (cmd == "bench" && argc >= 12) return cmd_bench(argc, argv);
     std::fprintf(stderr, "bad arguments for '%s'\n", cmd.c_str());
     return 2;
