@@ -256,6 +256,46 @@ tec_status tec_max_pool2d(const tec_pool_desc* d, const void* x, void* y, void* 
 tec_status tec_global_avg_pool(const tec_pool_desc* d, const void* x, void* y, void* stream);
 tec_status tec_pool_infer(const tec_pool_desc* d, int64_t out_shape[4]);
 
+/* ---- unary integer graph operators around the int8 conv path (int8
+ * ResNet-18 end to end). Not in the reference registry (like
+ * the pools): new registered ops (graph.py "cast", "requantize"; the
+ * reference's own "scale" and "relu") whose semantics elementwise.cu states
+ * and tests/graph_oracle.py restates. A program is the member chain of one
+ * fused elementwise node, applied per element in member order:
+ *   CAST        i8 -> i32 exact; i8 | i32 -> f32 (round to nearest)
+ *   SCALE       integer data: x * c, integral |c| < 2^32, int64 product with
+ *               the i32 range check (DenseTensor::set_i) -> err flag, which
+ *               the caller reports as TEC_E_FOLD_OVERFLOW; f32 data: x * (float)c
+ *   RELU        max(x, 0)
+ *   REQUANTIZE  i32 -> i8: clamp((x * mult + 2^(shift-1)) >> shift, -128, 127),
+ *               1 <= mult < 2^31, 0 <= shift <= 62 (ties toward +inf)
+ * x / y: device buffers, 16-byte aligned; count elements (any layout). */
+typedef enum {
+  TEC_ELEM_CAST = 1,
+  TEC_ELEM_SCALE = 2,
+  TEC_ELEM_RELU = 3,
+  TEC_ELEM_REQUANTIZE = 4
+} tec_elem_kind;
+
+#define TEC_MAX_ELEM_OPS 4
+typedef struct {
+  int32_t n_ops;
+  int32_t kind[TEC_MAX_ELEM_OPS];   /* tec_elem_kind                         */
+  int32_t shift[TEC_MAX_ELEM_OPS];  /* REQUANTIZE                            */
+  int32_t cast_to[TEC_MAX_ELEM_OPS];/* CAST: target tec_dtype                */
+  int64_t mult[TEC_MAX_ELEM_OPS];   /* REQUANTIZE multiplier                 */
+  double scale[TEC_MAX_ELEM_OPS];   /* SCALE factor                          */
+  int32_t src_dtype, dst_dtype;     /* tec_dtype of x and y                  */
+  int64_t count;
+} tec_elem_prog;
+
+/* Validates the program against the dtypes (a chain whose value type does
+ * not end in dst_dtype, a REQUANTIZE of non-integer data, ... are
+ * TEC_E_LOWERING) and launches it. err_flag (device int32, may be null) is
+ * set to 1 on an i32 range overflow. */
+tec_status tec_elementwise(const tec_elem_prog* p, const void* x, void* y,
+                           int32_t* err_flag, void* stream);
+
 /* ---- native launch plans: the executor's run loop (evaluate_graph for
  * target sm100, R/src/graph.cpp:227-256). A compiled graph is a list of
  * steps on caller-owned device buffers; the plan runs them in order or
@@ -268,7 +308,8 @@ typedef enum {
   TEC_STEP_UNPACK = 5,     /* tec_output_unpack(src, src_dtype -> dst)      */
   TEC_STEP_TO_NHWC = 6,    /* tec_nchw_to_nhwc(src, src_dtype -> dst)       */
   TEC_STEP_DEPTHWISE = 7,  /* tec_depthwise_fused                           */
-  TEC_STEP_PACK_NHWC = 8   /* tec_activation_pack_nhwc(conv, src -> dst)    */
+  TEC_STEP_PACK_NHWC = 8,  /* tec_activation_pack_nhwc(conv, src -> dst)    */
+  TEC_STEP_ELEMWISE = 9    /* tec_elementwise(elem, src -> dst)             */
 } tec_step_kind;
 
 typedef struct {
@@ -282,6 +323,7 @@ typedef struct {
   const void* w;           /* CONV, DEPTHWISE: packed weights               */
   void* dst;               /* output                                        */
   int64_t n, c, h, w_;     /* UNPACK / TO_NHWC logical NCHW dims            */
+  tec_elem_prog elem;      /* ELEMWISE */
 } tec_step;
 
 typedef struct tec_plan tec_plan;
@@ -296,6 +338,11 @@ tec_status tec_plan_capture(tec_plan* plan, void* stream);
 /* Runs steps [first, first + count) eagerly (per-launch profiling). */
 tec_status tec_plan_run_steps(tec_plan* plan, int32_t first, int32_t count, void* stream);
 int32_t tec_plan_size(const tec_plan* plan);
+/* Integer range overflow raised by any step since the last call (the plan
+ * owns one device flag that its conv and elementwise steps share):
+ * synchronizes `stream`, clears the flag, returns TEC_E_FOLD_OVERFLOW if it
+ * was set (the reference throws at the member that overflows). */
+tec_status tec_plan_status(tec_plan* plan, void* stream);
 void tec_plan_destroy(tec_plan* plan);
 
 /* ---- host-level path: eval_graph_node / native_eval for target sm100 ----

@@ -89,7 +89,18 @@ class ConvLayout(C.Structure):
 
 
 STEP_CONV, STEP_MAX_POOL, STEP_AVG_POOL, STEP_PACK, STEP_UNPACK, STEP_TO_NHWC, STEP_DEPTHWISE, \
-    STEP_PACK_NHWC = 1, 2, 3, 4, 5, 6, 7, 8
+    STEP_PACK_NHWC, STEP_ELEMWISE = 1, 2, 3, 4, 5, 6, 7, 8, 9
+
+ELEM_CAST, ELEM_SCALE, ELEM_RELU, ELEM_REQUANTIZE = 1, 2, 3, 4
+MAX_ELEM_OPS = 4
+
+
+class ElemProg(C.Structure):
+    """tec_elem_prog (include/tec_sm100.h): a unary member chain."""
+    _fields_ = [("n_ops", C.c_int32), ("kind", C.c_int32 * MAX_ELEM_OPS),
+                ("shift", C.c_int32 * MAX_ELEM_OPS), ("cast_to", C.c_int32 * MAX_ELEM_OPS),
+                ("mult", C.c_int64 * MAX_ELEM_OPS), ("scale", C.c_double * MAX_ELEM_OPS),
+                ("src_dtype", C.c_int32), ("dst_dtype", C.c_int32), ("count", C.c_int64)]
 
 
 class Step(C.Structure):
@@ -97,7 +108,8 @@ class Step(C.Structure):
     _fields_ = [("kind", C.c_int32), ("src_dtype", C.c_int32), ("dst_dtype", C.c_int32),
                 ("conv", ConvDesc), ("epi", Epilogue), ("knobs", Knobs), ("pool", PoolDesc),
                 ("src", C.c_void_p), ("w", C.c_void_p), ("dst", C.c_void_p),
-                ("n", C.c_int64), ("c", C.c_int64), ("h", C.c_int64), ("w_", C.c_int64)]
+                ("n", C.c_int64), ("c", C.c_int64), ("h", C.c_int64), ("w_", C.c_int64),
+                ("elem", ElemProg)]
 
 
 # Every symbol include/tec_sm100.h declares, with its ctypes signature.
@@ -137,6 +149,8 @@ SIGNATURES = {
     "tec_plan_capture": (C.c_int32, [_P, _P]),
     "tec_plan_run_steps": (C.c_int32, [_P, C.c_int32, C.c_int32, _P]),
     "tec_plan_size": (C.c_int32, [_P]),
+    "tec_plan_status": (C.c_int32, [_P, _P]),
+    "tec_elementwise": (C.c_int32, [C.POINTER(ElemProg), _P, _P, _P, _P]),
     "tec_plan_destroy": (None, [_P]),
 }
 

@@ -135,4 +135,21 @@ struct PoolParams {
   void* y;
 };
 
+// Unary member program of an elementwise graph node (elementwise.cu):
+// cast / scale / relu / requantize in member order.
+enum ElemOp : int32_t { kElemCast = 1, kElemScale = 2, kElemRelu = 3, kElemRequant = 4 };
+constexpr int kMaxElemOps = 4;
+
+struct ElemProg {
+  int32_t n_ops;
+  int32_t kind[kMaxElemOps];
+  int32_t shift[kMaxElemOps];      // REQUANTIZE
+  int32_t cast_to_f[kMaxElemOps];  // CAST: 1 = to f32 (else to an integer type)
+  int64_t mult[kMaxElemOps];       // REQUANTIZE multiplier / integral SCALE factor
+  float fscale[kMaxElemOps];       // float-rounded SCALE factor (f32 data)
+  int32_t in_type, out_type;       // ElemType
+  int32_t out_f;                   // final value is in the float domain
+  int64_t count;                   // elements
+};
+
 }  // namespace tec_sm100

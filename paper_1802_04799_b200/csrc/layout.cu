@@ -570,9 +570,18 @@ int launch_unpack_output(const void* in, int in_type, void* out, int out_type,
             static_cast<unsigned>((hw + 31) / 32), static_cast<unsigned>(n));
   dim3 block(32, 8);
   if (out_type == kI32) {
-    if (in_type != kI32) return cudaErrorInvalidValue;
-    unpack_nhwc_to_nchw_kernel<int32_t, int32_t><<<grid, block, 0, st>>>(
-        static_cast<const int32_t*>(in), static_cast<int32_t*>(out), c, hw);
+    if (in_type == kI8)
+      unpack_nhwc_to_nchw_kernel<int8_t, int32_t><<<grid, block, 0, st>>>(
+          static_cast<const int8_t*>(in), static_cast<int32_t*>(out), c, hw);
+    else if (in_type == kI32)
+      unpack_nhwc_to_nchw_kernel<int32_t, int32_t><<<grid, block, 0, st>>>(
+          static_cast<const int32_t*>(in), static_cast<int32_t*>(out), c, hw);
+    else
+      return cudaErrorInvalidValue;
+  } else if (out_type == kI8) {
+    if (in_type != kI8) return cudaErrorInvalidValue;
+    unpack_nhwc_to_nchw_kernel<int8_t, int8_t><<<grid, block, 0, st>>>(
+        static_cast<const int8_t*>(in), static_cast<int8_t*>(out), c, hw);
   } else if (in_type == kBF16) {
     unpack_nhwc_to_nchw_kernel<__nv_bfloat16, float><<<grid, block, 0, st>>>(
         static_cast<const __nv_bfloat16*>(in), static_cast<float*>(out), c, hw);

@@ -64,6 +64,8 @@ int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTma
 int launch_pool_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTmaShape& t,
                     int sms, cudaStream_t st);
 int launch_global_avg_pool(const PoolParams& p, cudaStream_t st);
+int launch_elementwise(const ElemProg& p, const void* x, void* y, int32_t* err, int sms,
+                       cudaStream_t st);
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int bn, int swz, bool inter, bool res, bool halo,
                       int prog, int grid, cudaStream_t st);
@@ -1700,6 +1702,70 @@ tec_status tec_global_avg_pool(const tec_pool_desc* d, const void* x, void* y, v
   return TEC_OK;
 }
 
+tec_status tec_elementwise(const tec_elem_prog* d, const void* x, void* y, int32_t* err_flag,
+                           void* stream) {
+  if (!d) return fail(TEC_E_INTERNAL, "null elementwise program");
+  if (d->n_ops < 0 || d->n_ops > TEC_MAX_ELEM_OPS)
+    return fail(TEC_E_LOWERING, "elementwise: 0.." + std::to_string(TEC_MAX_ELEM_OPS) + " members");
+  if (d->count < 0) return fail(TEC_E_SHAPE_MISMATCH, "elementwise: negative count");
+  const int32_t sd = d->src_dtype, dd = d->dst_dtype;
+  auto known = [](int32_t t) { return t == TEC_DT_F32 || t == TEC_DT_I32 || t == TEC_DT_I8; };
+  if (!known(sd) || !known(dd)) return fail(TEC_E_LOWERING, "elementwise: f32 / i32 / i8 data only");
+  ElemProg p{};
+  p.n_ops = d->n_ops;
+  p.in_type = elem_type_of(sd);
+  p.out_type = elem_type_of(dd);
+  p.count = d->count;
+  // walk the chain's value type (graph.py infer) so a bad program fails here
+  int32_t t = sd;
+  for (int k = 0; k < d->n_ops; ++k) {
+    const int32_t kind = d->kind[k];
+    p.kind[k] = kind;
+    const std::string at = "elementwise member " + std::to_string(k) + ": ";
+    if (kind == TEC_ELEM_CAST) {
+      const int32_t to = d->cast_to[k];
+      const bool ok = (t == TEC_DT_I8 && (to == TEC_DT_I32 || to == TEC_DT_F32 || to == TEC_DT_I8)) ||
+                      (t == TEC_DT_I32 && (to == TEC_DT_F32 || to == TEC_DT_I32)) ||
+                      (t == TEC_DT_F32 && to == TEC_DT_F32);
+      if (!ok) return fail(TEC_E_LOWERING, at + "unsupported cast");
+      p.cast_to_f[k] = to == TEC_DT_F32 && t != TEC_DT_F32;
+      t = to;
+    } else if (kind == TEC_ELEM_SCALE) {
+      const double c = d->scale[k];
+      if (t == TEC_DT_F32) {
+        p.fscale[k] = (float)c;  // the factor rounded to float (R/src/ops.cpp:260-281)
+      } else {
+        if (c != std::floor(c)) return fail(TEC_E_SHAPE_MISMATCH, at + "integer scale requires an integral factor");
+        if (std::fabs(c) >= 4294967296.0) return fail(TEC_E_LOWERING, at + "|integral scale| >= 2^32");
+        if (t == TEC_DT_I8) return fail(TEC_E_LOWERING, at + "scale of i8 data (cast to i32 first)");
+        p.mult[k] = (int64_t)c;
+      }
+    } else if (kind == TEC_ELEM_RELU) {
+    } else if (kind == TEC_ELEM_REQUANTIZE) {
+      if (t != TEC_DT_I32) return fail(TEC_E_SHAPE_MISMATCH, at + "requantize wants i32 data");
+      if (d->mult[k] < 1 || d->mult[k] >= (int64_t(1) << 31) || d->shift[k] < 0 || d->shift[k] > 62)
+        return fail(TEC_E_SHAPE_MISMATCH, at + "requantize needs 1 <= multiplier < 2^31, 0 <= shift <= 62");
+      p.mult[k] = d->mult[k];
+      p.shift[k] = d->shift[k];
+      t = TEC_DT_I8;
+    } else {
+      return fail(TEC_E_LOWERING, at + "unknown kind " + std::to_string(kind));
+    }
+  }
+  if (t != dd) return fail(TEC_E_SHAPE_MISMATCH, "elementwise: the chain ends in dtype " +
+                                                     std::to_string(t) + ", y is " + std::to_string(dd));
+  p.out_f = dd == TEC_DT_F32;
+  if (d->count == 0) return TEC_OK;
+  if (!x || !y) return fail(TEC_E_INTERNAL, "null buffer");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
+    return fail(TEC_E_LOWERING, "elementwise: x / y must be 16-byte aligned");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int e = launch_elementwise(p, x, y, err_flag, sm_count(dev), (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "elementwise launch");
+  return TEC_OK;
+}
+
 tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
                                const tec_knobs* knobs, const void* x,
                                const void* w, void* y, int device) {
@@ -1937,6 +2003,7 @@ struct tec_plan {
   // they share it; zero-filled once, left zeroed by every launch)
   void* ws = nullptr;
   size_t ws_bytes = 0;
+  int32_t* err = nullptr;  // integer range overflow flag shared by every step
 };
 
 namespace {
@@ -1944,10 +2011,12 @@ tec_status run_step(const tec_plan* p, const tec_step& s, void* stream) {
   switch (s.kind) {
     case TEC_STEP_CONV:
       return tec_conv2d_fused_ws(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype,
-                                 nullptr, p->ws, p->ws_bytes, stream);
+                                 p->err, p->ws, p->ws_bytes, stream);
     case TEC_STEP_DEPTHWISE:
       return tec_depthwise_fused(&s.conv, &s.epi, &s.knobs, s.src, s.w, s.dst, s.dst_dtype,
-                                 nullptr, stream);
+                                 p->err, stream);
+    case TEC_STEP_ELEMWISE:
+      return tec_elementwise(&s.elem, s.src, s.dst, p->err, stream);
     case TEC_STEP_MAX_POOL:
       return tec_max_pool2d(&s.pool, s.src, s.dst, stream);
     case TEC_STEP_AVG_POOL:
@@ -1993,10 +2062,17 @@ tec_status tec_plan_create(const tec_step* steps, int32_t n_steps, tec_plan** ou
     }
     p->ws_bytes = std::max(p->ws_bytes, (size_t)kp.workspace_bytes);
   }
+  if (cudaMalloc(reinterpret_cast<void**>(&p->err), sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(p->err, 0, sizeof(int32_t)) != cudaSuccess) {
+    if (p->err) cudaFree(p->err);
+    delete p;
+    return fail(TEC_E_CUDA, "plan error flag allocation failed");
+  }
   if (p->ws_bytes) {
     if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess ||
         cudaMemset(p->ws, 0, p->ws_bytes) != cudaSuccess) {
       if (p->ws) cudaFree(p->ws);
+      cudaFree(p->err);
       delete p;
       return fail(TEC_E_CUDA, "plan workspace allocation failed");
     }
@@ -2061,11 +2137,23 @@ tec_status tec_plan_run_steps(tec_plan* p, int32_t first, int32_t count, void* s
 
 int32_t tec_plan_size(const tec_plan* p) { return p ? (int32_t)p->steps.size() : 0; }
 
+tec_status tec_plan_status(tec_plan* p, void* stream) {
+  if (!p) return fail(TEC_E_INTERNAL, "null plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t h = 0;
+  TEC_CUDA(cudaMemcpyAsync(&h, p->err, sizeof(h), cudaMemcpyDeviceToHost, s));
+  TEC_CUDA(cudaMemsetAsync(p->err, 0, sizeof(int32_t), s));
+  TEC_CUDA(cudaStreamSynchronize(s));
+  if (h) return fail(TEC_E_FOLD_OVERFLOW, "value out of range for i32 in a plan step");
+  return TEC_OK;
+}
+
 void tec_plan_destroy(tec_plan* p) {
   if (!p) return;
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->graph) cudaGraphDestroy(p->graph);
   if (p->ws) cudaFree(p->ws);
+  if (p->err) cudaFree(p->err);
   delete p;
 }
 }  // extern "C"

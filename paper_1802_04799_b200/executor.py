@@ -25,9 +25,20 @@ list of kernel launches on device buffers:
     launch.
 
 Compute modes: "bf16" (activations bf16 NHWC, f32 accumulate; graph outputs
-f32) and "f32" (the bit-exact SIMT path: every conv equals the reference's
-evaluate_graph bit for bit). Unsupported nodes raise LoweringError -- there
-is no CPU fallback.
+f32), "f32" (the bit-exact SIMT path: every conv equals the reference's
+evaluate_graph bit for bit), "f32tc" (f32 on the tensor cores) and "i8"
+(int8 graphs: i8 activations NHWC, i32 accumulate, bit-exact).
+Members of a fused conv node that the conv epilogue cannot apply become
+elementwise launches (tec_elementwise) around the conv:
+  * a side chain -- unary members feeding an add / mul operand, e.g. the
+    int8 shortcut scale(cast(y, i32)) -- runs BEFORE the conv into a shared
+    operand buffer;
+  * the tail of the main chain from the first non-epilogue member on (e.g.
+    requantize, i32 -> i8) runs AFTER it, reading the conv's i32 result from
+    a shared scratch buffer.
+Integer range overflow in any step is reported by run() as FoldOverflow
+(tec_plan_status). Unsupported nodes raise LoweringError -- there is no CPU
+fallback.
 """
 from __future__ import annotations
 
@@ -45,6 +56,9 @@ from .graph import ComputeGraph, GraphNode, check_memory_plan, fuse_pass, plan_m
 E_LOWERING, E_IO, E_SHAPE = 15, 20, 2
 _EPI = {"scale": _abi.EPI_SCALE, "bias_add": _abi.EPI_BIAS, "add": _abi.EPI_ADD,
         "mul": _abi.EPI_MUL, "relu": _abi.EPI_RELU}
+_ELEM = {"cast": _abi.ELEM_CAST, "scale": _abi.ELEM_SCALE, "relu": _abi.ELEM_RELU,
+         "requantize": _abi.ELEM_REQUANTIZE}
+_DT = {"f32": _abi.DT_F32, "i32": _abi.DT_I32, "i8": _abi.DT_I8}
 _TORCH = {_abi.DT_F32: torch.float32, _abi.DT_BF16: torch.bfloat16,
           _abi.DT_I32: torch.int32, _abi.DT_I8: torch.int8}
 _BYTES = {_abi.DT_F32: 4, _abi.DT_BF16: 2, _abi.DT_I32: 4, _abi.DT_I8: 1}
@@ -128,11 +142,52 @@ def f32_output(n: GraphNode) -> bool:
     return root.op in ("matmul", "global_avg_pool", "scale")
 
 
+def split_conv_members(n: GraphNode):
+    """A conv-rooted fused node's members (graph.cpp:209-222 order) as
+    (root, main, sides, tail):
+      main  -- the chain from the root the conv epilogue applies;
+      sides -- unary chains (first input, last member id, members) that
+               compute an add / mul operand of the main chain from a
+               tensor outside the node (fuse_pass pulls them in);
+      tail  -- main-chain members from the first one the epilogue cannot
+               apply on (all unary elementwise)."""
+    ms = n.members if n.op == "fused" else [n]
+    root = ms[0]
+    if root.op not in ("conv2d", "depthwise_conv2d", "matmul"):
+        raise TecError(E_LOWERING, f"fused node '{n.id}' is not conv/matmul-rooted")
+    ids = {m.id for m in ms}
+    main, sides, side_of, prev = [], [], {}, root.id
+    for m in ms[1:]:
+        if prev in m.inputs:
+            main.append(m)
+            prev = m.id
+            continue
+        if m.op not in _ELEM or len(m.inputs) != 1:
+            raise TecError(E_LOWERING, f"fused member '{m.id}' ({m.op}) is off the conv chain")
+        src = m.inputs[0]
+        if src in side_of:  # extends a side chain
+            k = side_of.pop(src)
+            first, _, members = sides[k]
+            sides[k] = (first, m.id, members + [m])
+        elif src in ids:
+            raise TecError(E_LOWERING, f"fused member '{m.id}' reads an interior value")
+        else:
+            sides.append((src, m.id, [m]))
+            k = len(sides) - 1
+        side_of[m.id] = k
+    cut = next((i for i, m in enumerate(main) if m.op not in _EPI), len(main))
+    head, tail = main[:cut], main[cut:]
+    for m in tail:
+        if m.op not in _ELEM or len(m.inputs) != 1:
+            raise TecError(E_LOWERING, f"member '{m.op}' has no sm100 epilogue")
+    return root, head, sides, tail
+
+
 class DeviceGraph:
     def __init__(self, g: ComputeGraph, compute: str = "bf16", device: int = 0,
                  knobs: Optional[Dict[str, dict]] = None):
-        if compute not in ("bf16", "f32", "f32tc"):
-            raise TecError(E_LOWERING, f"executor compute mode '{compute}' (bf16 | f32 | f32tc)")
+        if compute not in ("bf16", "f32", "f32tc", "i8"):
+            raise TecError(E_LOWERING, f"executor compute mode '{compute}' (bf16 | f32 | f32tc | i8)")
         self.lib = _abi.load()
         self.dev = torch.device("cuda", device)
         self.compute = compute
@@ -140,8 +195,9 @@ class DeviceGraph:
         # NHWC activations between layers, each conv's input packed into its
         # three bf16 planes by a layout step
         self.cmode = {"bf16": _abi.COMPUTE_BF16, "f32": _abi.COMPUTE_F32,
-                      "f32tc": _abi.COMPUTE_F32TC}[compute]
-        self.act_dt = _abi.DT_BF16 if compute == "bf16" else _abi.DT_F32
+                      "f32tc": _abi.COMPUTE_F32TC, "i8": _abi.COMPUTE_I8}[compute]
+        self.act_dt = {"bf16": _abi.DT_BF16, "i8": _abi.DT_I8}.get(compute, _abi.DT_F32)
+        self.in_dtype = "i8" if compute == "i8" else "f32"  # graph input / weight dtype
         self.knobs = knobs or {}
         self.fused = fuse_pass(g)
         self.g = _resolve_aliases(self.fused)
@@ -203,8 +259,8 @@ class DeviceGraph:
         """bf16 mode: every activation is bf16 (a conv's add/mul operand
         must share its output dtype); graph outputs of the head (matmul-
         rooted nodes, pools) are produced in f32."""
-        if n.out_type.dtype == "i32":
-            return _abi.DT_I32
+        if n.out_type.dtype in ("i32", "i8"):
+            return _DT[n.out_type.dtype]
         return _abi.DT_F32 if n.id in self.outputs and f32_output(n) else self.act_dt
 
     def _dev_bytes(self, n: GraphNode) -> int:
@@ -215,6 +271,18 @@ class DeviceGraph:
         check_memory_plan(self.g, self.plan, nbytes=self._dev_bytes)
         self.arena = torch.empty(max(self.plan.total_bytes, ALIGN), dtype=torch.uint8,
                                  device=self.dev)
+        # shared buffers of the elementwise launches around fused convs
+        # (steps run in order on one stream, so one of each suffices)
+        tail_b, side_b = 0, 0
+        for n in self.g.nodes:
+            if n.op == "fused" and n.members[0].op in ("conv2d", "depthwise_conv2d", "matmul"):
+                _, _, sides, tail = split_conv_members(n)
+                if tail:
+                    tail_b = max(tail_b, n.out_type.num_elements() * 4)
+                for _, last, _ in sides:
+                    side_b = max(side_b, n.out_type.num_elements() * 4)
+        self.tail_buf = torch.empty(max(tail_b, ALIGN), dtype=torch.uint8, device=self.dev)
+        self.side_buf = torch.empty(max(side_b, ALIGN), dtype=torch.uint8, device=self.dev)
 
     def _out_buffer(self, n: GraphNode, dtype: int, nelem: int) -> torch.Tensor:
         nbytes = nelem * _BYTES[dtype]
@@ -236,7 +304,7 @@ class DeviceGraph:
             if n.op == "input":
                 if n.id in self.feed_names:
                     shape = list(n.out_type.shape)
-                    dt = {"f32": _abi.DT_F32, "i32": _abi.DT_I32, "i8": _abi.DT_I8}[n.out_type.dtype]
+                    dt = _DT[n.out_type.dtype]
                     buf = torch.empty(int(np.prod(shape)), dtype=_TORCH[dt], device=self.dev)
                     t = DevTensor(buf, shape, dt, "nchw")
                     self.feeds[n.id] = t
@@ -248,6 +316,8 @@ class DeviceGraph:
                 self._compile_maxpool(n)
             elif n.op == "global_avg_pool":
                 self._compile_avgpool(n, self.tensors[n.inputs[0]])
+            elif n.op in _ELEM or (n.op == "fused" and n.members[0].op in _ELEM):
+                self._compile_elemwise(n)
             else:
                 raise TecError(E_LOWERING, f"no sm100 lowering for node '{n.id}' ({n.op})")
         for o in self.outputs:
@@ -256,27 +326,26 @@ class DeviceGraph:
 
     # ---------------------------------------------------------------- conv
     def _conv_members(self, n: GraphNode):
-        ms = n.members if n.op == "fused" else [n]
-        root = ms[0]
-        if root.op not in ("conv2d", "depthwise_conv2d", "matmul"):
-            raise TecError(E_LOWERING, f"fused node '{n.id}' is not conv/matmul-rooted")
+        root, head, sides, tail = split_conv_members(n)
+        side_ids = {last for _, last, _ in sides}
         items, prev = [], root.id
-        for m in ms[1:]:
-            if m.op not in _EPI:
-                raise TecError(E_LOWERING, f"member '{m.op}' has no sm100 epilogue")
+        for m in head:
             others = [i for i in m.inputs if i != prev]
-            if prev not in m.inputs or len(others) != len(m.inputs) - 1:
+            if len(others) != len(m.inputs) - 1:
                 raise TecError(E_LOWERING, "fused members are not a single chain")
             if m.op == "bias_add" and int(m.attrs.get("axis", 1)) != 1:
                 raise TecError(E_LOWERING, "bias_add must broadcast over channels")
             items.append((m.op, others[0] if others else None, m))
             prev = m.id
+        used = {it[1] for it in items if it[0] in ("add", "mul")}
+        if side_ids - used:
+            raise TecError(E_LOWERING, f"fused node '{n.id}': a side chain feeds no add / mul")
         for op in ("bias_add", "add", "mul"):
             # one operand slot each in tec_epilogue: a second member of the
             # same kind would silently read the first one's operand
             if sum(1 for it in items if it[0] == op) > 1:
                 raise TecError(E_LOWERING, f"fused node '{n.id}' has more than one '{op}' member")
-        return root, items
+        return root, items, sides, tail
 
     def _conv_input(self, d: _abi.ConvDesc, src: DevTensor) -> int:
         """Device pointer of x in the packed layout conv `d` reads,
@@ -296,13 +365,16 @@ class DeviceGraph:
                                         dst=packed.data_ptr()))
             return packed.data_ptr()
         # src -> NCHW f32 (the reference layout) -> tec_activation_pack
-        if src.layout == "nchw" and src.dtype == _abi.DT_F32:
-            nchw = src.buf
+        if src.layout == "nchw" and src.dtype == _DT[self.in_dtype]:
+            nchw = src.buf  # the reference layout and dtype tec_activation_pack reads
+        elif self.compute == "i8" and (src.layout != "nhwc" or src.dtype != _abi.DT_I8):
+            raise TecError(E_LOWERING, "i8 conv input must be i8 (NCHW feed or NHWC activation)")
         else:
             n_, c_, h_, w_ = src.nchw4
-            nchw = self._scratch(n_ * c_ * h_ * w_ * 4)
+            udt = _DT[self.in_dtype]
+            nchw = self._scratch(n_ * c_ * h_ * w_ * _BYTES[udt])
             self.steps.append(_abi.Step(kind=_abi.STEP_UNPACK, src_dtype=src.dtype,
-                                        dst_dtype=_abi.DT_F32, src=src.ptr(),
+                                        dst_dtype=udt, src=src.ptr(),
                                         dst=nchw.data_ptr(), n=n_, c=c_, h=h_, w_=w_))
         if self.cmode == _abi.COMPUTE_F32 and not d.depthwise:
             return nchw.data_ptr()  # the exact path reads NCHW f32 as is
@@ -311,8 +383,41 @@ class DeviceGraph:
                                     dst=packed.data_ptr()))
         return packed.data_ptr()
 
+    def _elem_prog(self, members, src_dt: int, dst_dt: int, count: int) -> _abi.ElemProg:
+        if len(members) > _abi.MAX_ELEM_OPS:
+            raise TecError(E_LOWERING, f"more than {_abi.MAX_ELEM_OPS} elementwise members")
+        p = _abi.ElemProg(n_ops=len(members), src_dtype=src_dt, dst_dtype=dst_dt, count=count)
+        for k, m in enumerate(members):
+            p.kind[k] = _ELEM[m.op]
+            if m.op == "cast":
+                p.cast_to[k] = _DT[m.attrs.get("dtype", "i32")]
+            elif m.op == "scale":
+                p.scale[k] = float(m.attrs.get("scale", 1.0))
+            elif m.op == "requantize":
+                p.mult[k] = int(m.attrs.get("multiplier", 1))
+                p.shift[k] = int(m.attrs.get("shift", 0))
+        return p
+
+    def _elem_step(self, members, src: DevTensor, dst_ptr: int, dst_dt: int, count: int):
+        if src.layout != "nhwc":
+            src = self._to_nhwc(src, src.dtype)
+        self.steps.append(_abi.Step(kind=_abi.STEP_ELEMWISE, src=src.ptr(), dst=dst_ptr,
+                                    src_dtype=src.dtype, dst_dtype=dst_dt,
+                                    elem=self._elem_prog(members, src.dtype, dst_dt, count)))
+
+    def _compile_elemwise(self, n: GraphNode):
+        ms = n.members if n.op == "fused" else [n]
+        for a, b in zip(ms, ms[1:]):
+            if b.op not in _ELEM or b.inputs != [a.id]:
+                raise TecError(E_LOWERING, f"fused node '{n.id}' is not a unary elementwise chain")
+        x = self.tensors[ms[0].inputs[0]]
+        out_dt = self._node_dtype(n)
+        y = self._out_buffer(n, out_dt, n.out_type.num_elements())
+        self._elem_step(ms, x, y.data_ptr(), out_dt, n.out_type.num_elements())
+        self.tensors[n.id] = DevTensor(y, list(n.out_type.shape), out_dt, "nhwc")
+
     def _compile_conv(self, n: GraphNode):
-        root, items = self._conv_members(n)
+        root, items, sides, tail = self._conv_members(n)
         x = self.tensors[root.inputs[0]]
         wname = root.inputs[1]
         if wname not in self.param_names:
@@ -326,16 +431,32 @@ class DeviceGraph:
             from .ops import conv_desc
             d = conv_desc(root.op, self.g.node(root.inputs[0]).out_type.shape, wt.shape,
                           root.attrs, self.cmode)
-        if self.g.node(root.inputs[0]).out_type.dtype != "f32":
-            raise TecError(E_LOWERING, "executor graphs are f32 (run int8 ops one by one)")
+        if self.g.node(root.inputs[0]).out_type.dtype != self.in_dtype:
+            raise TecError(E_LOWERING, f"executor compute '{self.compute}' runs {self.in_dtype} "
+                                       "convolutions")
         xptr = self._conv_input(d, x)
         lay = _abi.ConvLayout()
         _abi.check(self.lib.tec_conv_layout_of(C.byref(d), C.byref(lay)))
         wpk = self._scratch(lay.wt_bytes)
         self._bind_weight(wname, d, wpk, transpose=root.op == "matmul")
-        out_dt = self._node_dtype(n)
+        node_dt = self._node_dtype(n)
         oh, ow = (lay.oh, lay.ow)
-        y = self._out_buffer(n, out_dt, d.n * d.k * oh * ow)
+        count = d.n * d.k * oh * ow
+        y = self._out_buffer(n, node_dt, count)
+        # the epilogue's result: the node's own buffer, or (with a tail) the
+        # accumulator-dtype scratch the tail's elementwise launch reads
+        if (tail or sides) and self.compute != "i8":
+            raise TecError(E_LOWERING, f"fused node '{n.id}': elementwise members around a conv "
+                                       "need compute 'i8'")
+        if len(sides) > 1:
+            raise TecError(E_LOWERING, f"fused node '{n.id}': more than one side chain")
+        out_dt = lay.acc_dtype if tail else node_dt
+        conv_dst = self.tail_buf.data_ptr() if tail else y.data_ptr()
+        side_dst = {}
+        for first, last, members in sides:
+            # the operand's dtype is the conv output's (epilogue operands)
+            self._elem_step(members, self.tensors[first], self.side_buf.data_ptr(), out_dt, count)
+            side_dst[last] = DevTensor(self.side_buf, list(n.out_type.shape), out_dt, "nhwc")
         epi = _abi.Epilogue()
         for i, (op, other, m) in enumerate(items):
             epi.ops[i] = _EPI[op]
@@ -348,7 +469,7 @@ class DeviceGraph:
                     raise TecError(E_LOWERING, "bias must be a graph input parameter")
                 epi.bias = self._bias_ptr(other)
             else:
-                r = self.tensors[other]
+                r = side_dst.get(other) or self.tensors[other]
                 if r.layout != "nhwc" or r.dtype != out_dt:
                     raise TecError(E_LOWERING, f"'{op}' operand must be an NHWC {out_dt} tensor")
                 if op == "add":
@@ -359,15 +480,20 @@ class DeviceGraph:
         kn = _abi.Knobs(**self.knobs.get(n.id, {}))
         self.steps.append(_abi.Step(kind=_abi.STEP_DEPTHWISE if d.depthwise else _abi.STEP_CONV,
                                     dst_dtype=out_dt, conv=d, epi=epi, knobs=kn, src=xptr,
-                                    w=wpk.data_ptr(), dst=y.data_ptr()))
+                                    w=wpk.data_ptr(), dst=conv_dst))
         shape = list(n.out_type.shape)
-        self.tensors[n.id] = DevTensor(y, shape, out_dt, "nhwc")
+        if tail:
+            acc = DevTensor(self.tail_buf, shape, out_dt, "nhwc")
+            self._elem_step(tail, acc, y.data_ptr(), node_dt, count)
+        self.tensors[n.id] = DevTensor(y, shape, node_dt, "nhwc")
 
     def _bind_weight(self, name: str, d: _abi.ConvDesc, wpk: torch.Tensor, transpose: bool):
         src_shape = self.g.node(name).out_type.shape
 
+        npdt = np.int8 if self.compute == "i8" else np.float32
+
         def prep(params: Dict[str, np.ndarray], st: int, d=d, wpk=wpk):
-            w = np.asarray(params[name], dtype=np.float32)
+            w = np.asarray(params[name], dtype=npdt)
             if list(w.shape) != list(src_shape):
                 raise TecError(E_SHAPE, f"parameter '{name}' is {list(w.shape)}, expected {src_shape}")
             if transpose:  # matmul [K, N] -> OIHW [N, K, 1, 1]
@@ -381,10 +507,12 @@ class DeviceGraph:
     def _bias_ptr(self, name: str) -> int:
         if name not in self.params:
             k = self.g.node(name).out_type.shape[0]
-            self.params[name] = torch.empty(k, dtype=torch.float32, device=self.dev)
+            integer = self.compute == "i8"
+            self.params[name] = torch.empty(k, dtype=torch.int32 if integer else torch.float32,
+                                            device=self.dev)
 
-            def prep(params, st, name=name):
-                b = np.asarray(params[name], dtype=np.float32)
+            def prep(params, st, name=name, npdt=np.int32 if integer else np.float32):
+                b = np.asarray(params[name], dtype=npdt)
                 if b.shape != tuple(self.params[name].shape):
                     raise TecError(E_SHAPE, f"parameter '{name}' has shape {b.shape}")
                 self.params[name].copy_(torch.from_numpy(b))
@@ -392,16 +520,17 @@ class DeviceGraph:
         return self.params[name].data_ptr()
 
     # ---------------------------------------------------------------- pools
-    def _to_nhwc(self, src: DevTensor) -> DevTensor:
+    def _to_nhwc(self, src: DevTensor, dtype: Optional[int] = None) -> DevTensor:
         if src.layout == "nhwc":
             return src
+        dt = self.act_dt if dtype is None else dtype
         n_, c_, h_, w_ = src.nchw4
-        out = self._scratch(n_ * c_ * h_ * w_ * _BYTES[self.act_dt]).view(_TORCH[self.act_dt])
+        out = self._scratch(n_ * c_ * h_ * w_ * _BYTES[dt]).view(_TORCH[dt])
 
         self.steps.append(_abi.Step(kind=_abi.STEP_TO_NHWC, src_dtype=src.dtype,
-                                    dst_dtype=self.act_dt, src=src.ptr(), dst=out.data_ptr(),
+                                    dst_dtype=dt, src=src.ptr(), dst=out.data_ptr(),
                                     n=n_, c=c_, h=h_, w_=w_))
-        return DevTensor(out, src.shape, self.act_dt, "nhwc")
+        return DevTensor(out, src.shape, dt, "nhwc")
 
     def _compile_maxpool(self, n: GraphNode):
         x = self._to_nhwc(self.tensors[n.inputs[0]])
@@ -480,17 +609,27 @@ class DeviceGraph:
         return int(self.lib.tec_plan_size(self._native))
 
     def output(self, name: str) -> torch.Tensor:
-        """The device output in the reference layout (NCHW / [N, K]), f32."""
+        """The device output in the reference layout (NCHW / [N, K]): f32,
+        or the node's own integer dtype (i8 / i32, exact)."""
         t = self.tensors[name]
         shape = t.shape
+        dt = t.dtype if t.dtype in (_abi.DT_I8, _abi.DT_I32) else _abi.DT_F32
         if t.layout == "nhwc" and len(shape) == 4 and shape[2] * shape[3] > 1:
             n_, c_, h_, w_ = shape
-            out = torch.empty(shape, dtype=torch.float32, device=self.dev)
-            _abi.check(self.lib.tec_output_unpack(t.ptr(), t.dtype, out.data_ptr(), _abi.DT_F32,
+            out = torch.empty(shape, dtype=_TORCH[dt], device=self.dev)
+            _abi.check(self.lib.tec_output_unpack(t.ptr(), t.dtype, out.data_ptr(), dt,
                                                   n_, c_, h_, w_,
                                                   torch.cuda.current_stream(self.dev).cuda_stream))
             return out
-        return t.buf[:int(np.prod(shape))].reshape(shape).float()
+        v = t.buf[:int(np.prod(shape))].reshape(shape)
+        return v if dt != _abi.DT_F32 else v.float()
+
+    def status(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Raises FoldOverflow if an integer step overflowed i32 since the
+        last check (synchronizes `stream`)."""
+        s = stream or torch.cuda.current_stream(self.dev)
+        with torch.cuda.device(self.dev):
+            _abi.check(self.lib.tec_plan_status(self._native, C.c_void_p(s.cuda_stream)))
 
     def run(self, feeds: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
         """evaluate_graph(g, feeds) on the device; host arrays in and out."""
@@ -501,5 +640,5 @@ class DeviceGraph:
                 self.set_feed(name, feeds[name])
             self.launch()
             outs = {o: self.output(o).cpu().numpy() for o in self.outputs}
-            torch.cuda.current_stream(self.dev).synchronize()
+            self.status()
         return outs

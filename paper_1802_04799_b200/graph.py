@@ -218,6 +218,29 @@ def _layout_transform(ins, attrs):
     _fail(E_SHAPE, f"unsupported layout pair {src} -> {dst}")
 
 
+def _cast(ins, attrs):
+    """cast(x, dtype): i8 -> i32 | f32, i32 -> f32 (and the identity). Not in
+    the reference registry: the int8 graph's shortcut operand (elementwise.cu)."""
+    to = attrs.get("dtype", "i32")
+    frm = ins[0].dtype
+    if (frm, to) not in (("i8", "i32"), ("i8", "f32"), ("i32", "f32"), ("i8", "i8"),
+                         ("i32", "i32"), ("f32", "f32")):
+        _fail(E_SHAPE, f"cast {frm} -> {to} is not supported")
+    return TensorType(list(ins[0].shape), to)
+
+
+def _requantize(ins, attrs):
+    """requantize(x: i32) -> i8 = clamp((x * multiplier + 2^(shift-1)) >> shift,
+    -128, 127). Not in the reference registry: the int8 graph's per-layer
+    output rescale (elementwise.cu states the arithmetic)."""
+    if ins[0].dtype != "i32":
+        _fail(E_SHAPE, "requantize wants i32 data")
+    m, sh = attrs.get("multiplier", 1), attrs.get("shift", 0)
+    if int(m) != m or int(sh) != sh or not (1 <= int(m) < 2 ** 31) or not (0 <= int(sh) <= 62):
+        _fail(E_SHAPE, "requantize needs an integer 1 <= multiplier < 2^31 and 0 <= shift <= 62")
+    return TensorType(list(ins[0].shape), "i8")
+
+
 # name -> (pattern, arity, infer)
 OPS: Dict[str, Tuple[str, int, Callable]] = {
     "add": (INJECTIVE, 2, _same_binary("add")),
@@ -237,6 +260,9 @@ OPS: Dict[str, Tuple[str, int, Callable]] = {
     "max_pool2d": (OPAQUE, 1, _max_pool2d),
     "global_avg_pool": (OPAQUE, 1, _global_avg_pool),
     "flatten": (INJECTIVE, 1, _flatten),
+    # int8 graph ops (not in the reference registry)
+    "cast": (INJECTIVE, 1, _cast),
+    "requantize": (INJECTIVE, 1, _requantize),
 }
 
 
@@ -603,6 +629,14 @@ def _fold_eval(n: GraphNode, ins: List[np.ndarray]) -> np.ndarray:
     if op == "relu":
         x = ins[0]
         return np.where(x < 0, np.zeros_like(x), x)
+    if op == "cast":
+        return ins[0].astype({"i8": np.int8, "i32": np.int32, "f32": np.float32}[n.attrs.get("dtype", "i32")])
+    if op == "requantize":
+        m, sh = int(n.attrs.get("multiplier", 1)), int(n.attrs.get("shift", 0))
+        t = ins[0].astype(np.int64) * m
+        if sh > 0:
+            t = (t + (1 << (sh - 1))) >> sh
+        return np.clip(t, -128, 127).astype(np.int8)
     if op == "exp":
         return _libm_expf(ins[0])
     if op == "sqrt":

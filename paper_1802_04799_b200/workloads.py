@@ -8,6 +8,7 @@ IC := 1); compulsory bytes = every operand + the output once
 """
 from __future__ import annotations
 
+import numpy as np
 from dataclasses import dataclass
 
 # name: (H=W, IC, OC, K, stride)
@@ -70,7 +71,8 @@ def mobilenet_layer(name: str, batch: int) -> ConvWorkload:
 
 # ------------------------------------------------ ResNet-18 graph (config 4)
 def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
-                   maxpool: bool = True, width: int = 64, head: bool = True):
+                   maxpool: bool = True, width: int = 64, head: bool = True,
+                   dtype: str = "f32"):
     """ResNet-18 inference as a reference-format ComputeGraph (SURVEY 8d
     config 4): BN folded into each conv's bias, so every conv is
     conv2d -> bias_add (-> add shortcut) -> relu, which fuse_pass groups
@@ -82,28 +84,52 @@ def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
     the reference composition scale(sum(sum(x, 3), 2)); `head=False` ends
     the graph at the last block's relu.
     Downsample branches are emitted before their block's first conv, so
-    the block's second conv fuses [conv2d, bias_add, add, relu]."""
+    the block's second conv fuses [conv2d, bias_add, add, relu].
+
+    dtype "i8" (SURVEY 8f.4, int8 end to end; body only, head=False): i8
+    image and weights, i32 biases; every relu'd conv ends in requantize
+    (i32 -> i8, multiplier / 2^16 ~ 1 / (4 sqrt(K)), about the accumulator's
+    spread for the synthetic operands of int8_resnet18_params), so
+    activations between layers are i8; an identity shortcut enters the
+    i32 accumulator domain as scale(cast(y, i32), round(4.6 sqrt(K))); the
+    downsample branch is [conv2d, bias_add] in i32."""
     from .graph import ComputeGraph, GraphNode, TensorType
 
+    if dtype not in ("f32", "i8"):
+        raise ValueError(f"resnet18_graph dtype {dtype!r} (f32 | i8)")
+    if dtype == "i8" and head:
+        raise ValueError("the int8 ResNet-18 graph is the body only (head=False)")
+    i8 = dtype == "i8"
     nodes = []
 
-    def inp(nid, shape):
-        nodes.append(GraphNode(nid, "input", out_type=TensorType(list(shape), "f32")))
+    def inp(nid, shape, dt=None):
+        nodes.append(GraphNode(nid, "input", out_type=TensorType(list(shape), dt or dtype)))
         return nid
 
     def conv(name, x, cin, cout, k, stride, relu=True, shortcut=None):
         w = inp(f"w_{name}", (cout, cin, k, k))
-        b = inp(f"b_{name}", (cout,))
+        b = inp(f"b_{name}", (cout,), "i32" if i8 else "f32")
         nodes.append(GraphNode(f"{name}", "conv2d", [x, w],
                                {"strides": [stride, stride], "padding": [k // 2, k // 2]}))
         nodes.append(GraphNode(f"{name}_bias", "bias_add", [name, b]))
         y = f"{name}_bias"
         if shortcut is not None:
-            nodes.append(GraphNode(f"{name}_add", "add", [y, shortcut]))
+            if i8 and shortcut[1]:  # identity shortcut: i8 -> accumulator domain
+                nodes.append(GraphNode(f"{name}_sc", "cast", [shortcut[0]], {"dtype": "i32"}))
+                nodes.append(GraphNode(f"{name}_scs", "scale", [f"{name}_sc"],
+                                       {"scale": float(round(4.6 * np.sqrt(cin * k * k)))}))
+                nodes.append(GraphNode(f"{name}_add", "add", [y, f"{name}_scs"]))
+            else:
+                nodes.append(GraphNode(f"{name}_add", "add", [y, shortcut[0]]))
             y = f"{name}_add"
         if relu:
             nodes.append(GraphNode(f"{name}_relu", "relu", [y]))
             y = f"{name}_relu"
+            if i8:
+                mult = max(1, int(round(65536.0 / (4.0 * np.sqrt(cin * k * k)))))
+                nodes.append(GraphNode(f"{name}_q", "requantize", [y],
+                                       {"multiplier": mult, "shift": 16}))
+                y = f"{name}_q"
         return y
 
     x = inp("x", (batch, 3, image, image))
@@ -118,9 +144,9 @@ def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
         for blk in range(2):
             s = stride if blk == 0 else 1
             pre = f"l{stage}_{blk}"
-            sc = y
+            sc = (y, True)
             if s != 1 or cin != cout:
-                sc = conv(f"{pre}_ds", y, cin, cout, 1, s, relu=False)
+                sc = (conv(f"{pre}_ds", y, cin, cout, 1, s, relu=False), False)
             h = conv(f"{pre}_a", y, cin, cout, 3, s)
             y = conv(f"{pre}_b", h, cout, cout, 3, 1, shortcut=sc)
             cin = cout
@@ -145,6 +171,24 @@ def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
     g = ComputeGraph(nodes, ["logits"])
     g.validate()
     return g
+
+
+def int8_resnet18_params(g, seed: int = 0):
+    """Synthetic operands of resnet18_graph(dtype="i8"): x in [-32, 32],
+    weights in [-8, 8], biases in [-100, 100] (i32). Returns (feeds, params)."""
+    rng = np.random.default_rng(seed)
+    feeds, params = {}, {}
+    for n in g.nodes:
+        if n.op != "input":
+            continue
+        shp = n.out_type.shape
+        if n.id == "x":
+            feeds["x"] = rng.integers(-32, 33, shp, dtype=np.int8)
+        elif n.id.startswith("w_"):
+            params[n.id] = rng.integers(-8, 9, shp, dtype=np.int8)
+        else:
+            params[n.id] = rng.integers(-100, 101, shp, dtype=np.int32)
+    return feeds, params
 
 
 # Conv GFLOP per image of resnet18_graph (SURVEY 8d config 4: 1.8136 GMAC

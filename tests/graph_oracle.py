@@ -9,6 +9,15 @@ deterministic -- conv/matmul operands rounded to bf16, f32 accumulation in
 the reference order, every activation rounded to bf16 (graph outputs of
 the head -- matmul, pools -- kept in f32, executor.f32_output) -- so the only remaining difference to the device is the
 tensor core's accumulation order.
+mode "i8": int8 graphs -- the conv itself through the oracle
+restatement (i8 x i8 -> i32, bit-identical to the reference), then every
+member of the fused node evaluated one by one in member order, as
+evaluate_graph does (R/src/graph.cpp:209-222): integer members in int64 with
+the i32 range check (DenseTensor::set_i, R/include/tec/tensor.hpp:63-69),
+plus the two int8-graph ops the reference registry lacks, restated here from
+their definition in paper_1802_04799_b200/csrc/elementwise.cu:
+  cast(x, dtype)                   value conversion;
+  requantize(x, multiplier, shift) clamp((x*m + 2^(shift-1)) >> shift, -128, 127).
 """
 from __future__ import annotations
 
@@ -34,9 +43,73 @@ def _epilogue(members, env, prev):
     return items
 
 
+class Overflow(Exception):
+    """An i32 range overflow (the reference throws FoldOverflow)."""
+
+
+def _i32(v):
+    if v.size and (v.min() < -2 ** 31 or v.max() > 2 ** 31 - 1):
+        raise Overflow()
+    return v.astype(np.int32)
+
+
+def _int_member(m, env):
+    """One member of an integer fused node (R/src/ops.cpp semantics)."""
+    x = env[m.inputs[0]]
+    op = m.op
+    if op == "bias_add":
+        b = env[m.inputs[1]].astype(np.int64)
+        return _i32(x.astype(np.int64) + b.reshape(1, -1, *([1] * (x.ndim - 2))))
+    if op in ("add", "mul"):
+        y = env[m.inputs[1]].astype(np.int64)
+        return _i32(x.astype(np.int64) + y if op == "add" else x.astype(np.int64) * y)
+    if op == "relu":
+        return np.where(x < 0, 0, x).astype(x.dtype)
+    if op == "scale":
+        c = float(m.attrs.get("scale", 1.0))
+        assert c == int(c)
+        return _i32(x.astype(np.int64) * int(c))
+    if op == "cast":
+        return x.astype({"i8": np.int8, "i32": np.int32, "f32": np.float32}[m.attrs.get("dtype", "i32")])
+    if op == "requantize":
+        t = x.astype(np.int64) * int(m.attrs.get("multiplier", 1))
+        sh = int(m.attrs.get("shift", 0))
+        if sh > 0:
+            t = (t + (1 << (sh - 1))) >> sh
+        return np.clip(t, -128, 127).astype(np.int8)
+    raise NotImplementedError(op)
+
+
+def _evaluate_int(g, feeds, params):
+    env = {}
+    env.update({k: np.asarray(v) for k, v in feeds.items()})
+    env.update({k: np.asarray(v) for k, v in params.items()})
+    for n in g.nodes:
+        if n.op == "input":
+            continue
+        ms = n.members if n.op == "fused" else [n]
+        local = dict(env)
+        for m in ms:
+            if m.op in ("conv2d", "depthwise_conv2d"):
+                st = tuple(m.attrs.get("strides", (1, 1)))
+                pd = tuple(m.attrs.get("padding", (0, 0)))
+                local[m.id] = fused_conv(m.op, local[m.inputs[0]], local[m.inputs[1]], st, pd, [])
+            elif m.op == "max_pool2d":
+                x = local[m.inputs[0]]  # i8 / i32 values are exact in f32
+                local[m.id] = max_pool2d(x, tuple(m.attrs.get("kernel", (3, 3))),
+                                         tuple(m.attrs.get("strides", (2, 2))),
+                                         tuple(m.attrs.get("padding", (1, 1)))).astype(x.dtype)
+            else:
+                local[m.id] = _int_member(m, local)
+        env[n.id] = local[ms[-1].id]
+    return {o: env[o] for o in g.outputs}
+
+
 def evaluate(g, feeds: Dict[str, np.ndarray], params: Dict[str, np.ndarray],
              mode: str = "f32") -> Dict[str, np.ndarray]:
     """g: a fuse_pass'ed ComputeGraph (paper_1802_04799_b200.graph)."""
+    if mode == "i8":
+        return _evaluate_int(g, feeds, params)
     rnd = bf16_round if mode == "bf16" else (lambda a: a)
     outs = set(g.outputs)
     env = {}

@@ -110,7 +110,9 @@ def test_struct_layouts_match_header(tmp_path):
         "tec_knobs": (_abi.Knobs, ["grid"]),
         "tec_pool_desc": (_abi.PoolDesc, ["out_dtype"]),
         "tec_kernel_plan": (_abi.KernelPlan, ["tma_store", "workspace_bytes"]),
-        "tec_step": (_abi.Step, ["conv", "epi", "knobs", "pool", "src", "w", "dst", "w_"]),
+        "tec_elem_prog": (_abi.ElemProg, ["kind", "shift", "cast_to", "mult", "scale", "src_dtype",
+                                          "count"]),
+        "tec_step": (_abi.Step, ["conv", "epi", "knobs", "pool", "src", "w", "dst", "w_", "elem"]),
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tec_sm100.h"',
              'int main(void) {']
