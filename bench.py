@@ -453,7 +453,7 @@ def impl_ours(args):
         rargs.no_cpu_baseline = True
         rargs.steps = min(args.steps, 50)
         resnet = {}
-        for rc in ("bf16", "f32tc"):
+        for rc in ("bf16", "f32tc", "i8"):
             rl = bench_workloads.resnet18_line(rargs, sys.modules[__name__], knobs_file=knobs_path,
                                                compute=rc)
             if rl is not None:

@@ -75,19 +75,24 @@ def resnet18(args, bench):
 
 def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
     """ResNet-18 b256 strong-scaling measurement; returns rank 0's JSON
-    line (None on other ranks). Knobs: `knobs_file`'s "resnet18_bf16" entry
-    ({fused node id: knobs}) when present, else tuned live (or defaults
-    with --no-tune)."""
+    line (None on other ranks). Knobs: `knobs_file`'s "resnet18_<compute>"
+    entry ({fused node id: knobs}) when present, else tuned live (or
+    defaults with --no-tune). compute "i8" runs the int8 body (SURVEY 8f.4:
+    i8 image in, i8 [N, 512, 7, 7] features out, requantize between
+    layers)."""
     import torch
 
     from paper_1802_04799_b200.executor import DeviceGraph
     from paper_1802_04799_b200.parallel import gather_rows, shard_batch
-    from paper_1802_04799_b200.workloads import RESNET18_GFLOP_PER_IMAGE, resnet18_graph
+    from paper_1802_04799_b200.workloads import (RESNET18_GFLOP_PER_IMAGE, int8_resnet18_params,
+                                                 resnet18_graph)
 
     rank, ws, local = _dist()
     gb = args.global_batch or 256
     start, cnt = shard_batch(gb, ws, rank)
-    g = resnet18_graph(cnt)
+    i8 = compute == "i8"
+    g = resnet18_graph(cnt, head=False, dtype="i8") if i8 else resnet18_graph(cnt)
+    out_name = g.outputs[0]
     knobs = None
     if knobs_file and os.path.exists(knobs_file):
         with open(knobs_file) as f:
@@ -97,18 +102,21 @@ def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
     dg = DeviceGraph(g, compute=compute, device=local, knobs=knobs)
     rng = np.random.default_rng(1234)  # same weights on every rank (replicated)
     params = {}
-    for n in g.nodes:
-        if n.op == "input" and n.id != "x":
-            shp = n.out_type.shape
-            if n.id.startswith("w_"):
-                fan = int(np.prod(shp[1:])) if len(shp) == 4 else shp[0]
-                params[n.id] = (rng.standard_normal(shp) * np.sqrt(2.0 / fan)).astype(np.float32)
-            else:
-                params[n.id] = rng.uniform(-0.1, 0.1, shp).astype(np.float32)
+    if i8:
+        _, params = int8_resnet18_params(g, seed=1234)
+        x_np = int8_resnet18_params(g, seed=rank)[0]["x"]
+    else:
+        for n in g.nodes:
+            if n.op == "input" and n.id != "x":
+                shp = n.out_type.shape
+                if n.id.startswith("w_"):
+                    fan = int(np.prod(shp[1:])) if len(shp) == 4 else shp[0]
+                    params[n.id] = (rng.standard_normal(shp) * np.sqrt(2.0 / fan)).astype(np.float32)
+                else:
+                    params[n.id] = rng.uniform(-0.1, 0.1, shp).astype(np.float32)
+        x_np = np.random.default_rng(rank).uniform(-1, 1, (cnt, 3, 224, 224)).astype(np.float32)
     dg.bind_params(params)
-    x_host = torch.from_numpy(
-        np.random.default_rng(rank).uniform(-1, 1, (cnt, 3, 224, 224)).astype(np.float32)
-    ).pin_memory()
+    x_host = torch.from_numpy(x_np).pin_memory()
     dg.set_feed("x", x_host)
     torch.cuda.synchronize()
     dg.capture()
@@ -118,15 +126,18 @@ def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
     torch.cuda.synchronize()
     with bench.ClockSampler(local) as clk:
         max_ms = _time_replays(lambda: dg.launch(stream), args.steps, stream)
+    dg.status(stream)  # no integer overflow anywhere in the timed replays
     img_s = gb * args.steps / (max_ms / 1e3)
-    gflop_step = RESNET18_GFLOP_PER_IMAGE * cnt
+    # the int8 body has no FC head (0.001 GFLOP of the 3.628)
+    gflop_step = (RESNET18_GFLOP_PER_IMAGE - (0.001 if i8 else 0.0)) * cnt
 
     # e2e: pinned host images -> device, replay, logits -> host, gather.
     # The host->device copy of step i+1 runs on a copy stream into a second
     # staging buffer while step i's network runs (double buffering); the
     # network then takes its input with a device-to-device copy.
-    logits = dg.tensors["logits"]
-    out_host = torch.empty((cnt, 1000), dtype=torch.float32).pin_memory()
+    logits = dg.tensors[out_name]
+    per_img = int(np.prod(logits.shape[1:]))
+    out_host = torch.empty((cnt, per_img), dtype=logits.buf.dtype).pin_memory()
     feed = dg.feeds["x"].buf
     staging = [torch.empty_like(feed), torch.empty_like(feed)]
     copy_stream = torch.cuda.Stream()
@@ -148,7 +159,7 @@ def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
         feed.copy_(staging[b], non_blocking=True)
         consumed[b].record(cur)
         dg.launch(cur)
-        full = gather_rows(logits.buf[:cnt * 1000].view(cnt, 1000), gb)
+        full = gather_rows(logits.buf[:cnt * per_img].view(cnt, per_img), gb)
         out_host.copy_(full[start:start + cnt] if ws > 1 else full, non_blocking=True)
     for _ in range(2):
         e2e_step()
@@ -161,28 +172,33 @@ def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
     torch.cuda.synchronize()
     e2e_ms = _max_over_ranks((time.perf_counter() - t0) * 1e3 / e_steps)
     peak_tf = bench.load_peaks()[0] / (6.0 if compute == "f32tc" else 1.0)
+    if i8:
+        peak_tf = bench.measure_int8_peak() or peak_tf  # TOPS of cuBLASLt int8 on this GPU
     line = {
         "metric": "ResNet-18 inference img/s (config 4)", "value": round(img_s, 1),
         "unit": "img/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "f32tc": "f32"}[compute], "data": "synthetic",
-        "config": {"workload": f"configs[3]: ResNet-18 224x224 inference ({compute}), global batch {gb} "
-                               f"sharded {cnt}/rank, random-init weights, BN folded",
+        "dtype": {"bf16": "bf16", "f32tc": "f32", "i8": "i8"}[compute], "data": "synthetic",
+        "config": {"workload": f"configs[3]: ResNet-18 224x224 inference ({compute}"
+                               f"{', body: i8 in, i8 features out, requantize between layers' if i8 else ''}"
+                               f"), global batch {gb} sharded {cnt}/rank, random-init weights, BN folded",
                    "global_batch": gb, "parallelism": f"batch-sharded x{ws}, logits gathered",
                    "timing": "CUDA graph of the whole network per rank, events, max over ranks"},
         "roofline": {"bound": "tensor", "achieved": round(gflop_step / (max_ms / args.steps), 1),
                      "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(gflop_step / (max_ms / args.steps) / peak_tf, 3),
-                     "traffic": None, "kernel": "all launches of one network step"},
+                     "traffic": None, "kernel": "all launches of one network step",
+                     **({"peak_source": "torch._int_mm (cuBLASLt int8) 8192^3 on this GPU"} if i8 else {})},
         "gpu_launches": len(dg.steps) * args.steps,
         "clocks": clk.summary(),
         "e2e": {"value": round(gb / (e2e_ms / 1e3), 1), "unit": "img/s",
-                "h2d_bytes_per_step": cnt * 3 * 224 * 224 * 4,
-                "d2h_bytes_per_step": cnt * 1000 * 4, "ms_per_step": round(e2e_ms, 3),
-                "path": "pinned host f32 NCHW -> device (copy stream, double-buffered: step "
-                        "i+1's upload overlaps step i's network), CUDA-graph replay, logits "
-                        "gathered (all_gather) and copied to host"},
+                "h2d_bytes_per_step": x_host.numel() * x_host.element_size(),
+                "d2h_bytes_per_step": out_host.numel() * out_host.element_size(),
+                "ms_per_step": round(e2e_ms, 3),
+                "path": f"pinned host {'i8' if i8 else 'f32'} NCHW -> device (copy stream, "
+                        "double-buffered: step i+1's upload overlaps step i's network), "
+                        "CUDA-graph replay, outputs gathered (all_gather) and copied to host"},
         "cpu_baseline": _resnet_cpu_baseline(bench) if rank == 0 and ws == 1 and
         not args.no_cpu_baseline else None,
         "knobs": knobs,
@@ -207,7 +223,8 @@ def _tune_graph_convs(g, device, args, compute="bf16"):
         xs = f.node(root.inputs[0]).out_type.shape if f.find(root.inputs[0]) else None
         ws_ = f.node(root.inputs[1]).out_type.shape
         d = conv_desc("conv2d", xs, ws_, root.attrs,
-                      {"bf16": _abi.COMPUTE_BF16, "f32tc": _abi.COMPUTE_F32TC}[compute])
+                      {"bf16": _abi.COMPUTE_BF16, "f32tc": _abi.COMPUTE_F32TC,
+                       "i8": _abi.COMPUTE_I8}[compute])
         key = (tuple(xs), tuple(ws_), tuple(root.attrs.get("strides", (1, 1))))
         if key not in best:
             space = conv_space(str(key), d)

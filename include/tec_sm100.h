@@ -102,7 +102,12 @@ typedef enum {
   TEC_EPI_BIAS = 2,   /* x + b[oc]        R/src/ops.cpp:282-305 */
   TEC_EPI_ADD = 3,    /* x + r            R/src/ops.cpp:216-223 */
   TEC_EPI_MUL = 4,    /* x * r            R/src/ops.cpp:224-231 */
-  TEC_EPI_RELU = 5    /* max(x, 0)        R/src/ops.cpp:250-259 */
+  TEC_EPI_RELU = 5,   /* max(x, 0)        R/src/ops.cpp:250-259 */
+  /* int8 graphs (graph.py "requantize", not in the reference
+   * registry): i32 -> i8 clamp((x * rq_mult + 2^(rq_shift-1)) >> rq_shift,
+   * -128, 127). I8 compute only, the LAST member; y is then i8
+   * (out_dtype TEC_DT_I8) and K a multiple of 16. */
+  TEC_EPI_REQUANTIZE = 6
 } tec_epi_op;
 
 #define TEC_MAX_EPILOGUE 8
@@ -124,6 +129,12 @@ typedef struct {
   const void* bias;        /* BIAS operand: [K], f32 (i32 for I8)        */
   const void* residual;    /* ADD operand: output-shaped                  */
   const void* mul_operand; /* MUL operand: output-shaped                  */
+  /* int8 graphs. Zero-initialised = unused. */
+  int64_t rq_mult;         /* REQUANTIZE multiplier, 1 <= m < 2^31         */
+  int32_t rq_shift;        /* REQUANTIZE shift, 0 <= s <= 62               */
+  int32_t residual_i8;     /* 1: the ADD operand is an i8 tensor entering  */
+  int64_t residual_scale;  /*    as scale(cast(r, i32), residual_scale)    */
+                           /*    (|residual_scale| <= 2^24: no overflow)   */
 } tec_epilogue;
 
 /* Schedule knobs (Config = map<string,int64>, R/include/tec/autotune.hpp:43),

@@ -26,7 +26,7 @@ TEC_E_CUDA = 64
 
 DT_F32, DT_I32, DT_I8, DT_BF16 = 0, 1, 2, 3
 COMPUTE_BF16, COMPUTE_F32TC, COMPUTE_I8, COMPUTE_F32 = 1, 2, 3, 4
-EPI_SCALE, EPI_BIAS, EPI_ADD, EPI_MUL, EPI_RELU = 1, 2, 3, 4, 5
+EPI_SCALE, EPI_BIAS, EPI_ADD, EPI_MUL, EPI_RELU, EPI_REQUANTIZE = 1, 2, 3, 4, 5, 6
 MAX_EPILOGUE = 8
 
 
@@ -57,7 +57,11 @@ class Epilogue(C.Structure):
                 ("scale", C.c_double * MAX_EPILOGUE),
                 ("bias", C.c_void_p),
                 ("residual", C.c_void_p),
-                ("mul_operand", C.c_void_p)]
+                ("mul_operand", C.c_void_p),
+                ("rq_mult", C.c_int64),
+                ("rq_shift", C.c_int32),
+                ("residual_i8", C.c_int32),
+                ("residual_scale", C.c_int64)]
 
 
 class Knobs(C.Structure):

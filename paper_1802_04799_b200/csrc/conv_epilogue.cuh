@@ -46,6 +46,14 @@ __device__ __forceinline__ EpiProg make_prog(const EpilogueParams& e) {
   return g;
 }
 
+// requantize (int8 graphs, elementwise.cu states the semantics): int64
+// product (|t| < 2^31, m < 2^31: exact), round half up, clamp to i8.
+__device__ __forceinline__ int64_t requant(int64_t t, int64_t m, int s) {
+  t *= m;
+  if (s > 0) t = (t + (int64_t(1) << (s - 1))) >> s;
+  return t < -128 ? -128 : (t > 127 ? 127 : t);
+}
+
 // 32 elements as raw 32-bit words: bf16 pairs packed (16 words) or f32/i32.
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
@@ -133,19 +141,55 @@ __device__ __forceinline__ bool apply_int(const EpiProg& g, const EpilogueParams
     uint32_t b[kChunk];
     if (op == kEpiBias) load_bias32(bias_s, b);
     const int64_t s = op == kEpiScale ? e.iscale[i] : 1;
+    // i8 residual (res_i8): 4 packed bytes per operand word, entering as
+    // scale(cast(r, i32), res_scale) -- |res_scale| <= 2^24, no overflow
+    const bool r8 = op == kEpiAdd && e.res_i8;
+    if (op == kEpiBias || op == kEpiAdd) {
+      // 32-bit adds with an explicit signed-overflow bit ((a^s) & (b^s) < 0)
+      const int32_t rs = static_cast<int32_t>(e.res_scale);  // |rs| <= 2^24
+      uint32_t bits = 0u;
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        const int32_t a = static_cast<int32_t>(acc[j]);
+        const int32_t o = op == kEpiBias ? static_cast<int32_t>(b[j])
+                          : r8 ? static_cast<int32_t>(static_cast<int8_t>(opnd[j >> 2] >> (8 * (j & 3)))) * rs
+                               : static_cast<int32_t>(opnd[j]);
+        const uint32_t x = static_cast<uint32_t>(a) + static_cast<uint32_t>(o);
+        if (j < ncols) bits |= (static_cast<uint32_t>(a) ^ x) & (static_cast<uint32_t>(o) ^ x);
+        acc[j] = x;
+      }
+      ovf |= live && (bits >> 31);
+      continue;
+    }
+    if (op == kEpiRelu) {
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        const int32_t a = static_cast<int32_t>(acc[j]);
+        acc[j] = static_cast<uint32_t>(a < 0 ? 0 : a);
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
       int64_t t = static_cast<int32_t>(acc[j]);
       if (op == kEpiScale) t *= s;
-      else if (op == kEpiBias) t += static_cast<int32_t>(b[j]);
-      else if (op == kEpiAdd) t += static_cast<int32_t>(opnd[j]);
       else if (op == kEpiMul) t *= static_cast<int32_t>(opnd[j]);
-      else if (op == kEpiRelu) t = t < 0 ? 0 : t;
+      else if (op == kEpiRequant) t = requant(t, e.rq_mult, e.rq_shift);
       ovf |= live && (j < ncols) && (t < INT32_MIN || t > INT32_MAX);
       acc[j] = static_cast<uint32_t>(static_cast<int32_t>(t));
     }
   }
   return ovf;
+}
+
+// 32 i8 results (values already in [-128, 127]) packed 4 per word.
+__device__ __forceinline__ void pack_i8x32(const uint32_t (&v)[kChunk], uint32_t (&w)[kChunk]) {
+#pragma unroll
+  for (int k = 0; k < kChunk / 4; ++k)
+    w[k] = (v[4 * k] & 0xFFu) | ((v[4 * k + 1] & 0xFFu) << 8) | ((v[4 * k + 2] & 0xFFu) << 16) |
+           ((v[4 * k + 3] & 0xFFu) << 24);
+#pragma unroll
+  for (int k = kChunk / 4; k < kChunk; ++k) w[k] = 0u;
 }
 
 // ------------------------------------------------- per-thread fallback
@@ -285,8 +329,11 @@ __device__ __forceinline__ void epi_warp_block(const P& p, const EpiProg& g, uin
   const long long t0 = prof ? clock64() : 0;
   const EpilogueParams& e = p.epi;
   const bool bf = !kInt && p.out_type == kBF16;
-  const int es = bf ? 2 : 4;
+  const bool i8_out = kInt && p.out_type == kI8;  // requantize member (host-checked)
+  const int es = bf ? 2 : (i8_out ? 1 : 4);
   const int ncols = min(kChunk, p.oc - col0);
+  // operand element bytes: the output's, or 1 for an i8 residual (res_i8)
+  auto opnd_es = [&](int op) { return kInt && op == kEpiAdd && e.res_i8 ? 1 : (kInt ? 4 : es); };
   // One operand buffer: the first same-shape operand in member order is
   // fetched before waiting on TMEM; any later one is fetched on demand.
   uint32_t opnd[kChunk];
@@ -296,14 +343,14 @@ __device__ __forceinline__ void epi_warp_block(const P& p, const EpiProg& g, uin
   uint32_t acc[kChunk];
   tmem_ld32(taddr, acc);
   if (first) {
-    coalesced_load_block(first == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0, ncols,
-                         lane, my_row, stage, opnd);
+    coalesced_load_block(first == kEpiAdd ? e.residual : e.mul_operand, opnd_es(first), p.oc,
+                         col0, ncols, lane, my_row, stage, opnd);
     have = first;
   }
   auto opnd_fn = [&](int op) {
     if (have != op) {
-      coalesced_load_block(op == kEpiAdd ? e.residual : e.mul_operand, es, p.oc, col0, ncols,
-                           lane, my_row, stage, opnd);
+      coalesced_load_block(op == kEpiAdd ? e.residual : e.mul_operand, opnd_es(op), p.oc, col0,
+                           ncols, lane, my_row, stage, opnd);
       have = op;
     }
   };
@@ -312,8 +359,12 @@ __device__ __forceinline__ void epi_warp_block(const P& p, const EpiProg& g, uin
   uint32_t out[kChunk];
   if constexpr (kInt) {
     if (apply_int(g, e, acc, bias_s, ncols, my_row >= 0, opnd, opnd_fn)) *overflow = true;
+    if (i8_out) {
+      pack_i8x32(acc, out);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kChunk; ++j) out[j] = acc[j];
+      for (int j = 0; j < kChunk; ++j) out[j] = acc[j];
+    }
   } else {
     float v[kChunk];
 #pragma unroll
@@ -342,15 +393,27 @@ __device__ __forceinline__ void epi_warp_block(const P& p, const EpiProg& g, uin
 // The member programs fuse_pass produces for the benchmark networks, fixed
 // at compile time so a block is ~100 instructions: no op decoding, no
 // partial-block predicates (full 32-column block, oc % 8 == 0).
+// The int8-graph programs end in requantize and store i8 (ES = 1):
+// kProgBiasReluQ [bias, relu, requantize], kProgBiasAddReluQ [bias,
+// add(i8 residual, scaled), relu, requantize], kProgBiasQ [bias,
+// requantize] (the downsample branch).
 enum FastProg : int { kProgGeneric = 0, kProgNone = 1, kProgBias = 2, kProgBiasRelu = 3,
-                      kProgBiasAddRelu = 4 };
+                      kProgBiasAddRelu = 4, kProgBiasReluQ = 5, kProgBiasAddReluQ = 6,
+                      kProgBiasQ = 7 };
 
 __device__ __forceinline__ int classify_prog(const EpilogueParams& e) {
   if (e.n_ops == 0) return kProgNone;
   if (e.n_ops == 1 && e.ops[0] == kEpiBias) return kProgBias;
   if (e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu) return kProgBiasRelu;
-  if (e.n_ops == 3 && e.ops[0] == kEpiBias && e.ops[1] == kEpiAdd && e.ops[2] == kEpiRelu)
+  if (e.n_ops == 3 && e.ops[0] == kEpiBias && e.ops[1] == kEpiAdd && e.ops[2] == kEpiRelu &&
+      !e.res_i8)
     return kProgBiasAddRelu;
+  if (e.n_ops == 3 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRelu && e.ops[2] == kEpiRequant)
+    return kProgBiasReluQ;
+  if (e.n_ops == 2 && e.ops[0] == kEpiBias && e.ops[1] == kEpiRequant) return kProgBiasQ;
+  if (e.n_ops == 4 && e.ops[0] == kEpiBias && e.ops[1] == kEpiAdd && e.ops[2] == kEpiRelu &&
+      e.ops[3] == kEpiRequant && e.res_i8)
+    return kProgBiasAddReluQ;
   return kProgGeneric;
 }
 
@@ -466,7 +529,9 @@ __device__ __forceinline__ void epi_block(const P& p, const EpiProg& g, int prog
 // bank-conflict free for the one-row-per-lane writes.
 template <int ES>
 __device__ __forceinline__ uint32_t box_off(int row, int chunk) {
-  if constexpr (ES == 2)
+  if constexpr (ES == 1)  // i8 rows of 32 B, SWIZZLE_32B: chunk ^ address bit 7
+    return static_cast<uint32_t>(row * 32 + ((chunk ^ ((row >> 2) & 1)) << 4));
+  else if constexpr (ES == 2)
     return static_cast<uint32_t>(row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4));
   else
     return static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
@@ -503,18 +568,77 @@ __device__ __forceinline__ void load_res_box(const uint8_t* rrow, int lane, uint
   }
 }
 
+// Requantize parameters of the Q programs (EpilogueParams fields).
+struct QParams {
+  int64_t mult = 1;
+  int32_t shift = 0;
+  int64_t res_scale = 1;
+};
+
 template <int PROG, int ES, bool kInt = false>
 __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane,
                                                const uint32_t* bias_s, uint32_t box,
                                                bool* ovf = nullptr,
-                                               const uint8_t* rrow = nullptr) {
+                                               const uint8_t* rrow = nullptr,
+                                               const QParams& qp = QParams{}) {
   static_assert(!(kInt && PROG == kProgBiasAddRelu), "int residual programs use the SIMT path");
+  if constexpr (PROG == kProgBiasReluQ || PROG == kProgBiasAddReluQ || PROG == kProgBiasQ) {
+    // int8 graphs: bias -> (+ i8 residual * res_scale) -> relu -> requantize,
+    // each integer member range-checked (as apply_int does in int64); 32 i8
+    // results = this lane's 32-byte box row.
+    static_assert(kInt && ES == 1, "the Q programs store i8");
+    uint32_t res[kChunk];
+    if constexpr (PROG == kProgBiasAddReluQ) load_res_box<1>(rrow, lane, box, res);
+    uint32_t b[kChunk];
+    load_bias32(bias_s, b);
+    // 32-bit arithmetic with explicit overflow bits (the int64 form of
+    // apply_int costs ~3x the instructions, and the epilogue is issue-bound
+    // at i8 output): signed a + b overflows iff (a ^ s) & (b ^ s) < 0.
+    uint32_t ovf_bits = 0u;
+    const uint32_t m = static_cast<uint32_t>(qp.mult);  // 1 <= m < 2^31 (host-checked)
+    const int sh = qp.shift;
+    const uint64_t half = sh > 0 ? (uint64_t(1) << (sh - 1)) : 0u;
+    const int32_t rs = static_cast<int32_t>(qp.res_scale);  // |rs| <= 2^24: r * rs fits i32
+    uint32_t w[kChunk / 4];
+#pragma unroll
+    for (int k = 0; k < kChunk / 4; ++k) w[k] = 0u;
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j) {
+      const int32_t a = static_cast<int32_t>(acc[j]), bj = static_cast<int32_t>(b[j]);
+      int32_t x = static_cast<int32_t>(static_cast<uint32_t>(a) + static_cast<uint32_t>(bj));
+      ovf_bits |= static_cast<uint32_t>((a ^ x) & (bj ^ x));
+      if constexpr (PROG == kProgBiasAddReluQ) {
+        const int32_t r = static_cast<int32_t>(static_cast<int8_t>(res[j >> 2] >> (8 * (j & 3)))) * rs;
+        const int32_t x2 = static_cast<int32_t>(static_cast<uint32_t>(x) + static_cast<uint32_t>(r));
+        ovf_bits |= static_cast<uint32_t>((x ^ x2) & (r ^ x2));
+        x = x2;
+      }
+      uint32_t q;
+      if constexpr (PROG != kProgBiasQ) {
+        // after relu x >= 0: an unsigned 32 x 32 -> 64 product
+        const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x < 0 ? 0 : x)) * m + half;
+        const uint64_t v = t >> sh;
+        q = v > 127u ? 127u : static_cast<uint32_t>(v);
+      } else {
+        const int64_t t = static_cast<int64_t>(x) * static_cast<int64_t>(static_cast<int32_t>(m)) +
+                          static_cast<int64_t>(half);
+        const int64_t v = t >> sh;  // arithmetic: floor
+        q = static_cast<uint32_t>(static_cast<int32_t>(v < -128 ? -128 : (v > 127 ? 127 : v)));
+      }
+      w[j >> 2] |= (q & 0xFFu) << (8 * (j & 3));
+    }
+    if ((ovf_bits >> 31) && ovf) *ovf = true;
+    sts128(box + box_off<1>(lane, 0), make_uint4(w[0], w[1], w[2], w[3]));
+    sts128(box + box_off<1>(lane, 1), make_uint4(w[4], w[5], w[6], w[7]));
+    return;
+  }
   uint32_t res[kChunk];
   if constexpr (PROG == kProgBiasAddRelu) load_res_box<ES>(rrow, lane, box, res);
   uint32_t b[kChunk];
   if constexpr (PROG != kProgNone) load_bias32(bias_s, b);
   if constexpr (kInt) {
-    static_assert(ES == 4, "int8 conv stores i32");
+    static_assert(ES == 4 || PROG == kProgBiasReluQ || PROG == kProgBiasAddReluQ || PROG == kProgBiasQ,
+                  "int8 conv stores i32 (i8 only through the Q programs above)");
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
@@ -593,11 +717,12 @@ __device__ __forceinline__ void row_col_to_box(const float* lo, const float* hi_
 template <int PROG, int ES, bool kInt = false>
 __device__ __forceinline__ void epi_block_box(uint32_t taddr, int lane, const uint32_t* bias_s,
                                               uint32_t box, bool* ovf = nullptr,
-                                              const uint8_t* rrow = nullptr) {
+                                              const uint8_t* rrow = nullptr,
+                                              const QParams& qp = QParams{}) {
   uint32_t acc[kChunk];
   tmem_ld32(taddr, acc);
   tmem_ld_wait();
-  epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s, box, ovf, rrow);
+  epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s, box, ovf, rrow, qp);
 }
 
 // One warp's 32 accumulator rows x BN columns through the TMA-store path.
@@ -610,7 +735,8 @@ template <int PROG, int ES, int BN, bool kInt, typename SrcFn, typename StoreFn>
 __device__ __forceinline__ void epi_rows_tma_src(SrcFn&& src, int lane, const uint32_t* bias_s,
                                                  uint32_t stage, int valid_cols, uint32_t& cnt,
                                                  bool* ovf, StoreFn&& store,
-                                                 const uint8_t* rrow = nullptr) {
+                                                 const uint8_t* rrow = nullptr,
+                                                 const QParams& qp = QParams{}) {
   constexpr uint32_t kBox = 32 * 32 * ES;
   constexpr uint32_t kSlots = 4096 / kBox;
 #pragma unroll 1
@@ -621,7 +747,7 @@ __device__ __forceinline__ void epi_rows_tma_src(SrcFn&& src, int lane, const ui
     if (lane == 0) bulk_wait_read<kSlots - 1>();  // the box's previous store has read it
     __syncwarp();
     epi_acc_to_box<PROG, ES, kInt>(acc, lane, bias_s + c0, box, ovf,
-                                   rrow ? rrow + c0 * ES : nullptr);
+                                   rrow ? rrow + c0 * ES : nullptr, qp);
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
@@ -636,13 +762,14 @@ template <int PROG, int ES, int BN, bool kInt, typename StoreFn>
 __device__ __forceinline__ void epi_rows_tma(uint32_t taddr0, int lane, const uint32_t* bias_s,
                                              uint32_t stage, int valid_cols, uint32_t& cnt,
                                              bool* ovf, StoreFn&& store,
-                                             const uint8_t* rrow = nullptr) {
+                                             const uint8_t* rrow = nullptr,
+                                             const QParams& qp = QParams{}) {
   epi_rows_tma_src<PROG, ES, BN, kInt>(
       [&](int c0, uint32_t (&acc)[kChunk]) {
         tmem_ld32(taddr0 + c0, acc);
         tmem_ld_wait();
       },
-      lane, bias_s, stage, valid_cols, cnt, ovf, store, rrow);
+      lane, bias_s, stage, valid_cols, cnt, ovf, store, rrow, qp);
 }
 
 // Cooperative per-tile bias staging: `nthreads` epilogue threads copy the

@@ -444,10 +444,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         epi::named_bar_sync(1 + grp, 128);
         staged_n_tile = n_tile;
       }
-      if (kResTma && tma_epi && fast == epi::kProgBiasAddRelu && !dummy) {
+      if (tma_epi && !dummy &&
+          ((kResTma && fast == epi::kProgBiasAddRelu) || fast == epi::kProgBiasAddReluQ)) {
         // The residual rows are read right after the accumulator lands: pull
         // this lane's lines into L2 while the MMAs still run.
-        const int es = p.out_type == kBF16 ? 2 : 4;
+        const int es = fast == epi::kProgBiasAddReluQ ? 1 : p.out_type == kBF16 ? 2 : 4;
         for (int ms = 0; ms < MS; ++ms) {
           const int v = ms * 128 + static_cast<int>(q * 32 + lane);
           const int ohl = v / p.wp, ow = v - ohl * p.wp, oh = band * p.th + ohl;
@@ -484,6 +485,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // Host guarantees: MS*128 rows x 32*ES bytes <= 16 KB and
           // wp*32*ES a multiple of 128 B (TMA source alignment); the
           // swizzle is absolute-address based, so any such row start works.
+          epi::QParams qp;  // the Q programs (int8 graphs)
+          qp.mult = p.epi.rq_mult;
+          qp.shift = p.epi.rq_shift;
+          qp.res_scale = p.epi.res_scale;
           auto run = [&](auto prog_c, auto es_c) {
             constexpr int kProg = decltype(prog_c)::value, kES = decltype(es_c)::value;
             constexpr uint32_t kRowB = 32 * kES;
@@ -504,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
               for (int ms = 0; ms < MS; ++ms) {
                 const uint8_t* rrow = nullptr;
-                if constexpr (kProg == epi::kProgBiasAddRelu) {
+                if constexpr (kProg == epi::kProgBiasAddRelu || kProg == epi::kProgBiasAddReluQ) {
                   // virtual row -> output pixel (junk rows: no residual, not stored)
                   const int v = ms * 128 + static_cast<int>(q * 32 + lane);
                   const int ohl = v / p.wp, ow = v - ohl * p.wp, oh = band * p.th + ohl;
@@ -545,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                   epi::epi_block_box<kProg, kES, kInt>(
                       tmem_base + ((q * 32) << 16) + acc * Cfg::kAccCols + ms * BN + c0,
-                      static_cast<int>(lane), bias_s + c0, box, &overflow, rrow);
+                      static_cast<int>(lane), bias_s + c0, box, &overflow, rrow, qp);
                 }
               }
               if constexpr (kPair) {
@@ -586,11 +591,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           using P1 = std::integral_constant<int, epi::kProgBias>;
           using P2 = std::integral_constant<int, epi::kProgBiasRelu>;
           using P3 = std::integral_constant<int, epi::kProgBiasAddRelu>;
+          using PQ = std::integral_constant<int, epi::kProgBiasReluQ>;
+          using PAQ = std::integral_constant<int, epi::kProgBiasAddReluQ>;
+          using PBQ = std::integral_constant<int, epi::kProgBiasQ>;
+          using E1 = std::integral_constant<int, 1>;
           using E2 = std::integral_constant<int, 2>;
           using E4 = std::integral_constant<int, 4>;
           if constexpr (kInt) {
             if (fast == epi::kProgNone) run(P0{}, E4{});
             else if (fast == epi::kProgBias) run(P1{}, E4{});
+            else if (fast == epi::kProgBiasReluQ) run(PQ{}, E1{});
+            else if (fast == epi::kProgBiasAddReluQ) run(PAQ{}, E1{});
+            else if (fast == epi::kProgBiasQ) run(PBQ{}, E1{});
             else run(P2{}, E4{});
           } else if (p.out_type == kBF16) {
             if (fast == epi::kProgNone) run(P0{}, E2{});

@@ -13,6 +13,7 @@ enum EpiOp : int32_t {
   kEpiAdd = 3,    // x + r (same shape) R/src/ops.cpp:216-223
   kEpiMul = 4,    // x * r (same shape) R/src/ops.cpp:224-231
   kEpiRelu = 5,   // max(x, 0)        R/src/ops.cpp:250-259
+  kEpiRequant = 6,  // i32 -> i8 clamp((x*m + 2^(s-1)) >> s) (int8 graphs; last member)
 };
 
 enum ElemType : int32_t { kF32 = 0, kI32 = 1, kI8 = 2, kBF16 = 3 };
@@ -25,8 +26,15 @@ struct EpilogueParams {
   float fscale[kMaxEpi];    // float-rounded scale factors (cstf)
   int64_t iscale[kMaxEpi];  // integral scale factors (cst)
   const void* bias;         // [OC], accumulator dtype (f32 / i32)
-  const void* residual;     // NHWC [M][OC], output dtype
+  const void* residual;     // NHWC [M][OC], output dtype (res_i8: i8)
   const void* mul_operand;  // NHWC [M][OC], output dtype
+  // int8 graphs: the requantize member's parameters, and an
+  // i8 residual entering as scale(cast(r, i32), res_scale) -- the identity
+  // shortcut side chain fused into the add's operand read.
+  int64_t rq_mult;
+  int32_t rq_shift;
+  int32_t res_i8;
+  int64_t res_scale;
 };
 
 // Implicit-GEMM convolution: GEMM M = N*OH*OW output pixels (NHWC order),

@@ -352,20 +352,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           constexpr bool kInt = KIND == MmaKind::kI8;
           auto run = [&](auto prog_c, auto es_c) {
             constexpr int kProg = decltype(prog_c)::value, kES = decltype(es_c)::value;
+            // the Q programs' i8 residual row (int8 graphs); NULL past M
+            const uint8_t* rrow = nullptr;
+            if constexpr (kProg == epi::kProgBiasAddReluQ)
+              if (row_ok)
+                rrow = static_cast<const uint8_t*>(p.epi.residual) +
+                       static_cast<int64_t>(row) * p.oc + n_tile * BN;
+            epi::QParams qp;
+            qp.mult = p.epi.rq_mult;
+            qp.shift = p.epi.rq_shift;
+            qp.res_scale = p.epi.res_scale;
             epi::epi_rows_tma<kProg, kES, BN, kInt>(
                 tmem_base + ((q * 32) << 16) + acc * BN, static_cast<int>(lane), bias_s,
                 stage_u32, p.oc - n_tile * BN, box_cnt, &overflow, [&](uint32_t box, int c0) {
                   tma_store_2d(&tm_y, box, n_tile * BN + c0, row0);
-                });
+                }, rrow, qp);
           };
           using P0 = std::integral_constant<int, epi::kProgNone>;
           using P1 = std::integral_constant<int, epi::kProgBias>;
           using P2 = std::integral_constant<int, epi::kProgBiasRelu>;
+          using PQ = std::integral_constant<int, epi::kProgBiasReluQ>;
+          using PAQ = std::integral_constant<int, epi::kProgBiasAddReluQ>;
+          using PBQ = std::integral_constant<int, epi::kProgBiasQ>;
+          using E1 = std::integral_constant<int, 1>;
           using E2 = std::integral_constant<int, 2>;
           using E4 = std::integral_constant<int, 4>;
           if constexpr (kInt) {
             if (fast == epi::kProgNone) run(P0{}, E4{});
             else if (fast == epi::kProgBias) run(P1{}, E4{});
+            else if (fast == epi::kProgBiasReluQ) run(PQ{}, E1{});
+            else if (fast == epi::kProgBiasAddReluQ) run(PAQ{}, E1{});
+            else if (fast == epi::kProgBiasQ) run(PBQ{}, E1{});
             else run(P2{}, E4{});
           } else if (p.out_type == kBF16) {
             if (fast == epi::kProgNone) run(P0{}, E2{});

@@ -285,6 +285,39 @@ __global__ void pack_s2d_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
   }
 }
 
+// int8 (cp = 32, c <= 8): one thread per space-to-depth pixel, its 32
+// channel bytes as two 16-byte stores (the per-element kernel above made
+// one 1-byte store per thread: 770 us for the ResNet-18 b256 stem).
+__global__ void pack_s2d_i8_kernel(const int8_t* __restrict__ in, int8_t* __restrict__ out,
+                                   int n, int c, int h, int w, int ph, int pw, int h2, int w2) {
+  const int total = n * h2 * w2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int jj = i % w2;
+    const int t = i / w2;
+    const int ii = t % h2;
+    const int nn = t / h2;
+    uint32_t wd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) wd[k] = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int y = 2 * ii + q / 2 - ph, x = 2 * jj + q % 2 - pw;
+      const bool in_img = y >= 0 && y < h && x >= 0 && x < w;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        if (cc >= c) break;
+        const uint32_t b =
+            in_img ? static_cast<uint8_t>(in[((static_cast<int64_t>(nn) * c + cc) * h + y) * w + x]) : 0u;
+        const int e = q * c + cc;  // channel (dy*2+dx)*C + c
+        wd[e >> 2] |= b << (8 * (e & 3));
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(i) * 32);
+    dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+  }
+}
+
 // Row-staged variant (bf16, cp = 16, w % 4 == 0): one CTA per space-to-depth
 // row (image nn, row ii). The CTA reads the two input rows of every channel
 // with coalesced float4 loads into shared memory (zero padding included),
@@ -517,6 +550,15 @@ int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c
     const int blocks = static_cast<int>(std::min<int64_t>((px + 255) / 256, 148 * 32));
     pack_s2d_bf16_kernel<<<blocks, 256, 0, st>>>(
         static_cast<const float*>(in), static_cast<__nv_bfloat16*>(out), static_cast<int>(n),
+        static_cast<int>(c), static_cast<int>(h), static_cast<int>(w), static_cast<int>(ph),
+        static_cast<int>(pw), static_cast<int>(h2), static_cast<int>(w2));
+    return cudaGetLastError();
+  }
+  if (in_type == kI8 && mode == kPackI8 && cp == 32 && c <= 8 && n * h2 * w2 < (1ll << 31)) {
+    const int64_t px = n * h2 * w2;
+    const int blocks = static_cast<int>(std::min<int64_t>((px + 255) / 256, 148 * 32));
+    pack_s2d_i8_kernel<<<blocks, 256, 0, st>>>(
+        static_cast<const int8_t*>(in), static_cast<int8_t*>(out), static_cast<int>(n),
         static_cast<int>(c), static_cast<int>(h), static_cast<int>(w), static_cast<int>(ph),
         static_cast<int>(pw), static_cast<int>(h2), static_cast<int>(w2));
     return cudaGetLastError();

@@ -72,6 +72,41 @@ __global__ void max_pool_kernel(PoolParams p) {
   }
 }
 
+// int8: the same walk on 16 channels as four SIMD words (__vmaxs4: a
+// per-byte signed max per instruction; the generic kernel's per-byte
+// compare/select went through local memory).
+__global__ void max_pool_i8_kernel(PoolParams p) {
+  const int cv = p.c / 16;
+  const uint32_t total = static_cast<uint32_t>(p.n) * p.oh * p.ow * cv;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t pix = i / cv;
+    const int v = static_cast<int>(i - pix * cv);
+    const uint32_t row = pix / p.ow;
+    const int ow = static_cast<int>(pix - row * p.ow);
+    const int n = static_cast<int>(row / p.oh);
+    const int oh = static_cast<int>(row - n * p.oh);
+    uint4 best = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);  // -128
+    bool any = false;
+    const int8_t* base = static_cast<const int8_t*>(p.x) + static_cast<int64_t>(n) * p.h * p.w * p.c + v * 16;
+    for (int rh = 0; rh < p.r; ++rh) {
+      const int ih = oh * p.sh + rh - p.ph;
+      if (ih < 0 || ih >= p.h) continue;
+      for (int rw = 0; rw < p.s; ++rw) {
+        const int iw = ow * p.sw + rw - p.pw;
+        if (iw < 0 || iw >= p.w) continue;
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * p.w + iw) * p.c));
+        best.x = __vmaxs4(best.x, t.x);
+        best.y = __vmaxs4(best.y, t.y);
+        best.z = __vmaxs4(best.z, t.z);
+        best.w = __vmaxs4(best.w, t.w);
+        any = true;
+      }
+    }
+    if (!any) best = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(static_cast<int8_t*>(p.y) + static_cast<int64_t>(pix) * p.c + v * 16) = best;
+  }
+}
+
 // One thread: one (n, 16-byte channel vector); loops the H x W plane.
 template <typename T, typename O>
 __global__ void global_avg_pool_kernel(PoolParams p) {
@@ -127,7 +162,7 @@ int launch_max_pool(const PoolParams& p, cudaStream_t st) {
     case kBF16: max_pool_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(p); break;
     case kF32: max_pool_kernel<float><<<grid, block, 0, st>>>(p); break;
     case kI32: max_pool_kernel<int32_t><<<grid, block, 0, st>>>(p); break;
-    case kI8: max_pool_kernel<int8_t><<<grid, block, 0, st>>>(p); break;
+    case kI8: max_pool_i8_kernel<<<grid, block, 0, st>>>(p); break;
     default: return -1;
   }
   return cudaGetLastError();

@@ -262,12 +262,16 @@ CUtensorMapSwizzle swizzle_of(int bytes) {
 // first (dims[0] = OC), box 32 channels x `box_px` pixels (x 1 x 1),
 // swizzled to match epi::box_off. Leaves *ok false when the layout does not
 // allow it (integer output, or an OC row pitch that is not a multiple of 16 B).
+int elem_bytes(int32_t t) { return t == TEC_DT_I8 ? 1 : t == TEC_DT_BF16 ? 2 : 4; }
+
 void make_store_map(CUtensorMap* tm, void* y, int32_t out_dtype, int rank,
                     const cuuint64_t* dims, int box_px, bool* ok) {
   *ok = false;
   std::memset(tm, 0, sizeof(*tm));
-  if (out_dtype != TEC_DT_BF16 && out_dtype != TEC_DT_F32 && out_dtype != TEC_DT_I32) return;
-  const int es = out_dtype == TEC_DT_BF16 ? 2 : 4;
+  if (out_dtype != TEC_DT_BF16 && out_dtype != TEC_DT_F32 && out_dtype != TEC_DT_I32 &&
+      out_dtype != TEC_DT_I8)
+    return;
+  const int es = elem_bytes(out_dtype);
   if ((dims[0] * es) % 16 || box_px < 1 || box_px > 256) return;
   cuuint64_t strides[3];
   cuuint64_t pitch = es;
@@ -276,16 +280,18 @@ void make_store_map(CUtensorMap* tm, void* y, int32_t out_dtype, int rank,
   cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = driver_fns().tiled(
       tm,
-      es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+      es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+      : es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
       : out_dtype == TEC_DT_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
       (cuuint32_t)rank, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      es == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+      // 32-column boxes: rows of 32 (i8), 64 (bf16) or 128 (f32 / i32) bytes,
+      // each with the swizzle of its row width (conv_epilogue.cuh box_off)
+      es == 1 ? CU_TENSOR_MAP_SWIZZLE_32B : es == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   *ok = r == CUDA_SUCCESS;
 }
 
 // ------------------------------------------------------ layout planning
-int elem_bytes(int32_t t) { return t == TEC_DT_I8 ? 1 : t == TEC_DT_BF16 ? 2 : 4; }
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -432,8 +438,14 @@ tec_status build_epilogue(const tec_epilogue* e, bool integer, EpilogueParams* o
     return fail(TEC_E_LOWERING, "more than one bias_add / add / mul member in one fused conv");
   for (int i = 0; i < e->n_ops; ++i) {
     const int op = e->ops[i];
-    if (op < TEC_EPI_SCALE || op > TEC_EPI_RELU)
+    if (op < TEC_EPI_SCALE || op > TEC_EPI_REQUANTIZE)
       return fail(TEC_E_UNKNOWN_OPERATOR, "unknown epilogue op " + std::to_string(op));
+    if (op == TEC_EPI_REQUANTIZE) {
+      if (!integer) return fail(TEC_E_SHAPE_MISMATCH, "requantize wants i32 data (I8 compute)");
+      if (i != e->n_ops - 1) return fail(TEC_E_LOWERING, "requantize must be the last member");
+      if (e->rq_mult < 1 || e->rq_mult >= (int64_t(1) << 31) || e->rq_shift < 0 || e->rq_shift > 62)
+        return fail(TEC_E_SHAPE_MISMATCH, "requantize needs 1 <= multiplier < 2^31, 0 <= shift <= 62");
+    }
     out->ops[i] = op;
     if (op == TEC_EPI_SCALE) {
       const double c = e->scale[i];
@@ -449,9 +461,35 @@ tec_status build_epilogue(const tec_epilogue* e, bool integer, EpilogueParams* o
     if (op == TEC_EPI_MUL && !e->mul_operand)
       return fail(TEC_E_SHAPE_MISMATCH, "mul needs a second operand");
   }
+  if (e->residual_i8) {
+    if (!integer || !n_add) return fail(TEC_E_LOWERING, "an i8 residual needs I8 compute and an add");
+    if (e->residual_scale < -(int64_t(1) << 24) || e->residual_scale > (int64_t(1) << 24))
+      return fail(TEC_E_LOWERING, "|residual_scale| > 2^24");
+  }
   out->bias = e->bias;
   out->residual = e->residual;
   out->mul_operand = e->mul_operand;
+  out->rq_mult = e->rq_mult;
+  out->rq_shift = e->rq_shift;
+  out->res_i8 = e->residual_i8 ? 1 : 0;
+  out->res_scale = e->residual_i8 ? e->residual_scale : 1;
+  return TEC_OK;
+}
+
+// The requantize member (last) makes y i8.
+bool epi_requant(const EpilogueParams& e) { return e.n_ops > 0 && e.ops[e.n_ops - 1] == kEpiRequant; }
+
+// I8 output / i8 residual constraints the kernels rely on (whole 16-byte
+// i8 vectors per row, the coalesced / TMA epilogues).
+tec_status check_int8_epilogue(const EpilogueParams& e, const tec_conv_desc* d, int32_t out_dtype,
+                               const tec_knobs* kn) {
+  const bool rq = epi_requant(e);
+  if (rq != (out_dtype == TEC_DT_I8))
+    return fail(TEC_E_SHAPE_MISMATCH, rq ? "a requantize epilogue writes i8 (out_dtype I8)"
+                                         : "i8 output needs a requantize member");
+  if ((rq || e.res_i8) && (d->k % (e.res_i8 ? 32 : 16) || (kn && kn->vec != 0)))
+    return fail(TEC_E_LOWERING, "i8 output / i8 residual: K a multiple of 16 (32 with an i8 "
+                                "residual) and the default epilogue");
   return TEC_OK;
 }
 
@@ -525,10 +563,18 @@ struct HaloChoice {
 // over the SMs. Returns false when no halo instance fits.
 // pair_ok: the epilogue program has the TMA-store path the paired-tap
 // instances need (kPair). Knob tile_k: 2 = halo without pairing, 4 = paired.
+// Padded halo row width: even (bf16 / f32 / i32 output) or a multiple of 4
+// (i8 output), so every output row of the group-staged TMA epilogue starts
+// on a 128-byte boundary (wp * 32 * elem % 128 == 0).
+int halo_wp(const tec_conv_desc* d, int32_t out_dtype) {
+  const int64_t a = out_dtype == TEC_DT_I8 ? 4 : 2;
+  return (int)((d->w + 2 * d->pad_w + a - 1) / a * a);
+}
+
 bool plan_halo(const tec_conv_desc* d, const Plan& pl, const tec_knobs* kn, int sms,
                int32_t out_dtype, bool pair_ok, HaloChoice* out) {
   if (d->stride_h != 1 || d->stride_w != 1) return false;
-  const int wp = (int)((d->w + 2 * d->pad_w + 1) & ~int64_t(1));  // even: 128-B aligned output rows in the TMA epilogue
+  const int wp = halo_wp(d, out_dtype);
   const int es = elem_bytes(pl.act);
   if (wp > 256 || (pl.oh + d->r - 1) < 1) return false;
   double best = 1e30;
@@ -634,7 +680,7 @@ tec_status run_conv_halo(const tec_conv_desc* d, const Plan& pl, const HaloChoic
   const DriverFns& fns = driver_fns();
   const int es = elem_bytes(pl.act);
   const int cb = pl.swz / es;
-  const int wp = (int)((d->w + 2 * d->pad_w + 1) & ~int64_t(1));  // even: 128-B aligned output rows in the TMA epilogue
+  const int wp = halo_wp(d, out_dtype);
   const CUtensorMapDataType tdt = pl.act == TEC_DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                   : pl.act == TEC_DT_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -823,8 +869,8 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   const int es = elem_bytes(pl.act);
   const int cb = pl.swz / es;  // channels per block
   if (pl.cp % cb) return fail(TEC_E_INTERNAL, "channel padding does not match block");
-  if (pl.kind == MmaKind::kI8 && out_dtype != TEC_DT_I32)
-    return fail(TEC_E_LOWERING, "int8 conv produces i32");
+  if (pl.kind == MmaKind::kI8 && out_dtype != TEC_DT_I32 && out_dtype != TEC_DT_I8)
+    return fail(TEC_E_LOWERING, "int8 conv produces i32 (i8 after a requantize member)");
   if (pl.kind != MmaKind::kI8 && out_dtype != TEC_DT_F32 && out_dtype != TEC_DT_BF16)
     return fail(TEC_E_LOWERING, "float conv produces f32 or bf16");
 
@@ -1439,6 +1485,7 @@ tec_status tec_conv2d_fused(const tec_conv_desc* d, const tec_epilogue* epi,
   EpilogueParams ep;
   st = build_epilogue(epi, pl.kind == MmaKind::kI8, &ep);
   if (st) return st;
+  if (pl.kind == MmaKind::kI8 && (st = check_int8_epilogue(ep, d, out_dtype, knobs))) return st;
   if (!x_packed || !w_packed || !y) return fail(TEC_E_INTERNAL, "null buffer");
   if (d->compute == TEC_COMPUTE_F32) {
     if (out_dtype != TEC_DT_F32) return fail(TEC_E_LOWERING, "f32 path produces f32");
@@ -1517,6 +1564,8 @@ tec_status tec_depthwise_fused(const tec_conv_desc* d, const tec_epilogue* epi,
   EpilogueParams ep;
   st = build_epilogue(epi, d->compute == TEC_COMPUTE_I8, &ep);
   if (st) return st;
+  if (epi_requant(ep) || ep.res_i8)
+    return fail(TEC_E_LOWERING, "depthwise: no requantize / i8-residual epilogue");
   DepthwiseParams p{};
   p.n = (int32_t)d->n; p.h = (int32_t)d->h; p.w = (int32_t)d->w; p.c = (int32_t)d->c;
   p.oh = (int32_t)pl.oh; p.ow = (int32_t)pl.ow;
@@ -1615,7 +1664,8 @@ tec_status tec_conv_plan(const tec_conv_desc* d, const tec_epilogue* epi,
     if (e.residual) e.residual = dummy;
     if (e.mul_operand) e.mul_operand = dummy;
   }
-  const int32_t out_t = d->compute == TEC_COMPUTE_I8 ? TEC_DT_I32
+  const bool rq = epi && epi->n_ops > 0 && epi->ops[epi->n_ops - 1] == TEC_EPI_REQUANTIZE;
+  const int32_t out_t = d->compute == TEC_COMPUTE_I8 ? (rq ? TEC_DT_I8 : TEC_DT_I32)
                         : d->compute == TEC_COMPUTE_BF16 ? TEC_DT_BF16 : TEC_DT_F32;
   g_plan = out;
   st = tec_conv2d_fused(d, epi ? &e : nullptr, knobs, dummy, dummy, dummy, out_t, nullptr, nullptr);
@@ -1920,7 +1970,8 @@ tec_status tec_measure(const tec_conv_desc* d, const tec_epilogue* epi,
   tec_conv_layout lay;
   if ((st = tec_conv_layout_of(d, &lay))) return st;
   const bool integer = d->compute == TEC_COMPUTE_I8;
-  const int32_t out_t = integer ? TEC_DT_I32
+  const bool rq = epi && epi->n_ops > 0 && epi->ops[epi->n_ops - 1] == TEC_EPI_REQUANTIZE;
+  const int32_t out_t = integer ? (rq ? TEC_DT_I8 : TEC_DT_I32)
                         : d->compute == TEC_COMPUTE_F32 || d->compute == TEC_COMPUTE_F32TC
                             ? TEC_DT_F32 : TEC_DT_BF16;
   void *x = nullptr, *w = nullptr, *y = nullptr, *b = nullptr, *r = nullptr, *fl = nullptr;

@@ -183,6 +183,21 @@ def split_conv_members(n: GraphNode):
     return root, head, sides, tail
 
 
+def _i8_shortcut_scale(members) -> Optional[int]:
+    """c for a side chain [cast(i32)] (c = 1) or [cast(i32), scale(c)] with an
+    integral |c| <= 2^24 (no i32 overflow for any i8 value), else None."""
+    if not members or members[0].op != "cast" or members[0].attrs.get("dtype", "i32") != "i32":
+        return None
+    if len(members) == 1:
+        return 1
+    if len(members) != 2 or members[1].op != "scale":
+        return None
+    c = float(members[1].attrs.get("scale", 1.0))
+    if c != int(c) or abs(c) > 2 ** 24:
+        return None
+    return int(c)
+
+
 class DeviceGraph:
     def __init__(self, g: ComputeGraph, compute: str = "bf16", device: int = 0,
                  knobs: Optional[Dict[str, dict]] = None):
@@ -450,14 +465,34 @@ class DeviceGraph:
                                        "need compute 'i8'")
         if len(sides) > 1:
             raise TecError(E_LOWERING, f"fused node '{n.id}': more than one side chain")
+        epi = _abi.Epilogue()
+        # int8 graphs: a [requantize] tail and a [cast(i32), scale(c)]
+        # shortcut fold into the conv epilogue itself (conv_epilogue.cuh Q
+        # programs: i8 residual in, i8 out) when the kernels' conditions
+        # hold; otherwise they run as elementwise launches around the conv.
+        fuse_tail = (len(tail) == 1 and tail[0].op == "requantize" and d.k % 16 == 0
+                     and not d.depthwise)
+        if fuse_tail:
+            epi.rq_mult = int(tail[0].attrs.get("multiplier", 1))
+            epi.rq_shift = int(tail[0].attrs.get("shift", 0))
+            tail = []
+        fused_side = {}
+        for first, last, members in list(sides):
+            c = _i8_shortcut_scale(members)
+            src = self.tensors[first]
+            adds = [it for it in items if it[0] == "add" and it[1] == last]
+            if (c is not None and fuse_tail and d.k % 32 == 0 and src.layout == "nhwc"
+                    and src.dtype == _abi.DT_I8 and adds):
+                fused_side[last] = (src, c)
+                sides.remove((first, last, members))
         out_dt = lay.acc_dtype if tail else node_dt
         conv_dst = self.tail_buf.data_ptr() if tail else y.data_ptr()
         side_dst = {}
         for first, last, members in sides:
             # the operand's dtype is the conv output's (epilogue operands)
-            self._elem_step(members, self.tensors[first], self.side_buf.data_ptr(), out_dt, count)
-            side_dst[last] = DevTensor(self.side_buf, list(n.out_type.shape), out_dt, "nhwc")
-        epi = _abi.Epilogue()
+            self._elem_step(members, self.tensors[first], self.side_buf.data_ptr(), lay.acc_dtype,
+                            count)
+            side_dst[last] = DevTensor(self.side_buf, list(n.out_type.shape), lay.acc_dtype, "nhwc")
         for i, (op, other, m) in enumerate(items):
             epi.ops[i] = _EPI[op]
             if op == "relu":
@@ -468,15 +503,24 @@ class DeviceGraph:
                 if other not in self.param_names:
                     raise TecError(E_LOWERING, "bias must be a graph input parameter")
                 epi.bias = self._bias_ptr(other)
+            elif other in fused_side:
+                r, c = fused_side[other]
+                epi.residual = r.ptr()
+                epi.residual_i8 = 1
+                epi.residual_scale = c
             else:
                 r = side_dst.get(other) or self.tensors[other]
-                if r.layout != "nhwc" or r.dtype != out_dt:
+                want_dt = lay.acc_dtype if self.compute == "i8" else out_dt
+                if r.layout != "nhwc" or r.dtype != want_dt:
                     raise TecError(E_LOWERING, f"'{op}' operand must be an NHWC {out_dt} tensor")
                 if op == "add":
                     epi.residual = r.ptr()
                 else:
                     epi.mul_operand = r.ptr()
         epi.n_ops = len(items)
+        if fuse_tail:
+            epi.ops[epi.n_ops] = _abi.EPI_REQUANTIZE
+            epi.n_ops += 1
         kn = _abi.Knobs(**self.knobs.get(n.id, {}))
         self.steps.append(_abi.Step(kind=_abi.STEP_DEPTHWISE if d.depthwise else _abi.STEP_CONV,
                                     dst_dtype=out_dt, conv=d, epi=epi, knobs=kn, src=xptr,

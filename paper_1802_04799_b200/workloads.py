@@ -87,12 +87,13 @@ def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
     the block's second conv fuses [conv2d, bias_add, add, relu].
 
     dtype "i8" (SURVEY 8f.4, int8 end to end; body only, head=False): i8
-    image and weights, i32 biases; every relu'd conv ends in requantize
-    (i32 -> i8, multiplier / 2^16 ~ 1 / (4 sqrt(K)), about the accumulator's
-    spread for the synthetic operands of int8_resnet18_params), so
-    activations between layers are i8; an identity shortcut enters the
-    i32 accumulator domain as scale(cast(y, i32), round(4.6 sqrt(K))); the
-    downsample branch is [conv2d, bias_add] in i32."""
+    image and weights, i32 biases; every conv ends in requantize (i32 ->
+    i8, multiplier / 2^16 ~ 1 / (4 sqrt(K)) -- 5.5 sqrt(K) with a shortcut or
+    without relu --, about the accumulator's spread
+    for the synthetic operands of int8_resnet18_params), so every
+    activation between layers is i8 -- the downsample branch too; a
+    shortcut enters the block's i32 accumulator domain as
+    scale(cast(y, i32), round(4.6 sqrt(K)))."""
     from .graph import ComputeGraph, GraphNode, TensorType
 
     if dtype not in ("f32", "i8"):
@@ -114,7 +115,7 @@ def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
         nodes.append(GraphNode(f"{name}_bias", "bias_add", [name, b]))
         y = f"{name}_bias"
         if shortcut is not None:
-            if i8 and shortcut[1]:  # identity shortcut: i8 -> accumulator domain
+            if i8:  # i8 shortcut (identity, or the requantized downsample) -> accumulator domain
                 nodes.append(GraphNode(f"{name}_sc", "cast", [shortcut[0]], {"dtype": "i32"}))
                 nodes.append(GraphNode(f"{name}_scs", "scale", [f"{name}_sc"],
                                        {"scale": float(round(4.6 * np.sqrt(cin * k * k)))}))
@@ -125,11 +126,13 @@ def resnet18_graph(batch: int, num_classes: int = 1000, image: int = 224,
         if relu:
             nodes.append(GraphNode(f"{name}_relu", "relu", [y]))
             y = f"{name}_relu"
-            if i8:
-                mult = max(1, int(round(65536.0 / (4.0 * np.sqrt(cin * k * k)))))
-                nodes.append(GraphNode(f"{name}_q", "requantize", [y],
-                                       {"multiplier": mult, "shift": 16}))
-                y = f"{name}_q"
+        if i8:
+            # wider accumulator spread with a shortcut added / without relu
+            spread = 4.0 if relu and shortcut is None else 5.5
+            mult = max(1, int(round(65536.0 / (spread * np.sqrt(cin * k * k)))))
+            nodes.append(GraphNode(f"{name}_q", "requantize", [y],
+                                   {"multiplier": mult, "shift": 16}))
+            y = f"{name}_q"
         return y
 
     x = inp("x", (batch, 3, image, image))

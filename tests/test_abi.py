@@ -106,7 +106,8 @@ def test_struct_layouts_match_header(tmp_path):
         pytest.skip("no host C compiler")
     checks = {
         "tec_conv_desc": (_abi.ConvDesc, []),
-        "tec_epilogue": (_abi.Epilogue, ["bias", "mul_operand"]),
+        "tec_epilogue": (_abi.Epilogue, ["bias", "mul_operand", "rq_mult", "rq_shift",
+                                         "residual_i8", "residual_scale"]),
         "tec_knobs": (_abi.Knobs, ["grid"]),
         "tec_pool_desc": (_abi.PoolDesc, ["out_dtype"]),
         "tec_kernel_plan": (_abi.KernelPlan, ["tma_store", "workspace_bytes"]),

@@ -35,18 +35,17 @@ def test_int8_graph_fuses_one_node_per_conv():
     kinds = {tuple(m.op for m in n.members) for n in convs}
     assert kinds == {
         ("conv2d", "bias_add", "relu", "requantize"),
-        ("conv2d", "bias_add", "cast", "scale", "add", "relu", "requantize"),  # identity shortcut
-        ("conv2d", "bias_add", "add", "relu", "requantize"),                  # downsample shortcut
-        ("conv2d", "bias_add"),                                               # the downsample itself
+        ("conv2d", "bias_add", "cast", "scale", "add", "relu", "requantize"),  # block with shortcut
+        ("conv2d", "bias_add", "requantize"),                                 # the downsample
     }
     for n in convs:
         root, head, sides, tail = split_conv_members(n)
         assert root.op == "conv2d"
-        assert [m.op for m in tail] in ([], ["requantize"])
+        assert [m.op for m in tail] == ["requantize"]
         assert all(m.op in ("bias_add", "add", "relu") for m in head)
         for first, last, members in sides:
             assert [m.op for m in members] == ["cast", "scale"] and first not in {m.id for m in n.members}
-        assert n.out_type.dtype == ("i32" if not tail else "i8")
+        assert n.out_type.dtype == "i8"
 
 
 def test_int8_graph_rejects_head_and_bad_ops():
@@ -192,6 +191,74 @@ def test_int8_resnet18_bit_exact(width, image, batch):
     again = dg.run(feeds)
     for o in g.outputs:
         assert np.array_equal(again[o], out[o])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,shortcut", [(24, False), (48, True), (64, True)])
+def test_int8_block_fused_and_unfused_lowerings(k, shortcut):
+    """One conv block in both lowerings: K = 24 keeps requantize (and the
+    shortcut) as elementwise launches; K = 48 folds requantize into the
+    epilogue with the shortcut as an i32 operand (the generic epilogue);
+    K = 64 folds both (the Q programs). All bit-exact vs the oracle."""
+    from paper_1802_04799_b200.executor import DeviceGraph
+    rng = np.random.default_rng(k)
+    # a 1x1 conv first, so the block input (and its shortcut) is an NHWC
+    # activation rather than the NCHW graph input
+    nodes = [GraphNode("x0", "input", out_type=TensorType([2, k, 12, 12], "i8")),
+             GraphNode("w0", "input", out_type=TensorType([k, k, 1, 1], "i8")),
+             GraphNode("c0", "conv2d", ["x0", "w0"]),
+             GraphNode("x", "requantize", ["c0"], {"multiplier": 3, "shift": 4}),
+             GraphNode("w", "input", out_type=TensorType([k, k, 3, 3], "i8")),
+             GraphNode("b", "input", out_type=TensorType([k], "i32")),
+             GraphNode("c", "conv2d", ["x", "w"], {"padding": [1, 1]}),
+             GraphNode("cb", "bias_add", ["c", "b"])]
+    y = "cb"
+    if shortcut:
+        nodes += [GraphNode("sc", "cast", ["x"], {"dtype": "i32"}),
+                  GraphNode("ss", "scale", ["sc"], {"scale": 37.0}),
+                  GraphNode("a", "add", [y, "ss"])]
+        y = "a"
+    nodes += [GraphNode("r", "relu", [y]),
+              GraphNode("q", "requantize", ["r"], {"multiplier": 911, "shift": 16})]
+    g = ComputeGraph(nodes, ["q"])
+    g.validate()
+    feeds = {"x0": rng.integers(-60, 61, (2, k, 12, 12), dtype=np.int8)}
+    params = {"w0": rng.integers(-8, 9, (k, k, 1, 1), dtype=np.int8),
+              "w": rng.integers(-8, 9, (k, k, 3, 3), dtype=np.int8),
+              "b": rng.integers(-500, 501, (k,), dtype=np.int32)}
+    dg = DeviceGraph(g, compute="i8")
+    dg.bind_params(params)
+    got = dg.run(feeds)["q"]
+    want = graph_oracle.evaluate(fuse_pass(g), feeds, params, "i8")["q"]
+    assert np.array_equal(got, want)
+    assert 0 < (got == 0).mean() < 1 and (got > 0).any()
+    n_elem = sum(1 for s in dg.steps if s.kind == _abi.STEP_ELEMWISE)
+    # K = 24: both requantizes and the shortcut unfused; 48: the shortcut
+    # (K % 32 != 0); 64: none
+    assert n_elem == {24: 2 + shortcut, 48: 1, 64: 0}[k]
+
+
+@pytest.mark.gpu
+def test_max_pool2d_i8_kernel():
+    """tec_max_pool2d on i8 NHWC (the int8 stem pool, SIMD byte max):
+    all-negative values, so a padded tap winning would show as 0."""
+    import torch
+    from oracle.oracle_api import max_pool2d
+    lib = _abi.load()
+    rng = np.random.default_rng(9)
+    n, c, h, w = 3, 48, 17, 23
+    x = rng.integers(-128, 0, (n, c, h, w), dtype=np.int8)
+    x[0, :, 0, 0] = -128
+    want = max_pool2d(x).astype(np.int8)
+    xd = torch.from_numpy(np.ascontiguousarray(x.transpose(0, 2, 3, 1))).to(_dev())
+    oh, ow = want.shape[2], want.shape[3]
+    yd = torch.empty((n, oh, ow, c), dtype=torch.int8, device=_dev())
+    pd = _abi.PoolDesc(n=n, c=c, h=h, w=w, r=3, s=3, stride_h=2, stride_w=2, pad_h=1, pad_w=1,
+                       dtype=_abi.DT_I8, out_dtype=_abi.DT_I8)
+    _abi.check(lib.tec_max_pool2d(C.byref(pd), xd.data_ptr(), yd.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream))
+    got = yd.cpu().numpy().transpose(0, 3, 1, 2)
+    assert np.array_equal(got, want)
 
 
 @pytest.mark.gpu
