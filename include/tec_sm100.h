@@ -177,6 +177,12 @@ tec_status tec_activation_pack(const tec_conv_desc* d, const void* x_nchw,
 /* OIHW f32 (or i8) -> packed weights (KRSC, or [R][S][C] for depthwise). */
 tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
                                    void* w_packed, void* stream);
+/* tec_weight_pretransform with batch-norm folding (SURVEY 8f.4,
+ * graph.py fold_batch_norm): packs w[k][c][r][s] * scale[k] (each product
+ * rounded to f32 once -- graph.py bn_fold_weight), scale = the device f32
+ * vector gamma / sqrt(var + eps). F32 / F32TC / BF16 weights (not I8). */
+tec_status tec_weight_pretransform_bn(const tec_conv_desc* d, const void* w_oihw,
+                                      const float* scale, void* w_packed, void* stream);
 /* f32 NHWC [n*h*w][c] (an f32tc layer's output) -> the packed input of an
  * f32tc dense conv (its three exact bf16 planes), without the NCHW detour. */
 tec_status tec_activation_pack_nhwc(const tec_conv_desc* d, const void* x_nhwc_f32,

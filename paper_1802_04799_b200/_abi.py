@@ -155,6 +155,7 @@ SIGNATURES = {
     "tec_plan_size": (C.c_int32, [_P]),
     "tec_plan_status": (C.c_int32, [_P, _P]),
     "tec_elementwise": (C.c_int32, [C.POINTER(ElemProg), _P, _P, _P, _P]),
+    "tec_weight_pretransform_bn": (C.c_int32, [_DESC, _P, _P, _P, _P]),
     "tec_plan_destroy": (None, [_P]),
 }
 

@@ -132,6 +132,24 @@ int launch_t(const ElemProg& p, const void* x, void* y, int32_t* err, int sms,
 
 }  // namespace
 
+// Batch-norm weight fold (tec_weight_pretransform_bn): y = x * s[i / per_row],
+// one f32 product per element (__fmul_rn: graph.py bn_fold_weight).
+__global__ void scale_rows_kernel(const float* __restrict__ x, const float* __restrict__ s,
+                                  float* __restrict__ y, int64_t count, int64_t per_row) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = __fmul_rn(x[i], s[i / per_row]);
+}
+
+int launch_scale_rows(const float* x, const float* s, float* y, int64_t count, int64_t per_row,
+                      int sms, cudaStream_t st) {
+  if (count <= 0) return 0;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > int64_t(sms) * 8) blocks = int64_t(sms) * 8;
+  scale_rows_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(x, s, y, count, per_row);
+  return static_cast<int>(cudaGetLastError());
+}
+
 // x / y must be 16-byte aligned (device allocations and 256-B arena slots
 // are). Supported (in, out): (i8, i32), (i8, i8), (i32, i8), (i32, i32),
 // (i8, f32), (i32, f32), (f32, f32); the host validates the program.

@@ -66,6 +66,8 @@ int launch_pool_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwT
 int launch_global_avg_pool(const PoolParams& p, cudaStream_t st);
 int launch_elementwise(const ElemProg& p, const void* x, void* y, int32_t* err, int sms,
                        cudaStream_t st);
+int launch_scale_rows(const float* x, const float* s, float* y, int64_t count, int64_t per_row,
+                      int sms, cudaStream_t st);
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int bn, int swz, bool inter, bool res, bool halo,
                       int prog, int grid, cudaStream_t st);
@@ -1431,6 +1433,35 @@ tec_status tec_weight_pretransform(const tec_conv_desc* d, const void* w_oihw,
                                     pl.cp, d->depthwise, pl.pack_mode, (cudaStream_t)stream);
   if (e) return cuda_fail(e, "pack_weights");
   return TEC_OK;
+}
+
+tec_status tec_weight_pretransform_bn(const tec_conv_desc* d, const void* w_oihw,
+                                      const float* scale, void* w_packed, void* stream) {
+  if (!d || !w_oihw || !scale || !w_packed) return fail(TEC_E_INTERNAL, "null argument");
+  if (d->compute == TEC_COMPUTE_I8)
+    return fail(TEC_E_LOWERING, "batch-norm folding applies to float weights");
+  Plan pl{};
+  tec_status st = make_plan(d, &pl);
+  if (st) return st;
+  const int64_t rows = d->k;
+  const int64_t per_row = (d->depthwise ? 1 : d->c) * d->r * d->s;
+  cudaStream_t s = (cudaStream_t)stream;
+  // parameter binding time, not the execution path: a stream-ordered
+  // temporary for the folded OIHW weights
+  void* tmp = nullptr;
+  TEC_CUDA(cudaMallocAsync(&tmp, rows * per_row * sizeof(float), s));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int e = launch_scale_rows(static_cast<const float*>(w_oihw), scale,
+                                  static_cast<float*>(tmp), rows * per_row, per_row,
+                                  sm_count(dev), s);
+  if (e) {
+    cudaFreeAsync(tmp, s);
+    return cuda_fail(e, "bn weight fold");
+  }
+  st = tec_weight_pretransform(d, tmp, w_packed, stream);
+  cudaFreeAsync(tmp, s);
+  return st;
 }
 
 tec_status tec_activation_pack_nhwc(const tec_conv_desc* d, const void* x_nhwc_f32,

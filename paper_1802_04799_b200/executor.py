@@ -51,7 +51,8 @@ import torch
 
 from . import _abi
 from ._abi import TecError
-from .graph import ComputeGraph, GraphNode, check_memory_plan, fuse_pass, plan_memory
+from .graph import (ComputeGraph, GraphNode, bn_eval, bn_scale, check_memory_plan,
+                    fold_batch_norm, fuse_pass, nhwc_layout_pass, plan_memory)
 
 E_LOWERING, E_IO, E_SHAPE = 15, 20, 2
 _EPI = {"scale": _abi.EPI_SCALE, "bias_add": _abi.EPI_BIAS, "add": _abi.EPI_ADD,
@@ -59,6 +60,7 @@ _EPI = {"scale": _abi.EPI_SCALE, "bias_add": _abi.EPI_BIAS, "add": _abi.EPI_ADD,
 _ELEM = {"cast": _abi.ELEM_CAST, "scale": _abi.ELEM_SCALE, "relu": _abi.ELEM_RELU,
          "requantize": _abi.ELEM_REQUANTIZE}
 _DT = {"f32": _abi.DT_F32, "i32": _abi.DT_I32, "i8": _abi.DT_I8}
+_BN_FOLD = ("bn_fold_weight", "bn_fold_bias")
 _TORCH = {_abi.DT_F32: torch.float32, _abi.DT_BF16: torch.bfloat16,
           _abi.DT_I32: torch.int32, _abi.DT_I8: torch.int8}
 _BYTES = {_abi.DT_F32: 4, _abi.DT_BF16: 2, _abi.DT_I32: 4, _abi.DT_I8: 1}
@@ -85,16 +87,40 @@ class DevTensor:
 
 
 def _resolve_aliases(g: ComputeGraph) -> ComputeGraph:
-    """The executor's view of a fused graph: nodes that only re-view a
-    buffer are removed and their consumers read the underlying tensor, so
-    plan_memory sees the true lifetimes.
+    """The executor's view of a fused, layout-annotated graph: nodes that
+    only re-view a buffer are removed and their consumers read the
+    underlying tensor, so plan_memory sees the true lifetimes.
+      * layout_transform row_major <-> nhwc (nhwc_layout_pass): realised by
+        the consuming launch (see DevTensor.layout);
       * flatten of an [N, C, 1, 1] tensor: same bytes in NHWC;
       * sum(axis=3) -> sum(axis=2) -> scale(1/(H*W)), each with a single
         consumer: one global_avg_pool node (the reference composition).
     The result is internal (node types are kept, not re-validated)."""
     import copy
-    cons = g.consumers()
     outs = set(g.outputs)
+    # an output's final NHWC -> row-major transform: the producer itself
+    # takes the output id (outputs own their buffers; the unpack happens in
+    # output())
+    ren: Dict[str, str] = {}
+    kinds = {n.id: n.op for n in g.nodes}
+    for n in g.nodes:
+        if (n.id in outs and n.op == "layout_transform" and
+                {n.attrs.get("src_layout"), n.attrs.get("dst_layout")} == {"row_major", "nhwc"}
+                and kinds[n.inputs[0]] not in ("input", "const") and n.inputs[0] not in outs):
+            ren[n.inputs[0]] = n.id
+    if ren:
+        g2 = ComputeGraph([], list(g.outputs))
+        for n in g.nodes:
+            if n.id in outs and n.op == "layout_transform" and n.inputs[0] in ren:
+                continue
+            m = copy.deepcopy(n)
+            m.id = ren.get(m.id, m.id)
+            m.inputs = [ren.get(i, i) for i in m.inputs]
+            for mm in m.members:
+                mm.inputs = [ren.get(i, i) for i in mm.inputs]
+            g2.nodes.append(m)
+        g = g2
+    cons = g.consumers()
     alias: Dict[str, str] = {}
     gap_of: Dict[str, str] = {}   # scale node id -> pooled input id
     dropped = set()
@@ -116,6 +142,14 @@ def _resolve_aliases(g: ComputeGraph) -> ComputeGraph:
         dropped |= {a.id, b.id}
     shapes = {n.id: n.out_type.shape for n in g.nodes}
     for n in g.nodes:
+        if (n.op == "layout_transform" and n.id not in outs and
+                {n.attrs.get("src_layout"), n.attrs.get("dst_layout")} == {"row_major", "nhwc"}):
+            # realised by the consumer (a conv's input pack reads NCHW, the
+            # pools convert on demand) or a no-op: DevTensor tracks the
+            # physical layout
+            alias[n.id] = alias.get(n.inputs[0], n.inputs[0])
+            dropped.add(n.id)
+            continue
         if n.op == "flatten" and n.id not in outs:
             src = n.inputs[0]
             sh = shapes[src]
@@ -214,8 +248,12 @@ class DeviceGraph:
         self.act_dt = {"bf16": _abi.DT_BF16, "i8": _abi.DT_I8}.get(compute, _abi.DT_F32)
         self.in_dtype = "i8" if compute == "i8" else "f32"  # graph input / weight dtype
         self.knobs = knobs or {}
-        self.fused = fuse_pass(g)
-        self.g = _resolve_aliases(self.fused)
+        # BN folded into conv weights / biases (parameters, bind time), then
+        # the reference's fusion
+        self.fused = fuse_pass(fold_batch_norm(g))
+        # the B200 layout pass: NHWC placement made explicit in the graph
+        self.laid = nhwc_layout_pass(self.fused)
+        self.g = _resolve_aliases(self.laid)
         self.outputs = list(self.g.outputs)
         self._classify_inputs()
         self.steps: List[_abi.Step] = []
@@ -257,15 +295,20 @@ class DeviceGraph:
                         role = "weight"
                     elif m.op == "bias_add" and pos == 1:
                         role = "bias"
+                    elif m.op in _BN_FOLD:
+                        role = "param"  # folded into a weight / bias at bind time
                     uses.setdefault(i, set()).add(role)
         self.param_names, self.feed_names = [], []
+        cons = self.g.consumers()
         for n in self.g.nodes:
             if n.op == "const":
+                if cons.get(n.id) and all(self.g.node(c).op == "bn_fold_bias" for c in cons[n.id]):
+                    continue  # fold_batch_norm's zero bias
                 raise TecError(E_LOWERING, "const nodes: bind them as parameters (inputs)")
             if n.op != "input":
                 continue
             u = uses.get(n.id, set())
-            if u and u <= {"weight"} or u == {"bias"}:
+            if u and (u <= {"weight", "param"} or u <= {"bias", "param"}):
                 self.param_names.append(n.id)
             else:
                 self.feed_names.append(n.id)
@@ -333,6 +376,12 @@ class DeviceGraph:
                 self._compile_avgpool(n, self.tensors[n.inputs[0]])
             elif n.op in _ELEM or (n.op == "fused" and n.members[0].op in _ELEM):
                 self._compile_elemwise(n)
+            elif n.op in _BN_FOLD or n.op == "const":
+                continue  # parameter derivations: computed in bind_params (see _bind_weight)
+            elif n.op == "layout_transform":
+                # an output's final NHWC -> NCHW transform: output() unpacks
+                # on read (tec_output_unpack)
+                self.tensors[n.id] = self.tensors[n.inputs[0]]
             else:
                 raise TecError(E_LOWERING, f"no sm100 lowering for node '{n.id}' ({n.op})")
         for o in self.outputs:
@@ -435,7 +484,12 @@ class DeviceGraph:
         root, items, sides, tail = self._conv_members(n)
         x = self.tensors[root.inputs[0]]
         wname = root.inputs[1]
-        if wname not in self.param_names:
+        bn = None
+        wnode = self.g.node(wname)
+        if wnode.op == "bn_fold_weight":  # fold_batch_norm: W * gamma / sqrt(var + eps)
+            bn = wnode
+            wname = wnode.inputs[0]
+        if wname not in self.param_names or (bn and not all(i in self.param_names for i in bn.inputs)):
             raise TecError(E_LOWERING, f"conv weight '{wname}' must be a graph input parameter")
         wt = self.g.node(wname).out_type
         if root.op == "matmul":
@@ -453,7 +507,7 @@ class DeviceGraph:
         lay = _abi.ConvLayout()
         _abi.check(self.lib.tec_conv_layout_of(C.byref(d), C.byref(lay)))
         wpk = self._scratch(lay.wt_bytes)
-        self._bind_weight(wname, d, wpk, transpose=root.op == "matmul")
+        self._bind_weight(wname, d, wpk, transpose=root.op == "matmul", bn=bn)
         node_dt = self._node_dtype(n)
         oh, ow = (lay.oh, lay.ow)
         count = d.n * d.k * oh * ow
@@ -500,7 +554,7 @@ class DeviceGraph:
             if op == "scale":
                 epi.scale[i] = float(m.attrs.get("scale", 1.0))
             elif op == "bias_add":
-                if other not in self.param_names:
+                if other not in self.param_names and self.g.node(other).op != "bn_fold_bias":
                     raise TecError(E_LOWERING, "bias must be a graph input parameter")
                 epi.bias = self._bias_ptr(other)
             elif other in fused_side:
@@ -521,7 +575,7 @@ class DeviceGraph:
         if fuse_tail:
             epi.ops[epi.n_ops] = _abi.EPI_REQUANTIZE
             epi.n_ops += 1
-        kn = _abi.Knobs(**self.knobs.get(n.id, {}))
+        kn = _abi.Knobs(**self.knobs.get(n.id, self.knobs.get(n.id.split("#")[0], {})))
         self.steps.append(_abi.Step(kind=_abi.STEP_DEPTHWISE if d.depthwise else _abi.STEP_CONV,
                                     dst_dtype=out_dt, conv=d, epi=epi, knobs=kn, src=xptr,
                                     w=wpk.data_ptr(), dst=conv_dst))
@@ -531,7 +585,8 @@ class DeviceGraph:
             self._elem_step(tail, acc, y.data_ptr(), node_dt, count)
         self.tensors[n.id] = DevTensor(y, shape, node_dt, "nhwc")
 
-    def _bind_weight(self, name: str, d: _abi.ConvDesc, wpk: torch.Tensor, transpose: bool):
+    def _bind_weight(self, name: str, d: _abi.ConvDesc, wpk: torch.Tensor, transpose: bool,
+                     bn: Optional[GraphNode] = None):
         src_shape = self.g.node(name).out_type.shape
 
         npdt = np.int8 if self.compute == "i8" else np.float32
@@ -543,19 +598,36 @@ class DeviceGraph:
             if transpose:  # matmul [K, N] -> OIHW [N, K, 1, 1]
                 w = np.ascontiguousarray(w.T).reshape(w.shape[1], w.shape[0], 1, 1)
             wd = torch.from_numpy(np.ascontiguousarray(w)).to(self.dev)
-            _abi.check(self.lib.tec_weight_pretransform(C.byref(d), wd.data_ptr(),
-                                                        wpk.data_ptr(), st))
+            if bn is not None:
+                # BN folded inside the pretransform: the per-channel factor
+                # gamma / sqrt(var + eps) (K values, host), the products on device
+                _, g_, v_ = bn.inputs
+                sc = bn_scale(params[g_], params[v_], float(bn.attrs.get("eps", 1e-5)))
+                sd = torch.from_numpy(sc).to(self.dev)
+                _abi.check(self.lib.tec_weight_pretransform_bn(C.byref(d), wd.data_ptr(),
+                                                               sd.data_ptr(), wpk.data_ptr(), st))
+            else:
+                _abi.check(self.lib.tec_weight_pretransform(C.byref(d), wd.data_ptr(),
+                                                            wpk.data_ptr(), st))
             torch.cuda.current_stream(self.dev).synchronize()
         self.param_prep.append(prep)
 
     def _bias_ptr(self, name: str) -> int:
         if name not in self.params:
-            k = self.g.node(name).out_type.shape[0]
+            node = self.g.node(name)
+            k = node.out_type.shape[0]
             integer = self.compute == "i8"
             self.params[name] = torch.empty(k, dtype=torch.int32 if integer else torch.float32,
                                             device=self.dev)
+            if node.op == "bn_fold_bias":  # (b - mean) * s + beta, K values on the host
+                for i in node.inputs:
+                    if i not in self.param_names and self.g.node(i).op != "const":
+                        raise TecError(E_LOWERING, f"bn_fold_bias operand '{i}' is not a parameter")
 
             def prep(params, st, name=name, npdt=np.int32 if integer else np.float32):
+                if node.op == "bn_fold_bias":
+                    vals = [params[i] if i in params else self.g.node(i).data for i in node.inputs]
+                    params = {name: bn_eval("bn_fold_bias", vals, float(node.attrs.get("eps", 1e-5)))}
                 b = np.asarray(params[name], dtype=npdt)
                 if b.shape != tuple(self.params[name].shape):
                     raise TecError(E_SHAPE, f"parameter '{name}' has shape {b.shape}")

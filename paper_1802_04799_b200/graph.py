@@ -213,6 +213,13 @@ def _layout_transform(ins, attrs):
         if x.rank() != 4 or h <= 0 or w <= 0:
             _fail(E_SHAPE, "tiled4x4 -> row_major needs a rank-4 source and height/width")
         return TensorType([h, w], x.dtype)
+    if {src, dst} == {"row_major", "nhwc"}:
+        # a physical relayout of a rank-4 activation (NCHW <-> NHWC); the
+        # type keeps the LOGICAL NCHW shape (logical shapes are
+        # NCHW, kernels run NHWC)
+        if x.rank() != 4:
+            _fail(E_SHAPE, "nhwc layout applies to rank-4 tensors")
+        return copy.deepcopy(x)
     if src == dst:
         return copy.deepcopy(x)
     _fail(E_SHAPE, f"unsupported layout pair {src} -> {dst}")
@@ -241,6 +248,24 @@ def _requantize(ins, attrs):
     return TensorType(list(ins[0].shape), "i8")
 
 
+def _per_channel(name, n_vec, data_first=True):
+    """Ops over a rank-4 x (NCHW, channel axis 1) and n_vec [C] vectors."""
+    def f(ins, attrs):
+        x = ins[0]
+        if x.rank() != 4 and data_first:
+            _fail(E_SHAPE, f"{name} wants NCHW data")
+        c = x.shape[0] if not data_first else x.shape[1]
+        for v in ins[1:1 + n_vec]:
+            if v.rank() != 1 or v.shape[0] != c or v.dtype != "f32":
+                _fail(E_SHAPE, f"{name}: per-channel operands must be f32 [{c}]")
+        if x.dtype != "f32":
+            _fail(E_SHAPE, f"{name} wants f32 data")
+        if float(attrs.get("eps", 1e-5)) < 0:
+            _fail(E_SHAPE, f"{name}: eps must be >= 0")
+        return copy.deepcopy(x)
+    return f
+
+
 # name -> (pattern, arity, infer)
 OPS: Dict[str, Tuple[str, int, Callable]] = {
     "add": (INJECTIVE, 2, _same_binary("add")),
@@ -263,6 +288,15 @@ OPS: Dict[str, Tuple[str, int, Callable]] = {
     # int8 graph ops (not in the reference registry)
     "cast": (INJECTIVE, 1, _cast),
     "requantize": (INJECTIVE, 1, _requantize),
+    # inference batch norm and its folded form (fold_batch_norm; not in the
+    # reference registry): s = gamma / sqrt(var + eps) per channel, every
+    # operation rounded to f32 separately (no FMA)
+    #   batch_norm(x, gamma, beta, mean, var) = (x - mean) * s + beta
+    #   bn_fold_weight(w[K,C,R,S], gamma, var) = w * s[k]
+    #   bn_fold_bias(b, gamma, beta, mean, var) = (b - mean) * s + beta
+    "batch_norm": (INJECTIVE, 5, _per_channel("batch_norm", 4)),
+    "bn_fold_weight": (INJECTIVE, 3, _per_channel("bn_fold_weight", 2, data_first=False)),
+    "bn_fold_bias": (INJECTIVE, 5, _per_channel("bn_fold_bias", 4, data_first=False)),
 }
 
 
@@ -612,6 +646,27 @@ def _libm_expf(x: np.ndarray) -> np.ndarray:
     return np.array([lib.expf(float(v)) for v in flat], dtype=np.float32).reshape(x.shape)
 
 
+def bn_scale(gamma: np.ndarray, var: np.ndarray, eps: float) -> np.ndarray:
+    """s = gamma / sqrt(var + eps), each step rounded to f32."""
+    g, v = np.asarray(gamma, np.float32), np.asarray(var, np.float32)
+    return (g / np.sqrt(v + np.float32(eps))).astype(np.float32)
+
+
+def bn_eval(op: str, ins: List[np.ndarray], eps: float) -> np.ndarray:
+    """The batch-norm ops' f32 semantics (see OPS)."""
+    if op == "bn_fold_weight":
+        w, g, v = ins
+        s = bn_scale(g, v, eps)
+        return (np.asarray(w, np.float32) * s.reshape(-1, *([1] * (w.ndim - 1)))).astype(np.float32)
+    x, g, b, m, v = ins
+    s = bn_scale(g, v, eps)
+    shp = (1, -1, 1, 1) if op == "batch_norm" else (-1,)
+    x = np.asarray(x, np.float32)
+    y = (x - np.asarray(m, np.float32).reshape(shp)).astype(np.float32)
+    y = (y * s.reshape(shp)).astype(np.float32)
+    return (y + np.asarray(b, np.float32).reshape(shp)).astype(np.float32)
+
+
 def _fold_eval(n: GraphNode, ins: List[np.ndarray]) -> np.ndarray:
     """Compile-time evaluation of one node whose inputs are all constants.
     Elementwise / reduction / layout ops follow the reference's host
@@ -629,6 +684,8 @@ def _fold_eval(n: GraphNode, ins: List[np.ndarray]) -> np.ndarray:
     if op == "relu":
         x = ins[0]
         return np.where(x < 0, np.zeros_like(x), x)
+    if op in ("batch_norm", "bn_fold_weight", "bn_fold_bias"):
+        return bn_eval(op, ins, float(n.attrs.get("eps", 1e-5)))
     if op == "cast":
         return ins[0].astype({"i8": np.int8, "i32": np.int32, "f32": np.float32}[n.attrs.get("dtype", "i32")])
     if op == "requantize":
@@ -742,27 +799,46 @@ def fold_constants(g: ComputeGraph) -> ComputeGraph:
 _LAYOUT_ELEMWISE = ("add", "mul", "exp", "sqrt", "relu", "scale")
 
 
+# Ops that run on NHWC activations on the device (the "nhwc" preference):
+# the conv / pool kernels and the per-element ops around them.
+_NHWC_OPS = ("conv2d", "depthwise_conv2d", "max_pool2d", "global_avg_pool", "bias_add", "add",
+             "mul", "relu", "scale", "cast", "requantize", "fused")
+_SUFFIX = {"tiled4x4": "#t", "nhwc": "#h"}
+
+
 def apply_layouts(g: ComputeGraph, prefs: Dict[str, str]) -> ComputeGraph:
-    """graph_passes.cpp:84-178: realise per-node layout preferences
-    ("row_major" | "tiled4x4") by inserting layout_transform nodes; graph
-    outputs stay row-major by contract."""
+    """graph_passes.cpp:84-178: realise per-node layout preferences by
+    inserting layout_transform nodes; graph outputs stay row-major by
+    contract. Preferences: "row_major", "tiled4x4" (the reference's: rank-2
+    elementwise ops) and "nhwc" (the B200 pass, see nhwc_layout_pass:
+    rank-4 device ops). A node with a non-row-major preference runs as
+    "<id>#t" / "<id>#h"; a transform of producer X into a layout is
+    "X#t" / "X#h", back to row-major "X#r"; an output's final transform
+    takes over the output's id."""
     for nid, pf in prefs.items():
-        if pf not in ("row_major", "tiled4x4"):
+        if pf not in ("row_major", "tiled4x4", "nhwc"):
             _fail(E_SHAPE, f"unknown layout preference '{pf}'")
         if pf == "row_major":
             continue
         n = g.node(nid)
-        if n.op not in _LAYOUT_ELEMWISE:
-            _fail(E_SHAPE, f"tiled4x4 preference on '{nid}' ({n.op}): only elementwise ops can carry it")
-        if n.out_type.rank() != 2:
-            _fail(E_SHAPE, f"tiled4x4 preference on '{nid}' needs a rank-2 tensor")
+        if pf == "tiled4x4":
+            if n.op not in _LAYOUT_ELEMWISE:
+                _fail(E_SHAPE, f"tiled4x4 preference on '{nid}' ({n.op}): only elementwise ops can carry it")
+            if n.out_type.rank() != 2:
+                _fail(E_SHAPE, f"tiled4x4 preference on '{nid}' needs a rank-2 tensor")
+        else:
+            if n.op not in _NHWC_OPS:
+                _fail(E_SHAPE, f"nhwc preference on '{nid}' ({n.op}): not a device NHWC op")
+            if n.out_type.rank() != 4:
+                _fail(E_SHAPE, f"nhwc preference on '{nid}' needs a rank-4 tensor")
     pref_of = lambda i: prefs.get(i, "row_major")  # noqa: E731
     out = ComputeGraph([], list(g.outputs))
     rm_type = {n.id: n.out_type for n in g.nodes}
     realized: Dict[Tuple[str, str], str] = {}
+    made_in: Dict[str, str] = {}  # node id -> the layout it was computed in
     for n in g.nodes:
         pf = pref_of(n.id)
-        run_id = n.id + "#t" if pf == "tiled4x4" else n.id
+        run_id = n.id + _SUFFIX.get(pf, "")
         c = copy.deepcopy(n)
         c.id = run_id
         c.out_type = TensorType()
@@ -770,35 +846,134 @@ def apply_layouts(g: ComputeGraph, prefs: Dict[str, str]) -> ComputeGraph:
             c.out_type = copy.deepcopy(n.out_type)
             out.nodes.append(c)
             realized[(n.id, "row_major")] = n.id
+            made_in[n.id] = "row_major"
             continue
         new_inputs = []
-        for i in c.inputs:
-            key = (i, pf)
+        # weights (operand 1 of a conv, also inside a fused node) and
+        # per-channel vectors stay row-major: they are parameters, packed
+        # once by tec_weight_pretransform
+        weights = {m.inputs[1] for m in (n.members or [n])
+                   if m.op in ("conv2d", "depthwise_conv2d") and len(m.inputs) > 1}
+        for pos, i in enumerate(c.inputs):
+            want = pf if rm_type[i].rank() == 4 or pf == "tiled4x4" else "row_major"
+            if pf == "nhwc" and i in weights:
+                want = "row_major"
+            key = (i, want)
             if key in realized:
                 new_inputs.append(realized[key])
                 continue
             rt = rm_type[i]
-            if pf == "tiled4x4":
-                tr = GraphNode(i + "#t", "layout_transform", [realized[(i, "row_major")]],
-                               {"src_layout": "row_major", "dst_layout": "tiled4x4"})
+            src_l = made_in[i]
+            if want != "row_major":
+                tr = GraphNode(i + _SUFFIX[want], "layout_transform", [realized[(i, src_l)]],
+                               {"src_layout": "row_major", "dst_layout": want})
+                if (i, "row_major") not in realized:
+                    _fail(E_SHAPE, f"no row-major form of '{i}' to transform")
+                tr.inputs = [realized[(i, "row_major")]]
             else:
-                tr = GraphNode(i + "#r", "layout_transform", [realized[(i, "tiled4x4")]],
-                               {"src_layout": "tiled4x4", "dst_layout": "row_major",
-                                "height": rt.shape[0], "width": rt.shape[1]})
+                attrs = {"src_layout": src_l, "dst_layout": "row_major"}
+                if src_l == "tiled4x4":
+                    attrs.update({"height": rt.shape[0], "width": rt.shape[1]})
+                tr = GraphNode(i + "#r", "layout_transform", [realized[(i, src_l)]], attrs)
             realized[key] = tr.id
             new_inputs.append(tr.id)
             out.nodes.append(tr)
         c.inputs = new_inputs
+        if c.members:  # a fused node reads its operands by the outer ids
+            ren = dict(zip(n.inputs, new_inputs))
+            for m in c.members:
+                m.inputs = [ren.get(x, x) for x in m.inputs]
         out.nodes.append(c)
         realized[(n.id, pf)] = run_id
+        made_in[n.id] = pf
     for o in out.outputs:
         if (o, "row_major") in realized:
             continue
         rt = rm_type[o]
-        out.nodes.append(GraphNode(o, "layout_transform", [realized[(o, "tiled4x4")]],
-                                   {"src_layout": "tiled4x4", "dst_layout": "row_major",
-                                    "height": rt.shape[0], "width": rt.shape[1]}))
+        src_l = made_in[o]
+        attrs = {"src_layout": src_l, "dst_layout": "row_major"}
+        if src_l == "tiled4x4":
+            attrs.update({"height": rt.shape[0], "width": rt.shape[1]})
+        out.nodes.append(GraphNode(o, "layout_transform", [realized[(o, src_l)]], attrs))
         realized[(o, "row_major")] = o
     out = _strip_dead(out)
+    out.validate()
+    return out
+
+
+def nhwc_layout_pass(g: ComputeGraph) -> ComputeGraph:
+    """The B200 layout pass: every rank-4 device op runs NHWC
+    (apply_layouts with an "nhwc" preference on each), so layout_transform
+    nodes appear exactly where an activation crosses between the reference
+    NCHW layout and the kernels' NHWC one -- graph inputs feeding the
+    network, rank-4 graph outputs, and row-major consumers (the matmul
+    head). The executor realises each transform inside a neighbouring
+    launch (the conv's input pack, the output unpack) or as a no-op when
+    the two layouts coincide ([N, C, 1, 1])."""
+    prefs = {n.id: "nhwc" for n in g.nodes
+             if n.op in _NHWC_OPS and n.out_type.rank() == 4
+             and not (n.op == "fused" and n.members[0].op == "matmul")}
+    return apply_layouts(g, prefs)
+
+
+def fold_batch_norm(g: ComputeGraph) -> ComputeGraph:
+    """BN folding: conv2d(x, W) [-> bias_add(., B)] ->
+    batch_norm(., gamma, beta, mean, var) becomes
+    conv2d(x, bn_fold_weight(W, gamma, var)) -> bias_add(., bn_fold_bias(B,
+    gamma, beta, mean, var)) (B = zeros when there was no bias_add). The
+    fold nodes depend on parameters only: fold_constants evaluates them at
+    compile time when they are consts, and the device executor runs them
+    inside tec_weight_pretransform_bn when they are bound parameters."""
+    cons = g.consumers()
+    outs = set(g.outputs)
+    by_id = {n.id: n for n in g.nodes}
+    rewrite: Dict[str, Tuple[str, Optional[str]]] = {}  # bn id -> (conv id, bias_add id)
+    for n in g.nodes:
+        if n.op != "batch_norm":
+            continue
+        src = by_id[n.inputs[0]]
+        bias = None
+        if src.op == "bias_add" and len(cons.get(src.id, [])) == 1 and src.id not in outs:
+            bias, src = src, by_id[src.inputs[0]]
+        if src.op != "conv2d" or len(cons.get(src.id, [])) != 1 or src.id in outs:
+            continue
+        if by_id[src.inputs[1]].op not in ("input", "const"):
+            continue
+        rewrite[n.id] = (src.id, bias.id if bias else None)
+    if not rewrite:
+        return copy.deepcopy(g)
+    conv_of = {c: bn for bn, (c, _) in rewrite.items()}
+    bias_of = {b: bn for bn, (_, b) in rewrite.items() if b}
+    out = ComputeGraph([], list(g.outputs))
+    for bn_node in g.nodes:
+        # everything is emitted where the batch_norm was: its parameters
+        # and the conv's operands all precede it
+        if bn_node.id not in rewrite:
+            if bn_node.id not in conv_of and bn_node.id not in bias_of:
+                out.nodes.append(copy.deepcopy(bn_node))
+            continue
+        n = by_id[rewrite[bn_node.id][0]]
+        if True:
+            bn = bn_node
+            eps = {"eps": float(bn.attrs.get("eps", 1e-5))}
+            _, gm, bt, mu, vr = bn.inputs
+            wf = GraphNode(n.id + "#bnw", "bn_fold_weight", [n.inputs[1], gm, vr], dict(eps))
+            out.nodes.append(wf)
+            b_in = by_id[rewrite[bn.id][1]].inputs[1] if rewrite[bn.id][1] else None
+            if b_in is None:
+                z = GraphNode(n.id + "#b0", "const",
+                              out_type=TensorType([by_id[n.inputs[1]].out_type.shape[0]], "f32"))
+                z.data = np.zeros(z.out_type.shape, np.float32)
+                out.nodes.append(z)
+                b_in = z.id
+            # the fold nodes precede the conv, so fuse_pass groups the conv
+            # with its epilogue only (a parameter computation never joins it)
+            bf = GraphNode(n.id + "#bnb", "bn_fold_bias", [b_in, gm, bt, mu, vr], dict(eps))
+            out.nodes.append(bf)
+            c = copy.deepcopy(n)
+            c.inputs = [n.inputs[0], wf.id]
+            out.nodes.append(c)
+            # the bias_add takes over the batch_norm's id (its consumers)
+            out.nodes.append(GraphNode(bn.id, "bias_add", [c.id, bf.id]))
     out.validate()
     return out

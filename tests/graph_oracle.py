@@ -135,6 +135,13 @@ def evaluate(g, feeds: Dict[str, np.ndarray], params: Dict[str, np.ndarray],
                 st = tuple(root.attrs.get("strides", (1, 1)))
                 pd = tuple(root.attrs.get("padding", (0, 0)))
                 y = fused_conv(root.op, rnd(x), rnd(w), st, pd, items)
+        elif n.op in ("bn_fold_weight", "bn_fold_bias"):
+            # parameters: kept in f32 (the device folds before packing)
+            env[n.id] = _bn_fold(n, [env[i] for i in n.inputs])
+            continue
+        elif n.op == "const":
+            env[n.id] = np.asarray(n.data, np.float32)
+            continue
         elif n.op == "max_pool2d":
             y = max_pool2d(env[n.inputs[0]], tuple(n.attrs.get("kernel", (3, 3))),
                            tuple(n.attrs.get("strides", (2, 2))),
@@ -161,6 +168,20 @@ def evaluate(g, feeds: Dict[str, np.ndarray], params: Dict[str, np.ndarray],
         env[n.id] = y
     del cons
     return {o: env[o] for o in g.outputs}
+
+
+def _bn_fold(n, ins):
+    """fold_batch_norm's parameter ops, restated: s = gamma / sqrt(var + eps)
+    and every product / sum rounded to f32 once."""
+    f32 = np.float32
+    eps = f32(float(n.attrs.get("eps", 1e-5)))
+    if n.op == "bn_fold_weight":
+        w, g, v = (np.asarray(a, f32) for a in ins)
+        s = (g / np.sqrt(v + eps)).astype(f32)
+        return (w * s[:, None, None, None]).astype(f32)
+    b, g, beta, mu, v = (np.asarray(a, f32) for a in ins)
+    s = (g / np.sqrt(v + eps)).astype(f32)
+    return (((b - mu).astype(f32) * s).astype(f32) + beta).astype(f32)
 
 
 def _reshape_items(items):
