@@ -170,16 +170,22 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
     const int items = nimg * rows * strips;
     // kTW consecutive output columns per item: each loaded (and unpacked)
     // input column serves up to 3 taps of neighbouring outputs.
-    // (image, row, strip) of item it2, stepped by pix_step with carries:
-    // the divisions run once per tile instead of twice per item.
-    const int ds = pix_step % strips, dq = pix_step / strips;
-    const int dr = dq % rows, dim = dq / rows;
-    int s_i = lane_pix % strips, r_i = (lane_pix / strips) % rows, im_i = lane_pix / strips / rows;
+    // (image, strip, row) of item it2 -- ROW fastest: neighbouring items
+    // are the same strip of consecutive rows, cols_in * cb * ES bytes apart
+    // (cols_in odd for 64-byte channel rows, see dw_tma_plan), so the two
+    // pixels a 64-byte-row layer (D1: 32 bf16 channels) puts in one
+    // 128-byte shared-memory wavefront fall in different banks;
+    // strip-fastest put them kTW * 64 B apart, a 2-way conflict on every
+    // tap read. Stepped by pix_step with carries: the divisions run once
+    // per tile instead of twice per item.
+    const int dr = pix_step % rows, dq = pix_step / rows;
+    const int ds = dq % strips, dim = dq / strips;
+    int r_i = lane_pix % rows, s_i = (lane_pix / rows) % strips, im_i = lane_pix / rows / strips;
     auto advance = [&]() {
-      s_i += ds;
-      if (s_i >= strips) { s_i -= strips; ++r_i; }
       r_i += dr;
-      if (r_i >= rows) { r_i -= rows; ++im_i; }
+      if (r_i >= rows) { r_i -= rows; ++s_i; }
+      s_i += ds;
+      if (s_i >= strips) { s_i -= strips; ++im_i; }
       im_i += dim;
     };
     for (int it2 = lane_pix; it2 < items; it2 += pix_step, advance()) {
@@ -385,6 +391,10 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
   t->cblocks = p.c / cb;
   // whole kTW-column strips: the last strip reads TMA zero-fill columns
   t->cols_in = (((p.ow + kTW - 1) / kTW) * kTW - 1) * p.sw + 3;
+  // 64-byte channel rows (D1: 32 bf16 channels): an odd number of columns
+  // per input row, so vertically adjacent pixels (the row-fastest items'
+  // neighbours) sit 64 B apart modulo 128 -- different banks
+  if ((cb * es) % 128 && t->cols_in % 2 == 0) ++t->cols_in;
   if (t->cols_in > 256) return false;
   const int budget = 100 * 1024;  // per buffer (two buffers + slack < 227 KB)
   int th_max = p.oh;
@@ -416,9 +426,15 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
       const long tiles = static_cast<long>(p.n) * bands * t->cblocks;
       const int grid = tiles < sms ? static_cast<int>(tiles) : sms;
       std::fill(load.begin(), load.end(), 0L);
+      // a tile's cost: its passes over the CTA's threads (items of kTW
+      // outputs, pix_step per pass; a part-filled last pass costs a whole
+      // one) plus ~one pass of load / barrier overhead
+      const int strips = (p.ow + kTW - 1) / kTW;
+      const int pix_step = kDwtThreads / (cb * es / 16);
       for (long tile = 0; tile < tiles; ++tile) {
         const int band = static_cast<int>(tile % bands);
-        load[tile % grid] += std::min(h, p.oh - band * h) + 2;
+        const int rows = std::min(h, p.oh - band * h);
+        load[tile % grid] += (rows * strips + pix_step - 1) / pix_step + 1;
       }
       const long span = *std::max_element(load.begin(), load.begin() + grid);
       if (best < 0 || span < best) { best = span; th = h; }
