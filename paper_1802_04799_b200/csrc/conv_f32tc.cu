@@ -64,6 +64,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
+constexpr int kMaxRows = 8;    // row-ring slots (ConvGemmParams::rows)
 
 template <int BN, int SWZ, int STAGES, bool INTER, bool RES = false, bool HALO = false>
 struct F32tcCfg {
@@ -104,7 +105,7 @@ struct F32tcCfg {
   static constexpr int kYBase = 2 * kXCols;
   static constexpr uint32_t kTmemCols = 2 * kXCols + kYBufs * kYCols <= 256 ? 256 : 512;
   // + res_bytes (RES) + hbuf x kAPlanes x halo_bytes (HALO)
-  static constexpr int kSmem = 1024 + STAGES * kStage + 8 * 4096 + 256 + BN * 4;
+  static constexpr int kSmem = 1024 + STAGES * kStage + 8 * 4096 + 512 + BN * 4;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   static_assert(2 * kXCols + kYBufs * kYCols <= 512, "TMEM budget");
   static_assert(!INTER || SWZ == 128, "interleaved planes live in one 128-B row");
@@ -134,6 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // of the interleaved row
   constexpr int kPlaneA = INTER ? 32 : Cfg::kA;
   constexpr int kPlaneB = Cfg::kBPlane;
+  // shared-memory descriptors without their start address (make_smem_desc)
+  constexpr uint64_t kADescHi = (1ull << 16) | (static_cast<uint64_t>((8 * SWZ) >> 4) << 32) |
+                                (1ull << 46) | (static_cast<uint64_t>(SWZ == 128 ? 2 : SWZ == 64 ? 4 : 6) << 61);
+  constexpr uint64_t kBDescHi = (1ull << 16) | (static_cast<uint64_t>((8 * kBSW) >> 4) << 32) |
+                                (1ull << 46) | (static_cast<uint64_t>(kBSW == 128 ? 2 : kBSW == 64 ? 4 : 6) << 61);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -148,11 +154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = sempty + 2;
   uint64_t* tempty = tfull + 2;
   uint64_t* wfull = tempty + 2;  // RES: the resident B tiles landed
-  uint64_t* hfull = wfull + 1;   // HALO: halo buffer landed / free
-  uint64_t* hempty = hfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
+  uint64_t* hfull = wfull + 1;   // HALO: halo buffer (row ring: row slot) landed / free
+  uint64_t* hempty = hfull + kMaxRows;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + kMaxRows);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
-  uint32_t* sBias = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
+  uint32_t* sBias = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -171,6 +177,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int chunk = p.chunk_iters;               // k-iterations per hh chunk
   const int cpp = p.cp;                          // channels per plane
   const int pix = INTER ? 64 : 3 * cpp;          // packed channels per pixel
+  // work items of this CTA: strided over the grid, or (row ring) one
+  // contiguous range, so consecutive items are consecutive output rows
+  const bool ring = HALO && p.rows > 0;
+  const int it_lo = ring ? static_cast<int>(static_cast<int64_t>(num_items) * blockIdx.x / gridDim.x)
+                         : static_cast<int>(blockIdx.x);
+  const int it_hi = ring ? static_cast<int>(static_cast<int64_t>(num_items) * (blockIdx.x + 1) / gridDim.x)
+                         : num_items;
+  const int it_step = ring ? 1 : static_cast<int>(gridDim.x);
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_a);
@@ -187,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[i], 256);
     }
     mbar_init(wfull, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kMaxRows; ++i) {
       mbar_init(&hfull[i], 1);
       mbar_init(&hempty[i], 1);
     }
@@ -241,13 +255,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         // then one weight stage per filter tap (the B thread)
         int hb = 0;
         uint32_t hphase = 0;
-        for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
+        // row ring: next input row (as v = ih + ph) to load, per-slot fill
+        // parity / ever-filled bits
+        int ring_img = -1, ring_v = 0;
+        uint32_t fillpar = 0, filled = 0;
+        for (int item = it_lo; item < it_hi; item += it_step) {
           const int m_tile = item / p.n_tiles;
           const int n_tile = item - m_tile * p.n_tiles;
           const int img = m_tile / p.bands;
           const int oh0 = (m_tile - img * p.bands) * p.th;
+          if (ring && issue_a) {
+            if (img != ring_img) {
+              ring_img = img;
+              ring_v = oh0;
+            }
+            for (; ring_v < oh0 + p.r; ++ring_v) {
+              const int slot = ring_v % p.rows;
+              const uint32_t bit = 1u << slot;
+              if (filled & bit)  // the MMAs of the last reader of this slot have landed
+                twait(&hempty[slot], ((fillpar & bit) ? 0u : 1u), prof, &dw[0]);
+              filled |= bit;
+              fillpar ^= bit;
+              mbar_arrive_expect_tx(&hfull[slot], static_cast<uint32_t>(p.halo_box_bytes));
+              tma_load_4d(sHalo + slot * p.halo_bytes, &tm_a, &hfull[slot], 0, -p.pw,
+                          ring_v - p.ph, img);
+            }
+          }
           for (int cb = 0; cb < p.cblocks; ++cb) {
-            if (issue_a) {
+            if (issue_a && !ring) {
               twait(&hempty[hb], hphase ^ 1, prof, &dw[0]);
               mbar_arrive_expect_tx(&hfull[hb],
                                     static_cast<uint32_t>(Cfg::kAPlanes * p.halo_box_bytes));
@@ -347,7 +382,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       int hb = 0;
       uint32_t hphase = 0;
-      for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
+      int ring_img = -1, ring_v = 0;
+      uint32_t fillpar = 0;
+      // the fast ring path (C1: interleaved planes, resident weights, GRP):
+      // parameters in registers (the asm "memory" clobbers would otherwise
+      // reload them from the constant bank every tap) and descriptors
+      // advanced by adding to their 16-byte address field
+      constexpr bool kFast = HALO && RES && INTER && Cfg::kGrp;
+      const int R = p.r, S = p.s, nrows = p.rows > 0 ? p.rows : 1, hbytes = p.halo_bytes;
+      const int ntl = p.n_tiles, bands = p.bands;
+      const uint64_t adesc0 = make_smem_desc<SWZ>(smem_u32(sHalo), 8 * SWZ);
+      const uint64_t hstep = static_cast<uint64_t>(hbytes >> 4);  // one row slot, in 16-B units
+      int f_img = 0, f_oh = 0, f_s0 = 0, ring_slot = 0;
+      const uint64_t bdesc0 = make_smem_desc<kBSW>(smem_u32(sRes), 8 * kBSW);
+      for (int item = it_lo; item < it_hi; item += it_step, ++local) {
         const int tb = local % Cfg::kYBufs;
         const int tuse = local / Cfg::kYBufs;
         if (Cfg::kHasY) {
@@ -367,14 +415,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             s_tmem = tmem_base + sb * Cfg::kXCols;
           }
+          // descriptors by adding to the 16-byte address field (shared
+          // addresses < 256 KB: no carry out of its 14 bits) -- the issuing
+          // thread's scalar work between MMA batches is tensor-pipe idle time
+          const uint64_t ad = kADescHi | (abase >> 4), bd = kBDescHi | (bbase >> 4);
+          const uint32_t ap = a_plane >> 4;
 #pragma unroll
           for (int kk = 0; kk < Cfg::kKSteps; ++kk) {
-            const uint32_t a0 = abase + kk * 32;
-            const uint32_t b0 = bbase + kk * 32;
-            const uint64_t ah = make_smem_desc<SWZ>(a0, 8 * SWZ);
-            const uint64_t am = make_smem_desc<SWZ>(a0 + a_plane, 8 * SWZ);
-            const uint64_t al = make_smem_desc<SWZ>(a0 + 2 * a_plane, 8 * SWZ);
-            const uint64_t bh = make_smem_desc<kBSW>(b0, 8 * kBSW);
+            const uint64_t ah = ad + 2 * kk;  // K16 slice kk: +32 B
+            const uint64_t am = ah + ap;
+            const uint64_t al = ah + 2 * ap;
+            const uint64_t bh = bd + 2 * kk;
             const uint32_t t_acc = (first && kk == 0) ? 0u : 1u;
             const uint32_t s_acc = (in_chunk | kk) != 0 ? 1u : 0u;
             if constexpr (Cfg::kGrp) {
@@ -384,8 +435,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_mma<MmaKind::kF16>(s_tmem + BN, am, bh, idesc2, 1u);
               tc_mma<MmaKind::kF16>(s_tmem + BN, al, bh, idesc, 1u);
             } else {
-              const uint64_t bm = make_smem_desc<kBSW>(b0 + kPlaneB, 8 * kBSW);
-              const uint64_t bl = make_smem_desc<kBSW>(b0 + 2 * kPlaneB, 8 * kBSW);
+              const uint64_t bm = bh + (kPlaneB >> 4);
+              const uint64_t bl = bh + 2 * (kPlaneB >> 4);
               tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc, s_acc);
               tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, t_acc);
               tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
@@ -401,7 +452,119 @@ __global__ void __launch_bounds__(kThreads, 1)
             in_chunk = 0;
           }
         };
-        if constexpr (HALO) {
+        if (ring && kFast && p.chunk_iters >= R * S) {
+          // the row ring with the issue loop reduced to descriptor adds and
+          // incrementally stepped row / slot counters: the issue of a tile
+          // blocks on the tensor pipe's queue, so any scalar work between
+          // two tiles (divisions, modulo) is a pipe bubble
+          if (item == it_lo) {
+            f_img = item / bands;  // n_tiles == 1 in ring mode
+            f_oh = item - f_img * bands;
+            f_s0 = f_oh % nrows;
+            ring_img = f_img;
+            ring_v = f_oh;
+            ring_slot = f_s0;
+          } else if (f_oh + 1 == bands) {  // the next image
+            ++f_img;
+            f_oh = 0;
+            f_s0 = 0;
+            ring_v = 0;
+            ring_slot = 0;
+          } else {
+            ++f_oh;
+            f_s0 = f_s0 + 1 == nrows ? 0 : f_s0 + 1;
+          }
+          for (; ring_v < f_oh + R; ++ring_v) {
+            twait(&hfull[ring_slot], (fillpar >> ring_slot) & 1u, prof, &dw[4]);
+            fillpar ^= 1u << ring_slot;
+            ring_slot = ring_slot + 1 == nrows ? 0 : ring_slot + 1;
+          }
+          tc_fence_after();
+          // one hh chunk per tile (chunk_iters >= r * s)
+          const int sb = g & 1;
+          twait(&sempty[sb], ((g >> 1) & 1) ^ 1, prof, &dw[3]);
+          tc_fence_after();
+          const uint32_t x = tmem_base + sb * Cfg::kXCols;
+          uint64_t bh = bdesc0;
+          int slot = f_s0;
+          for (int r = 0; r < R; ++r) {
+            uint64_t ah = adesc0 + static_cast<uint64_t>(slot) * hstep;
+            slot = slot + 1 == nrows ? 0 : slot + 1;
+            for (int s = 0; s < S; ++s) {
+              tc_mma<MmaKind::kF16>(x, ah, bh, idesc3, (r | s) != 0 ? 1u : 0u);
+              tc_mma<MmaKind::kF16>(x + BN, ah + 2, bh, idesc2, 1u);  // A_m: +32 B
+              tc_mma<MmaKind::kF16>(x + BN, ah + 4, bh, idesc, 1u);   // A_l: +64 B
+              ah += SWZ >> 4;
+              bh += Cfg::kBStage >> 4;
+            }
+          }
+          tc_commit(&sfull[sb]);
+          ++g;
+          // the next item is the next row of the same image: only row f_oh
+          // is done; otherwise all r rows are
+          if (item + 1 < it_hi && f_oh + 1 < bands) {
+            tc_commit(&hempty[f_s0]);
+          } else {
+            int sl = f_s0;
+            for (int r = 0; r < R; ++r) {
+              tc_commit(&hempty[sl]);
+              sl = sl + 1 == nrows ? 0 : sl + 1;
+            }
+          }
+        } else if (ring) {
+          // one output row: taps (r, s) read row slot (oh0 + r) % rows from
+          // pixel s on; rows land once, in order, and are released when the
+          // last of their r readers is issued
+          const int m_tile = item / p.n_tiles;
+          const int img = m_tile / p.bands;
+          const int oh0 = (m_tile - img * p.bands) * p.th;
+          if (img != ring_img) {
+            ring_img = img;
+            ring_v = oh0;
+          }
+          for (; ring_v < oh0 + p.r; ++ring_v) {
+            const int slot = ring_v % p.rows;
+            twait(&hfull[slot], (fillpar >> slot) & 1u, prof, &dw[4]);
+            fillpar ^= 1u << slot;
+          }
+          tc_fence_after();
+          const uint32_t a_plane = INTER ? 32u : static_cast<uint32_t>(p.halo_bytes);
+          for (int r = 0; r < p.r; ++r) {
+            const uint32_t row = smem_u32(sHalo + ((oh0 + r) % p.rows) * p.halo_bytes);
+            for (int s = 0; s < p.s; ++s) {
+              const int k = r * p.s + s;
+              uint32_t bbase;
+              if (RES) {
+                bbase = smem_u32(sRes) + k * Cfg::kBStage;
+              } else {
+                twait(&full[stage], phase, prof, &dw[4]);
+                tc_fence_after();
+                bbase = smem_u32(sRing + stage * Cfg::kStage);
+              }
+              step(row + s * SWZ, bbase, a_plane, r + 1 == p.r && s + 1 == p.s);
+              if (!RES) {
+                tc_commit(&empty[stage]);
+                if (++stage == STAGES) {
+                  stage = 0;
+                  phase ^= 1;
+                }
+              }
+            }
+          }
+          // the next item is the next row of the same image: only row oh0
+          // is done; otherwise all r rows are (and any prefetched beyond)
+          bool next_row = false;
+          if (item + 1 < it_hi) {
+            const int nm = (item + 1) / p.n_tiles;
+            const int nimg = nm / p.bands;
+            next_row = nimg == img && (nm - nimg * p.bands) * p.th == oh0 + 1;
+          }
+          if (next_row) {
+            tc_commit(&hempty[oh0 % p.rows]);
+          } else {
+            for (int v = oh0; v < oh0 + p.r; ++v) tc_commit(&hempty[v % p.rows]);
+          }
+        } else if constexpr (HALO) {
           const uint32_t a_plane = INTER ? 32u : static_cast<uint32_t>(p.halo_bytes);
           for (int cb = 0; cb < p.cblocks; ++cb) {
             twait(&hfull[hb], hphase, prof, &dw[4]);
@@ -465,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int g = 0;
     int local = 0;
     int staged_n = -1;
-    for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++local) {
+    for (int item = it_lo; item < it_hi; item += it_step, ++local) {
       const int mn = item / splits;
       const int split = item - mn * splits;
       const int m_tile = mn / p.n_tiles;
@@ -633,8 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (dw[i]) atomicAdd(&p.dbg[i], static_cast<unsigned long long>(dw[i]));
     if (threadIdx.x == 0) {
       atomicAdd(&p.dbg[8], static_cast<unsigned long long>(clock64() - t_start));
-      atomicAdd(&p.dbg[9], static_cast<unsigned long long>(
-                               (num_items - blockIdx.x + gridDim.x - 1) / gridDim.x));
+      atomicAdd(&p.dbg[9], static_cast<unsigned long long>((it_hi - it_lo + it_step - 1) / it_step));
     }
   }
 }

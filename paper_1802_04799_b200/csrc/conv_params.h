@@ -77,7 +77,13 @@ struct ConvGemmParams {
   int32_t th, wp, bands;
   int32_t halo_bytes;      // smem bytes per halo plane buffer (1024-aligned)
   int32_t halo_box_bytes;  // bytes one halo box lands (th + r - 1) * wp * 128
-  int32_t hbuf;            // halo buffers (1 or 2)
+  int32_t hbuf;            // halo buffers (1 or 2), or the row ring's size
+  // f32tc row ring (rows > 0; th == 1, one channel block, one N tile): each
+  // CTA walks a CONTIGUOUS range of output rows, and the `rows` halo
+  // buffers hold single input rows -- a row is loaded once and serves the
+  // r consecutive output rows that read it (a per-tile halo box re-reads
+  // r - 1 of its r rows). halo_bytes / halo_box_bytes are then per row.
+  int32_t rows;
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA

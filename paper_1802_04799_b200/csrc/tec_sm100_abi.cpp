@@ -1096,12 +1096,32 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   // 107 vs 86 / 70 / 70 us) -- with three planes the halo plus a weight
   // ring leave room for one halo buffer, and th > 1 tiles store per element.
   bool halo = false, res = false;
-  int th = 0, wp = 0, bands = 0, halo_bytes = 0, halo_box = 0, hbuf = 0;
+  int th = 0, wp = 0, bands = 0, halo_bytes = 0, halo_box = 0, hbuf = 0, ring_rows = 0;
+  // Row ring (th == 1, one channel block, one N tile -- the stem C1): the
+  // halo buffers hold single input rows, each CTA walks a contiguous range
+  // of output rows, and a row is loaded once for the r rows that read it
+  // (conv_f32tc.cu `ring`); TEC_SM100_F32TC_NO_RING=1 keeps per-tile boxes.
+  static const bool no_ring = std::getenv("TEC_SM100_F32TC_NO_RING") != nullptr;
   if (path != 1 && d->stride_h == 1 && d->stride_w == 1 && swz == 128 &&
       !(kn && kn->split_k > 1)) {
     wp = (int)(d->w + 2 * d->pad_w);
     th = (int)std::min<int64_t>(pl.oh, 128 / std::max(1, wp));
-    if (path == 2 && th >= 1 && wp <= 256 && th + d->r - 1 <= 256) {
+    const int row_px = 128 + (int)d->s - 1;  // an A operand: 128 virtual rows from pixel s
+    if (path == 2 && !no_ring && th == 1 && pl.cpp / cb == 1 && n_tiles == 1 && inter &&
+        want_res != 1 && row_px <= 256) {
+      const int fixed = conv_f32tc_smem_bytes(bn, swz, inter, true, true);
+      const int row_bytes = (row_px * 128 + 1023) & ~1023;
+      const int rows = fixed > 0 ? std::min(8, (kBudget - fixed - res_bytes) / row_bytes) : 0;
+      if (rows >= d->r + 1) {
+        halo = true;
+        res = true;
+        ring_rows = hbuf = rows;
+        halo_bytes = row_bytes;
+        halo_box = row_px * 128;
+        bands = (int)pl.oh;
+      }
+    }
+    if (path == 2 && !halo && th >= 1 && wp <= 256 && th + d->r - 1 <= 256) {
       const int halo_px = 128 + (int)((d->r - 1) * wp + d->s);
       halo_bytes = (halo_px * 128 + 1023) & ~1023;
       halo_box = 128 * wp * (int)(th + d->r - 1);
@@ -1129,7 +1149,9 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     cuuint64_t dims[4] = {(cuuint64_t)pl.cp, (cuuint64_t)d->w, (cuuint64_t)d->h, (cuuint64_t)d->n};
     cuuint64_t strides[3] = {(cuuint64_t)(pl.cp * 2), (cuuint64_t)(pl.cp * 2 * d->w),
                              (cuuint64_t)(pl.cp * 2 * d->w * d->h)};
-    cuuint32_t box[4] = {64, (cuuint32_t)wp, (cuuint32_t)(th + d->r - 1), 1};
+    // row ring: one input row of 128 + s - 1 pixels (past the row end: zero fill)
+    cuuint32_t box[4] = {64, ring_rows ? (cuuint32_t)(halo_box / 128) : (cuuint32_t)wp,
+                         ring_rows ? 1u : (cuuint32_t)(th + d->r - 1), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = fns.tiled(&tm_a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1212,7 +1234,7 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   p.epi = epi;
   p.tma_store = tma_ok ? 1 : 0;
   p.th = th; p.wp = wp; p.bands = bands;
-  p.halo_bytes = halo_bytes; p.halo_box_bytes = halo_box; p.hbuf = hbuf;
+  p.halo_bytes = halo_bytes; p.halo_box_bytes = halo_box; p.hbuf = hbuf; p.rows = ring_rows;
   // hh promotion chunk: 256 K elements per plane (TEC_SM100_F32TC_CHUNK
   // overrides, for the accuracy experiments only)
   static const int chunk_k = [] {
@@ -1297,11 +1319,11 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     cudaFree(dbg);
     const double c = (double)grid;
     std::fprintf(stderr,
-                 "[tec-prof] f32tc halo=%d res=%d bn=%d inter=%d splits=%d items/cta=%.2f "
+                 "[tec-prof] f32tc halo=%d ring=%d res=%d bn=%d inter=%d splits=%d items/cta=%.2f "
                  "cta_cycles=%.0f | prodA_wait=%.0f prodB_wait=%.0f mma_wait_tile=%.0f "
                  "mma_wait_chunk=%.0f mma_wait_data=%.0f epi_wait_chunk=%.0f epi_wait_tile=%.0f "
                  "epi_busy=%.0f (per CTA)\n",
-                 (int)halo, (int)res, bn, (int)inter, p.splits, h[9] / c, h[8] / c, h[0] / c, h[1] / c,
+                 (int)halo, ring_rows, (int)res, bn, (int)inter, p.splits, h[9] / c, h[8] / c, h[0] / c, h[1] / c,
                  h[2] / c, h[3] / c, h[4] / c, h[5] / c, h[6] / c, h[7] / c);
   }
   return TEC_OK;

@@ -418,13 +418,20 @@ def test_split_k_scratch_shared_across_shapes():
 
 
 @pytest.mark.parametrize("path", [1, 2])
-@pytest.mark.parametrize("case", ["C1", "C2", "C6", "C9", "odd5x5", "odd_res"])
+@pytest.mark.parametrize("case", ["C1", "C2", "C6", "C9", "odd5x5", "odd_res", "stem30", "stem46"])
 def test_f32tc_im2col_and_shifted_window(case, path):
     """f32tc A-operand paths (knob tile_k): 1 = im2col TMA, 2 = shifted
     window (one halo load per tile and channel block, every tap a row
-    shift; th = 1 rows store by TMA, th > 1 per element). 'odd*': 5x5,
-    padding 2, W not a multiple of anything, a batch tail, residual."""
-    if case.startswith("odd"):
+    shift; th = 1 rows store by TMA, th > 1 per element) -- for the
+    space-to-depth stems the row ring (each CTA a contiguous range of
+    output rows, input rows loaded once). 'odd*': 5x5, padding 2, W not a
+    multiple of anything, a batch tail, residual. 'stem*': 7x7 / 2 stems on
+    small images, so CTA row ranges start, end and cross image boundaries
+    (fewer rows than CTAs; several images per CTA)."""
+    if case.startswith("stem"):
+        hw = int(case[4:])
+        shape_x, shape_w, s, pad = ((5 if hw == 30 else 21), 3, hw, hw), (64, 3, 7, 7), 2, 3
+    elif case.startswith("odd"):
         shape_x, shape_w, s, pad = (3, 64, 11, 13), (64, 64, 5, 5), 1, 2
     else:
         hw, c, k, r, s = RESNET18_CONVS[case]
