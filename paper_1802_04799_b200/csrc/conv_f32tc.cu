@@ -756,12 +756,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (PROG == epi::kProgBiasAddRelu && orow >= 0)
         rrow = static_cast<const uint8_t*>(p.epi.residual) +
                (static_cast<int64_t>(orow) * p.oc + n_tile * BN + hf * HB) * 4;
+      // shifted window with th > 1: a warp's 32 virtual rows can straddle
+      // two output rows, so the half's 4 warps stage all 128 rows (their 4
+      // KB stages are consecutive) and one thread stores each output row of
+      // the tile as a {32 ch, OW px} box from staged row ohl * wp
+      const bool group = HALO && p.th > 1;
 #pragma unroll
       for (int c0 = 0; c0 < HB; c0 += 32) {
         if (n_tile * BN + hf * HB + c0 < p.oc) {
           uint32_t acc[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) acc[j] = __float_as_uint(sum[c0 + j]);
+          if (group) {
+            if (q == 0 && lane == 0) bulk_wait_read<0>();  // the half's previous stores have read it
+            epi::named_bar_sync(3 + hf, 128);
+            epi::epi_acc_to_box<PROG, 4>(acc, static_cast<int>(lane), sBias + hf * HB + c0,
+                                         stage_u32, &overflow, rrow ? rrow + c0 * 4 : nullptr);
+            fence_proxy_async_smem();
+            epi::named_bar_sync(3 + hf, 128);
+            if (q == 0 && lane == 0) {
+              const uint32_t half = smem_u32(sStage + hf * 4 * 4096);
+              for (int ohl = 0; ohl < p.th && oh0 + ohl < p.oh; ++ohl)
+                tma_store_3d(&tm_y, half + static_cast<uint32_t>(ohl * p.wp) * 128,
+                             n_tile * BN + hf * HB + c0, 0, img * p.oh + oh0 + ohl);
+              bulk_commit();
+            }
+            continue;
+          }
           if (lane == 0) bulk_wait_read<0>();  // the box's previous store has read it
           __syncwarp();
           epi::epi_acc_to_box<PROG, 4>(acc, static_cast<int>(lane), sBias + hf * HB + c0,

@@ -1214,9 +1214,12 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     if (!halo) {
       cuuint64_t dims[2] = {(cuuint64_t)d->k, (cuuint64_t)pl.m};
       make_store_map(&tm_y, y, TEC_DT_F32, 2, dims, 32, &tma_ok);
-    } else if (th == 1) {
+    } else {
+      // (OC, OW, N*OH): th == 1 -- a 32-pixel box per warp (pixels past OW
+      // clipped); th > 1 -- one {32 ch, OW px} box per output row, stored
+      // from the half-group's staged rows (conv_f32tc.cu `group`)
       cuuint64_t dims[3] = {(cuuint64_t)d->k, (cuuint64_t)pl.ow, (cuuint64_t)(d->n * pl.oh)};
-      make_store_map(&tm_y, y, TEC_DT_F32, 3, dims, 32, &tma_ok);
+      make_store_map(&tm_y, y, TEC_DT_F32, 3, dims, th == 1 ? 32 : (int)pl.ow, &tma_ok);
     }
   }
   ConvGemmParams p{};

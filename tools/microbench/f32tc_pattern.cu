@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(128, 1) k(int tiles, int wp, long long* cyc, i
 // The kernel's chunk handshake: the MMA thread commits sfull[b] per tile
 // and, before tile t, waits sempty[b] (arrived by 256 "epilogue" threads
 // once they see sfull[b] of tile t - 2) -- no TMEM reads.
-__global__ void __launch_bounds__(384, 1) hs(int tiles, long long* cyc, int sleep_wait) {
+__global__ void __launch_bounds__(384, 1) hs(int tiles, long long* cyc, int sleep_wait, int tap_waits = 0) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = sm;
@@ -119,7 +119,9 @@ __global__ void __launch_bounds__(384, 1) hs(int tiles, long long* cyc, int slee
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 256); }
+    mbar_init(&bar[1], 1);
     fence_barrier_init();
+    mbar_arrive(&bar[1]);  // phase 0 completes
   }
   if (threadIdx.x / 32 == 2) tmem_alloc<512>(slot);
   tc_fence_before(); __syncthreads(); tc_fence_after();
@@ -144,6 +146,11 @@ __global__ void __launch_bounds__(384, 1) hs(int tiles, long long* cyc, int slee
         tc_mma<MmaKind::kF16>(x, ah, bh, id192, tap ? 1u : 0u);
         tc_mma<MmaKind::kF16>(x + 64, ah + 2, bh, id128, 1u);
         tc_mma<MmaKind::kF16>(x + 64, ah + 4, bh, id64, 1u);
+        // the kernels' per-stage operand wait, on an already completed phase
+        for (int w = 0; w < tap_waits; ++w) {
+          mbar_wait(&bar[1], 0);
+          tc_fence_after();
+        }
       }
       tc_commit(&sfull[b]);
     }
@@ -163,12 +170,12 @@ __global__ void __launch_bounds__(384, 1) hs(int tiles, long long* cyc, int slee
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-void run_hs(const char* name, int sleep_wait) {
+void run_hs(const char* name, int sleep_wait, int tap_waits = 0) {
   long long* d; cudaMalloc(&d, 148 * 8);
   const int smem = 200 * 1024 + 2048;
   cudaFuncSetAttribute(hs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int tiles = 200;
-  hs<<<148, 384, smem>>>(tiles, d, sleep_wait);
+  hs<<<148, 384, smem>>>(tiles, d, sleep_wait, tap_waits);
   long long h[148];
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("%s: kernel failed\n", name); exit(1); }
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -193,6 +200,8 @@ void run(const char* name, int random = 0) {
 }
 
 int main() {
+  run_hs("handshake + 1 completed-barrier wait per tap", 1, 1);
+  run_hs("handshake + 2 completed-barrier waits per tap", 1, 2);
   run_hs("handshake sfull/sempty, sleeping waits", 1);
   run_hs("handshake sfull/sempty, spinning waits", 0);
   run<32, true, true, 1, 1>("grp3, X targets, 1 commit per tile", 1);
