@@ -394,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t adesc0 = make_smem_desc<SWZ>(smem_u32(sHalo), 8 * SWZ);
       const uint64_t hstep = static_cast<uint64_t>(hbytes >> 4);  // one row slot, in 16-B units
       int f_img = 0, f_oh = 0, f_s0 = 0, ring_slot = 0;
+      bool f_prepared = false;  // the next tile's waits already done
       const uint64_t bdesc0 = make_smem_desc<kBSW>(smem_u32(sRes), 8 * kBSW);
       for (int item = it_lo; item < it_hi; item += it_step, ++local) {
         const int tb = local % Cfg::kYBufs;
@@ -454,58 +455,73 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         if (ring && kFast && p.chunk_iters >= R * S) {
           // the row ring with the issue loop reduced to descriptor adds and
-          // incrementally stepped row / slot counters: the issue of a tile
-          // blocks on the tensor pipe's queue, so any scalar work between
-          // two tiles (divisions, modulo) is a pipe bubble
-          if (item == it_lo) {
-            f_img = item / bands;  // n_tiles == 1 in ring mode
-            f_oh = item - f_img * bands;
-            f_s0 = f_oh % nrows;
-            ring_img = f_img;
-            ring_v = f_oh;
-            ring_slot = f_s0;
-          } else if (f_oh + 1 == bands) {  // the next image
-            ++f_img;
-            f_oh = 0;
-            f_s0 = 0;
-            ring_v = 0;
-            ring_slot = 0;
-          } else {
-            ++f_oh;
-            f_s0 = f_s0 + 1 == nrows ? 0 : f_s0 + 1;
+          // incrementally stepped row / slot counters. The tensor pipe queues
+          // only about one tap of MMAs, so every wait or scalar step between
+          // two tiles is pipe idle time: the next tile's waits (its new row,
+          // its chunk buffer) run DURING this tile's last taps when the next
+          // tile is the next row of the same image (at an image change the
+          // new image's rows may need this tile's slots, released at its end)
+          if (!f_prepared) {
+            if (item == it_lo) {
+              f_img = item / bands;  // n_tiles == 1 in ring mode
+              f_oh = item - f_img * bands;
+              f_s0 = f_oh % nrows;
+              ring_v = f_oh;
+              ring_slot = f_s0;
+            } else {  // the next image
+              ++f_img;
+              f_oh = 0;
+              f_s0 = 0;
+              ring_v = 0;
+              ring_slot = 0;
+            }
+            for (; ring_v < f_oh + R; ++ring_v) {
+              twait(&hfull[ring_slot], (fillpar >> ring_slot) & 1u, prof, &dw[4]);
+              fillpar ^= 1u << ring_slot;
+              ring_slot = ring_slot + 1 == nrows ? 0 : ring_slot + 1;
+            }
+            twait(&sempty[g & 1], ((g >> 1) & 1) ^ 1, prof, &dw[3]);
+            tc_fence_after();
           }
-          for (; ring_v < f_oh + R; ++ring_v) {
-            twait(&hfull[ring_slot], (fillpar >> ring_slot) & 1u, prof, &dw[4]);
-            fillpar ^= 1u << ring_slot;
-            ring_slot = ring_slot + 1 == nrows ? 0 : ring_slot + 1;
-          }
-          tc_fence_after();
-          // one hh chunk per tile (chunk_iters >= r * s)
+          const int cur_oh = f_oh, cur_s0 = f_s0;
+          const bool next_same = item + 1 < it_hi && cur_oh + 1 < bands;
+          f_prepared = false;
           const int sb = g & 1;
-          twait(&sempty[sb], ((g >> 1) & 1) ^ 1, prof, &dw[3]);
-          tc_fence_after();
           const uint32_t x = tmem_base + sb * Cfg::kXCols;
+          const int prep_at = R * S > 3 ? R * S - 3 : 0;
           uint64_t bh = bdesc0;
-          int slot = f_s0;
+          int slot = cur_s0, tap = 0;
           for (int r = 0; r < R; ++r) {
             uint64_t ah = adesc0 + static_cast<uint64_t>(slot) * hstep;
             slot = slot + 1 == nrows ? 0 : slot + 1;
-            for (int s = 0; s < S; ++s) {
+            for (int s = 0; s < S; ++s, ++tap) {
               tc_mma<MmaKind::kF16>(x, ah, bh, idesc3, (r | s) != 0 ? 1u : 0u);
               tc_mma<MmaKind::kF16>(x + BN, ah + 2, bh, idesc2, 1u);  // A_m: +32 B
               tc_mma<MmaKind::kF16>(x + BN, ah + 4, bh, idesc, 1u);   // A_l: +64 B
               ah += SWZ >> 4;
               bh += Cfg::kBStage >> 4;
+              if (tap == prep_at && next_same) {
+                ++f_oh;
+                f_s0 = f_s0 + 1 == nrows ? 0 : f_s0 + 1;
+                for (; ring_v < f_oh + R; ++ring_v) {  // the next tile's new row
+                  twait(&hfull[ring_slot], (fillpar >> ring_slot) & 1u, prof, &dw[4]);
+                  fillpar ^= 1u << ring_slot;
+                  ring_slot = ring_slot + 1 == nrows ? 0 : ring_slot + 1;
+                }
+                twait(&sempty[(g + 1) & 1], (((g + 1) >> 1) & 1) ^ 1, prof, &dw[3]);
+                tc_fence_after();
+                f_prepared = true;
+              }
             }
           }
           tc_commit(&sfull[sb]);
           ++g;
-          // the next item is the next row of the same image: only row f_oh
+          // the next item is the next row of the same image: only row cur_oh
           // is done; otherwise all r rows are
-          if (item + 1 < it_hi && f_oh + 1 < bands) {
-            tc_commit(&hempty[f_s0]);
+          if (next_same) {
+            tc_commit(&hempty[cur_s0]);
           } else {
-            int sl = f_s0;
+            int sl = cur_s0;
             for (int r = 0; r < R; ++r) {
               tc_commit(&hempty[sl]);
               sl = sl + 1 == nrows ? 0 : sl + 1;
