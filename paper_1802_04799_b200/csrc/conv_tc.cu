@@ -198,29 +198,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles;
-           tile += gridDim.x, ++local) {
+      // The tensor pipe queues only about one group of MMAs, so the scalar
+      // work between stages on this thread is pipe idle time: descriptors
+      // are advanced by adding to their 16-byte address field (shared
+      // addresses < 256 KB), parameters live in registers (the asm "memory"
+      // clobbers would re-read them from the constant bank), the split of a
+      // tile is stepped instead of divided.
+      const uint64_t adesc0 = make_smem_desc<SWZ>(smem_u32(sA), 8 * SWZ);
+      const uint64_t bdesc0 = make_smem_desc<SWZ>(smem_u32(sB), 8 * SWZ);
+      const int nsplit = splits, kps_ = kps, kit = k_iters, ntiles = num_tiles;
+      const bool dbg = p.dbg != nullptr;
+      int split = static_cast<int>(blockIdx.x) % nsplit;
+      const int dsplit = static_cast<int>(gridDim.x) % nsplit;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
         const int acc = local & (nacc - 1);
         const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
-        { const long long t0 = p.dbg ? clock64() : 0;
+        { const long long t0 = dbg ? clock64() : 0;
           mbar_wait(&tempty[acc], (use & 1) ^ 1);
-          if (p.dbg) dbg_wait[2] += clock64() - t0; }
+          if (dbg) dbg_wait[2] += clock64() - t0; }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int kb = (tile % splits) * kps, ke = min(k_iters, kb + kps);
+        const int kb = split * kps_, ke = min(kit, kb + kps_);
+        split += dsplit;
+        if (split >= nsplit) split -= nsplit;
         for (int k = kb; k < ke; ++k) {
-          { const long long t0 = p.dbg ? clock64() : 0;
+          { const long long t0 = dbg ? clock64() : 0;
             mbar_wait(&full[stage], phase);
-            if (p.dbg) dbg_wait[1] += clock64() - t0; }
+            if (dbg) dbg_wait[1] += clock64() - t0; }
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * Cfg::kABytes);
-          const uint32_t b_base = smem_u32(sB + stage * Cfg::kBBytes);
+          const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (Cfg::kABytes >> 4));
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>(stage * (Cfg::kBBytes >> 4));
 #pragma unroll
-          for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
-            const uint64_t ad = make_smem_desc<SWZ>(a_base + kk * 32, 8 * SWZ);
-            const uint64_t bd = make_smem_desc<SWZ>(b_base + kk * 32, 8 * SWZ);
-            tc_mma<KIND>(d_tmem, ad, bd, idesc, (k != kb || kk != 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk)
+            tc_mma<KIND>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,  // K slice kk: +32 B
+                         (k != kb || kk != 0) ? 1u : 0u);
           tc_commit(&empty[stage]);  // frees the smem slot when MMAs land
           if (++stage == STAGES) {
             stage = 0;
