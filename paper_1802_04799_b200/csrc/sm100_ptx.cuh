@@ -240,6 +240,20 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 }
 // Arrive on the mbarrier at the same smem offset in every CTA of `mask`
 // once this thread's prior tcgen05 ops completed (cluster-shared release).
+// A operand from tensor memory (the "ts" form): D += A[tmem] x B[smem desc]
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// smem -> TMEM copy of one 128-row x 32-byte tile (a K16 slice of a bf16
+// operand) described by a shared-memory matrix descriptor
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t src_desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(src_desc));
+}
+
 __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
