@@ -111,6 +111,45 @@ struct F32tcCfg {
   static_assert(!INTER || SWZ == 128, "interleaved planes live in one 128-B row");
 };
 
+// The work items of one CTA: (output tile mn, k-iterations [kb, ke), its
+// segment index seg of nseg). Modes: items strided over the grid (split-K
+// splits of kps k-iterations, splits = 1 without), one contiguous range of
+// items (the row ring), or stream-K ranges of the flattened (tile, k) space.
+struct WorkIter {
+  int mode;  // 0 strided, 1 contiguous, 2 stream-K
+  int item, hi, step, splits, kps, k_iters, G, c;
+  long long pos, end, W;
+  // the CTA owning work position x: max c with floor(c W / G) <= x
+  __device__ __forceinline__ int owner(long long x) const {
+    return static_cast<int>(((x + 1) * G + W - 1) / W) - 1;
+  }
+  __device__ __forceinline__ bool next(int& it, int& mn, int& kb, int& ke, int& seg, int& nseg) {
+    if (mode < 2) {
+      if (item >= hi) return false;
+      it = item;
+      mn = item / splits;
+      seg = item - mn * splits;
+      nseg = splits;
+      kb = seg * kps;
+      ke = min(k_iters, kb + kps);
+      item += step;
+      return true;
+    }
+    if (pos >= end) return false;
+    mn = static_cast<int>(pos / k_iters);
+    const long long t0 = static_cast<long long>(mn) * k_iters;
+    const long long se = min(end, t0 + k_iters);
+    kb = static_cast<int>(pos - t0);
+    ke = static_cast<int>(se - t0);
+    const int o0 = owner(t0);
+    seg = c - o0;
+    nseg = owner(t0 + k_iters - 1) - o0 + 1;
+    it = mn;
+    pos = se;
+    return true;
+  }
+};
+
 // mbar_wait that adds its waiting cycles to *acc when profiling (p.dbg)
 __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool prof, long long* acc) {
   if (!prof) {
@@ -185,6 +224,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int it_hi = ring ? static_cast<int>(static_cast<int64_t>(num_items) * (blockIdx.x + 1) / gridDim.x)
                          : num_items;
   const int it_step = ring ? 1 : static_cast<int>(gridDim.x);
+  const bool sk = !HALO && p.stream_k;
+  auto make_iter = [&]() {
+    WorkIter w;
+    w.mode = sk ? 2 : (ring ? 1 : 0);
+    w.item = it_lo;
+    w.hi = it_hi;
+    w.step = it_step;
+    w.splits = sk ? 1 : splits;
+    w.kps = kps;
+    w.k_iters = k_iters;
+    w.G = static_cast<int>(gridDim.x);
+    w.c = static_cast<int>(blockIdx.x);
+    w.W = static_cast<long long>(p.m_tiles) * p.n_tiles * k_iters;
+    w.pos = w.W * w.c / w.G;
+    w.end = w.W * (w.c + 1) / w.G;
+    return w;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_a);
@@ -318,10 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-      } else
-      for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-        const int mn = item / splits;
-        const int split = item - mn * splits;
+      } else {
+      WorkIter wi = make_iter();
+      int item, mn, kb, ke, seg, nseg;
+      while (wi.next(item, mn, kb, ke, seg, nseg)) {
         const int m_tile = mn / p.n_tiles;
         const int n_tile = mn - m_tile * p.n_tiles;
         const int m0 = m_tile * kBM;
@@ -331,7 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ow = rem - oh * p.ow;
         const int w0 = ow * p.sw - p.pw;
         const int h0 = oh * p.sh - p.ph;
-        const int kb = split * kps, ke = min(k_iters, kb + kps);
         int r = kb / sc, rem_k = kb - r * sc;
         int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
         for (int k = kb; k < ke; ++k) {
@@ -365,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------ single-thread MMA issuer
@@ -396,7 +452,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int f_img = 0, f_oh = 0, f_s0 = 0, ring_slot = 0;
       bool f_prepared = false;  // the next tile's waits already done
       const uint64_t bdesc0 = make_smem_desc<kBSW>(smem_u32(sRes), 8 * kBSW);
-      for (int item = it_lo; item < it_hi; item += it_step, ++local) {
+      WorkIter wi = make_iter();
+      int item, w_mn, w_kb, w_ke, w_seg, w_nseg;
+      for (; wi.next(item, w_mn, w_kb, w_ke, w_seg, w_nseg); ++local) {
         const int tb = local % Cfg::kYBufs;
         const int tuse = local / Cfg::kYBufs;
         if (Cfg::kHasY) {
@@ -615,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
-          const int kb = (item % splits) * kps, ke = min(k_iters, kb + kps);
+          const int kb = w_kb, ke = w_ke;
           for (int k = kb; k < ke; ++k) {
             twait(&full[stage], phase, prof, &dw[4]);
             tc_fence_after();
@@ -644,9 +702,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int g = 0;
     int local = 0;
     int staged_n = -1;
-    for (int item = it_lo; item < it_hi; item += it_step, ++local) {
-      const int mn = item / splits;
-      const int split = item - mn * splits;
+    WorkIter wi = make_iter();
+    int item, mn, kb, ke, split, nseg;
+    for (; wi.next(item, mn, kb, ke, split, nseg); ++local) {
       const int m_tile = mn / p.n_tiles;
       const int n_tile = mn - m_tile * p.n_tiles;
       const int row0 = m_tile * kBM + static_cast<int>(q * 32);
@@ -665,7 +723,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = row0 + static_cast<int>(lane);
         orow = row < p.m ? row : -1;
       }
-      const int kb = split * kps, ke = min(k_iters, kb + kps);
       const int nch = (ke - kb + chunk - 1) / chunk;
       float sum[HB];
       float cross[Cfg::kGrp ? HB : 1];  // GRP: the cross terms of the X chunks
@@ -715,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < HB; ++j) sum[j] = __fadd_rn(sum[j], cross[j]);
       }
-      if (splits > 1) {
+      if (nseg > 1) {
         // publish this split's partial ([item][warp][column][lane]: one
         // 128-B line per column); the last split of the tile sums them all
         // in split order
@@ -724,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < HB; ++j) __stcg(mine + j * 32, sum[j]);
         __threadfence();
         epi::named_bar_sync(1, 256);
-        if (etid == 0) *s_last = atomicAdd(&p.tile_cnt[mn], 1) == splits - 1;
+        if (etid == 0) *s_last = atomicAdd(&p.tile_cnt[mn], 1) == nseg - 1;
         epi::named_bar_sync(1, 256);
         if (!*s_last) continue;
         __threadfence();
@@ -732,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < HB; ++j) sum[j] = __ldcg(part + j * 32);
 #pragma unroll 1
-        for (int sp = 1; sp < splits; ++sp) {
+        for (int sp = 1; sp < nseg; ++sp) {
           const float* ps = part + static_cast<size_t>(sp) * 8 * HB * 32;
 #pragma unroll
           for (int j = 0; j < HB; ++j) sum[j] = __fadd_rn(sum[j], __ldcg(ps + j * 32));

@@ -84,6 +84,12 @@ struct ConvGemmParams {
   // r consecutive output rows that read it (a per-tile halo box re-reads
   // r - 1 of its r rows). halo_bytes / halo_box_bytes are then per row.
   int32_t rows;
+  // f32tc stream-K (stream_k = 1, im2col): CTA c of the grid owns work
+  // positions [c*W/G, (c+1)*W/G) of W = tiles x k-iterations, so every CTA
+  // does the same number of k-iterations; a tile cut by CTA boundaries is
+  // finished by its last segment (partials summed in segment order; splits
+  // = the most segments any tile has)
+  int32_t stream_k;
 };
 
 // Shifted-window ("halo") implicit GEMM for stride-1 convolutions. A CTA

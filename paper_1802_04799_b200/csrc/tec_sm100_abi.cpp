@@ -1259,7 +1259,14 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   // Split-K (knob split_k; 0 = auto, im2col only): for outputs with few
   // tiles, the split count with the smallest makespan waves x (k-iterations
   // per split + ~2 k-iterations of partial write/read per item).
-  int splits = halo ? 1 : (kn && kn->split_k > 0 ? (int)kn->split_k : 0);
+  // knob split_k = -1: stream-K (im2col) -- every CTA takes an equal share of
+  // the flattened (tile, k-iteration) work; a tile cut by a share boundary is
+  // finished by its last segment. Removes the tile-count quantisation
+  // (2.65 tiles per SM -> 3 rounds) at the cost of partial round trips for
+  // the cut tiles. Results then depend on the grid / batch through the cuts
+  // (within the f32tc bar), so it is a tuner knob, not a default.
+  const bool stream_k = !halo && kn && kn->split_k == -1;
+  int splits = halo || stream_k ? 1 : (kn && kn->split_k > 0 ? (int)kn->split_k : 0);
   if (!splits) {
     double best = 1e30;
     for (int sp : {1, 2, 3, 4, 6, 8}) {
@@ -1273,9 +1280,19 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   p.splits = splits;
   p.kps = (k_iters + splits - 1) / splits;
   p.splits = (k_iters + p.kps - 1) / p.kps;  // no empty split
+  if (stream_k) {
+    // segments per tile <= 1 + the share boundaries inside it
+    const int64_t w = tiles * k_iters;
+    const int64_t g = std::min<int64_t>(sms, w);
+    const int64_t share = w / g;
+    p.stream_k = 1;
+    p.splits = (int32_t)std::min<int64_t>(k_iters, (k_iters + share - 1) / std::max<int64_t>(1, share) + 1);
+    p.kps = k_iters;
+  }
   const size_t partials = (size_t)tiles * p.splits * 128 * bn * sizeof(float);
   if (g_plan) g_plan->workspace_bytes = p.splits > 1 ? (int64_t)splitk_bytes(partials, tiles) : 0;
-  int grid = (int)std::min<int64_t>(tiles * p.splits, sms);
+  int grid = p.stream_k ? (int)std::min<int64_t>(sms, tiles * k_iters)
+                        : (int)std::min<int64_t>(tiles * p.splits, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
   // Resident weights (im2col: knob stages 1 streamed, 2 resident, 0 =
   // resident when they fit): every B tile of the CTA's output-channel tile
@@ -1284,7 +1301,7 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   // multiple of the N tiles.
   if (!halo) {
     const int res_fixed = conv_f32tc_smem_bytes(bn, swz, inter, true, false);
-    res = want_res != 1 && p.splits == 1 && res_fixed > 0 &&
+    res = want_res != 1 && p.splits == 1 && !p.stream_k && res_fixed > 0 &&
           res_fixed + res_bytes <= kBudget && grid >= p.n_tiles;
     if (want_res == 2 && !res)
       return fail(TEC_E_LOWERING, "f32tc: resident weights do not fit (or split-K is on)");

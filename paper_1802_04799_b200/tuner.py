@@ -224,10 +224,11 @@ def conv_space(name: str, desc: _abi.ConvDesc,
         resident weights), split_k (im2col: K split over CTAs, partials
         summed in order), cluster_n (halo, streamed weights: CTA pairs share
         weight tiles by TMA multicast);
-      f32tc: tile_n and split_k of the split-bf16 f32 kernel."""
+      f32tc: tile_k, tile_n, stages (resident weights) and split_k of the
+        split-bf16 f32 kernel (split_k = -1: stream-K, equal (tile, k) shares)."""
     if desc.compute == _abi.COMPUTE_F32TC:
         knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128]),
-                 KnobDef("stages", [1, 2]), KnobDef("split_k", [1, 2, 3, 4, 6, 8])]
+                 KnobDef("stages", [1, 2]), KnobDef("split_k", [1, 2, 3, 4, 6, 8, -1])]
     else:
         knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
                  KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2]),

@@ -417,6 +417,30 @@ def test_split_k_scratch_shared_across_shapes():
             assert same_values(y, want, tol), (layer, sk, compute, max_rel_err(y, want))
 
 
+@pytest.mark.parametrize("case,batch", [("C7", 2), ("C12", 2), ("C12", 9), ("C6", 1), ("odd5x5", 3)])
+def test_f32tc_stream_k(case, batch):
+    """split_k = -1 (stream-K): every CTA takes an equal share of the
+    flattened (tile, k-iteration) work, tiles cut by share boundaries are
+    finished by their last segment in segment order. Batches chosen so the
+    work is smaller than, about equal to and larger than one share per SM."""
+    if case == "odd5x5":
+        shape_x, shape_w, s, pad = (batch, 64, 11, 13), (64, 64, 5, 5), 1, 2
+    else:
+        hw, c, k, r, s = RESNET18_CONVS[case]
+        shape_x, shape_w, pad = (batch, c, hw, hw), (k, c, r, r), r // 2
+    x, w, b = _inputs(shape_x, shape_w, shape_w[0], False, 23)
+    attrs = {"strides": (s, s), "padding": (pad, pad)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc",
+                   knobs={"tile_k": 1, "tile_n": 128, "split_k": -1})
+    want = oracle_conv("conv2d", x, w, (s, s), (pad, pad), epi)
+    assert same_values(y, want, TOL_F32TC), f"max rel err {max_rel_err(y, want)}"
+    # deterministic: a second launch gives the same bytes
+    y2 = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc",
+                    knobs={"tile_k": 1, "tile_n": 128, "split_k": -1})
+    assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
+
+
 @pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("case", ["C1", "C2", "C6", "C9", "odd5x5", "odd_res", "stem30", "stem46"])
 def test_f32tc_im2col_and_shifted_window(case, path):
