@@ -7,7 +7,7 @@
 #include "sm100_ptx.cuh"
 using namespace tec_sm100;
 
-template <int N, int SWZ, int NACC = 1, int M = 128>
+template <int N, int SWZ, int NACC = 1, int M = 128, MmaKind KIND = MmaKind::kF16>
 __global__ void __launch_bounds__(128, 1) k(int iters, int shift_rows, long long* cyc) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int shift_rows, long long
   tc_fence_before(); __syncthreads(); tc_fence_after();
   uint32_t tmem = *slot;
   if (threadIdx.x == 0) {
-    uint32_t idesc = make_idesc<MmaKind::kF16>(M, N);
+    uint32_t idesc = make_idesc<KIND>(M, N);
     long long t0 = clock64();
     uint32_t a0 = smem_u32(sA) + shift_rows * 128, b0 = smem_u32(sB);
     for (int it = 0; it < iters; ++it) {
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int shift_rows, long long
                                  : make_smem_desc<SWZ>(a0 + (it & 1) * 16384 + kk * 128 * SWZ, 8 * SWZ);
         uint64_t bd = SWZ == 128 ? make_smem_desc<128>(b0 + kk * 32, 1024)
                                  : make_smem_desc<SWZ>(b0 + kk * 256 * SWZ, 8 * SWZ);
-        tc_mma<MmaKind::kF16>(tmem + (NACC > 1 ? (kk % NACC) * N : 0), ad, bd, idesc, 1);
+        tc_mma<KIND>(tmem + (NACC > 1 ? (kk % NACC) * N : 0), ad, bd, idesc, 1);
       }
     }
     tc_commit(bar);
@@ -46,10 +46,10 @@ __global__ void __launch_bounds__(128, 1) k(int iters, int shift_rows, long long
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-template <int N, int SWZ = 128, int NACC = 1, int M = 128>
+template <int N, int SWZ = 128, int NACC = 1, int M = 128, MmaKind KIND = MmaKind::kF16>
 void run(int shift) {
   long long* d; cudaMalloc(&d, 148 * 8);
-  auto f = k<N, SWZ, NACC, M>;
+  auto f = k<N, SWZ, NACC, M, KIND>;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 110000);
   int iters = 4000;
   f<<<148, 128, 110000>>>(iters, shift, d);
@@ -59,13 +59,17 @@ void run(int shift) {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   long long h[148]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-  double flops = 2.0 * M * N * 16 * 4 * (double)iters * 148;
-  printf("M=%d N=%3d shift=%d SWZ=%d NACC=%d: %.1f cycles/MMA (ideal %d), %.0f TFLOP/s\n", M, N, shift,
-         SWZ, NACC, (double)h[0] / (iters * 4), M * N / 256, flops / (ms * 1e-3) / 1e12);
+  const int kdim = KIND == MmaKind::kI8 ? 32 : 16;  // 32 bytes of K per MMA either way
+  double flops = 2.0 * M * N * kdim * 4 * (double)iters * 148;
+  printf("%s M=%d N=%3d shift=%d SWZ=%d NACC=%d: %.1f cycles/MMA (ideal %d), %.0f T(FL)OP/s\n",
+         KIND == MmaKind::kI8 ? "i8  " : "bf16", M, N, shift, SWZ, NACC, (double)h[0] / (iters * 4),
+         KIND == MmaKind::kI8 ? M * N / 512 : M * N / 256, flops / (ms * 1e-3) / 1e12);
   cudaFree(d);
 }
 
 int main() {
+  run<64, 128, 1, 128, MmaKind::kI8>(0); run<128, 128, 1, 128, MmaKind::kI8>(0);
+  run<256, 128, 1, 128, MmaKind::kI8>(0);
   run<64, 128, 1>(0); run<128, 128, 1>(0); run<256, 128, 1>(0);
   run<64, 128, 1, 64>(0); run<128, 128, 1, 64>(0); run<256, 128, 1, 64>(0); run<256, 128, 2, 64>(0);
   return 0;
