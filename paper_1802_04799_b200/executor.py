@@ -565,6 +565,10 @@ class DeviceGraph:
             else:
                 r = side_dst.get(other) or self.tensors[other]
                 want_dt = lay.acc_dtype if self.compute == "i8" else out_dt
+                if r.layout == "nchw" and r.dtype != _abi.DT_I8:
+                    # a graph input (the reference's NCHW) as the shortcut:
+                    # one relayout launch into the conv output's NHWC / dtype
+                    r = self._to_nhwc(r, want_dt)
                 if r.layout != "nhwc" or r.dtype != want_dt:
                     raise TecError(E_LOWERING, f"'{op}' operand must be an NHWC {out_dt} tensor")
                 if op == "add":

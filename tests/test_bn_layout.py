@@ -153,3 +153,37 @@ def test_executor_runs_batch_norm_graphs(compute):
         want = graph_oracle.evaluate(folded, feeds, vals, "bf16")["bn2"]
         rel = np.linalg.norm(got - want) / np.linalg.norm(want)
         assert rel < 3e-2, rel
+
+
+@pytest.mark.gpu
+def test_executor_bn_resnet_block_f32():
+    """conv -> batch_norm -> relu -> conv -> batch_norm -> add(shortcut) -> relu,
+    the residual block the way frameworks export it: folded on the device,
+    bit-identical in f32 to the oracle evaluation of the folded graph."""
+    from paper_1802_04799_b200.executor import DeviceGraph
+    rng = np.random.default_rng(8)
+    c = 32
+    vals = {"w1": (rng.standard_normal((c, c, 3, 3)) * 0.1).astype(np.float32),
+            "w2": (rng.standard_normal((c, c, 3, 3)) * 0.1).astype(np.float32)}
+    nodes = [GraphNode("x", "input", out_type=TensorType([2, c, 12, 12], "f32"))]
+    for name in ("w1", "w2"):
+        nodes.append(GraphNode(name, "input", out_type=TensorType([c, c, 3, 3], "f32")))
+    for j in (1, 2):
+        for nm, lo, hi in (("g", 0.5, 1.5), ("be", -0.2, 0.2), ("mu", -0.3, 0.3), ("var", 0.2, 2.0)):
+            vals[f"{nm}{j}"] = rng.uniform(lo, hi, c).astype(np.float32)
+            nodes.append(GraphNode(f"{nm}{j}", "input", out_type=TensorType([c], "f32")))
+    nodes += [GraphNode("c1", "conv2d", ["x", "w1"], {"padding": [1, 1]}),
+              GraphNode("bn1", "batch_norm", ["c1", "g1", "be1", "mu1", "var1"]),
+              GraphNode("r1", "relu", ["bn1"]),
+              GraphNode("c2", "conv2d", ["r1", "w2"], {"padding": [1, 1]}),
+              GraphNode("bn2", "batch_norm", ["c2", "g2", "be2", "mu2", "var2"]),
+              GraphNode("a", "add", ["bn2", "x"]),
+              GraphNode("r2", "relu", ["a"])]
+    g = ComputeGraph(nodes, ["r2"])
+    g.validate()
+    feeds = {"x": rng.uniform(-1, 1, (2, c, 12, 12)).astype(np.float32)}
+    dg = DeviceGraph(g, compute="f32")
+    dg.bind_params(vals)
+    got = dg.run(feeds)["r2"]
+    want = graph_oracle.evaluate(fuse_pass(fold_batch_norm(g)), feeds, vals, "f32")["r2"]
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

@@ -239,6 +239,42 @@ def test_int8_block_fused_and_unfused_lowerings(k, shortcut):
 
 
 @pytest.mark.gpu
+def test_int8_depthwise_block():
+    """A MobileNet-style int8 block: depthwise 3x3 + bias + relu + requantize
+    (the depthwise kernels take no requantize epilogue: the tail runs as an
+    elementwise launch) -> pointwise 1x1 + bias + relu + requantize (fused)."""
+    from paper_1802_04799_b200.executor import DeviceGraph
+    rng = np.random.default_rng(11)
+    c, k = 64, 96
+    nodes = [GraphNode("x", "input", out_type=TensorType([2, c, 14, 14], "i8")),
+             GraphNode("wd", "input", out_type=TensorType([c, 1, 3, 3], "i8")),
+             GraphNode("bd", "input", out_type=TensorType([c], "i32")),
+             GraphNode("wp", "input", out_type=TensorType([k, c, 1, 1], "i8")),
+             GraphNode("bp", "input", out_type=TensorType([k], "i32")),
+             GraphNode("d", "depthwise_conv2d", ["x", "wd"], {"padding": [1, 1]}),
+             GraphNode("db", "bias_add", ["d", "bd"]),
+             GraphNode("dr", "relu", ["db"]),
+             GraphNode("dq", "requantize", ["dr"], {"multiplier": 1500, "shift": 12}),
+             GraphNode("p", "conv2d", ["dq", "wp"]),
+             GraphNode("pb", "bias_add", ["p", "bp"]),
+             GraphNode("pr", "relu", ["pb"]),
+             GraphNode("pq", "requantize", ["pr"], {"multiplier": 700, "shift": 14})]
+    g = ComputeGraph(nodes, ["pq"])
+    g.validate()
+    feeds = {"x": rng.integers(-50, 51, (2, c, 14, 14), dtype=np.int8)}
+    params = {"wd": rng.integers(-8, 9, (c, 1, 3, 3), dtype=np.int8),
+              "bd": rng.integers(-200, 201, (c,), dtype=np.int32),
+              "wp": rng.integers(-8, 9, (k, c, 1, 1), dtype=np.int8),
+              "bp": rng.integers(-200, 201, (k,), dtype=np.int32)}
+    dg = DeviceGraph(g, compute="i8")
+    dg.bind_params(params)
+    got = dg.run(feeds)["pq"]
+    want = graph_oracle.evaluate(fuse_pass(g), feeds, params, "i8")["pq"]
+    assert np.array_equal(got, want)
+    assert 0 < (got == 0).mean() < 1
+
+
+@pytest.mark.gpu
 def test_max_pool2d_i8_kernel():
     """tec_max_pool2d on i8 NHWC (the int8 stem pool, SIMD byte max):
     all-negative values, so a padded tap winning would show as 0."""
