@@ -441,6 +441,23 @@ def test_f32tc_stream_k(case, batch):
     assert np.array_equal(y.view(np.uint32), y2.view(np.uint32))
 
 
+@pytest.mark.parametrize("split", [-1, 2])
+def test_f32tc_split_and_stream_k_with_residual(split):
+    """The segment finisher runs the whole member program: bias + add
+    (shortcut) + relu after the partial sums (C7 shape, batch 3)."""
+    hw, c, k, r, s = RESNET18_CONVS["C7"]
+    shape_x, shape_w, pad = (3, c, hw, hw), (k, c, r, r), r // 2
+    x, w, b = _inputs(shape_x, shape_w, k, False, 29)
+    oh = (hw + 2 * pad - r) // s + 1
+    res = np.random.default_rng(30).uniform(-1, 1, (3, k, oh, oh)).astype(np.float32)
+    attrs = {"strides": (s, s), "padding": (pad, pad)}
+    epi = [("bias_add", b), ("add", res), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc",
+                   knobs={"tile_k": 1, "tile_n": 128, "split_k": split})
+    want = oracle_conv("conv2d", x, w, (s, s), (pad, pad), epi)
+    assert same_values(y, want, TOL_F32TC), f"max rel err {max_rel_err(y, want)}"
+
+
 @pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("case", ["C1", "C2", "C6", "C9", "odd5x5", "odd_res", "stem30", "stem46"])
 def test_f32tc_im2col_and_shifted_window(case, path):
