@@ -598,6 +598,11 @@ __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane
     const uint32_t m = static_cast<uint32_t>(qp.mult);  // 1 <= m < 2^31 (host-checked)
     const int sh = qp.shift;
     const uint64_t half = sh > 0 ? (uint64_t(1) << (sh - 1)) : 0u;
+    // requantize of x >= 0 as one 32 x 32 high product when m < 2^sh <= 2^32:
+    // (x*m + 2^(sh-1)) >> sh == hi32(x * m' + 2^31) with m' = m << (32 - sh),
+    // exact (x < 2^31, m' < 2^32); the carry of the low half adds the rounding
+    const bool hi_form = sh >= 1 && sh <= 32 && (static_cast<uint64_t>(m) >> sh) == 0;
+    const uint32_t mp = hi_form ? static_cast<uint32_t>(static_cast<uint64_t>(m) << (32 - sh)) : 0u;
     const int32_t rs = static_cast<int32_t>(qp.res_scale);  // |rs| <= 2^24: r * rs fits i32
     uint32_t w[kChunk / 4];
 #pragma unroll
@@ -615,10 +620,17 @@ __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane
       }
       uint32_t q;
       if constexpr (PROG != kProgBiasQ) {
-        // after relu x >= 0: an unsigned 32 x 32 -> 64 product
-        const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(x < 0 ? 0 : x)) * m + half;
-        const uint64_t v = t >> sh;
-        q = v > 127u ? 127u : static_cast<uint32_t>(v);
+        // after relu x >= 0
+        const uint32_t xu = static_cast<uint32_t>(x < 0 ? 0 : x);
+        if (hi_form) {
+          const uint32_t lo = xu * mp;
+          const uint32_t v = __umulhi(xu, mp) + (lo >> 31);
+          q = v > 127u ? 127u : v;
+        } else {  // an unsigned 32 x 32 -> 64 product
+          const uint64_t t = static_cast<uint64_t>(xu) * m + half;
+          const uint64_t v = t >> sh;
+          q = v > 127u ? 127u : static_cast<uint32_t>(v);
+        }
       } else {
         const int64_t t = static_cast<int64_t>(x) * static_cast<int64_t>(static_cast<int32_t>(m)) +
                           static_cast<int64_t>(half);
@@ -639,18 +651,24 @@ __device__ __forceinline__ void epi_acc_to_box(uint32_t (&acc)[kChunk], int lane
   if constexpr (kInt) {
     static_assert(ES == 4 || PROG == kProgBiasReluQ || PROG == kProgBiasAddReluQ || PROG == kProgBiasQ,
                   "int8 conv stores i32 (i8 only through the Q programs above)");
-    bool bad = false;
+    // 32-bit adds with an explicit signed-overflow bit, (a ^ s) & (b ^ s) < 0
+    // (the int64 form costs ~2x the instructions in an issue-bound epilogue)
+    uint32_t bits = 0u;
 #pragma unroll
     for (int j = 0; j < kChunk; ++j) {
-      int64_t x = static_cast<int32_t>(acc[j]);
+      uint32_t x = acc[j];
       if constexpr (PROG != kProgNone) {
-        x += static_cast<int32_t>(b[j]);
-        bad |= x < INT32_MIN || x > INT32_MAX;
+        const uint32_t a = acc[j];
+        x = a + b[j];
+        bits |= (a ^ x) & (b[j] ^ x);
       }
-      if constexpr (PROG == kProgBiasRelu) x = x < 0 ? 0 : x;
-      acc[j] = static_cast<uint32_t>(static_cast<int32_t>(x));
+      if constexpr (PROG == kProgBiasRelu) {
+        const int32_t xi = static_cast<int32_t>(x);
+        x = static_cast<uint32_t>(xi < 0 ? 0 : xi);
+      }
+      acc[j] = x;
     }
-    if (bad && ovf) *ovf = true;
+    if ((bits >> 31) && ovf) *ovf = true;
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       sts128(box + box_off<4>(lane, c),

@@ -239,6 +239,34 @@ def test_int8_block_fused_and_unfused_lowerings(k, shortcut):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mult,shift", [(911, 16), (2 ** 31 - 1, 40), (5, 1), (1, 0), (3, 32)])
+def test_int8_requantize_epilogue_parameters(mult, shift):
+    """The fused requantize (Q epilogue) for multiplier / shift pairs on both
+    sides of its fast form (m < 2^shift <= 2^32: one 32x32 high product)."""
+    from paper_1802_04799_b200.executor import DeviceGraph
+    rng = np.random.default_rng(mult % 97 + shift)
+    k = 64
+    nodes = [GraphNode("x", "input", out_type=TensorType([2, k, 10, 10], "i8")),
+             GraphNode("w", "input", out_type=TensorType([k, k, 3, 3], "i8")),
+             GraphNode("b", "input", out_type=TensorType([k], "i32")),
+             GraphNode("c", "conv2d", ["x", "w"], {"padding": [1, 1]}),
+             GraphNode("cb", "bias_add", ["c", "b"]),
+             GraphNode("r", "relu", ["cb"]),
+             GraphNode("q", "requantize", ["r"], {"multiplier": mult, "shift": shift})]
+    g = ComputeGraph(nodes, ["q"])
+    g.validate()
+    feeds = {"x": rng.integers(-60, 61, (2, k, 10, 10), dtype=np.int8)}
+    params = {"w": rng.integers(-8, 9, (k, k, 3, 3), dtype=np.int8),
+              "b": rng.integers(-2000, 2001, (k,), dtype=np.int32)}
+    dg = DeviceGraph(g, compute="i8")
+    dg.bind_params(params)
+    assert sum(1 for st in dg.steps if st.kind == _abi.STEP_ELEMWISE) == 0  # fused
+    got = dg.run(feeds)["q"]
+    want = graph_oracle.evaluate(fuse_pass(g), feeds, params, "i8")["q"]
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
 def test_int8_depthwise_block():
     """A MobileNet-style int8 block: depthwise 3x3 + bias + relu + requantize
     (the depthwise kernels take no requantize epilogue: the tail runs as an
