@@ -45,10 +45,11 @@ constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kEpiThreads = 256;
 using epi::kChunk;
 
-template <MmaKind KIND, int BN, int STAGES, int SWZ>
+template <MmaKind KIND, int BN, int STAGES, int SWZ, bool PAIR = false>
 struct ConvCfg {
   static constexpr int kABytes = kBM * SWZ;  // one stage of A
-  static constexpr int kBBytes = BN * SWZ;   // one stage of B
+  // one stage of B (a CTA of a pair holds half of the tile's weight rows)
+  static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * SWZ;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kMmaPerStage = SWZ / 32;  // each MMA eats 32 B of K
   // TMEM accumulator ring: 4 buffers when they fit (knob acc_bufs), else 2
@@ -64,13 +65,13 @@ struct ConvCfg {
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 };
 
-template <MmaKind KIND, int BN, int STAGES, int SWZ>
+template <MmaKind KIND, int BN, int STAGES, int SWZ, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fprop_tc_kernel(const __grid_constant__ CUtensorMap tm_a,
                          const __grid_constant__ CUtensorMap tm_b,
                          const __grid_constant__ CUtensorMap tm_y,
                          const ConvGemmParams p) {
-  using Cfg = ConvCfg<KIND, BN, STAGES, SWZ>;
+  using Cfg = ConvCfg<KIND, BN, STAGES, SWZ, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -100,6 +101,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long t_start = p.dbg ? clock64() : 0;
   constexpr int kCB =
       SWZ / (KIND == MmaKind::kF16 ? 2 : KIND == MmaKind::kTF32 ? 4 : 1);
+  // CTA pair (PAIR, cta_group::2, cluster of 2): the pair computes a 256-row
+  // M tile -- rows [0,128) in the leader's TMEM from its A, [128,256) in the
+  // peer's -- with one MMA stream issued by the leader; each CTA loads its
+  // own A rows and HALF of the BN weight rows, so a CTA's shared memory
+  // feeds the tensor cores A + B/2 per K step instead of A + B. Both CTAs'
+  // TMA bytes complete on the leader's full barrier, the leader's commits
+  // release both CTAs' stages and accumulators, and the peer's epilogue
+  // hands its accumulator back through the leader's tempty barrier. Work
+  // unit u = (M-tile pair, N tile); splits == 1.
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int t_first = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int t_step = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const int t_count = PAIR ? ((p.m_tiles + 1) / 2) * p.n_tiles : num_tiles;
+  auto tile_of = [&](int u) -> int {  // work unit -> this CTA's tile index
+    if constexpr (!PAIR) return u;
+    const int mp = u / p.n_tiles;
+    return (2 * mp + static_cast<int>(rank)) * p.n_tiles + (u - mp * p.n_tiles);
+  };
+  constexpr uint32_t kStageTx = PAIR ? 2 * Cfg::kStageBytes : Cfg::kStageBytes;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_a);
@@ -111,13 +131,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);  // the epilogue group (4 warps) of the accumulator
+      // the epilogue group (4 warps) of the accumulator; a pair: both CTAs'
+      mbar_init(&tempty[i], PAIR ? 256 : 128);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // barriers initialised in both CTAs
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Prologue done: let the next layer launch. Only the producer waits for
@@ -130,27 +155,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ TMA producer warp
     if (elect_one()) {
       int pre = 0;  // stages whose B box went out before the wait
-      if (static_cast<int>(blockIdx.x) < num_tiles) {
-        const int mn = static_cast<int>(blockIdx.x) / splits;
+      // the full barrier the loads complete on: the leader's for a pair
+      const uint32_t full_l = PAIR ? mapa_u32(smem_u32(full), 0) : 0u;
+      const int b_row = PAIR ? static_cast<int>(rank) * (BN / 2) : 0;
+      auto load_b = [&](int st, int kcol, int n_tile) {
+        if constexpr (PAIR)
+          tma_load_2d_pair(sB + st * Cfg::kBBytes, &tm_b, full_l + 8 * st, kcol, n_tile * BN + b_row);
+        else
+          tma_load_2d(sB + st * Cfg::kBBytes, &tm_b, &full[st], kcol, n_tile * BN);
+      };
+      if (t_first < t_count) {
+        const int t0 = tile_of(t_first);
+        const int mn = t0 / splits;
         const int n_tile0 = mn % p.n_tiles;
-        const int kb = (static_cast<int>(blockIdx.x) - mn * splits) * kps;
+        const int kb = (t0 - mn * splits) * kps;
         const int ke = min(k_iters, kb + kps);
         for (int k = kb; k < ke && pre < STAGES; ++k, ++pre) {
-          mbar_arrive_expect_tx(&full[pre], Cfg::kStageBytes);
+          if (!PAIR || rank == 0) mbar_arrive_expect_tx(&full[pre], kStageTx);
           // k = (r * S + s) * cblocks + cb -> weight column k * kCB
-          tma_load_2d(sB + pre * Cfg::kBBytes, &tm_b, &full[pre], k * kCB, n_tile0 * BN);
+          load_b(pre, k * kCB, n_tile0);
         }
       }
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       const int ohw = p.oh * p.ow;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int u = t_first; u < t_count; u += t_step) {
+        const int tile = tile_of(u);
         const int mn = tile / splits;
         const int split = tile - mn * splits;
         const int m_tile = mn / p.n_tiles;
         const int n_tile = mn - m_tile * p.n_tiles;
-        const int m0 = m_tile * kBM;
+        // a pair's phantom tile (odd m_tiles) reads its partner's rows
+        const int m0 = min(m_tile, p.m_tiles - 1) * kBM;
         const int img = m0 / ohw;
         const int rem = m0 - img * ohw;
         const int oh = rem / p.ow;
@@ -162,23 +199,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         int r = kb / sc, rem_k = kb - r * sc;
         int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
         for (int k = kb; k < ke; ++k) {
+          auto load_a = [&]() {
+            if constexpr (PAIR)
+              tma_load_im2col_4d_pair(sA + stage * Cfg::kABytes, &tm_a, full_l + 8 * stage,
+                                      cb * kCB, w0, h0, img, static_cast<uint16_t>(s),
+                                      static_cast<uint16_t>(r));
+            else
+              tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a, &full[stage], cb * kCB, w0,
+                                 h0, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+          };
           if (pre > 0) {  // B already in flight, the stage known free
             --pre;
-            tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a,
-                               &full[stage], cb * kCB, w0, h0, img,
-                               static_cast<uint16_t>(s),
-                               static_cast<uint16_t>(r));
+            load_a();
           } else {
           { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&empty[stage], phase ^ 1);
             if (p.dbg) dbg_wait[0] += clock64() - t0; }
-          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          tma_load_im2col_4d(sA + stage * Cfg::kABytes, &tm_a,
-                             &full[stage], cb * kCB, w0, h0, img,
-                             static_cast<uint16_t>(s),
-                             static_cast<uint16_t>(r));
-          tma_load_2d(sB + stage * Cfg::kBBytes, &tm_b, &full[stage],
-                      (r * p.s + s) * p.cp + cb * kCB, n_tile * BN);
+          if (!PAIR || rank == 0) mbar_arrive_expect_tx(&full[stage], kStageTx);
+          load_a();
+          load_b(stage, (r * p.s + s) * p.cp + cb * kCB, n_tile);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -191,10 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && (!PAIR || rank == 0)) {
     // ------------------------------------------ single-thread MMA issuer
     if (elect_one()) {
-      constexpr uint32_t idesc = make_idesc<KIND>(kBM, BN);
+      constexpr uint32_t idesc = make_idesc<KIND>(PAIR ? 2 * kBM : kBM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -210,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool dbg = p.dbg != nullptr;
       int split = static_cast<int>(blockIdx.x) % nsplit;
       const int dsplit = static_cast<int>(gridDim.x) % nsplit;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++local) {
+      (void)ntiles;
+      for (int u = t_first; u < t_count; u += t_step, ++local) {
         const int acc = local & (nacc - 1);
         const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
         { const long long t0 = dbg ? clock64() : 0;
@@ -229,16 +269,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t ad = adesc0 + static_cast<uint64_t>(stage * (Cfg::kABytes >> 4));
           const uint64_t bd = bdesc0 + static_cast<uint64_t>(stage * (Cfg::kBBytes >> 4));
 #pragma unroll
-          for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk)
-            tc_mma<KIND>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,  // K slice kk: +32 B
-                         (k != kb || kk != 0) ? 1u : 0u);
-          tc_commit(&empty[stage]);  // frees the smem slot when MMAs land
+          for (int kk = 0; kk < Cfg::kMmaPerStage; ++kk) {
+            if constexpr (PAIR)
+              tc_mma_pair<KIND>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,
+                                (k != kb || kk != 0) ? 1u : 0u);
+            else
+              tc_mma<KIND>(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc,  // K slice kk: +32 B
+                           (k != kb || kk != 0) ? 1u : 0u);
+          }
+          // frees the smem slot (both CTAs' for a pair) when the MMAs land
+          if constexpr (PAIR) tc_commit_pair(&empty[stage], 3);
+          else tc_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue (both CTAs' for a pair)
+        if constexpr (PAIR) tc_commit_pair(&tfull[acc], 3);
+        else tc_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -262,8 +311,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     int staged_n_tile = -1;
     bool overflow = false;
-    for (int tile = blockIdx.x; tile < num_tiles;
-         tile += gridDim.x, ++local) {
+    // hand the accumulator back: the peer of a pair arrives on the leader's
+    const uint32_t tempty_l = PAIR ? mapa_u32(smem_u32(tempty), 0) : 0u;
+    auto release_acc = [&](int a) {
+      if constexpr (PAIR) {
+        if (rank != 0) {
+          mbar_arrive_cluster(tempty_l + 8 * a);
+          return;
+        }
+      }
+      mbar_arrive(&tempty[a]);
+    };
+    for (int u = t_first; u < t_count; u += t_step, ++local) {
+      const int tile = tile_of(u);
       if ((local & 1) != grp) continue;
       const int acc = local & (nacc - 1);
       const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
@@ -289,6 +349,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tw1 = p.dbg ? clock64() : 0;
       if (p.dbg) dbg_wait[3] += tw1 - tw0;
       tc_fence_after();
+      if (PAIR && m_tile >= p.m_tiles) {  // a pair's phantom tile: nothing to store
+        tc_fence_before();
+        release_acc(acc);
+        continue;
+      }
       if (splits > 1 && tma_epi) {
         // ---- split-K: publish this split's f32 partial tile, then the last
         // split of the tile (arrival counter) sums all partials IN SPLIT
@@ -306,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < kChunk; ++j) __stcg(mine + (c0 + j) * 32, __uint_as_float(v[j]));
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);  // TMEM free: the partial lives in ws now
+        release_acc(acc);  // TMEM free: the partial lives in ws now
         __threadfence();
         epi::named_bar_sync(1 + grp, 128);
         if (gtid == 0) s_last[grp] = atomicAdd(&p.tile_cnt[mn], 1) == splits - 1;
@@ -405,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else run(P2{}, E4{});
           }
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          release_acc(acc);
           if (p.dbg) dbg_wait[4] += clock64() - tw1;
           continue;
         }
@@ -431,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // All of this thread's TMEM reads of the accumulator are complete
       // (each block waited on tcgen05.ld): hand it back to the MMA warp.
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      release_acc(acc);
       if (p.dbg) dbg_wait[4] += clock64() - tw1;
     }
     if (lane == 0) bulk_wait_all();  // TMA stores done before smem goes away
@@ -439,9 +504,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // no DSMEM traffic may target an exited CTA
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<ConvCfg<KIND, BN, STAGES, SWZ>::kTmemCols>(tmem_base);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+    else tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
   if (p.dbg) {
     // one representative thread per role: producer / MMA lane 0 of warps
     // 0 / 1, and epilogue thread 0 (its waits are typical of the group).
@@ -460,22 +529,31 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Launch wrapper, instantiated for the supported (kind, BN, swizzle) set.
 // Returns a cudaError_t.
-template <MmaKind KIND, int BN, int STAGES, int SWZ>
+// PAIR: grid even, launched in clusters of 2 (the CTA pairs).
+template <MmaKind KIND, int BN, int STAGES, int SWZ, bool PAIR>
 int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
                          const CUtensorMap& tm_y, const ConvGemmParams& p, int grid,
                          cudaStream_t stream) {
-  using Cfg = ConvCfg<KIND, BN, STAGES, SWZ>;
-  auto kfn = conv_fprop_tc_kernel<KIND, BN, STAGES, SWZ>;
+  using Cfg = ConvCfg<KIND, BN, STAGES, SWZ, PAIR>;
+  auto kfn = conv_fprop_tc_kernel<KIND, BN, STAGES, SWZ, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(
       kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, tm_a, tm_b, tm_y, p);
+  if constexpr (PAIR)
+    e = launch_pdl_cluster(kfn, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, 2, tm_a,
+                           tm_b, tm_y, p);
+  else
+    e = launch_pdl(kfn, dim3(grid), dim3(kThreads), Cfg::kSmemBytes, stream, tm_a, tm_b, tm_y, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 #define TEC_INST(KIND, BN, ST, SWZ)                                         \
-  template int launch_conv_fprop_tc<KIND, BN, ST, SWZ>(                    \
+  template int launch_conv_fprop_tc<KIND, BN, ST, SWZ, false>(             \
+      const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,          \
+      const ConvGemmParams&, int, cudaStream_t);
+#define TEC_INST_PAIR(KIND, BN, ST, SWZ)                                    \
+  template int launch_conv_fprop_tc<KIND, BN, ST, SWZ, true>(              \
       const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,          \
       const ConvGemmParams&, int, cudaStream_t);
 
@@ -492,7 +570,18 @@ TEC_INST(MmaKind::kI8, 256, 3, 128)
 TEC_INST(MmaKind::kI8, 64, 8, 64)
 TEC_INST(MmaKind::kI8, 128, 6, 64)
 TEC_INST(MmaKind::kI8, 64, 8, 32)
+// CTA pairs (knob cluster_n = 2 on the im2col path)
+// (the half-size weight stages buy deeper rings in the same shared memory)
+TEC_INST_PAIR(MmaKind::kF16, 64, 9, 128)
+TEC_INST_PAIR(MmaKind::kF16, 128, 8, 128)
+TEC_INST_PAIR(MmaKind::kF16, 256, 5, 128)
+TEC_INST_PAIR(MmaKind::kI8, 64, 9, 128)
+TEC_INST_PAIR(MmaKind::kI8, 128, 8, 128)
+TEC_INST_PAIR(MmaKind::kI8, 256, 5, 128)
+TEC_INST_PAIR(MmaKind::kI8, 64, 9, 64)
+TEC_INST_PAIR(MmaKind::kI8, 128, 8, 64)
 
 #undef TEC_INST
+#undef TEC_INST_PAIR
 
 }  // namespace tec_sm100

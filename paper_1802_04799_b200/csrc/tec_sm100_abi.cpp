@@ -26,7 +26,7 @@
 #include "sm100_ptx.cuh"
 
 namespace tec_sm100 {
-template <MmaKind KIND, int BN, int STAGES, int SWZ>
+template <MmaKind KIND, int BN, int STAGES, int SWZ, bool PAIR>
 int launch_conv_fprop_tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b,
                          const CUtensorMap& tm_y, const ConvGemmParams& p, int grid,
                          cudaStream_t stream);
@@ -505,9 +505,21 @@ int sm_count(int dev) {
 using Launcher = int (*)(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                          const ConvGemmParams&, int, cudaStream_t);
 
-Launcher pick_launcher(MmaKind kind, int bn, int swz) {
+Launcher pick_launcher(MmaKind kind, int bn, int swz, bool pair = false) {
+#define TEC_CASE_PAIR(K, BN, ST, SW) \
+  if (pair && kind == K && bn == BN && swz == SW) return &launch_conv_fprop_tc<K, BN, ST, SW, true>;
+  TEC_CASE_PAIR(MmaKind::kF16, 64, 9, 128)
+  TEC_CASE_PAIR(MmaKind::kF16, 128, 8, 128)
+  TEC_CASE_PAIR(MmaKind::kF16, 256, 5, 128)
+  TEC_CASE_PAIR(MmaKind::kI8, 64, 9, 128)
+  TEC_CASE_PAIR(MmaKind::kI8, 128, 8, 128)
+  TEC_CASE_PAIR(MmaKind::kI8, 256, 5, 128)
+  TEC_CASE_PAIR(MmaKind::kI8, 64, 9, 64)
+  TEC_CASE_PAIR(MmaKind::kI8, 128, 8, 64)
+#undef TEC_CASE_PAIR
+  if (pair) return nullptr;
 #define TEC_CASE(K, BN, ST, SW) \
-  if (kind == K && bn == BN && swz == SW) return &launch_conv_fprop_tc<K, BN, ST, SW>;
+  if (kind == K && bn == BN && swz == SW) return &launch_conv_fprop_tc<K, BN, ST, SW, false>;
   TEC_CASE(MmaKind::kF16, 64, 8, 128)
   TEC_CASE(MmaKind::kF16, 128, 6, 128)
   TEC_CASE(MmaKind::kF16, 256, 3, 128)
@@ -883,8 +895,10 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   // TMA (conv_tc.cu), 2 shifted-window halo (conv_halo.cu, stride 1 only),
   // 4 halo with paired filter taps (N=128 MMAs, conv_halo.cu kPair).
   const int64_t path = kn ? kn->tile_k : 0;
-  if (path == 1 && kn && kn->cluster_n > 1)
-    return fail(TEC_E_LOWERING, "cluster_n (weight multicast) applies to the halo path");
+  // knob cluster_n on the im2col path: 2 = CTA pairs (cta_group::2, M = 256,
+  // each CTA loading half the weight rows); the halo path multicasts weights
+  if (path == 1 && kn && kn->cluster_n > 2)
+    return fail(TEC_E_LOWERING, "cluster_n on the im2col path is 1 or 2 (CTA pair)");
   if ((path == 2 || path == 4) && kn && kn->split_k > 1)
     return fail(TEC_E_LOWERING, "split_k applies to the im2col path (tile_k=1)");
   if (path != 1 && !(kn && kn->split_k > 1)) {
@@ -907,11 +921,13 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     if (pl.swz != 128) bn = 64;
     while (bn > 64 && m_tiles * ((d->k + bn - 1) / bn) * 5 < 3 * sms) bn /= 2;
   }
-  Launcher launch = pick_launcher(pl.kind, bn, pl.swz);
+  const bool pair = kn && kn->cluster_n == 2;
+  Launcher launch = pick_launcher(pl.kind, bn, pl.swz, pair);
   if (!launch)
     return fail(TEC_E_LOWERING, "no sm100 conv instance for tile_n=" +
                                     std::to_string(bn) + " block=" +
-                                    std::to_string(pl.swz) + "B");
+                                    std::to_string(pl.swz) + "B" + (pair ? " (CTA pair)" : ""));
+  if (pair && kn->split_k > 1) return fail(TEC_E_LOWERING, "CTA pairs do not split K");
   if (kn && kn->tile_m && kn->tile_m != 128)
     return fail(TEC_E_LOWERING, "tile_m must be 128 (tcgen05 M)");
 
@@ -949,7 +965,8 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     const int64_t ktot = d->r * d->s * pl.cp;
     cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)d->k};
     cuuint64_t strides[1] = {(cuuint64_t)(ktot * es)};
-    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)bn};
+    // a CTA of a pair loads half of the tile's weight rows
+    cuuint32_t box[2] = {(cuuint32_t)cb, (cuuint32_t)(pair ? bn / 2 : bn)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fns.tiled(&tm_b, tdt, 2, const_cast<void*>(w), dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(pl.swz),
@@ -1014,6 +1031,12 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
   }
   int grid = (int)std::min<int64_t>(tiles * p.splits, sms);
   if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
+  if (pair) {  // whole pairs, one per (M-tile pair, N tile) unit at most
+    const int64_t units = ((m_tiles + 1) / 2) * p.n_tiles;
+    int pairs = (int)std::min<int64_t>(units, sms / 2);
+    if (kn->grid > 0) pairs = std::max(1, std::min(pairs, (int)kn->grid / 2));
+    grid = 2 * pairs;
+  }
   // TEC_SM100_PROFILE=1: per-role pipeline wait breakdown on stderr
   // (synchronises the stream; diagnostics only).
   static const bool prof = std::getenv("TEC_SM100_PROFILE") != nullptr;
@@ -1023,8 +1046,8 @@ tec_status run_conv(const tec_conv_desc* d, const Plan& pl,
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 8 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
-  if (plan_only(TEC_KERNEL_IM2COL, bn, 128, 0, grid, 0, tmem_cols_for((4 * bn <= 512 ? 4 : 2) * bn), p.tma_store,
-                p.splits, 1))
+  if (plan_only(TEC_KERNEL_IM2COL, bn, pair ? 256 : 128, 0, grid, 0,
+                tmem_cols_for((4 * bn <= 512 ? 4 : 2) * bn), p.tma_store, p.splits, pair ? 2 : 1))
     return TEC_OK;
   const int e = launch(tm_a, tm_b, tm_y, p, grid, st);
   if (e) return cuda_fail(e, "conv_fprop_tc launch");

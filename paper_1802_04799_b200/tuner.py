@@ -223,7 +223,8 @@ def conv_space(name: str, desc: _abi.ConvDesc,
         tile (halo: MMA sub-tiles x 128), stages (halo: 1 streamed / 2
         resident weights), split_k (im2col: K split over CTAs, partials
         summed in order), cluster_n (halo, streamed weights: CTA pairs share
-        weight tiles by TMA multicast);
+        weight tiles by TMA multicast; im2col: CTA pairs -- cta_group::2,
+        M = 256, each CTA loading half of the weight rows);
       f32tc: tile_k, tile_n, stages (resident weights) and split_k of the
         split-bf16 f32 kernel (split_k = -1: stream-K, equal (tile, k) shares)."""
     if desc.compute == _abi.COMPUTE_F32TC:

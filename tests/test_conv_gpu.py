@@ -298,6 +298,41 @@ def test_halo_weight_multicast_cluster(layer, batch):
     assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
 
 
+@pytest.mark.parametrize("compute", ["bf16", "i8"])
+@pytest.mark.parametrize("layer,batch,bn", [("C4", 3, 128), ("C7", 1, 128), ("C12", 1, 128),
+                                            ("C12", 3, 256), ("C6", 2, 64), ("C10", 3, 128),
+                                            ("C3", 1, 64), ("C11", 1, 128)])
+def test_im2col_cta_pair(layer, batch, bn, compute):
+    """knob cluster_n = 2 on the im2col path: CTA pairs (cta_group::2, M = 256,
+    each CTA loading half the weight rows, the leader issuing the MMAs). Odd
+    M-tile counts (C12 b1: 25 tiles) leave the last pair a phantom tile."""
+    hw, c, k, r, s = RESNET18_CONVS[layer]
+    x, w, b = _inputs((batch, c, hw, hw), (k, c, r, r), k, compute == "i8",
+                      seed=5 + batch + sum(map(ord, layer)))
+    attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+    epi = [("bias_add", b), ("relu",)]
+    y = fused_conv("conv2d", x, w, attrs, epi, compute=None if compute == "i8" else compute,
+                   knobs={"tile_k": 1, "tile_n": bn, "cluster_n": 2})
+    # the pair sums every output's K in the same order as one CTA: identical
+    y1 = fused_conv("conv2d", x, w, attrs, epi, compute=None if compute == "i8" else compute,
+                    knobs={"tile_k": 1, "tile_n": bn})
+    assert np.array_equal(bits(y), bits(y1))
+    xr, wr = (bf16_round(x), bf16_round(w)) if compute == "bf16" else (x, w)
+    want = oracle_conv("conv2d", xr, wr, attrs["strides"], attrs["padding"], epi)
+    if compute == "i8":
+        assert np.array_equal(y, want)
+    else:
+        assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
+
+
+def test_cta_pair_rejects_split_k():
+    hw, c, k, r, s = RESNET18_CONVS["C12"]
+    x, w, b = _inputs((1, c, hw, hw), (k, c, r, r), k, False, 3)
+    with pytest.raises(TecError):
+        fused_conv("conv2d", x, w, {"strides": (1, 1), "padding": (1, 1)}, [("bias_add", b)],
+                   compute="bf16", knobs={"tile_k": 1, "cluster_n": 2, "split_k": 2})
+
+
 @pytest.mark.parametrize("path", [1, 2])
 @pytest.mark.parametrize("k", [64, 48])
 def test_residual_epilogue_both_paths(path, k):
