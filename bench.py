@@ -625,12 +625,43 @@ def run_e2e(args, batch, device, compute, world):
         t = torch.tensor([dt], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
+    pcie = pcie_duplex_gbs()
+    moved = (h2d + d2h) / dt / 1e9
     return {"value": round(world * flops / dt / 1e12, 3),
             "unit": "TOPS" if compute == "i8" else "TFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": round(dt * 1e3, 2), "compute": compute,
+            # the e2e roofline: this box's pinned PCIe rate with both
+            # directions busy (the step moves h2d + d2h bytes)
+            "pcie_gbs": round(moved, 1), "pcie_duplex_peak_gbs": round(pcie, 1),
+            "frac_of_pcie": round(moved / pcie, 3) if pcie else None,
             "path": "tec_eval_fused_conv (C ABI, host NCHW buffers, pinned), wall clock incl. "
                     "H2D, layout packing, kernel, unpack, D2H; max over ranks"}
+
+
+def pcie_duplex_gbs(nbytes=128 << 20, reps=4):
+    """Pinned host<->device copy rate with an H2D and a D2H stream running
+    together (GB/s of both directions summed): what a step that uploads its
+    inputs and downloads its outputs can reach."""
+    import torch
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+    both()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        both()
+    torch.cuda.synchronize()
+    return 2 * nbytes * reps / (time.perf_counter() - t0) / 1e9
 
 
 # ------------------------------------------------------------ multi-rank plumbing

@@ -1991,8 +1991,11 @@ tec_status tec_eval_fused_conv(const tec_conv_desc* d, const tec_epilogue* epi,
     const char* e = std::getenv("TEC_SM100_CHUNK_KB");  // tuning override
     return e ? std::max<int64_t>(64, std::atoll(e)) << 10 : int64_t(6) << 20;
   }();
-  int64_t chunks = std::min<int64_t>(d->n, std::max<int64_t>(1, x_elems * in_es / chunk_bytes));
-  chunks = std::min<int64_t>(chunks, 32);
+  // sized by the larger direction (the stem's output is 5x its input): the
+  // first chunk's upload and the last chunk's download are the exposed ends
+  const int64_t io_bytes = std::max<int64_t>(x_elems * in_es, y_elems * 4);
+  int64_t chunks = std::min<int64_t>(d->n, std::max<int64_t>(1, io_bytes / chunk_bytes));
+  chunks = std::min<int64_t>(chunks, 64);
   if (!same_shape_ops && chunks > 1 && lay.act_bytes % d->n == 0) {
     if (!ws.h2d) TEC_CUDA(cudaStreamCreateWithFlags(&ws.h2d, cudaStreamNonBlocking));
     if (!ws.d2h) TEC_CUDA(cudaStreamCreateWithFlags(&ws.d2h, cudaStreamNonBlocking));
