@@ -74,12 +74,16 @@ enum { kDwtNone = 0, kDwtBias = 1, kDwtBiasRelu = 2 };
 constexpr int kDwtThreads = 384;  // 12 warps, up to 168 registers per thread
 constexpr int kTW = 4;            // output columns per work item
 
-template <typename InT, typename OutT, int SW, int PROG>
+// COLB: bytes per staged pixel (channel block) when known at compile time
+// (128: every layer with >= 128 B of channels) -- the tap reads' addresses
+// then become immediate offsets off one row address; 0 = runtime t.cb * ES.
+template <typename InT, typename OutT, int SW, int PROG, int COLB = 0>
 __global__ void __launch_bounds__(kDwtThreads, 1)
     dw_tma_kernel(const __grid_constant__ CUtensorMap tm_x, const DepthwiseParams p,
                   const DwTmaShape t) {
   constexpr int VEC = 16 / static_cast<int>(sizeof(InT));
   constexpr int ES = static_cast<int>(sizeof(InT));
+  const int colb = COLB ? COLB : t.cb * ES;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                              ~uintptr_t(127));
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
 #pragma unroll
       for (int rh = 0; rh < 3; ++rh) {
         const uint32_t rowa = sbase + im * img_bytes +
-            static_cast<uint32_t>(((r * SW + rh) * t.cols_in + ow0 * SW) * t.cb * ES);
+            static_cast<uint32_t>(((r * SW + rh) * t.cols_in + ow0 * SW) * colb);
 #pragma unroll
         for (int jc = 0; jc < (kTW - 1) * SW + 3; ++jc) {
           float x[kBF ? 1 : VEC];
@@ -206,9 +210,9 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
           if constexpr (kBF) {
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(xb[0]), "=r"(xb[1]), "=r"(xb[2]), "=r"(xb[3])
-                         : "r"(rowa + static_cast<uint32_t>(jc * t.cb * ES)));
+                         : "r"(rowa + static_cast<uint32_t>(jc * colb)));
           } else {
-            lds_vec(rowa + static_cast<uint32_t>(jc * t.cb * ES), x);
+            lds_vec(rowa + static_cast<uint32_t>(jc * colb), x);
           }
 #pragma unroll
           for (int i = 0; i < kTW; ++i) {
@@ -249,10 +253,15 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
         if (ow >= p.ow) break;
         float acc[VEC];
 #pragma unroll
-        for (int j = 0; j < V2; ++j) { acc[2 * j] = acc2[i][j].x; acc[2 * j + 1] = acc2[i][j].y; }
+        for (int j = 0; j < V2; ++j) {
+          float2 a = acc2[i][j];
+          if constexpr (PROG != kDwtNone)  // packed, each component rounded
+            a = __fadd2_rn(a, make_float2(bias[2 * j], bias[2 * j + 1]));
+          acc[2 * j] = a.x;
+          acc[2 * j + 1] = a.y;
+        }
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
-          if constexpr (PROG != kDwtNone) acc[j] = __fadd_rn(acc[j], bias[j]);
           if constexpr (PROG == kDwtBiasRelu) acc[j] = acc[j] < 0.0f ? 0.0f : acc[j];
         }
         const int64_t o = ((static_cast<int64_t>(n + im) * p.oh + oh0 + r) * p.ow + ow) * p.c + c0;
@@ -485,12 +494,16 @@ int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTma
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   };
-#define TEC_DWT(IN, OUT, SW_)                                                    \
+  const bool col128 = t.cb * (p.in_type == kBF16 ? 2 : 4) == 128;
+#define TEC_DWT_C(IN, OUT, SW_, CB_)                                             \
   switch (prog) {                                                               \
-    case kDwtNone: return go(dw_tma_kernel<IN, OUT, SW_, kDwtNone>);            \
-    case kDwtBias: return go(dw_tma_kernel<IN, OUT, SW_, kDwtBias>);            \
-    default: return go(dw_tma_kernel<IN, OUT, SW_, kDwtBiasRelu>);              \
+    case kDwtNone: return go(dw_tma_kernel<IN, OUT, SW_, kDwtNone, CB_>);       \
+    case kDwtBias: return go(dw_tma_kernel<IN, OUT, SW_, kDwtBias, CB_>);       \
+    default: return go(dw_tma_kernel<IN, OUT, SW_, kDwtBiasRelu, CB_>);         \
   }
+#define TEC_DWT(IN, OUT, SW_)                                                    \
+  if (col128) { TEC_DWT_C(IN, OUT, SW_, 128) }                                  \
+  TEC_DWT_C(IN, OUT, SW_, 0)
   if (p.in_type == kBF16 && p.out_type == kBF16) {
     if (p.sw == 1) { TEC_DWT(__nv_bfloat16, __nv_bfloat16, 1) }
     TEC_DWT(__nv_bfloat16, __nv_bfloat16, 2)
@@ -504,6 +517,7 @@ int launch_dw_tma(const DepthwiseParams& p, const CUtensorMap& tm_x, const DwTma
     TEC_DWT(float, float, 2)
   }
 #undef TEC_DWT
+#undef TEC_DWT_C
   return -1;
 }
 
