@@ -5,6 +5,7 @@
 // top of these; no CUTLASS/CuTe types are used.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -437,6 +438,11 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, ui
   }
 }
 
+// TEC_SM100_NO_PDL=1 (experiments): plain stream order instead of PDL.
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("TEC_SM100_NO_PDL") == nullptr;
+  return on;
+}
 // Host: launch with programmatic stream serialization (PDL) allowed, so a
 // kernel that calls pdl_launch_dependents() lets this one start early.
 template <typename... KArgs, typename... Args>
@@ -449,7 +455,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
@@ -467,7 +473,7 @@ inline cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = static_cast<unsigned>(cluster);
   attr[1].val.clusterDim.y = 1;
