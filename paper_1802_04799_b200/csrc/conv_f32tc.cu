@@ -66,7 +66,8 @@ constexpr int kBM = 128;
 constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
 constexpr int kMaxRows = 8;    // row-ring slots (ConvGemmParams::rows)
 
-template <int BN, int SWZ, int STAGES, bool INTER, bool RES = false, bool HALO = false>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES = false, bool HALO = false,
+          bool PAIR = false>
 struct F32tcCfg {
   static constexpr int kAPlanes = INTER ? 1 : 3;  // A boxes per k-iteration
   static constexpr int kA = kBM * SWZ;            // one A box
@@ -74,7 +75,8 @@ struct F32tcCfg {
   // box [plane][BN rows][16 ch] with the 32-B swizzle. Either way the planes
   // are consecutive row blocks: [B_h; B_m; B_l] is one N-concatenated operand.
   static constexpr int kBSW = INTER ? 32 : SWZ;      // B row bytes / swizzle
-  static constexpr int kBPlane = BN * kBSW;          // bytes per B plane
+  // bytes per B plane (a CTA of a pair holds half of the tile's rows)
+  static constexpr int kBPlane = (PAIR ? BN / 2 : BN) * kBSW;
   static constexpr int kBBoxes = INTER ? 1 : 3;
   static constexpr int kBBox = INTER ? 3 * kBPlane : kBPlane;
   static constexpr int kBStage = 3 * kBPlane;       // B bytes per k-iteration
@@ -109,6 +111,7 @@ struct F32tcCfg {
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   static_assert(2 * kXCols + kYBufs * kYCols <= 512, "TMEM budget");
   static_assert(!INTER || SWZ == 128, "interleaved planes live in one 128-B row");
+  static_assert(!PAIR || (BN == 128 && !INTER && !RES && !HALO), "CTA pairs: the im2col BN=128 path");
 };
 
 // The work items of one CTA: (output tile mn, k-iterations [kb, ke), its
@@ -161,12 +164,12 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, bool prof,
   *acc += clock64() - t0;
 }
 
-template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_f32tc_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvGemmParams p) {
-  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER, RES, HALO>;
+  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER, RES, HALO, PAIR>;
   constexpr int kCB = SWZ / 2;  // bf16 channels per box row
   constexpr int HB = BN / 2;    // columns per epilogue warp
   constexpr int kBSW = Cfg::kBSW;
@@ -202,7 +205,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
   const int splits = p.splits > 1 ? p.splits : 1;
-  const int num_items = p.m_tiles * p.n_tiles * splits;
+  // CTA pair (PAIR, cluster of 2, cta_group::2 -- as conv_tc.cu): the pair
+  // runs one MMA stream (the leader's) over a 256-row M tile, each CTA
+  // loading its own A rows and half of the weight rows; work units are
+  // (M-tile pair, N tile) and own_mn() maps a unit to this CTA's tile
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const int m_units = PAIR ? (p.m_tiles + 1) / 2 : p.m_tiles;
+  auto own_mn = [&](int mnu) -> int {
+    if constexpr (!PAIR) return mnu;
+    const int mp = mnu / p.n_tiles;
+    return (2 * mp + static_cast<int>(rank)) * p.n_tiles + (mnu - mp * p.n_tiles);
+  };
+  const int num_items = m_units * p.n_tiles * splits;
   // TEC_SM100_PROFILE: per-role waiting cycles, summed over CTAs into p.dbg --
   // [0] producer A (halo/ring) free, [1] producer B ring free, [2] MMA
   // tile accumulator free, [3] MMA chunk accumulator free, [4] MMA operands
@@ -219,11 +233,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // work items of this CTA: strided over the grid, or (row ring) one
   // contiguous range, so consecutive items are consecutive output rows
   const bool ring = HALO && p.rows > 0;
+  const int cta = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ctas = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   const int it_lo = ring ? static_cast<int>(static_cast<int64_t>(num_items) * blockIdx.x / gridDim.x)
-                         : static_cast<int>(blockIdx.x);
+                         : cta;
   const int it_hi = ring ? static_cast<int>(static_cast<int64_t>(num_items) * (blockIdx.x + 1) / gridDim.x)
                          : num_items;
-  const int it_step = ring ? 1 : static_cast<int>(gridDim.x);
+  const int it_step = ring ? 1 : ctas;
   const bool sk = !HALO && p.stream_k;
   auto make_iter = [&]() {
     WorkIter w;
@@ -234,9 +250,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     w.splits = sk ? 1 : splits;
     w.kps = kps;
     w.k_iters = k_iters;
-    w.G = static_cast<int>(gridDim.x);
-    w.c = static_cast<int>(blockIdx.x);
-    w.W = static_cast<long long>(p.m_tiles) * p.n_tiles * k_iters;
+    w.G = ctas;
+    w.c = cta;
+    w.W = static_cast<long long>(m_units) * p.n_tiles * k_iters;
     w.pos = w.W * w.c / w.G;
     w.end = w.W * (w.c + 1) / w.G;
     return w;
@@ -252,9 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 256);
+      mbar_init(&sempty[i], PAIR ? 512 : 256);  // a pair: both CTAs' epilogues
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 256);
+      mbar_init(&tempty[i], PAIR ? 512 : 256);
     }
     mbar_init(wfull, 1);
     for (int i = 0; i < kMaxRows; ++i) {
@@ -263,9 +279,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+    else tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // both CTAs' barriers initialised
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
@@ -376,11 +396,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
       WorkIter wi = make_iter();
-      int item, mn, kb, ke, seg, nseg;
-      while (wi.next(item, mn, kb, ke, seg, nseg)) {
+      int item, mnu, kb, ke, seg, nseg;
+      // a pair's loads complete on the leader's full barrier
+      const uint32_t full_l = PAIR ? mapa_u32(smem_u32(full), 0) : 0u;
+      while (wi.next(item, mnu, kb, ke, seg, nseg)) {
+        const int mn = own_mn(mnu);
         const int m_tile = mn / p.n_tiles;
         const int n_tile = mn - m_tile * p.n_tiles;
-        const int m0 = m_tile * kBM;
+        // a pair's phantom tile (odd M-tile count) reads its partner's rows
+        const int m0 = (PAIR ? min(m_tile, p.m_tiles - 1) : m_tile) * kBM;
         const int img = m0 / ohw;
         const int rem = m0 - img * ohw;
         const int oh = rem / p.ow;
@@ -391,23 +415,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         int s = rem_k / p.cblocks, cb = rem_k - s * p.cblocks;
         for (int k = kb; k < ke; ++k) {
           twait(&empty[stage], phase ^ 1, prof, &dw[0]);
-          if (issue_a) mbar_arrive_expect_tx(&full[stage], Cfg::kStage);
+          if (issue_a && (!PAIR || rank == 0))
+            mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * Cfg::kStage : Cfg::kStage);
           uint8_t* base = sRing + stage * Cfg::kStage;
           uint8_t* bbase = base + Cfg::kAPlanes * Cfg::kA;
 #pragma unroll
           for (int pl = 0; pl < Cfg::kAPlanes; ++pl)
-            if (issue_a)
-              tma_load_im2col_4d(base + pl * Cfg::kA, &tm_a, &full[stage], pl * cpp + cb * kCB,
-                                 w0, h0, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            if (issue_a) {
+              if constexpr (PAIR)
+                tma_load_im2col_4d_pair(base + pl * Cfg::kA, &tm_a, full_l + 8 * stage,
+                                        pl * cpp + cb * kCB, w0, h0, img,
+                                        static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+              else
+                tma_load_im2col_4d(base + pl * Cfg::kA, &tm_a, &full[stage], pl * cpp + cb * kCB,
+                                   w0, h0, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            }
           if (issue_b && !RES) {
             if constexpr (INTER) {
               tma_load_3d(bbase, &tm_b, &full[stage], 0, n_tile * BN, 3 * (r * p.s + s));
             } else {
               const int wcol = (r * p.s + s) * pix + cb * kCB;
 #pragma unroll
-              for (int pl = 0; pl < 3; ++pl)
-                tma_load_2d(bbase + pl * kPlaneB, &tm_b, &full[stage], wcol + pl * cpp,
-                            n_tile * BN);
+              for (int pl = 0; pl < 3; ++pl) {
+                if constexpr (PAIR)  // this CTA's half of the tile's weight rows
+                  tma_load_2d_pair(bbase + pl * kPlaneB, &tm_b, full_l + 8 * stage, wcol + pl * cpp,
+                                   n_tile * BN + static_cast<int>(rank) * (BN / 2));
+                else
+                  tma_load_2d(bbase + pl * kPlaneB, &tm_b, &full[stage], wcol + pl * cpp,
+                              n_tile * BN);
+              }
             }
           }
           if (++stage == STAGES) {
@@ -422,10 +458,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && (!PAIR || rank == 0)) {
     // ------------------------------------------ single-thread MMA issuer
     if (elect_one()) {
-      constexpr uint32_t idesc = make_idesc<MmaKind::kF16>(kBM, BN);
+      constexpr uint32_t idesc = make_idesc<MmaKind::kF16>(PAIR ? 2 * kBM : kBM, BN);
       constexpr uint32_t idesc3 = make_idesc<MmaKind::kF16>(kBM, 3 * BN);
       constexpr uint32_t idesc2 = make_idesc<MmaKind::kF16>(kBM, 2 * BN);
       int stage = 0;
@@ -496,17 +532,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
               const uint64_t bm = bh + (kPlaneB >> 4);
               const uint64_t bl = bh + 2 * (kPlaneB >> 4);
-              tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc, s_acc);
-              tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, t_acc);
-              tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
-              tc_mma<MmaKind::kF16>(t_tmem, ah, bl, idesc, 1u);
-              tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
-              tc_mma<MmaKind::kF16>(t_tmem, am, bm, idesc, 1u);
+              if constexpr (PAIR) {
+                tc_mma_pair<MmaKind::kF16>(s_tmem, ah, bh, idesc, s_acc);
+                tc_mma_pair<MmaKind::kF16>(t_tmem, ah, bm, idesc, t_acc);
+                tc_mma_pair<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
+                tc_mma_pair<MmaKind::kF16>(t_tmem, ah, bl, idesc, 1u);
+                tc_mma_pair<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
+                tc_mma_pair<MmaKind::kF16>(t_tmem, am, bm, idesc, 1u);
+              } else {
+                tc_mma<MmaKind::kF16>(s_tmem, ah, bh, idesc, s_acc);
+                tc_mma<MmaKind::kF16>(t_tmem, ah, bm, idesc, t_acc);
+                tc_mma<MmaKind::kF16>(t_tmem, am, bh, idesc, 1u);
+                tc_mma<MmaKind::kF16>(t_tmem, ah, bl, idesc, 1u);
+                tc_mma<MmaKind::kF16>(t_tmem, al, bh, idesc, 1u);
+                tc_mma<MmaKind::kF16>(t_tmem, am, bm, idesc, 1u);
+              }
             }
           }
           first = false;
           if (++in_chunk == chunk || last_of_tile) {
-            tc_commit(&sfull[g & 1]);  // chunk ready to fold
+            if constexpr (PAIR) tc_commit_pair(&sfull[g & 1], 3);  // both CTAs' epilogues
+            else tc_commit(&sfull[g & 1]);  // chunk ready to fold
             ++g;
             in_chunk = 0;
           }
@@ -680,14 +726,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t base = smem_u32(sRing + stage * Cfg::kStage);
             step(base, RES ? smem_u32(sRes) + k * Cfg::kBStage : base + Cfg::kAPlanes * Cfg::kA,
                  kPlaneA, k + 1 == ke);
-            tc_commit(&empty[stage]);  // frees the smem slot when the MMAs land
+            // frees the smem slot (a pair: both CTAs') when the MMAs land
+            if constexpr (PAIR) tc_commit_pair(&empty[stage], 3);
+            else tc_commit(&empty[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
         }
-        if (Cfg::kHasY) tc_commit(&tfull[tb]);
+        if (Cfg::kHasY) {
+          if constexpr (PAIR) tc_commit_pair(&tfull[tb], 3);
+          else tc_commit(&tfull[tb]);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -703,8 +754,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     int staged_n = -1;
     WorkIter wi = make_iter();
-    int item, mn, kb, ke, split, nseg;
-    for (; wi.next(item, mn, kb, ke, split, nseg); ++local) {
+    int item, mnu, kb, ke, split, nseg;
+    // accumulator hand-back: a pair's peer arrives on the leader's barriers
+    const uint32_t sempty_l = PAIR ? mapa_u32(smem_u32(sempty), 0) : 0u;
+    const uint32_t tempty_l = PAIR ? mapa_u32(smem_u32(tempty), 0) : 0u;
+    auto release = [&](uint64_t* bar, uint32_t bar_l) {
+      if constexpr (PAIR) {
+        if (rank != 0) {
+          mbar_arrive_cluster(bar_l);
+          return;
+        }
+      }
+      mbar_arrive(bar);
+    };
+    for (; wi.next(item, mnu, kb, ke, split, nseg); ++local) {
+      const int mn = own_mn(mnu);
       const int m_tile = mn / p.n_tiles;
       const int n_tile = mn - m_tile * p.n_tiles;
       const int row0 = m_tile * kBM + static_cast<int>(q * 32);
@@ -755,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         // GRP (no tile accumulator): the fault test drops a chunk arrive
-        if (!(Cfg::kGrp && p.fault == 1 && local == 0 && c == 0)) mbar_arrive(&sempty[sb]);
+        if (!(Cfg::kGrp && p.fault == 1 && local == 0 && c == 0)) release(&sempty[sb], sempty_l + 8 * sb);
       }
       if constexpr (Cfg::kHasY) {
         // + the tile's cross-term accumulator
@@ -766,12 +830,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         // p.fault == 1 (tests only): lose one arrive -- the MMA warp then
         // waits for this accumulator forever and the mbarrier watchdog must trap
-        if (!(p.fault == 1 && local == 0)) mbar_arrive(&tempty[tb]);
+        if (!(p.fault == 1 && local == 0)) release(&tempty[tb], tempty_l + 8 * tb);
       }
       if constexpr (Cfg::kGrp) {
 #pragma unroll
         for (int j = 0; j < HB; ++j) sum[j] = __fadd_rn(sum[j], cross[j]);
       }
+      if (PAIR && m_tile >= p.m_tiles) continue;  // a pair's phantom tile: nothing to store
       if (nseg > 1) {
         // publish this split's partial ([item][warp][column][lane]: one
         // 128-B line per column); the last split of the tile sums them all
@@ -878,9 +943,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // no DSMEM traffic may target an exited CTA
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
+    else tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
   if (prof) {
     // one representative thread per role: producer warps 0 / 3, MMA warp 1,
     // the first epilogue thread
@@ -895,29 +964,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, int PROG, bool PAIR>
 int launch_f32tc_inst(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int grid, cudaStream_t stream) {
-  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER, RES, HALO>;
-  auto kfn = conv_f32tc_kernel<BN, SWZ, STAGES, INTER, RES, HALO, PROG>;
+  using Cfg = F32tcCfg<BN, SWZ, STAGES, INTER, RES, HALO, PAIR>;
+  auto kfn = conv_f32tc_kernel<BN, SWZ, STAGES, INTER, RES, HALO, PROG, PAIR>;
   const int smem = Cfg::kSmem + (RES ? p.res_bytes : 0) +
                    (HALO ? p.hbuf * Cfg::kAPlanes * p.halo_bytes : 0);
   if (smem > 227 * 1024) return -1;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_a, tm_b, tm_y, p);
+  if constexpr (PAIR)
+    e = launch_pdl_cluster(kfn, dim3(grid), dim3(kThreads), smem, stream, 2, tm_a, tm_b, tm_y, p);
+  else
+    e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, stream, tm_a, tm_b, tm_y, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO>
+template <int BN, int SWZ, int STAGES, bool INTER, bool RES, bool HALO, bool PAIR = false>
 int launch_f32tc_prog(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int prog, int grid, cudaStream_t st) {
   switch (prog) {
-    case epi::kProgNone: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgNone>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBias: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBias>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBiasRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBiasRelu>(tm_a, tm_b, tm_y, p, grid, st);
-    case epi::kProgBiasAddRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBiasAddRelu>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgNone: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgNone, PAIR>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBias: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBias, PAIR>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBiasRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBiasRelu, PAIR>(tm_a, tm_b, tm_y, p, grid, st);
+    case epi::kProgBiasAddRelu: return launch_f32tc_inst<BN, SWZ, STAGES, INTER, RES, HALO, epi::kProgBiasAddRelu, PAIR>(tm_a, tm_b, tm_y, p, grid, st);
     default: return -1;
   }
 }
@@ -965,10 +1037,22 @@ int conv_f32tc_b_stage_bytes(int bn, int swz, bool inter) {
   return 3 * bn * (inter ? 32 : swz);
 }
 
+// The CTA-pair instance (im2col, BN = 128, 128-B channel blocks): its
+// shared memory per CTA, or -1 for another configuration.
+int conv_f32tc_pair_smem_bytes(int bn, int swz, bool inter, bool res, bool halo) {
+  if (bn != 128 || swz != 128 || inter || res || halo) return -1;
+  return F32tcCfg<128, 128, 2, false, false, false, true>::kSmem;
+}
+
 // Returns a cudaError_t, or -1 for an unsupported (bn, swz, program).
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int bn, int swz, bool inter, bool res, bool halo,
-                      int prog, int grid, cudaStream_t st) {
+                      int prog, int grid, cudaStream_t st, bool pair) {
+  if (pair) {
+    if (conv_f32tc_pair_smem_bytes(bn, swz, inter, res, halo) < 0) return -1;
+    return launch_f32tc_prog<128, 128, 2, false, false, false, true>(tm_a, tm_b, tm_y, p, prog,
+                                                                    grid, st);
+  }
 #define TEC_X(BN, SW, ST, IN, RS, HA)                                     \
   if (bn == BN && swz == SW && inter == IN && res == RS && halo == HA) \
     return launch_f32tc_prog<BN, SW, ST, IN, RS, HA>(tm_a, tm_b, tm_y, p, prog, grid, st);

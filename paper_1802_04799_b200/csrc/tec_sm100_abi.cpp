@@ -70,8 +70,9 @@ int launch_scale_rows(const float* x, const float* s, float* y, int64_t count, i
                       int sms, cudaStream_t st);
 int launch_conv_f32tc(const CUtensorMap& tm_a, const CUtensorMap& tm_b, const CUtensorMap& tm_y,
                       const ConvGemmParams& p, int bn, int swz, bool inter, bool res, bool halo,
-                      int prog, int grid, cudaStream_t st);
+                      int prog, int grid, cudaStream_t st, bool pair);
 int conv_f32tc_smem_bytes(int bn, int swz, bool inter, bool res, bool halo);
+int conv_f32tc_pair_smem_bytes(int bn, int swz, bool inter, bool res, bool halo);
 int conv_f32tc_stages(int bn, int swz, bool inter, bool res, bool halo);
 int conv_f32tc_b_stage_bytes(int bn, int swz, bool inter);
 }  // namespace tec_sm100
@@ -1087,7 +1088,9 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
            epi.ops[2] == kEpiRelu) prog = 4;
   else return fail(TEC_E_LOWERING, "f32tc: fused program not supported (compute f32 runs it)");
   if (kn && kn->tile_m && kn->tile_m != 128) return fail(TEC_E_LOWERING, "tile_m must be 128 (tcgen05 M)");
-  if (kn && kn->cluster_n > 1) return fail(TEC_E_LOWERING, "f32tc: no cluster knob");
+  // knob cluster_n = 2: CTA pairs (cta_group::2) on the im2col path, tile_n 128
+  if (kn && kn->cluster_n > 2) return fail(TEC_E_LOWERING, "f32tc: cluster_n is 1 or 2 (CTA pair)");
+  const bool pair = kn && kn->cluster_n == 2;
   const int path = kn ? (int)kn->tile_k : 0;  // 0 auto, 1 im2col, 2 shifted window
   if (path != 0 && path != 1 && path != 2) return fail(TEC_E_LOWERING, "f32tc: tile_k is 1 or 2");
   const int swz = pl.swz;
@@ -1164,6 +1167,8 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     if (path == 2 && !halo) return fail(TEC_E_LOWERING, "f32tc: no shifted-window configuration fits");
   }
   if (path == 2 && !halo) return fail(TEC_E_LOWERING, "f32tc: the shifted window needs stride 1");
+  if (pair && (halo || conv_f32tc_pair_smem_bytes(bn, swz, inter, false, false) < 0))
+    return fail(TEC_E_LOWERING, "f32tc: CTA pairs run the im2col path at tile_n 128");
 
   CUtensorMap tm_a, tm_b, tm_y;
   if (halo) {
@@ -1219,7 +1224,8 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     const int64_t ktot = d->r * d->s * pl.cp;
     cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)d->k};
     cuuint64_t strides[1] = {(cuuint64_t)(ktot * 2)};
-    cuuint32_t box[2] = {(cuuint32_t)(swz / 2), (cuuint32_t)bn};
+    // a CTA of a pair loads half of the tile's weight rows
+    cuuint32_t box[2] = {(cuuint32_t)(swz / 2), (cuuint32_t)(pair ? bn / 2 : bn)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fns.tiled(&tm_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(swz),
@@ -1303,10 +1309,13 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   p.splits = splits;
   p.kps = (k_iters + splits - 1) / splits;
   p.splits = (k_iters + p.kps - 1) / p.kps;  // no empty split
+  // a pair's work unit is (M-tile pair, N tile), run by sms / 2 clusters
+  const int64_t units = pair ? ((p.m_tiles + 1) / 2) * (int64_t)p.n_tiles : tiles;
+  const int64_t slots = pair ? sms / 2 : sms;
   if (stream_k) {
     // segments per tile <= 1 + the share boundaries inside it
-    const int64_t w = tiles * k_iters;
-    const int64_t g = std::min<int64_t>(sms, w);
+    const int64_t w = units * k_iters;
+    const int64_t g = std::min<int64_t>(slots, w);
     const int64_t share = w / g;
     p.stream_k = 1;
     p.splits = (int32_t)std::min<int64_t>(k_iters, (k_iters + share - 1) / std::max<int64_t>(1, share) + 1);
@@ -1314,9 +1323,10 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   }
   const size_t partials = (size_t)tiles * p.splits * 128 * bn * sizeof(float);
   if (g_plan) g_plan->workspace_bytes = p.splits > 1 ? (int64_t)splitk_bytes(partials, tiles) : 0;
-  int grid = p.stream_k ? (int)std::min<int64_t>(sms, tiles * k_iters)
-                        : (int)std::min<int64_t>(tiles * p.splits, sms);
-  if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, kn->grid);
+  int grid = p.stream_k ? (int)std::min<int64_t>(slots, units * k_iters)
+                        : (int)std::min<int64_t>(units * p.splits, slots);
+  if (kn && kn->grid > 0) grid = (int)std::min<int64_t>(grid, pair ? kn->grid / 2 : kn->grid);
+  if (pair) grid = 2 * std::max(1, grid);  // whole CTA pairs
   // Resident weights (im2col: knob stages 1 streamed, 2 resident, 0 =
   // resident when they fit): every B tile of the CTA's output-channel tile
   // loaded once per CTA, the ring carries activations only -- fewer TMA
@@ -1324,7 +1334,7 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   // multiple of the N tiles.
   if (!halo) {
     const int res_fixed = conv_f32tc_smem_bytes(bn, swz, inter, true, false);
-    res = want_res != 1 && p.splits == 1 && !p.stream_k && res_fixed > 0 &&
+    res = !pair && want_res != 1 && p.splits == 1 && !p.stream_k && res_fixed > 0 &&
           res_fixed + res_bytes <= kBudget && grid >= p.n_tiles;
     if (want_res == 2 && !res)
       return fail(TEC_E_LOWERING, "f32tc: resident weights do not fit (or split-K is on)");
@@ -1336,10 +1346,12 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
   }
   const int stages = conv_f32tc_stages(bn, swz, inter, res, halo);
   if (stages < 0) return fail(TEC_E_LOWERING, "f32tc: no instance for this tile / block");
-  const int smem = conv_f32tc_smem_bytes(bn, swz, inter, res, halo) + (res ? res_bytes : 0) +
-                   (halo ? hbuf * a_planes * halo_bytes : 0);
-  if (plan_only(halo ? TEC_KERNEL_F32TC_HALO : TEC_KERNEL_F32TC, bn, 128, res ? 2 : 1, grid,
-                smem, bn == 64 ? 512 : 4 * bn <= 256 ? 256 : 512, p.tma_store, p.splits, 1))
+  const int smem = (pair ? conv_f32tc_pair_smem_bytes(bn, swz, inter, res, halo)
+                        : conv_f32tc_smem_bytes(bn, swz, inter, res, halo)) +
+                   (res ? res_bytes : 0) + (halo ? hbuf * a_planes * halo_bytes : 0);
+  if (plan_only(halo ? TEC_KERNEL_F32TC_HALO : TEC_KERNEL_F32TC, bn, pair ? 256 : 128,
+                res ? 2 : 1, grid, smem, bn == 64 ? 512 : 4 * bn <= 256 ? 256 : 512, p.tma_store,
+                p.splits, pair ? 2 : 1))
     return TEC_OK;
   if (p.splits > 1) {
     tec_status wst = splitk_workspace(dev, partials, (size_t)tiles, st, &p.ws, &p.tile_cnt);
@@ -1352,7 +1364,8 @@ tec_status run_conv_f32tc(const tec_conv_desc* d, const Plan& pl, const Epilogue
     TEC_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st));
     p.dbg = dbg;
   }
-  const int e = launch_conv_f32tc(tm_a, tm_b, tm_y, p, bn, swz, inter, res, halo, prog, grid, st);
+  const int e = launch_conv_f32tc(tm_a, tm_b, tm_y, p, bn, swz, inter, res, halo, prog, grid, st,
+                                  pair);
   if (e == -1) return fail(TEC_E_LOWERING, "f32tc: no instance for this tile / block");
   if (e) return cuda_fail(e, "conv_f32tc launch");
   if (prof) {

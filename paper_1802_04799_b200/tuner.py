@@ -225,11 +225,13 @@ def conv_space(name: str, desc: _abi.ConvDesc,
         summed in order), cluster_n (halo, streamed weights: CTA pairs share
         weight tiles by TMA multicast; im2col: CTA pairs -- cta_group::2,
         M = 256, each CTA loading half of the weight rows);
-      f32tc: tile_k, tile_n, stages (resident weights) and split_k of the
-        split-bf16 f32 kernel (split_k = -1: stream-K, equal (tile, k) shares)."""
+      f32tc: tile_k, tile_n, stages (resident weights), split_k (-1: stream-K,
+        equal (tile, k) shares) and cluster_n (2: CTA pairs on the im2col path
+        at tile_n 128) of the split-bf16 f32 kernel."""
     if desc.compute == _abi.COMPUTE_F32TC:
         knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128]),
-                 KnobDef("stages", [1, 2]), KnobDef("split_k", [1, 2, 3, 4, 6, 8, -1])]
+                 KnobDef("stages", [1, 2]), KnobDef("split_k", [1, 2, 3, 4, 6, 8, -1]),
+                 KnobDef("cluster_n", [1, 2])]
     else:
         knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
                  KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2]),

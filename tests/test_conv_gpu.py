@@ -325,6 +325,29 @@ def test_im2col_cta_pair(layer, batch, bn, compute):
         assert same_values(y, want, TOL_BF16), f"max rel err {max_rel_err(y, want)}"
 
 
+@pytest.mark.parametrize("split_k", [1, -1, 2])
+@pytest.mark.parametrize("layer,batch", [("C4", 3), ("C6", 2), ("C7", 1), ("C10", 3), ("C12", 1),
+                                         ("C9", 2)])
+def test_f32tc_cta_pair(layer, batch, split_k):
+    """f32tc im2col at tile_n 128 as CTA pairs (knob cluster_n = 2): the six
+    products of each K16 slice as M = 256 pair MMAs, each CTA loading half of
+    the three weight planes' rows. Without split-K every output sums the same
+    products in the same order as one CTA (bit-identical); split-K / stream-K
+    segment boundaries follow the pair grid (1e-4 bar). Odd M-tile counts
+    leave a phantom tile."""
+    hw, c, k, r, s = RESNET18_CONVS[layer]
+    x, w, b = _inputs((batch, c, hw, hw), (k, c, r, r), k, False, seed=3 + batch + sum(map(ord, layer)))
+    attrs = {"strides": (s, s), "padding": (r // 2, r // 2)}
+    epi = [("bias_add", b), ("relu",)]
+    kn = {"tile_k": 1, "tile_n": 128, "split_k": split_k}
+    y = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc", knobs=dict(kn, cluster_n=2))
+    if split_k == 1:
+        y1 = fused_conv("conv2d", x, w, attrs, epi, compute="f32tc", knobs=kn)
+        assert np.array_equal(bits(y), bits(y1))
+    want = oracle_conv("conv2d", x, w, attrs["strides"], attrs["padding"], epi)
+    assert same_values(y, want, TOL_F32TC), f"max rel err {max_rel_err(y, want)}"
+
+
 def test_cta_pair_rejects_split_k():
     hw, c, k, r, s = RESNET18_CONVS["C12"]
     x, w, b = _inputs((1, c, hw, hw), (k, c, r, r), k, False, 3)
