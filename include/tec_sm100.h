@@ -145,7 +145,13 @@ typedef struct {
  *   acc_bufs virtual_thread -> TMEM accumulator buffers (2)
  *   grid     bind(blockIdx) extent -> persistent CTAs (<= #SMs)
  *   vec      vectorize width of the depthwise kernel (channels per thread)
- *   raster   reorder of the tile loop (0 = N fastest)                  */
+ *   raster   reorder of the tile loop (0 = N fastest)
+ *   tile_k   A-operand strategy: 1 im2col TMA, 2 shifted-window halo
+ *   split_k  rfactor of the reduction over CTAs (-1: stream-K, f32tc)
+ *   cluster_n 2 = two CTAs per cluster: the halo path multicasts weight
+ *            tiles; the im2col path runs CTA pairs (tcgen05 cta_group::2,
+ *            M = 256, each CTA loading half of the weight rows)
+ *   cta_pair reserved (0)                                              */
 typedef struct {
   int64_t tile_m, tile_n, tile_k, stages, cta_pair, cluster_m, cluster_n;
   int64_t raster, swizzle, split_k, vec, unroll, acc_bufs, grid;
