@@ -286,32 +286,6 @@ def measure_int8_peak():
         return None
 
 
-def _graph_of(fn, stream):
-    import torch
-    with torch.cuda.stream(stream):
-        fn()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=stream):
-        fn()
-    return g
-
-
-def _median_ms(g, stream):
-    import torch
-    ts = []
-    for _ in range(3):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            a.record(stream)
-            g.replay()
-            b.record(stream)
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    return statistics.median(ts)
-
-
 def measure_step(compute, knobs, batch, local, rank, world, steps, warmup, peak, hbm_gbs,
                  sampler=None):
     """Times the 12-layer step at one arithmetic: K CUDA-graph replays
@@ -372,16 +346,14 @@ def measure_step(compute, knobs, batch, local, rank, world, steps, warmup, peak,
     # timestamps here move in ~2 us steps, too coarse for one 6-45 us launch:
     # a CUDA graph of R x (flush, launch) is timed against R x flush alone
     # (median of 3 each) and the difference / R is the launch's device time.
+    # The flush-only baseline is re-measured next to every layer
+    # (bench_workloads._flushed_launch_us): one baseline taken before the
+    # loop drifted with the clocks over the pass and ate the small layers.
+    from bench_workloads import _flushed_launch_us
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    reps = 10
-    flush_ms = _median_ms(_graph_of(lambda: [flush.zero_() for _ in range(reps)], stream), stream)
     per_layer = []
     for l, fl in zip(layers, flops):
-        def body(l=l):
-            for _ in range(reps):
-                flush.zero_()
-                l.launch(stream)
-        us = max(1e-3, (_median_ms(_graph_of(body, stream), stream) - flush_ms) * 1e3 / reps)
+        us = _flushed_launch_us(lambda l=l: l.launch(stream), flush, stream)
         byts = l.wl.bytes(in_b, out_b)
         ai = fl / byts
         bound_tf = min(peak, ai * hbm_gbs / 1e3)
