@@ -35,8 +35,11 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   constexpr int kA = 16384, kBP = (PAIR ? BN / 2 : BN) * 128;
-  constexpr int kPl = PROD == 6 ? 3 : 1;  // operand planes (f32tc: h, m, l)
-  constexpr int kStage = kPl * kA + kPl * kBP;
+  constexpr int kPl = PROD == 1 ? 1 : 3;  // operand planes (f32tc: h, m, l)
+  // grouped (PROD 3, BN 64): a pair CTA holds R1 = its half of [h m l] (rank
+  // order h m l / m l h) + R2 = its half of [h m] -- 5 boxes of 32 rows
+  constexpr int kBBoxes = PROD == 3 && PAIR ? 5 : kPl;
+  constexpr int kStage = kPl * kA + kBBoxes * kBP;
   uint64_t* bars = (uint64_t*)(sm + NST * kStage);
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
@@ -73,15 +76,15 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
       }
       if (LOAD) {
         const int base = (blockIdx.x / (PAIR ? 2 : 1)) * 37 + it * 11;
-        for (int pl = 0; pl < kPl; ++pl) {
+        for (int pl = 0; pl < kBBoxes; ++pl) {
           const int ra = ((base + pl * 5 + rank * 3) % 1000) * 128;
           const int rb = ((base + pl * 7 + 500) % 1000) * 128 + (PAIR ? rank * (BN / 2) : 0);
           if (PAIR) {
             const uint32_t fb = full_leader0 + s * 8;
-            tma_load_2d_pair(st + pl * kA, &tm16, fb, 0, ra);
+            if (pl < kPl) tma_load_2d_pair(st + pl * kA, &tm16, fb, 0, ra);
             tma_load_2d_pair(st + kPl * kA + pl * kBP, BN == 128 ? &tm8 : &tm4, fb, 0, rb);
           } else {
-            tma_load_2d(st + pl * kA, &tm16, &full[s], 0, ra);
+            if (pl < kPl) tma_load_2d(st + pl * kA, &tm16, &full[s], 0, ra);
             tma_load_2d(st + kPl * kA + pl * kBP, BN == 128 ? &tm16 : &tm8, &full[s], 0, rb);
           }
         }
@@ -104,6 +107,21 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
         const uint32_t acc = (it | kk) ? 1u : 0u;
         if (PROD == 1) {
           if (PAIR) mma2(S, ah, bh, id, acc); else tc_mma<MmaKind::kF16>(S, ah, bh, id, acc);
+        } else if (PROD == 3) {
+          // X = [hh0 hm0 hl0 hm1 hl1 hh1] (pair) / [hh hm hl] (one CTA)
+          constexpr uint32_t i3 = make_idesc<MmaKind::kF16>(PAIR ? 256 : 128, 3 * BN);
+          constexpr uint32_t i2 = make_idesc<MmaKind::kF16>(PAIR ? 256 : 128, 2 * BN);
+          constexpr uint32_t i1 = make_idesc<MmaKind::kF16>(PAIR ? 256 : 128, BN);
+          if (PAIR) {
+            const uint64_t r2 = make_smem_desc<128>(b + 3 * kBP + kk * 32, 1024);
+            mma2(S, ah, bh, i3, acc);
+            mma2(S + BN / 2, am, r2, i2, 1u);
+            mma2(S + BN, al, r2, i1, 1u);
+          } else {
+            tc_mma<MmaKind::kF16>(S, ah, bh, i3, acc);
+            tc_mma<MmaKind::kF16>(S + BN, am, bh, i2, 1u);
+            tc_mma<MmaKind::kF16>(S + BN, al, bh, i1, 1u);
+          }
         } else if (PAIR) {
           mma2(S, ah, bh, id, acc); mma2(T, ah, bm, id, acc); mma2(T, am, bh, id, 1u);
           mma2(T, ah, bl, id, 1u); mma2(T, al, bh, id, 1u); mma2(T, am, bm, id, 1u);
@@ -144,8 +162,8 @@ static CUtensorMap make_map(void* base, int rows, int box_rows) {
 template <bool PAIR, bool LOAD, int BN = 128, int PROD = 6, int NST = 2>
 void run(const char* name, const CUtensorMap& m16, const CUtensorMap& m8, const CUtensorMap& m4) {
   auto f = k<PAIR, LOAD, BN, PROD, NST>;
-  constexpr int kPl = PROD == 6 ? 3 : 1;
-  constexpr int kStage = kPl * 16384 + kPl * (PAIR ? BN / 2 : BN) * 128;
+  constexpr int kPl = PROD == 1 ? 1 : 3;
+  constexpr int kStage = kPl * 16384 + (PROD == 3 && PAIR ? 5 : kPl) * (PAIR ? BN / 2 : BN) * 128;
   const int smem = NST * kStage + 2048;
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   long long* d; cudaMalloc(&d, 148 * 8); cudaMemset(d, 0, 148 * 8);
@@ -167,7 +185,7 @@ void run(const char* name, const CUtensorMap& m16, const CUtensorMap& m8, const 
   std::vector<long long> h(148); cudaMemcpy(h.data(), d, 148 * 8, cudaMemcpyDeviceToHost);
   long long mx = 0; for (auto v : h) mx = v > mx ? v : mx;
   // per SM: iters x 4 K16 slices of a 128-row tile x N=128 x 6 products
-  const double flops = 148.0 * iters * 4 * PROD * 2.0 * 128 * BN * 16;
+  const double flops = 148.0 * iters * 4 * (PROD == 3 ? 6 : PROD) * 2.0 * 128 * BN * 16;
   printf("%-44s %7.1f cycles per K16 (ideal %d), %6.0f bf16 TFLOP/s\n", name, (double)mx / (iters * 4), PROD * BN / 2,
          flops / (ms * 1e-3) / 1e12);
   cudaFree(d);
@@ -184,6 +202,10 @@ int main() {
   run<false, true>("f32tc N=128: 1 CTA, A 48 KB + B 48 KB / stage", m16, m8, m4);
   run<true, false>("f32tc N=128: CTA pair, no loads", m16, m8, m4);
   run<true, true>("f32tc N=128: CTA pair, A 48 KB + B 24 KB / CTA", m16, m8, m4);
+  run<false, false, 64, 3>("f32tc grouped N=64: 1 CTA, no loads", m16, m8, m4);
+  run<false, true, 64, 3>("f32tc grouped N=64: 1 CTA, A 48 KB + B 24 KB", m16, m8, m4);
+  run<true, false, 64, 3>("f32tc grouped N=64: CTA pair, no loads", m16, m8, m4);
+  run<true, true, 64, 3>("f32tc grouped N=64: CTA pair, A 48 KB + B 20 KB", m16, m8, m4);
   run<false, false, 64, 1, 8>("bf16 N=64 x8 stages: 1 CTA, no loads", m16, m8, m4);
   run<false, true, 64, 1, 8>("bf16 N=64 x8: 1 CTA, A 16 KB + B 8 KB", m16, m8, m4);
   run<true, false, 64, 1, 8>("bf16 N=64 x8: CTA pair, no loads", m16, m8, m4);
