@@ -144,6 +144,7 @@ struct DwTmaShape {
   int32_t cblocks;    // c / cb
   int32_t buf_bytes;  // ni * rows_in * cols_in * cb * elem, rounded to 128
   int32_t ni;         // images per tile (TMA box N extent)
+  float neg_zero;     // -0.0f, set by the host: the packed f32 products' addend
 };
 
 // max_pool2d / global_avg_pool on NHWC activations (pool.cu).

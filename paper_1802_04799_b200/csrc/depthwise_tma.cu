@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
   constexpr int VEC = 16 / static_cast<int>(sizeof(InT));
   constexpr int ES = static_cast<int>(sizeof(InT));
   const int colb = COLB ? COLB : t.cb * ES;
+  const float nz = t.neg_zero;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
                                              ~uintptr_t(127));
@@ -232,14 +233,23 @@ __global__ void __launch_bounds__(kDwtThreads, 1)
                         : "+f"(acc2[i][j].x), "+f"(acc2[i][j].y)
                         : "r"(xb[j]), "r"(wb[rh * 3 + rw][j]));
                   } else {
-                    // scalar products (FMUL), packed adds (FADD2): the
-                    // reference's facc + x*w, each rounded, with a quarter
-                    // fewer FP instructions. (Packed products -- mul.rn.f32x2,
-                    // __fmul2_rn -- are contracted with the add into FFMA2 by
-                    // ptxas even at -fmad=false: not bit-exact.)
-                    acc2[i][j] = __fadd2_rn(acc2[i][j],
-                                            make_float2(__fmul_rn(x[2 * j], w2[rh * 3 + rw][j].x),
-                                                        __fmul_rn(x[2 * j + 1], w2[rh * 3 + rw][j].y)));
+                    // the reference's facc + x*w, each rounded, two lanes
+                    // at a time: the product as FFMA2 x*w + (-0) -- exactly
+                    // the rounded product -- with the -0 a kernel parameter
+                    // ptxas cannot see through, then FADD2. (A plain packed
+                    // multiply -- mul.rn.f32x2, __fmul2_rn -- is contracted
+                    // with the add into one FFMA2 by ptxas even at
+                    // -fmad=false: not bit-exact.)
+                    float2 prod;
+                    asm("{.reg .b64 xa, za, pa;\n\t"
+                        "mov.b64 xa, {%2, %3};\n\t"
+                        "mov.b64 za, {%5, %5};\n\t"
+                        "fma.rn.f32x2 pa, xa, %4, za;\n\t"
+                        "mov.b64 {%0, %1}, pa;}"
+                        : "=f"(prod.x), "=f"(prod.y)
+                        : "f"(x[2 * j]), "f"(x[2 * j + 1]),
+                          "l"(*reinterpret_cast<const uint64_t*>(&w2[rh * 3 + rw][j])), "f"(nz));
+                    acc2[i][j] = __fadd2_rn(acc2[i][j], prod);
                   }
                 }
               }
@@ -404,6 +414,7 @@ bool dw_tma_plan(const DepthwiseParams& p, DwTmaShape* t) {
   if (p.c % cb || (cb * es) % 16) return false;
   t->cb = cb;
   t->cblocks = p.c / cb;
+  t->neg_zero = -0.0f;
   // whole kTW-column strips: the last strip reads TMA zero-fill columns
   t->cols_in = (((p.ow + kTW - 1) / kTW) * kTW - 1) * p.sw + 3;
   // 64-byte channel rows (D1: 32 bf16 channels): an odd number of columns
