@@ -36,6 +36,15 @@ CASES = [
     ("bf16-halo-multicast", "conv2d", (3, 64, 12, 12), (64, 64, 3, 3), 1, 1, "bf16",
      {"tile_k": 2, "stages": 1, "cluster_n": 2}, False),
     ("bf16-s2d-stem", "conv2d", (1, 3, 32, 32), (64, 3, 7, 7), 2, 3, "bf16", {}, False),
+    # CTA pairs (cta_group::2): M = 49 leaves the pair's second tile a phantom
+    ("bf16-im2col-pair", "conv2d", (1, 128, 7, 7), (256, 128, 3, 3), 1, 1, "bf16",
+     {"tile_k": 1, "tile_n": 128, "cluster_n": 2}, False),
+    ("i8-im2col-pair", "conv2d", (3, 64, 9, 9), (128, 64, 3, 3), 1, 1, "i8",
+     {"tile_k": 1, "tile_n": 64, "cluster_n": 2}, False),
+    ("f32tc-pair-streamk", "conv2d", (1, 128, 14, 14), (128, 128, 3, 3), 1, 1, "f32tc",
+     {"tile_k": 1, "tile_n": 128, "split_k": -1, "cluster_n": 2}, False),
+    ("f32tc-pair", "conv2d", (3, 64, 9, 9), (128, 64, 3, 3), 1, 1, "f32tc",
+     {"tile_k": 1, "tile_n": 128, "cluster_n": 2}, True),
     ("i8-im2col", "conv2d", (2, 64, 9, 9), (64, 64, 3, 3), 2, 1, "i8", {"tile_k": 1}, False),
     ("i8-halo", "conv2d", (2, 64, 10, 10), (64, 64, 3, 3), 1, 1, "i8", {"tile_k": 2}, False),
     ("f32-exact", "conv2d", (1, 16, 8, 8), (16, 16, 3, 3), 1, 1, "f32", {}, True),
@@ -147,7 +156,12 @@ def device_guard_and_determinism(name, op, xs, ws, s, p, compute, knobs, residua
         torch.cuda.synchronize()
         outs.append(buf[guard:guard + n_out * es].clone())
     canary_ok = bool((buf[:guard] == 0xA5).all() and (buf[guard + n_out * es:] == 0xA5).all())
-    same = all(torch.equal(o, outs[0]) for o in outs[1:])
+    if knobs.get("split_k") == -1:
+        # stream-K: the segment boundaries follow the grid (each grid sums in
+        # a fixed order); repeats at one grid must match bit for bit
+        same = torch.equal(outs[0], outs[1])
+    else:
+        same = all(torch.equal(o, outs[0]) for o in outs[1:])
     return canary_ok, same
 
 
