@@ -25,6 +25,8 @@
 //    -> scale/bias/residual/relu on 32-wide register vectors with 128-bit
 //    operand loads -> 128-bit global stores; intermediates never touch HBM.
 //  * persistent grid (one CTA per SM), tiles strided by gridDim.x.
+//  * CTA pairs (knob cluster_n = 2): tcgen05 cta_group::2, a 256-row tile
+//    per pair with half of the weight rows in each CTA (`PAIR` below).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -245,11 +247,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // tile is stepped instead of divided.
       const uint64_t adesc0 = make_smem_desc<SWZ>(smem_u32(sA), 8 * SWZ);
       const uint64_t bdesc0 = make_smem_desc<SWZ>(smem_u32(sB), 8 * SWZ);
-      const int nsplit = splits, kps_ = kps, kit = k_iters, ntiles = num_tiles;
+      const int nsplit = splits, kps_ = kps, kit = k_iters;
       const bool dbg = p.dbg != nullptr;
       int split = static_cast<int>(blockIdx.x) % nsplit;
       const int dsplit = static_cast<int>(gridDim.x) % nsplit;
-      (void)ntiles;
       for (int u = t_first; u < t_count; u += t_step, ++local) {
         const int acc = local & (nacc - 1);
         const uint32_t use = static_cast<uint32_t>(local >> acc_shift);
