@@ -207,9 +207,34 @@ def resnet18_line(args, bench, knobs_file=None, compute="bf16"):
     return line if rank == 0 else None
 
 
+def _graph_conv_epilogue(n, compute):
+    """The epilogue program the executor runs for a fused conv node, for
+    tuning: its op codes and (int8) the requantize / i8-shortcut scalars --
+    a residual or requantizing epilogue changes which kernel is fastest
+    (the halo kernel's i8 residual reads cost it 2x on the 56x56 blocks)."""
+    from paper_1802_04799_b200 import _abi
+    from paper_1802_04799_b200.executor import _i8_shortcut_scale, split_conv_members
+    try:
+        _, items, sides, tail = split_conv_members(n)
+    except Exception:  # noqa: BLE001 -- not an epilogue the executor fuses
+        return (_abi.EPI_BIAS, _abi.EPI_RELU), None
+    code = {"bias_add": _abi.EPI_BIAS, "add": _abi.EPI_ADD, "relu": _abi.EPI_RELU,
+            "scale": _abi.EPI_SCALE, "mul": _abi.EPI_MUL}
+    ops = [code[m.op] for m in items if m.op in code]
+    params = None
+    if compute == "i8" and len(tail) == 1 and tail[0].op == "requantize":
+        ops.append(_abi.EPI_REQUANTIZE)
+        # representative scalars (the cost does not depend on their values
+        # within the 32-bit form): one tuning per shape and program
+        params = {"rq_mult": 900, "rq_shift": 16}
+        if _abi.EPI_ADD in ops and sides and _i8_shortcut_scale(sides[0][2]) is not None:
+            params.update(residual_i8=1, residual_scale=37)
+    return tuple(ops), params
+
+
 def _tune_graph_convs(g, device, args, compute="bf16"):
-    """Tune each distinct conv shape of the graph once (bias+relu epilogue
-    as the stand-in cost); returns knobs keyed by fused node id."""
+    """Tune each distinct (conv shape, epilogue program) of the graph once;
+    returns knobs keyed by fused node id."""
     from paper_1802_04799_b200 import _abi
     from paper_1802_04799_b200.graph import fuse_pass
     from paper_1802_04799_b200.ops import conv_desc
@@ -225,9 +250,11 @@ def _tune_graph_convs(g, device, args, compute="bf16"):
         d = conv_desc("conv2d", xs, ws_, root.attrs,
                       {"bf16": _abi.COMPUTE_BF16, "f32tc": _abi.COMPUTE_F32TC,
                        "i8": _abi.COMPUTE_I8}[compute])
-        key = (tuple(xs), tuple(ws_), tuple(root.attrs.get("strides", (1, 1))))
+        ops, params = _graph_conv_epilogue(n, compute)
+        key = (tuple(xs), tuple(ws_), tuple(root.attrs.get("strides", (1, 1))), ops,
+               tuple(sorted((params or {}).items())))
         if key not in best:
-            space = conv_space(str(key), d)
+            space = conv_space(str(key), d, ops, params)
             rec = tune(space, budget=min(space.size(), 16), batch_size=8, method="ml",
                        devices=[device], repeats=3)
             best[key] = rec.config if rec else {}

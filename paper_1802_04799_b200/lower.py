@@ -112,8 +112,11 @@ class KernelPlan:
 
 def lower(desc: _abi.ConvDesc, config: Optional[Dict[str, int]] = None,
           epilogue: Sequence[int] = (_abi.EPI_BIAS, _abi.EPI_RELU),
-          opts: Optional[LowerOptions] = None) -> KernelPlan:
-    """Config -> the kernel the sm100 backend runs for it (no launch)."""
+          opts: Optional[LowerOptions] = None,
+          epi_params: Optional[Dict[str, int]] = None) -> KernelPlan:
+    """Config -> the kernel the sm100 backend runs for it (no launch).
+    epi_params: the int8 epilogue's scalars (rq_mult, rq_shift, residual_i8,
+    residual_scale) when the program requantizes / reads an i8 shortcut."""
     opts = opts or LowerOptions()
     if opts.target != "sm100":
         raise TecError(E_LOWERING, f"target '{opts.target}' is not this backend (use 'sm100')")
@@ -128,6 +131,8 @@ def lower(desc: _abi.ConvDesc, config: Optional[Dict[str, int]] = None,
         epi.residual = 1
     if _abi.EPI_MUL in epilogue:
         epi.mul_operand = 1
+    for k, v in (epi_params or {}).items():
+        setattr(epi, k, v)
     kn = _abi.Knobs(**(config or {}))
     out = _abi.KernelPlan()
     _abi.check(_abi.load().tec_conv_plan(C.byref(desc), C.byref(epi), C.byref(kn), C.byref(out)))

@@ -75,6 +75,8 @@ class KnobSpace:
     knobs: List[KnobDef]
     desc: Optional[_abi.ConvDesc] = None
     epilogue: Sequence[int] = (_abi.EPI_BIAS, _abi.EPI_RELU)
+    # int8 epilogue scalars (rq_mult, rq_shift, residual_i8, residual_scale)
+    epi_params: Optional[Dict[str, int]] = None
     target: str = "sm100"
     instantiate: Optional[Callable[[Config], object]] = None
     _legal: Optional[List[Config]] = field(default=None, repr=False)
@@ -202,20 +204,22 @@ def load_trials(path: str) -> List[TrialRecord]:
     return out
 
 
-def _plan_instantiate(desc: _abi.ConvDesc, epilogue: Sequence[int]):
+def _plan_instantiate(desc: _abi.ConvDesc, epilogue: Sequence[int],
+                      epi_params: Optional[Dict[str, int]] = None):
     """Config -> the kernel the native lowering picks (lower.lower, i.e.
     tec_conv_plan); a LoweringError marks the config illegal."""
     from .lower import lower
 
     def inst(cfg: Config):
-        p = lower(desc, cfg, epilogue)
+        p = lower(desc, cfg, epilogue, epi_params=epi_params)
         return (p.family, p.tile_m, p.tile_n, p.stages, p.split_k, p.cluster, p.grid,
                 p.smem_bytes, p.tmem_cols, p.tma_store)
     return inst
 
 
 def conv_space(name: str, desc: _abi.ConvDesc,
-               epilogue: Sequence[int] = (_abi.EPI_BIAS, _abi.EPI_RELU)) -> KnobSpace:
+               epilogue: Sequence[int] = (_abi.EPI_BIAS, _abi.EPI_RELU),
+               epi_params: Optional[Dict[str, int]] = None) -> KnobSpace:
     """The B200 conv template's knob grid (SURVEY 8a knob mapping), made
     conditional by the native lowering:
       bf16 / i8: tile_k = A-operand strategy (1 im2col TMA, 2 shifted-window
@@ -236,8 +240,8 @@ def conv_space(name: str, desc: _abi.ConvDesc,
         knobs = [KnobDef("tile_k", [1, 2]), KnobDef("tile_n", [64, 128, 256]),
                  KnobDef("tile_m", [128, 256, 512]), KnobDef("stages", [1, 2]),
                  KnobDef("split_k", [1, 2, 3, 4]), KnobDef("cluster_n", [1, 2])]
-    return KnobSpace(name, knobs, desc, tuple(epilogue),
-                     instantiate=_plan_instantiate(desc, tuple(epilogue)))
+    return KnobSpace(name, knobs, desc, tuple(epilogue), epi_params=epi_params,
+                     instantiate=_plan_instantiate(desc, tuple(epilogue), epi_params))
 
 
 def dw_space(name: str, desc: _abi.ConvDesc,
@@ -365,6 +369,8 @@ def _measure_one(space: KnobSpace, cfg: Config, device: int, warmup: int,
     epi.n_ops = len(space.epilogue)
     epi.bias = 1 if _abi.EPI_BIAS in space.epilogue else None  # replaced on device
     epi.residual = 1 if _abi.EPI_ADD in space.epilogue else None
+    for k, v in (space.epi_params or {}).items():
+        setattr(epi, k, v)
     us = C.c_double(0)
     st = lib.tec_measure(C.byref(space.desc), C.byref(epi), C.byref(kn), device, warmup,
                          repeats, 1, C.byref(us))
