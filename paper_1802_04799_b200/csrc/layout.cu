@@ -286,46 +286,66 @@ __global__ void pack_s2d_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
 }
 
 // f32tc interleaved split (cp = 64, c <= 4): one thread per space-to-depth
-// pixel writes its [h16 | m16 | l16 | 0] 128-byte pixel as eight 16-byte
-// stores (the per-element kernel above took 1.7 ms for the ResNet-18 b256
-// stem: 64-bit divisions and 2-byte stores).
-__global__ void pack_s2d_split3i_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                                        int n, int c, int h, int w, int ph, int pw, int h2, int w2) {
+// pixel builds its [h16 | m16 | l16 | 0] 128-byte pixel; the block's 256
+// pixels (32 KB, contiguous in the output) go through shared memory so the
+// stores are coalesced 16-byte runs across the warp (the per-element kernel
+// above took 1.7 ms for the ResNet-18 b256 stem; per-thread 128-byte rows
+// stored directly, 254 us). Chunk c of pixel p sits at slot p * 8 + (c ^ (p
+// & 7)): the row-per-thread writes are bank-conflict free.
+constexpr int kS2dSplitPx = 256;
+__global__ void __launch_bounds__(kS2dSplitPx) pack_s2d_split3i_kernel(
+    const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int n, int c, int h, int w,
+    int ph, int pw, int h2, int w2) {
+  __shared__ uint4 st[kS2dSplitPx * 8];
   const int total = n * h2 * w2;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int jj = i % w2;
-    const int t = i / w2;
-    const int ii = t % h2;
-    const int nn = t / h2;
+  const int t = static_cast<int>(threadIdx.x);
+  for (int base = blockIdx.x * kS2dSplitPx; base < total; base += gridDim.x * kS2dSplitPx) {
+    const int i = base + t;
     uint32_t wd[3][8];  // plane x 16 channels as bf16 pairs
 #pragma unroll
     for (int pl = 0; pl < 3; ++pl)
 #pragma unroll
       for (int k = 0; k < 8; ++k) wd[pl][k] = 0u;
+    if (i < total) {
+      const int jj = i % w2;
+      const int tt = i / w2;
+      const int ii = tt % h2;
+      const int nn = tt / h2;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int y = 2 * ii + q / 2 - ph, x = 2 * jj + q % 2 - pw;
-      const bool in_img = y >= 0 && y < h && x >= 0 && x < w;
+      for (int q = 0; q < 4; ++q) {
+        const int y = 2 * ii + q / 2 - ph, x = 2 * jj + q % 2 - pw;
+        const bool in_img = y >= 0 && y < h && x >= 0 && x < w;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        if (cc >= c) break;
-        const float v = in_img ? in[((static_cast<int64_t>(nn) * c + cc) * h + y) * w + x] : 0.0f;
-        const int e = q * c + cc;  // channel (dy*2+dx)*C + c
+        for (int cc = 0; cc < 4; ++cc) {
+          if (cc >= c) break;
+          const float v = in_img ? in[((static_cast<int64_t>(nn) * c + cc) * h + y) * w + x] : 0.0f;
+          const int e = q * c + cc;  // channel (dy*2+dx)*C + c
 #pragma unroll
-        for (int pl = 0; pl < 3; ++pl) {
-          const uint32_t b = __bfloat16_as_ushort(split3(v, pl));
-          wd[pl][e >> 1] |= (e & 1) ? (b << 16) : b;
+          for (int pl = 0; pl < 3; ++pl) {
+            const uint32_t b = __bfloat16_as_ushort(split3(v, pl));
+            wd[pl][e >> 1] |= (e & 1) ? (b << 16) : b;
+          }
         }
       }
     }
-    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(i) * 64);
+    __syncthreads();  // the previous round's reads of st are done
+    const int sw = t & 7;
 #pragma unroll
     for (int pl = 0; pl < 3; ++pl) {
-      dst[2 * pl] = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
-      dst[2 * pl + 1] = make_uint4(wd[pl][4], wd[pl][5], wd[pl][6], wd[pl][7]);
+      st[t * 8 + ((2 * pl) ^ sw)] = make_uint4(wd[pl][0], wd[pl][1], wd[pl][2], wd[pl][3]);
+      st[t * 8 + ((2 * pl + 1) ^ sw)] = make_uint4(wd[pl][4], wd[pl][5], wd[pl][6], wd[pl][7]);
     }
-    dst[6] = make_uint4(0u, 0u, 0u, 0u);
-    dst[7] = make_uint4(0u, 0u, 0u, 0u);
+    st[t * 8 + (6 ^ sw)] = make_uint4(0u, 0u, 0u, 0u);
+    st[t * 8 + (7 ^ sw)] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    const int npx = min(kS2dSplitPx, total - base);
+    uint4* dst = reinterpret_cast<uint4*>(out + static_cast<int64_t>(base) * 64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = k * kS2dSplitPx + t;  // 16-byte chunk of the block's output
+      const int p = idx >> 3, ch = idx & 7;
+      if (p < npx) dst[idx] = st[p * 8 + (ch ^ (p & 7))];
+    }
   }
 }
 
@@ -600,8 +620,8 @@ int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c
   }
   if (in_type == kF32 && mode == kPackSplit3I && cp == 64 && c <= 4 && n * h2 * w2 < (1ll << 31)) {
     const int64_t px = n * h2 * w2;
-    const int blocks = static_cast<int>(std::min<int64_t>((px + 255) / 256, 148 * 32));
-    pack_s2d_split3i_kernel<<<blocks, 256, 0, st>>>(
+    const int blocks = static_cast<int>(std::min<int64_t>((px + kS2dSplitPx - 1) / kS2dSplitPx, 148 * 16));
+    pack_s2d_split3i_kernel<<<blocks, kS2dSplitPx, 0, st>>>(
         static_cast<const float*>(in), static_cast<__nv_bfloat16*>(out), static_cast<int>(n),
         static_cast<int>(c), static_cast<int>(h), static_cast<int>(w), static_cast<int>(ph),
         static_cast<int>(pw), static_cast<int>(h2), static_cast<int>(w2));
