@@ -293,9 +293,14 @@ __global__ void pack_s2d_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
 // stored directly, 254 us). Chunk c of pixel p sits at slot p * 8 + (c ^ (p
 // & 7)): the row-per-thread writes are bank-conflict free.
 constexpr int kS2dSplitPx = 256;
+// C > 0: the channel count at compile time (the RGB stem: 3) -- the
+// channel slot of every value is then a constant and the packed words stay
+// in registers (with a runtime count they are dynamically indexed arrays)
+template <int C>
 __global__ void __launch_bounds__(kS2dSplitPx) pack_s2d_split3i_kernel(
-    const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int n, int c, int h, int w,
-    int ph, int pw, int h2, int w2) {
+    const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int n, int c_arg, int h,
+    int w, int ph, int pw, int h2, int w2) {
+  const int c = C ? C : c_arg;
   __shared__ uint4 st[kS2dSplitPx * 8];
   const int total = n * h2 * w2;
   const int t = static_cast<int>(threadIdx.x);
@@ -352,8 +357,10 @@ __global__ void __launch_bounds__(kS2dSplitPx) pack_s2d_split3i_kernel(
 // int8 (cp = 32, c <= 8): one thread per space-to-depth pixel, its 32
 // channel bytes as two 16-byte stores (the per-element kernel above made
 // one 1-byte store per thread: 770 us for the ResNet-18 b256 stem).
+template <int C>  // compile-time channel count (0: runtime), as above
 __global__ void pack_s2d_i8_kernel(const int8_t* __restrict__ in, int8_t* __restrict__ out,
-                                   int n, int c, int h, int w, int ph, int pw, int h2, int w2) {
+                                   int n, int c_arg, int h, int w, int ph, int pw, int h2, int w2) {
+  const int c = C ? C : c_arg;
   const int total = n * h2 * w2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int jj = i % w2;
@@ -390,9 +397,11 @@ __global__ void pack_s2d_i8_kernel(const int8_t* __restrict__ in, int8_t* __rest
 // this one streams both directions.
 constexpr int kS2dMaxW2 = 128;
 constexpr int kS2dRows = 4;  // s2d rows per CTA
+template <int C>  // compile-time channel count (0: runtime), as above
 __global__ void __launch_bounds__(256) pack_s2d_rows_bf16_kernel(
-    const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int c, int h, int w, int ph,
+    const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int c_arg, int h, int w, int ph,
     int pw, int h2, int w2) {
+  const int c = C ? C : c_arg;
   // [channel][input row of the CTA][staged column]
   __shared__ float tile[4][2 * kS2dRows][2 * kS2dMaxW2];
   const int ii0 = blockIdx.x * kS2dRows, nn = blockIdx.y;
@@ -600,9 +609,9 @@ int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c
                     int mode, cudaStream_t st) {
   if (in_type != kI8 && mode == kPackBF16 && cp == 16 && c <= 4 && w % 4 == 0 &&
       w2 <= kS2dMaxW2 && 2 * w2 >= w + pw && n <= 65535 && h2 <= (1 << 30)) {
-    pack_s2d_rows_bf16_kernel<<<dim3(static_cast<unsigned>((h2 + kS2dRows - 1) / kS2dRows),
-                                     static_cast<unsigned>(n)),
-                                256, 0, st>>>(static_cast<const float*>(in),
+    auto kfn = c == 3 ? pack_s2d_rows_bf16_kernel<3> : pack_s2d_rows_bf16_kernel<0>;
+    kfn<<<dim3(static_cast<unsigned>((h2 + kS2dRows - 1) / kS2dRows), static_cast<unsigned>(n)),
+          256, 0, st>>>(static_cast<const float*>(in),
                                          static_cast<__nv_bfloat16*>(out), static_cast<int>(c),
                                          static_cast<int>(h), static_cast<int>(w),
                                          static_cast<int>(ph), static_cast<int>(pw),
@@ -621,7 +630,8 @@ int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c
   if (in_type == kF32 && mode == kPackSplit3I && cp == 64 && c <= 4 && n * h2 * w2 < (1ll << 31)) {
     const int64_t px = n * h2 * w2;
     const int blocks = static_cast<int>(std::min<int64_t>((px + kS2dSplitPx - 1) / kS2dSplitPx, 148 * 16));
-    pack_s2d_split3i_kernel<<<blocks, kS2dSplitPx, 0, st>>>(
+    auto kfn = c == 3 ? pack_s2d_split3i_kernel<3> : pack_s2d_split3i_kernel<0>;
+    kfn<<<blocks, kS2dSplitPx, 0, st>>>(
         static_cast<const float*>(in), static_cast<__nv_bfloat16*>(out), static_cast<int>(n),
         static_cast<int>(c), static_cast<int>(h), static_cast<int>(w), static_cast<int>(ph),
         static_cast<int>(pw), static_cast<int>(h2), static_cast<int>(w2));
@@ -630,7 +640,8 @@ int launch_pack_s2d(const void* in, int in_type, void* out, int64_t n, int64_t c
   if (in_type == kI8 && mode == kPackI8 && cp == 32 && c <= 8 && n * h2 * w2 < (1ll << 31)) {
     const int64_t px = n * h2 * w2;
     const int blocks = static_cast<int>(std::min<int64_t>((px + 255) / 256, 148 * 32));
-    pack_s2d_i8_kernel<<<blocks, 256, 0, st>>>(
+    auto kfn = c == 3 ? pack_s2d_i8_kernel<3> : pack_s2d_i8_kernel<0>;
+    kfn<<<blocks, 256, 0, st>>>(
         static_cast<const int8_t*>(in), static_cast<int8_t*>(out), static_cast<int>(n),
         static_cast<int>(c), static_cast<int>(h), static_cast<int>(w), static_cast<int>(ph),
         static_cast<int>(pw), static_cast<int>(h2), static_cast<int>(w2));

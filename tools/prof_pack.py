@@ -1,5 +1,5 @@
-"""Time tec_activation_pack (NCHW f32 -> the conv's packed layout) for a
-ResNet-18 layer at a batch: python tools/prof_pack.py [LAYER] [BATCH]."""
+"""Time tec_activation_pack (NCHW input -> the conv's packed layout) for a
+ResNet-18 layer at a batch: python tools/prof_pack.py [LAYER] [BATCH] [bf16|i8|f32tc]."""
 import ctypes as C
 import os
 import sys
@@ -14,10 +14,12 @@ from paper_1802_04799_b200.workloads import resnet_layer
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 lib = _abi.load()
-d = make_desc(resnet_layer(name, batch), "bf16")
+compute = sys.argv[3] if len(sys.argv) > 3 else "bf16"
+d = make_desc(resnet_layer(name, batch), compute)
 lay = _abi.ConvLayout()
 _abi.check(lib.tec_conv_layout_of(C.byref(d), C.byref(lay)))
-x = torch.rand(d.n * d.c * d.h * d.w, device="cuda")
+x = (torch.randint(-8, 8, (d.n * d.c * d.h * d.w,), dtype=torch.int8, device="cuda")
+     if compute == "i8" else torch.rand(d.n * d.c * d.h * d.w, device="cuda"))
 y = torch.empty(lay.act_bytes, dtype=torch.uint8, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 for _ in range(3):
@@ -31,5 +33,5 @@ for _ in range(reps):
 b.record()
 torch.cuda.synchronize()
 us = a.elapsed_time(b) * 1e3 / reps
-nbytes = x.numel() * 4 + lay.act_bytes
-print(f"{name} b{batch} pack: {us:.1f} us, {nbytes / 1e6:.0f} MB, {nbytes / us / 1e6:.2f} TB/s")
+nbytes = x.numel() * x.element_size() + lay.act_bytes
+print(f"{name} b{batch} {compute} pack: {us:.1f} us, {nbytes / 1e6:.0f} MB, {nbytes / us / 1e6:.2f} TB/s")
