@@ -30,9 +30,13 @@ __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
 // One thread: one output pixel x 16 bytes of channels (32-bit index math:
-// 64-bit divisions per element dominated the first version).
-template <typename T>
+// 64-bit divisions per element dominated the first version). K3 = the
+// ResNet stem's 3x3 / stride-2 window at compile time: the tap loops unroll
+// and the nine 16-byte loads issue together (runtime bounds kept the walk
+// one dependent load at a time).
+template <typename T, bool K3 = false>
 __global__ void max_pool_kernel(PoolParams p) {
+  const int pr = K3 ? 3 : p.r, ps = K3 ? 3 : p.s, psh = K3 ? 2 : p.sh, psw = K3 ? 2 : p.sw;
   constexpr int V = Lanes<T>::N;
   const int cv = p.c / V;
   const uint32_t total = static_cast<uint32_t>(p.n) * p.oh * p.ow * cv;
@@ -46,11 +50,13 @@ __global__ void max_pool_kernel(PoolParams p) {
     T best[V];
     bool any = false;
     const T* base = static_cast<const T*>(p.x) + static_cast<int64_t>(n) * p.h * p.w * p.c + v * V;
-    for (int rh = 0; rh < p.r; ++rh) {
-      const int ih = oh * p.sh + rh - p.ph;
+#pragma unroll
+    for (int rh = 0; rh < pr; ++rh) {
+      const int ih = oh * psh + rh - p.ph;
       if (ih < 0 || ih >= p.h) continue;
-      for (int rw = 0; rw < p.s; ++rw) {
-        const int iw = ow * p.sw + rw - p.pw;
+#pragma unroll
+      for (int rw = 0; rw < ps; ++rw) {
+        const int iw = ow * psw + rw - p.pw;
         if (iw < 0 || iw >= p.w) continue;
         uint4 raw = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * p.w + iw) * p.c));
         const T* t = reinterpret_cast<const T*>(&raw);
@@ -75,7 +81,9 @@ __global__ void max_pool_kernel(PoolParams p) {
 // int8: the same walk on 16 channels as four SIMD words (__vmaxs4: a
 // per-byte signed max per instruction; the generic kernel's per-byte
 // compare/select went through local memory).
+template <bool K3 = false>
 __global__ void max_pool_i8_kernel(PoolParams p) {
+  const int pr = K3 ? 3 : p.r, ps = K3 ? 3 : p.s, psh = K3 ? 2 : p.sh, psw = K3 ? 2 : p.sw;
   const int cv = p.c / 16;
   const uint32_t total = static_cast<uint32_t>(p.n) * p.oh * p.ow * cv;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -88,11 +96,13 @@ __global__ void max_pool_i8_kernel(PoolParams p) {
     uint4 best = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);  // -128
     bool any = false;
     const int8_t* base = static_cast<const int8_t*>(p.x) + static_cast<int64_t>(n) * p.h * p.w * p.c + v * 16;
-    for (int rh = 0; rh < p.r; ++rh) {
-      const int ih = oh * p.sh + rh - p.ph;
+#pragma unroll
+    for (int rh = 0; rh < pr; ++rh) {
+      const int ih = oh * psh + rh - p.ph;
       if (ih < 0 || ih >= p.h) continue;
-      for (int rw = 0; rw < p.s; ++rw) {
-        const int iw = ow * p.sw + rw - p.pw;
+#pragma unroll
+      for (int rw = 0; rw < ps; ++rw) {
+        const int iw = ow * psw + rw - p.pw;
         if (iw < 0 || iw >= p.w) continue;
         const uint4 t = __ldg(reinterpret_cast<const uint4*>(base + (static_cast<int64_t>(ih) * p.w + iw) * p.c));
         best.x = __vmaxs4(best.x, t.x);
@@ -158,11 +168,21 @@ int launch_max_pool(const PoolParams& p, cudaStream_t st) {
   if (static_cast<int64_t>(p.n) * p.oh * p.ow * (p.c * bytes / 16) >= (int64_t(1) << 31)) return -1;
   const int64_t threads = static_cast<int64_t>(p.n) * p.oh * p.ow * (p.c * bytes / 16);
   const int block = 256, grid = grid_for(threads, block);
+  const bool k3 = p.r == 3 && p.s == 3 && p.sh == 2 && p.sw == 2;
   switch (p.type) {
-    case kBF16: max_pool_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(p); break;
-    case kF32: max_pool_kernel<float><<<grid, block, 0, st>>>(p); break;
+    case kBF16:
+      if (k3) max_pool_kernel<__nv_bfloat16, true><<<grid, block, 0, st>>>(p);
+      else max_pool_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(p);
+      break;
+    case kF32:
+      if (k3) max_pool_kernel<float, true><<<grid, block, 0, st>>>(p);
+      else max_pool_kernel<float><<<grid, block, 0, st>>>(p);
+      break;
     case kI32: max_pool_kernel<int32_t><<<grid, block, 0, st>>>(p); break;
-    case kI8: max_pool_i8_kernel<<<grid, block, 0, st>>>(p); break;
+    case kI8:
+      if (k3) max_pool_i8_kernel<true><<<grid, block, 0, st>>>(p);
+      else max_pool_i8_kernel<<<grid, block, 0, st>>>(p);
+      break;
     default: return -1;
   }
   return cudaGetLastError();
