@@ -344,3 +344,24 @@ def test_int8_graph_overflow_is_reported():
     assert ei.value.code == "FoldOverflow"
     small = dg.run({"x": np.zeros((1, 32, 8, 8), np.int8)})["q"]
     assert not small.any()
+
+
+def test_graph_tuning_keys_carry_the_epilogue_program():
+    """bench_workloads tunes each (conv shape, epilogue program) of a graph:
+    the int8 residual blocks are measured with their bias + i8-shortcut add +
+    relu + requantize program, the plain ones with bias (+ relu) + requantize,
+    bf16 blocks with or without the residual add."""
+    import bench_workloads as bw
+    from paper_1802_04799_b200 import _abi
+    progs = {}
+    for compute, g in (("i8", resnet18_graph(2, image=64, width=16, head=False, dtype="i8")),
+                       ("bf16", resnet18_graph(2, image=64, width=16))):
+        f = fuse_pass(g)
+        progs[compute] = {bw._graph_conv_epilogue(n, compute)[0]: bw._graph_conv_epilogue(n, compute)[1]
+                          for n in f.nodes if n.op == "fused" and n.members[0].op == "conv2d"}
+    res_q = (_abi.EPI_BIAS, _abi.EPI_ADD, _abi.EPI_RELU, _abi.EPI_REQUANTIZE)
+    assert res_q in progs["i8"] and progs["i8"][res_q]["residual_i8"] == 1
+    assert (_abi.EPI_BIAS, _abi.EPI_RELU, _abi.EPI_REQUANTIZE) in progs["i8"]
+    assert all(p["rq_shift"] == 16 for p in progs["i8"].values())
+    assert (_abi.EPI_BIAS, _abi.EPI_ADD, _abi.EPI_RELU) in progs["bf16"]
+    assert all(p is None for p in progs["bf16"].values())
