@@ -283,6 +283,9 @@ int main() {
       {"bf16x6, small acc, chunk 256", 6, {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 1}, {2, 0, 1}, {1, 1, 1}}, 256},
       {"bf16x6, small acc, chunk 128", 6, {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 1}, {2, 0, 1}, {1, 1, 1}}, 128},
       {"bf16x6, small acc, chunk 64", 6, {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 1}, {2, 0, 1}, {1, 1, 1}}, 64},
+      {"bf16x5 (no mm), small acc, chunk 256", 5, {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {0, 2, 1}, {2, 0, 1}}, 256},
+      {"bf16x4 (no hl, lh), small acc, chunk 256", 4, {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}, {1, 1, 1}}, 256},
+      {"bf16x3 (hh,hm,mh), small acc, chunk 256", 3, {{0, 0, 0}, {0, 1, 1}, {1, 0, 1}}, 256},
   };
   for (auto& c : bc) {
     Job j{}; j.kind = 1; j.K = K; j.chunk = c.chunk; j.nprod = c.nprod; j.planes = 3;
