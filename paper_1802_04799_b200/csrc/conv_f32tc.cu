@@ -594,27 +594,48 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t x = tmem_base + sb * Cfg::kXCols;
           const int prep_at = R * S > 3 ? R * S - 3 : 0;
           uint64_t bh = bdesc0;
-          int slot = cur_s0, tap = 0;
-          for (int r = 0; r < R; ++r) {
-            uint64_t ah = adesc0 + static_cast<uint64_t>(slot) * hstep;
-            slot = slot + 1 == nrows ? 0 : slot + 1;
-            for (int s = 0; s < S; ++s, ++tap) {
-              tc_mma<MmaKind::kF16>(x, ah, bh, idesc3, (r | s) != 0 ? 1u : 0u);
-              tc_mma<MmaKind::kF16>(x + BN, ah + 2, bh, idesc2, 1u);  // A_m: +32 B
-              tc_mma<MmaKind::kF16>(x + BN, ah + 4, bh, idesc, 1u);   // A_l: +64 B
-              ah += SWZ >> 4;
-              bh += Cfg::kBStage >> 4;
-              if (tap == prep_at && next_same) {
-                ++f_oh;
-                f_s0 = f_s0 + 1 == nrows ? 0 : f_s0 + 1;
-                for (; ring_v < f_oh + R; ++ring_v) {  // the next tile's new row
-                  twait(&hfull[ring_slot], (fillpar >> ring_slot) & 1u, prof, &dw[4]);
-                  fillpar ^= 1u << ring_slot;
-                  ring_slot = ring_slot + 1 == nrows ? 0 : ring_slot + 1;
-                }
-                twait(&sempty[(g + 1) & 1], (((g + 1) >> 1) & 1) ^ 1, prof, &dw[3]);
-                tc_fence_after();
-                f_prepared = true;
+          int slot = cur_s0;
+          auto prep_next = [&]() {  // the next tile's new row and chunk buffer
+            ++f_oh;
+            f_s0 = f_s0 + 1 == nrows ? 0 : f_s0 + 1;
+            for (; ring_v < f_oh + R; ++ring_v) {
+              twait(&hfull[ring_slot], (fillpar >> ring_slot) & 1u, prof, &dw[4]);
+              fillpar ^= 1u << ring_slot;
+              ring_slot = ring_slot + 1 == nrows ? 0 : ring_slot + 1;
+            }
+            twait(&sempty[(g + 1) & 1], (((g + 1) >> 1) & 1) ^ 1, prof, &dw[3]);
+            tc_fence_after();
+            f_prepared = true;
+          };
+          auto tap3 = [&](uint64_t ah, uint32_t acc) {
+            tc_mma<MmaKind::kF16>(x, ah, bh, idesc3, acc);
+            tc_mma<MmaKind::kF16>(x + BN, ah + 2, bh, idesc2, 1u);  // A_m: +32 B
+            tc_mma<MmaKind::kF16>(x + BN, ah + 4, bh, idesc, 1u);   // A_l: +64 B
+            bh += Cfg::kBStage >> 4;
+          };
+          if (R == 4 && S == 4) {
+            // the space-to-depth stem (4 x 4 taps): fully unrolled, so the
+            // issuing thread only adds descriptors between MMAs
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              uint64_t ah = adesc0 + static_cast<uint64_t>(slot) * hstep;
+              slot = slot + 1 == nrows ? 0 : slot + 1;
+#pragma unroll
+              for (int s = 0; s < 4; ++s) {
+                tap3(ah, (r | s) != 0 ? 1u : 0u);
+                ah += SWZ >> 4;
+                if (r * 4 + s == 13 && next_same) prep_next();
+              }
+            }
+          } else {
+            int tap = 0;
+            for (int r = 0; r < R; ++r) {
+              uint64_t ah = adesc0 + static_cast<uint64_t>(slot) * hstep;
+              slot = slot + 1 == nrows ? 0 : slot + 1;
+              for (int s = 0; s < S; ++s, ++tap) {
+                tap3(ah, (r | s) != 0 ? 1u : 0u);
+                ah += SWZ >> 4;
+                if (tap == prep_at && next_same) prep_next();
               }
             }
           }
