@@ -486,6 +486,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t adesc0 = make_smem_desc<SWZ>(smem_u32(sHalo), 8 * SWZ);
       const uint64_t hstep = static_cast<uint64_t>(hbytes >> 4);  // one row slot, in 16-B units
       int f_img = 0, f_oh = 0, f_s0 = 0, ring_slot = 0;
+      // the fast path's tile-end commits (chunk ready, ring row free), issued
+      // after the NEXT tile's first tap so the tensor pipe never runs dry at
+      // a tile boundary (only within an image: the next tile's rows are then
+      // already resident)
+      int pend_sb = -1, pend_s0 = 0;
       bool f_prepared = false;  // the next tile's waits already done
       const uint64_t bdesc0 = make_smem_desc<kBSW>(smem_u32(sRes), 8 * kBSW);
       WorkIter wi = make_iter();
@@ -624,6 +629,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int s = 0; s < 4; ++s) {
                 tap3(ah, (r | s) != 0 ? 1u : 0u);
                 ah += SWZ >> 4;
+                if (r == 0 && s == 0 && pend_sb >= 0) {
+                  tc_commit(&sfull[pend_sb]);
+                  tc_commit(&hempty[pend_s0]);
+                  pend_sb = -1;
+                }
                 if (r * 4 + s == 13 && next_same) prep_next();
               }
             }
@@ -638,6 +648,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (tap == prep_at && next_same) prep_next();
               }
             }
+          }
+          if (next_same && R == 4 && S == 4) {  // committed after the next tile's first tap
+            pend_sb = sb;
+            pend_s0 = cur_s0;
+            ++g;
+            continue;
           }
           tc_commit(&sfull[sb]);
           ++g;
@@ -760,6 +776,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (PAIR) tc_commit_pair(&tfull[tb], 3);
           else tc_commit(&tfull[tb]);
         }
+      }
+      if (pend_sb >= 0) {  // (the last tile never defers; kept for safety)
+        tc_commit(&sfull[pend_sb]);
+        tc_commit(&hempty[pend_s0]);
       }
     }
   } else if (warp >= 4) {
